@@ -1,0 +1,182 @@
+/*
+ * porediff_b200.h — C ABI of the B200-native FTCS reaction-diffusion step on
+ * the 8^Dims sparse block grid (arXiv 2304.11165; reference `porediff`).
+ *
+ * The reference has no C ABI: its surface is the header-only C++ templates in
+ * /root/reference/proj/include/porediff (SparseBlockGrid, FtcsStepper,
+ * ftcs_step, run_simulation, total_mass, max_diffusivity). Every entry point
+ * below replaces one of those members, cited as file:line. The C++ drop-in
+ * headers in include/porediff/ (and the Python mirror in
+ * paper_2304_11165_b200/porediff.py) are thin layers over exactly these calls.
+ *
+ * Conventions
+ *  - All functions return an int status (PD_OK or one PD_E_* code); on error
+ *    the message is retrievable with pd_last_error() (thread-local).
+ *  - Codes 1..6 map one-to-one onto the reference exception taxonomy
+ *    (errors.hpp:9-41); PD_E_CUDA signals a device/driver failure.
+ *  - Chunk arrays are in ascending chunk linear index (the reference's
+ *    traversal order, sparse_block_grid.hpp:283-293); a chunk's ordinal is its
+ *    position in that order. Keys are int32[Dims] per chunk (x fastest).
+ *    Masks are uint64[V/64] per chunk, bit (offset&63) of word (offset>>6)
+ *    (sparse_block_grid.hpp:45-50). Offsets are x-fastest inside the chunk
+ *    (sparse_block_grid.hpp:99-103). Slabs are V scalars per chunk,
+ *    chunk-ordinal-major (sparse_block_grid.hpp:43,180-187).
+ *  - scalar_bytes is 8 (double, the parity mode) or 4 (float).
+ *  - Calls are synchronous at return (stream-ordered internally).
+ */
+#ifndef POREDIFF_B200_H
+#define POREDIFF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PD_OK = 0,
+    PD_E_INPUT = 1,     /* porediff::input_error     (errors.hpp:14) */
+    PD_E_BOUNDS = 2,    /* porediff::bounds_error    (errors.hpp:19) */
+    PD_E_PROPERTY = 3,  /* porediff::property_error  (errors.hpp:24) */
+    PD_E_IO = 4,        /* porediff::io_error        (errors.hpp:29) */
+    PD_E_STABILITY = 5, /* porediff::stability_error (errors.hpp:34) */
+    PD_E_NUMERIC = 6,   /* porediff::numeric_error   (errors.hpp:39) */
+    PD_E_CUDA = 7       /* device / driver failure (no reference analogue) */
+};
+
+enum { PD_REACTION_NONE = 0, PD_REACTION_SURFACE_SINK = 1, PD_REACTION_VOLUMETRIC = 2 };
+enum { PD_BC_NO_FLUX = 0, PD_BC_DIRICHLET = 1 };
+
+/* porediff::SimulationConfig + ReactionSpec + FaceBc (solver.hpp:38-97).
+ * The volumetric time factor std::function is replaced by per-step factors
+ * passed to pd_stepper_run (the host evaluates T(time_factor(s*dt)) as
+ * solver.hpp:230-234 does). */
+typedef struct pd_sim_config {
+    double dt;
+    int64_t n_steps;
+    double b_low, b_up;            /* PhaseBand (geometry.hpp:43-46) */
+    double boundary_epsilon;
+    int32_t reaction_kind;         /* PD_REACTION_* */
+    int32_t source_prop;           /* volumetric: property index of f(x) */
+    double rate;                   /* surface sink k >= 0 */
+    double band_half_width;        /* surface sink w > 0 */
+    int32_t bc_type[6];            /* [axis*2+side], PD_BC_* */
+    double bc_value[6];
+    int64_t record_every;
+    int32_t enforce_stability;
+    int32_t has_time_factor;       /* volumetric: factors array supplied */
+} pd_sim_config;
+
+/* porediff::StepDiagnostics (solver.hpp:99-106) minus wall_seconds. */
+typedef struct pd_diag {
+    int64_t step;
+    double time;
+    double total_mass;
+    double min_u;
+    double max_u;
+} pd_diag;
+
+typedef struct pd_grid pd_grid;
+typedef struct pd_stepper pd_stepper;
+
+/* Last error message of the calling thread ("" if none). */
+const char* pd_last_error(void);
+/* Number of CUDA devices visible (0 on a CPU-only host; never errors). */
+int pd_device_count(void);
+/* Library build string (arch, precision modes). */
+const char* pd_version(void);
+
+/* ---- device sparse block grid (replaces SparseBlockGrid storage,
+ *      sparse_block_grid.hpp:30-304) ---------------------------------------- */
+
+/* Creates a device grid: geometry (grid_geometry.hpp:23-112), chunk keys and
+ * masks in ascending linear order, n_props zero-initialised columns
+ * (sparse_block_grid.hpp:58-73,268-281). `device` selects the CUDA device. */
+int pd_grid_create(int dims, int scalar_bytes, const int64_t* size, const double* spacing,
+                   int64_t n_chunks, const int32_t* keys, const uint64_t* masks,
+                   int n_props, int device, pd_grid** out);
+int pd_grid_destroy(pd_grid* g);
+/* Host<->device copy of one logical property's slabs (n_chunks*V scalars).
+ * Resolves the double-buffer column mapping like channel_data
+ * (sparse_block_grid.hpp:180-187). */
+int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs);
+int pd_grid_download(pd_grid* g, int prop, void* host_slabs);
+/* Same, device pointer to device pointer (no host staging). */
+int pd_grid_upload_device(pd_grid* g, int prop, const void* dev_slabs);
+/* O(1) column swap (sparse_block_grid.hpp:88-91). */
+int pd_grid_swap(pd_grid* g, int prop_a, int prop_b);
+/* Current physical column of a logical property (for host mirrors). */
+int pd_grid_column_of(const pd_grid* g, int prop, int* column);
+/* Raw device pointer of a logical property's slabs (stream-ordered use). */
+int pd_grid_device_ptr(pd_grid* g, int prop, void** ptr);
+int pd_grid_info(const pd_grid* g, int64_t* n_chunks, int64_t* active_nodes);
+/* Chunk arrays back to the host (keys int32[n*dims], masks uint64[n*words]). */
+int pd_grid_download_layout(const pd_grid* g, int32_t* keys, uint64_t* masks);
+
+/* total_mass (solver.hpp:158-171): per-chunk sequential sum of active values,
+ * pairwise_sum over ordinals (parallel.hpp:68-84), times cell volume. */
+int pd_grid_total_mass(pd_grid* g, int prop, double* out);
+/* max_diffusivity (solver.hpp:139-154): max over active nodes, 0 if none. */
+int pd_grid_max_active(pd_grid* g, int prop, double* out);
+/* min/max over active nodes with the reference's fold semantics
+ * (snapshot_diagnostics, solver.hpp:282-301). */
+int pd_grid_minmax_active(pd_grid* g, int prop, double* mn, double* mx);
+
+/* ---- FTCS stepper (replaces FtcsStepper, solver.hpp:183-467) ------------- */
+
+/* Validates the config (solver.hpp:304-331; messages identical) and builds the
+ * per-run constants, neighbour table (solver.hpp:333-351) and the static
+ * fluid / sink bitmasks derived from phi. prop_* are logical property
+ * indices of phi, u, D, u_next (and the volumetric source, or -1). */
+int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int prop_u,
+                      int prop_d, int prop_next, pd_stepper** out);
+int pd_stepper_destroy(pd_stepper* s);
+/* Strict stability bound for the grid's current D (solver.hpp:220-224). */
+int pd_stepper_stability_bound(pd_stepper* s, double* out);
+/* Step-0 row (snapshot_diagnostics, solver.hpp:282-301). */
+int pd_stepper_snapshot_diag(pd_stepper* s, pd_diag* out);
+/* Advances n_steps steps starting at global step index step0 (the state
+ * entering is u at step0*dt), exactly as n calls of FtcsStepper::step
+ * (solver.hpp:228-279): after each step u and u_next are swapped. A row is
+ * produced for every step s (global, 0-based) with (s+1) % record_every == 0
+ * or s+1 == final_step, where final_step is the caller's run length
+ * (run_simulation's record rule, solver.hpp:512-517); rows receives at most
+ * n_steps rows and *n_rows the count. factors: per-step source factor T(g(t))
+ * (volumetric with time factor) or NULL (=1). On a non-finite node the
+ * numeric_error message of solver.hpp:250-260 is returned and the grid is left
+ * exactly as the reference leaves it (u = pre-step state, u_next written). */
+int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_step,
+                   const double* factors, pd_diag* rows, int64_t* n_rows);
+/* Device time (ms, CUDA events) of the last pd_stepper_run's step kernels. */
+int pd_stepper_last_ms(const pd_stepper* s, double* ms);
+/* Launches of the step kernel so far (benchmark accounting). */
+int pd_stepper_launch_count(const pd_stepper* s, int64_t* launches);
+
+/* ---- geometry build on the device (north_star subsystem 1; reference
+ *      build_sparse_grid geometry.hpp:148-176 on synthetic::SpherePacking
+ *      synthetic.hpp:25-56 and the hash initial condition config.hpp:558) ---- */
+
+/* Evaluates the sphere-pack fluid SDF (synthetic.hpp:32-40) at every node of
+ * a cell-centred geometry, activates b_low+eps < phi < b_up-eps
+ * (geometry.hpp:163-170), allocates chunks in ascending linear order and
+ * fills phi. n_props columns; phi goes to prop_phi. The resulting grid is
+ * bit-identical (keys, masks, phi) to build_sparse_grid on field_from(sdf). */
+int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const double* spacing,
+                              const double* origin, int64_t n_spheres,
+                              const double* centers /* n*3 */, const double* radii,
+                              double b_low, double b_up, int n_props, int prop_phi,
+                              int device, pd_grid** out);
+/* D = d_min + d_max/(1+exp(-(g1+g2*phi))) on active nodes
+ * (geometry.hpp:182-206; device exp, may differ from glibc by <= 1 ulp). */
+int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_min,
+                               double d_max, double gamma1, double gamma2);
+/* u = hash_unit_value(seed, flat_index) on active nodes (config.hpp:558-564). */
+int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed);
+/* Fills a property with a constant on active nodes. */
+int pd_grid_fill_const(pd_grid* g, int prop, double value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POREDIFF_B200_H */

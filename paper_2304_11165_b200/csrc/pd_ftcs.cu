@@ -1,0 +1,675 @@
+// Fused FTCS reaction-diffusion step on the device sparse block grid
+// (north_star subsystem 3). Restates FtcsStepper (solver.hpp:183-467) for
+// sm_100a:
+//   - one CTA per chunk: the chunk's u/D and its 2*Dims one-node face layers
+//     from the neighbour chunks are staged in shared memory as a 10^Dims tile
+//     with a per-cell face status, so every gather (solver.hpp:360-383) is a
+//     shared-memory read;
+//   - only active nodes are loaded and written (predicated), so 32-B sectors
+//     without an active node cost no HBM traffic and inactive slots keep their
+//     contents exactly as in the reference;
+//   - phi is never read per step: the static wall / sink predicates
+//     (solver.hpp:210-212,413,436) are precomputed once per stepper into
+//     per-chunk bitmasks;
+//   - arithmetic mirrors the reference expression tree with FMA contraction
+//     disabled (--fmad=false; reference builds with -ffp-contract=off,
+//     CMakeLists.txt:14), so results are bit-identical;
+//   - diagnostics (mass / min / max, solver.hpp:444-454,264-278) are produced
+//     only on record steps; every step still detects non-finite values with
+//     the reference's lowest-ordinal/first-offset rule (solver.hpp:250-260).
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <initializer_list>
+#include <limits>
+
+#include "pd_internal.cuh"
+
+namespace pdb {
+
+template <class T>
+struct StepArgs {
+    const T* __restrict__ u;
+    T* __restrict__ un;
+    const T* __restrict__ d;
+    const T* __restrict__ src;
+    const uint64_t* __restrict__ active;
+    const uint64_t* __restrict__ fluid;
+    const uint64_t* __restrict__ sink;
+    const int32_t* __restrict__ nbr;
+    const int32_t* __restrict__ keys;
+    int64_t size[3];
+    T inv_dx2[3];
+    T dt, neg_k, src_factor;
+    T bcv[6];
+    int dirichlet;  // bit (axis*2+side)
+    int reaction;   // PD_REACTION_*
+    double* p_mass;
+    double* p_mn;
+    double* p_mx;
+    unsigned long long* bad_key;  // (ordinal << 10) | offset, atomicMin
+    int* flags;                   // per step of the batch: 1 bad, 2 huge, 4 mass
+    int k;                        // step index within the batch
+};
+
+__device__ __forceinline__ double min_left(double l, double r) { return (r < l) ? r : l; }
+__device__ __forceinline__ double max_left(double l, double r) { return (l < r) ? r : l; }
+
+// |x| >= 2^990 (or non-finite): a non-record step whose values are this large
+// could overflow the total mass, which the reference checks every step
+// (solver.hpp:514-515); such steps fall back to an exact mass evaluation.
+__device__ __forceinline__ bool is_huge(double x) { return !(fabs(x) < 0x1p990); }
+
+template <class T, int D, bool DIAG>
+__global__ void __launch_bounds__(Geo<D>::V) ftcs_step_kernel(StepArgs<T> a) {
+    constexpr int V = Geo<D>::V, W = Geo<D>::W, FA = Geo<D>::FA, NH = Geo<D>::NH;
+    constexpr int TV = Geo<D>::TV;
+    __shared__ T su[TV];
+    __shared__ T sd[TV];
+    __shared__ uint8_t st[TV];  // 0 substitute centre, 1 neighbour, 2 Dirichlet halo
+
+    const int64_t i = blockIdx.x;
+    const int off = threadIdx.x;
+    if (a.k > 0) {
+        const int prev = a.flags[a.k - 1];
+        if (prev) {  // an earlier step of the batch failed: stay a no-op
+            if (off == 0) a.flags[a.k] = prev;
+            return;
+        }
+    }
+    int c[3];
+    c[0] = off & 7;
+    c[1] = (off >> 3) & 7;
+    c[2] = D == 3 ? (off >> 6) : 0;
+    int64_t base[3];
+#pragma unroll
+    for (int ax = 0; ax < D; ++ax) base[ax] = (int64_t)a.keys[i * D + ax] << 3;
+
+    const uint64_t aw = a.active[i * W + (off >> 6)];
+    const uint64_t fw = a.fluid[i * W + (off >> 6)];
+    const bool act = (aw >> (off & 63)) & 1u;
+    const bool flu = (fw >> (off & 63)) & 1u;
+    T u_c = T(0), d_c = T(0);
+    if (act) u_c = a.u[i * V + off];
+    if (flu) d_c = a.d[i * V + off];
+
+    const int t = (c[0] + 1) + 10 * (c[1] + 1) + (D == 3 ? 100 * (c[2] + 1) : 0);
+    {
+        uint8_t s = flu ? 1 : 0;
+        T tu = u_c;
+        if (!act) {
+            // in-chunk node beyond the box edge (size not a multiple of 8):
+            // acts as the outer face (solver.hpp:363-369)
+#pragma unroll
+            for (int ax = 0; ax < D; ++ax)
+                if (base[ax] + c[ax] >= a.size[ax]) {
+                    if (a.dirichlet & (1 << (ax * 2 + 1))) {
+                        s = 2;
+                        tu = a.bcv[ax * 2 + 1];
+                    }
+                    break;
+                }
+        }
+        su[t] = tu;
+        sd[t] = d_c;
+        st[t] = s;
+    }
+    // halo face layers from the 2*Dims neighbour chunks (build_neighbor_table,
+    // solver.hpp:333-351; cross-chunk branch of gather, solver.hpp:377-382)
+    for (int h = off; h < NH; h += V) {
+        const int f = h / FA;
+        const int p = h % FA;
+        const int ax = f >> 1, side = f & 1;
+        int q[3] = {0, 0, 0};
+        {
+            int r = p, b = 0;
+#pragma unroll
+            for (int bx = 0; bx < D; ++bx) {
+                if (bx == ax) continue;
+                q[bx] = (b == 0) ? (r & 7) : (r >> 3);
+                ++b;
+            }
+        }
+        q[ax] = side ? 8 : -1;
+        const int th = (q[0] + 1) + 10 * (q[1] + 1) + (D == 3 ? 100 * (q[2] + 1) : 0);
+        const int64_t g = base[ax] + q[ax];
+        uint8_t s = 0;
+        T tu = T(0), td = T(0);
+        if (g < 0 || g >= a.size[ax]) {
+            if (a.dirichlet & (1 << f)) {
+                s = 2;
+                tu = a.bcv[f];
+            }
+        } else {
+            const int32_t j = a.nbr[i * 2 * D + f];
+            if (j >= 0) {
+                q[ax] = side ? 0 : 7;
+                const int o2 = q[0] | (q[1] << 3) | (D == 3 ? (q[2] << 6) : 0);
+                if ((a.fluid[(int64_t)j * W + (o2 >> 6)] >> (o2 & 63)) & 1u) {
+                    s = 1;
+                    tu = a.u[(int64_t)j * V + o2];
+                    td = a.d[(int64_t)j * V + o2];
+                }
+            }
+        }
+        su[th] = tu;
+        sd[th] = td;
+        st[th] = s;
+    }
+    __syncthreads();
+
+    T un = u_c;
+    if (flu) {
+        T lap = T(0);
+#pragma unroll
+        for (int ax = 0; ax < D; ++ax) {
+            const int ts = ax == 0 ? 1 : (ax == 1 ? 10 : 100);
+            const int tm = t - ts, tp = t + ts;
+            const uint8_t sm = st[tm], sp = st[tp];
+            const T mu = sm ? su[tm] : u_c;
+            const T md = sm == 1 ? sd[tm] : d_c;
+            const T pu = sp ? su[tp] : u_c;
+            const T pdd = sp == 1 ? sd[tp] : d_c;
+            const T dh_m = (d_c + md) * T(0.5);
+            const T dh_p = (d_c + pdd) * T(0.5);
+            lap += (dh_p * (pu - u_c) - dh_m * (u_c - mu)) * a.inv_dx2[ax];
+        }
+        T rate = T(0);
+        if (a.reaction == PD_REACTION_SURFACE_SINK) {
+            if ((a.sink[i * W + (off >> 6)] >> (off & 63)) & 1u) rate = a.neg_k * u_c;
+        } else if (a.reaction == PD_REACTION_VOLUMETRIC) {
+            rate = a.src[i * V + off] * a.src_factor;
+        }
+        un = u_c + a.dt * lap + a.dt * rate;
+    }
+    if (act) a.un[i * V + off] = un;
+
+    const double v = (double)un;
+    const bool bad = act && !isfinite(v);
+    if (bad) {
+        atomicMin(a.bad_key, ((unsigned long long)i << 10) | (unsigned long long)off);
+        atomicOr(&a.flags[a.k], 1);
+    }
+    if constexpr (!DIAG) {
+        if (act && !bad && is_huge(v)) atomicOr(&a.flags[a.k], 2);
+    } else {
+        // per-chunk partials (solver.hpp:444-454)
+        __syncthreads();  // tile no longer needed: reuse su as scratch
+        double* sv = reinterpret_cast<double*>(su);
+        __shared__ double smn[V], smx[V];
+        __shared__ uint64_t am[W];
+        if (off < W) am[off] = a.active[i * W + off];
+        if constexpr (sizeof(T) == 8) {
+            sv[off] = v;
+        }
+        const bool ok = act && !isnan(v);
+        smn[off] = ok ? v : INFINITY;
+        smx[off] = ok ? v : -INFINITY;
+        __syncthreads();
+        for (int s = 1; s < V; s <<= 1) {
+            if ((off & (2 * s - 1)) == 0) {
+                smn[off] = min_left(smn[off], smn[off + s]);
+                smx[off] = max_left(smx[off], smx[off + s]);
+            }
+            __syncthreads();
+        }
+        if constexpr (sizeof(T) != 8) {
+            // float tile is too small for V doubles: reuse smx after the tree
+            const double m0 = smn[0], x0 = smx[0];
+            __syncthreads();
+            smx[off] = v;
+            __syncthreads();
+            if (off == 0) {
+                double acc = 0.0;
+                for (int w = 0; w < W; ++w) {
+                    uint64_t bits = am[w];
+                    while (bits) {
+                        const int b = __ffsll((long long)bits) - 1;
+                        acc += smx[w * 64 + b];
+                        bits &= bits - 1;
+                    }
+                }
+                a.p_mass[i] = acc;
+                a.p_mn[i] = m0;
+                a.p_mx[i] = x0;
+            }
+        } else {
+            if (off == 0) {
+                double acc = 0.0;
+                for (int w = 0; w < W; ++w) {
+                    uint64_t bits = am[w];
+                    while (bits) {
+                        const int b = __ffsll((long long)bits) - 1;
+                        acc += sv[w * 64 + b];
+                        bits &= bits - 1;
+                    }
+                }
+                a.p_mass[i] = acc;
+                a.p_mn[i] = smn[0];
+                a.p_mx[i] = smx[0];
+            }
+        }
+    }
+}
+
+// Static per-stepper predicates from phi (never re-read per step):
+//   fluid = active && !(phi <= wall)          (solver.hpp:374,381,413)
+//   sink  = fluid && |double(phi)| <= w*hmin  (solver.hpp:436)
+template <class T, int D>
+__global__ void __launch_bounds__(Geo<D>::V)
+    predicate_kernel(const T* __restrict__ phi, const uint64_t* __restrict__ active, T wall,
+                     double sink_band, uint64_t* __restrict__ fluid, uint64_t* __restrict__ sink) {
+    constexpr int V = Geo<D>::V, W = Geo<D>::W;
+    const int64_t i = blockIdx.x;
+    const int off = threadIdx.x;
+    const bool act = (active[i * W + (off >> 6)] >> (off & 63)) & 1u;
+    bool fl = false, sk = false;
+    if (act) {
+        const T p = phi[i * V + off];
+        fl = !(p <= wall);
+        sk = fl && fabs((double)p) <= sink_band;
+    }
+    const unsigned bf = __ballot_sync(0xffffffffu, fl);
+    const unsigned bs = __ballot_sync(0xffffffffu, sk);
+    if ((off & 31) == 0) {
+        const int w = off >> 6, hi = (off >> 5) & 1;
+        reinterpret_cast<unsigned*>(fluid)[(i * W + w) * 2 + hi] = bf;
+        reinterpret_cast<unsigned*>(sink)[(i * W + w) * 2 + hi] = bs;
+    }
+}
+
+template <int D>
+__global__ void neighbor_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ table,
+                                int64_t n, int64_t cc0, int64_t cc1, int64_t cc2,
+                                int32_t* __restrict__ nbr) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t cc[3] = {cc0, cc1, cc2};
+    for (int ax = 0; ax < D; ++ax)
+        for (int s = 0; s < 2; ++s) {
+            int64_t k[3] = {0, 0, 0};
+            for (int b = 0; b < D; ++b) k[b] = keys[i * D + b];
+            k[ax] += s == 0 ? -1 : 1;
+            int32_t o = -1;
+            if (k[ax] >= 0 && k[ax] < cc[ax]) {
+                int64_t lin = k[D - 1];
+                for (int b = D - 2; b >= 0; --b) lin = lin * cc[b] + k[b];
+                o = table[lin];
+            }
+            nbr[i * 2 * D + ax * 2 + s] = o;
+        }
+}
+
+}  // namespace pdb
+
+using namespace pdb;
+
+struct pd_stepper {
+    pd_grid* g = nullptr;
+    pd_sim_config cfg{};
+    int prop_phi = -1, prop_u = -1, prop_d = -1, prop_next = -1, prop_src = -1;
+    uint64_t* d_fluid = nullptr;
+    uint64_t* d_sink = nullptr;
+    int32_t* d_nbr = nullptr;
+    int* d_flags = nullptr;
+    unsigned long long* d_bad = nullptr;
+    double* d_rows = nullptr;  // 3 per row of the batch
+    int64_t batch_cap = 0;
+    double inv_dx2[3] = {0, 0, 0};
+    double hmin = 0.0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_ms = 0.0;
+    int64_t launches = 0;
+};
+
+namespace {
+
+constexpr int64_t kBatch = 512;
+
+void validate(const pd_grid* g, const pd_sim_config* c, int prop_src,
+              std::initializer_list<int> solver_props) {
+    // solver.hpp:304-331, messages verbatim
+    if (!(c->dt > 0.0) || !std::isfinite(c->dt))
+        fail(PD_E_INPUT, "time step must be positive and finite");
+    if (c->n_steps < 1) fail(PD_E_INPUT, "step count must be at least 1");
+    if (c->record_every < 1) fail(PD_E_INPUT, "record_every must be at least 1");
+    if (!(c->b_low < c->b_up)) fail(PD_E_INPUT, "phase band is empty (b_low must be < b_up)");
+    if (c->boundary_epsilon < 0.0 || !std::isfinite(c->boundary_epsilon))
+        fail(PD_E_INPUT, "boundary_epsilon must be finite and >= 0");
+    if (c->reaction_kind == PD_REACTION_SURFACE_SINK) {
+        if (c->rate < 0.0) fail(PD_E_INPUT, "surface sink rate must be >= 0");
+        if (!(c->band_half_width > 0.0))
+            fail(PD_E_INPUT, "surface sink band half-width must be > 0");
+    }
+    for (int p : solver_props)
+        if (p < 0 || p >= (int)g->column_of.size())
+            fail(PD_E_INPUT,
+                 "grid lacks a solver channel; build simulation grids with channels "
+                 "{phi, u, D, u_next}");
+    if (c->reaction_kind == PD_REACTION_VOLUMETRIC &&
+        (prop_src < 0 || prop_src >= (int)g->column_of.size()))
+        fail(PD_E_PROPERTY, "unknown property (volumetric source channel)");
+}
+
+template <class T>
+void fill_args(const pd_stepper* s, StepArgs<T>& a, const void* u, void* un, double factor) {
+    const pd_grid* g = s->g;
+    const pd_sim_config& c = s->cfg;
+    a.u = (const T*)u;
+    a.un = (T*)un;
+    a.d = (const T*)g->cols[(size_t)g->column_of[(size_t)s->prop_d]];
+    a.src = s->prop_src >= 0 ? (const T*)g->cols[(size_t)g->column_of[(size_t)s->prop_src]]
+                             : nullptr;
+    a.active = g->d_masks;
+    a.fluid = s->d_fluid;
+    a.sink = s->d_sink;
+    a.nbr = s->d_nbr;
+    a.keys = g->d_keys;
+    for (int ax = 0; ax < 3; ++ax) a.size[ax] = g->size[ax];
+    // inv_dx2[a] = T(1) / T(h_a * h_a)   (solver.hpp:202-205)
+    for (int ax = 0; ax < 3; ++ax)
+        a.inv_dx2[ax] = ax < g->dims ? T(1) / static_cast<T>(g->spacing[ax] * g->spacing[ax]) : T(0);
+    a.dt = static_cast<T>(c.dt);                 // solver.hpp:206
+    a.neg_k = -static_cast<T>(c.rate);           // solver.hpp:437
+    a.src_factor = static_cast<T>(factor);       // solver.hpp:231-234
+    a.dirichlet = 0;
+    for (int f = 0; f < 6; ++f) {
+        a.bcv[f] = static_cast<T>(c.bc_value[f]);  // solver.hpp:367
+        if (f < 2 * g->dims && c.bc_type[f] == PD_BC_DIRICHLET) a.dirichlet |= 1 << f;
+    }
+    a.reaction = c.reaction_kind;
+    a.p_mass = g->red.part[0];
+    a.p_mn = g->red.part[1];
+    a.p_mx = g->red.part[2];
+    a.bad_key = s->d_bad;
+    a.flags = s->d_flags;
+}
+
+void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool diag, int k) {
+    pd_grid* g = s->g;
+    if (g->n_chunks == 0) return;
+    const unsigned nb = (unsigned)g->n_chunks;
+    if (g->tbytes == 8) {
+        StepArgs<double> a;
+        fill_args<double>(s, a, u, un, factor);
+        a.k = k;
+        if (g->dims == 3) {
+            if (diag) ftcs_step_kernel<double, 3, true><<<nb, 512, 0, g->stream>>>(a);
+            else ftcs_step_kernel<double, 3, false><<<nb, 512, 0, g->stream>>>(a);
+        } else {
+            if (diag) ftcs_step_kernel<double, 2, true><<<nb, 64, 0, g->stream>>>(a);
+            else ftcs_step_kernel<double, 2, false><<<nb, 64, 0, g->stream>>>(a);
+        }
+    } else {
+        StepArgs<float> a;
+        fill_args<float>(s, a, u, un, factor);
+        a.k = k;
+        if (g->dims == 3) {
+            if (diag) ftcs_step_kernel<float, 3, true><<<nb, 512, 0, g->stream>>>(a);
+            else ftcs_step_kernel<float, 3, false><<<nb, 512, 0, g->stream>>>(a);
+        } else {
+            if (diag) ftcs_step_kernel<float, 2, true><<<nb, 64, 0, g->stream>>>(a);
+            else ftcs_step_kernel<float, 2, false><<<nb, 64, 0, g->stream>>>(a);
+        }
+    }
+    PD_CUDA(cudaGetLastError());
+    s->launches++;
+}
+
+std::string node_message(const pd_grid* g, int64_t step_number, unsigned long long key) {
+    const int64_t ordinal = (int64_t)(key >> 10);
+    const int off = (int)(key & 1023u);
+    std::vector<int32_t> k((size_t)g->dims);
+    PD_CUDA(cudaMemcpy(k.data(), g->d_keys + ordinal * g->dims, sizeof(int32_t) * (size_t)g->dims,
+                       cudaMemcpyDeviceToHost));
+    // solver.hpp:253-258 (node_index, sparse_block_grid.hpp:244-250)
+    std::string m = "non-finite value at step " + std::to_string(step_number) + ", node (";
+    for (int a = 0; a < g->dims; ++a) {
+        const int64_t idx = ((int64_t)k[(size_t)a] << 3) | ((off >> (3 * a)) & 7);
+        m += (a ? "," : "") + std::to_string(idx);
+    }
+    return m + ")";
+}
+
+}  // namespace
+
+extern "C" {
+
+int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int prop_u, int prop_d,
+                      int prop_next, pd_stepper** out) {
+    return guarded([&] {
+        *out = nullptr;
+        const int prop_src = cfg->reaction_kind == PD_REACTION_VOLUMETRIC ? cfg->source_prop : -1;
+        validate(g, cfg, prop_src, {prop_phi, prop_u, prop_d, prop_next});
+        DeviceGuard dg(g->device);
+        auto* s = new pd_stepper();
+        try {
+            s->g = g;
+            s->cfg = *cfg;
+            s->prop_phi = prop_phi;
+            s->prop_u = prop_u;
+            s->prop_d = prop_d;
+            s->prop_next = prop_next;
+            s->prop_src = prop_src;
+            s->hmin = g->spacing[0];
+            for (int a = 1; a < g->dims; ++a) s->hmin = std::min(s->hmin, g->spacing[a]);
+            const int64_t n = std::max<int64_t>(1, g->n_chunks);
+            PD_CUDA(cudaMalloc(&s->d_fluid, sizeof(uint64_t) * (size_t)(n * g->W)));
+            PD_CUDA(cudaMalloc(&s->d_sink, sizeof(uint64_t) * (size_t)(n * g->W)));
+            PD_CUDA(cudaMalloc(&s->d_nbr, sizeof(int32_t) * (size_t)(n * 2 * g->dims)));
+            PD_CUDA(cudaMalloc(&s->d_flags, sizeof(int) * (size_t)kBatch));
+            PD_CUDA(cudaMalloc(&s->d_bad, sizeof(unsigned long long)));
+            PD_CUDA(cudaMalloc(&s->d_rows, sizeof(double) * 3 * (size_t)kBatch));
+            PD_CUDA(cudaEventCreate(&s->ev0));
+            PD_CUDA(cudaEventCreate(&s->ev1));
+            if (g->n_chunks > 0) {
+                const void* phi = g->cols[(size_t)g->column_of[(size_t)prop_phi]];
+                const double sink_band = cfg->band_half_width * s->hmin;  // solver.hpp:212
+                const unsigned nb = (unsigned)g->n_chunks;
+                if (g->tbytes == 8) {
+                    // wall = T(b_low) + T(eps)   (solver.hpp:210-211)
+                    const double wall = (double)cfg->b_low + (double)cfg->boundary_epsilon;
+                    if (g->dims == 3)
+                        predicate_kernel<double, 3><<<nb, 512, 0, g->stream>>>(
+                            (const double*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+                    else
+                        predicate_kernel<double, 2><<<nb, 64, 0, g->stream>>>(
+                            (const double*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+                } else {
+                    const float wall = (float)cfg->b_low + (float)cfg->boundary_epsilon;
+                    if (g->dims == 3)
+                        predicate_kernel<float, 3><<<nb, 512, 0, g->stream>>>(
+                            (const float*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+                    else
+                        predicate_kernel<float, 2><<<nb, 64, 0, g->stream>>>(
+                            (const float*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+                }
+                PD_CUDA(cudaGetLastError());
+                const int blocks = (int)((g->n_chunks + 255) / 256);
+                if (g->dims == 3)
+                    neighbor_kernel<3><<<blocks, 256, 0, g->stream>>>(
+                        g->d_keys, g->d_table, g->n_chunks, g->cc[0], g->cc[1], g->cc[2], s->d_nbr);
+                else
+                    neighbor_kernel<2><<<blocks, 256, 0, g->stream>>>(
+                        g->d_keys, g->d_table, g->n_chunks, g->cc[0], g->cc[1], 1, s->d_nbr);
+                PD_CUDA(cudaGetLastError());
+            }
+            ensure_scratch(g);
+            PD_CUDA(cudaStreamSynchronize(g->stream));
+        } catch (...) {
+            pd_stepper_destroy(s);
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int pd_stepper_destroy(pd_stepper* s) {
+    if (!s) return PD_OK;
+    {
+        DeviceGuard dg(s->g->device);
+        cudaStreamSynchronize(s->g->stream);
+        cudaFree(s->d_fluid);
+        cudaFree(s->d_sink);
+        cudaFree(s->d_nbr);
+        cudaFree(s->d_flags);
+        cudaFree(s->d_bad);
+        cudaFree(s->d_rows);
+        if (s->ev0) cudaEventDestroy(s->ev0);
+        if (s->ev1) cudaEventDestroy(s->ev1);
+    }
+    delete s;
+    return PD_OK;
+}
+
+int pd_stepper_stability_bound(pd_stepper* s, double* out) {
+    return guarded([&] {
+        double dmax = 0.0;
+        const int rc = pd_grid_max_active(s->g, s->prop_d, &dmax);
+        if (rc != PD_OK) fail(rc, pd_last_error());
+        if (!(dmax > 0.0)) {
+            *out = std::numeric_limits<double>::infinity();
+            return;
+        }
+        // stability_dt (solver.hpp:111-120)
+        double inv_sum = 0.0;
+        for (int a = 0; a < s->g->dims; ++a) {
+            const double h = s->g->spacing[a];
+            inv_sum += 1.0 / (h * h);
+        }
+        *out = 1.0 / (2.0 * dmax) / inv_sum;
+    });
+}
+
+int pd_stepper_snapshot_diag(pd_stepper* s, pd_diag* out) {
+    return guarded([&] {
+        pd_grid* g = s->g;
+        DeviceGuard dg(g->device);
+        const void* u = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
+        launch_chunk_stats(g, u, g->d_masks);
+        launch_pairwise_finalize(g, g->d_row, nullptr);
+        double row[3];
+        PD_CUDA(cudaMemcpyAsync(row, g->d_row, sizeof row, cudaMemcpyDeviceToHost, g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        out->step = 0;
+        out->time = 0.0;
+        out->total_mass = row[0];
+        out->min_u = row[1];
+        out->max_u = row[2];
+    });
+}
+
+int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_step,
+                   const double* factors, pd_diag* rows, int64_t* n_rows) {
+    return guarded([&] {
+        *n_rows = 0;
+        if (n_steps <= 0) return;
+        pd_grid* g = s->g;
+        DeviceGuard dg(g->device);
+        const pd_sim_config& c = s->cfg;
+        const int64_t rec = c.record_every;
+        double total_ms = 0.0;
+        int64_t j = 0;
+        std::vector<int> hflags((size_t)kBatch);
+        std::vector<double> hrows((size_t)kBatch * 3);
+        std::vector<int64_t> row_step((size_t)kBatch);
+        while (j < n_steps) {
+            const int64_t nb = std::min<int64_t>(kBatch, n_steps - j);
+            PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)nb, g->stream));
+            PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
+            int64_t nr = 0;
+            PD_CUDA(cudaEventRecord(s->ev0, g->stream));
+            for (int64_t k = 0; k < nb; ++k) {
+                const int64_t st = step0 + j + k;  // global step index being taken
+                const bool record = ((st + 1) % rec == 0) || (st + 1 == final_step);
+                const int cu = g->column_of[(size_t)s->prop_u];
+                const int cn = g->column_of[(size_t)s->prop_next];
+                const double f = factors ? factors[j + k] : 1.0;
+                launch_step(s, g->cols[(size_t)cu], g->cols[(size_t)cn], f, record, (int)k);
+                if (record) {
+                    launch_pairwise_finalize(g, s->d_rows + 3 * nr, s->d_flags + k);
+                    row_step[(size_t)nr] = st + 1;
+                    ++nr;
+                }
+                // swap_channels("u", "u_next")  (solver.hpp:262)
+                std::swap(g->column_of[(size_t)s->prop_u], g->column_of[(size_t)s->prop_next]);
+            }
+            PD_CUDA(cudaEventRecord(s->ev1, g->stream));
+            PD_CUDA(cudaMemcpyAsync(hflags.data(), s->d_flags, sizeof(int) * (size_t)nb,
+                                    cudaMemcpyDeviceToHost, g->stream));
+            if (nr > 0)
+                PD_CUDA(cudaMemcpyAsync(hrows.data(), s->d_rows, sizeof(double) * 3 * (size_t)nr,
+                                        cudaMemcpyDeviceToHost, g->stream));
+            PD_CUDA(cudaStreamSynchronize(g->stream));
+            float ms = 0.f;
+            PD_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+            total_ms += ms;
+
+            int64_t fail_k = -1;
+            for (int64_t k = 0; k < nb; ++k)
+                if (hflags[(size_t)k]) {
+                    fail_k = k;
+                    break;
+                }
+            // rows of steps before the failing one are valid
+            for (int64_t r = 0; r < nr; ++r) {
+                const int64_t step_no = row_step[(size_t)r];
+                if (fail_k >= 0 && step_no > step0 + j + fail_k) break;
+                pd_diag& d = rows[(*n_rows)++];
+                d.step = step_no;
+                d.time = static_cast<double>(step_no) * c.dt;  // solver.hpp:266
+                d.total_mass = hrows[(size_t)r * 3];
+                d.min_u = hrows[(size_t)r * 3 + 1];
+                d.max_u = hrows[(size_t)r * 3 + 2];
+            }
+            if (fail_k < 0) {
+                j += nb;
+                continue;
+            }
+            const int code = hflags[(size_t)fail_k];
+            const int64_t st = step0 + j + fail_k;
+            // undo the swaps of the steps that did not complete: the failing
+            // step itself is undone only for a non-finite node (the reference
+            // throws before its swap, solver.hpp:250-262)
+            int64_t undo = nb - fail_k - ((code & 1) ? 0 : 1);
+            if (undo % 2)
+                std::swap(g->column_of[(size_t)s->prop_u], g->column_of[(size_t)s->prop_next]);
+            if (code & 1) {
+                unsigned long long key = 0;
+                PD_CUDA(cudaMemcpy(&key, s->d_bad, sizeof key, cudaMemcpyDeviceToHost));
+                s->last_ms = total_ms;
+                fail(PD_E_NUMERIC, node_message(g, st + 1, key));
+            }
+            if (code & 4) {  // recorded step with a non-finite total mass
+                s->last_ms = total_ms;
+                fail(PD_E_NUMERIC, "non-finite total mass at step " + std::to_string(st + 1));
+            }
+            // code 2: huge values on a non-recorded step: evaluate that step's
+            // total mass exactly (same per-chunk order as step()).
+            const void* u_now = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
+            launch_chunk_stats(g, u_now, g->d_masks);
+            launch_pairwise_finalize(g, g->d_row, nullptr);
+            double row[3];
+            PD_CUDA(cudaMemcpyAsync(row, g->d_row, sizeof row, cudaMemcpyDeviceToHost, g->stream));
+            PD_CUDA(cudaStreamSynchronize(g->stream));
+            if (!std::isfinite(row[0])) {
+                s->last_ms = total_ms;
+                fail(PD_E_NUMERIC, "non-finite total mass at step " + std::to_string(st + 1));
+            }
+            j += fail_k + 1;
+        }
+        s->last_ms = total_ms;
+    });
+}
+
+int pd_stepper_last_ms(const pd_stepper* s, double* ms) {
+    *ms = s->last_ms;
+    return PD_OK;
+}
+
+int pd_stepper_launch_count(const pd_stepper* s, int64_t* launches) {
+    *launches = s->launches;
+    return PD_OK;
+}
+
+}  // extern "C"

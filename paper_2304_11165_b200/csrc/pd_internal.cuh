@@ -1,0 +1,115 @@
+// Internal declarations shared by the porediff_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "porediff_b200.h"
+
+namespace pdb {
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define PD_CUDA(x)                                                                       \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess)                                                           \
+            ::pdb::fail(PD_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+void set_error(const std::string& msg);
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        set_error("");
+        return PD_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return PD_E_CUDA;
+    }
+}
+
+// Chunk geometry per dimensionality (sparse_block_grid.hpp:33-35).
+template <int D>
+struct Geo {
+    static constexpr int V = D == 3 ? 512 : 64;  // nodes per chunk
+    static constexpr int W = V / 64;             // mask words per chunk
+    static constexpr int FA = D == 3 ? 64 : 8;   // nodes per chunk face
+    static constexpr int NH = 2 * D * FA;        // halo cells (face layers)
+    static constexpr int TE = 10;                // staged tile edge (8 + 2 halo)
+    static constexpr int TV = D == 3 ? 1000 : 100;
+};
+
+// Partial-reduction scratch (per-chunk mass / min / max, then pairwise tree).
+struct ReduceScratch {
+    double* part[3] = {nullptr, nullptr, nullptr};
+    double* tmp_a[3] = {nullptr, nullptr, nullptr};
+    double* tmp_b[3] = {nullptr, nullptr, nullptr};
+    int64_t cap = 0;
+};
+
+}  // namespace pdb
+
+struct pd_grid {
+    int dims = 3, tbytes = 8, V = 512, W = 8, device = 0;
+    int64_t size[3] = {1, 1, 1};
+    double spacing[3] = {1, 1, 1};
+    double cell_volume = 1.0;
+    int64_t cc[3] = {1, 1, 1};
+    int64_t table_size = 1;
+    int64_t n_chunks = 0, active = 0;
+    int32_t* d_keys = nullptr;
+    uint64_t* d_masks = nullptr;
+    int32_t* d_table = nullptr;  // chunk linear index -> ordinal, -1 absent
+    std::vector<void*> cols;     // physical columns
+    std::vector<int> column_of;  // logical property -> physical column
+    cudaStream_t stream = nullptr;
+    pdb::ReduceScratch red;
+    double* d_row = nullptr;  // 3 doubles: mass, min, max
+};
+
+namespace pdb {
+
+// Chunk-level reductions (pd_grid.cu).
+void ensure_scratch(pd_grid* g);
+// Per-chunk sequential mass + left-preference min/max of an active-masked
+// column into red.part[0..2] (solver.hpp:158-171, 282-301).
+void launch_chunk_stats(pd_grid* g, const void* col, const uint64_t* masks);
+// pairwise_sum (parallel.hpp:68-84) of red.part[0] and min/max fold of
+// part[1..2] over ordinals; writes {mass*cell_volume, min, max} to dst
+// (device) and, when flags != nullptr, ORs 4 into *flags if the mass is not
+// finite. Empty grids produce {0, +inf, -inf}.
+void launch_pairwise_finalize(pd_grid* g, double* dst, int* flags);
+// max over active nodes of a column (solver.hpp:139-154) into red.part.
+void launch_chunk_max(pd_grid* g, const void* col);
+
+int device_of(const pd_grid* g);
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace pdb
