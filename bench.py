@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the fused FTCS sparse-block step (BASELINE.json metric:
+active-point updates/s and % of the HBM roofline, vs the host CPU).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[4], the configuration the metric is quoted
+on; it fits one B200): a 2048^3 cell-centred box on [0,1]^3, pore space =
+complement of a random overlapping-sphere pack (radius 128 voxels, count for
+~20% porosity, seed 12345), FP64 (the parity mode), sigmoid D(phi), surface
+sink on the interface band, u0 = hash_unit_value(1, flat). Built on the
+device (pd_build_sphere_pack_grid), so nothing but the stepper is timed.
+
+A "step" is one FTCS time step over every active node. value = active
+nodes x K / (max-over-ranks device time of the K steps). The grid (~3 x 25 GB
+of u/u_next/D) is far larger than L2, so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun, one rank per GPU): z-slab decomposition by chunk
+layers; each rank builds its slab plus one ghost chunk layer per side and
+exchanges boundary u layers with NCCL every step (weak scaling: --n-per-gpu
+z-extent per rank). See DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "active-point updates/s (GPts/s) & % HBM roofline"
+BYTES_PER_UPDATE = 24  # FP64: u_n read + D read + u_{n+1} write
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=2048, help="box edge in nodes")
+    ap.add_argument("--psi", type=float, default=0.2, help="target porosity")
+    ap.add_argument("--radius-vox", type=float, default=128.0)
+    ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--cpu-sample", type=int, default=128, help="edge of the CPU sample crop")
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--e2e-n", type=int, default=512, help="box edge of the end-to-end host-buffer run")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_2304_11165_b200 import synthetic as sy
+    r = args.radius_vox / args.n
+    pack = sy.pack_for_porosity(args.psi, r, args.seed)
+    return pack
+
+
+def config_dict(args, n_gpus):
+    return {"workload": f"C5 sparse {args.n}^3 random overlapping-sphere pore space, ~{int(args.psi*100)}% "
+                        f"porosity, r={int(args.radius_vox)} vox, surface sink, FP64",
+            "box": args.n, "porosity_target": args.psi, "sphere_radius_vox": args.radius_vox,
+            "seed": args.seed, "precision": "fp64", "parallelism": f"zslab{n_gpus}",
+            "l2": "inputs larger than L2 (no flush needed)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    def __init__(self, index=0):
+        self.samples = []
+        self.stop = threading.Event()
+        self.index = index
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and not s[2 + i].startswith("Not")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the step kernel from the committed ncu
+    capture summary (profiles/*_traffic.json), or None."""
+    f = ROOT / "profiles" / "ftcs_step_traffic.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d.get("dram_bytes_per_launch"), d
+    return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU baselines (reference compiled in place; test infrastructure)
+# ---------------------------------------------------------------------------
+
+
+def cpu_sample(args, pack, edge, steps, threads=None):
+    """Times the reference's own run_simulation on a crop [0,edge)^3 of the
+    same pore geometry (same spheres and spacing); geometry build untimed."""
+    import ctypes as C
+
+    from oracle.pyoracle import Ref, make_config
+    from paper_2304_11165_b200 import porediff as pd
+
+    R = Ref()
+    if threads:
+        R.L.ref_set_worker_count(threads)
+    h = 1.0 / args.n
+    geom = pd.GridGeometry.make((edge,) * 3, (h,) * 3, (0.5 * h,) * 3)
+    centers, radii = pack.arrays()
+    # spheres that can touch the crop (exact: the others are never the min)
+    lo, hi = 0.0, edge * h
+    near = np.all((centers > lo - radii[:, None] - 2 * h) & (centers < hi + radii[:, None] + 2 * h), axis=1)
+    sub = type(pack)(list(map(tuple, centers[near])), list(radii[near]))
+    sdf = sub.fluid_sdf_field(geom)
+    g = R.grid_from_sdf(geom.size, geom.spacing, geom.origin, sdf)
+    g.populate_diffusion(0.0, 1.0, 0.0, 4.0 * args.n)
+    g.fill_hash("u", 1)
+    dmax = g.max_diffusivity()
+    dt = 0.4 * pd.stability_dt(geom, dmax)
+    cfg = make_config(dt, steps, reaction="surface_sink", rate=1.0, band_half_width=1.0, record_every=steps)
+    t0 = time.perf_counter()
+    code, msg, rows = g.run(cfg)
+    secs = time.perf_counter() - t0
+    assert code == 0, msg
+    active = g.active_count()
+    cores = R.L.ref_worker_count()
+    if threads:
+        R.L.ref_set_worker_count(0)
+    return active * steps / secs, active, secs, cores
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_11165_b200 import porediff as pd
+    from paper_2304_11165_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    pack = workload(args)
+    dom = shard.build_domain(args.n, pack, rank, world, device=local)
+    stepper = dom.stepper(dt_frac=0.4, sink_rate=1.0)
+
+    def sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    dom.run(stepper, 0, args.warmup)
+    sync()
+    launches0 = dom.launches(stepper)
+    with Clocks(local) as clk:
+        sync()
+        t0 = time.perf_counter()
+        ms = dom.run(stepper, args.warmup, args.steps)
+        sync()
+        wall = time.perf_counter() - t0
+    # step kernels + (N>1) two face packs and two unpacks per step
+    launches = dom.launches(stepper) - launches0
+    if world > 1:
+        launches += 4 * args.steps
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    act_t = torch.tensor([dom.owned_active], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(act_t, op=dist.ReduceOp.SUM)
+    ms_max = float(ms_t.item())
+    active = float(act_t.item())
+    step_ms = ms_max / args.steps
+    value = active * args.steps / (ms_max / 1e3)
+    peak, peak_src = measured_peak()
+    # dominant kernel: the step kernel alone (CUDA events on its stream)
+    kern_ms = dom.kernel_ms(stepper)
+    achieved = dom.owned_active * BYTES_PER_UPDATE / (kern_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic()
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = run_e2e(args, pack)
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        try:
+            v, a, secs, cores = cpu_sample(args, pack, args.cpu_sample, args.cpu_steps)
+            cpu = {"value": v / 1e9, "unit": "GPts/s", "cores": cores, "kind": "reference",
+                   "sample": f"reference run_simulation (oracle/_ref, -O3 -ffp-contract=off) on the "
+                             f"[0,{args.cpu_sample})^3 crop of the same geometry: {a} active nodes x "
+                             f"{args.cpu_steps} steps in {secs:.2f} s"}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "GPts/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value / 1e9, "unit": "GPts/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-built sphere pack)",
+            "config": config_dict(args, world),
+            "active_nodes": int(active), "chunks": int(dom.total_chunks(world)),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src, "bytes_per_update": BYTES_PER_UPDATE,
+                         "kernel_ms_per_step": kern_ms, "traffic_source": traffic_src and "profiles/ftcs_step_traffic.json"},
+            "roofline_frac_of_step": dom.owned_active * BYTES_PER_UPDATE / (step_ms / 1e3) / 1e9 / peak,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "wall_s_timed_region": wall,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, pack):
+    """Same metric through the reference-facing API with HOST buffers: one
+    run_simulation call on a host SparseBlockGrid (pinned upload of every
+    channel, the FTCS steps, diagnostics rows, download of u and u_next), on a
+    --e2e-n^3 crop of the same geometry."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2304_11165_b200 import porediff as pd
+
+    n = args.e2e_n
+    h = 1.0 / args.n
+    geom = pd.GridGeometry.make((n,) * 3, (h,) * 3, (0.5 * h,) * 3)
+    centers, radii = pack.arrays()
+    dev = pd.DeviceGrid.sphere_pack(geom, centers, radii, n_props=4, prop_phi=0)
+    dev.populate_diffusion(0, 2, pd.DiffusionProfile(0.0, 1.0, 0.0, 4.0 * args.n))
+    dev.fill_hash(1, 1)
+    keys, masks = dev.layout()
+    nch = len(keys)
+    # pinned host slabs (the caller's grid)
+    host = {}
+    for p, name in enumerate(pd.solver_channels()):
+        t = torch.empty((nch, 512), dtype=torch.float64, pin_memory=True)
+        arr = t.numpy()
+        arr[:] = dev.download(p)
+        host[name] = (t, arr)
+    dev.close()
+    dmax = float(host["D"][1].max())
+    cfg = pd.SimulationConfig(dt=0.4 * pd.stability_dt(geom, dmax), n_steps=args.e2e_steps,
+                              record_every=args.e2e_steps)
+    cfg.reaction = pd.ReactionSpec.surface_sink(1.0, 1.0)
+
+    def once():
+        g = pd.SparseBlockGrid.from_layout(geom, pd.solver_channels(), keys, masks, None)
+        for name in pd.solver_channels():
+            g._data[name] = host[name][1]  # zero-copy: the pinned host buffers
+        t0 = time.perf_counter()
+        res = pd.run_simulation(g, cfg)
+        out_u = g.channel_data("u")
+        out_un = g.channel_data("u_next")
+        secs = time.perf_counter() - t0
+        g.close()
+        return secs, res
+
+    once()  # warm-up (context, allocator)
+    secs, res = once()
+    active = int(host["phi"][1].size and sum(bin(int(w)).count("1") for w in masks.ravel()))
+    slab = nch * 512 * 8
+    return {"value": active * args.e2e_steps / secs / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": 4 * slab,
+            "d2h_bytes_per_step": 4 * slab + 40 * len(res.diagnostics),
+            "workload": f"run_simulation on a host grid, [0,{n})^3 crop of the same geometry, "
+                        f"{args.e2e_steps} steps per call (one call = one e2e step)",
+            "active_nodes": active, "seconds": secs}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pack = workload(args)
+    edge = args.cpu_sample
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(args, pack, edge, max(1, args.cpu_steps // 4))
+    total_pts, total_s, cores, active = 0.0, 0.0, None, 0
+    for _ in range(args.steps):
+        v, active, secs, cores = cpu_sample(args, pack, edge, args.cpu_steps)
+        total_pts += active * args.cpu_steps
+        total_s += secs
+        vals.append(v)
+    value = total_pts / total_s / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args, world),
+        "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": cores, "kind": "reference",
+                         "sample": f"each step = reference run_simulation of {args.cpu_steps} FTCS steps on the "
+                                   f"[0,{edge})^3 crop ({active} active nodes) of the same geometry"},
+        "e2e": {"value": value, "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

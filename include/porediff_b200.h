@@ -104,6 +104,18 @@ int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs);
 int pd_grid_download(pd_grid* g, int prop, void* host_slabs);
 /* Same, device pointer to device pointer (no host staging). */
 int pd_grid_upload_device(pd_grid* g, int prop, const void* dev_slabs);
+/* Runs all further work of this grid (and its steppers) on an external CUDA
+ * stream (cudaStream_t, e.g. torch.cuda.current_stream()); NULL restores the
+ * grid's own stream. Used to order the step with NCCL halo exchanges. */
+int pd_grid_set_stream(pd_grid* g, void* stream);
+/* Packs / unpacks the one-node face plane `face` (axis*2+side: side 0 = the
+ * chunk's coordinate-0 plane, 1 = coordinate-7 plane) of n chunks (device
+ * ordinal list) of one logical property to / from a contiguous device
+ * buffer of n*V/8 scalars (halo exchange for z-slab sharding). */
+int pd_grid_pack_face(pd_grid* g, int prop, const int32_t* dev_ordinals, int64_t n, int face,
+                      void* dev_out);
+int pd_grid_unpack_face(pd_grid* g, int prop, const int32_t* dev_ordinals, int64_t n, int face,
+                        const void* dev_in);
 /* O(1) column swap (sparse_block_grid.hpp:88-91). */
 int pd_grid_swap(pd_grid* g, int prop_a, int prop_b);
 /* Current physical column of a logical property (for host mirrors). */
@@ -132,6 +144,10 @@ int pd_grid_minmax_active(pd_grid* g, int prop, double* mn, double* mx);
 int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int prop_u,
                       int prop_d, int prop_next, pd_stepper** out);
 int pd_stepper_destroy(pd_stepper* s);
+/* Restricts the step (and its diagnostics partials) to the chunk ordinals
+ * [begin, end) — the chunks a rank owns under z-slab sharding; the other
+ * chunks of the grid are read-only ghost halos. Default: all chunks. */
+int pd_stepper_set_range(pd_stepper* s, int64_t begin, int64_t end);
 /* Strict stability bound for the grid's current D (solver.hpp:220-224). */
 int pd_stepper_stability_bound(pd_stepper* s, double* out);
 /* Step-0 row (snapshot_diagnostics, solver.hpp:282-301). */
@@ -167,6 +183,14 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
                               const double* centers /* n*3 */, const double* radii,
                               double b_low, double b_up, int n_props, int prop_phi,
                               int device, pd_grid** out);
+/* Same, but only the chunks whose key lies in [chunk_lo, chunk_hi) per axis
+ * are built (keys stay global): one shard of a decomposed domain, including
+ * its ghost chunk layers. An empty region yields a grid with 0 chunks. */
+int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const double* spacing,
+                                const double* origin, int64_t n_spheres, const double* centers,
+                                const double* radii, double b_low, double b_up,
+                                const int64_t* chunk_lo, const int64_t* chunk_hi, int n_props,
+                                int prop_phi, int device, pd_grid** out);
 /* D = d_min + d_max/(1+exp(-(g1+g2*phi))) on active nodes
  * (geometry.hpp:182-206; device exp, may differ from glibc by <= 1 ulp). */
 int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_min,

@@ -73,6 +73,9 @@ _SIGNATURES = [
     ("pd_grid_upload", C.c_int, [_P, C.c_int, _P]),
     ("pd_grid_download", C.c_int, [_P, C.c_int, _P]),
     ("pd_grid_upload_device", C.c_int, [_P, C.c_int, _P]),
+    ("pd_grid_set_stream", C.c_int, [_P, _P]),
+    ("pd_grid_pack_face", C.c_int, [_P, C.c_int, _P, C.c_int64, C.c_int, _P]),
+    ("pd_grid_unpack_face", C.c_int, [_P, C.c_int, _P, C.c_int64, C.c_int, _P]),
     ("pd_grid_swap", C.c_int, [_P, C.c_int, C.c_int]),
     ("pd_grid_column_of", C.c_int, [_P, C.c_int, C.POINTER(C.c_int)]),
     ("pd_grid_device_ptr", C.c_int, [_P, C.c_int, C.POINTER(_P)]),
@@ -83,12 +86,14 @@ _SIGNATURES = [
     ("pd_grid_minmax_active", C.c_int, [_P, C.c_int, _DP, _DP]),
     ("pd_stepper_create", C.c_int, [_P, C.POINTER(pd_sim_config), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     ("pd_stepper_destroy", C.c_int, [_P]),
+    ("pd_stepper_set_range", C.c_int, [_P, C.c_int64, C.c_int64]),
     ("pd_stepper_stability_bound", C.c_int, [_P, _DP]),
     ("pd_stepper_snapshot_diag", C.c_int, [_P, C.POINTER(pd_diag)]),
     ("pd_stepper_run", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _DP, C.POINTER(pd_diag), _I64P]),
     ("pd_stepper_last_ms", C.c_int, [_P, _DP]),
     ("pd_stepper_launch_count", C.c_int, [_P, _I64P]),
     ("pd_build_sphere_pack_grid", C.c_int, [C.c_int, _I64P, _DP, _DP, C.c_int64, _DP, _DP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("pd_build_sphere_pack_region", C.c_int, [C.c_int, _I64P, _DP, _DP, C.c_int64, _DP, _DP, C.c_double, C.c_double, _I64P, _I64P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     ("pd_grid_populate_diffusion", C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double]),
     ("pd_grid_fill_hash", C.c_int, [_P, C.c_int, C.c_uint64]),
     ("pd_grid_fill_const", C.c_int, [_P, C.c_int, C.c_double]),

@@ -50,6 +50,7 @@ struct StepArgs {
     unsigned long long* bad_key;  // (ordinal << 10) | offset, atomicMin
     int* flags;                   // per step of the batch: 1 bad, 2 huge, 4 mass
     int k;                        // step index within the batch
+    int64_t ord0;                 // first chunk ordinal of the launch
 };
 
 __device__ __forceinline__ double min_left(double l, double r) { return (r < l) ? r : l; }
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(Geo<D>::V) ftcs_step_kernel(StepArgs<T> a) {
     __shared__ T sd[TV];
     __shared__ uint8_t st[TV];  // 0 substitute centre, 1 neighbour, 2 Dirichlet halo
 
-    const int64_t i = blockIdx.x;
+    const int64_t i = a.ord0 + blockIdx.x;
     const int off = threadIdx.x;
     if (a.k > 0) {
         const int prev = a.flags[a.k - 1];
@@ -320,6 +321,7 @@ struct pd_stepper {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_ms = 0.0;
     int64_t launches = 0;
+    int64_t begin = 0, end = 0;  // owned ordinal range
 };
 
 namespace {
@@ -387,12 +389,13 @@ void fill_args(const pd_stepper* s, StepArgs<T>& a, const void* u, void* un, dou
 
 void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool diag, int k) {
     pd_grid* g = s->g;
-    if (g->n_chunks == 0) return;
-    const unsigned nb = (unsigned)g->n_chunks;
+    if (s->end <= s->begin) return;
+    const unsigned nb = (unsigned)(s->end - s->begin);
     if (g->tbytes == 8) {
         StepArgs<double> a;
         fill_args<double>(s, a, u, un, factor);
         a.k = k;
+        a.ord0 = s->begin;
         if (g->dims == 3) {
             if (diag) ftcs_step_kernel<double, 3, true><<<nb, 512, 0, g->stream>>>(a);
             else ftcs_step_kernel<double, 3, false><<<nb, 512, 0, g->stream>>>(a);
@@ -404,6 +407,7 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         StepArgs<float> a;
         fill_args<float>(s, a, u, un, factor);
         a.k = k;
+        a.ord0 = s->begin;
         if (g->dims == 3) {
             if (diag) ftcs_step_kernel<float, 3, true><<<nb, 512, 0, g->stream>>>(a);
             else ftcs_step_kernel<float, 3, false><<<nb, 512, 0, g->stream>>>(a);
@@ -451,6 +455,8 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             s->prop_d = prop_d;
             s->prop_next = prop_next;
             s->prop_src = prop_src;
+            s->begin = 0;
+            s->end = g->n_chunks;
             s->hmin = g->spacing[0];
             for (int a = 1; a < g->dims; ++a) s->hmin = std::min(s->hmin, g->spacing[a]);
             const int64_t n = std::max<int64_t>(1, g->n_chunks);
@@ -522,6 +528,15 @@ int pd_stepper_destroy(pd_stepper* s) {
     return PD_OK;
 }
 
+int pd_stepper_set_range(pd_stepper* s, int64_t begin, int64_t end) {
+    return guarded([&] {
+        if (begin < 0 || end > s->g->n_chunks || begin > end)
+            fail(PD_E_INPUT, "stepper ordinal range outside the grid");
+        s->begin = begin;
+        s->end = end;
+    });
+}
+
 int pd_stepper_stability_bound(pd_stepper* s, double* out) {
     return guarded([&] {
         double dmax = 0.0;
@@ -587,7 +602,8 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                 const double f = factors ? factors[j + k] : 1.0;
                 launch_step(s, g->cols[(size_t)cu], g->cols[(size_t)cn], f, record, (int)k);
                 if (record) {
-                    launch_pairwise_finalize(g, s->d_rows + 3 * nr, s->d_flags + k);
+                    launch_pairwise_finalize(g, s->d_rows + 3 * nr, s->d_flags + k, s->begin,
+                                             s->end - s->begin);
                     row_step[(size_t)nr] = st + 1;
                     ++nr;
                 }

@@ -221,6 +221,7 @@ struct PackArgs {
     int64_t size[3];
     double spacing[3], origin[3];
     int64_t cc[3];
+    int64_t rlo[3], rext[3];  // chunk-key region [rlo, rlo+rext)
     const double* centers;
     const double* radii;
     int64_t n_spheres;
@@ -312,9 +313,9 @@ __global__ void __launch_bounds__(512)
     __shared__ double s_ub[16];
     const int64_t slot = blockIdx.x;
     int64_t k[3];
-    k[0] = slot % p.cc[0];
-    k[1] = (slot / p.cc[0]) % p.cc[1];
-    k[2] = slot / (p.cc[0] * p.cc[1]);
+    k[0] = p.rlo[0] + slot % p.rext[0];
+    k[1] = p.rlo[1] + (slot / p.rext[0]) % p.rext[1];
+    k[2] = p.rlo[2] + slot / (p.rext[0] * p.rext[1]);
     const int nc = gather_candidates(p, k, cand, &n_cand, s_ub);
     const int off = threadIdx.x;
     const int64_t gx = k[0] * 8 + (off & 7), gy = k[1] * 8 + ((off >> 3) & 7),
@@ -349,20 +350,17 @@ __global__ void __launch_bounds__(512)
     __shared__ int n_cand;
     __shared__ double s_ub[16];
     const int64_t slot = blockIdx.x;
-    if (!slot_flag[slot]) {
-        if (threadIdx.x == 0) table[slot] = -1;
-        return;
-    }
+    if (!slot_flag[slot]) return;
     const int64_t i = ordinal[slot];
     int64_t k[3];
-    k[0] = slot % p.cc[0];
-    k[1] = (slot / p.cc[0]) % p.cc[1];
-    k[2] = slot / (p.cc[0] * p.cc[1]);
+    k[0] = p.rlo[0] + slot % p.rext[0];
+    k[1] = p.rlo[1] + (slot / p.rext[0]) % p.rext[1];
+    k[2] = p.rlo[2] + slot / (p.rext[0] * p.rext[1]);
     const int nc = gather_candidates(p, k, cand, &n_cand, s_ub);
     const int off = threadIdx.x;
     if (off < 3) keys[i * 3 + off] = (int32_t)k[off];
     if (off < 8) masks[i * 8 + off] = slot_masks[slot * 8 + off];
-    if (off == 0) table[slot] = (int32_t)i;
+    if (off == 0) table[(k[2] * p.cc[1] + k[1]) * p.cc[0] + k[0]] = (int32_t)i;
     const bool act = (slot_masks[slot * 8 + (off >> 6)] >> (off & 63)) & 1u;
     T v = 0;
     if (act) {
@@ -381,6 +379,33 @@ __global__ void popcount_kernel(const uint64_t* __restrict__ masks, int64_t n_wo
         c += __popcll(masks[w]);
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// one-node face plane of a chunk: side 0 -> coordinate 0, side 1 -> 7
+template <class T, int D>
+__global__ void face_pack_kernel(const T* __restrict__ col, const int32_t* __restrict__ ords,
+                                 int64_t n, int face, T* __restrict__ out, bool unpack,
+                                 const T* __restrict__ in, T* __restrict__ dst) {
+    constexpr int V = Geo<D>::V, FA = Geo<D>::FA;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * FA) return;
+    const int64_t c = t / FA;
+    const int p = (int)(t % FA);
+    const int ax = face >> 1, side = face & 1;
+    int q[3] = {0, 0, 0};
+    int b = 0;
+    for (int bx = 0; bx < D; ++bx) {
+        if (bx == ax) continue;
+        q[bx] = b == 0 ? (p & 7) : (p >> 3);
+        ++b;
+    }
+    q[ax] = side ? 7 : 0;
+    const int off = q[0] | (q[1] << 3) | (D == 3 ? (q[2] << 6) : 0);
+    const int64_t j = ords[c];
+    if (unpack)
+        dst[j * V + off] = in[t];
+    else
+        out[t] = col[j * V + off];
 }
 
 // ---------------------------------------------------------------------------
@@ -438,15 +463,16 @@ void launch_chunk_max(pd_grid* g, const void* col) {
     PD_CUDA(cudaGetLastError());
 }
 
-void launch_pairwise_finalize(pd_grid* g, double* dst, int* flags) {
+void launch_pairwise_finalize(pd_grid* g, double* dst, int* flags, int64_t begin, int64_t count) {
     ensure_scratch(g);
-    if (g->n_chunks == 0) {
+    if (count < 0) count = g->n_chunks - begin;
+    if (count <= 0) {
         empty_row_kernel<<<1, 1, 0, g->stream>>>(dst);
         PD_CUDA(cudaGetLastError());
         return;
     }
-    const double* in[3] = {g->red.part[0], g->red.part[1], g->red.part[2]};
-    int64_t n = g->n_chunks;
+    const double* in[3] = {g->red.part[0] + begin, g->red.part[1] + begin, g->red.part[2] + begin};
+    int64_t n = count;
     bool use_a = true;
     while (true) {
         const int64_t nb = (n + kPairBlock - 1) / kPairBlock;
@@ -574,7 +600,8 @@ int pd_grid_create(int dims, int scalar_bytes, const int64_t* size, const double
                 prev = lin;
             }
             DeviceGuard dg(device);
-            PD_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+            PD_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+            g->stream = g->own_stream;
             g->n_chunks = n_chunks;
             PD_CUDA(cudaMalloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
             PD_CUDA(cudaMemsetAsync(g->d_table, 0xff, sizeof(int32_t) * (size_t)g->table_size,
@@ -613,6 +640,7 @@ int pd_grid_destroy(pd_grid* g) {
     {
         DeviceGuard dg(g->device);
         if (g->stream) cudaStreamSynchronize(g->stream);
+        if (g->own_stream) cudaStreamSynchronize(g->own_stream);
         for (void* c : g->cols) cudaFree(c);
         cudaFree(g->d_keys);
         cudaFree(g->d_masks);
@@ -623,7 +651,7 @@ int pd_grid_destroy(pd_grid* g) {
             cudaFree(g->red.tmp_a[k]);
             cudaFree(g->red.tmp_b[k]);
         }
-        if (g->stream) cudaStreamDestroy(g->stream);
+        if (g->own_stream) cudaStreamDestroy(g->own_stream);
     }
     delete g;
     return PD_OK;
@@ -657,6 +685,38 @@ int pd_grid_download(pd_grid* g, int prop, void* host_slabs) {
         PD_CUDA(cudaMemcpyAsync(host_slabs, c, slab_bytes(g), cudaMemcpyDeviceToHost, g->stream));
         PD_CUDA(cudaStreamSynchronize(g->stream));
     });
+}
+
+int pd_grid_set_stream(pd_grid* g, void* stream) {
+    return guarded([&] { g->stream = stream ? (cudaStream_t)stream : g->own_stream; });
+}
+
+static int face_io(pd_grid* g, int prop, const int32_t* ords, int64_t n, int face, void* out,
+                   const void* in, bool unpack) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        void* col = col_ptr(g, prop);
+        if (face < 0 || face >= 2 * g->dims) fail(PD_E_INPUT, "face index out of range");
+        if (n <= 0) return;
+        const int fa = g->dims == 3 ? 64 : 8;
+        const unsigned blocks = (unsigned)((n * fa + 255) / 256);
+        dispatch(g, [&](auto tp, auto dc) {
+            using T = std::remove_pointer_t<decltype(tp)>;
+            constexpr int D = decltype(dc)::value;
+            face_pack_kernel<T, D><<<blocks, 256, 0, g->stream>>>((const T*)col, ords, n, face, (T*)out,
+                                                                  unpack, (const T*)in, (T*)col);
+        });
+        PD_CUDA(cudaGetLastError());
+    });
+}
+
+int pd_grid_pack_face(pd_grid* g, int prop, const int32_t* ords, int64_t n, int face, void* out) {
+    return face_io(g, prop, ords, n, face, out, nullptr, false);
+}
+
+int pd_grid_unpack_face(pd_grid* g, int prop, const int32_t* ords, int64_t n, int face,
+                        const void* in) {
+    return face_io(g, prop, ords, n, face, nullptr, in, true);
 }
 
 int pd_grid_swap(pd_grid* g, int a, int b) {
@@ -798,6 +858,15 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
                               const double* origin, int64_t n_spheres, const double* centers,
                               const double* radii, double b_low, double b_up, int n_props,
                               int prop_phi, int device, pd_grid** out) {
+    return pd_build_sphere_pack_region(scalar_bytes, size, spacing, origin, n_spheres, centers, radii,
+                                       b_low, b_up, nullptr, nullptr, n_props, prop_phi, device, out);
+}
+
+int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const double* spacing,
+                                const double* origin, int64_t n_spheres, const double* centers,
+                                const double* radii, double b_low, double b_up,
+                                const int64_t* chunk_lo, const int64_t* chunk_hi, int n_props,
+                                int prop_phi, int device, pd_grid** out) {
     return guarded([&] {
         *out = nullptr;
         if (!(b_low < b_up))
@@ -813,14 +882,21 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
         try {
             init_geometry(g, 3, scalar_bytes, size, spacing, device);
             DeviceGuard dg(device);
-            PD_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+            PD_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+            g->stream = g->own_stream;
             PD_CUDA(cudaMalloc(&g->d_row, sizeof(double) * 4));
             PackArgs p;
+            int64_t slots = 1;
             for (int a = 0; a < 3; ++a) {
                 p.size[a] = size[a];
                 p.spacing[a] = spacing[a];
                 p.origin[a] = origin[a];
                 p.cc[a] = g->cc[a];
+                const int64_t lo = chunk_lo ? std::max<int64_t>(0, chunk_lo[a]) : 0;
+                const int64_t hi = chunk_hi ? std::min<int64_t>(g->cc[a], chunk_hi[a]) : g->cc[a];
+                p.rlo[a] = lo;
+                p.rext[a] = std::max<int64_t>(0, hi - lo);
+                slots *= p.rext[a];
             }
             p.n_spheres = n_spheres;
             PD_CUDA(cudaMalloc(&d_centers, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres * 3)));
@@ -833,11 +909,22 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
             }
             p.centers = (const double*)d_centers;
             p.radii = (const double*)d_radii;
-            const int64_t slots = g->table_size;
+            PD_CUDA(cudaMalloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
+            PD_CUDA(cudaMemsetAsync(g->d_table, 0xff, sizeof(int32_t) * (size_t)g->table_size, g->stream));
+            if (slots == 0) {
+                if (chunk_lo == nullptr)
+                    fail(PD_E_INPUT, "no node lies inside the phase band: the grid would be empty");
+                alloc_columns(g, n_props);
+                ensure_scratch(g);
+                PD_CUDA(cudaStreamSynchronize(g->stream));
+                cudaFree(d_centers);
+                cudaFree(d_radii);
+                *out = g;
+                return;
+            }
             PD_CUDA(cudaMalloc(&slot_masks, sizeof(uint64_t) * (size_t)slots * 8));
             PD_CUDA(cudaMalloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
             PD_CUDA(cudaMalloc(&ordinal, sizeof(int32_t) * (size_t)slots));
-            PD_CUDA(cudaMalloc(&g->d_table, sizeof(int32_t) * (size_t)slots));
             if (scalar_bytes == 8) {
                 const double eps = std::numeric_limits<double>::epsilon();
                 pack_mask_kernel<double><<<(unsigned)slots, 512, 0, g->stream>>>(
@@ -861,7 +948,7 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
                                     cudaMemcpyDeviceToHost, g->stream));
             PD_CUDA(cudaStreamSynchronize(g->stream));
             g->n_chunks = (int64_t)last_ord + last_flag;
-            if (g->n_chunks == 0)
+            if (g->n_chunks == 0 && chunk_lo == nullptr)
                 fail(PD_E_INPUT, "no node lies inside the phase band: the grid would be empty");
             PD_CUDA(cudaMalloc(&g->d_keys, sizeof(int32_t) * (size_t)(g->n_chunks * 3)));
             PD_CUDA(cudaMalloc(&g->d_masks, sizeof(uint64_t) * (size_t)(g->n_chunks * 8)));

@@ -77,7 +77,8 @@ struct pd_grid {
     int32_t* d_table = nullptr;  // chunk linear index -> ordinal, -1 absent
     std::vector<void*> cols;     // physical columns
     std::vector<int> column_of;  // logical property -> physical column
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;      // stream all work is issued on
+    cudaStream_t own_stream = nullptr;  // the grid's own stream
     pdb::ReduceScratch red;
     double* d_row = nullptr;  // 3 doubles: mass, min, max
 };
@@ -93,7 +94,8 @@ void launch_chunk_stats(pd_grid* g, const void* col, const uint64_t* masks);
 // part[1..2] over ordinals; writes {mass*cell_volume, min, max} to dst
 // (device) and, when flags != nullptr, ORs 4 into *flags if the mass is not
 // finite. Empty grids produce {0, +inf, -inf}.
-void launch_pairwise_finalize(pd_grid* g, double* dst, int* flags);
+void launch_pairwise_finalize(pd_grid* g, double* dst, int* flags, int64_t begin = 0,
+                              int64_t count = -1);
 // max over active nodes of a column (solver.hpp:139-154) into red.part.
 void launch_chunk_max(pd_grid* g, const void* col);
 

@@ -1,0 +1,255 @@
+"""Multi-GPU z-slab decomposition of the sparse block grid (north_star
+subsystem 4).
+
+Chunk ordinals ascend with the chunk linear index, which is z-slowest
+(sparse_block_grid.hpp:105-109), so a contiguous range of chunk layers is a
+contiguous ordinal range. Rank r owns chunk layers [z0, z1) and additionally
+holds one read-only ghost layer on each side (z0-1 and z1). Keys stay global,
+so the step kernel's box / neighbour logic is unchanged; the stepper runs on
+the owned ordinal range only (pd_stepper_set_range).
+
+Every update reads only step-n state of its 2*Dims face neighbours
+(solver.hpp:29-33), and an owned chunk reads only the one-node face plane of
+a ghost chunk that touches it. So after each step rank r sends
+  * the z=0 plane of its bottom owned layer to rank r-1 (its upper ghost), and
+  * the z=7 plane of its top owned layer to rank r+1 (its lower ghost),
+64 nodes x 8 B per chunk, over NCCL. D and phi are static and built
+identically on both sides, so they are never exchanged.
+
+The plan functions below are pure host logic (tested with gloo on CPU);
+``Domain`` binds them to the device grid and torch.distributed NCCL.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+FACE_ZLO = 4  # axis 2, side 0: the chunk's z=0 plane
+FACE_ZHI = 5  # axis 2, side 1: the chunk's z=7 plane
+
+
+def slab_bounds(n_layers: int, world: int, rank: int, weights: Optional[np.ndarray] = None):
+    """Chunk layers [z0, z1) owned by `rank`. With per-layer weights (e.g.
+    active nodes per layer) the cuts balance work (prefix sums), else layers
+    are split evenly."""
+    if weights is None:
+        z0 = (n_layers * rank) // world
+        z1 = (n_layers * (rank + 1)) // world
+        return z0, z1
+    c = np.concatenate([[0.0], np.cumsum(np.asarray(weights, np.float64))])
+    tot = c[-1]
+    cuts = [0] + [int(np.searchsorted(c, tot * k / world, side="left")) for k in range(1, world)] + [n_layers]
+    cuts = [min(max(x, 0), n_layers) for x in cuts]
+    for k in range(1, len(cuts)):
+        cuts[k] = max(cuts[k], cuts[k - 1])
+    return cuts[rank], cuts[rank + 1]
+
+
+@dataclass
+class ExchangePlan:
+    z0: int
+    z1: int
+    begin: int  # owned ordinal range [begin, end)
+    end: int
+    send_down: np.ndarray  # ordinals of the bottom owned layer (to rank-1)
+    send_up: np.ndarray  # ordinals of the top owned layer (to rank+1)
+    recv_down: np.ndarray  # lower ghost layer ordinals (from rank-1)
+    recv_up: np.ndarray  # upper ghost layer ordinals (from rank+1)
+
+
+def exchange_plan(keys: np.ndarray, z0: int, z1: int, rank: int, world: int) -> ExchangePlan:
+    """keys: (n, 3) int32 chunk keys of the local grid (owned + ghost layers)
+    in ascending linear order."""
+    kz = np.asarray(keys)[:, 2]
+    owned = np.nonzero((kz >= z0) & (kz < z1))[0]
+    begin = int(owned[0]) if owned.size else int(np.searchsorted(kz, z0))
+    end = int(owned[-1]) + 1 if owned.size else begin
+    assert np.all((kz[begin:end] >= z0) & (kz[begin:end] < z1)), "owned chunks must be contiguous"
+    none = np.zeros(0, np.int32)
+    send_down = np.nonzero(kz == z0)[0].astype(np.int32) if rank > 0 and z1 > z0 else none
+    send_up = np.nonzero(kz == z1 - 1)[0].astype(np.int32) if rank < world - 1 and z1 > z0 else none
+    recv_down = np.nonzero(kz == z0 - 1)[0].astype(np.int32) if rank > 0 else none
+    recv_up = np.nonzero(kz == z1)[0].astype(np.int32) if rank < world - 1 else none
+    return ExchangePlan(z0, z1, begin, end, send_down, send_up, recv_down, recv_up)
+
+
+def exchange_numpy(plan: ExchangePlan, u: np.ndarray, rank: int, world: int, dist) -> None:
+    """Host (gloo) version of the per-step halo exchange on (n, 512) slabs;
+    the device version is Domain.exchange. Same plan, same planes."""
+    import torch
+
+    def plane(ords, zc):
+        return np.ascontiguousarray(u[ords][:, zc * 64:(zc + 1) * 64])
+
+    ops = []
+    bufs = []
+    if rank > 0:
+        s = torch.from_numpy(plane(plan.send_down, 0).copy())
+        r = torch.empty((len(plan.recv_down), 64), dtype=s.dtype)
+        ops += [dist.P2POp(dist.isend, s, rank - 1), dist.P2POp(dist.irecv, r, rank - 1)]
+        bufs.append((plan.recv_down, 7, r))
+    if rank < world - 1:
+        s = torch.from_numpy(plane(plan.send_up, 7).copy())
+        r = torch.empty((len(plan.recv_up), 64), dtype=s.dtype)
+        ops += [dist.P2POp(dist.isend, s, rank + 1), dist.P2POp(dist.irecv, r, rank + 1)]
+        bufs.append((plan.recv_up, 0, r))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for ords, zc, r in bufs:
+        u[ords, zc * 64:(zc + 1) * 64] = r.numpy()
+
+
+class Domain:
+    """One rank's shard of a sphere-pack domain on its GPU."""
+
+    def __init__(self, n, pack, rank, world, device, dtype=np.float64):
+        import torch
+
+        from . import porediff as pd
+        from ._lib import lib
+
+        self.pd, self.lib = pd, lib
+        self.n, self.rank, self.world, self.device = n, rank, world, device
+        self.geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
+        cc = [(n + 7) // 8] * 3
+        self.cc = cc
+        z0, z1 = slab_bounds(cc[2], world, rank)
+        lo = (C.c_int64 * 3)(0, 0, max(0, z0 - 1))
+        hi = (C.c_int64 * 3)(cc[0], cc[1], min(cc[2], z1 + 1))
+        centers, radii = pack.arrays()
+        size = (C.c_int64 * 3)(*self.geom.size)
+        spacing = (C.c_double * 3)(*self.geom.spacing)
+        origin = (C.c_double * 3)(*self.geom.origin)
+        h = C.c_void_p()
+        pd._check(lib.pd_build_sphere_pack_region(
+            np.dtype(dtype).itemsize, size, spacing, origin, len(radii),
+            centers.ctypes.data_as(C.POINTER(C.c_double)), radii.ctypes.data_as(C.POINTER(C.c_double)),
+            0.0, math.inf, lo, hi, 4, 0, device, C.byref(h)))
+        nch = C.c_int64()
+        lib.pd_grid_info(h, C.byref(nch), None)
+        self.dev = pd.DeviceGrid(h, self.geom, dtype, int(nch.value), 4)
+        # sigmoid D across the interface (geometry.hpp:182-206), u0 hash
+        self.dev.populate_diffusion(0, 2, pd.DiffusionProfile(0.0, 1.0, 0.0, 4.0 * n))
+        self.dev.fill_hash(1, 1)
+        keys, masks = self.dev.layout()
+        self.plan = exchange_plan(keys, z0, z1, rank, world)
+        act = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).sum(axis=1)
+        self.owned_active = int(act[self.plan.begin:self.plan.end].sum())
+        self.owned_chunks = self.plan.end - self.plan.begin
+        self.torch = torch
+        self.stream = torch.cuda.current_stream(device)
+        lib.pd_grid_set_stream(self.dev.h, C.c_void_p(self.stream.cuda_stream))
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(f"cuda:{device}")
+        self.d_send_down, self.d_send_up = t(self.plan.send_down), t(self.plan.send_up)
+        self.d_recv_down, self.d_recv_up = t(self.plan.recv_down), t(self.plan.recv_up)
+        tt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+        mk = lambda k: torch.empty((max(1, k), 64), dtype=tt, device=f"cuda:{device}")
+        self.b_send_down, self.b_send_up = mk(len(self.plan.send_down)), mk(len(self.plan.send_up))
+        self.b_recv_down, self.b_recv_up = mk(len(self.plan.recv_down)), mk(len(self.plan.recv_up))
+        self._kernel_ms = 0.0
+        self._steps = 0
+
+    def total_chunks(self, world):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([self.owned_chunks], dtype=torch.float64, device=f"cuda:{self.device}")
+        if world > 1:
+            dist.all_reduce(t)
+        return int(t.item())
+
+    def stepper(self, dt_frac=0.4, sink_rate=1.0, sink_width=1.0):
+        import torch
+        import torch.distributed as dist
+        pd = self.pd
+        dmax = self.dev.max_active(2)
+        t = torch.tensor([dmax], dtype=torch.float64, device=f"cuda:{self.device}")
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dmax = float(t.item())
+        cfg = pd.SimulationConfig(dt=dt_frac * pd.stability_dt(self.geom, dmax), n_steps=1 << 40,
+                                  record_every=1 << 40)
+        cfg.reaction = pd.ReactionSpec.surface_sink(sink_rate, sink_width)
+        ccfg = pd._to_c_config(cfg, -1)
+        h = C.c_void_p()
+        pd._check(self.lib.pd_stepper_create(self.dev.h, C.byref(ccfg), 0, 1, 2, 3, C.byref(h)))
+        pd._check(self.lib.pd_stepper_set_range(h, self.plan.begin, self.plan.end))
+        self.cfg = cfg
+        return h
+
+    def exchange(self):
+        """Device halo exchange of the logical "u" planes (after a step)."""
+        import torch.distributed as dist
+        lib, pd = self.lib, self.pd
+        P = lambda t: C.c_void_p(t.data_ptr())
+        ops = []
+        if self.rank > 0 and len(self.plan.send_down):
+            pd._check(lib.pd_grid_pack_face(self.dev.h, 1, P(self.d_send_down), len(self.plan.send_down),
+                                            FACE_ZLO, P(self.b_send_down)))
+        if self.rank < self.world - 1 and len(self.plan.send_up):
+            pd._check(lib.pd_grid_pack_face(self.dev.h, 1, P(self.d_send_up), len(self.plan.send_up),
+                                            FACE_ZHI, P(self.b_send_up)))
+        if self.rank > 0:
+            if len(self.plan.send_down):
+                ops.append(dist.P2POp(dist.isend, self.b_send_down[:len(self.plan.send_down)], self.rank - 1))
+            if len(self.plan.recv_down):
+                ops.append(dist.P2POp(dist.irecv, self.b_recv_down[:len(self.plan.recv_down)], self.rank - 1))
+        if self.rank < self.world - 1:
+            if len(self.plan.send_up):
+                ops.append(dist.P2POp(dist.isend, self.b_send_up[:len(self.plan.send_up)], self.rank + 1))
+            if len(self.plan.recv_up):
+                ops.append(dist.P2POp(dist.irecv, self.b_recv_up[:len(self.plan.recv_up)], self.rank + 1))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if self.rank > 0 and len(self.plan.recv_down):
+            pd._check(lib.pd_grid_unpack_face(self.dev.h, 1, P(self.d_recv_down), len(self.plan.recv_down),
+                                              FACE_ZHI, P(self.b_recv_down)))
+        if self.rank < self.world - 1 and len(self.plan.recv_up):
+            pd._check(lib.pd_grid_unpack_face(self.dev.h, 1, P(self.d_recv_up), len(self.plan.recv_up),
+                                              FACE_ZLO, P(self.b_recv_up)))
+
+    def run(self, stepper, step0: int, n: int) -> float:
+        """Advances n steps; returns the device milliseconds (CUDA events on
+        the grid's stream) of the whole sequence."""
+        torch, lib, pd = self.torch, self.lib, self.pd
+        rows = (pd._lib.pd_diag * 1)()
+        nr = C.c_int64()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        kms = 0.0
+        e0.record(self.stream)
+        if self.world == 1:
+            pd._check(lib.pd_stepper_run(stepper, step0, n, 1 << 40, None, rows, C.byref(nr)))
+            ms_k = C.c_double()
+            lib.pd_stepper_last_ms(stepper, C.byref(ms_k))
+            kms = ms_k.value
+        else:
+            for s in range(n):
+                pd._check(lib.pd_stepper_run(stepper, step0 + s, 1, 1 << 40, None, rows, C.byref(nr)))
+                ms_k = C.c_double()
+                lib.pd_stepper_last_ms(stepper, C.byref(ms_k))
+                kms += ms_k.value
+                self.exchange()
+        e1.record(self.stream)
+        e1.synchronize()
+        self._kernel_ms += kms
+        self._steps += n
+        return e0.elapsed_time(e1)
+
+    def kernel_ms(self, stepper) -> float:
+        """Average device time of one step kernel launch so far."""
+        return self._kernel_ms / max(1, self._steps)
+
+    def launches(self, stepper) -> int:
+        n = C.c_int64()
+        self.lib.pd_stepper_launch_count(stepper, C.byref(n))
+        return int(n.value)
+
+
+def build_domain(n, pack, rank, world, device=0, dtype=np.float64) -> Domain:
+    return Domain(n, pack, rank, world, device, dtype)

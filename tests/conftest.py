@@ -1,0 +1,43 @@
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+for p in (str(ROOT), str(ROOT / "tests")):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running CPU oracle case")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+    return json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def ref():
+    """The reference compiled in place (oracle/_ref); skipped if not built."""
+    from oracle.pyoracle import REF_SO, Ref
+    if not REF_SO.exists():
+        pytest.skip("oracle/_ref not built (reference absent at build time)")
+    return Ref()
+
+
+@pytest.fixture(scope="session")
+def port():
+    from oracle.pyoracle import Port
+    return Port()
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    from paper_2304_11165_b200 import _lib
+    if _lib.device_count() < 1:
+        pytest.fail("no CUDA device visible to libporediff_b200 (gpu tests need a B200)")
+    return _lib
