@@ -17,8 +17,8 @@ of u/u_next/D) is far larger than L2, so no L2 flush is needed between steps.
 
 Multi-GPU (torchrun, one rank per GPU): z-slab decomposition by chunk
 layers; each rank builds its slab plus one ghost chunk layer per side and
-exchanges boundary u layers with NCCL every step (weak scaling: --n-per-gpu
-z-extent per rank). See DESIGN.md.
+exchanges boundary u planes with NCCL every step. Strong scaling: the same
+2048^3 domain is split over N GPUs. See DESIGN.md.
 """
 from __future__ import annotations
 
@@ -252,7 +252,7 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value / 1e9, "unit": "GPts/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-built sphere pack)",
             "config": config_dict(args, world),
             "active_nodes": int(active), "chunks": int(dom.total_chunks(world)),
@@ -345,7 +345,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(args, world),
         "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": cores, "kind": "reference",
                          "sample": f"each step = reference run_simulation of {args.cpu_steps} FTCS steps on the "

@@ -18,6 +18,7 @@
 //     only on record steps; every step still detects non-finite values with
 //     the reference's lowest-ordinal/first-offset rule (solver.hpp:250-260).
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <initializer_list>
@@ -27,31 +28,7 @@
 
 namespace pdb {
 
-template <class T>
-struct StepArgs {
-    const T* __restrict__ u;
-    T* __restrict__ un;
-    const T* __restrict__ d;
-    const T* __restrict__ src;
-    const uint64_t* __restrict__ active;
-    const uint64_t* __restrict__ fluid;
-    const uint64_t* __restrict__ sink;
-    const int32_t* __restrict__ nbr;
-    const int32_t* __restrict__ keys;
-    int64_t size[3];
-    T inv_dx2[3];
-    T dt, neg_k, src_factor;
-    T bcv[6];
-    int dirichlet;  // bit (axis*2+side)
-    int reaction;   // PD_REACTION_*
-    double* p_mass;
-    double* p_mn;
-    double* p_mx;
-    unsigned long long* bad_key;  // (ordinal << 10) | offset, atomicMin
-    int* flags;                   // per step of the batch: 1 bad, 2 huge, 4 mass
-    int k;                        // step index within the batch
-    int64_t ord0;                 // first chunk ordinal of the launch
-};
+
 
 __device__ __forceinline__ double min_left(double l, double r) { return (r < l) ? r : l; }
 __device__ __forceinline__ double max_left(double l, double r) { return (l < r) ? r : l; }
@@ -322,6 +299,8 @@ struct pd_stepper {
     double last_ms = 0.0;
     int64_t launches = 0;
     int64_t begin = 0, end = 0;  // owned ordinal range
+    pdb::MarchPlan plan;         // 3-D FP64 column-march fast path
+    bool use_march = true;
 };
 
 namespace {
@@ -396,7 +375,9 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         fill_args<double>(s, a, u, un, factor);
         a.k = k;
         a.ord0 = s->begin;
-        if (g->dims == 3) {
+        if (!diag && s->use_march && s->plan.ready) {
+            march_launch(g, s->plan, a, s->cfg.reaction_kind);
+        } else if (g->dims == 3) {
             if (diag) ftcs_step_kernel<double, 3, true><<<nb, 512, 0, g->stream>>>(a);
             else ftcs_step_kernel<double, 3, false><<<nb, 512, 0, g->stream>>>(a);
         } else {
@@ -501,6 +482,9 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
                 PD_CUDA(cudaGetLastError());
             }
             ensure_scratch(g);
+            const char* nm = getenv("PD_NO_MARCH");
+            s->use_march = !(nm && nm[0] == '1');
+            if (s->use_march) march_build(g, s->d_nbr, 0, g->n_chunks, &s->plan);
             PD_CUDA(cudaStreamSynchronize(g->stream));
         } catch (...) {
             pd_stepper_destroy(s);
@@ -521,6 +505,7 @@ int pd_stepper_destroy(pd_stepper* s) {
         cudaFree(s->d_flags);
         cudaFree(s->d_bad);
         cudaFree(s->d_rows);
+        march_free(&s->plan);
         if (s->ev0) cudaEventDestroy(s->ev0);
         if (s->ev1) cudaEventDestroy(s->ev1);
     }
@@ -534,6 +519,10 @@ int pd_stepper_set_range(pd_stepper* s, int64_t begin, int64_t end) {
             fail(PD_E_INPUT, "stepper ordinal range outside the grid");
         s->begin = begin;
         s->end = end;
+        if (s->use_march && s->g->dims == 3 && s->g->tbytes == 8) {
+            DeviceGuard dg(s->g->device);
+            march_build(s->g, s->d_nbr, begin, end, &s->plan);
+        }
     });
 }
 

@@ -101,6 +101,46 @@ void launch_chunk_max(pd_grid* g, const void* col);
 
 int device_of(const pd_grid* g);
 
+// Arguments of one FTCS step launch (all pointers are device pointers).
+template <class T>
+struct StepArgs {
+    const T* __restrict__ u;
+    T* __restrict__ un;
+    const T* __restrict__ d;
+    const T* __restrict__ src;
+    const uint64_t* __restrict__ active;
+    const uint64_t* __restrict__ fluid;
+    const uint64_t* __restrict__ sink;
+    const int32_t* __restrict__ nbr;
+    const int32_t* __restrict__ keys;
+    int64_t size[3];
+    T inv_dx2[3];
+    T dt, neg_k, src_factor;
+    T bcv[6];
+    int dirichlet;  // bit (axis*2+side)
+    int reaction;   // PD_REACTION_*
+    double* p_mass;
+    double* p_mn;
+    double* p_mx;
+    unsigned long long* bad_key;  // (ordinal << 10) | offset, atomicMin
+    int* flags;                   // per step of the batch: 1 bad, 2 huge, 4 mass
+    int k;                        // step index within the batch
+    int64_t ord0;                 // first chunk ordinal of the launch
+};
+
+// Column-march plan of the 3-D FP64 fast path (pd_march.cu).
+struct MarchPlan {
+    int32_t* d_stream = nullptr;      // chunk ordinals, per-CTA streams concatenated
+    int32_t* d_stream_off = nullptr;  // grid+1 offsets
+    int4* d_desc = nullptr;           // 2 x int4 per chunk: nbr[0..5], packed key, flags
+    int grid = 0;
+    int64_t n = 0;
+    bool ready = false;
+};
+void march_build(pd_grid* g, const int32_t* d_nbr, int64_t begin, int64_t end, MarchPlan* plan);
+void march_free(MarchPlan* plan);
+void march_launch(pd_grid* g, const MarchPlan& plan, const StepArgs<double>& a, int reaction);
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

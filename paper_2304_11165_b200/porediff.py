@@ -282,6 +282,7 @@ def pairwise_sum(values) -> float:
 def hash_unit_value(seed: int, key: int) -> float:
     """config.hpp:558-564."""
     m = (1 << 64) - 1
+    seed, key = int(seed), int(key)
     z = (seed + 0x9E3779B97F4A7C15 * (key + 1)) & m
     z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
     z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m

@@ -100,7 +100,9 @@ def test_error_messages_match_oracle(cuda, port):
     base = host_case("disk24_sink")
     keys, masks = base.keys(), base.masks()
     props = {c: base.channel_data(c).copy() for c in ("phi", "u", "D", "u_next")}
-    props["u"][4, 9] = np.inf
+    act = base.active_bool()
+    j, off = [int(v[len(v) // 2]) for v in np.nonzero(act)]
+    props["u"][j, off] = np.inf
     h = 2.0 / 24
     dmax = float(props["D"][base.active_bool()].max())
     bound = pd.stability_dt(base.geom, dmax)
@@ -132,7 +134,9 @@ def test_nonfinite_after_several_steps_keeps_state(cuda, port):
     base = host_case("disk24_sink")
     keys, masks = base.keys(), base.masks()
     props = {c: base.channel_data(c).copy() for c in ("phi", "u", "D", "u_next")}
-    props["u"][3, 10] = 1e300
+    act = base.active_bool()
+    j, off = [int(v[len(v) // 3]) for v in np.nonzero(act)]
+    props["u"][j, off] = 1e300
     h = 2.0 / 24
     dt = 0.9 * pd.stability_dt(base.geom, float(props["D"][base.active_bool()].max()))
     ocfg = make_config(dt * 3.0, 40, enforce_stability=False)  # unstable: grows until overflow

@@ -1,0 +1,135 @@
+"""z-slab sharding on ONE GPU: two (or three) shard grids built with their
+ghost chunk layers (pd_build_sphere_pack_region), stepped on their owned
+ordinal range (pd_stepper_set_range) and exchanging face planes with
+pd_grid_pack_face / pd_grid_unpack_face after every step, reproduce the
+unsharded run bit for bit. The NCCL transport used by bench.py moves exactly
+these buffers (shard.Domain.exchange)."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(pd, lib, geom, centers, radii, lo, hi):
+    h = C.c_void_p()
+    pd._check(lib.pd_build_sphere_pack_region(
+        8, (C.c_int64 * 3)(*geom.size), (C.c_double * 3)(*geom.spacing), (C.c_double * 3)(*geom.origin),
+        len(radii), centers.ctypes.data_as(C.POINTER(C.c_double)), radii.ctypes.data_as(C.POINTER(C.c_double)),
+        0.0, math.inf, (C.c_int64 * 3)(*lo), (C.c_int64 * 3)(*hi), 4, 0, 0, C.byref(h)))
+    n = C.c_int64()
+    lib.pd_grid_info(h, C.byref(n), None)
+    dev = pd.DeviceGrid(h, geom, np.float64, int(n.value), 4)
+    dev.populate_diffusion(0, 2, pd.DiffusionProfile(0.02, 1.0, 0.0, 4.0 * geom.size[0]))
+    dev.fill_hash(1, 11)
+    return dev
+
+
+def _stepper(pd, lib, dev, dt, rng=None):
+    cfg = pd.SimulationConfig(dt=dt, n_steps=1 << 40, record_every=1 << 40)
+    cfg.reaction = pd.ReactionSpec.surface_sink(2.0, 1.0)
+    cfg.outer_bc[0] = pd.FaceBc.dirichlet(1.0)
+    cc = pd._to_c_config(cfg, -1)
+    h = C.c_void_p()
+    pd._check(lib.pd_stepper_create(dev.h, C.byref(cc), 0, 1, 2, 3, C.byref(h)))
+    if rng is not None:
+        pd._check(lib.pd_stepper_set_range(h, *rng))
+    return h
+
+
+@pytest.mark.parametrize("world,n", [(2, 48), (3, 61)])
+def test_sharded_run_equals_unsharded(world, n, cuda):
+    import torch
+
+    from paper_2304_11165_b200 import porediff as pd
+    from paper_2304_11165_b200 import shard
+    from paper_2304_11165_b200._lib import lib
+    from paper_2304_11165_b200.synthetic import SpherePacking
+
+    geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
+    pk = SpherePacking.random((0, 0, 0), (1, 1, 1), 40, 0.06, 0.14, 99)
+    centers, radii = pk.arrays()
+    cc = (n + 7) // 8
+    full = _build(pd, lib, geom, centers, radii, (0, 0, 0), (cc, cc, cc))
+    dmax = full.max_active(2)
+    dt = 0.45 * pd.stability_dt(geom, dmax)
+    steps = 12
+
+    s_full = _stepper(pd, lib, full, dt)
+    rows = (pd._lib.pd_diag * 1)()
+    nr = C.c_int64()
+    pd._check(lib.pd_stepper_run(s_full, 0, steps, 1 << 40, None, rows, C.byref(nr)))
+    u_full = full.download(1)
+    keys_full, _ = full.layout()
+
+    shards = []
+    for r in range(world):
+        z0, z1 = shard.slab_bounds(cc, world, r)
+        dev = _build(pd, lib, geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)))
+        keys, _ = dev.layout()
+        plan = shard.exchange_plan(keys, z0, z1, r, world)
+        s = _stepper(pd, lib, dev, dt, (plan.begin, plan.end))
+        shards.append((dev, plan, s, keys))
+
+    def ords(a):
+        return torch.from_numpy(np.ascontiguousarray(a, np.int32)).cuda()
+
+    for step in range(steps):
+        for dev, plan, s, _ in shards:
+            pd._check(lib.pd_stepper_run(s, step, 1, 1 << 40, None, rows, C.byref(nr)))
+        torch.cuda.synchronize()
+        # exchange: plane z=0 of my bottom layer -> lower rank's upper ghost
+        # (its z=0 plane), plane z=7 of my top layer -> upper rank's lower ghost
+        sent = {}
+        for r, (dev, plan, s, _) in enumerate(shards):
+            for lst, face, to in ((plan.send_down, shard.FACE_ZLO, r - 1), (plan.send_up, shard.FACE_ZHI, r + 1)):
+                if len(lst) == 0:
+                    continue
+                buf = torch.empty((len(lst), 64), dtype=torch.float64, device="cuda")
+                o = ords(lst)
+                pd._check(lib.pd_grid_pack_face(dev.h, 1, C.c_void_p(o.data_ptr()), len(lst), face,
+                                                C.c_void_p(buf.data_ptr())))
+                sent[(r, to)] = (buf, o)
+        torch.cuda.synchronize()
+        for r, (dev, plan, s, _) in enumerate(shards):
+            for lst, face, frm in ((plan.recv_down, shard.FACE_ZHI, r - 1), (plan.recv_up, shard.FACE_ZLO, r + 1)):
+                if len(lst) == 0:
+                    continue
+                buf, _ = sent[(frm, r)]
+                assert buf.shape[0] == len(lst)
+                o = ords(lst)
+                pd._check(lib.pd_grid_unpack_face(dev.h, 1, C.c_void_p(o.data_ptr()), len(lst), face,
+                                                  C.c_void_p(buf.data_ptr())))
+        torch.cuda.synchronize()
+
+    lin_full = (keys_full[:, 2].astype(np.int64) * cc + keys_full[:, 1]) * cc + keys_full[:, 0]
+    pos = {int(l): i for i, l in enumerate(lin_full)}
+    covered = 0
+    for dev, plan, s, keys in shards:
+        u = dev.download(1)
+        for i in range(plan.begin, plan.end):
+            l = (int(keys[i, 2]) * cc + int(keys[i, 1])) * cc + int(keys[i, 0])
+            j = pos[l]
+            assert np.array_equal(u[i].view(np.uint64), u_full[j].view(np.uint64)), (i, keys[i])
+            covered += 1
+    assert covered == len(keys_full)
+    for dev, plan, s, _ in shards:
+        lib.pd_stepper_destroy(s)
+        dev.close()
+    lib.pd_stepper_destroy(s_full)
+    full.close()
+
+
+def test_march_and_tile_kernels_agree(cuda, golden, monkeypatch):
+    """The column-march fast path (non-record steps) and the staged-tile
+    kernel (record steps / PD_NO_MARCH=1) give identical bits."""
+    from cases import CASES, host_case, sha, sim_config
+    from paper_2304_11165_b200 import porediff as pd
+    name = "contract40"
+    spec, gold = CASES[name], golden[name]
+    monkeypatch.setenv("PD_NO_MARCH", "1")
+    grid = host_case(name)
+    pd.run_simulation(grid, sim_config(spec, float.fromhex(gold["dt"])))
+    assert sha(grid.channel_data("u")) == gold["sha_outputs"]["u"]
