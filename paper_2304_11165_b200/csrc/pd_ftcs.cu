@@ -307,6 +307,15 @@ namespace {
 
 constexpr int64_t kBatch = 512;
 
+void march_build_for(pd_stepper* s, int64_t begin, int64_t end) {
+    pd_grid* g = s->g;
+    int dir = 0;
+    for (int f = 0; f < 2 * g->dims; ++f)
+        if (s->cfg.bc_type[f] == PD_BC_DIRICHLET) dir |= 1 << f;
+    const void* dcol = g->cols[(size_t)g->column_of[(size_t)s->prop_d]];
+    march_build(g, s->d_nbr, s->d_fluid, dcol, dir, begin, end, &s->plan);
+}
+
 void validate(const pd_grid* g, const pd_sim_config* c, int prop_src,
               std::initializer_list<int> solver_props) {
     // solver.hpp:304-331, messages verbatim
@@ -484,7 +493,7 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             ensure_scratch(g);
             const char* nm = getenv("PD_NO_MARCH");
             s->use_march = !(nm && nm[0] == '1');
-            if (s->use_march) march_build(g, s->d_nbr, 0, g->n_chunks, &s->plan);
+            if (s->use_march) march_build_for(s, 0, g->n_chunks);
             PD_CUDA(cudaStreamSynchronize(g->stream));
         } catch (...) {
             pd_stepper_destroy(s);
@@ -521,7 +530,7 @@ int pd_stepper_set_range(pd_stepper* s, int64_t begin, int64_t end) {
         s->end = end;
         if (s->use_march && s->g->dims == 3 && s->g->tbytes == 8) {
             DeviceGuard dg(s->g->device);
-            march_build(s->g, s->d_nbr, begin, end, &s->plan);
+            march_build_for(s, begin, end);
         }
     });
 }

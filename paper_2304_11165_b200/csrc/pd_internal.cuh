@@ -130,14 +130,16 @@ struct StepArgs {
 
 // Column-march plan of the 3-D FP64 fast path (pd_march.cu).
 struct MarchPlan {
-    int32_t* d_stream = nullptr;      // chunk ordinals, per-CTA streams concatenated
-    int32_t* d_stream_off = nullptr;  // grid+1 offsets
+    int32_t* d_stream = nullptr;      // owned chunk ordinals in schedule order
+    int32_t* d_stream_off = nullptr;  // (unused, reserved)
     int4* d_desc = nullptr;           // 2 x int4 per chunk: nbr[0..5], packed key, flags
+    double* d_deff = nullptr;         // D on fluid nodes, -inf elsewhere (static per run)
     int grid = 0;
     int64_t n = 0;
     bool ready = false;
 };
-void march_build(pd_grid* g, const int32_t* d_nbr, int64_t begin, int64_t end, MarchPlan* plan);
+void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const void* d_dcol,
+                 int dirichlet, int64_t begin, int64_t end, MarchPlan* plan);
 void march_free(MarchPlan* plan);
 void march_launch(pd_grid* g, const MarchPlan& plan, const StepArgs<double>& a, int reaction);
 
