@@ -27,6 +27,7 @@
 //   fast path uses 0. Nodes whose fast result is non-finite, and chunks that
 //   touch a Dirichlet outer face, take the exact generic path.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -90,7 +91,7 @@ __device__ __forceinline__ Desc load_desc(const StepArgs<double>& A, const int4*
 // and of the six neighbour face layers; absent neighbours get the sentinel.
 __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<double>& A,
                                       const double* __restrict__ deff, int c, const Desc& D,
-                                      int t) {
+                                      int t, int dbg) {
     const int z = t >> 5, y = (t >> 2) & 7, xp = t & 3, x0 = 2 * xp, lane = t & 31;
     const int o = z * 64 + y * 8 + x0;
     const int bp = y * 8 + x0;
@@ -104,7 +105,7 @@ __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<
     else
         *reinterpret_cast<double2*>(&S.d[T]) = make_double2(sent, sent);
     if (xp == 0) {
-        const int j = D.a.x;
+        const int j = (dbg & 1) ? -1 : D.a.x;
         if (j >= 0) {
             const int64_t src = (int64_t)j * 512 + z * 64 + y * 8 + 7;
             cp8(&S.u[T - 1], U + src);
@@ -114,7 +115,7 @@ __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<
         }
     }
     if (xp == 3) {
-        const int j = D.a.y;
+        const int j = (dbg & 1) ? -1 : D.a.y;
         if (j >= 0) {
             const int64_t src = (int64_t)j * 512 + z * 64 + y * 8;
             cp8(&S.u[T + 2], U + src);
@@ -124,7 +125,7 @@ __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<
         }
     }
     if (y == 0) {
-        const int j = D.a.z;
+        const int j = (dbg & 2) ? -1 : D.a.z;
         if (j >= 0) {
             const int64_t src = (int64_t)j * 512 + z * 64 + 56 + x0;
             cp16(&S.u[T - 10], U + src);
@@ -134,7 +135,7 @@ __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<
         }
     }
     if (y == 7) {
-        const int j = D.a.w;
+        const int j = (dbg & 2) ? -1 : D.a.w;
         if (j >= 0) {
             const int64_t src = (int64_t)j * 512 + z * 64 + x0;
             cp16(&S.u[T + 10], U + src);
@@ -144,7 +145,7 @@ __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<
         }
     }
     if (z == 0) {
-        const int j = D.b.x;
+        const int j = (dbg & 4) ? -1 : D.b.x;
         if (j >= 0) {
             const int64_t src = (int64_t)j * 512 + 448 + y * 8 + x0;
             cp16(&S.u[T - 100], U + src);
@@ -154,7 +155,7 @@ __device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<
         }
     }
     if (z == 7) {
-        const int j = D.b.y;
+        const int j = (dbg & 4) ? -1 : D.b.y;
         if (j >= 0) {
             const int64_t src = (int64_t)j * 512 + y * 8 + x0;
             cp16(&S.u[T + 100], U + src);
@@ -321,7 +322,7 @@ __device__ __forceinline__ void compute(const MarchStage& S, const int4 meta,
 template <int REACTION>
 __global__ void __launch_bounds__(kMarchThreads, 3)
     ftcs_march_kernel(StepArgs<double> A, const int32_t* __restrict__ sched, int64_t n,
-                      const int4* __restrict__ desc, const double* __restrict__ deff) {
+                      const int4* __restrict__ desc, const double* __restrict__ deff, int dbg) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchStage* st = reinterpret_cast<MarchStage*>(smem_raw);
     __shared__ int4 meta[kStages];
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(kMarchThreads, 3)
         int c_after = 0;
         if (s + 1 < cnt) d_next = load_desc(A, desc, c_next, z);
         if (s + 2 < cnt) c_after = ids[s + 2];
-        if (s < cnt) issue(st[s], meta[s], A, deff, c_issue, d_issue, t);
+        if (s < cnt) issue(st[s], meta[s], A, deff, c_issue, d_issue, t, dbg);
         cp_commit();
         c_issue = c_next;
         d_issue = d_next;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kMarchThreads, 3)
         int c_after = 0;
         if (qi + 1 < cnt) d_next = load_desc(A, desc, c_next, z);
         if (qi + 2 < cnt) c_after = ids[qi + 2];
-        if (qi < cnt) issue(st[qi % kStages], meta[qi % kStages], A, deff, c_issue, d_issue, t);
+        if (qi < cnt) issue(st[qi % kStages], meta[qi % kStages], A, deff, c_issue, d_issue, t, dbg);
         cp_commit();
         c_issue = c_next;
         d_issue = d_next;
@@ -487,12 +488,18 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
 
 void march_launch(pd_grid* g, const MarchPlan& p, const StepArgs<double>& a, int reaction) {
     const size_t bytes = sizeof(MarchStage) * kStages;
+    // PD_MARCH_DBG: measurement-only switch that skips halo classes
+    // (1 x, 2 y, 4 z); results are then wrong. Never set in tests/bench.
+    static const int dbg = [] {
+        const char* e = getenv("PD_MARCH_DBG");
+        return e ? atoi(e) : 0;
+    }();
     if (reaction == PD_REACTION_SURFACE_SINK)
-        ftcs_march_kernel<1><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff);
+        ftcs_march_kernel<1><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff, dbg);
     else if (reaction == PD_REACTION_VOLUMETRIC)
-        ftcs_march_kernel<2><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff);
+        ftcs_march_kernel<2><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff, dbg);
     else
-        ftcs_march_kernel<0><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff);
+        ftcs_march_kernel<0><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff, dbg);
     PD_CUDA(cudaGetLastError());
 }
 
