@@ -659,6 +659,7 @@ int pd_grid_destroy(pd_grid* g) {
 
 int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs) {
     return guarded([&] {
+        g->generation++;
         DeviceGuard dg(g->device);
         void* c = col_ptr(g, prop);
         if (g->n_chunks == 0) return;
@@ -669,6 +670,7 @@ int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs) {
 
 int pd_grid_upload_device(pd_grid* g, int prop, const void* dev_slabs) {
     return guarded([&] {
+        g->generation++;
         DeviceGuard dg(g->device);
         void* c = col_ptr(g, prop);
         if (g->n_chunks == 0) return;
@@ -724,6 +726,7 @@ int pd_grid_swap(pd_grid* g, int a, int b) {
         check_prop(g, a);
         check_prop(g, b);
         std::swap(g->column_of[(size_t)a], g->column_of[(size_t)b]);
+        g->generation++;
     });
 }
 
@@ -735,7 +738,8 @@ int pd_grid_column_of(const pd_grid* g, int prop, int* column) {
 }
 
 int pd_grid_device_ptr(pd_grid* g, int prop, void** ptr) {
-    return guarded([&] { *ptr = col_ptr(g, prop); });
+    return guarded([&] {
+        g->generation++; *ptr = col_ptr(g, prop); });
 }
 
 int pd_grid_info(const pd_grid* g, int64_t* n_chunks, int64_t* active_nodes) {
@@ -805,6 +809,7 @@ int pd_grid_max_active(pd_grid* g, int prop, double* out) {
 int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_min, double d_max,
                                double gamma1, double gamma2) {
     return guarded([&] {
+        g->generation++;
         if (d_min < 0.0) fail(PD_E_INPUT, "d_min must be non-negative");
         if (!(d_max > 0.0)) fail(PD_E_INPUT, "d_max must be positive");
         DeviceGuard dg(g->device);
@@ -824,6 +829,7 @@ int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_mi
 
 int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed) {
     return guarded([&] {
+        g->generation++;
         DeviceGuard dg(g->device);
         void* x = col_ptr(g, prop);
         if (g->n_chunks == 0) return;
@@ -840,6 +846,7 @@ int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed) {
 
 int pd_grid_fill_const(pd_grid* g, int prop, double value) {
     return guarded([&] {
+        g->generation++;
         DeviceGuard dg(g->device);
         void* x = col_ptr(g, prop);
         if (g->n_chunks == 0) return;

@@ -81,6 +81,7 @@ struct pd_grid {
     cudaStream_t own_stream = nullptr;  // the grid's own stream
     pdb::ReduceScratch red;
     double* d_row = nullptr;  // 3 doubles: mass, min, max
+    uint64_t generation = 0;  // bumped by every host-visible write to a column
 };
 
 namespace pdb {
@@ -128,20 +129,24 @@ struct StepArgs {
     int64_t ord0;                 // first chunk ordinal of the launch
 };
 
-// Column-march plan of the 3-D FP64 fast path (pd_march.cu).
+// Warp-specialized march plan of the 3-D FP64 fast path (pd_march.cu).
 struct MarchPlan {
-    int32_t* d_stream = nullptr;      // owned chunk ordinals in schedule order
-    int32_t* d_stream_off = nullptr;  // (unused, reserved)
-    int4* d_desc = nullptr;           // 2 x int4 per chunk: nbr[0..5], packed key, flags
-    double* d_deff = nullptr;         // D on fluid nodes, -inf elsewhere (static per run)
+    int32_t* d_stream = nullptr;   // owned chunk ordinals in schedule order
+    int32_t* d_desc = nullptr;     // 8 ints per chunk: nbr[0..5], packed key, flags
+    double* d_deff = nullptr;      // D on fluid nodes, -inf elsewhere (static per run)
+    double* d_xfd = nullptr;       // x=0 / x=7 planes of D_eff [c][2][64]
+    double* d_xf[2] = {nullptr, nullptr};  // x planes of u / u_next (double-buffered)
+    int* d_counter = nullptr;      // per-step dynamic batch counters
     int grid = 0;
+    int cur = 0;                   // d_xf[cur] mirrors the current u
     int64_t n = 0;
     bool ready = false;
 };
 void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const void* d_dcol,
                  int dirichlet, int64_t begin, int64_t end, MarchPlan* plan);
 void march_free(MarchPlan* plan);
-void march_launch(pd_grid* g, const MarchPlan& plan, const StepArgs<double>& a, int reaction);
+void march_extract_xfaces(pd_grid* g, MarchPlan& plan, const void* col);
+void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction);
 
 struct DeviceGuard {
     int prev = -1;

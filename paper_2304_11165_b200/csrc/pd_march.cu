@@ -1,31 +1,38 @@
-// Column-ordered, cp.async-pipelined FTCS step for 3-D FP64 grids — the
+// Warp-specialized, mbarrier-pipelined FTCS step for 3-D FP64 grids — the
 // bandwidth path (BASELINE.json configs C1-C5).
 //
 // Same per-node result, bit for bit, as ftcs_step_kernel (pd_ftcs.cu) and the
 // reference (solver.hpp:360-455); what changes is how bytes and instructions
-// are spent:
+// are spent.
 //
 // * Schedule. Chunks are ordered (z-block of kSeg layers, y, x, z): runs of a
-//   chunk column inside a z-block are contiguous, neighbouring columns follow
-//   each other. Each CTA takes kBatch consecutive chunks of that order; the
-//   hardware dispatches CTAs in order as SM slots free up, so the set of chunks
-//   in flight is always a contiguous window of the schedule and every x/y/z
-//   face halo a CTA reads was just streamed by its neighbours (L2 hit).
-// * Staging. A kStages-deep cp.async ring stages each chunk's u / D into a
-//   padded 10^3 tile (body + the six one-node face layers of the neighbour
-//   chunks). Body pairs without an active (u) or fluid (D) node are never read
-//   from HBM.
-// * Usability without masks. The stepper keeps D_eff = fluid ? D : -inf
-//   (static per run). A neighbour is usable iff it is fluid
-//   (solver.hpp:374,379-381), i.e. iff the face sum d_a + d_b is not -inf, so
-//   the substitution rule costs one integer compare per face.
+//   chunk column inside a z-block are contiguous and neighbouring columns
+//   follow each other. Persistent CTAs (2 per SM) grab kBatch consecutive
+//   chunks of that order with an atomic counter, so the chunks in flight are
+//   always a contiguous window of the schedule and the face halos a CTA reads
+//   were just streamed by its neighbours (L2 hits).
+// * Producer warp. One warp per CTA streams chunk after chunk into a
+//   kStages-deep shared-memory ring with cp.async (16-B copies; body pairs
+//   with no active / fluid node are never read from HBM) and signals each
+//   stage through an mbarrier (cp.async.mbarrier.arrive). Descriptors and
+//   masks are prefetched one chunk ahead, chunk ids one batch ahead, so the
+//   producer never waits on its own loads.
+// * Contiguous halos. x faces are 8-B strided in a chunk slab, so every step
+//   also writes the x=0 / x=7 planes of u_next into a side array (64 doubles
+//   per face, contiguous) and the stepper keeps the same for D_eff; y and z
+//   face layers are read directly (64-B rows / 512-B planes).
+// * Consumer warps (8). Warp w computes z-plane w, two x-adjacent nodes per
+//   thread, from shared memory only.
+// * Usability without masks. D_eff = fluid ? D : -inf (static per run). A
+//   neighbour is usable iff it is fluid (solver.hpp:374,379-381), i.e. iff the
+//   face sum d_a + d_b is not -inf.
 // * Face fluxes. F(a|b) = ((d_a+d_b)*0.5)*(u_b-u_a) is exactly the value both
 //   endpoints compute in the reference (dh_p*(p.u-u_c) for a, dh_m*(u_c-m.u)
-//   for b), so it is computed once per face. For a substituted face the
-//   reference computes ((d_c+d_c)*0.5)*(u_c-u_c) = +-0 when u_c, d_c are
-//   finite, and any +-0 term leaves lap = 0.0 + ... bitwise unchanged, so the
-//   fast path uses 0. Nodes whose fast result is non-finite, and chunks that
-//   touch a Dirichlet outer face, take the exact generic path.
+//   for b). For a substituted face the reference computes
+//   ((d_c+d_c)*0.5)*(u_c-u_c) = +-0 when u_c, d_c are finite, and a +-0 term
+//   leaves lap = 0.0 + ... bitwise unchanged, so the fast path uses 0. Nodes
+//   whose fast result is non-finite, and chunks that touch a Dirichlet outer
+//   face, take the exact generic path on the same loaded values.
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
@@ -35,140 +42,159 @@
 
 namespace pdb {
 
-constexpr int kMarchThreads = 256;
-constexpr int kStages = 4;
+constexpr int kConsumerWarps = 8;
+constexpr int kMarchThreads = 32 * (kConsumerWarps + 1);
+constexpr int kStages = 6;
 constexpr int kSeg = 16;
-constexpr int kBatch = 32;
-constexpr int kTile = 1002;  // 1 pad + 10^3 + 1
+constexpr int kBatch = 16;
+constexpr int kCtasPerSm = 2;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
-constexpr int kFlagInterior = 1, kFlagDirichlet = 2;
+constexpr int kFlagDirichlet = 2;
 
-struct MarchStage {
-    double u[kTile];
-    double d[kTile];
+struct __align__(16) MarchStage {
+    double u[512], d[512];
+    double hxu[2][64], hxd[2][64];  // x- / x+ halo, index z*8+y
+    double hyu[2][64], hyd[2][64];  // y- / y+ halo, index z*8+x
+    double hzu[2][64], hzd[2][64];  // z- / z+ halo, index y*8+x
     uint64_t act[8], snk[8];
+    int4 meta;  // chunk ordinal (-1 = end), packed key, flags
+    int4 pad;
 };
 
-__device__ __forceinline__ int tix(int x, int y, int z) {
-    return 2 + x + 10 * (y + 1) + 100 * (z + 1);
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
 }
-
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
-__device__ __forceinline__ void cp8(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 __device__ __forceinline__ bool sentinel(double d) {
     return (unsigned)__double2hiint(d) == kSentHi;
 }
+__device__ __forceinline__ double sent() { return __hiloint2double((int)kSentHi, 0); }
 
-struct Desc {
-    int4 a, b;  // a = nbr 0..3, b = {nbr4, nbr5, key packed 10:10:10, flags}
-    uint64_t act, flu, snk;
-};
-
-__device__ __forceinline__ Desc load_desc(const StepArgs<double>& A, const int4* __restrict__ desc,
-                                          int c, int z) {
-    Desc d;
-    d.a = __ldg(&desc[2 * (int64_t)c]);
-    d.b = __ldg(&desc[2 * (int64_t)c + 1]);
-    d.act = __ldg(&A.active[(int64_t)c * 8 + z]);
-    d.flu = __ldg(&A.fluid[(int64_t)c * 8 + z]);
-    d.snk = A.reaction == PD_REACTION_SURFACE_SINK ? __ldg(&A.sink[(int64_t)c * 8 + z]) : 0ull;
-    return d;
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+    const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, src);
+    const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)(v >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
 }
 
-// Stage one chunk: u and D_eff (sentinel -inf on non-fluid nodes) of the body
-// and of the six neighbour face layers; absent neighbours get the sentinel.
-__device__ __forceinline__ void issue(MarchStage& S, int4& meta, const StepArgs<double>& A,
-                                      const double* __restrict__ deff, int c, const Desc& D,
-                                      int t, int dbg) {
-    const int z = t >> 5, y = (t >> 2) & 7, xp = t & 3, x0 = 2 * xp, lane = t & 31;
-    const int o = z * 64 + y * 8 + x0;
-    const int bp = y * 8 + x0;
-    const int T = tix(x0, y, z);
-    const double* U = A.u;
-    const int64_t cb = (int64_t)c * 512;
-    const double sent = __hiloint2double((int)kSentHi, 0);
-    if ((D.act >> bp) & 3ull) cp16(&S.u[T], U + cb + o);
-    if ((D.flu >> bp) & 3ull)
-        cp16(&S.d[T], deff + cb + o);
-    else
-        *reinterpret_cast<double2*>(&S.d[T]) = make_double2(sent, sent);
-    if (xp == 0) {
-        const int j = (dbg & 1) ? -1 : D.a.x;
-        if (j >= 0) {
-            const int64_t src = (int64_t)j * 512 + z * 64 + y * 8 + 7;
-            cp8(&S.u[T - 1], U + src);
-            cp8(&S.d[T - 1], deff + src);
-        } else {
-            S.d[T - 1] = sent;
+struct MarchArgs {
+    StepArgs<double> A;
+    const int32_t* __restrict__ sched;
+    int64_t n;
+    const int32_t* __restrict__ desc;  // 8 ints per chunk
+    const double* __restrict__ deff;
+    const double* __restrict__ xfu;  // x-face planes of u       [c][side][64]
+    const double* __restrict__ xfd;  // x-face planes of D_eff   [c][side][64]
+    double* __restrict__ xfun;       // x-face planes of u_next (written)
+    int* counter;                    // per-step batch counter
+};
+
+// Per-lane prefetch of one chunk's descriptor: lanes 0-7 active words,
+// 8-15 fluid words, 16-23 sink words, 24-31 the 8 descriptor ints.
+__device__ __forceinline__ uint64_t load_lane_desc(const MarchArgs& M, int c, int lane) {
+    if (c < 0) return 0;
+    if (lane < 8) return __ldg(&M.A.active[(int64_t)c * 8 + lane]);
+    if (lane < 16) return __ldg(&M.A.fluid[(int64_t)c * 8 + lane - 8]);
+    if (lane < 24)
+        return M.A.reaction == PD_REACTION_SURFACE_SINK ? __ldg(&M.A.sink[(int64_t)c * 8 + lane - 16])
+                                                         : 0ull;
+    return (uint64_t)(uint32_t)__ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
+}
+
+__device__ __forceinline__ void produce(MarchStage& S, uint64_t* full, const MarchArgs& M, int c,
+                                        uint64_t V, int lane) {
+    const double* U = M.A.u;
+    const double* Dd = M.deff;
+    const double sv = sent();
+    if (c >= 0) {
+        const int64_t cb = (int64_t)c * 512;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint64_t aw = shfl64(V, r);
+            const uint64_t fw = shfl64(V, 8 + r);
+            const int off = r * 64 + 2 * lane;
+            if ((aw >> (2 * lane)) & 3ull) cp16(&S.u[off], U + cb + off);
+            if ((fw >> (2 * lane)) & 3ull)
+                cp16(&S.d[off], Dd + cb + off);
+            else
+                *reinterpret_cast<double2*>(&S.d[off]) = make_double2(sv, sv);
         }
-    }
-    if (xp == 3) {
-        const int j = (dbg & 1) ? -1 : D.a.y;
-        if (j >= 0) {
-            const int64_t src = (int64_t)j * 512 + z * 64 + y * 8;
-            cp8(&S.u[T + 2], U + src);
-            cp8(&S.d[T + 2], deff + src);
-        } else {
-            S.d[T + 2] = sent;
+        int nb[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) nb[f] = (int)__shfl_sync(0xffffffffu, (unsigned)V, 24 + f);
+        const int key = (int)__shfl_sync(0xffffffffu, (unsigned)V, 30);
+        const int flg = (int)__shfl_sync(0xffffffffu, (unsigned)V, 31);
+        // x faces from the contiguous side arrays: x- halo = neighbour's x=7
+        // plane (side 1), x+ halo = neighbour's x=0 plane (side 0)
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            const int j = nb[f];
+            if (j >= 0) {
+                const int64_t src = ((int64_t)j * 2 + (1 - f)) * 64 + 2 * lane;
+                cp16(&S.hxu[f][2 * lane], M.xfu + src);
+                cp16(&S.hxd[f][2 * lane], M.xfd + src);
+            } else {
+                *reinterpret_cast<double2*>(&S.hxd[f][2 * lane]) = make_double2(sv, sv);
+            }
         }
-    }
-    if (y == 0) {
-        const int j = (dbg & 2) ? -1 : D.a.z;
-        if (j >= 0) {
-            const int64_t src = (int64_t)j * 512 + z * 64 + 56 + x0;
-            cp16(&S.u[T - 10], U + src);
-            cp16(&S.d[T - 10], deff + src);
-        } else {
-            *reinterpret_cast<double2*>(&S.d[T - 10]) = make_double2(sent, sent);
+        // y faces: row y=7 (y- halo) / y=0 (y+ halo) of every plane
+        {
+            const int z = lane >> 2, k = 2 * (lane & 3);
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                const int j = nb[2 + f];
+                if (j >= 0) {
+                    const int64_t src = (int64_t)j * 512 + z * 64 + (f == 0 ? 56 : 0) + k;
+                    cp16(&S.hyu[f][z * 8 + k], U + src);
+                    cp16(&S.hyd[f][z * 8 + k], Dd + src);
+                } else {
+                    *reinterpret_cast<double2*>(&S.hyd[f][z * 8 + k]) = make_double2(sv, sv);
+                }
+            }
         }
-    }
-    if (y == 7) {
-        const int j = (dbg & 2) ? -1 : D.a.w;
-        if (j >= 0) {
-            const int64_t src = (int64_t)j * 512 + z * 64 + x0;
-            cp16(&S.u[T + 10], U + src);
-            cp16(&S.d[T + 10], deff + src);
-        } else {
-            *reinterpret_cast<double2*>(&S.d[T + 10]) = make_double2(sent, sent);
+        // z faces: plane z=7 (z- halo) / z=0 (z+ halo)
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            const int j = nb[4 + f];
+            if (j >= 0) {
+                const int64_t src = (int64_t)j * 512 + (f == 0 ? 448 : 0) + 2 * lane;
+                cp16(&S.hzu[f][2 * lane], U + src);
+                cp16(&S.hzd[f][2 * lane], Dd + src);
+            } else {
+                *reinterpret_cast<double2*>(&S.hzd[f][2 * lane]) = make_double2(sv, sv);
+            }
         }
+        if (lane < 8) S.act[lane] = V;
+        if (lane >= 16 && lane < 24) S.snk[lane - 16] = V;
+        if (lane == 0) S.meta = make_int4(c, key, flg, 0);
+    } else if (lane == 0) {
+        S.meta = make_int4(-1, 0, 0, 0);
     }
-    if (z == 0) {
-        const int j = (dbg & 4) ? -1 : D.b.x;
-        if (j >= 0) {
-            const int64_t src = (int64_t)j * 512 + 448 + y * 8 + x0;
-            cp16(&S.u[T - 100], U + src);
-            cp16(&S.d[T - 100], deff + src);
-        } else {
-            *reinterpret_cast<double2*>(&S.d[T - 100]) = make_double2(sent, sent);
-        }
-    }
-    if (z == 7) {
-        const int j = (dbg & 4) ? -1 : D.b.y;
-        if (j >= 0) {
-            const int64_t src = (int64_t)j * 512 + y * 8 + x0;
-            cp16(&S.u[T + 100], U + src);
-            cp16(&S.d[T + 100], deff + src);
-        } else {
-            *reinterpret_cast<double2*>(&S.d[T + 100]) = make_double2(sent, sent);
-        }
-    }
-    if (lane == 0) {
-        S.act[z] = D.act;
-        S.snk[z] = D.snk;
-    }
-    if (t == 0) meta = make_int4(c, D.b.z, D.b.w, 0);
+    cp_async_arrive_noinc(full);  // completes when this lane's copies land
+    mbar_arrive(full);            // orders this lane's plain smem stores
 }
 
 // Face flux F(a|b) shared by both endpoints; 0 when either side is not fluid.
@@ -178,11 +204,6 @@ __device__ __forceinline__ double face(double da, double db, double ua, double u
     return ((unsigned)__double2hiint(s) == kSentHi) ? 0.0 : f;
 }
 
-// Exact generic node update (solver.hpp:360-441 with the tile as the data
-// source): used for Dirichlet-exposed chunks and to re-derive any non-finite
-// fast-path result so post-error state matches the reference bit for bit.
-// Per-launch constants of the generic path, copied to shared memory once so
-// the out-of-line slow path does not force the kernel arguments onto the stack.
 struct SlowConsts {
     int64_t size[3];
     double inv_dx2[3];
@@ -191,59 +212,79 @@ struct SlowConsts {
     int dirichlet;
 };
 
+// Exact generic node update (solver.hpp:360-441) on already-loaded neighbour
+// values nu/nd[axis*2+side]; usability from the D_eff sentinel, outer faces
+// from global coordinates.
 template <int REACTION>
-__device__ __noinline__ double slow_node(const MarchStage& S, const SlowConsts& A, int T, int x,
-                                         int y, int z, int kx, int ky, int kz, bool sink,
-                                         double src) {
-    const double u_c = S.u[T], d_c = S.d[T];
-    const int64_t g[3] = {(int64_t)kx * 8 + x, (int64_t)ky * 8 + y, (int64_t)kz * 8 + z};
-    const int stride[3] = {1, 10, 100};
+__device__ __noinline__ double slow_node(const SlowConsts& K, double u_c, double d_c,
+                                         const double* nu, const double* nd, int64_t gx,
+                                         int64_t gy, int64_t gz, bool sink, double src) {
+    const int64_t g[3] = {gx, gy, gz};
     double lap = 0.0;
-#pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        double nu[2], nd[2];
-#pragma unroll
+        double u2[2], d2[2];
         for (int side = 0; side < 2; ++side) {
-            const int Tn = T + (side ? stride[ax] : -stride[ax]);
+            const int f = ax * 2 + side;
             const int64_t gg = g[ax] + (side ? 1 : -1);
-            if (gg < 0 || gg >= A.size[ax]) {
-                const int f = ax * 2 + side;
-                nu[side] = (A.dirichlet >> f) & 1 ? A.bcv[f] : u_c;
-                nd[side] = d_c;
-            } else if (sentinel(S.d[Tn])) {
-                nu[side] = u_c;
-                nd[side] = d_c;
+            if (gg < 0 || gg >= K.size[ax]) {
+                u2[side] = (K.dirichlet >> f) & 1 ? K.bcv[f] : u_c;
+                d2[side] = d_c;
+            } else if (sentinel(nd[f])) {
+                u2[side] = u_c;
+                d2[side] = d_c;
             } else {
-                nu[side] = S.u[Tn];
-                nd[side] = S.d[Tn];
+                u2[side] = nu[f];
+                d2[side] = nd[f];
             }
         }
-        const double dh_m = (d_c + nd[0]) * 0.5;
-        const double dh_p = (d_c + nd[1]) * 0.5;
-        lap += (dh_p * (nu[1] - u_c) - dh_m * (u_c - nu[0])) * A.inv_dx2[ax];
+        const double dh_m = (d_c + d2[0]) * 0.5;
+        const double dh_p = (d_c + d2[1]) * 0.5;
+        lap += (dh_p * (u2[1] - u_c) - dh_m * (u_c - u2[0])) * K.inv_dx2[ax];
     }
     double rate = 0.0;
     if (REACTION == PD_REACTION_SURFACE_SINK) {
-        if (sink) rate = A.neg_k * u_c;
+        if (sink) rate = K.neg_k * u_c;
     } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-        rate = src * A.src_factor;
+        rate = src * K.src_factor;
     }
-    return u_c + A.dt * lap + A.dt * rate;
+    return u_c + K.dt * lap + K.dt * rate;
 }
 
 template <int REACTION>
-__device__ __forceinline__ void compute(const MarchStage& S, const int4 meta,
-                                        const StepArgs<double>& A, const SlowConsts& K, int t) {
-    const int z = t >> 5, y = (t >> 2) & 7, xp = t & 3, x0 = 2 * xp;
+__device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
+                                        const SlowConsts& K, int z, int lane) {
+    const StepArgs<double>& A = M.A;
+    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
     const int o = z * 64 + y * 8 + x0;
     const int bp = y * 8 + x0;
     const uint64_t actw = S.act[z];
     const bool a0 = (actw >> bp) & 1ull, a1 = (actw >> (bp + 1)) & 1ull;
     if (!(a0 | a1)) return;
+    const int4 meta = S.meta;
     const int c = meta.x;
-    const int T = tix(x0, y, z);
-    const double2 uc = *reinterpret_cast<const double2*>(&S.u[T]);
-    const double2 dc = *reinterpret_cast<const double2*>(&S.d[T]);
+    const double2 uc = *reinterpret_cast<const double2*>(&S.u[o]);
+    const double2 dc = *reinterpret_cast<const double2*>(&S.d[o]);
+    const double* pul = xp == 0 ? &S.hxu[0][z * 8 + y] : &S.u[o - 1];
+    const double* pdl = xp == 0 ? &S.hxd[0][z * 8 + y] : &S.d[o - 1];
+    const double* pur = xp == 3 ? &S.hxu[1][z * 8 + y] : &S.u[o + 2];
+    const double* pdr = xp == 3 ? &S.hxd[1][z * 8 + y] : &S.d[o + 2];
+    const double* puy0 = y == 0 ? &S.hyu[0][z * 8 + x0] : &S.u[o - 8];
+    const double* pdy0 = y == 0 ? &S.hyd[0][z * 8 + x0] : &S.d[o - 8];
+    const double* puy1 = y == 7 ? &S.hyu[1][z * 8 + x0] : &S.u[o + 8];
+    const double* pdy1 = y == 7 ? &S.hyd[1][z * 8 + x0] : &S.d[o + 8];
+    const double* puz0 = z == 0 ? &S.hzu[0][y * 8 + x0] : &S.u[o - 64];
+    const double* pdz0 = z == 0 ? &S.hzd[0][y * 8 + x0] : &S.d[o - 64];
+    const double* puz1 = z == 7 ? &S.hzu[1][y * 8 + x0] : &S.u[o + 64];
+    const double* pdz1 = z == 7 ? &S.hzd[1][y * 8 + x0] : &S.d[o + 64];
+    const double uL = *pul, dL = *pdl, uR = *pur, dR = *pdr;
+    const double2 uym = *reinterpret_cast<const double2*>(puy0);
+    const double2 dym = *reinterpret_cast<const double2*>(pdy0);
+    const double2 uyp = *reinterpret_cast<const double2*>(puy1);
+    const double2 dyp = *reinterpret_cast<const double2*>(pdy1);
+    const double2 uzm = *reinterpret_cast<const double2*>(puz0);
+    const double2 dzm = *reinterpret_cast<const double2*>(pdz0);
+    const double2 uzp = *reinterpret_cast<const double2*>(puz1);
+    const double2 dzp = *reinterpret_cast<const double2*>(pdz1);
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((S.snk[z] >> bp) & 1ull);
     const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((S.snk[z] >> (bp + 1)) & 1ull);
     double src0 = 0.0, src1 = 0.0;
@@ -251,28 +292,14 @@ __device__ __forceinline__ void compute(const MarchStage& S, const int4 meta,
         src0 = A.src[(int64_t)c * 512 + o];
         src1 = A.src[(int64_t)c * 512 + o + 1];
     }
-    double out0, out1;
-    if (meta.z & kFlagDirichlet) {
-        const int kx = meta.y & 1023, ky = (meta.y >> 10) & 1023, kz = (meta.y >> 20) & 1023;
-        out0 = sentinel(dc.x) ? uc.x : slow_node<REACTION>(S, K, T, x0, y, z, kx, ky, kz, s0, src0);
-        out1 = sentinel(dc.y) ? uc.y : slow_node<REACTION>(S, K, T + 1, x0 + 1, y, z, kx, ky, kz, s1, src1);
-    } else {
-        const double uL = S.u[T - 1], dL = S.d[T - 1];
-        const double uR = S.u[T + 2], dR = S.d[T + 2];
-        const double2 uym = *reinterpret_cast<const double2*>(&S.u[T - 10]);
-        const double2 dym = *reinterpret_cast<const double2*>(&S.d[T - 10]);
-        const double2 uyp = *reinterpret_cast<const double2*>(&S.u[T + 10]);
-        const double2 dyp = *reinterpret_cast<const double2*>(&S.d[T + 10]);
-        const double2 uzm = *reinterpret_cast<const double2*>(&S.u[T - 100]);
-        const double2 dzm = *reinterpret_cast<const double2*>(&S.d[T - 100]);
-        const double2 uzp = *reinterpret_cast<const double2*>(&S.u[T + 100]);
-        const double2 dzp = *reinterpret_cast<const double2*>(&S.d[T + 100]);
+    double out0 = 0.0, out1 = 0.0;
+    bool slow0 = (meta.z & kFlagDirichlet) != 0, slow1 = slow0;
+    if (!slow0) {
         const double fxl = face(dL, dc.x, uL, uc.x);
         const double fxi = face(dc.x, dc.y, uc.x, uc.y);
         const double fxr = face(dc.y, dR, uc.y, uR);
-        const double ix = A.inv_dx2[0], iy = A.inv_dx2[1], iz = A.inv_dx2[2];
-        // node 0 (lap starts at T{0}, solver.hpp:420)
-        double lap0 = 0.0;
+        const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
+        double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
         lap0 += (fxi - fxl) * ix;
         lap0 += (face(dc.x, dyp.x, uc.x, uyp.x) - face(dym.x, dc.x, uym.x, uc.x)) * iy;
         lap0 += (face(dc.x, dzp.x, uc.x, uzp.x) - face(dzm.x, dc.x, uzm.x, uc.x)) * iz;
@@ -282,26 +309,34 @@ __device__ __forceinline__ void compute(const MarchStage& S, const int4 meta,
         lap1 += (face(dc.y, dzp.y, uc.y, uzp.y) - face(dzm.y, dc.y, uzm.y, uc.y)) * iz;
         double r0 = 0.0, r1 = 0.0;
         if (REACTION == PD_REACTION_SURFACE_SINK) {
-            if (s0) r0 = A.neg_k * uc.x;
-            if (s1) r1 = A.neg_k * uc.y;
+            if (s0) r0 = K.neg_k * uc.x;
+            if (s1) r1 = K.neg_k * uc.y;
         } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-            r0 = src0 * A.src_factor;
-            r1 = src1 * A.src_factor;
+            r0 = src0 * K.src_factor;
+            r1 = src1 * K.src_factor;
         }
-        out0 = uc.x + A.dt * lap0 + A.dt * r0;
-        out1 = uc.y + A.dt * lap1 + A.dt * r1;
-        // walls (active, not fluid) stay frozen (solver.hpp:413-417)
-        if (sentinel(dc.x)) out0 = uc.x;
-        if (sentinel(dc.y)) out1 = uc.y;
-        if (!isfinite(out0) && !sentinel(dc.x)) {
-            const int kx = meta.y & 1023, ky = (meta.y >> 10) & 1023, kz = (meta.y >> 20) & 1023;
-            out0 = slow_node<REACTION>(S, K, T, x0, y, z, kx, ky, kz, s0, src0);
+        out0 = uc.x + K.dt * lap0 + K.dt * r0;
+        out1 = uc.y + K.dt * lap1 + K.dt * r1;
+        slow0 = !isfinite(out0);
+        slow1 = !isfinite(out1);
+    }
+    if (slow0 | slow1) {
+        const int kx = meta.y & 1023, ky = (meta.y >> 10) & 1023, kz = (meta.y >> 20) & 1023;
+        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
+        if (slow0) {
+            const double nu[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+            const double nd[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+            out0 = slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
         }
-        if (!isfinite(out1) && !sentinel(dc.y)) {
-            const int kx = meta.y & 1023, ky = (meta.y >> 10) & 1023, kz = (meta.y >> 20) & 1023;
-            out1 = slow_node<REACTION>(S, K, T + 1, x0 + 1, y, z, kx, ky, kz, s1, src1);
+        if (slow1) {
+            const double nu[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+            const double nd[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+            out1 = slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
         }
     }
+    // walls (active, not fluid) stay frozen (solver.hpp:413-417)
+    if (sentinel(dc.x)) out0 = uc.x;
+    if (sentinel(dc.y)) out1 = uc.y;
     double* dst = A.un + (int64_t)c * 512 + o;
     if (a0 && a1)
         *reinterpret_cast<double2*>(dst) = make_double2(out0, out1);
@@ -309,6 +344,9 @@ __device__ __forceinline__ void compute(const MarchStage& S, const int4 meta,
         dst[0] = out0;
     else
         dst[1] = out1;
+    // x-face side planes of u_next for the next step's x halos
+    if (xp == 0 && a0) M.xfun[((int64_t)c * 2 + 0) * 64 + z * 8 + y] = out0;
+    if (xp == 3 && a1) M.xfun[((int64_t)c * 2 + 1) * 64 + z * 8 + y] = out1;
     // non-finite / huge detection (solver.hpp:444, 250-260, 514-515)
     const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
     if (bad0 | bad1) {
@@ -320,16 +358,26 @@ __device__ __forceinline__ void compute(const MarchStage& S, const int4 meta,
 }
 
 template <int REACTION>
-__global__ void __launch_bounds__(kMarchThreads, 3)
-    ftcs_march_kernel(StepArgs<double> A, const int32_t* __restrict__ sched, int64_t n,
-                      const int4* __restrict__ desc, const double* __restrict__ deff, int dbg) {
+__global__ void __launch_bounds__(kMarchThreads, kCtasPerSm) ftcs_march_kernel(MarchArgs M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MarchStage* st = reinterpret_cast<MarchStage*>(smem_raw);
-    __shared__ int4 meta[kStages];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
-    const int z = t >> 5;
+    const int warp = t >> 5, lane = t & 31;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
     if (t == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 64);               // 32 async + 32 plain arrivals
+            mbar_init(&empty[s], kConsumerWarps);  // one per consumer warp
+        }
         for (int a = 0; a < 3; ++a) {
             K.size[a] = A.size[a];
             K.inv_dx2[a] = A.inv_dx2[a];
@@ -340,67 +388,73 @@ __global__ void __launch_bounds__(kMarchThreads, 3)
         K.src_factor = A.src_factor;
         K.dirichlet = A.dirichlet;
     }
-    if (A.k > 0) {
-        const int prev = A.flags[A.k - 1];
-        if (prev) {
-            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
-            return;
-        }
-    }
-    const int64_t q0 = (int64_t)blockIdx.x * kBatch;
-    const int cnt = (int)min((int64_t)kBatch, n - q0);
-    const int32_t* ids = sched + q0;
+    __syncthreads();
 
-    int c_issue = ids[0];
-    Desc d_issue = load_desc(A, desc, c_issue, z);
-    int c_next = cnt > 1 ? ids[1] : 0;
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
-        Desc d_next = d_issue;
-        int c_after = 0;
-        if (s + 1 < cnt) d_next = load_desc(A, desc, c_next, z);
-        if (s + 2 < cnt) c_after = ids[s + 2];
-        if (s < cnt) issue(st[s], meta[s], A, deff, c_issue, d_issue, t, dbg);
-        cp_commit();
-        c_issue = c_next;
-        d_issue = d_next;
-        c_next = c_after;
-    }
-    for (int k = 0; k < cnt; ++k) {
-        const int qi = k + kStages - 1;
-        Desc d_next = d_issue;
-        int c_after = 0;
-        if (qi + 1 < cnt) d_next = load_desc(A, desc, c_next, z);
-        if (qi + 2 < cnt) c_after = ids[qi + 2];
-        if (qi < cnt) issue(st[qi % kStages], meta[qi % kStages], A, deff, c_issue, d_issue, t, dbg);
-        cp_commit();
-        c_issue = c_next;
-        d_issue = d_next;
-        c_next = c_after;
-        cp_wait<kStages - 1>();
-        __syncthreads();
-        compute<REACTION>(st[k % kStages], meta[k % kStages], A, K, t);
-        __syncthreads();
+    if (warp == kConsumerWarps) {
+        // ---- producer ----
+        int base = 0, nxt = 0;
+        if (lane == 0) {
+            base = atomicAdd(M.counter, kBatch);
+            nxt = atomicAdd(M.counter, kBatch);
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        int i = 0;  // position inside the current batch
+        auto id_at = [&](int b, int k) -> int {
+            const int64_t p = (int64_t)b + k;
+            return p < M.n ? __ldg(&M.sched[p]) : -1;
+        };
+        int c_cur = id_at(base, 0);
+        uint64_t v_cur = load_lane_desc(M, c_cur, lane);
+        for (int q = 0;; ++q) {
+            // chunk after c_cur (may come from the next batch)
+            int nb_base = base, ni = i + 1;
+            if (ni == kBatch) {
+                nb_base = __shfl_sync(0xffffffffu, nxt, 0);
+                ni = 0;
+            }
+            const int c_nxt = c_cur < 0 ? -1 : id_at(nb_base, ni);
+            const uint64_t v_nxt = load_lane_desc(M, c_nxt, lane);
+            const int s = q % kStages;
+            if (q >= kStages) mbar_wait(&empty[s], ((q / kStages) - 1) & 1);
+            produce(st[s], &full[s], M, c_cur, v_cur, lane);
+            if (c_cur < 0) break;
+            if (ni == 0) {  // moved to the next batch: prefetch the one after
+                base = nb_base;
+                if (lane == 0) nxt = atomicAdd(M.counter, kBatch);
+            }
+            i = ni;
+            c_cur = c_nxt;
+            v_cur = v_nxt;
+        }
+    } else {
+        // ---- consumers: warp w = z-plane w ----
+        for (int q = 0;; ++q) {
+            const int s = q % kStages;
+            mbar_wait(&full[s], (q / kStages) & 1);
+            if (st[s].meta.x < 0) break;
+            consume<REACTION>(st[s], M, K, warp, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
     }
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
                             int64_t n, int64_t s0, int64_t s1, int64_t s2, int dirichlet,
-                            int4* __restrict__ desc) {
+                            int32_t* __restrict__ desc) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int k[3] = {keys[i * 3], keys[i * 3 + 1], keys[i * 3 + 2]};
     const int64_t s[3] = {s0, s1, s2};
-    bool interior = true, exposed = false;
+    bool exposed = false;
     for (int a = 0; a < 3; ++a) {
         const bool lo = k[a] == 0;
         const bool hi = (int64_t)k[a] * 8 + 8 >= s[a];
-        interior = interior && !lo && !hi;
         exposed = exposed || (lo && ((dirichlet >> (2 * a)) & 1)) || (hi && ((dirichlet >> (2 * a + 1)) & 1));
     }
-    desc[2 * i] = make_int4(nbr[i * 6 + 0], nbr[i * 6 + 1], nbr[i * 6 + 2], nbr[i * 6 + 3]);
-    desc[2 * i + 1] = make_int4(nbr[i * 6 + 4], nbr[i * 6 + 5], k[0] | (k[1] << 10) | (k[2] << 20),
-                                (interior ? kFlagInterior : 0) | (exposed ? kFlagDirichlet : 0));
+    for (int f = 0; f < 6; ++f) desc[i * 8 + f] = nbr[i * 6 + f];
+    desc[i * 8 + 6] = k[0] | (k[1] << 10) | (k[2] << 20);
+    desc[i * 8 + 7] = exposed ? kFlagDirichlet : 0;
 }
 
 // D_eff = fluid ? D : -inf over every slot; counts fluid nodes whose D is not
@@ -411,16 +465,37 @@ __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __r
     if (i >= n_slots) return;
     const bool fl = (fluid[i >> 6] >> (i & 63)) & 1ull;
     const double v = dcol[i];
-    deff[i] = fl ? v : __hiloint2double((int)kSentHi, 0);
+    deff[i] = fl ? v : sent();
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
+}
+
+// x=0 / x=7 planes of a column into the side array [c][side][z*8+y].
+__global__ void xface_kernel(const double* __restrict__ col, int64_t n, double* __restrict__ xf) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * 128) return;
+    const int64_t c = t >> 7;
+    const int side = (int)((t >> 6) & 1), p = (int)(t & 63);
+    const int z = p >> 3, y = p & 7;
+    xf[t] = col[c * 512 + z * 64 + y * 8 + (side ? 7 : 0)];
 }
 
 void march_free(MarchPlan* p) {
     cudaFree(p->d_stream);
-    cudaFree(p->d_stream_off);
     cudaFree(p->d_desc);
     cudaFree(p->d_deff);
+    cudaFree(p->d_xfd);
+    cudaFree(p->d_xf[0]);
+    cudaFree(p->d_xf[1]);
+    cudaFree(p->d_counter);
     *p = MarchPlan{};
+}
+
+void march_extract_xfaces(pd_grid* g, MarchPlan& p, const void* col) {
+    const int64_t n = g->n_chunks;
+    if (n == 0 || !p.ready) return;
+    xface_kernel<<<(unsigned)((n * 128 + 255) / 256), 256, 0, g->stream>>>((const double*)col, n,
+                                                                          p.d_xf[p.cur]);
+    PD_CUDA(cudaGetLastError());
 }
 
 void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const void* d_dcol,
@@ -429,27 +504,33 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     if (g->dims != 3 || g->tbytes != 8) return;
     if (g->cc[0] > 1024 || g->cc[1] > 1024 || g->cc[2] > 1024) return;  // key packing limit
     const int64_t n_all = g->n_chunks;
-    if (n_all == 0) return;
-    PD_CUDA(cudaMalloc(&plan->d_desc, sizeof(int4) * 2 * (size_t)n_all));
+    if (n_all == 0 || end <= begin) return;
+    PD_CUDA(cudaMalloc(&plan->d_desc, sizeof(int32_t) * 8 * (size_t)n_all));
     desc_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(
         d_nbr, g->d_keys, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
     PD_CUDA(cudaGetLastError());
     const int64_t slots = n_all * 512;
     PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)slots));
+    PD_CUDA(cudaMalloc(&plan->d_xfd, sizeof(double) * 128 * (size_t)n_all));
+    PD_CUDA(cudaMalloc(&plan->d_xf[0], sizeof(double) * 128 * (size_t)n_all));
+    PD_CUDA(cudaMalloc(&plan->d_xf[1], sizeof(double) * 128 * (size_t)n_all));
+    PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024));
     unsigned long long* d_bad = nullptr;
     PD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
     PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
     deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>(
         (const double*)d_dcol, d_fluid, slots, plan->d_deff, d_bad);
     PD_CUDA(cudaGetLastError());
+    xface_kernel<<<(unsigned)((n_all * 128 + 255) / 256), 256, 0, g->stream>>>(plan->d_deff, n_all,
+                                                                              plan->d_xfd);
+    PD_CUDA(cudaGetLastError());
     unsigned long long bad = 0;
     PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
     // schedule of the owned range: (zblock, y, x, z)
     const int64_t n = end - begin;
-    std::vector<int32_t> keys((size_t)std::max<int64_t>(1, n) * 3);
-    if (n > 0)
-        PD_CUDA(cudaMemcpyAsync(keys.data(), g->d_keys + begin * 3, sizeof(int32_t) * 3 * (size_t)n,
-                                cudaMemcpyDeviceToHost, g->stream));
+    std::vector<int32_t> keys((size_t)n * 3);
+    PD_CUDA(cudaMemcpyAsync(keys.data(), g->d_keys + begin * 3, sizeof(int32_t) * 3 * (size_t)n,
+                            cudaMemcpyDeviceToHost, g->stream));
     PD_CUDA(cudaStreamSynchronize(g->stream));
     cudaFree(d_bad);
     if (bad) {  // non-finite D on a fluid node: keep the exact tile kernel
@@ -468,14 +549,16 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
         return ka[2] < kb[2];
     });
     for (auto& o : order) o = (int32_t)(o + begin);
-    PD_CUDA(cudaMalloc(&plan->d_stream, sizeof(int32_t) * std::max<size_t>(1, order.size())));
-    if (!order.empty())
-        PD_CUDA(cudaMemcpyAsync(plan->d_stream, order.data(), sizeof(int32_t) * order.size(),
-                                cudaMemcpyHostToDevice, g->stream));
+    PD_CUDA(cudaMalloc(&plan->d_stream, sizeof(int32_t) * order.size()));
+    PD_CUDA(cudaMemcpyAsync(plan->d_stream, order.data(), sizeof(int32_t) * order.size(),
+                            cudaMemcpyHostToDevice, g->stream));
     PD_CUDA(cudaStreamSynchronize(g->stream));
-    plan->grid = (int)((n + kBatch - 1) / kBatch);
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    plan->grid = sms * kCtasPerSm;
     plan->n = n;
-    plan->ready = n > 0;
+    plan->ready = true;
+    plan->cur = 0;
     static bool attr_set = false;
     if (!attr_set) {
         const int bytes = (int)(sizeof(MarchStage) * kStages);
@@ -486,21 +569,26 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     }
 }
 
-void march_launch(pd_grid* g, const MarchPlan& p, const StepArgs<double>& a, int reaction) {
+void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction) {
     const size_t bytes = sizeof(MarchStage) * kStages;
-    // PD_MARCH_DBG: measurement-only switch that skips halo classes
-    // (1 x, 2 y, 4 z); results are then wrong. Never set in tests/bench.
-    static const int dbg = [] {
-        const char* e = getenv("PD_MARCH_DBG");
-        return e ? atoi(e) : 0;
-    }();
+    MarchArgs M;
+    M.A = a;
+    M.sched = p.d_stream;
+    M.n = p.n;
+    M.desc = p.d_desc;
+    M.deff = p.d_deff;
+    M.xfu = p.d_xf[p.cur];
+    M.xfd = p.d_xfd;
+    M.xfun = p.d_xf[1 - p.cur];
+    M.counter = p.d_counter + (a.k & 1023);
     if (reaction == PD_REACTION_SURFACE_SINK)
-        ftcs_march_kernel<1><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff, dbg);
+        ftcs_march_kernel<1><<<p.grid, kMarchThreads, bytes, g->stream>>>(M);
     else if (reaction == PD_REACTION_VOLUMETRIC)
-        ftcs_march_kernel<2><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff, dbg);
+        ftcs_march_kernel<2><<<p.grid, kMarchThreads, bytes, g->stream>>>(M);
     else
-        ftcs_march_kernel<0><<<p.grid, kMarchThreads, bytes, g->stream>>>(a, p.d_stream, p.n, p.d_desc, p.d_deff, dbg);
+        ftcs_march_kernel<0><<<p.grid, kMarchThreads, bytes, g->stream>>>(M);
     PD_CUDA(cudaGetLastError());
+    p.cur = 1 - p.cur;
 }
 
 }  // namespace pdb
