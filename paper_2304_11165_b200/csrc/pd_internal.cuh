@@ -137,6 +137,7 @@ struct MarchPlan {
     double* d_xfd = nullptr;       // x=0 / x=7 planes of D_eff [c][2][64]
     double* d_xf[2] = {nullptr, nullptr};  // x planes of u / u_next (double-buffered)
     int* d_counter = nullptr;      // per-step dynamic batch counters
+    uint16_t* d_pm = nullptr;      // producer pair masks [c][32]
     int grid = 0;
     int cur = 0;                   // d_xf[cur] mirrors the current u
     int64_t n = 0;

@@ -46,16 +46,19 @@ constexpr int kConsumerWarps = 8;
 constexpr int kMarchThreads = 32 * (kConsumerWarps + 1);
 constexpr int kStages = 6;
 constexpr int kSeg = 16;
-constexpr int kBatch = 16;
+constexpr int kBatch = 32;
 constexpr int kCtasPerSm = 2;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;
 
+// One pipeline stage. The u region and the D_eff region have identical
+// layouts, kDOff doubles apart, so every D load is the matching u address plus
+// an immediate.
+constexpr int kRegion = 896;  // body 512 + x faces 128 + y faces 128 + z faces 128
+constexpr int kHX = 512, kHY = 640, kHZ = 768;
+constexpr int kDOff = kRegion;
 struct __align__(16) MarchStage {
-    double u[512], d[512];
-    double hxu[2][64], hxd[2][64];  // x- / x+ halo, index z*8+y
-    double hyu[2][64], hyd[2][64];  // y- / y+ halo, index z*8+x
-    double hzu[2][64], hzd[2][64];  // z- / z+ halo, index y*8+x
+    double v[2 * kRegion];  // [0, 896): u, [896, 1792): D_eff
     uint64_t act[8], snk[8];
     int4 meta;  // chunk ordinal (-1 = end), packed key, flags
     int4 pad;
@@ -94,17 +97,12 @@ __device__ __forceinline__ bool sentinel(double d) {
 }
 __device__ __forceinline__ double sent() { return __hiloint2double((int)kSentHi, 0); }
 
-__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
-    const unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, src);
-    const unsigned hi = __shfl_sync(0xffffffffu, (unsigned)(v >> 32), src);
-    return ((uint64_t)hi << 32) | lo;
-}
-
 struct MarchArgs {
     StepArgs<double> A;
     const int32_t* __restrict__ sched;
     int64_t n;
     const int32_t* __restrict__ desc;  // 8 ints per chunk
+    const uint16_t* __restrict__ pm;   // per chunk, per lane: pair has active / fluid node
     const double* __restrict__ deff;
     const double* __restrict__ xfu;  // x-face planes of u       [c][side][64]
     const double* __restrict__ xfd;  // x-face planes of D_eff   [c][side][64]
@@ -113,82 +111,92 @@ struct MarchArgs {
 };
 
 // Per-lane prefetch of one chunk's descriptor: lanes 0-7 active words,
-// 8-15 fluid words, 16-23 sink words, 24-31 the 8 descriptor ints.
-__device__ __forceinline__ uint64_t load_lane_desc(const MarchArgs& M, int c, int lane) {
-    if (c < 0) return 0;
-    if (lane < 8) return __ldg(&M.A.active[(int64_t)c * 8 + lane]);
-    if (lane < 16) return __ldg(&M.A.fluid[(int64_t)c * 8 + lane - 8]);
-    if (lane < 24)
-        return M.A.reaction == PD_REACTION_SURFACE_SINK ? __ldg(&M.A.sink[(int64_t)c * 8 + lane - 16])
-                                                         : 0ull;
-    return (uint64_t)(uint32_t)__ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
+// 16-23 sink words, 24-31 the 8 descriptor ints; plus the lane's pair mask.
+struct LaneDesc {
+    uint64_t v;
+    unsigned pm;
+};
+__device__ __forceinline__ LaneDesc load_lane_desc(const MarchArgs& M, int c, int lane) {
+    LaneDesc d{0ull, 0u};
+    if (c < 0) return d;
+    d.pm = __ldg(&M.pm[(int64_t)c * 32 + lane]);
+    if (lane < 8)
+        d.v = __ldg(&M.A.active[(int64_t)c * 8 + lane]);
+    else if (lane >= 16 && lane < 24)
+        d.v = M.A.reaction == PD_REACTION_SURFACE_SINK ? __ldg(&M.A.sink[(int64_t)c * 8 + lane - 16])
+                                                        : 0ull;
+    else if (lane >= 24)
+        d.v = (uint64_t)(uint32_t)__ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
+    return d;
 }
 
 __device__ __forceinline__ void produce(MarchStage& S, uint64_t* full, const MarchArgs& M, int c,
-                                        uint64_t V, int lane) {
+                                        const LaneDesc& L, int lane) {
     const double* U = M.A.u;
     const double* Dd = M.deff;
     const double sv = sent();
+    double* V = S.v;
     if (c >= 0) {
         const int64_t cb = (int64_t)c * 512;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            const uint64_t aw = shfl64(V, r);
-            const uint64_t fw = shfl64(V, 8 + r);
             const int off = r * 64 + 2 * lane;
-            if ((aw >> (2 * lane)) & 3ull) cp16(&S.u[off], U + cb + off);
-            if ((fw >> (2 * lane)) & 3ull)
-                cp16(&S.d[off], Dd + cb + off);
+            if ((L.pm >> (2 * r)) & 1u) cp16(&V[off], U + cb + off);
+            if ((L.pm >> (2 * r + 1)) & 1u)
+                cp16(&V[kDOff + off], Dd + cb + off);
             else
-                *reinterpret_cast<double2*>(&S.d[off]) = make_double2(sv, sv);
+                *reinterpret_cast<double2*>(&V[kDOff + off]) = make_double2(sv, sv);
         }
         int nb[6];
 #pragma unroll
-        for (int f = 0; f < 6; ++f) nb[f] = (int)__shfl_sync(0xffffffffu, (unsigned)V, 24 + f);
-        const int key = (int)__shfl_sync(0xffffffffu, (unsigned)V, 30);
-        const int flg = (int)__shfl_sync(0xffffffffu, (unsigned)V, 31);
+        for (int f = 0; f < 6; ++f) nb[f] = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 24 + f);
+        const int key = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 30);
+        const int flg = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 31);
         // x faces from the contiguous side arrays: x- halo = neighbour's x=7
         // plane (side 1), x+ halo = neighbour's x=0 plane (side 0)
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
             const int j = nb[f];
+            const int dst = kHX + f * 64 + 2 * lane;
             if (j >= 0) {
                 const int64_t src = ((int64_t)j * 2 + (1 - f)) * 64 + 2 * lane;
-                cp16(&S.hxu[f][2 * lane], M.xfu + src);
-                cp16(&S.hxd[f][2 * lane], M.xfd + src);
+                cp16(&V[dst], M.xfu + src);
+                cp16(&V[kDOff + dst], M.xfd + src);
             } else {
-                *reinterpret_cast<double2*>(&S.hxd[f][2 * lane]) = make_double2(sv, sv);
+                *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
             }
         }
-        // y faces: row y=7 (y- halo) / y=0 (y+ halo) of every plane
+        // y faces: row y=7 (y- halo) / y=0 (y+ halo) of every plane, index z*8+x
         {
             const int z = lane >> 2, k = 2 * (lane & 3);
 #pragma unroll
             for (int f = 0; f < 2; ++f) {
                 const int j = nb[2 + f];
+                const int dst = kHY + f * 64 + z * 8 + k;
                 if (j >= 0) {
                     const int64_t src = (int64_t)j * 512 + z * 64 + (f == 0 ? 56 : 0) + k;
-                    cp16(&S.hyu[f][z * 8 + k], U + src);
-                    cp16(&S.hyd[f][z * 8 + k], Dd + src);
+                    cp16(&V[dst], U + src);
+                    cp16(&V[kDOff + dst], Dd + src);
                 } else {
-                    *reinterpret_cast<double2*>(&S.hyd[f][z * 8 + k]) = make_double2(sv, sv);
+                    *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
                 }
             }
         }
-        // z faces: plane z=7 (z- halo) / z=0 (z+ halo)
+        // z faces: plane z=7 (z- halo) / z=0 (z+ halo), index y*8+x
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
             const int j = nb[4 + f];
+            const int dst = kHZ + f * 64 + 2 * lane;
             if (j >= 0) {
                 const int64_t src = (int64_t)j * 512 + (f == 0 ? 448 : 0) + 2 * lane;
-                cp16(&S.hzu[f][2 * lane], U + src);
-                cp16(&S.hzd[f][2 * lane], Dd + src);
+                cp16(&V[dst], U + src);
+                cp16(&V[kDOff + dst], Dd + src);
             } else {
-                *reinterpret_cast<double2*>(&S.hzd[f][2 * lane]) = make_double2(sv, sv);
+                *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
             }
         }
-        if (lane < 8) S.act[lane] = V;
-        if (lane >= 16 && lane < 24) S.snk[lane - 16] = V;
+        if (lane < 8) S.act[lane] = L.v;
+        if (lane >= 16 && lane < 24) S.snk[lane - 16] = L.v;
         if (lane == 0) S.meta = make_int4(c, key, flg, 0);
     } else if (lane == 0) {
         S.meta = make_int4(-1, 0, 0, 0);
@@ -250,43 +258,38 @@ __device__ __noinline__ double slow_node(const SlowConsts& K, double u_c, double
     return u_c + K.dt * lap + K.dt * rate;
 }
 
+// Loop-invariant per-thread element offsets inside a stage region.
+struct Offs {
+    int c, l, r, ym, yp, zm, zp;
+};
+
 template <int REACTION>
 __device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
-                                        const SlowConsts& K, int z, int lane) {
+                                        const SlowConsts& K, const Offs& O, int z, int lane) {
     const StepArgs<double>& A = M.A;
     const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
-    const int o = z * 64 + y * 8 + x0;
     const int bp = y * 8 + x0;
     const uint64_t actw = S.act[z];
     const bool a0 = (actw >> bp) & 1ull, a1 = (actw >> (bp + 1)) & 1ull;
     if (!(a0 | a1)) return;
+    const double* V = S.v;
     const int4 meta = S.meta;
     const int c = meta.x;
-    const double2 uc = *reinterpret_cast<const double2*>(&S.u[o]);
-    const double2 dc = *reinterpret_cast<const double2*>(&S.d[o]);
-    const double* pul = xp == 0 ? &S.hxu[0][z * 8 + y] : &S.u[o - 1];
-    const double* pdl = xp == 0 ? &S.hxd[0][z * 8 + y] : &S.d[o - 1];
-    const double* pur = xp == 3 ? &S.hxu[1][z * 8 + y] : &S.u[o + 2];
-    const double* pdr = xp == 3 ? &S.hxd[1][z * 8 + y] : &S.d[o + 2];
-    const double* puy0 = y == 0 ? &S.hyu[0][z * 8 + x0] : &S.u[o - 8];
-    const double* pdy0 = y == 0 ? &S.hyd[0][z * 8 + x0] : &S.d[o - 8];
-    const double* puy1 = y == 7 ? &S.hyu[1][z * 8 + x0] : &S.u[o + 8];
-    const double* pdy1 = y == 7 ? &S.hyd[1][z * 8 + x0] : &S.d[o + 8];
-    const double* puz0 = z == 0 ? &S.hzu[0][y * 8 + x0] : &S.u[o - 64];
-    const double* pdz0 = z == 0 ? &S.hzd[0][y * 8 + x0] : &S.d[o - 64];
-    const double* puz1 = z == 7 ? &S.hzu[1][y * 8 + x0] : &S.u[o + 64];
-    const double* pdz1 = z == 7 ? &S.hzd[1][y * 8 + x0] : &S.d[o + 64];
-    const double uL = *pul, dL = *pdl, uR = *pur, dR = *pdr;
-    const double2 uym = *reinterpret_cast<const double2*>(puy0);
-    const double2 dym = *reinterpret_cast<const double2*>(pdy0);
-    const double2 uyp = *reinterpret_cast<const double2*>(puy1);
-    const double2 dyp = *reinterpret_cast<const double2*>(pdy1);
-    const double2 uzm = *reinterpret_cast<const double2*>(puz0);
-    const double2 dzm = *reinterpret_cast<const double2*>(pdz0);
-    const double2 uzp = *reinterpret_cast<const double2*>(puz1);
-    const double2 dzp = *reinterpret_cast<const double2*>(pdz1);
+    const double2 uc = *reinterpret_cast<const double2*>(&V[O.c]);
+    const double2 dc = *reinterpret_cast<const double2*>(&V[O.c + kDOff]);
+    const double uL = V[O.l], dL = V[O.l + kDOff];
+    const double uR = V[O.r], dR = V[O.r + kDOff];
+    const double2 uym = *reinterpret_cast<const double2*>(&V[O.ym]);
+    const double2 dym = *reinterpret_cast<const double2*>(&V[O.ym + kDOff]);
+    const double2 uyp = *reinterpret_cast<const double2*>(&V[O.yp]);
+    const double2 dyp = *reinterpret_cast<const double2*>(&V[O.yp + kDOff]);
+    const double2 uzm = *reinterpret_cast<const double2*>(&V[O.zm]);
+    const double2 dzm = *reinterpret_cast<const double2*>(&V[O.zm + kDOff]);
+    const double2 uzp = *reinterpret_cast<const double2*>(&V[O.zp]);
+    const double2 dzp = *reinterpret_cast<const double2*>(&V[O.zp + kDOff]);
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((S.snk[z] >> bp) & 1ull);
     const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((S.snk[z] >> (bp + 1)) & 1ull);
+    const int o = O.c;  // body offset of node 0 == in-chunk offset
     double src0 = 0.0, src1 = 0.0;
     if (REACTION == PD_REACTION_VOLUMETRIC) {
         src0 = A.src[(int64_t)c * 512 + o];
@@ -391,50 +394,85 @@ __global__ void __launch_bounds__(kMarchThreads, kCtasPerSm) ftcs_march_kernel(M
     __syncthreads();
 
     if (warp == kConsumerWarps) {
-        // ---- producer ----
-        int base = 0, nxt = 0;
+        // ---- producer: ids per batch in lane registers, descriptors kAhead
+        // chunks ahead, the batch after next claimed while this one streams ----
+        constexpr int kAhead = 4;
+        int b_cur = 0, b_nxt = 0, b_far = 0;
         if (lane == 0) {
-            base = atomicAdd(M.counter, kBatch);
-            nxt = atomicAdd(M.counter, kBatch);
+            b_cur = atomicAdd(M.counter, kBatch);
+            b_nxt = atomicAdd(M.counter, kBatch);
         }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        int i = 0;  // position inside the current batch
-        auto id_at = [&](int b, int k) -> int {
-            const int64_t p = (int64_t)b + k;
+        b_cur = __shfl_sync(0xffffffffu, b_cur, 0);
+        b_nxt = __shfl_sync(0xffffffffu, b_nxt, 0);
+        auto ld_id = [&](int b) -> int {
+            const int64_t p = (int64_t)b + lane;
             return p < M.n ? __ldg(&M.sched[p]) : -1;
         };
-        int c_cur = id_at(base, 0);
-        uint64_t v_cur = load_lane_desc(M, c_cur, lane);
-        for (int q = 0;; ++q) {
-            // chunk after c_cur (may come from the next batch)
-            int nb_base = base, ni = i + 1;
-            if (ni == kBatch) {
-                nb_base = __shfl_sync(0xffffffffu, nxt, 0);
-                ni = 0;
+        int id_cur = ld_id(b_cur), id_nxt = ld_id(b_nxt), id_far = -1;
+        int pos = 0;  // position of the chunk being produced inside batch b_cur
+        auto id_ahead = [&](int k) -> int {  // chunk id k positions after pos
+            const int p = pos + k;
+            return p < kBatch ? __shfl_sync(0xffffffffu, id_cur, p)
+                              : __shfl_sync(0xffffffffu, id_nxt, p - kBatch);
+        };
+        int cid[kAhead];
+        LaneDesc ring[kAhead];
+#pragma unroll
+        for (int k = 0; k < kAhead; ++k) {
+            cid[k] = id_ahead(k);
+            ring[k] = load_lane_desc(M, cid[k], lane);
+        }
+        bool done = false;
+        for (int q0 = 0; !done; q0 += kStages) {
+#pragma unroll
+            for (int s = 0; s < kStages; ++s) {
+                if (q0 > 0) mbar_wait(&empty[s], ((q0 / kStages) - 1) & 1);
+                const int c = cid[0];
+                produce(st[s], &full[s], M, c, ring[0], lane);
+                if (c < 0) {
+                    done = true;
+                    break;
+                }
+                // advance the prefetch window by one chunk
+                const int c_new = cid[kAhead - 1] < 0 ? -1 : id_ahead(kAhead);
+#pragma unroll
+                for (int k = 0; k + 1 < kAhead; ++k) {
+                    cid[k] = cid[k + 1];
+                    ring[k] = ring[k + 1];
+                }
+                cid[kAhead - 1] = c_new;
+                ring[kAhead - 1] = load_lane_desc(M, c_new, lane);
+                ++pos;
+                if (pos == 1 && lane == 0) b_far = atomicAdd(M.counter, kBatch);
+                if (pos == kBatch / 2) id_far = ld_id(__shfl_sync(0xffffffffu, b_far, 0));
+                if (pos == kBatch) {
+                    pos = 0;
+                    id_cur = id_nxt;
+                    id_nxt = id_far;
+                }
             }
-            const int c_nxt = c_cur < 0 ? -1 : id_at(nb_base, ni);
-            const uint64_t v_nxt = load_lane_desc(M, c_nxt, lane);
-            const int s = q % kStages;
-            if (q >= kStages) mbar_wait(&empty[s], ((q / kStages) - 1) & 1);
-            produce(st[s], &full[s], M, c_cur, v_cur, lane);
-            if (c_cur < 0) break;
-            if (ni == 0) {  // moved to the next batch: prefetch the one after
-                base = nb_base;
-                if (lane == 0) nxt = atomicAdd(M.counter, kBatch);
-            }
-            i = ni;
-            c_cur = c_nxt;
-            v_cur = v_nxt;
         }
     } else {
         // ---- consumers: warp w = z-plane w ----
-        for (int q = 0;; ++q) {
-            const int s = q % kStages;
-            mbar_wait(&full[s], (q / kStages) & 1);
-            if (st[s].meta.x < 0) break;
-            consume<REACTION>(st[s], M, K, warp, lane);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+        const int z = warp, y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
+        const int o = z * 64 + y * 8 + x0;
+        Offs O;
+        O.c = o;
+        O.l = xp == 0 ? kHX + z * 8 + y : o - 1;
+        O.r = xp == 3 ? kHX + 64 + z * 8 + y : o + 2;
+        O.ym = y == 0 ? kHY + z * 8 + x0 : o - 8;
+        O.yp = y == 7 ? kHY + 64 + z * 8 + x0 : o + 8;
+        O.zm = z == 0 ? kHZ + y * 8 + x0 : o - 64;
+        O.zp = z == 7 ? kHZ + 64 + y * 8 + x0 : o + 64;
+        for (int q0 = 0;; q0 += kStages) {
+#pragma unroll
+            for (int s = 0; s < kStages; ++s) {
+                mbar_wait(&full[s], (q0 / kStages) & 1);
+                if (st[s].meta.x < 0) return;
+                consume<REACTION>(st[s], M, K, O, z, lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
         }
     }
 }
@@ -469,6 +507,22 @@ __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __r
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
 }
 
+// Per chunk and producer lane: bit 2r = the lane's pair in plane r has an
+// active node, bit 2r+1 = it has a fluid node.
+__global__ void pairmask_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ flu,
+                                int64_t n, uint16_t* __restrict__ pm) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * 32) return;
+    const int64_t c = t >> 5;
+    const int lane = (int)(t & 31);
+    unsigned v = 0;
+    for (int r = 0; r < 8; ++r) {
+        if ((act[c * 8 + r] >> (2 * lane)) & 3ull) v |= 1u << (2 * r);
+        if ((flu[c * 8 + r] >> (2 * lane)) & 3ull) v |= 1u << (2 * r + 1);
+    }
+    pm[t] = (uint16_t)v;
+}
+
 // x=0 / x=7 planes of a column into the side array [c][side][z*8+y].
 __global__ void xface_kernel(const double* __restrict__ col, int64_t n, double* __restrict__ xf) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -487,6 +541,7 @@ void march_free(MarchPlan* p) {
     cudaFree(p->d_xf[0]);
     cudaFree(p->d_xf[1]);
     cudaFree(p->d_counter);
+    cudaFree(p->d_pm);
     *p = MarchPlan{};
 }
 
@@ -515,6 +570,10 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaMalloc(&plan->d_xf[0], sizeof(double) * 128 * (size_t)n_all));
     PD_CUDA(cudaMalloc(&plan->d_xf[1], sizeof(double) * 128 * (size_t)n_all));
     PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024));
+    PD_CUDA(cudaMalloc(&plan->d_pm, sizeof(uint16_t) * 32 * (size_t)n_all));
+    pairmask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_fluid,
+                                                                                n_all, plan->d_pm);
+    PD_CUDA(cudaGetLastError());
     unsigned long long* d_bad = nullptr;
     PD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
     PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
@@ -576,6 +635,7 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     M.sched = p.d_stream;
     M.n = p.n;
     M.desc = p.d_desc;
+    M.pm = p.d_pm;
     M.deff = p.d_deff;
     M.xfu = p.d_xf[p.cur];
     M.xfd = p.d_xfd;
