@@ -49,7 +49,10 @@ constexpr int kSeg = 16;
 constexpr int kBatch = 32;
 constexpr int kCtasPerSm = 2;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
-constexpr int kFlagDirichlet = 2;
+constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
+constexpr int kFlagBulk = 4;       // dense chunk: stream body slabs with TMA bulk copies
+// bits 8..15: plane z is interior-fluid (all nodes and all their face
+// neighbours fluid) -> select-free consumer path
 
 // One pipeline stage. The u region and the D_eff region have identical
 // layouts, kDOff doubles apart, so every D load is the matching u address plus
@@ -69,6 +72,18 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+// TMA bulk copy global -> shared, completion reported to an mbarrier (tx bytes)
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -138,34 +153,62 @@ __device__ __forceinline__ void produce(MarchStage& S, uint64_t* full, const Mar
     double* V = S.v;
     if (c >= 0) {
         const int64_t cb = (int64_t)c * 512;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int off = r * 64 + 2 * lane;
-            if ((L.pm >> (2 * r)) & 1u) cp16(&V[off], U + cb + off);
-            if ((L.pm >> (2 * r + 1)) & 1u)
-                cp16(&V[kDOff + off], Dd + cb + off);
-            else
-                *reinterpret_cast<double2*>(&V[kDOff + off]) = make_double2(sv, sv);
-        }
         int nb[6];
 #pragma unroll
         for (int f = 0; f < 6; ++f) nb[f] = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 24 + f);
         const int key = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 30);
         const int flg = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 31);
-        // x faces from the contiguous side arrays: x- halo = neighbour's x=7
-        // plane (side 1), x+ halo = neighbour's x=0 plane (side 0)
+        const bool bulk = flg & kFlagBulk;
+        if (lane == 0) {
+            // stage memory was last touched through the generic proxy
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            // bytes of every bulk copy of this stage, registered before issue
+            unsigned bytes = bulk ? 8192u : 0u;
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
-            const int j = nb[f];
-            const int dst = kHX + f * 64 + 2 * lane;
-            if (j >= 0) {
-                const int64_t src = ((int64_t)j * 2 + (1 - f)) * 64 + 2 * lane;
-                cp16(&V[dst], M.xfu + src);
-                cp16(&V[kDOff + dst], M.xfd + src);
-            } else {
-                *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
+            for (int f = 0; f < 6; ++f)
+                if ((f < 2 || f >= 4) && nb[f] >= 0) bytes += 1024u;
+            if (bytes) mbar_expect_tx(full, bytes);
+            if (bulk) {
+                bulk_g2s(&V[0], U + cb, 4096u, full);
+                bulk_g2s(&V[kDOff], Dd + cb, 4096u, full);
+            }
+            // x faces from the contiguous side arrays: x- halo = neighbour's
+            // x=7 plane (side 1), x+ halo = neighbour's x=0 plane (side 0)
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+                if (nb[f] >= 0) {
+                    const int64_t src = ((int64_t)nb[f] * 2 + (1 - f)) * 64;
+                    bulk_g2s(&V[kHX + f * 64], M.xfu + src, 512u, full);
+                    bulk_g2s(&V[kDOff + kHX + f * 64], M.xfd + src, 512u, full);
+                }
+            // z faces: plane z=7 (z- halo) / z=0 (z+ halo)
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+                if (nb[4 + f] >= 0) {
+                    const int64_t src = (int64_t)nb[4 + f] * 512 + (f == 0 ? 448 : 0);
+                    bulk_g2s(&V[kHZ + f * 64], U + src, 512u, full);
+                    bulk_g2s(&V[kDOff + kHZ + f * 64], Dd + src, 512u, full);
+                }
+        }
+        if (!bulk) {
+            // sparse chunk: 16-B copies of pairs holding an active (u) /
+            // fluid (D) node only, so empty sectors are never read
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int off = r * 64 + 2 * lane;
+                if ((L.pm >> (2 * r)) & 1u) cp16(&V[off], U + cb + off);
+                if ((L.pm >> (2 * r + 1)) & 1u)
+                    cp16(&V[kDOff + off], Dd + cb + off);
+                else
+                    *reinterpret_cast<double2*>(&V[kDOff + off]) = make_double2(sv, sv);
             }
         }
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+            if ((f < 2 || f >= 4) && nb[f] < 0) {
+                const int base = f < 2 ? kHX + f * 64 : kHZ + (f - 4) * 64;
+                *reinterpret_cast<double2*>(&V[kDOff + base + 2 * lane]) = make_double2(sv, sv);
+            }
         // y faces: row y=7 (y- halo) / y=0 (y+ halo) of every plane, index z*8+x
         {
             const int z = lane >> 2, k = 2 * (lane & 3);
@@ -180,19 +223,6 @@ __device__ __forceinline__ void produce(MarchStage& S, uint64_t* full, const Mar
                 } else {
                     *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
                 }
-            }
-        }
-        // z faces: plane z=7 (z- halo) / z=0 (z+ halo), index y*8+x
-#pragma unroll
-        for (int f = 0; f < 2; ++f) {
-            const int j = nb[4 + f];
-            const int dst = kHZ + f * 64 + 2 * lane;
-            if (j >= 0) {
-                const int64_t src = (int64_t)j * 512 + (f == 0 ? 448 : 0) + 2 * lane;
-                cp16(&V[dst], U + src);
-                cp16(&V[kDOff + dst], Dd + src);
-            } else {
-                *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
             }
         }
         if (lane < 8) S.act[lane] = L.v;
@@ -297,7 +327,37 @@ __device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
     }
     double out0 = 0.0, out1 = 0.0;
     bool slow0 = (meta.z & kFlagDirichlet) != 0, slow1 = slow0;
-    if (!slow0) {
+    if ((meta.z >> (8 + z)) & 1) {
+        // interior-fluid plane: every node and every neighbour is fluid, so
+        // no face needs the substitution select (warp-uniform branch)
+        auto fface = [](double da, double db, double ua, double ub) {
+            return ((da + db) * 0.5) * (ub - ua);
+        };
+        const double fxl = fface(dL, dc.x, uL, uc.x);
+        const double fxi = fface(dc.x, dc.y, uc.x, uc.y);
+        const double fxr = fface(dc.y, dR, uc.y, uR);
+        const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
+        double lap0 = 0.0;
+        lap0 += (fxi - fxl) * ix;
+        lap0 += (fface(dc.x, dyp.x, uc.x, uyp.x) - fface(dym.x, dc.x, uym.x, uc.x)) * iy;
+        lap0 += (fface(dc.x, dzp.x, uc.x, uzp.x) - fface(dzm.x, dc.x, uzm.x, uc.x)) * iz;
+        double lap1 = 0.0;
+        lap1 += (fxr - fxi) * ix;
+        lap1 += (fface(dc.y, dyp.y, uc.y, uyp.y) - fface(dym.y, dc.y, uym.y, uc.y)) * iy;
+        lap1 += (fface(dc.y, dzp.y, uc.y, uzp.y) - fface(dzm.y, dc.y, uzm.y, uc.y)) * iz;
+        double r0 = 0.0, r1 = 0.0;
+        if (REACTION == PD_REACTION_SURFACE_SINK) {
+            if (s0) r0 = K.neg_k * uc.x;
+            if (s1) r1 = K.neg_k * uc.y;
+        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+            r0 = src0 * K.src_factor;
+            r1 = src1 * K.src_factor;
+        }
+        out0 = uc.x + K.dt * lap0 + K.dt * r0;
+        out1 = uc.y + K.dt * lap1 + K.dt * r1;
+        slow0 = !isfinite(out0);
+        slow1 = !isfinite(out1);
+    } else if (!slow0) {
         const double fxl = face(dL, dc.x, uL, uc.x);
         const double fxi = face(dc.x, dc.y, uc.x, uc.y);
         const double fxr = face(dc.y, dR, uc.y, uR);
@@ -478,6 +538,7 @@ __global__ void __launch_bounds__(kMarchThreads, kCtasPerSm) ftcs_march_kernel(M
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
+                            const uint64_t* __restrict__ act, const uint64_t* __restrict__ flu,
                             int64_t n, int64_t s0, int64_t s1, int64_t s2, int dirichlet,
                             int32_t* __restrict__ desc) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -490,9 +551,34 @@ __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __re
         const bool hi = (int64_t)k[a] * 8 + 8 >= s[a];
         exposed = exposed || (lo && ((dirichlet >> (2 * a)) & 1)) || (hi && ((dirichlet >> (2 * a + 1)) & 1));
     }
-    for (int f = 0; f < 6; ++f) desc[i * 8 + f] = nbr[i * 6 + f];
+    int nb[6];
+    for (int f = 0; f < 6; ++f) nb[f] = nbr[i * 6 + f];
+    // dense chunks stream their body with bulk copies
+    int pairs = 0;
+    uint64_t F[8];
+    for (int z = 0; z < 8; ++z) {
+        const uint64_t w = act[i * 8 + z];
+        pairs += __popcll((w | (w >> 1)) & 0x5555555555555555ull);
+        F[z] = flu[i * 8 + z];
+    }
+    int flags = (exposed ? kFlagDirichlet : 0) | (pairs >= 128 ? kFlagBulk : 0);
+    // interior-fluid planes: the plane and every face neighbour of its nodes fluid
+    const uint64_t ALL = ~0ull;
+    const uint64_t zlo = nb[4] >= 0 ? flu[(int64_t)nb[4] * 8 + 7] : 0ull;
+    const uint64_t zhi = nb[5] >= 0 ? flu[(int64_t)nb[5] * 8 + 0] : 0ull;
+    for (int z = 0; z < 8 && !exposed; ++z) {
+        bool ok = F[z] == ALL;
+        ok = ok && (z > 0 ? F[z - 1] == ALL : zlo == ALL);
+        ok = ok && (z < 7 ? F[z + 1] == ALL : zhi == ALL);
+        ok = ok && nb[0] >= 0 && (flu[(int64_t)nb[0] * 8 + z] & 0x8080808080808080ull) == 0x8080808080808080ull;
+        ok = ok && nb[1] >= 0 && (flu[(int64_t)nb[1] * 8 + z] & 0x0101010101010101ull) == 0x0101010101010101ull;
+        ok = ok && nb[2] >= 0 && (flu[(int64_t)nb[2] * 8 + z] >> 56) == 0xFFull;
+        ok = ok && nb[3] >= 0 && (flu[(int64_t)nb[3] * 8 + z] & 0xFFull) == 0xFFull;
+        if (ok) flags |= 1 << (8 + z);
+    }
+    for (int f = 0; f < 6; ++f) desc[i * 8 + f] = nb[f];
     desc[i * 8 + 6] = k[0] | (k[1] << 10) | (k[2] << 20);
-    desc[i * 8 + 7] = exposed ? kFlagDirichlet : 0;
+    desc[i * 8 + 7] = flags;
 }
 
 // D_eff = fluid ? D : -inf over every slot; counts fluid nodes whose D is not
@@ -562,7 +648,8 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     if (n_all == 0 || end <= begin) return;
     PD_CUDA(cudaMalloc(&plan->d_desc, sizeof(int32_t) * 8 * (size_t)n_all));
     desc_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(
-        d_nbr, g->d_keys, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
+        d_nbr, g->d_keys, g->d_masks, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet,
+        plan->d_desc);
     PD_CUDA(cudaGetLastError());
     const int64_t slots = n_all * 512;
     PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)slots));
