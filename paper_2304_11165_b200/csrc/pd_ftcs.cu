@@ -315,7 +315,7 @@ void march_build_for(pd_stepper* s, int64_t begin, int64_t end) {
     for (int f = 0; f < 2 * g->dims; ++f)
         if (s->cfg.bc_type[f] == PD_BC_DIRICHLET) dir |= 1 << f;
     const void* dcol = g->cols[(size_t)g->column_of[(size_t)s->prop_d]];
-    march_build(g, s->d_nbr, s->d_fluid, dcol, dir, begin, end, &s->plan);
+    march_build(g, s->d_nbr, s->d_fluid, s->d_sink, dcol, dir, begin, end, &s->plan);
 }
 
 void validate(const pd_grid* g, const pd_sim_config* c, int prop_src,
@@ -599,7 +599,8 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
             PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)nb, g->stream));
             PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
             if (s->plan.ready)
-                PD_CUDA(cudaMemsetAsync(s->plan.d_counter, 0, sizeof(int) * (size_t)nb, g->stream));
+                PD_CUDA(cudaMemsetAsync(s->plan.d_counter, 0,
+                                        sizeof(int) * (size_t)(nb * march_counters_per_step()), g->stream));
             int64_t nr = 0;
             PD_CUDA(cudaEventRecord(s->ev0, g->stream));
             for (int64_t k = 0; k < nb; ++k) {

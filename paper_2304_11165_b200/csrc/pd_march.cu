@@ -1,38 +1,41 @@
-// Warp-specialized, mbarrier-pipelined FTCS step for 3-D FP64 grids — the
+// Warp-per-chunk, register-marching FTCS step for 3-D FP64 grids — the
 // bandwidth path (BASELINE.json configs C1-C5).
 //
 // Same per-node result, bit for bit, as ftcs_step_kernel (pd_ftcs.cu) and the
-// reference (solver.hpp:360-455); what changes is how bytes and instructions
-// are spent.
+// reference (solver.hpp:360-455). Design (measured alternatives — a staged
+// 10^3 smem tile with CTA barriers, and a TMA/cp.async producer warp feeding
+// mbarrier-synchronised consumer warps — were latency- or producer-bound, see
+// DESIGN.md):
 //
-// * Schedule. Chunks are ordered (z-block of kSeg layers, y, x, z): runs of a
-//   chunk column inside a z-block are contiguous and neighbouring columns
-//   follow each other. Persistent CTAs (2 per SM) grab kBatch consecutive
-//   chunks of that order with an atomic counter, so the chunks in flight are
-//   always a contiguous window of the schedule and the face halos a CTA reads
-//   were just streamed by its neighbours (L2 hits).
-// * Producer warp. One warp per CTA streams chunk after chunk into a
-//   kStages-deep shared-memory ring with cp.async (16-B copies; body pairs
-//   with no active / fluid node are never read from HBM) and signals each
-//   stage through an mbarrier (cp.async.mbarrier.arrive). Descriptors and
-//   masks are prefetched one chunk ahead, chunk ids one batch ahead, so the
-//   producer never waits on its own loads.
+// * One warp owns one chunk at a time and marches its 8 z-planes; lane
+//   (y, xp) holds the x-adjacent node pair (2xp, 2xp+1) of row y in every
+//   plane. u and D of the planes z-1, z, z+1 live in registers (the z
+//   stencil), x and y neighbours come from warp shuffles, and only the
+//   chunk-face lanes read halo values from memory. No shared memory, no
+//   barriers; loads for plane z+2 are in flight while plane z is computed, and
+//   20 warps per SM keep enough bytes in flight to cover HBM latency.
+// * Pairs without an active node are never loaded (predicated 16-B loads), so
+//   empty 32-B sectors cost no HBM traffic.
 // * Contiguous halos. x faces are 8-B strided in a chunk slab, so every step
 //   also writes the x=0 / x=7 planes of u_next into a side array (64 doubles
-//   per face, contiguous) and the stepper keeps the same for D_eff; y and z
-//   face layers are read directly (64-B rows / 512-B planes).
-// * Consumer warps (8). Warp w computes z-plane w, two x-adjacent nodes per
-//   thread, from shared memory only.
-// * Usability without masks. D_eff = fluid ? D : -inf (static per run). A
+//   per face, contiguous) and the stepper keeps the same for D_eff; y halos
+//   are 64-B rows and z halos 512-B planes of the neighbour chunks.
+// * Schedule. Chunks are ordered (z-block of kSeg layers, y, x, z); the order
+//   is cut into kParts contiguous parts, each consumed in kBatch-chunk claims
+//   by the warps assigned to it (atomic counter per part), so the chunks in
+//   flight form kParts short windows of the order and neighbour halos are
+//   L2 hits.
+// * Usability without masks. D_eff = fluid ? D : -inf (static per run); a
 //   neighbour is usable iff it is fluid (solver.hpp:374,379-381), i.e. iff the
 //   face sum d_a + d_b is not -inf.
 // * Face fluxes. F(a|b) = ((d_a+d_b)*0.5)*(u_b-u_a) is exactly the value both
 //   endpoints compute in the reference (dh_p*(p.u-u_c) for a, dh_m*(u_c-m.u)
 //   for b). For a substituted face the reference computes
 //   ((d_c+d_c)*0.5)*(u_c-u_c) = +-0 when u_c, d_c are finite, and a +-0 term
-//   leaves lap = 0.0 + ... bitwise unchanged, so the fast path uses 0. Nodes
+//   leaves lap = 0.0 + ... bitwise unchanged, so the fast path uses 0. Planes
+//   whose nodes and neighbours are all fluid skip the selects entirely. Nodes
 //   whose fast result is non-finite, and chunks that touch a Dirichlet outer
-//   face, take the exact generic path on the same loaded values.
+//   face, take the exact generic path on the same register values.
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
@@ -42,205 +45,49 @@
 
 namespace pdb {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kMarchThreads = 32 * (kConsumerWarps + 1);
-constexpr int kStages = 6;
+constexpr int kWarps = 4;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=3 selects 3)
+constexpr int kBatch = 4;
+constexpr int kParts = 32;
 constexpr int kSeg = 16;
-constexpr int kBatch = 32;
-constexpr int kCtasPerSm = 2;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
-constexpr int kFlagBulk = 4;       // dense chunk: stream body slabs with TMA bulk copies
-// bits 8..15: plane z is interior-fluid (all nodes and all their face
-// neighbours fluid) -> select-free consumer path
-
-// One pipeline stage. The u region and the D_eff region have identical
-// layouts, kDOff doubles apart, so every D load is the matching u address plus
-// an immediate.
-constexpr int kRegion = 896;  // body 512 + x faces 128 + y faces 128 + z faces 128
-constexpr int kHX = 512, kHY = 640, kHZ = 768;
-constexpr int kDOff = kRegion;
-struct __align__(16) MarchStage {
-    double v[2 * kRegion];  // [0, 896): u, [896, 1792): D_eff
-    uint64_t act[8], snk[8];
-    int4 meta;  // chunk ordinal (-1 = end), packed key, flags
-    int4 pad;
-};
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-// TMA bulk copy global -> shared, completion reported to an mbarrier (tx bytes)
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(smem)),
-        "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
+// desc flag bits 8..15: plane z is interior-fluid (every node and every face
+// neighbour fluid) -> select-free path
 
 __device__ __forceinline__ bool sentinel(double d) {
     return (unsigned)__double2hiint(d) == kSentHi;
 }
 __device__ __forceinline__ double sent() { return __hiloint2double((int)kSentHi, 0); }
 
+__device__ __forceinline__ double shfl_up_d(double v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+__device__ __forceinline__ double shfl_dn_d(double v, int d) {
+    return __shfl_down_sync(0xffffffffu, v, d);
+}
+
 struct MarchArgs {
     StepArgs<double> A;
     const int32_t* __restrict__ sched;
     int64_t n;
-    const int32_t* __restrict__ desc;  // 8 ints per chunk
-    const uint16_t* __restrict__ pm;   // per chunk, per lane: pair has active / fluid node
+    const int32_t* __restrict__ desc;  // 8 ints per chunk: nbr[6], key, flags
+    const uint32_t* __restrict__ lm;   // per chunk and lane: active / sink bits
     const double* __restrict__ deff;
     const double* __restrict__ xfu;  // x-face planes of u       [c][side][64]
     const double* __restrict__ xfd;  // x-face planes of D_eff   [c][side][64]
     double* __restrict__ xfun;       // x-face planes of u_next (written)
-    int* counter;                    // per-step batch counter
+    int* counter;                    // kParts counters of this step
 };
 
-// Per-lane prefetch of one chunk's descriptor: lanes 0-7 active words,
-// 16-23 sink words, 24-31 the 8 descriptor ints; plus the lane's pair mask.
-struct LaneDesc {
-    uint64_t v;
-    unsigned pm;
+struct Plane {  // a lane's node pair in one plane
+    double2 u, d;
 };
-__device__ __forceinline__ LaneDesc load_lane_desc(const MarchArgs& M, int c, int lane) {
-    LaneDesc d{0ull, 0u};
-    if (c < 0) return d;
-    d.pm = __ldg(&M.pm[(int64_t)c * 32 + lane]);
-    if (lane < 8)
-        d.v = __ldg(&M.A.active[(int64_t)c * 8 + lane]);
-    else if (lane >= 16 && lane < 24)
-        d.v = M.A.reaction == PD_REACTION_SURFACE_SINK ? __ldg(&M.A.sink[(int64_t)c * 8 + lane - 16])
-                                                        : 0ull;
-    else if (lane >= 24)
-        d.v = (uint64_t)(uint32_t)__ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
-    return d;
-}
-
-__device__ __forceinline__ void produce(MarchStage& S, uint64_t* full, const MarchArgs& M, int c,
-                                        const LaneDesc& L, int lane) {
-    const double* U = M.A.u;
-    const double* Dd = M.deff;
-    const double sv = sent();
-    double* V = S.v;
-    if (c >= 0) {
-        const int64_t cb = (int64_t)c * 512;
-        int nb[6];
-#pragma unroll
-        for (int f = 0; f < 6; ++f) nb[f] = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 24 + f);
-        const int key = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 30);
-        const int flg = (int)__shfl_sync(0xffffffffu, (unsigned)L.v, 31);
-        const bool bulk = flg & kFlagBulk;
-        if (lane == 0) {
-            // stage memory was last touched through the generic proxy
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            // bytes of every bulk copy of this stage, registered before issue
-            unsigned bytes = bulk ? 8192u : 0u;
-#pragma unroll
-            for (int f = 0; f < 6; ++f)
-                if ((f < 2 || f >= 4) && nb[f] >= 0) bytes += 1024u;
-            if (bytes) mbar_expect_tx(full, bytes);
-            if (bulk) {
-                bulk_g2s(&V[0], U + cb, 4096u, full);
-                bulk_g2s(&V[kDOff], Dd + cb, 4096u, full);
-            }
-            // x faces from the contiguous side arrays: x- halo = neighbour's
-            // x=7 plane (side 1), x+ halo = neighbour's x=0 plane (side 0)
-#pragma unroll
-            for (int f = 0; f < 2; ++f)
-                if (nb[f] >= 0) {
-                    const int64_t src = ((int64_t)nb[f] * 2 + (1 - f)) * 64;
-                    bulk_g2s(&V[kHX + f * 64], M.xfu + src, 512u, full);
-                    bulk_g2s(&V[kDOff + kHX + f * 64], M.xfd + src, 512u, full);
-                }
-            // z faces: plane z=7 (z- halo) / z=0 (z+ halo)
-#pragma unroll
-            for (int f = 0; f < 2; ++f)
-                if (nb[4 + f] >= 0) {
-                    const int64_t src = (int64_t)nb[4 + f] * 512 + (f == 0 ? 448 : 0);
-                    bulk_g2s(&V[kHZ + f * 64], U + src, 512u, full);
-                    bulk_g2s(&V[kDOff + kHZ + f * 64], Dd + src, 512u, full);
-                }
-        }
-        if (!bulk) {
-            // sparse chunk: 16-B copies of pairs holding an active (u) /
-            // fluid (D) node only, so empty sectors are never read
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int off = r * 64 + 2 * lane;
-                if ((L.pm >> (2 * r)) & 1u) cp16(&V[off], U + cb + off);
-                if ((L.pm >> (2 * r + 1)) & 1u)
-                    cp16(&V[kDOff + off], Dd + cb + off);
-                else
-                    *reinterpret_cast<double2*>(&V[kDOff + off]) = make_double2(sv, sv);
-            }
-        }
-#pragma unroll
-        for (int f = 0; f < 6; ++f)
-            if ((f < 2 || f >= 4) && nb[f] < 0) {
-                const int base = f < 2 ? kHX + f * 64 : kHZ + (f - 4) * 64;
-                *reinterpret_cast<double2*>(&V[kDOff + base + 2 * lane]) = make_double2(sv, sv);
-            }
-        // y faces: row y=7 (y- halo) / y=0 (y+ halo) of every plane, index z*8+x
-        {
-            const int z = lane >> 2, k = 2 * (lane & 3);
-#pragma unroll
-            for (int f = 0; f < 2; ++f) {
-                const int j = nb[2 + f];
-                const int dst = kHY + f * 64 + z * 8 + k;
-                if (j >= 0) {
-                    const int64_t src = (int64_t)j * 512 + z * 64 + (f == 0 ? 56 : 0) + k;
-                    cp16(&V[dst], U + src);
-                    cp16(&V[kDOff + dst], Dd + src);
-                } else {
-                    *reinterpret_cast<double2*>(&V[kDOff + dst]) = make_double2(sv, sv);
-                }
-            }
-        }
-        if (lane < 8) S.act[lane] = L.v;
-        if (lane >= 16 && lane < 24) S.snk[lane - 16] = L.v;
-        if (lane == 0) S.meta = make_int4(c, key, flg, 0);
-    } else if (lane == 0) {
-        S.meta = make_int4(-1, 0, 0, 0);
-    }
-    cp_async_arrive_noinc(full);  // completes when this lane's copies land
-    mbar_arrive(full);            // orders this lane's plain smem stores
-}
-
-// Face flux F(a|b) shared by both endpoints; 0 when either side is not fluid.
-__device__ __forceinline__ double face(double da, double db, double ua, double ub) {
-    const double s = da + db;
-    const double f = (s * 0.5) * (ub - ua);
-    return ((unsigned)__double2hiint(s) == kSentHi) ? 0.0 : f;
-}
+struct Halo {  // face-lane halo values of one plane
+    double xu, xd;   // x- (xp==0) or x+ (xp==3)
+    double2 yu, yd;  // y- (y==0) or y+ (y==7)
+};
 
 struct SlowConsts {
     int64_t size[3];
@@ -288,56 +135,112 @@ __device__ __noinline__ double slow_node(const SlowConsts& K, double u_c, double
     return u_c + K.dt * lap + K.dt * rate;
 }
 
-// Loop-invariant per-thread element offsets inside a stage region.
-struct Offs {
-    int c, l, r, ym, yp, zm, zp;
+// Face flux F(a|b) shared by both endpoints; 0 when either side is not fluid.
+__device__ __forceinline__ double face(double da, double db, double ua, double ub) {
+    const double s = da + db;
+    const double f = (s * 0.5) * (ub - ua);
+    return ((unsigned)__double2hiint(s) == kSentHi) ? 0.0 : f;
+}
+__device__ __forceinline__ double fface(double da, double db, double ua, double ub) {
+    return ((da + db) * 0.5) * (ub - ua);
+}
+
+struct ChunkCtx {
+    int c, key, flags;
+    int nb[6];
+    uint32_t lm;
 };
 
+// Loads the lane's pair of plane p of the chunk (p = -1 / 8: the z halo
+// planes of the z-neighbours). Missing data reads as the sentinel.
+__device__ __forceinline__ Plane load_plane(const MarchArgs& M, const ChunkCtx& C, int p, int bp) {
+    Plane P;
+    P.u = make_double2(0.0, 0.0);
+    P.d = make_double2(sent(), sent());
+    int64_t off = -1;
+    if (p < 0) {
+        if (C.nb[4] >= 0) off = (int64_t)C.nb[4] * 512 + 448 + bp;
+    } else if (p > 7) {
+        if (C.nb[5] >= 0) off = (int64_t)C.nb[5] * 512 + bp;
+    } else if ((C.lm >> (2 * p)) & 3u) {
+        off = (int64_t)C.c * 512 + p * 64 + bp;
+    }
+    if (off >= 0) {
+        P.u = __ldg(reinterpret_cast<const double2*>(M.A.u + off));
+        P.d = __ldg(reinterpret_cast<const double2*>(M.deff + off));
+    }
+    return P;
+}
+
+__device__ __forceinline__ Halo load_halo(const MarchArgs& M, const ChunkCtx& C, int p, int y,
+                                          int xp, int x0) {
+    Halo H;
+    H.xu = 0.0;
+    H.xd = sent();
+    H.yu = make_double2(0.0, 0.0);
+    H.yd = make_double2(sent(), sent());
+    if (xp == 0 || xp == 3) {
+        const int j = xp == 0 ? C.nb[0] : C.nb[1];
+        if (j >= 0) {
+            // x- halo = neighbour's x=7 plane (side 1), x+ = its x=0 plane
+            const int64_t off = ((int64_t)j * 2 + (xp == 0 ? 1 : 0)) * 64 + p * 8 + y;
+            H.xu = __ldg(M.xfu + off);
+            H.xd = __ldg(M.xfd + off);
+        }
+    }
+    if (y == 0 || y == 7) {
+        const int j = y == 0 ? C.nb[2] : C.nb[3];
+        if (j >= 0) {
+            const int64_t off = (int64_t)j * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
+            H.yu = __ldg(reinterpret_cast<const double2*>(M.A.u + off));
+            H.yd = __ldg(reinterpret_cast<const double2*>(M.deff + off));
+        }
+    }
+    return H;
+}
+
 template <int REACTION>
-__device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
-                                        const SlowConsts& K, const Offs& O, int z, int lane) {
-    const StepArgs<double>& A = M.A;
+__device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
+                                              const ChunkCtx& C, int z, const Plane& Pm,
+                                              const Plane& P0, const Plane& Pp, const Halo& H,
+                                              int lane) {
     const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
-    const int bp = y * 8 + x0;
-    const uint64_t actw = S.act[z];
-    const bool a0 = (actw >> bp) & 1ull, a1 = (actw >> (bp + 1)) & 1ull;
+    // neighbours within the plane: shuffles first (all lanes converged)
+    const double sUL = shfl_up_d(P0.u.y, 1), sDL = shfl_up_d(P0.d.y, 1);
+    const double sUR = shfl_dn_d(P0.u.x, 1), sDR = shfl_dn_d(P0.d.x, 1);
+    const double sUYm0 = shfl_up_d(P0.u.x, 4), sUYm1 = shfl_up_d(P0.u.y, 4);
+    const double sDYm0 = shfl_up_d(P0.d.x, 4), sDYm1 = shfl_up_d(P0.d.y, 4);
+    const double sUYp0 = shfl_dn_d(P0.u.x, 4), sUYp1 = shfl_dn_d(P0.u.y, 4);
+    const double sDYp0 = shfl_dn_d(P0.d.x, 4), sDYp1 = shfl_dn_d(P0.d.y, 4);
+    const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
     if (!(a0 | a1)) return;
-    const double* V = S.v;
-    const int4 meta = S.meta;
-    const int c = meta.x;
-    const double2 uc = *reinterpret_cast<const double2*>(&V[O.c]);
-    const double2 dc = *reinterpret_cast<const double2*>(&V[O.c + kDOff]);
-    const double uL = V[O.l], dL = V[O.l + kDOff];
-    const double uR = V[O.r], dR = V[O.r + kDOff];
-    const double2 uym = *reinterpret_cast<const double2*>(&V[O.ym]);
-    const double2 dym = *reinterpret_cast<const double2*>(&V[O.ym + kDOff]);
-    const double2 uyp = *reinterpret_cast<const double2*>(&V[O.yp]);
-    const double2 dyp = *reinterpret_cast<const double2*>(&V[O.yp + kDOff]);
-    const double2 uzm = *reinterpret_cast<const double2*>(&V[O.zm]);
-    const double2 dzm = *reinterpret_cast<const double2*>(&V[O.zm + kDOff]);
-    const double2 uzp = *reinterpret_cast<const double2*>(&V[O.zp]);
-    const double2 dzp = *reinterpret_cast<const double2*>(&V[O.zp + kDOff]);
-    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((S.snk[z] >> bp) & 1ull);
-    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((S.snk[z] >> (bp + 1)) & 1ull);
-    const int o = O.c;  // body offset of node 0 == in-chunk offset
+    const double uL = xp == 0 ? H.xu : sUL, dL = xp == 0 ? H.xd : sDL;
+    const double uR = xp == 3 ? H.xu : sUR, dR = xp == 3 ? H.xd : sDR;
+    const double2 uym = y == 0 ? H.yu : make_double2(sUYm0, sUYm1);
+    const double2 dym = y == 0 ? H.yd : make_double2(sDYm0, sDYm1);
+    const double2 uyp = y == 7 ? H.yu : make_double2(sUYp0, sUYp1);
+    const double2 dyp = y == 7 ? H.yd : make_double2(sDYp0, sDYp1);
+    const double2 uc = P0.u, dc = P0.d;
+    const double2 uzm = Pm.u, dzm = Pm.d, uzp = Pp.u, dzp = Pp.d;
+    const StepArgs<double>& A = M.A;
+    const int o = z * 64 + y * 8 + x0;
+    const int c = C.c;
+    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
+    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
     double src0 = 0.0, src1 = 0.0;
     if (REACTION == PD_REACTION_VOLUMETRIC) {
         src0 = A.src[(int64_t)c * 512 + o];
         src1 = A.src[(int64_t)c * 512 + o + 1];
     }
+    const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
     double out0 = 0.0, out1 = 0.0;
-    bool slow0 = (meta.z & kFlagDirichlet) != 0, slow1 = slow0;
-    if ((meta.z >> (8 + z)) & 1) {
-        // interior-fluid plane: every node and every neighbour is fluid, so
-        // no face needs the substitution select (warp-uniform branch)
-        auto fface = [](double da, double db, double ua, double ub) {
-            return ((da + db) * 0.5) * (ub - ua);
-        };
+    bool slow0 = (C.flags & kFlagDirichlet) != 0, slow1 = slow0;
+    if ((C.flags >> (8 + z)) & 1) {
+        // interior-fluid plane (warp-uniform): no substitution anywhere
         const double fxl = fface(dL, dc.x, uL, uc.x);
         const double fxi = fface(dc.x, dc.y, uc.x, uc.y);
         const double fxr = fface(dc.y, dR, uc.y, uR);
-        const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
-        double lap0 = 0.0;
+        double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
         lap0 += (fxi - fxl) * ix;
         lap0 += (fface(dc.x, dyp.x, uc.x, uyp.x) - fface(dym.x, dc.x, uym.x, uc.x)) * iy;
         lap0 += (fface(dc.x, dzp.x, uc.x, uzp.x) - fface(dzm.x, dc.x, uzm.x, uc.x)) * iz;
@@ -361,8 +264,7 @@ __device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
         const double fxl = face(dL, dc.x, uL, uc.x);
         const double fxi = face(dc.x, dc.y, uc.x, uc.y);
         const double fxr = face(dc.y, dR, uc.y, uR);
-        const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
-        double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
+        double lap0 = 0.0;
         lap0 += (fxi - fxl) * ix;
         lap0 += (face(dc.x, dyp.x, uc.x, uyp.x) - face(dym.x, dc.x, uym.x, uc.x)) * iy;
         lap0 += (face(dc.x, dzp.x, uc.x, uzp.x) - face(dzm.x, dc.x, uzm.x, uc.x)) * iz;
@@ -380,26 +282,27 @@ __device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
         }
         out0 = uc.x + K.dt * lap0 + K.dt * r0;
         out1 = uc.y + K.dt * lap1 + K.dt * r1;
-        slow0 = !isfinite(out0);
-        slow1 = !isfinite(out1);
+        // walls (active, not fluid) stay frozen (solver.hpp:413-417)
+        if (sentinel(dc.x)) out0 = uc.x;
+        if (sentinel(dc.y)) out1 = uc.y;
+        slow0 = !isfinite(out0) && !sentinel(dc.x);
+        slow1 = !isfinite(out1) && !sentinel(dc.y);
     }
     if (slow0 | slow1) {
-        const int kx = meta.y & 1023, ky = (meta.y >> 10) & 1023, kz = (meta.y >> 20) & 1023;
+        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
         const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
         if (slow0) {
             const double nu[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
             const double nd[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-            out0 = slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
+            out0 = sentinel(dc.x) ? uc.x : slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
         }
         if (slow1) {
             const double nu[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
             const double nd[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-            out1 = slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
+            out1 = sentinel(dc.y) ? uc.y
+                                  : slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
         }
     }
-    // walls (active, not fluid) stay frozen (solver.hpp:413-417)
-    if (sentinel(dc.x)) out0 = uc.x;
-    if (sentinel(dc.y)) out1 = uc.y;
     double* dst = A.un + (int64_t)c * 512 + o;
     if (a0 && a1)
         *reinterpret_cast<double2*>(dst) = make_double2(out0, out1);
@@ -421,13 +324,42 @@ __device__ __forceinline__ void consume(const MarchStage& S, const MarchArgs& M,
 }
 
 template <int REACTION>
-__global__ void __launch_bounds__(kMarchThreads, kCtasPerSm) ftcs_march_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    MarchStage* st = reinterpret_cast<MarchStage*>(smem_raw);
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+__device__ __forceinline__ void march_chunk(const MarchArgs& M, const SlowConsts& K,
+                                            const ChunkCtx& C, int lane) {
+    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp, bp = y * 8 + x0;
+    Plane pm = load_plane(M, C, -1, bp);
+    Plane p0 = load_plane(M, C, 0, bp);
+    Plane p1 = load_plane(M, C, 1, bp);
+    Halo h0 = load_halo(M, C, 0, y, xp, x0);
+    Halo h1 = load_halo(M, C, 1, y, xp, x0);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) {
+        Plane p2;
+        Halo h2;
+        if (z + 2 <= 8) p2 = load_plane(M, C, z + 2, bp);
+        if (z + 2 <= 7) h2 = load_halo(M, C, z + 2, y, xp, x0);
+        compute_plane<REACTION>(M, K, C, z, pm, p0, p1, h0, lane);
+        pm = p0;
+        p0 = p1;
+        p1 = p2;
+        h0 = h1;
+        h1 = h2;
+    }
+}
+
+__device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
+    lm = 0u;
+    dv = -1;
+    if (c < 0) return;
+    lm = __ldg(&M.lm[(int64_t)c * 32 + lane]);
+    if (lane >= 24) dv = __ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
+}
+
+template <int REACTION, int OCC>
+__global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
+    const int lane = t & 31;
     const StepArgs<double>& A = M.A;
     if (A.k > 0) {
         const int prev = A.flags[A.k - 1];
@@ -437,10 +369,6 @@ __global__ void __launch_bounds__(kMarchThreads, kCtasPerSm) ftcs_march_kernel(M
         }
     }
     if (t == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 64);               // 32 async + 32 plain arrivals
-            mbar_init(&empty[s], kConsumerWarps);  // one per consumer warp
-        }
         for (int a = 0; a < 3; ++a) {
             K.size[a] = A.size[a];
             K.inv_dx2[a] = A.inv_dx2[a];
@@ -452,95 +380,61 @@ __global__ void __launch_bounds__(kMarchThreads, kCtasPerSm) ftcs_march_kernel(M
         K.dirichlet = A.dirichlet;
     }
     __syncthreads();
-
-    if (warp == kConsumerWarps) {
-        // ---- producer: ids per batch in lane registers, descriptors kAhead
-        // chunks ahead, the batch after next claimed while this one streams ----
-        constexpr int kAhead = 4;
-        int b_cur = 0, b_nxt = 0, b_far = 0;
-        if (lane == 0) {
-            b_cur = atomicAdd(M.counter, kBatch);
-            b_nxt = atomicAdd(M.counter, kBatch);
+    // this warp's part of the schedule
+    const int gw = blockIdx.x * kWarps + (t >> 5);
+    const int part = gw % kParts;
+    const int64_t p_begin = M.n * part / kParts, p_end = M.n * (part + 1) / kParts;
+    int* ctr = M.counter + part;
+    auto claim = [&]() -> int64_t {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(ctr, kBatch);
+        return p_begin + __shfl_sync(0xffffffffu, v, 0);
+    };
+    int64_t pos = claim();
+    int64_t nxt = claim();
+    int i = 0;
+    auto chunk_at = [&](int64_t b, int k) -> int {
+        const int64_t p = b + k;
+        return p < p_end ? __ldg(&M.sched[p]) : -1;
+    };
+    int c = chunk_at(pos, 0);
+    uint32_t lm;
+    int dv;
+    load_ctx(M, c, lane, lm, dv);
+    while (c >= 0) {
+        // next chunk id and context, prefetched while this chunk marches
+        int64_t nb_pos = pos;
+        int ni = i + 1;
+        if (ni == kBatch) {
+            nb_pos = nxt;
+            ni = 0;
         }
-        b_cur = __shfl_sync(0xffffffffu, b_cur, 0);
-        b_nxt = __shfl_sync(0xffffffffu, b_nxt, 0);
-        auto ld_id = [&](int b) -> int {
-            const int64_t p = (int64_t)b + lane;
-            return p < M.n ? __ldg(&M.sched[p]) : -1;
-        };
-        int id_cur = ld_id(b_cur), id_nxt = ld_id(b_nxt), id_far = -1;
-        int pos = 0;  // position of the chunk being produced inside batch b_cur
-        auto id_ahead = [&](int k) -> int {  // chunk id k positions after pos
-            const int p = pos + k;
-            return p < kBatch ? __shfl_sync(0xffffffffu, id_cur, p)
-                              : __shfl_sync(0xffffffffu, id_nxt, p - kBatch);
-        };
-        int cid[kAhead];
-        LaneDesc ring[kAhead];
+        const int c_next = chunk_at(nb_pos, ni);
+        uint32_t lm_n;
+        int dv_n;
+        load_ctx(M, c_next, lane, lm_n, dv_n);
+        ChunkCtx C;
+        C.c = c;
+        C.lm = lm;
 #pragma unroll
-        for (int k = 0; k < kAhead; ++k) {
-            cid[k] = id_ahead(k);
-            ring[k] = load_lane_desc(M, cid[k], lane);
+        for (int f = 0; f < 6; ++f) C.nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
+        C.key = __shfl_sync(0xffffffffu, dv, 30);
+        C.flags = __shfl_sync(0xffffffffu, dv, 31);
+        march_chunk<REACTION>(M, K, C, lane);
+        if (ni == 0) {
+            pos = nxt;
+            nxt = claim();
         }
-        bool done = false;
-        for (int q0 = 0; !done; q0 += kStages) {
-#pragma unroll
-            for (int s = 0; s < kStages; ++s) {
-                if (q0 > 0) mbar_wait(&empty[s], ((q0 / kStages) - 1) & 1);
-                const int c = cid[0];
-                produce(st[s], &full[s], M, c, ring[0], lane);
-                if (c < 0) {
-                    done = true;
-                    break;
-                }
-                // advance the prefetch window by one chunk
-                const int c_new = cid[kAhead - 1] < 0 ? -1 : id_ahead(kAhead);
-#pragma unroll
-                for (int k = 0; k + 1 < kAhead; ++k) {
-                    cid[k] = cid[k + 1];
-                    ring[k] = ring[k + 1];
-                }
-                cid[kAhead - 1] = c_new;
-                ring[kAhead - 1] = load_lane_desc(M, c_new, lane);
-                ++pos;
-                if (pos == 1 && lane == 0) b_far = atomicAdd(M.counter, kBatch);
-                if (pos == kBatch / 2) id_far = ld_id(__shfl_sync(0xffffffffu, b_far, 0));
-                if (pos == kBatch) {
-                    pos = 0;
-                    id_cur = id_nxt;
-                    id_nxt = id_far;
-                }
-            }
-        }
-    } else {
-        // ---- consumers: warp w = z-plane w ----
-        const int z = warp, y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
-        const int o = z * 64 + y * 8 + x0;
-        Offs O;
-        O.c = o;
-        O.l = xp == 0 ? kHX + z * 8 + y : o - 1;
-        O.r = xp == 3 ? kHX + 64 + z * 8 + y : o + 2;
-        O.ym = y == 0 ? kHY + z * 8 + x0 : o - 8;
-        O.yp = y == 7 ? kHY + 64 + z * 8 + x0 : o + 8;
-        O.zm = z == 0 ? kHZ + y * 8 + x0 : o - 64;
-        O.zp = z == 7 ? kHZ + 64 + y * 8 + x0 : o + 64;
-        for (int q0 = 0;; q0 += kStages) {
-#pragma unroll
-            for (int s = 0; s < kStages; ++s) {
-                mbar_wait(&full[s], (q0 / kStages) & 1);
-                if (st[s].meta.x < 0) return;
-                consume<REACTION>(st[s], M, K, O, z, lane);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-            }
-        }
+        i = ni;
+        c = c_next;
+        lm = lm_n;
+        dv = dv_n;
     }
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
-                            const uint64_t* __restrict__ act, const uint64_t* __restrict__ flu,
-                            int64_t n, int64_t s0, int64_t s1, int64_t s2, int dirichlet,
-                            int32_t* __restrict__ desc) {
+                            const uint64_t* __restrict__ flu, int64_t n, int64_t s0, int64_t s1,
+                            int64_t s2, int dirichlet, int32_t* __restrict__ desc) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int k[3] = {keys[i * 3], keys[i * 3 + 1], keys[i * 3 + 2]};
@@ -553,15 +447,9 @@ __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __re
     }
     int nb[6];
     for (int f = 0; f < 6; ++f) nb[f] = nbr[i * 6 + f];
-    // dense chunks stream their body with bulk copies
-    int pairs = 0;
     uint64_t F[8];
-    for (int z = 0; z < 8; ++z) {
-        const uint64_t w = act[i * 8 + z];
-        pairs += __popcll((w | (w >> 1)) & 0x5555555555555555ull);
-        F[z] = flu[i * 8 + z];
-    }
-    int flags = (exposed ? kFlagDirichlet : 0) | (pairs >= 128 ? kFlagBulk : 0);
+    for (int z = 0; z < 8; ++z) F[z] = flu[i * 8 + z];
+    int flags = exposed ? kFlagDirichlet : 0;
     // interior-fluid planes: the plane and every face neighbour of its nodes fluid
     const uint64_t ALL = ~0ull;
     const uint64_t zlo = nb[4] >= 0 ? flu[(int64_t)nb[4] * 8 + 7] : 0ull;
@@ -581,6 +469,23 @@ __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __re
     desc[i * 8 + 7] = flags;
 }
 
+// Per chunk and lane (y = lane>>2, pair x0 = 2*(lane&3)): bit 2z+n = node n of
+// the lane's pair in plane z is active, bit 16+2z+n = it is a sink node.
+__global__ void lanemask_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ snk,
+                                int64_t n, uint32_t* __restrict__ lm) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * 32) return;
+    const int64_t c = t >> 5;
+    const int lane = (int)(t & 31);
+    const int bp = (lane >> 2) * 8 + 2 * (lane & 3);
+    uint32_t v = 0;
+    for (int z = 0; z < 8; ++z) {
+        v |= (uint32_t)((act[c * 8 + z] >> bp) & 3ull) << (2 * z);
+        v |= (uint32_t)((snk[c * 8 + z] >> bp) & 3ull) << (16 + 2 * z);
+    }
+    lm[t] = v;
+}
+
 // D_eff = fluid ? D : -inf over every slot; counts fluid nodes whose D is not
 // finite (then the fast path is disabled: its sentinel logic assumes finite D).
 __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __restrict__ fluid,
@@ -591,22 +496,6 @@ __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __r
     const double v = dcol[i];
     deff[i] = fl ? v : sent();
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
-}
-
-// Per chunk and producer lane: bit 2r = the lane's pair in plane r has an
-// active node, bit 2r+1 = it has a fluid node.
-__global__ void pairmask_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ flu,
-                                int64_t n, uint16_t* __restrict__ pm) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n * 32) return;
-    const int64_t c = t >> 5;
-    const int lane = (int)(t & 31);
-    unsigned v = 0;
-    for (int r = 0; r < 8; ++r) {
-        if ((act[c * 8 + r] >> (2 * lane)) & 3ull) v |= 1u << (2 * r);
-        if ((flu[c * 8 + r] >> (2 * lane)) & 3ull) v |= 1u << (2 * r + 1);
-    }
-    pm[t] = (uint16_t)v;
 }
 
 // x=0 / x=7 planes of a column into the side array [c][side][z*8+y].
@@ -627,7 +516,7 @@ void march_free(MarchPlan* p) {
     cudaFree(p->d_xf[0]);
     cudaFree(p->d_xf[1]);
     cudaFree(p->d_counter);
-    cudaFree(p->d_pm);
+    cudaFree(p->d_lm);
     *p = MarchPlan{};
 }
 
@@ -639,8 +528,8 @@ void march_extract_xfaces(pd_grid* g, MarchPlan& p, const void* col) {
     PD_CUDA(cudaGetLastError());
 }
 
-void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const void* d_dcol,
-                 int dirichlet, int64_t begin, int64_t end, MarchPlan* plan) {
+void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const uint64_t* d_sink,
+                 const void* d_dcol, int dirichlet, int64_t begin, int64_t end, MarchPlan* plan) {
     march_free(plan);
     if (g->dims != 3 || g->tbytes != 8) return;
     if (g->cc[0] > 1024 || g->cc[1] > 1024 || g->cc[2] > 1024) return;  // key packing limit
@@ -648,19 +537,18 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     if (n_all == 0 || end <= begin) return;
     PD_CUDA(cudaMalloc(&plan->d_desc, sizeof(int32_t) * 8 * (size_t)n_all));
     desc_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(
-        d_nbr, g->d_keys, g->d_masks, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet,
-        plan->d_desc);
+        d_nbr, g->d_keys, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
+    PD_CUDA(cudaGetLastError());
+    PD_CUDA(cudaMalloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
+    lanemask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink,
+                                                                                n_all, plan->d_lm);
     PD_CUDA(cudaGetLastError());
     const int64_t slots = n_all * 512;
     PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)slots));
     PD_CUDA(cudaMalloc(&plan->d_xfd, sizeof(double) * 128 * (size_t)n_all));
     PD_CUDA(cudaMalloc(&plan->d_xf[0], sizeof(double) * 128 * (size_t)n_all));
     PD_CUDA(cudaMalloc(&plan->d_xf[1], sizeof(double) * 128 * (size_t)n_all));
-    PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024));
-    PD_CUDA(cudaMalloc(&plan->d_pm, sizeof(uint16_t) * 32 * (size_t)n_all));
-    pairmask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_fluid,
-                                                                                n_all, plan->d_pm);
-    PD_CUDA(cudaGetLastError());
+    PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024 * kParts));
     unsigned long long* d_bad = nullptr;
     PD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
     PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
@@ -701,39 +589,43 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaStreamSynchronize(g->stream));
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-    plan->grid = sms * kCtasPerSm;
+    static const int occ = [] {
+        const char* e = getenv("PD_MARCH_OCC");
+        return (e && atoi(e) == 3) ? 3 : kCtasPerSm;
+    }();
+    plan->grid = sms * occ;
     plan->n = n;
     plan->ready = true;
     plan->cur = 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        const int bytes = (int)(sizeof(MarchStage) * kStages);
-        PD_CUDA(cudaFuncSetAttribute(ftcs_march_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        PD_CUDA(cudaFuncSetAttribute(ftcs_march_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        PD_CUDA(cudaFuncSetAttribute(ftcs_march_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-        attr_set = true;
-    }
 }
 
+int march_counters_per_step() { return kParts; }
+
 void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction) {
-    const size_t bytes = sizeof(MarchStage) * kStages;
     MarchArgs M;
     M.A = a;
     M.sched = p.d_stream;
     M.n = p.n;
     M.desc = p.d_desc;
-    M.pm = p.d_pm;
+    M.lm = p.d_lm;
     M.deff = p.d_deff;
     M.xfu = p.d_xf[p.cur];
     M.xfd = p.d_xfd;
     M.xfun = p.d_xf[1 - p.cur];
-    M.counter = p.d_counter + (a.k & 1023);
-    if (reaction == PD_REACTION_SURFACE_SINK)
-        ftcs_march_kernel<1><<<p.grid, kMarchThreads, bytes, g->stream>>>(M);
-    else if (reaction == PD_REACTION_VOLUMETRIC)
-        ftcs_march_kernel<2><<<p.grid, kMarchThreads, bytes, g->stream>>>(M);
-    else
-        ftcs_march_kernel<0><<<p.grid, kMarchThreads, bytes, g->stream>>>(M);
+    M.counter = p.d_counter + (int64_t)(a.k & 1023) * kParts;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    const bool occ3 = p.grid == sms * 3;
+    if (reaction == PD_REACTION_SURFACE_SINK) {
+        if (occ3) ftcs_march_kernel<1, 3><<<p.grid, kThreads, 0, g->stream>>>(M);
+        else ftcs_march_kernel<1, kCtasPerSm><<<p.grid, kThreads, 0, g->stream>>>(M);
+    } else if (reaction == PD_REACTION_VOLUMETRIC) {
+        if (occ3) ftcs_march_kernel<2, 3><<<p.grid, kThreads, 0, g->stream>>>(M);
+        else ftcs_march_kernel<2, kCtasPerSm><<<p.grid, kThreads, 0, g->stream>>>(M);
+    } else {
+        if (occ3) ftcs_march_kernel<0, 3><<<p.grid, kThreads, 0, g->stream>>>(M);
+        else ftcs_march_kernel<0, kCtasPerSm><<<p.grid, kThreads, 0, g->stream>>>(M);
+    }
     PD_CUDA(cudaGetLastError());
     p.cur = 1 - p.cur;
 }
