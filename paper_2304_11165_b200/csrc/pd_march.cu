@@ -20,11 +20,13 @@
 //   also writes the x=0 / x=7 planes of u_next into a side array (64 doubles
 //   per face, contiguous) and the stepper keeps the same for D_eff; y halos
 //   are 64-B rows and z halos 512-B planes of the neighbour chunks.
-// * Schedule. Chunks are ordered (z-block of kSeg layers, y, x, z); the order
-//   is cut into kParts contiguous parts, each consumed in kBatch-chunk claims
-//   by the warps assigned to it (atomic counter per part), so the chunks in
-//   flight form kParts short windows of the order and neighbour halos are
-//   L2 hits.
+// * Schedule. Chunks are ordered (z-block of kSeg layers, 4x4 tiles of chunk
+//   columns, column, z) and claimed kBatch at a time from one atomic counter,
+//   so the chunks in flight always form one short window of that order: the
+//   z halos were streamed by the same warp a moment ago and the x/y halos by
+//   the warps next to it in the window (L2 hits). (Cutting the order into
+//   several independently claimed parts spreads y neighbours hundreds of
+//   microseconds apart and was measured to miss L2.)
 // * Usability without masks. D_eff = fluid ? D : -inf (static per run); a
 //   neighbour is usable iff it is fluid (solver.hpp:374,379-381), i.e. iff the
 //   face sum d_a + d_b is not -inf.
@@ -48,8 +50,8 @@ namespace pdb {
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=3 selects 3)
-constexpr int kBatch = 4;
-constexpr int kParts = 32;
+constexpr int kBatch = 8;
+constexpr int kParts = 1;
 constexpr int kSeg = 16;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
@@ -79,6 +81,7 @@ struct MarchArgs {
     const double* __restrict__ xfd;  // x-face planes of D_eff   [c][side][64]
     double* __restrict__ xfun;       // x-face planes of u_next (written)
     int* counter;                    // kParts counters of this step
+    int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
 };
 
 struct Plane {  // a lane's node pair in one plane
@@ -159,9 +162,9 @@ __device__ __forceinline__ Plane load_plane(const MarchArgs& M, const ChunkCtx& 
     P.d = make_double2(sent(), sent());
     int64_t off = -1;
     if (p < 0) {
-        if (C.nb[4] >= 0) off = (int64_t)C.nb[4] * 512 + 448 + bp;
+        if (C.nb[4] >= 0 && !(M.dbg & 4)) off = (int64_t)C.nb[4] * 512 + 448 + bp;
     } else if (p > 7) {
-        if (C.nb[5] >= 0) off = (int64_t)C.nb[5] * 512 + bp;
+        if (C.nb[5] >= 0 && !(M.dbg & 4)) off = (int64_t)C.nb[5] * 512 + bp;
     } else if ((C.lm >> (2 * p)) & 3u) {
         off = (int64_t)C.c * 512 + p * 64 + bp;
     }
@@ -179,7 +182,7 @@ __device__ __forceinline__ Halo load_halo(const MarchArgs& M, const ChunkCtx& C,
     H.xd = sent();
     H.yu = make_double2(0.0, 0.0);
     H.yd = make_double2(sent(), sent());
-    if (xp == 0 || xp == 3) {
+    if ((xp == 0 || xp == 3) && !(M.dbg & 1)) {
         const int j = xp == 0 ? C.nb[0] : C.nb[1];
         if (j >= 0) {
             // x- halo = neighbour's x=7 plane (side 1), x+ = its x=0 plane
@@ -188,7 +191,7 @@ __device__ __forceinline__ Halo load_halo(const MarchArgs& M, const ChunkCtx& C,
             H.xd = __ldg(M.xfd + off);
         }
     }
-    if (y == 0 || y == 7) {
+    if ((y == 0 || y == 7) && !(M.dbg & 2)) {
         const int j = y == 0 ? C.nb[2] : C.nb[3];
         if (j >= 0) {
             const int64_t off = (int64_t)j * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
@@ -332,7 +335,7 @@ __device__ __forceinline__ void march_chunk(const MarchArgs& M, const SlowConsts
     Plane p1 = load_plane(M, C, 1, bp);
     Halo h0 = load_halo(M, C, 0, y, xp, x0);
     Halo h1 = load_halo(M, C, 1, y, xp, x0);
-#pragma unroll
+#pragma unroll 1
     for (int z = 0; z < 8; ++z) {
         Plane p2;
         Halo h2;
@@ -576,8 +579,11 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
         const int32_t* ka = &keys[(size_t)a * 3];
         const int32_t* kb = &keys[(size_t)b * 3];
+        // z-block, then 4x4 column tiles, then columns inside the tile, then z
         const int za = ka[2] / kSeg, zb = kb[2] / kSeg;
         if (za != zb) return za < zb;
+        if (ka[1] / 4 != kb[1] / 4) return ka[1] / 4 < kb[1] / 4;
+        if (ka[0] / 4 != kb[0] / 4) return ka[0] / 4 < kb[0] / 4;
         if (ka[1] != kb[1]) return ka[1] < kb[1];
         if (ka[0] != kb[0]) return ka[0] < kb[0];
         return ka[2] < kb[2];
@@ -613,6 +619,11 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     M.xfd = p.d_xfd;
     M.xfun = p.d_xf[1 - p.cur];
     M.counter = p.d_counter + (int64_t)(a.k & 1023) * kParts;
+    static const int dbg = [] {
+        const char* e = getenv("PD_MARCH_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    M.dbg = dbg;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const bool occ3 = p.grid == sms * 3;
