@@ -49,7 +49,7 @@ namespace pdb {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=3 selects 3)
+constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=5 selects 5)
 constexpr int kBatch = 8;
 constexpr int kParts = 1;
 constexpr int kSeg = 16;
@@ -63,12 +63,6 @@ __device__ __forceinline__ bool sentinel(double d) {
 }
 __device__ __forceinline__ double sent() { return __hiloint2double((int)kSentHi, 0); }
 
-__device__ __forceinline__ double shfl_up_d(double v, int d) {
-    return __shfl_up_sync(0xffffffffu, v, d);
-}
-__device__ __forceinline__ double shfl_dn_d(double v, int d) {
-    return __shfl_down_sync(0xffffffffu, v, d);
-}
 
 struct MarchArgs {
     StepArgs<double> A;
@@ -84,13 +78,6 @@ struct MarchArgs {
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
 };
 
-struct Plane {  // a lane's node pair in one plane
-    double2 u, d;
-};
-struct Halo {  // face-lane halo values of one plane
-    double xu, xd;   // x- (xp==0) or x+ (xp==3)
-    double2 yu, yd;  // y- (y==0) or y+ (y==7)
-};
 
 struct SlowConsts {
     int64_t size[3];
@@ -154,12 +141,46 @@ struct ChunkCtx {
     uint32_t lm;
 };
 
-// Loads the lane's pair of plane p of the chunk (p = -1 / 8: the z halo
-// planes of the z-neighbours). Missing data reads as the sentinel.
-__device__ __forceinline__ Plane load_plane(const MarchArgs& M, const ChunkCtx& C, int p, int bp) {
-    Plane P;
-    P.u = make_double2(0.0, 0.0);
-    P.d = make_double2(sent(), sent());
+// Per-warp ring of plane tiles in shared memory. A tile holds u and D_eff of
+// one z-plane of a chunk on a 10x10 (x, y in [-1, 8]) footprint: the 8x8 body
+// plus the one-node x / y halo ring. Cell (x, y) lives at tix(x, y) (+1 pad so
+// that x-pairs are 16-B aligned).
+constexpr int kTileN = 102;  // doubles per array per tile
+constexpr int kRing = 6;     // kAhead + 3 (planes z-1, z, z+1 resident)
+constexpr int kAhead = 3;    // plane loads in flight beyond the one needed
+struct Tile {
+    double u[kTileN];
+    double d[kTileN];
+};
+__device__ __forceinline__ int tix(int x, int y) { return 2 + x + 10 * (y + 1); }
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Issues the lane's share of plane p (-1..8) of chunk C into tile T:
+// predicated 16-B copies of its node pair (pairs with no active node are
+// never read; their D_eff cells get the sentinel) and, for chunk-face lanes,
+// the x / y halo cells. p = -1 / 8 are the z halo planes of the z neighbours.
+__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const ChunkCtx& C, int p,
+                                            int y, int xp, int x0) {
+    const int t0 = tix(x0, y);
+    const double sv = sent();
+    const double* U = M.A.u;
+    const double* Dd = M.deff;
+    const int bp = y * 8 + x0;
     int64_t off = -1;
     if (p < 0) {
         if (C.nb[4] >= 0 && !(M.dbg & 4)) off = (int64_t)C.nb[4] * 512 + 448 + bp;
@@ -169,62 +190,57 @@ __device__ __forceinline__ Plane load_plane(const MarchArgs& M, const ChunkCtx& 
         off = (int64_t)C.c * 512 + p * 64 + bp;
     }
     if (off >= 0) {
-        P.u = __ldg(reinterpret_cast<const double2*>(M.A.u + off));
-        P.d = __ldg(reinterpret_cast<const double2*>(M.deff + off));
+        cp16(&T.u[t0], U + off);
+        cp16(&T.d[t0], Dd + off);
+    } else {
+        *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
     }
-    return P;
-}
-
-__device__ __forceinline__ Halo load_halo(const MarchArgs& M, const ChunkCtx& C, int p, int y,
-                                          int xp, int x0) {
-    Halo H;
-    H.xu = 0.0;
-    H.xd = sent();
-    H.yu = make_double2(0.0, 0.0);
-    H.yd = make_double2(sent(), sent());
-    if ((xp == 0 || xp == 3) && !(M.dbg & 1)) {
-        const int j = xp == 0 ? C.nb[0] : C.nb[1];
+    if (p < 0 || p > 7) return;
+    if (xp == 0 || xp == 3) {
+        const int j = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
+        const int tx = xp == 0 ? t0 - 1 : t0 + 2;
         if (j >= 0) {
             // x- halo = neighbour's x=7 plane (side 1), x+ = its x=0 plane
-            const int64_t off = ((int64_t)j * 2 + (xp == 0 ? 1 : 0)) * 64 + p * 8 + y;
-            H.xu = __ldg(M.xfu + off);
-            H.xd = __ldg(M.xfd + off);
+            const int64_t o = ((int64_t)j * 2 + (xp == 0 ? 1 : 0)) * 64 + p * 8 + y;
+            cp8(&T.u[tx], M.xfu + o);
+            cp8(&T.d[tx], M.xfd + o);
+        } else {
+            T.d[tx] = sv;
         }
     }
-    if ((y == 0 || y == 7) && !(M.dbg & 2)) {
-        const int j = y == 0 ? C.nb[2] : C.nb[3];
+    if (y == 0 || y == 7) {
+        const int j = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
+        const int ty = y == 0 ? t0 - 10 : t0 + 10;
         if (j >= 0) {
-            const int64_t off = (int64_t)j * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
-            H.yu = __ldg(reinterpret_cast<const double2*>(M.A.u + off));
-            H.yd = __ldg(reinterpret_cast<const double2*>(M.deff + off));
+            const int64_t o = (int64_t)j * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
+            cp16(&T.u[ty], U + o);
+            cp16(&T.d[ty], Dd + o);
+        } else {
+            *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
         }
     }
-    return H;
 }
 
 template <int REACTION>
 __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
-                                              const ChunkCtx& C, int z, const Plane& Pm,
-                                              const Plane& P0, const Plane& Pp, const Halo& H,
-                                              int lane) {
+                                              const ChunkCtx& C, int z, const Tile& Tm,
+                                              const Tile& T0, const Tile& Tp, int lane) {
     const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
-    // neighbours within the plane: shuffles first (all lanes converged)
-    const double sUL = shfl_up_d(P0.u.y, 1), sDL = shfl_up_d(P0.d.y, 1);
-    const double sUR = shfl_dn_d(P0.u.x, 1), sDR = shfl_dn_d(P0.d.x, 1);
-    const double sUYm0 = shfl_up_d(P0.u.x, 4), sUYm1 = shfl_up_d(P0.u.y, 4);
-    const double sDYm0 = shfl_up_d(P0.d.x, 4), sDYm1 = shfl_up_d(P0.d.y, 4);
-    const double sUYp0 = shfl_dn_d(P0.u.x, 4), sUYp1 = shfl_dn_d(P0.u.y, 4);
-    const double sDYp0 = shfl_dn_d(P0.d.x, 4), sDYp1 = shfl_dn_d(P0.d.y, 4);
     const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
     if (!(a0 | a1)) return;
-    const double uL = xp == 0 ? H.xu : sUL, dL = xp == 0 ? H.xd : sDL;
-    const double uR = xp == 3 ? H.xu : sUR, dR = xp == 3 ? H.xd : sDR;
-    const double2 uym = y == 0 ? H.yu : make_double2(sUYm0, sUYm1);
-    const double2 dym = y == 0 ? H.yd : make_double2(sDYm0, sDYm1);
-    const double2 uyp = y == 7 ? H.yu : make_double2(sUYp0, sUYp1);
-    const double2 dyp = y == 7 ? H.yd : make_double2(sDYp0, sDYp1);
-    const double2 uc = P0.u, dc = P0.d;
-    const double2 uzm = Pm.u, dzm = Pm.d, uzp = Pp.u, dzp = Pp.d;
+    const int t0 = tix(x0, y);
+    const double2 uc = *reinterpret_cast<const double2*>(&T0.u[t0]);
+    const double2 dc = *reinterpret_cast<const double2*>(&T0.d[t0]);
+    const double uL = T0.u[t0 - 1], dL = T0.d[t0 - 1];
+    const double uR = T0.u[t0 + 2], dR = T0.d[t0 + 2];
+    const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 10]);
+    const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 10]);
+    const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 10]);
+    const double2 dyp = *reinterpret_cast<const double2*>(&T0.d[t0 + 10]);
+    const double2 uzm = *reinterpret_cast<const double2*>(&Tm.u[t0]);
+    const double2 dzm = *reinterpret_cast<const double2*>(&Tm.d[t0]);
+    const double2 uzp = *reinterpret_cast<const double2*>(&Tp.u[t0]);
+    const double2 dzp = *reinterpret_cast<const double2*>(&Tp.d[t0]);
     const StepArgs<double>& A = M.A;
     const int o = z * 64 + y * 8 + x0;
     const int c = C.c;
@@ -326,30 +342,6 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
     }
 }
 
-template <int REACTION>
-__device__ __forceinline__ void march_chunk(const MarchArgs& M, const SlowConsts& K,
-                                            const ChunkCtx& C, int lane) {
-    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp, bp = y * 8 + x0;
-    Plane pm = load_plane(M, C, -1, bp);
-    Plane p0 = load_plane(M, C, 0, bp);
-    Plane p1 = load_plane(M, C, 1, bp);
-    Halo h0 = load_halo(M, C, 0, y, xp, x0);
-    Halo h1 = load_halo(M, C, 1, y, xp, x0);
-#pragma unroll 1
-    for (int z = 0; z < 8; ++z) {
-        Plane p2;
-        Halo h2;
-        if (z + 2 <= 8) p2 = load_plane(M, C, z + 2, bp);
-        if (z + 2 <= 7) h2 = load_halo(M, C, z + 2, y, xp, x0);
-        compute_plane<REACTION>(M, K, C, z, pm, p0, p1, h0, lane);
-        pm = p0;
-        p0 = p1;
-        p1 = p2;
-        h0 = h1;
-        h1 = h2;
-    }
-}
-
 __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
     lm = 0u;
     dv = -1;
@@ -358,11 +350,29 @@ __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, ui
     if (lane >= 24) dv = __ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
 }
 
+__device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
+    ChunkCtx C;
+    C.c = c;
+    C.lm = lm;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) C.nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
+    C.key = __shfl_sync(0xffffffffu, dv, 30);
+    C.flags = __shfl_sync(0xffffffffu, dv, 31);
+    return C;
+}
+
+// One warp streams a sequence of chunks. Its plane loads (10 per chunk:
+// z-halo below, the 8 body planes, z-halo above) form one continuous
+// sequence through a kRing-slot tile ring, kAhead loads ahead of the plane
+// being computed, across chunk boundaries.
 template <int REACTION, int OCC>
 __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
-    const int lane = t & 31;
+    const int lane = t & 31, warp = t >> 5;
+    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
+    Tile* ring = reinterpret_cast<Tile*>(smem_raw) + warp * kRing;
     const StepArgs<double>& A = M.A;
     if (A.k > 0) {
         const int prev = A.flags[A.k - 1];
@@ -383,56 +393,71 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         K.dirichlet = A.dirichlet;
     }
     __syncthreads();
-    // this warp's part of the schedule
-    const int gw = blockIdx.x * kWarps + (t >> 5);
-    const int part = gw % kParts;
-    const int64_t p_begin = M.n * part / kParts, p_end = M.n * (part + 1) / kParts;
-    int* ctr = M.counter + part;
+
+    // ---- chunk stream: kBatch-chunk claims from one counter ----
+    int* ctr = M.counter;
     auto claim = [&]() -> int64_t {
         int v = 0;
         if (lane == 0) v = atomicAdd(ctr, kBatch);
-        return p_begin + __shfl_sync(0xffffffffu, v, 0);
+        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
     };
-    int64_t pos = claim();
-    int64_t nxt = claim();
-    int i = 0;
-    auto chunk_at = [&](int64_t b, int k) -> int {
-        const int64_t p = b + k;
-        return p < p_end ? __ldg(&M.sched[p]) : -1;
+    int64_t b_cur = claim(), b_nxt = claim();
+    int bi = 0;  // position of the next chunk to fetch inside b_cur
+    auto next_id = [&]() -> int {
+        if (bi == kBatch) {
+            b_cur = b_nxt;
+            b_nxt = claim();
+            bi = 0;
+        }
+        const int64_t p = b_cur + bi++;
+        return p < M.n ? __ldg(&M.sched[p]) : -1;
     };
-    int c = chunk_at(pos, 0);
-    uint32_t lm;
-    int dv;
-    load_ctx(M, c, lane, lm, dv);
-    while (c >= 0) {
-        // next chunk id and context, prefetched while this chunk marches
-        int64_t nb_pos = pos;
-        int ni = i + 1;
-        if (ni == kBatch) {
-            nb_pos = nxt;
-            ni = 0;
+
+    // loading side: chunk whose planes are being issued, and the next one
+    int c_ld = next_id();
+    if (c_ld < 0) return;
+    uint32_t lm0, lm1;
+    int dv0, dv1;
+    load_ctx(M, c_ld, lane, lm0, dv0);
+    ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
+    int c_nx = next_id();
+    load_ctx(M, c_nx, lane, lm1, dv1);
+    int p_ld = -1;    // next plane of Cld to issue (-1..8)
+    int64_t L = 0;    // loads issued
+    auto issue_next = [&]() {
+        if (Cld.c >= 0) issue_plane(ring[L % kRing], M, Cld, p_ld, y, xp, x0);
+        cp_commit();
+        ++L;
+        if (++p_ld == 9) {  // advance the load side to the next chunk
+            p_ld = -1;
+            Cld = make_ctx(c_nx, lm1, dv1);
+            c_nx = Cld.c >= 0 ? next_id() : -1;
+            load_ctx(M, c_nx, lane, lm1, dv1);
         }
-        const int c_next = chunk_at(nb_pos, ni);
-        uint32_t lm_n;
-        int dv_n;
-        load_ctx(M, c_next, lane, lm_n, dv_n);
-        ChunkCtx C;
-        C.c = c;
-        C.lm = lm;
-#pragma unroll
-        for (int f = 0; f < 6; ++f) C.nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
-        C.key = __shfl_sync(0xffffffffu, dv, 30);
-        C.flags = __shfl_sync(0xffffffffu, dv, 31);
-        march_chunk<REACTION>(M, K, C, lane);
-        if (ni == 0) {
-            pos = nxt;
-            nxt = claim();
+    };
+    // compute side: follows the load side, which is never more than one
+    // chunk ahead (kAhead + 3 < 10 loads)
+    ChunkCtx Cc = Cld;
+    int64_t base = 0;  // load index of plane -1 of Cc
+    // prologue: planes -1, 0, 1 needed for z = 0, plus kAhead more
+    for (int k = 0; k < 3 + kAhead; ++k) issue_next();
+    while (Cc.c >= 0) {
+#pragma unroll 1
+        for (int z = 0; z < 8; ++z) {
+            // loads up to index base+z+2 complete; exactly kAhead newer groups
+            // are in flight at this point of every iteration
+            cp_wait<kAhead>();
+            __syncwarp();
+            compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) % kRing], ring[(base + z + 1) % kRing],
+                                    ring[(base + z + 2) % kRing], lane);
+            __syncwarp();
+            const int64_t need_next = z < 7 ? base + z + 3 : base + 12;
+            while (L <= need_next + kAhead) issue_next();
         }
-        i = ni;
-        c = c_next;
-        lm = lm_n;
-        dv = dv_n;
+        base += 10;
+        Cc = Cld;
     }
+    cp_wait<0>();
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
@@ -597,7 +622,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
     static const int occ = [] {
         const char* e = getenv("PD_MARCH_OCC");
-        return (e && atoi(e) == 3) ? 3 : kCtasPerSm;
+        return (e && atoi(e) == 5) ? 5 : kCtasPerSm;
     }();
     plan->grid = sms * occ;
     plan->n = n;
@@ -626,16 +651,25 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     M.dbg = dbg;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-    const bool occ3 = p.grid == sms * 3;
+    const bool occ5 = p.grid == sms * 5;
+    const size_t bytes = sizeof(Tile) * kRing * kWarps;
+    auto go = [&](auto kern) {
+        static bool set = false;  // one flag per kernel instantiation
+        if (!set) {
+            PD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            set = true;
+        }
+        kern<<<p.grid, kThreads, bytes, g->stream>>>(M);
+    };
     if (reaction == PD_REACTION_SURFACE_SINK) {
-        if (occ3) ftcs_march_kernel<1, 3><<<p.grid, kThreads, 0, g->stream>>>(M);
-        else ftcs_march_kernel<1, kCtasPerSm><<<p.grid, kThreads, 0, g->stream>>>(M);
+        if (occ5) go(ftcs_march_kernel<1, 5>);
+        else go(ftcs_march_kernel<1, kCtasPerSm>);
     } else if (reaction == PD_REACTION_VOLUMETRIC) {
-        if (occ3) ftcs_march_kernel<2, 3><<<p.grid, kThreads, 0, g->stream>>>(M);
-        else ftcs_march_kernel<2, kCtasPerSm><<<p.grid, kThreads, 0, g->stream>>>(M);
+        if (occ5) go(ftcs_march_kernel<2, 5>);
+        else go(ftcs_march_kernel<2, kCtasPerSm>);
     } else {
-        if (occ3) ftcs_march_kernel<0, 3><<<p.grid, kThreads, 0, g->stream>>>(M);
-        else ftcs_march_kernel<0, kCtasPerSm><<<p.grid, kThreads, 0, g->stream>>>(M);
+        if (occ5) go(ftcs_march_kernel<0, 5>);
+        else go(ftcs_march_kernel<0, kCtasPerSm>);
     }
     PD_CUDA(cudaGetLastError());
     p.cur = 1 - p.cur;
