@@ -39,6 +39,7 @@
 //   whose fast result is non-finite, and chunks that touch a Dirichlet outer
 //   face, take the exact generic path on the same register values.
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -142,27 +143,30 @@ struct ChunkCtx {
 };
 
 // Per-warp ring of plane tiles in shared memory. A tile holds u and D_eff of
-// one z-plane of a chunk on a 10x10 (x, y in [-1, 8]) footprint: the 8x8 body
-// plus the one-node x / y halo ring. Cell (x, y) lives at tix(x, y) (+1 pad so
-// that x-pairs are 16-B aligned).
-constexpr int kTileN = 102;  // doubles per array per tile
-constexpr int kRing = 6;     // kAhead + 3 (planes z-1, z, z+1 resident)
-constexpr int kAhead = 3;    // plane loads in flight beyond the one needed
+// one z-plane of a chunk: rows y = -1..8 of the 8 body columns (pitch 8, so
+// the lanes' 16-B pair accesses are bank-conflict free) and the x- / x+ halo
+// cells of rows 0..7 in two side columns.
+constexpr int kRing = 8;   // power of two: slot = load index & 7
+constexpr int kAhead = 5;  // kRing - 3 (planes z-1, z, z+1 resident)
 struct Tile {
-    double u[kTileN];
-    double d[kTileN];
+    double u[80], hxu[2][8];
+    double d[80], hxd[2][8];
 };
-__device__ __forceinline__ int tix(int x, int y) { return 2 + x + 10 * (y + 1); }
+__device__ __forceinline__ int tix(int x, int y) { return x + 8 * (y + 1); }
 
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem));
+__device__ __forceinline__ void cp16_if(void* smem, const void* gmem, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(smem)),
+        "l"(gmem), "r"((int)pred));
 }
-__device__ __forceinline__ void cp8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem));
+__device__ __forceinline__ void cp8_if(void* smem, const void* gmem, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(smem)),
+        "l"(gmem), "r"((int)pred));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -178,47 +182,39 @@ __device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const C
                                             int y, int xp, int x0) {
     const int t0 = tix(x0, y);
     const double sv = sent();
-    const double* U = M.A.u;
-    const double* Dd = M.deff;
     const int bp = y * 8 + x0;
-    int64_t off = -1;
-    if (p < 0) {
-        if (C.nb[4] >= 0 && !(M.dbg & 4)) off = (int64_t)C.nb[4] * 512 + 448 + bp;
-    } else if (p > 7) {
-        if (C.nb[5] >= 0 && !(M.dbg & 4)) off = (int64_t)C.nb[5] * 512 + bp;
-    } else if ((C.lm >> (2 * p)) & 3u) {
-        off = (int64_t)C.c * 512 + p * 64 + bp;
-    }
-    if (off >= 0) {
-        cp16(&T.u[t0], U + off);
-        cp16(&T.d[t0], Dd + off);
-    } else {
-        *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
-    }
-    if (p < 0 || p > 7) return;
-    if (xp == 0 || xp == 3) {
-        const int j = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
-        const int tx = xp == 0 ? t0 - 1 : t0 + 2;
-        if (j >= 0) {
-            // x- halo = neighbour's x=7 plane (side 1), x+ = its x=0 plane
-            const int64_t o = ((int64_t)j * 2 + (xp == 0 ? 1 : 0)) * 64 + p * 8 + y;
-            cp8(&T.u[tx], M.xfu + o);
-            cp8(&T.d[tx], M.xfd + o);
-        } else {
-            T.d[tx] = sv;
-        }
-    }
-    if (y == 0 || y == 7) {
-        const int j = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
-        const int ty = y == 0 ? t0 - 10 : t0 + 10;
-        if (j >= 0) {
-            const int64_t o = (int64_t)j * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
-            cp16(&T.u[ty], U + o);
-            cp16(&T.d[ty], Dd + o);
-        } else {
-            *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
-        }
-    }
+    const bool body = p >= 0 && p <= 7;
+    // own pair (or the z-halo plane's pair)
+    const int jz = p < 0 ? C.nb[4] : C.nb[5];
+    const bool zok = !(M.dbg & 4) && jz >= 0;
+    const bool ok = body ? ((C.lm >> (2 * p)) & 3u) != 0 : zok;
+    const int64_t off = body ? (int64_t)C.c * 512 + p * 64 + bp
+                             : (int64_t)(jz < 0 ? 0 : jz) * 512 + (p < 0 ? 448 : 0) + bp;
+    cp16_if(&T.u[t0], M.A.u + off, ok);
+    cp16_if(&T.d[t0], M.deff + off, ok);
+    if (!ok) *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
+    if (!body) return;  // warp-uniform
+    // x halo (lanes xp == 0 / 3): neighbour's x=7 / x=0 side plane
+    const bool xl = xp == 0 || xp == 3;
+    const int side = xp == 0 ? 0 : 1;
+    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
+    const int64_t ox = ((int64_t)(jx < 0 ? 0 : jx) * 2 + (1 - side)) * 64 + p * 8 + y;
+    cp8_if(&T.hxu[side][y], M.xfu + ox, xl && jx >= 0);
+    cp8_if(&T.hxd[side][y], M.xfd + ox, xl && jx >= 0);
+    if (xl && jx < 0) T.hxd[side][y] = sv;
+    // y halo (lanes y == 0 / 7): neighbour's row y=7 / y=0
+    const bool yl = y == 0 || y == 7;
+    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
+    const int ty = y == 0 ? t0 - 8 : t0 + 8;
+    const int64_t oy = (int64_t)(jy < 0 ? 0 : jy) * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
+    cp16_if(&T.u[ty], M.A.u + oy, yl && jy >= 0);
+    cp16_if(&T.d[ty], M.deff + oy, yl && jy >= 0);
+    if (yl && jy < 0) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
+}
+
+// |x| >= 2^990 or non-finite, from the high word (integer pipe)
+__device__ __forceinline__ bool huge(double x) {
+    return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
 }
 
 template <int REACTION>
@@ -231,12 +227,15 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
     const int t0 = tix(x0, y);
     const double2 uc = *reinterpret_cast<const double2*>(&T0.u[t0]);
     const double2 dc = *reinterpret_cast<const double2*>(&T0.d[t0]);
-    const double uL = T0.u[t0 - 1], dL = T0.d[t0 - 1];
-    const double uR = T0.u[t0 + 2], dR = T0.d[t0 + 2];
-    const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 10]);
-    const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 10]);
-    const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 10]);
-    const double2 dyp = *reinterpret_cast<const double2*>(&T0.d[t0 + 10]);
+    const double* pl = xp == 0 ? &T0.hxu[0][y] : &T0.u[t0 - 1];
+    const double* pr = xp == 3 ? &T0.hxu[1][y] : &T0.u[t0 + 2];
+    constexpr int kD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
+    const double uL = pl[0], dL = pl[kD];
+    const double uR = pr[0], dR = pr[kD];
+    const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 8]);
+    const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 8]);
+    const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 8]);
+    const double2 dyp = *reinterpret_cast<const double2*>(&T0.d[t0 + 8]);
     const double2 uzm = *reinterpret_cast<const double2*>(&Tm.u[t0]);
     const double2 dzm = *reinterpret_cast<const double2*>(&Tm.d[t0]);
     const double2 uzp = *reinterpret_cast<const double2*>(&Tp.u[t0]);
@@ -252,21 +251,44 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
         src1 = A.src[(int64_t)c * 512 + o + 1];
     }
     const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
-    double out0 = 0.0, out1 = 0.0;
-    bool slow0 = (C.flags & kFlagDirichlet) != 0, slow1 = slow0;
-    if ((C.flags >> (8 + z)) & 1) {
-        // interior-fluid plane (warp-uniform): no substitution anywhere
-        const double fxl = fface(dL, dc.x, uL, uc.x);
-        const double fxi = fface(dc.x, dc.y, uc.x, uc.y);
-        const double fxr = fface(dc.y, dR, uc.y, uR);
+    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
+    double out0, out1;
+    if (!dirichlet) {
+        double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
+        if ((C.flags >> (8 + z)) & 1) {
+            // interior-fluid plane (warp-uniform): no substitution anywhere
+            fxl = fface(dL, dc.x, uL, uc.x);
+            fxi = fface(dc.x, dc.y, uc.x, uc.y);
+            fxr = fface(dc.y, dR, uc.y, uR);
+            fy0m = fface(dym.x, dc.x, uym.x, uc.x);
+            fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
+            fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
+            fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
+            fy1m = fface(dym.y, dc.y, uym.y, uc.y);
+            fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
+            fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
+            fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
+        } else {
+            fxl = face(dL, dc.x, uL, uc.x);
+            fxi = face(dc.x, dc.y, uc.x, uc.y);
+            fxr = face(dc.y, dR, uc.y, uR);
+            fy0m = face(dym.x, dc.x, uym.x, uc.x);
+            fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
+            fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
+            fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
+            fy1m = face(dym.y, dc.y, uym.y, uc.y);
+            fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
+            fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
+            fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
+        }
         double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
         lap0 += (fxi - fxl) * ix;
-        lap0 += (fface(dc.x, dyp.x, uc.x, uyp.x) - fface(dym.x, dc.x, uym.x, uc.x)) * iy;
-        lap0 += (fface(dc.x, dzp.x, uc.x, uzp.x) - fface(dzm.x, dc.x, uzm.x, uc.x)) * iz;
+        lap0 += (fy0p - fy0m) * iy;
+        lap0 += (fz0p - fz0m) * iz;
         double lap1 = 0.0;
         lap1 += (fxr - fxi) * ix;
-        lap1 += (fface(dc.y, dyp.y, uc.y, uyp.y) - fface(dym.y, dc.y, uym.y, uc.y)) * iy;
-        lap1 += (fface(dc.y, dzp.y, uc.y, uzp.y) - fface(dzm.y, dc.y, uzm.y, uc.y)) * iz;
+        lap1 += (fy1p - fy1m) * iy;
+        lap1 += (fz1p - fz1m) * iz;
         double r0 = 0.0, r1 = 0.0;
         if (REACTION == PD_REACTION_SURFACE_SINK) {
             if (s0) r0 = K.neg_k * uc.x;
@@ -277,69 +299,55 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
         }
         out0 = uc.x + K.dt * lap0 + K.dt * r0;
         out1 = uc.y + K.dt * lap1 + K.dt * r1;
-        slow0 = !isfinite(out0);
-        slow1 = !isfinite(out1);
-    } else if (!slow0) {
-        const double fxl = face(dL, dc.x, uL, uc.x);
-        const double fxi = face(dc.x, dc.y, uc.x, uc.y);
-        const double fxr = face(dc.y, dR, uc.y, uR);
-        double lap0 = 0.0;
-        lap0 += (fxi - fxl) * ix;
-        lap0 += (face(dc.x, dyp.x, uc.x, uyp.x) - face(dym.x, dc.x, uym.x, uc.x)) * iy;
-        lap0 += (face(dc.x, dzp.x, uc.x, uzp.x) - face(dzm.x, dc.x, uzm.x, uc.x)) * iz;
-        double lap1 = 0.0;
-        lap1 += (fxr - fxi) * ix;
-        lap1 += (face(dc.y, dyp.y, uc.y, uyp.y) - face(dym.y, dc.y, uym.y, uc.y)) * iy;
-        lap1 += (face(dc.y, dzp.y, uc.y, uzp.y) - face(dzm.y, dc.y, uzm.y, uc.y)) * iz;
-        double r0 = 0.0, r1 = 0.0;
-        if (REACTION == PD_REACTION_SURFACE_SINK) {
-            if (s0) r0 = K.neg_k * uc.x;
-            if (s1) r1 = K.neg_k * uc.y;
-        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-            r0 = src0 * K.src_factor;
-            r1 = src1 * K.src_factor;
-        }
-        out0 = uc.x + K.dt * lap0 + K.dt * r0;
-        out1 = uc.y + K.dt * lap1 + K.dt * r1;
-        // walls (active, not fluid) stay frozen (solver.hpp:413-417)
-        if (sentinel(dc.x)) out0 = uc.x;
-        if (sentinel(dc.y)) out1 = uc.y;
-        slow0 = !isfinite(out0) && !sentinel(dc.x);
-        slow1 = !isfinite(out1) && !sentinel(dc.y);
-    }
-    if (slow0 | slow1) {
+    } else {
         const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
         const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-        if (slow0) {
+        const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+        const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+        out0 = slow_node<REACTION>(K, uc.x, dc.x, nu0, nd0, gx, gy, gz, s0, src0);
+        const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+        const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+        out1 = slow_node<REACTION>(K, uc.y, dc.y, nu1, nd1, gx + 1, gy, gz, s1, src1);
+    }
+    // walls (active, not fluid) stay frozen (solver.hpp:413-417)
+    if (sentinel(dc.x)) out0 = uc.x;
+    if (sentinel(dc.y)) out1 = uc.y;
+    const bool h0 = a0 && huge(out0), h1 = a1 && huge(out1);
+    if (h0 | h1) {
+        // rare: a non-finite fast-path result is re-derived exactly (the
+        // +-0 substitution shortcut needs finite operands), then the
+        // reference's non-finite / total-mass checks are flagged
+        // (solver.hpp:444, 250-260, 514-515)
+        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
+        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
+        if (h0 && !isfinite(out0) && !sentinel(dc.x) && !dirichlet) {
             const double nu[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
             const double nd[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-            out0 = sentinel(dc.x) ? uc.x : slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
+            out0 = slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
         }
-        if (slow1) {
+        if (h1 && !isfinite(out1) && !sentinel(dc.y) && !dirichlet) {
             const double nu[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
             const double nd[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-            out1 = sentinel(dc.y) ? uc.y
-                                  : slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
+            out1 = slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
+        }
+        const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
+        if (bad0 | bad1) {
+            atomicMin(A.bad_key, ((unsigned long long)c << 10) | (unsigned long long)(o + (bad0 ? 0 : 1)));
+            atomicOr(&A.flags[A.k], 1);
+        } else {
+            atomicOr(&A.flags[A.k], 2);
         }
     }
     double* dst = A.un + (int64_t)c * 512 + o;
-    if (a0 && a1)
+    if (a0 && a1) {
         *reinterpret_cast<double2*>(dst) = make_double2(out0, out1);
-    else if (a0)
-        dst[0] = out0;
-    else
-        dst[1] = out1;
+    } else {
+        if (a0) dst[0] = out0;
+        if (a1) dst[1] = out1;
+    }
     // x-face side planes of u_next for the next step's x halos
     if (xp == 0 && a0) M.xfun[((int64_t)c * 2 + 0) * 64 + z * 8 + y] = out0;
     if (xp == 3 && a1) M.xfun[((int64_t)c * 2 + 1) * 64 + z * 8 + y] = out1;
-    // non-finite / huge detection (solver.hpp:444, 250-260, 514-515)
-    const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
-    if (bad0 | bad1) {
-        atomicMin(A.bad_key, ((unsigned long long)c << 10) | (unsigned long long)(o + (bad0 ? 0 : 1)));
-        atomicOr(&A.flags[A.k], 1);
-    } else if ((a0 && !(fabs(out0) < 0x1p990)) || (a1 && !(fabs(out1) < 0x1p990))) {
-        atomicOr(&A.flags[A.k], 2);
-    }
 }
 
 __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
@@ -396,21 +404,22 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
 
     // ---- chunk stream: kBatch-chunk claims from one counter ----
     int* ctr = M.counter;
-    auto claim = [&]() -> int64_t {
+    auto claim = [&]() -> int {
         int v = 0;
         if (lane == 0) v = atomicAdd(ctr, kBatch);
-        return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+        return __shfl_sync(0xffffffffu, v, 0);
     };
-    int64_t b_cur = claim(), b_nxt = claim();
+    int b_cur = claim(), b_nxt = claim();
     int bi = 0;  // position of the next chunk to fetch inside b_cur
+    const int n = (int)M.n;
     auto next_id = [&]() -> int {
         if (bi == kBatch) {
             b_cur = b_nxt;
             b_nxt = claim();
             bi = 0;
         }
-        const int64_t p = b_cur + bi++;
-        return p < M.n ? __ldg(&M.sched[p]) : -1;
+        const int p = b_cur + bi++;
+        return p < n ? __ldg(&M.sched[p]) : -1;
     };
 
     // loading side: chunk whose planes are being issued, and the next one
@@ -422,10 +431,10 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
     int c_nx = next_id();
     load_ctx(M, c_nx, lane, lm1, dv1);
-    int p_ld = -1;    // next plane of Cld to issue (-1..8)
-    int64_t L = 0;    // loads issued
+    int p_ld = -1;  // next plane of Cld to issue (-1..8)
+    int L = 0;      // loads issued
     auto issue_next = [&]() {
-        if (Cld.c >= 0) issue_plane(ring[L % kRing], M, Cld, p_ld, y, xp, x0);
+        if (Cld.c >= 0) issue_plane(ring[L & (kRing - 1)], M, Cld, p_ld, y, xp, x0);
         cp_commit();
         ++L;
         if (++p_ld == 9) {  // advance the load side to the next chunk
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     // compute side: follows the load side, which is never more than one
     // chunk ahead (kAhead + 3 < 10 loads)
     ChunkCtx Cc = Cld;
-    int64_t base = 0;  // load index of plane -1 of Cc
+    int base = 0;  // load index of plane -1 of Cc
     // prologue: planes -1, 0, 1 needed for z = 0, plus kAhead more
     for (int k = 0; k < 3 + kAhead; ++k) issue_next();
     while (Cc.c >= 0) {
@@ -448,11 +457,15 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
             // are in flight at this point of every iteration
             cp_wait<kAhead>();
             __syncwarp();
-            compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) % kRing], ring[(base + z + 1) % kRing],
-                                    ring[(base + z + 2) % kRing], lane);
+            compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
+                                    ring[(base + z + 1) & (kRing - 1)],
+                                    ring[(base + z + 2) & (kRing - 1)], lane);
             __syncwarp();
-            const int64_t need_next = z < 7 ? base + z + 3 : base + 12;
-            while (L <= need_next + kAhead) issue_next();
+            issue_next();
+            if (z == 7) {  // planes 8 of this chunk and -1 of the next
+                issue_next();
+                issue_next();
+            }
         }
         base += 10;
         Cc = Cld;
