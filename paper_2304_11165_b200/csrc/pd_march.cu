@@ -666,14 +666,16 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const bool occ5 = p.grid == sms * 5;
     const size_t bytes = sizeof(Tile) * kRing * kWarps;
-    auto go = [&](auto kern) {
-        static bool set = false;  // one flag per kernel instantiation
-        if (!set) {
-            PD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-            set = true;
-        }
-        kern<<<p.grid, kThreads, bytes, g->stream>>>(M);
-    };
+    static bool attr_set = false;
+    if (!attr_set) {
+        void (*kerns[])(MarchArgs) = {ftcs_march_kernel<0, 5>, ftcs_march_kernel<1, 5>, ftcs_march_kernel<2, 5>,
+                                      ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
+                                      ftcs_march_kernel<2, kCtasPerSm>};
+        for (auto k : kerns)
+            PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        attr_set = true;
+    }
+    auto go = [&](void (*kern)(MarchArgs)) { kern<<<p.grid, kThreads, bytes, g->stream>>>(M); };
     if (reaction == PD_REACTION_SURFACE_SINK) {
         if (occ5) go(ftcs_march_kernel<1, 5>);
         else go(ftcs_march_kernel<1, kCtasPerSm>);
