@@ -44,15 +44,16 @@ BYTES_PER_UPDATE = 24  # FP64: u_n read + D read + u_{n+1} write (SURVEY.md §8d
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=2048, help="box edge in nodes")
     ap.add_argument("--psi", type=float, default=0.2, help="target porosity")
     ap.add_argument("--radius-vox", type=float, default=128.0)
     ap.add_argument("--seed", type=int, default=12345)
-    ap.add_argument("--cpu-sample", type=int, default=128, help="edge of the CPU sample crop")
+    ap.add_argument("--cpu-sample", type=int, default=192, help="edge of the CPU sample crop")
     ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     ap.add_argument("--e2e-n", type=int, default=512, help="box edge of the end-to-end host-buffer run")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
@@ -143,9 +144,14 @@ def ncu_traffic():
 # ---------------------------------------------------------------------------
 
 
-def cpu_sample(args, pack, edge, steps, threads=None):
+_REF_GRID_CACHE = {}
+
+
+def cpu_sample(args, pack, edge, steps, threads=None, target_s=None):
     """Times the reference's own run_simulation on a crop [0,edge)^3 of the
-    same pore geometry (same spheres and spacing); geometry build untimed."""
+    same pore geometry (same spheres and spacing); geometry build untimed.
+    With target_s, a short calibration run sizes the step count so the timed
+    run takes about target_s seconds of CPU wall time."""
     import ctypes as C
 
     from oracle.pyoracle import Ref, make_config
@@ -167,6 +173,12 @@ def cpu_sample(args, pack, edge, steps, threads=None):
     g.fill_hash("u", 1)
     dmax = g.max_diffusivity()
     dt = 0.4 * pd.stability_dt(geom, dmax)
+    if target_s:
+        cal = make_config(dt, 5, reaction="surface_sink", rate=1.0, band_half_width=1.0, record_every=5)
+        t0 = time.perf_counter()
+        g.run(cal)
+        per_step = (time.perf_counter() - t0) / 5
+        steps = max(5, int(target_s / max(per_step, 1e-6)))
     cfg = make_config(dt, steps, reaction="surface_sink", rate=1.0, band_half_width=1.0, record_every=steps)
     t0 = time.perf_counter()
     code, msg, rows = g.run(cfg)
@@ -176,7 +188,7 @@ def cpu_sample(args, pack, edge, steps, threads=None):
     cores = R.L.ref_worker_count()
     if threads:
         R.L.ref_set_worker_count(0)
-    return active * steps / secs, active, secs, cores
+    return active * steps / secs, active, secs, cores, steps
 
 
 # ---------------------------------------------------------------------------
@@ -231,8 +243,9 @@ def run_ours(args):
     step_ms = ms_max / args.steps
     value = active * args.steps / (ms_max / 1e3)
     peak, peak_src = measured_peak()
-    # dominant kernel: the step kernel alone (CUDA events on its stream)
-    kern_ms = dom.kernel_ms(stepper)
+    # dominant kernel: the step kernel alone (CUDA events on its stream),
+    # timed region only
+    kern_ms = dom.last_kernel_ms / args.steps
     achieved = dom.owned_active * BYTES_PER_UPDATE / (kern_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic()
 
@@ -242,11 +255,12 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu and rank == 0:
         try:
-            v, a, secs, cores = cpu_sample(args, pack, args.cpu_sample, args.cpu_steps)
+            v, a, secs, cores, st = cpu_sample(args, pack, args.cpu_sample, args.cpu_steps,
+                                               target_s=args.cpu_seconds)
             cpu = {"value": v / 1e9, "unit": "GPts/s", "cores": cores, "kind": "reference",
-                   "sample": f"reference run_simulation (oracle/_ref, -O3 -ffp-contract=off) on the "
-                             f"[0,{args.cpu_sample})^3 crop of the same geometry: {a} active nodes x "
-                             f"{args.cpu_steps} steps in {secs:.2f} s"}
+                   "sample": f"reference run_simulation (oracle/_ref, -O3 -ffp-contract=off, "
+                             f"{cores} std::thread workers) on the [0,{args.cpu_sample})^3 crop of the same "
+                             f"geometry: {a} active nodes x {st} steps in {secs:.2f} s"}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "GPts/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
     if rank == 0:
@@ -333,12 +347,14 @@ def run_reference(args):
     pack = workload(args)
     edge = args.cpu_sample
     vals = []
-    for _ in range(args.warmup):
-        cpu_sample(args, pack, edge, max(1, args.cpu_steps // 4))
-    total_pts, total_s, cores, active = 0.0, 0.0, None, 0
+    for _ in range(min(args.warmup, 1)):
+        cpu_sample(args, pack, edge, 3)
+    # each timed step is a bounded sample: ~cpu_seconds / steps of CPU work
+    per = max(1.0, args.cpu_seconds / max(1, args.steps))
+    total_pts, total_s, cores, active, st = 0.0, 0.0, None, 0, 0
     for _ in range(args.steps):
-        v, active, secs, cores = cpu_sample(args, pack, edge, args.cpu_steps)
-        total_pts += active * args.cpu_steps
+        v, active, secs, cores, st = cpu_sample(args, pack, edge, args.cpu_steps, target_s=per)
+        total_pts += active * st
         total_s += secs
         vals.append(v)
     value = total_pts / total_s / 1e9
@@ -348,8 +364,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(args, world),
         "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": cores, "kind": "reference",
-                         "sample": f"each step = reference run_simulation of {args.cpu_steps} FTCS steps on the "
-                                   f"[0,{edge})^3 crop ({active} active nodes) of the same geometry"},
+                         "sample": f"each step = reference run_simulation (oracle/_ref, {cores} std::thread "
+                                   f"workers) of ~{st} FTCS steps on the [0,{edge})^3 crop ({active} active "
+                                   f"nodes) of the same geometry"},
         "e2e": {"value": value, "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

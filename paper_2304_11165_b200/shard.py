@@ -237,6 +237,7 @@ class Domain:
                 self.exchange()
         e1.record(self.stream)
         e1.synchronize()
+        self.last_kernel_ms = kms
         self._kernel_ms += kms
         self._steps += n
         return e0.elapsed_time(e1)
