@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     ap.add_argument("--e2e-n", type=int, default=512, help="box edge of the end-to-end host-buffer run")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -129,11 +129,12 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(n):
     """dram bytes per launch of the step kernel from the committed ncu
-    capture summary (profiles/*_traffic.json), or None."""
+    capture summary (profiles/ftcs_step_traffic.json; captured at 2048^3),
+    or None for other box sizes."""
     f = ROOT / "profiles" / "ftcs_step_traffic.json"
-    if f.exists():
+    if f.exists() and n == 2048:
         d = json.loads(f.read_text())
         return d.get("dram_bytes_per_launch"), d
     return None, None
@@ -247,7 +248,7 @@ def run_ours(args):
     # timed region only
     kern_ms = dom.last_kernel_ms / args.steps
     achieved = dom.owned_active * BYTES_PER_UPDATE / (kern_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(args.n)
 
     e2e = None
     if not args.no_e2e and rank == 0:
@@ -271,7 +272,8 @@ def run_ours(args):
             "config": config_dict(args, world),
             "active_nodes": int(active), "chunks": int(dom.total_chunks(world)),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
+                         "algorithmic_bytes_per_launch": dom.owned_active * BYTES_PER_UPDATE,
                          "peak_source": peak_src, "bytes_per_update": BYTES_PER_UPDATE,
                          "kernel_ms_per_step": kern_ms, "traffic_source": traffic_src and "profiles/ftcs_step_traffic.json"},
             "roofline_frac_of_step": dom.owned_active * BYTES_PER_UPDATE / (step_ms / 1e3) / 1e9 / peak,

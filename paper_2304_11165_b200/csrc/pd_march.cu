@@ -50,8 +50,8 @@ namespace pdb {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=5 selects 5)
-constexpr int kBatch = 8;
+constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=3 selects 3)
+constexpr int kBatch = 1;  // one chunk per claim: neighbours in the schedule run close in time
 constexpr int kParts = 1;
 constexpr int kSeg = 16;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
@@ -635,7 +635,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
     static const int occ = [] {
         const char* e = getenv("PD_MARCH_OCC");
-        return (e && atoi(e) == 5) ? 5 : kCtasPerSm;
+        return (e && atoi(e) == 3) ? 3 : kCtasPerSm;
     }();
     plan->grid = sms * occ;
     plan->n = n;
@@ -664,11 +664,11 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     M.dbg = dbg;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-    const bool occ5 = p.grid == sms * 5;
+    const bool occ3 = p.grid == sms * 3;
     const size_t bytes = sizeof(Tile) * kRing * kWarps;
     static bool attr_set = false;
     if (!attr_set) {
-        void (*kerns[])(MarchArgs) = {ftcs_march_kernel<0, 5>, ftcs_march_kernel<1, 5>, ftcs_march_kernel<2, 5>,
+        void (*kerns[])(MarchArgs) = {ftcs_march_kernel<0, 3>, ftcs_march_kernel<1, 3>, ftcs_march_kernel<2, 3>,
                                       ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
                                       ftcs_march_kernel<2, kCtasPerSm>};
         for (auto k : kerns)
@@ -677,13 +677,13 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     }
     auto go = [&](void (*kern)(MarchArgs)) { kern<<<p.grid, kThreads, bytes, g->stream>>>(M); };
     if (reaction == PD_REACTION_SURFACE_SINK) {
-        if (occ5) go(ftcs_march_kernel<1, 5>);
+        if (occ3) go(ftcs_march_kernel<1, 3>);
         else go(ftcs_march_kernel<1, kCtasPerSm>);
     } else if (reaction == PD_REACTION_VOLUMETRIC) {
-        if (occ5) go(ftcs_march_kernel<2, 5>);
+        if (occ3) go(ftcs_march_kernel<2, 3>);
         else go(ftcs_march_kernel<2, kCtasPerSm>);
     } else {
-        if (occ5) go(ftcs_march_kernel<0, 5>);
+        if (occ3) go(ftcs_march_kernel<0, 3>);
         else go(ftcs_march_kernel<0, kCtasPerSm>);
     }
     PD_CUDA(cudaGetLastError());
