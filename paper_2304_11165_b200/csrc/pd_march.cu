@@ -147,11 +147,12 @@ struct ChunkCtx {
 // the lanes' 16-B pair accesses are bank-conflict free) and the x- / x+ halo
 // cells of rows 0..7 in two side columns.
 constexpr int kRing = 8;   // power of two: slot = load index & 7
-constexpr int kAhead = 5;  // kRing - 3 (planes z-1, z, z+1 resident)
+constexpr int kAhead = 4;  // loads in flight beyond the 4 planes a step reads
 struct Tile {
     double u[80], hxu[2][8];
     double d[80], hxd[2][8];
 };
+constexpr int kTileD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
 __device__ __forceinline__ int tix(int x, int y) { return x + 8 * (y + 1); }
 
 __device__ __forceinline__ void cp16_if(void* smem, const void* gmem, bool pred) {
@@ -174,42 +175,63 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Issues the lane's share of plane p (-1..8) of chunk C into tile T:
-// predicated 16-B copies of its node pair (pairs with no active node are
-// never read; their D_eff cells get the sentinel) and, for chunk-face lanes,
-// the x / y halo cells. p = -1 / 8 are the z halo planes of the z neighbours.
-__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const ChunkCtx& C, int p,
+// Lane-specific source offsets of one chunk, computed once per chunk.
+struct LoadCtx {
+    int c;
+    uint32_t lm;
+    int64_t own;    // element offset of the lane's pair in plane 0
+    int64_t zlo;    // pair in the z- neighbour's plane 7, or -1
+    int64_t zhi;    // pair in the z+ neighbour's plane 0, or -1
+    int64_t xoff;   // x-halo cell of plane 0 in the side planes, or -1 (non-face lane / absent)
+    int64_t yoff;   // y-halo pair of plane 0, or -1
+};
+
+__device__ __forceinline__ LoadCtx make_load_ctx(const ChunkCtx& C, const MarchArgs& M, int y, int xp,
+                                                 int x0) {
+    LoadCtx L;
+    L.c = C.c;
+    L.lm = C.lm;
+    const int bp = y * 8 + x0;
+    L.own = (int64_t)(C.c < 0 ? 0 : C.c) * 512 + bp;
+    const bool zk = !(M.dbg & 4);
+    L.zlo = (zk && C.nb[4] >= 0) ? (int64_t)C.nb[4] * 512 + 448 + bp : -1;
+    L.zhi = (zk && C.nb[5] >= 0) ? (int64_t)C.nb[5] * 512 + bp : -1;
+    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
+    L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? ((int64_t)jx * 2 + (xp == 0 ? 1 : 0)) * 64 + y : -1;
+    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
+    L.yoff = ((y == 0 || y == 7) && jy >= 0) ? (int64_t)jy * 512 + (y == 0 ? 56 : 0) + x0 : -1;
+    return L;
+}
+
+// Issues the lane's share of plane p (-1..8) into tile T: predicated 16-B
+// copies of its node pair (pairs with no active node are never read; their
+// D_eff cells get the sentinel) and, for chunk-face lanes, the x / y halo
+// cells. p = -1 / 8 are the z halo planes of the z neighbours.
+__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const LoadCtx& L, int p,
                                             int y, int xp, int x0) {
     const int t0 = tix(x0, y);
     const double sv = sent();
-    const int bp = y * 8 + x0;
-    const bool body = p >= 0 && p <= 7;
-    // own pair (or the z-halo plane's pair)
-    const int jz = p < 0 ? C.nb[4] : C.nb[5];
-    const bool zok = !(M.dbg & 4) && jz >= 0;
-    const bool ok = body ? ((C.lm >> (2 * p)) & 3u) != 0 : zok;
-    const int64_t off = body ? (int64_t)C.c * 512 + p * 64 + bp
-                             : (int64_t)(jz < 0 ? 0 : jz) * 512 + (p < 0 ? 448 : 0) + bp;
-    cp16_if(&T.u[t0], M.A.u + off, ok);
-    cp16_if(&T.d[t0], M.deff + off, ok);
+    const bool body = (unsigned)p <= 7u;
+    const int64_t o = body ? L.own + p * 64 : (p < 0 ? L.zlo : L.zhi);
+    const bool ok = L.c >= 0 && (body ? ((L.lm >> (2 * p)) & 3u) != 0 : o >= 0);
+    const int64_t oo = ok ? o : 0;
+    cp16_if(&T.u[t0], M.A.u + oo, ok);
+    cp16_if(&T.d[t0], M.deff + oo, ok);
     if (!ok) *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
     if (!body) return;  // warp-uniform
-    // x halo (lanes xp == 0 / 3): neighbour's x=7 / x=0 side plane
-    const bool xl = xp == 0 || xp == 3;
+    const bool xl = xp == 0 || xp == 3, yl = y == 0 || y == 7;
     const int side = xp == 0 ? 0 : 1;
-    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
-    const int64_t ox = ((int64_t)(jx < 0 ? 0 : jx) * 2 + (1 - side)) * 64 + p * 8 + y;
-    cp8_if(&T.hxu[side][y], M.xfu + ox, xl && jx >= 0);
-    cp8_if(&T.hxd[side][y], M.xfd + ox, xl && jx >= 0);
-    if (xl && jx < 0) T.hxd[side][y] = sv;
-    // y halo (lanes y == 0 / 7): neighbour's row y=7 / y=0
-    const bool yl = y == 0 || y == 7;
-    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
+    const bool xok = L.xoff >= 0;
+    const int64_t ox = xok ? L.xoff + p * 8 : 0;
+    cp8_if(&T.hxu[side][y], M.xfu + ox, xok);
+    cp8_if(&T.hxd[side][y], M.xfd + ox, xok);
+    if (xl && !xok) T.hxd[side][y] = sv;
+    const bool yok = L.yoff >= 0;
     const int ty = y == 0 ? t0 - 8 : t0 + 8;
-    const int64_t oy = (int64_t)(jy < 0 ? 0 : jy) * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
-    cp16_if(&T.u[ty], M.A.u + oy, yl && jy >= 0);
-    cp16_if(&T.d[ty], M.deff + oy, yl && jy >= 0);
-    if (yl && jy < 0) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
+    const int64_t oy = yok ? L.yoff + p * 64 : 0;
+    cp16_if(&T.u[ty], M.A.u + oy, yok);
+    cp16_if(&T.d[ty], M.deff + oy, yok);
+    if (yl && !yok) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
 }
 
 // |x| >= 2^990 or non-finite, from the high word (integer pipe)
@@ -217,30 +239,82 @@ __device__ __forceinline__ bool huge(double x) {
     return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
 }
 
+// One node pair of one plane as loaded from the tiles.
+struct PairIn {
+    double2 uc, dc, uym, dym, uyp, dyp;
+    double uL, dL, uR, dR;
+};
+__device__ __forceinline__ PairIn load_pair(const Tile& T, int t0, int lofs, int rofs) {
+    PairIn P;
+    const double* U = T.u;
+    P.uc = *reinterpret_cast<const double2*>(&U[t0]);
+    P.dc = *reinterpret_cast<const double2*>(&U[t0 + kTileD]);
+    P.uym = *reinterpret_cast<const double2*>(&U[t0 - 8]);
+    P.dym = *reinterpret_cast<const double2*>(&U[t0 - 8 + kTileD]);
+    P.uyp = *reinterpret_cast<const double2*>(&U[t0 + 8]);
+    P.dyp = *reinterpret_cast<const double2*>(&U[t0 + 8 + kTileD]);
+    P.uL = U[lofs];
+    P.dL = U[lofs + kTileD];
+    P.uR = U[rofs];
+    P.dR = U[rofs + kTileD];
+    return P;
+}
+
+template <bool SEL>
+__device__ __forceinline__ double fx(double da, double db, double ua, double ub) {
+    return SEL ? face(da, db, ua, ub) : fface(da, db, ua, ub);
+}
+
+// Fast path of the two planes z, z+1 (node pairs P0 = plane z, P1 = plane
+// z+1, below = plane z-1, above = plane z+2). The z face between the planes is
+// computed once and shared.
+template <bool SEL>
+__device__ __forceinline__ void lap4(const PairIn& P0, const PairIn& P1, double2 ub, double2 db,
+                                     double2 ua, double2 da, const SlowConsts& K, double (&lap)[4]) {
+    const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
+    // plane z
+    {
+        const double fxl = fx<SEL>(P0.dL, P0.dc.x, P0.uL, P0.uc.x);
+        const double fxi = fx<SEL>(P0.dc.x, P0.dc.y, P0.uc.x, P0.uc.y);
+        const double fxr = fx<SEL>(P0.dc.y, P0.dR, P0.uc.y, P0.uR);
+        lap[0] = 0.0;  // lap starts at T{0} (solver.hpp:420)
+        lap[0] += (fxi - fxl) * ix;
+        lap[1] = 0.0;
+        lap[1] += (fxr - fxi) * ix;
+    }
+    {
+        const double fxl = fx<SEL>(P1.dL, P1.dc.x, P1.uL, P1.uc.x);
+        const double fxi = fx<SEL>(P1.dc.x, P1.dc.y, P1.uc.x, P1.uc.y);
+        const double fxr = fx<SEL>(P1.dc.y, P1.dR, P1.uc.y, P1.uR);
+        lap[2] = 0.0;
+        lap[2] += (fxi - fxl) * ix;
+        lap[3] = 0.0;
+        lap[3] += (fxr - fxi) * ix;
+    }
+    lap[0] += (fx<SEL>(P0.dc.x, P0.dyp.x, P0.uc.x, P0.uyp.x) - fx<SEL>(P0.dym.x, P0.dc.x, P0.uym.x, P0.uc.x)) * iy;
+    lap[1] += (fx<SEL>(P0.dc.y, P0.dyp.y, P0.uc.y, P0.uyp.y) - fx<SEL>(P0.dym.y, P0.dc.y, P0.uym.y, P0.uc.y)) * iy;
+    lap[2] += (fx<SEL>(P1.dc.x, P1.dyp.x, P1.uc.x, P1.uyp.x) - fx<SEL>(P1.dym.x, P1.dc.x, P1.uym.x, P1.uc.x)) * iy;
+    lap[3] += (fx<SEL>(P1.dc.y, P1.dyp.y, P1.uc.y, P1.uyp.y) - fx<SEL>(P1.dym.y, P1.dc.y, P1.uym.y, P1.uc.y)) * iy;
+    const double fzb0 = fx<SEL>(db.x, P0.dc.x, ub.x, P0.uc.x);
+    const double fzb1 = fx<SEL>(db.y, P0.dc.y, ub.y, P0.uc.y);
+    const double fzm0 = fx<SEL>(P0.dc.x, P1.dc.x, P0.uc.x, P1.uc.x);
+    const double fzm1 = fx<SEL>(P0.dc.y, P1.dc.y, P0.uc.y, P1.uc.y);
+    const double fza0 = fx<SEL>(P1.dc.x, da.x, P1.uc.x, ua.x);
+    const double fza1 = fx<SEL>(P1.dc.y, da.y, P1.uc.y, ua.y);
+    lap[0] += (fzm0 - fzb0) * iz;
+    lap[1] += (fzm1 - fzb1) * iz;
+    lap[2] += (fza0 - fzm0) * iz;
+    lap[3] += (fza1 - fzm1) * iz;
+}
+
 template <int REACTION>
-__device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
-                                              const ChunkCtx& C, int z, const Tile& Tm,
-                                              const Tile& T0, const Tile& Tp, int lane) {
-    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
+__device__ __forceinline__ void finish_plane(const MarchArgs& M, const SlowConsts& K, const ChunkCtx& C,
+                                             int z, const PairIn& P, double2 uzm, double2 dzm,
+                                             double2 uzp, double2 dzp, double lap0, double lap1,
+                                             bool dirichlet, int y, int xp, int x0) {
+    const StepArgs<double>& A = M.A;
     const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
     if (!(a0 | a1)) return;
-    const int t0 = tix(x0, y);
-    const double2 uc = *reinterpret_cast<const double2*>(&T0.u[t0]);
-    const double2 dc = *reinterpret_cast<const double2*>(&T0.d[t0]);
-    const double* pl = xp == 0 ? &T0.hxu[0][y] : &T0.u[t0 - 1];
-    const double* pr = xp == 3 ? &T0.hxu[1][y] : &T0.u[t0 + 2];
-    constexpr int kD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
-    const double uL = pl[0], dL = pl[kD];
-    const double uR = pr[0], dR = pr[kD];
-    const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 8]);
-    const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 8]);
-    const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 8]);
-    const double2 dyp = *reinterpret_cast<const double2*>(&T0.d[t0 + 8]);
-    const double2 uzm = *reinterpret_cast<const double2*>(&Tm.u[t0]);
-    const double2 dzm = *reinterpret_cast<const double2*>(&Tm.d[t0]);
-    const double2 uzp = *reinterpret_cast<const double2*>(&Tp.u[t0]);
-    const double2 dzp = *reinterpret_cast<const double2*>(&Tp.d[t0]);
-    const StepArgs<double>& A = M.A;
     const int o = z * 64 + y * 8 + x0;
     const int c = C.c;
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
@@ -250,85 +324,47 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
         src0 = A.src[(int64_t)c * 512 + o];
         src1 = A.src[(int64_t)c * 512 + o + 1];
     }
-    const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
-    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
     double out0, out1;
     if (!dirichlet) {
-        double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
-        if ((C.flags >> (8 + z)) & 1) {
-            // interior-fluid plane (warp-uniform): no substitution anywhere
-            fxl = fface(dL, dc.x, uL, uc.x);
-            fxi = fface(dc.x, dc.y, uc.x, uc.y);
-            fxr = fface(dc.y, dR, uc.y, uR);
-            fy0m = fface(dym.x, dc.x, uym.x, uc.x);
-            fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
-            fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
-            fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
-            fy1m = fface(dym.y, dc.y, uym.y, uc.y);
-            fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
-            fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
-            fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
-        } else {
-            fxl = face(dL, dc.x, uL, uc.x);
-            fxi = face(dc.x, dc.y, uc.x, uc.y);
-            fxr = face(dc.y, dR, uc.y, uR);
-            fy0m = face(dym.x, dc.x, uym.x, uc.x);
-            fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
-            fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
-            fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
-            fy1m = face(dym.y, dc.y, uym.y, uc.y);
-            fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
-            fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
-            fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
-        }
-        double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
-        lap0 += (fxi - fxl) * ix;
-        lap0 += (fy0p - fy0m) * iy;
-        lap0 += (fz0p - fz0m) * iz;
-        double lap1 = 0.0;
-        lap1 += (fxr - fxi) * ix;
-        lap1 += (fy1p - fy1m) * iy;
-        lap1 += (fz1p - fz1m) * iz;
         double r0 = 0.0, r1 = 0.0;
         if (REACTION == PD_REACTION_SURFACE_SINK) {
-            if (s0) r0 = K.neg_k * uc.x;
-            if (s1) r1 = K.neg_k * uc.y;
+            if (s0) r0 = K.neg_k * P.uc.x;
+            if (s1) r1 = K.neg_k * P.uc.y;
         } else if (REACTION == PD_REACTION_VOLUMETRIC) {
             r0 = src0 * K.src_factor;
             r1 = src1 * K.src_factor;
         }
-        out0 = uc.x + K.dt * lap0 + K.dt * r0;
-        out1 = uc.y + K.dt * lap1 + K.dt * r1;
-    } else {
-        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
-        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-        const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
-        const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-        out0 = slow_node<REACTION>(K, uc.x, dc.x, nu0, nd0, gx, gy, gz, s0, src0);
-        const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
-        const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-        out1 = slow_node<REACTION>(K, uc.y, dc.y, nu1, nd1, gx + 1, gy, gz, s1, src1);
+        out0 = P.uc.x + K.dt * lap0 + K.dt * r0;
+        out1 = P.uc.y + K.dt * lap1 + K.dt * r1;
+    }
+    const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
+    const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
+    if (dirichlet) {
+        const double nu0[6] = {P.uL, P.uc.y, P.uym.x, P.uyp.x, uzm.x, uzp.x};
+        const double nd0[6] = {P.dL, P.dc.y, P.dym.x, P.dyp.x, dzm.x, dzp.x};
+        out0 = slow_node<REACTION>(K, P.uc.x, P.dc.x, nu0, nd0, gx, gy, gz, s0, src0);
+        const double nu1[6] = {P.uc.x, P.uR, P.uym.y, P.uyp.y, uzm.y, uzp.y};
+        const double nd1[6] = {P.dc.x, P.dR, P.dym.y, P.dyp.y, dzm.y, dzp.y};
+        out1 = slow_node<REACTION>(K, P.uc.y, P.dc.y, nu1, nd1, gx + 1, gy, gz, s1, src1);
     }
     // walls (active, not fluid) stay frozen (solver.hpp:413-417)
-    if (sentinel(dc.x)) out0 = uc.x;
-    if (sentinel(dc.y)) out1 = uc.y;
+    if (sentinel(P.dc.x)) out0 = P.uc.x;
+    if (sentinel(P.dc.y)) out1 = P.uc.y;
     const bool h0 = a0 && huge(out0), h1 = a1 && huge(out1);
     if (h0 | h1) {
         // rare: a non-finite fast-path result is re-derived exactly (the
         // +-0 substitution shortcut needs finite operands), then the
         // reference's non-finite / total-mass checks are flagged
         // (solver.hpp:444, 250-260, 514-515)
-        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
-        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-        if (h0 && !isfinite(out0) && !sentinel(dc.x) && !dirichlet) {
-            const double nu[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
-            const double nd[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-            out0 = slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
+        if (h0 && !isfinite(out0) && !sentinel(P.dc.x) && !dirichlet) {
+            const double nu[6] = {P.uL, P.uc.y, P.uym.x, P.uyp.x, uzm.x, uzp.x};
+            const double nd[6] = {P.dL, P.dc.y, P.dym.x, P.dyp.x, dzm.x, dzp.x};
+            out0 = slow_node<REACTION>(K, P.uc.x, P.dc.x, nu, nd, gx, gy, gz, s0, src0);
         }
-        if (h1 && !isfinite(out1) && !sentinel(dc.y) && !dirichlet) {
-            const double nu[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
-            const double nd[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-            out1 = slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
+        if (h1 && !isfinite(out1) && !sentinel(P.dc.y) && !dirichlet) {
+            const double nu[6] = {P.uc.x, P.uR, P.uym.y, P.uyp.y, uzm.y, uzp.y};
+            const double nd[6] = {P.dc.x, P.dR, P.dym.y, P.dyp.y, dzm.y, dzp.y};
+            out1 = slow_node<REACTION>(K, P.uc.y, P.dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
         }
         const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
         if (bad0 | bad1) {
@@ -348,6 +384,31 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
     // x-face side planes of u_next for the next step's x halos
     if (xp == 0 && a0) M.xfun[((int64_t)c * 2 + 0) * 64 + z * 8 + y] = out0;
     if (xp == 3 && a1) M.xfun[((int64_t)c * 2 + 1) * 64 + z * 8 + y] = out1;
+}
+
+// Planes z and z+1 of chunk C from tiles Tb (z-1), T0 (z), T1 (z+1), Ta (z+2).
+template <int REACTION>
+__device__ __forceinline__ void compute_two(const MarchArgs& M, const SlowConsts& K, const ChunkCtx& C,
+                                            int z, const Tile& Tb, const Tile& T0, const Tile& T1,
+                                            const Tile& Ta, int y, int xp, int x0, int t0, int lofs,
+                                            int rofs) {
+    if (!((C.lm >> (2 * z)) & 15u)) return;  // no active node in this lane's 4 nodes
+    const PairIn P0 = load_pair(T0, t0, lofs, rofs);
+    const PairIn P1 = load_pair(T1, t0, lofs, rofs);
+    const double2 ub = *reinterpret_cast<const double2*>(&Tb.u[t0]);
+    const double2 db = *reinterpret_cast<const double2*>(&Tb.d[t0]);
+    const double2 ua = *reinterpret_cast<const double2*>(&Ta.u[t0]);
+    const double2 da = *reinterpret_cast<const double2*>(&Ta.d[t0]);
+    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
+    double lap[4];
+    if (!dirichlet) {
+        if (((C.flags >> (8 + z)) & 3) == 3)
+            lap4<false>(P0, P1, ub, db, ua, da, K, lap);  // interior-fluid planes
+        else
+            lap4<true>(P0, P1, ub, db, ua, da, K, lap);
+    }
+    finish_plane<REACTION>(M, K, C, z, P0, ub, db, P1.uc, P1.dc, lap[0], lap[1], dirichlet, y, xp, x0);
+    finish_plane<REACTION>(M, K, C, z + 1, P1, P0.uc, P0.dc, ua, da, lap[2], lap[3], dirichlet, y, xp, x0);
 }
 
 __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
@@ -371,8 +432,8 @@ __device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
 
 // One warp streams a sequence of chunks. Its plane loads (10 per chunk:
 // z-halo below, the 8 body planes, z-halo above) form one continuous
-// sequence through a kRing-slot tile ring, kAhead loads ahead of the plane
-// being computed, across chunk boundaries.
+// sequence through a kRing-slot tile ring, kAhead loads beyond the four planes
+// a step reads, across chunk boundaries. A step computes two planes.
 template <int REACTION, int OCC>
 __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -401,6 +462,10 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         K.dirichlet = A.dirichlet;
     }
     __syncthreads();
+    // lane-constant tile offsets (u array; D is +kTileD)
+    const int t0 = tix(x0, y);
+    const int lofs = xp == 0 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + y : t0 - 1;
+    const int rofs = xp == 3 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + 8 + y : t0 + 2;
 
     // ---- chunk stream: kBatch-chunk claims from one counter ----
     int* ctr = M.counter;
@@ -429,40 +494,43 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     int dv0, dv1;
     load_ctx(M, c_ld, lane, lm0, dv0);
     ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
+    LoadCtx Lld = make_load_ctx(Cld, M, y, xp, x0);
     int c_nx = next_id();
     load_ctx(M, c_nx, lane, lm1, dv1);
     int p_ld = -1;  // next plane of Cld to issue (-1..8)
     int L = 0;      // loads issued
     auto issue_next = [&]() {
-        if (Cld.c >= 0) issue_plane(ring[L & (kRing - 1)], M, Cld, p_ld, y, xp, x0);
+        issue_plane(ring[L & (kRing - 1)], M, Lld, p_ld, y, xp, x0);
         cp_commit();
         ++L;
         if (++p_ld == 9) {  // advance the load side to the next chunk
             p_ld = -1;
             Cld = make_ctx(c_nx, lm1, dv1);
+            Lld = make_load_ctx(Cld, M, y, xp, x0);
             c_nx = Cld.c >= 0 ? next_id() : -1;
             load_ctx(M, c_nx, lane, lm1, dv1);
         }
     };
     // compute side: follows the load side, which is never more than one
-    // chunk ahead (kAhead + 3 < 10 loads)
+    // chunk ahead (kAhead + 4 < 10 loads)
     ChunkCtx Cc = Cld;
     int base = 0;  // load index of plane -1 of Cc
-    // prologue: planes -1, 0, 1 needed for z = 0, plus kAhead more
-    for (int k = 0; k < 3 + kAhead; ++k) issue_next();
+    // prologue: planes -1..2 read by the first step, plus kAhead more
+    for (int k = 0; k < 4 + kAhead; ++k) issue_next();
     while (Cc.c >= 0) {
 #pragma unroll 1
-        for (int z = 0; z < 8; ++z) {
-            // loads up to index base+z+2 complete; exactly kAhead newer groups
-            // are in flight at this point of every iteration
+        for (int z = 0; z < 8; z += 2) {
+            // loads up to index base+z+3 complete; exactly kAhead newer groups
+            // are in flight at this point of every step
             cp_wait<kAhead>();
             __syncwarp();
-            compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
-                                    ring[(base + z + 1) & (kRing - 1)],
-                                    ring[(base + z + 2) & (kRing - 1)], lane);
+            compute_two<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
+                                  ring[(base + z + 1) & (kRing - 1)], ring[(base + z + 2) & (kRing - 1)],
+                                  ring[(base + z + 3) & (kRing - 1)], y, xp, x0, t0, lofs, rofs);
             __syncwarp();
             issue_next();
-            if (z == 7) {  // planes 8 of this chunk and -1 of the next
+            issue_next();
+            if (z == 6) {  // planes 8 of this chunk and -1 of the next
                 issue_next();
                 issue_next();
             }
