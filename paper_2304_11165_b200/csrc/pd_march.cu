@@ -142,96 +142,138 @@ struct ChunkCtx {
     uint32_t lm;
 };
 
-// Per-warp ring of plane tiles in shared memory. A tile holds u and D_eff of
-// one z-plane of a chunk: rows y = -1..8 of the 8 body columns (pitch 8, so
-// the lanes' 16-B pair accesses are bank-conflict free) and the x- / x+ halo
-// cells of rows 0..7 in two side columns.
+// Per-warp ring of plane tiles in shared memory, filled by TMA bulk copies.
+// A tile holds u and D_eff of one z-plane of a chunk: rows y = -1..8 of the 8
+// body columns (pitch 8: lanes' 16-B pair accesses are bank-conflict free;
+// rows 0..7 are one contiguous 512-B plane, rows -1 / 8 are 64-B rows of the y
+// neighbours) and the x- / x+ halo columns (64 B each, from the side planes).
 constexpr int kRing = 8;   // power of two: slot = load index & 7
-constexpr int kAhead = 4;  // loads in flight beyond the 4 planes a step reads
+constexpr int kAhead = 5;  // loads in flight beyond the 3 planes a step reads
 struct Tile {
     double u[80], hxu[2][8];
     double d[80], hxd[2][8];
 };
 constexpr int kTileD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
+constexpr int kHX = (int)(offsetof(Tile, hxu) / sizeof(double));
 __device__ __forceinline__ int tix(int x, int y) { return x + 8 * (y + 1); }
 
-__device__ __forceinline__ void cp16_if(void* smem, const void* gmem, bool pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
-        " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(
-            (unsigned)__cvta_generic_to_shared(smem)),
-        "l"(gmem), "r"((int)pred));
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void cp8_if(void* smem, const void* gmem, bool pred) {
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
     asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
-        " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(
-            (unsigned)__cvta_generic_to_shared(smem)),
-        "l"(gmem), "r"((int)pred));
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void mbar_init(unsigned bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 
-// Lane-specific source offsets of one chunk, computed once per chunk.
+// Lane roles of the per-plane bulk copies (lane < 10): 0/1 body u / D_eff
+// (512 B), 2/3 x- halo column, 4/5 x+ halo column (64 B, side planes), 6/7 y-
+// halo row, 8/9 y+ halo row (64 B). Computed once per chunk.
 struct LoadCtx {
+    const char* src;  // role source for plane 0 (nullptr: role absent)
+    unsigned dst;     // byte offset of the role's destination inside a tile
+    unsigned bytes;
+    unsigned stride;  // source bytes per plane
+    unsigned halo_tx; // bytes of the valid halo roles of a body plane (lane-uniform)
+    const char* zlo;  // roles 0/1: z- neighbour's plane 7 (halo plane -1)
+    const char* zhi;  // roles 0/1: z+ neighbour's plane 0 (halo plane 8)
+    uint32_t pact;    // bit p: body plane p has an active node (lane-uniform)
     int c;
-    uint32_t lm;
-    int64_t own;    // element offset of the lane's pair in plane 0
-    int64_t zlo;    // pair in the z- neighbour's plane 7, or -1
-    int64_t zhi;    // pair in the z+ neighbour's plane 0, or -1
-    int64_t xoff;   // x-halo cell of plane 0 in the side planes, or -1 (non-face lane / absent)
-    int64_t yoff;   // y-halo pair of plane 0, or -1
 };
 
-__device__ __forceinline__ LoadCtx make_load_ctx(const ChunkCtx& C, const MarchArgs& M, int y, int xp,
-                                                 int x0) {
+__device__ __forceinline__ LoadCtx make_load_ctx(const ChunkCtx& C, const MarchArgs& M, int lane) {
     LoadCtx L;
     L.c = C.c;
-    L.lm = C.lm;
-    const int bp = y * 8 + x0;
-    L.own = (int64_t)(C.c < 0 ? 0 : C.c) * 512 + bp;
-    const bool zk = !(M.dbg & 4);
-    L.zlo = (zk && C.nb[4] >= 0) ? (int64_t)C.nb[4] * 512 + 448 + bp : -1;
-    L.zhi = (zk && C.nb[5] >= 0) ? (int64_t)C.nb[5] * 512 + bp : -1;
-    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
-    L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? ((int64_t)jx * 2 + (xp == 0 ? 1 : 0)) * 64 + y : -1;
-    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
-    L.yoff = ((y == 0 || y == 7) && jy >= 0) ? (int64_t)jy * 512 + (y == 0 ? 56 : 0) + x0 : -1;
+    L.src = nullptr;
+    L.zlo = L.zhi = nullptr;
+    L.dst = 0;
+    L.bytes = 0;
+    L.stride = 512;
+    const bool isd = lane & 1;
+    const char* U = reinterpret_cast<const char*>(isd ? M.deff : M.A.u);
+    const char* XF = reinterpret_cast<const char*>(isd ? M.xfd : M.xfu);
+    const unsigned dbase = isd ? kTileD * 8 : 0;
+    const int role = lane >> 1;
+    if (C.c >= 0 && lane < 10) {
+        if (role == 0) {
+            L.src = U + (int64_t)C.c * 4096;
+            L.dst = dbase + 64;
+            L.bytes = 512;
+            if (!(M.dbg & 4)) {
+                if (C.nb[4] >= 0) L.zlo = U + (int64_t)C.nb[4] * 4096 + 448 * 8;
+                if (C.nb[5] >= 0) L.zhi = U + (int64_t)C.nb[5] * 4096;
+            }
+        } else if (role <= 2) {  // x- (role 1) / x+ (role 2): neighbour's x=7 / x=0 side plane
+            const int j = (M.dbg & 1) ? -1 : C.nb[role - 1];
+            if (j >= 0) L.src = XF + ((int64_t)j * 2 + (role == 1 ? 1 : 0)) * 512;
+            L.dst = dbase + (kHX + (role - 1) * 8) * 8;
+            L.bytes = 64;
+            L.stride = 64;
+        } else {  // y- (role 3) / y+ (role 4): neighbour's row y=7 / y=0
+            const int j = (M.dbg & 2) ? -1 : C.nb[role - 1];
+            if (j >= 0) L.src = U + (int64_t)j * 4096 + (role == 3 ? 56 * 8 : 0);
+            L.dst = dbase + (role == 3 ? 0 : 72 * 8);
+            L.bytes = 64;
+        }
+    }
+    const unsigned mine = (lane >= 2 && lane < 10 && L.src) ? L.bytes : 0u;
+    L.halo_tx = __reduce_add_sync(0xffffffffu, mine);
+    uint32_t pa = 0;
+    for (int z = 0; z < 8; ++z)
+        if (__any_sync(0xffffffffu, ((C.lm >> (2 * z)) & 3u) != 0)) pa |= 1u << z;
+    L.pact = pa;
     return L;
 }
 
-// Issues the lane's share of plane p (-1..8) into tile T: predicated 16-B
-// copies of its node pair (pairs with no active node are never read; their
-// D_eff cells get the sentinel) and, for chunk-face lanes, the x / y halo
-// cells. p = -1 / 8 are the z halo planes of the z neighbours.
-__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const LoadCtx& L, int p,
-                                            int y, int xp, int x0) {
-    const int t0 = tix(x0, y);
+// Issues plane p (-1..8) of the load-side chunk into tile slot T (mbarrier
+// bar): TMA bulk copies by the role lanes; D_eff sentinel fills where a body
+// plane has no active node or a neighbour is absent.
+__device__ __forceinline__ void issue_plane(Tile& T, unsigned bar, const LoadCtx& L, int p, int lane) {
     const double sv = sent();
     const bool body = (unsigned)p <= 7u;
-    const int64_t o = body ? L.own + p * 64 : (p < 0 ? L.zlo : L.zhi);
-    const bool ok = L.c >= 0 && (body ? ((L.lm >> (2 * p)) & 3u) != 0 : o >= 0);
-    const int64_t oo = ok ? o : 0;
-    cp16_if(&T.u[t0], M.A.u + oo, ok);
-    cp16_if(&T.d[t0], M.deff + oo, ok);
-    if (!ok) *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
-    if (!body) return;  // warp-uniform
-    const bool xl = xp == 0 || xp == 3, yl = y == 0 || y == 7;
-    const int side = xp == 0 ? 0 : 1;
-    const bool xok = L.xoff >= 0;
-    const int64_t ox = xok ? L.xoff + p * 8 : 0;
-    cp8_if(&T.hxu[side][y], M.xfu + ox, xok);
-    cp8_if(&T.hxd[side][y], M.xfd + ox, xok);
-    if (xl && !xok) T.hxd[side][y] = sv;
-    const bool yok = L.yoff >= 0;
-    const int ty = y == 0 ? t0 - 8 : t0 + 8;
-    const int64_t oy = yok ? L.yoff + p * 64 : 0;
-    cp16_if(&T.u[ty], M.A.u + oy, yok);
-    cp16_if(&T.d[ty], M.deff + oy, yok);
-    if (yl && !yok) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
+    const char* src0 = body ? ((L.pact >> p) & 1u ? L.src : nullptr) : (p < 0 ? L.zlo : L.zhi);
+    // bytes this plane will deliver (lane-uniform)
+    const unsigned lane01 = (L.c >= 0 && ((body && ((L.pact >> p) & 1u)) || (!body && src0 != nullptr))) ? 1024u : 0u;
+    const unsigned tx = __shfl_sync(0xffffffffu, lane01, 0) + (body && L.c >= 0 ? L.halo_tx : 0u);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    if (lane == 0) mbar_arrive_tx(bar, tx);
+    const unsigned tbase = smem_u32(&T);
+    if (lane < 2) {
+        if (L.c >= 0 && src0) bulk_g2s(tbase + L.dst, src0 + (body ? (int64_t)p * 512 : 0), 512u, bar);
+    } else if (lane < 10 && body) {
+        if (L.src) bulk_g2s(tbase + L.dst, L.src + (int64_t)p * L.stride, 64u, bar);
+    }
+    // sentinel D_eff where nothing is copied
+    const bool body_missing = !(L.c >= 0 && src0 != nullptr);
+    const bool body_missing0 = __shfl_sync(0xffffffffu, body_missing ? 1 : 0, 0);
+    if (body_missing0) *reinterpret_cast<double2*>(&T.d[8 + 2 * lane]) = make_double2(sv, sv);
+    if (body) {
+        // roles 3 (x-), 5 (x+), 7 (y-), 9 (y+) own the D halo destinations
+        if (lane < 10 && (lane & 1) && lane >= 3 && !L.src) {
+            double* dd = reinterpret_cast<double*>(reinterpret_cast<char*>(&T) + L.dst);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dd[k] = sv;
+        }
+    }
 }
 
 // |x| >= 2^990 or non-finite, from the high word (integer pipe)
@@ -239,82 +281,27 @@ __device__ __forceinline__ bool huge(double x) {
     return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
 }
 
-// One node pair of one plane as loaded from the tiles.
-struct PairIn {
-    double2 uc, dc, uym, dym, uyp, dyp;
-    double uL, dL, uR, dR;
-};
-__device__ __forceinline__ PairIn load_pair(const Tile& T, int t0, int lofs, int rofs) {
-    PairIn P;
-    const double* U = T.u;
-    P.uc = *reinterpret_cast<const double2*>(&U[t0]);
-    P.dc = *reinterpret_cast<const double2*>(&U[t0 + kTileD]);
-    P.uym = *reinterpret_cast<const double2*>(&U[t0 - 8]);
-    P.dym = *reinterpret_cast<const double2*>(&U[t0 - 8 + kTileD]);
-    P.uyp = *reinterpret_cast<const double2*>(&U[t0 + 8]);
-    P.dyp = *reinterpret_cast<const double2*>(&U[t0 + 8 + kTileD]);
-    P.uL = U[lofs];
-    P.dL = U[lofs + kTileD];
-    P.uR = U[rofs];
-    P.dR = U[rofs + kTileD];
-    return P;
-}
-
-template <bool SEL>
-__device__ __forceinline__ double fx(double da, double db, double ua, double ub) {
-    return SEL ? face(da, db, ua, ub) : fface(da, db, ua, ub);
-}
-
-// Fast path of the two planes z, z+1 (node pairs P0 = plane z, P1 = plane
-// z+1, below = plane z-1, above = plane z+2). The z face between the planes is
-// computed once and shared.
-template <bool SEL>
-__device__ __forceinline__ void lap4(const PairIn& P0, const PairIn& P1, double2 ub, double2 db,
-                                     double2 ua, double2 da, const SlowConsts& K, double (&lap)[4]) {
-    const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
-    // plane z
-    {
-        const double fxl = fx<SEL>(P0.dL, P0.dc.x, P0.uL, P0.uc.x);
-        const double fxi = fx<SEL>(P0.dc.x, P0.dc.y, P0.uc.x, P0.uc.y);
-        const double fxr = fx<SEL>(P0.dc.y, P0.dR, P0.uc.y, P0.uR);
-        lap[0] = 0.0;  // lap starts at T{0} (solver.hpp:420)
-        lap[0] += (fxi - fxl) * ix;
-        lap[1] = 0.0;
-        lap[1] += (fxr - fxi) * ix;
-    }
-    {
-        const double fxl = fx<SEL>(P1.dL, P1.dc.x, P1.uL, P1.uc.x);
-        const double fxi = fx<SEL>(P1.dc.x, P1.dc.y, P1.uc.x, P1.uc.y);
-        const double fxr = fx<SEL>(P1.dc.y, P1.dR, P1.uc.y, P1.uR);
-        lap[2] = 0.0;
-        lap[2] += (fxi - fxl) * ix;
-        lap[3] = 0.0;
-        lap[3] += (fxr - fxi) * ix;
-    }
-    lap[0] += (fx<SEL>(P0.dc.x, P0.dyp.x, P0.uc.x, P0.uyp.x) - fx<SEL>(P0.dym.x, P0.dc.x, P0.uym.x, P0.uc.x)) * iy;
-    lap[1] += (fx<SEL>(P0.dc.y, P0.dyp.y, P0.uc.y, P0.uyp.y) - fx<SEL>(P0.dym.y, P0.dc.y, P0.uym.y, P0.uc.y)) * iy;
-    lap[2] += (fx<SEL>(P1.dc.x, P1.dyp.x, P1.uc.x, P1.uyp.x) - fx<SEL>(P1.dym.x, P1.dc.x, P1.uym.x, P1.uc.x)) * iy;
-    lap[3] += (fx<SEL>(P1.dc.y, P1.dyp.y, P1.uc.y, P1.uyp.y) - fx<SEL>(P1.dym.y, P1.dc.y, P1.uym.y, P1.uc.y)) * iy;
-    const double fzb0 = fx<SEL>(db.x, P0.dc.x, ub.x, P0.uc.x);
-    const double fzb1 = fx<SEL>(db.y, P0.dc.y, ub.y, P0.uc.y);
-    const double fzm0 = fx<SEL>(P0.dc.x, P1.dc.x, P0.uc.x, P1.uc.x);
-    const double fzm1 = fx<SEL>(P0.dc.y, P1.dc.y, P0.uc.y, P1.uc.y);
-    const double fza0 = fx<SEL>(P1.dc.x, da.x, P1.uc.x, ua.x);
-    const double fza1 = fx<SEL>(P1.dc.y, da.y, P1.uc.y, ua.y);
-    lap[0] += (fzm0 - fzb0) * iz;
-    lap[1] += (fzm1 - fzb1) * iz;
-    lap[2] += (fza0 - fzm0) * iz;
-    lap[3] += (fza1 - fzm1) * iz;
-}
-
 template <int REACTION>
-__device__ __forceinline__ void finish_plane(const MarchArgs& M, const SlowConsts& K, const ChunkCtx& C,
-                                             int z, const PairIn& P, double2 uzm, double2 dzm,
-                                             double2 uzp, double2 dzp, double lap0, double lap1,
-                                             bool dirichlet, int y, int xp, int x0) {
-    const StepArgs<double>& A = M.A;
+__device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
+                                              const ChunkCtx& C, int z, const Tile& Tm,
+                                              const Tile& T0, const Tile& Tp, int y, int xp, int x0,
+                                              int t0, int lofs, int rofs) {
     const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
     if (!(a0 | a1)) return;
+    const double* U0 = T0.u;
+    const double2 uc = *reinterpret_cast<const double2*>(&U0[t0]);
+    const double2 dc = *reinterpret_cast<const double2*>(&U0[t0 + kTileD]);
+    const double uL = U0[lofs], dL = U0[lofs + kTileD];
+    const double uR = U0[rofs], dR = U0[rofs + kTileD];
+    const double2 uym = *reinterpret_cast<const double2*>(&U0[t0 - 8]);
+    const double2 dym = *reinterpret_cast<const double2*>(&U0[t0 - 8 + kTileD]);
+    const double2 uyp = *reinterpret_cast<const double2*>(&U0[t0 + 8]);
+    const double2 dyp = *reinterpret_cast<const double2*>(&U0[t0 + 8 + kTileD]);
+    const double2 uzm = *reinterpret_cast<const double2*>(&Tm.u[t0]);
+    const double2 dzm = *reinterpret_cast<const double2*>(&Tm.d[t0]);
+    const double2 uzp = *reinterpret_cast<const double2*>(&Tp.u[t0]);
+    const double2 dzp = *reinterpret_cast<const double2*>(&Tp.d[t0]);
+    const StepArgs<double>& A = M.A;
     const int o = z * 64 + y * 8 + x0;
     const int c = C.c;
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
@@ -324,47 +311,85 @@ __device__ __forceinline__ void finish_plane(const MarchArgs& M, const SlowConst
         src0 = A.src[(int64_t)c * 512 + o];
         src1 = A.src[(int64_t)c * 512 + o + 1];
     }
+    const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
+    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
     double out0, out1;
     if (!dirichlet) {
+        double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
+        if ((C.flags >> (8 + z)) & 1) {
+            // interior-fluid plane (warp-uniform): no substitution anywhere
+            fxl = fface(dL, dc.x, uL, uc.x);
+            fxi = fface(dc.x, dc.y, uc.x, uc.y);
+            fxr = fface(dc.y, dR, uc.y, uR);
+            fy0m = fface(dym.x, dc.x, uym.x, uc.x);
+            fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
+            fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
+            fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
+            fy1m = fface(dym.y, dc.y, uym.y, uc.y);
+            fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
+            fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
+            fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
+        } else {
+            fxl = face(dL, dc.x, uL, uc.x);
+            fxi = face(dc.x, dc.y, uc.x, uc.y);
+            fxr = face(dc.y, dR, uc.y, uR);
+            fy0m = face(dym.x, dc.x, uym.x, uc.x);
+            fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
+            fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
+            fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
+            fy1m = face(dym.y, dc.y, uym.y, uc.y);
+            fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
+            fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
+            fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
+        }
+        double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
+        lap0 += (fxi - fxl) * ix;
+        lap0 += (fy0p - fy0m) * iy;
+        lap0 += (fz0p - fz0m) * iz;
+        double lap1 = 0.0;
+        lap1 += (fxr - fxi) * ix;
+        lap1 += (fy1p - fy1m) * iy;
+        lap1 += (fz1p - fz1m) * iz;
         double r0 = 0.0, r1 = 0.0;
         if (REACTION == PD_REACTION_SURFACE_SINK) {
-            if (s0) r0 = K.neg_k * P.uc.x;
-            if (s1) r1 = K.neg_k * P.uc.y;
+            if (s0) r0 = K.neg_k * uc.x;
+            if (s1) r1 = K.neg_k * uc.y;
         } else if (REACTION == PD_REACTION_VOLUMETRIC) {
             r0 = src0 * K.src_factor;
             r1 = src1 * K.src_factor;
         }
-        out0 = P.uc.x + K.dt * lap0 + K.dt * r0;
-        out1 = P.uc.y + K.dt * lap1 + K.dt * r1;
-    }
-    const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
-    const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-    if (dirichlet) {
-        const double nu0[6] = {P.uL, P.uc.y, P.uym.x, P.uyp.x, uzm.x, uzp.x};
-        const double nd0[6] = {P.dL, P.dc.y, P.dym.x, P.dyp.x, dzm.x, dzp.x};
-        out0 = slow_node<REACTION>(K, P.uc.x, P.dc.x, nu0, nd0, gx, gy, gz, s0, src0);
-        const double nu1[6] = {P.uc.x, P.uR, P.uym.y, P.uyp.y, uzm.y, uzp.y};
-        const double nd1[6] = {P.dc.x, P.dR, P.dym.y, P.dyp.y, dzm.y, dzp.y};
-        out1 = slow_node<REACTION>(K, P.uc.y, P.dc.y, nu1, nd1, gx + 1, gy, gz, s1, src1);
+        out0 = uc.x + K.dt * lap0 + K.dt * r0;
+        out1 = uc.y + K.dt * lap1 + K.dt * r1;
+    } else {
+        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
+        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
+        const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+        const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+        out0 = slow_node<REACTION>(K, uc.x, dc.x, nu0, nd0, gx, gy, gz, s0, src0);
+        const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+        const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+        out1 = slow_node<REACTION>(K, uc.y, dc.y, nu1, nd1, gx + 1, gy, gz, s1, src1);
     }
     // walls (active, not fluid) stay frozen (solver.hpp:413-417)
-    if (sentinel(P.dc.x)) out0 = P.uc.x;
-    if (sentinel(P.dc.y)) out1 = P.uc.y;
+    if (sentinel(dc.x)) out0 = uc.x;
+    if (sentinel(dc.y)) out1 = uc.y;
     const bool h0 = a0 && huge(out0), h1 = a1 && huge(out1);
     if (h0 | h1) {
         // rare: a non-finite fast-path result is re-derived exactly (the
         // +-0 substitution shortcut needs finite operands), then the
         // reference's non-finite / total-mass checks are flagged
         // (solver.hpp:444, 250-260, 514-515)
-        if (h0 && !isfinite(out0) && !sentinel(P.dc.x) && !dirichlet) {
-            const double nu[6] = {P.uL, P.uc.y, P.uym.x, P.uyp.x, uzm.x, uzp.x};
-            const double nd[6] = {P.dL, P.dc.y, P.dym.x, P.dyp.x, dzm.x, dzp.x};
-            out0 = slow_node<REACTION>(K, P.uc.x, P.dc.x, nu, nd, gx, gy, gz, s0, src0);
+        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
+        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
+        if (h0 && !isfinite(out0) && !sentinel(dc.x) && !dirichlet) {
+            const double nu[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+            const double nd[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+            out0 = slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
         }
-        if (h1 && !isfinite(out1) && !sentinel(P.dc.y) && !dirichlet) {
-            const double nu[6] = {P.uc.x, P.uR, P.uym.y, P.uyp.y, uzm.y, uzp.y};
-            const double nd[6] = {P.dc.x, P.dR, P.dym.y, P.dyp.y, dzm.y, dzp.y};
-            out1 = slow_node<REACTION>(K, P.uc.y, P.dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
+        if (h1 && !isfinite(out1) && !sentinel(dc.y) && !dirichlet) {
+            const double nu[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+            const double nd[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+            out1 = slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
         }
         const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
         if (bad0 | bad1) {
@@ -384,31 +409,6 @@ __device__ __forceinline__ void finish_plane(const MarchArgs& M, const SlowConst
     // x-face side planes of u_next for the next step's x halos
     if (xp == 0 && a0) M.xfun[((int64_t)c * 2 + 0) * 64 + z * 8 + y] = out0;
     if (xp == 3 && a1) M.xfun[((int64_t)c * 2 + 1) * 64 + z * 8 + y] = out1;
-}
-
-// Planes z and z+1 of chunk C from tiles Tb (z-1), T0 (z), T1 (z+1), Ta (z+2).
-template <int REACTION>
-__device__ __forceinline__ void compute_two(const MarchArgs& M, const SlowConsts& K, const ChunkCtx& C,
-                                            int z, const Tile& Tb, const Tile& T0, const Tile& T1,
-                                            const Tile& Ta, int y, int xp, int x0, int t0, int lofs,
-                                            int rofs) {
-    if (!((C.lm >> (2 * z)) & 15u)) return;  // no active node in this lane's 4 nodes
-    const PairIn P0 = load_pair(T0, t0, lofs, rofs);
-    const PairIn P1 = load_pair(T1, t0, lofs, rofs);
-    const double2 ub = *reinterpret_cast<const double2*>(&Tb.u[t0]);
-    const double2 db = *reinterpret_cast<const double2*>(&Tb.d[t0]);
-    const double2 ua = *reinterpret_cast<const double2*>(&Ta.u[t0]);
-    const double2 da = *reinterpret_cast<const double2*>(&Ta.d[t0]);
-    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
-    double lap[4];
-    if (!dirichlet) {
-        if (((C.flags >> (8 + z)) & 3) == 3)
-            lap4<false>(P0, P1, ub, db, ua, da, K, lap);  // interior-fluid planes
-        else
-            lap4<true>(P0, P1, ub, db, ua, da, K, lap);
-    }
-    finish_plane<REACTION>(M, K, C, z, P0, ub, db, P1.uc, P1.dc, lap[0], lap[1], dirichlet, y, xp, x0);
-    finish_plane<REACTION>(M, K, C, z + 1, P1, P0.uc, P0.dc, ua, da, lap[2], lap[3], dirichlet, y, xp, x0);
 }
 
 __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
@@ -432,16 +432,18 @@ __device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
 
 // One warp streams a sequence of chunks. Its plane loads (10 per chunk:
 // z-halo below, the 8 body planes, z-halo above) form one continuous
-// sequence through a kRing-slot tile ring, kAhead loads beyond the four planes
-// a step reads, across chunk boundaries. A step computes two planes.
+// sequence through a kRing-slot tile ring (one mbarrier per slot), kAhead
+// loads ahead of the plane being computed, across chunk boundaries.
 template <int REACTION, int OCC>
 __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ SlowConsts K;
+    __shared__ __align__(8) uint64_t bars[kWarps][kRing];
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
     Tile* ring = reinterpret_cast<Tile*>(smem_raw) + warp * kRing;
+    const unsigned bar0 = smem_u32(&bars[warp][0]);
     const StepArgs<double>& A = M.A;
     if (A.k > 0) {
         const int prev = A.flags[A.k - 1];
@@ -461,11 +463,13 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         K.src_factor = A.src_factor;
         K.dirichlet = A.dirichlet;
     }
+    if (lane < kRing) mbar_init(bar0 + 8 * lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
     // lane-constant tile offsets (u array; D is +kTileD)
     const int t0 = tix(x0, y);
-    const int lofs = xp == 0 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + y : t0 - 1;
-    const int rofs = xp == 3 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + 8 + y : t0 + 2;
+    const int lofs = xp == 0 ? kHX + y : t0 - 1;
+    const int rofs = xp == 3 ? kHX + 8 + y : t0 + 2;
 
     // ---- chunk stream: kBatch-chunk claims from one counter ----
     int* ctr = M.counter;
@@ -494,43 +498,41 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     int dv0, dv1;
     load_ctx(M, c_ld, lane, lm0, dv0);
     ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
-    LoadCtx Lld = make_load_ctx(Cld, M, y, xp, x0);
+    LoadCtx Lld = make_load_ctx(Cld, M, lane);
     int c_nx = next_id();
     load_ctx(M, c_nx, lane, lm1, dv1);
     int p_ld = -1;  // next plane of Cld to issue (-1..8)
     int L = 0;      // loads issued
     auto issue_next = [&]() {
-        issue_plane(ring[L & (kRing - 1)], M, Lld, p_ld, y, xp, x0);
-        cp_commit();
+        const int s = L & (kRing - 1);
+        issue_plane(ring[s], bar0 + 8 * s, Lld, p_ld, lane);
         ++L;
         if (++p_ld == 9) {  // advance the load side to the next chunk
             p_ld = -1;
             Cld = make_ctx(c_nx, lm1, dv1);
-            Lld = make_load_ctx(Cld, M, y, xp, x0);
+            Lld = make_load_ctx(Cld, M, lane);
             c_nx = Cld.c >= 0 ? next_id() : -1;
             load_ctx(M, c_nx, lane, lm1, dv1);
         }
     };
     // compute side: follows the load side, which is never more than one
-    // chunk ahead (kAhead + 4 < 10 loads)
+    // chunk ahead (kAhead + 3 < 10 loads)
     ChunkCtx Cc = Cld;
     int base = 0;  // load index of plane -1 of Cc
-    // prologue: planes -1..2 read by the first step, plus kAhead more
-    for (int k = 0; k < 4 + kAhead; ++k) issue_next();
+    // prologue: planes -1, 0, 1 needed for z = 0, plus kAhead more
+    for (int k = 0; k < 3 + kAhead; ++k) issue_next();
     while (Cc.c >= 0) {
 #pragma unroll 1
-        for (int z = 0; z < 8; z += 2) {
-            // loads up to index base+z+3 complete; exactly kAhead newer groups
-            // are in flight at this point of every step
-            cp_wait<kAhead>();
+        for (int z = 0; z < 8; ++z) {
+            const int need = base + z + 2;  // newest load the step reads
+            mbar_wait(bar0 + 8 * (need & (kRing - 1)), (unsigned)(need / kRing) & 1u);
             __syncwarp();
-            compute_two<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
-                                  ring[(base + z + 1) & (kRing - 1)], ring[(base + z + 2) & (kRing - 1)],
-                                  ring[(base + z + 3) & (kRing - 1)], y, xp, x0, t0, lofs, rofs);
+            compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
+                                    ring[(base + z + 1) & (kRing - 1)], ring[need & (kRing - 1)], y, xp,
+                                    x0, t0, lofs, rofs);
             __syncwarp();
             issue_next();
-            issue_next();
-            if (z == 6) {  // planes 8 of this chunk and -1 of the next
+            if (z == 7) {  // planes 8 of this chunk and -1 of the next
                 issue_next();
                 issue_next();
             }
@@ -538,7 +540,9 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         base += 10;
         Cc = Cld;
     }
-    cp_wait<0>();
+    // drain: every issued phase must complete before the CTA exits
+    for (int k = L - kRing; k < L; ++k)
+        if (k >= 0) mbar_wait(bar0 + 8 * (k & (kRing - 1)), (unsigned)(k / kRing) & 1u);
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
