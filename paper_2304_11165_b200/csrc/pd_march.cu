@@ -142,138 +142,74 @@ struct ChunkCtx {
     uint32_t lm;
 };
 
-// Per-warp ring of plane tiles in shared memory, filled by TMA bulk copies.
-// A tile holds u and D_eff of one z-plane of a chunk: rows y = -1..8 of the 8
-// body columns (pitch 8: lanes' 16-B pair accesses are bank-conflict free;
-// rows 0..7 are one contiguous 512-B plane, rows -1 / 8 are 64-B rows of the y
-// neighbours) and the x- / x+ halo columns (64 B each, from the side planes).
+// Per-warp ring of plane tiles in shared memory. A tile holds u and D_eff of
+// one z-plane of a chunk: rows y = -1..8 of the 8 body columns (pitch 8, so
+// the lanes' 16-B pair accesses are bank-conflict free) and the x- / x+ halo
+// cells of rows 0..7 in two side columns.
 constexpr int kRing = 8;   // power of two: slot = load index & 7
-constexpr int kAhead = 5;  // loads in flight beyond the 3 planes a step reads
+constexpr int kAhead = 5;  // kRing - 3 (planes z-1, z, z+1 resident)
 struct Tile {
     double u[80], hxu[2][8];
     double d[80], hxd[2][8];
 };
-constexpr int kTileD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
-constexpr int kHX = (int)(offsetof(Tile, hxu) / sizeof(double));
 __device__ __forceinline__ int tix(int x, int y) { return x + 8 * (y + 1); }
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+__device__ __forceinline__ void cp16_if(void* smem, const void* gmem, bool pred) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(smem)),
+        "l"(gmem), "r"((int)pred));
 }
-__device__ __forceinline__ void mbar_init(unsigned bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+__device__ __forceinline__ void cp8_if(void* smem, const void* gmem, bool pred) {
     asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(smem)),
+        "l"(gmem), "r"((int)pred));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Lane roles of the per-plane bulk copies (lane < 10): 0/1 body u / D_eff
-// (512 B), 2/3 x- halo column, 4/5 x+ halo column (64 B, side planes), 6/7 y-
-// halo row, 8/9 y+ halo row (64 B). Computed once per chunk.
-struct LoadCtx {
-    const char* src;  // role source for plane 0 (nullptr: role absent)
-    unsigned dst;     // byte offset of the role's destination inside a tile
-    unsigned bytes;
-    unsigned stride;  // source bytes per plane
-    unsigned halo_tx; // bytes of the valid halo roles of a body plane (lane-uniform)
-    const char* zlo;  // roles 0/1: z- neighbour's plane 7 (halo plane -1)
-    const char* zhi;  // roles 0/1: z+ neighbour's plane 0 (halo plane 8)
-    uint32_t pact;    // bit p: body plane p has an active node (lane-uniform)
-    int c;
-};
-
-__device__ __forceinline__ LoadCtx make_load_ctx(const ChunkCtx& C, const MarchArgs& M, int lane) {
-    LoadCtx L;
-    L.c = C.c;
-    L.src = nullptr;
-    L.zlo = L.zhi = nullptr;
-    L.dst = 0;
-    L.bytes = 0;
-    L.stride = 512;
-    const bool isd = lane & 1;
-    const char* U = reinterpret_cast<const char*>(isd ? M.deff : M.A.u);
-    const char* XF = reinterpret_cast<const char*>(isd ? M.xfd : M.xfu);
-    const unsigned dbase = isd ? kTileD * 8 : 0;
-    const int role = lane >> 1;
-    if (C.c >= 0 && lane < 10) {
-        if (role == 0) {
-            L.src = U + (int64_t)C.c * 4096;
-            L.dst = dbase + 64;
-            L.bytes = 512;
-            if (!(M.dbg & 4)) {
-                if (C.nb[4] >= 0) L.zlo = U + (int64_t)C.nb[4] * 4096 + 448 * 8;
-                if (C.nb[5] >= 0) L.zhi = U + (int64_t)C.nb[5] * 4096;
-            }
-        } else if (role <= 2) {  // x- (role 1) / x+ (role 2): neighbour's x=7 / x=0 side plane
-            const int j = (M.dbg & 1) ? -1 : C.nb[role - 1];
-            if (j >= 0) L.src = XF + ((int64_t)j * 2 + (role == 1 ? 1 : 0)) * 512;
-            L.dst = dbase + (kHX + (role - 1) * 8) * 8;
-            L.bytes = 64;
-            L.stride = 64;
-        } else {  // y- (role 3) / y+ (role 4): neighbour's row y=7 / y=0
-            const int j = (M.dbg & 2) ? -1 : C.nb[role - 1];
-            if (j >= 0) L.src = U + (int64_t)j * 4096 + (role == 3 ? 56 * 8 : 0);
-            L.dst = dbase + (role == 3 ? 0 : 72 * 8);
-            L.bytes = 64;
-        }
-    }
-    const unsigned mine = (lane >= 2 && lane < 10 && L.src) ? L.bytes : 0u;
-    L.halo_tx = __reduce_add_sync(0xffffffffu, mine);
-    uint32_t pa = 0;
-    for (int z = 0; z < 8; ++z)
-        if (__any_sync(0xffffffffu, ((C.lm >> (2 * z)) & 3u) != 0)) pa |= 1u << z;
-    L.pact = pa;
-    return L;
-}
-
-// Issues plane p (-1..8) of the load-side chunk into tile slot T (mbarrier
-// bar): TMA bulk copies by the role lanes; D_eff sentinel fills where a body
-// plane has no active node or a neighbour is absent.
-__device__ __forceinline__ void issue_plane(Tile& T, unsigned bar, const LoadCtx& L, int p, int lane) {
+// Issues the lane's share of plane p (-1..8) of chunk C into tile T:
+// predicated 16-B copies of its node pair (pairs with no active node are
+// never read; their D_eff cells get the sentinel) and, for chunk-face lanes,
+// the x / y halo cells. p = -1 / 8 are the z halo planes of the z neighbours.
+__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const ChunkCtx& C, int p,
+                                            int y, int xp, int x0) {
+    const int t0 = tix(x0, y);
     const double sv = sent();
-    const bool body = (unsigned)p <= 7u;
-    const char* src0 = body ? ((L.pact >> p) & 1u ? L.src : nullptr) : (p < 0 ? L.zlo : L.zhi);
-    // bytes this plane will deliver (lane-uniform)
-    const unsigned lane01 = (L.c >= 0 && ((body && ((L.pact >> p) & 1u)) || (!body && src0 != nullptr))) ? 1024u : 0u;
-    const unsigned tx = __shfl_sync(0xffffffffu, lane01, 0) + (body && L.c >= 0 ? L.halo_tx : 0u);
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    if (lane == 0) mbar_arrive_tx(bar, tx);
-    const unsigned tbase = smem_u32(&T);
-    if (lane < 2) {
-        if (L.c >= 0 && src0) bulk_g2s(tbase + L.dst, src0 + (body ? (int64_t)p * 512 : 0), 512u, bar);
-    } else if (lane < 10 && body) {
-        if (L.src) bulk_g2s(tbase + L.dst, L.src + (int64_t)p * L.stride, 64u, bar);
-    }
-    // sentinel D_eff where nothing is copied
-    const bool body_missing = !(L.c >= 0 && src0 != nullptr);
-    const bool body_missing0 = __shfl_sync(0xffffffffu, body_missing ? 1 : 0, 0);
-    if (body_missing0) *reinterpret_cast<double2*>(&T.d[8 + 2 * lane]) = make_double2(sv, sv);
-    if (body) {
-        // roles 3 (x-), 5 (x+), 7 (y-), 9 (y+) own the D halo destinations
-        if (lane < 10 && (lane & 1) && lane >= 3 && !L.src) {
-            double* dd = reinterpret_cast<double*>(reinterpret_cast<char*>(&T) + L.dst);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dd[k] = sv;
-        }
-    }
+    const int bp = y * 8 + x0;
+    const bool body = p >= 0 && p <= 7;
+    // own pair (or the z-halo plane's pair)
+    const int jz = p < 0 ? C.nb[4] : C.nb[5];
+    const bool zok = !(M.dbg & 4) && jz >= 0;
+    const bool ok = body ? ((C.lm >> (2 * p)) & 3u) != 0 : zok;
+    const int64_t off = body ? (int64_t)C.c * 512 + p * 64 + bp
+                             : (int64_t)(jz < 0 ? 0 : jz) * 512 + (p < 0 ? 448 : 0) + bp;
+    cp16_if(&T.u[t0], M.A.u + off, ok);
+    cp16_if(&T.d[t0], M.deff + off, ok);
+    if (!ok) *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
+    if (!body) return;  // warp-uniform
+    // x halo (lanes xp == 0 / 3): neighbour's x=7 / x=0 side plane
+    const bool xl = xp == 0 || xp == 3;
+    const int side = xp == 0 ? 0 : 1;
+    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
+    const int64_t ox = ((int64_t)(jx < 0 ? 0 : jx) * 2 + (1 - side)) * 64 + p * 8 + y;
+    cp8_if(&T.hxu[side][y], M.xfu + ox, xl && jx >= 0);
+    cp8_if(&T.hxd[side][y], M.xfd + ox, xl && jx >= 0);
+    if (xl && jx < 0) T.hxd[side][y] = sv;
+    // y halo (lanes y == 0 / 7): neighbour's row y=7 / y=0
+    const bool yl = y == 0 || y == 7;
+    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
+    const int ty = y == 0 ? t0 - 8 : t0 + 8;
+    const int64_t oy = (int64_t)(jy < 0 ? 0 : jy) * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
+    cp16_if(&T.u[ty], M.A.u + oy, yl && jy >= 0);
+    cp16_if(&T.d[ty], M.deff + oy, yl && jy >= 0);
+    if (yl && jy < 0) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
 }
 
 // |x| >= 2^990 or non-finite, from the high word (integer pipe)
@@ -284,19 +220,22 @@ __device__ __forceinline__ bool huge(double x) {
 template <int REACTION>
 __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
                                               const ChunkCtx& C, int z, const Tile& Tm,
-                                              const Tile& T0, const Tile& Tp, int y, int xp, int x0,
-                                              int t0, int lofs, int rofs) {
+                                              const Tile& T0, const Tile& Tp, int lane) {
+    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
     const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
     if (!(a0 | a1)) return;
-    const double* U0 = T0.u;
-    const double2 uc = *reinterpret_cast<const double2*>(&U0[t0]);
-    const double2 dc = *reinterpret_cast<const double2*>(&U0[t0 + kTileD]);
-    const double uL = U0[lofs], dL = U0[lofs + kTileD];
-    const double uR = U0[rofs], dR = U0[rofs + kTileD];
-    const double2 uym = *reinterpret_cast<const double2*>(&U0[t0 - 8]);
-    const double2 dym = *reinterpret_cast<const double2*>(&U0[t0 - 8 + kTileD]);
-    const double2 uyp = *reinterpret_cast<const double2*>(&U0[t0 + 8]);
-    const double2 dyp = *reinterpret_cast<const double2*>(&U0[t0 + 8 + kTileD]);
+    const int t0 = tix(x0, y);
+    const double2 uc = *reinterpret_cast<const double2*>(&T0.u[t0]);
+    const double2 dc = *reinterpret_cast<const double2*>(&T0.d[t0]);
+    const double* pl = xp == 0 ? &T0.hxu[0][y] : &T0.u[t0 - 1];
+    const double* pr = xp == 3 ? &T0.hxu[1][y] : &T0.u[t0 + 2];
+    constexpr int kD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
+    const double uL = pl[0], dL = pl[kD];
+    const double uR = pr[0], dR = pr[kD];
+    const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 8]);
+    const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 8]);
+    const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 8]);
+    const double2 dyp = *reinterpret_cast<const double2*>(&T0.d[t0 + 8]);
     const double2 uzm = *reinterpret_cast<const double2*>(&Tm.u[t0]);
     const double2 dzm = *reinterpret_cast<const double2*>(&Tm.d[t0]);
     const double2 uzp = *reinterpret_cast<const double2*>(&Tp.u[t0]);
@@ -432,18 +371,16 @@ __device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
 
 // One warp streams a sequence of chunks. Its plane loads (10 per chunk:
 // z-halo below, the 8 body planes, z-halo above) form one continuous
-// sequence through a kRing-slot tile ring (one mbarrier per slot), kAhead
-// loads ahead of the plane being computed, across chunk boundaries.
+// sequence through a kRing-slot tile ring, kAhead loads ahead of the plane
+// being computed, across chunk boundaries.
 template <int REACTION, int OCC>
 __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SlowConsts K;
-    __shared__ __align__(8) uint64_t bars[kWarps][kRing];
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
     Tile* ring = reinterpret_cast<Tile*>(smem_raw) + warp * kRing;
-    const unsigned bar0 = smem_u32(&bars[warp][0]);
     const StepArgs<double>& A = M.A;
     if (A.k > 0) {
         const int prev = A.flags[A.k - 1];
@@ -463,13 +400,7 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         K.src_factor = A.src_factor;
         K.dirichlet = A.dirichlet;
     }
-    if (lane < kRing) mbar_init(bar0 + 8 * lane, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
-    // lane-constant tile offsets (u array; D is +kTileD)
-    const int t0 = tix(x0, y);
-    const int lofs = xp == 0 ? kHX + y : t0 - 1;
-    const int rofs = xp == 3 ? kHX + 8 + y : t0 + 2;
 
     // ---- chunk stream: kBatch-chunk claims from one counter ----
     int* ctr = M.counter;
@@ -498,19 +429,17 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     int dv0, dv1;
     load_ctx(M, c_ld, lane, lm0, dv0);
     ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
-    LoadCtx Lld = make_load_ctx(Cld, M, lane);
     int c_nx = next_id();
     load_ctx(M, c_nx, lane, lm1, dv1);
     int p_ld = -1;  // next plane of Cld to issue (-1..8)
     int L = 0;      // loads issued
     auto issue_next = [&]() {
-        const int s = L & (kRing - 1);
-        issue_plane(ring[s], bar0 + 8 * s, Lld, p_ld, lane);
+        if (Cld.c >= 0) issue_plane(ring[L & (kRing - 1)], M, Cld, p_ld, y, xp, x0);
+        cp_commit();
         ++L;
         if (++p_ld == 9) {  // advance the load side to the next chunk
             p_ld = -1;
             Cld = make_ctx(c_nx, lm1, dv1);
-            Lld = make_load_ctx(Cld, M, lane);
             c_nx = Cld.c >= 0 ? next_id() : -1;
             load_ctx(M, c_nx, lane, lm1, dv1);
         }
@@ -524,12 +453,13 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     while (Cc.c >= 0) {
 #pragma unroll 1
         for (int z = 0; z < 8; ++z) {
-            const int need = base + z + 2;  // newest load the step reads
-            mbar_wait(bar0 + 8 * (need & (kRing - 1)), (unsigned)(need / kRing) & 1u);
+            // loads up to index base+z+2 complete; exactly kAhead newer groups
+            // are in flight at this point of every iteration
+            cp_wait<kAhead>();
             __syncwarp();
             compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
-                                    ring[(base + z + 1) & (kRing - 1)], ring[need & (kRing - 1)], y, xp,
-                                    x0, t0, lofs, rofs);
+                                    ring[(base + z + 1) & (kRing - 1)],
+                                    ring[(base + z + 2) & (kRing - 1)], lane);
             __syncwarp();
             issue_next();
             if (z == 7) {  // planes 8 of this chunk and -1 of the next
@@ -540,9 +470,7 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         base += 10;
         Cc = Cld;
     }
-    // drain: every issued phase must complete before the CTA exits
-    for (int k = L - kRing; k < L; ++k)
-        if (k >= 0) mbar_wait(bar0 + 8 * (k & (kRing - 1)), (unsigned)(k / kRing) & 1u);
+    cp_wait<0>();
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
