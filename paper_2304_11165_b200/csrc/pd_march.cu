@@ -136,9 +136,8 @@ __device__ __forceinline__ double fface(double da, double db, double ua, double 
     return ((da + db) * 0.5) * (ub - ua);
 }
 
-struct ChunkCtx {
+struct ChunkCtx {  // what the compute side needs of a chunk
     int c, key, flags;
-    int nb[6];
     uint32_t lm;
 };
 
@@ -174,42 +173,68 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Issues the lane's share of plane p (-1..8) of chunk C into tile T:
-// predicated 16-B copies of its node pair (pairs with no active node are
-// never read; their D_eff cells get the sentinel) and, for chunk-face lanes,
-// the x / y halo cells. p = -1 / 8 are the z halo planes of the z neighbours.
-__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const ChunkCtx& C, int p,
-                                            int y, int xp, int x0) {
-    const int t0 = tix(x0, y);
+// Lane-specific source offsets (elements, 32-bit: u holds < 2^32 slots, see
+// march_build) of one chunk, computed once per chunk on the load side.
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+struct LoadCtx {
+    int c;
+    uint32_t lm;
+    uint32_t own;   // the lane's pair in plane 0
+    uint32_t zlo;   // pair in the z- neighbour's plane 7
+    uint32_t zhi;   // pair in the z+ neighbour's plane 0
+    uint32_t xoff;  // x-halo cell of plane 0 in the side planes (face lanes)
+    uint32_t yoff;  // y-halo pair of plane 0 (face lanes)
+};
+
+__device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, const MarchArgs& M, int y,
+                                                 int xp, int x0) {
+    int nb[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
+    LoadCtx L;
+    L.c = c;
+    L.lm = lm;
+    const uint32_t bp = (uint32_t)(y * 8 + x0);
+    L.own = (uint32_t)(c < 0 ? 0 : c) * 512u + bp;
+    const bool zk = !(M.dbg & 4);
+    L.zlo = (zk && nb[4] >= 0) ? (uint32_t)nb[4] * 512u + 448u + bp : kNone;
+    L.zhi = (zk && nb[5] >= 0) ? (uint32_t)nb[5] * 512u + bp : kNone;
+    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? nb[0] : nb[1]);
+    L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? ((uint32_t)jx * 2u + (xp == 0 ? 1u : 0u)) * 64u + (uint32_t)y
+                                               : kNone;
+    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? nb[2] : nb[3]);
+    L.yoff = ((y == 0 || y == 7) && jy >= 0) ? (uint32_t)jy * 512u + (y == 0 ? 56u : 0u) + (uint32_t)x0 : kNone;
+    return L;
+}
+
+// Issues the lane's share of plane p (-1..8) into tile T: predicated 16-B
+// copies of its node pair (pairs with no active node are never read; their
+// D_eff cells get the sentinel) and, for chunk-face lanes, the x / y halo
+// cells. p = -1 / 8 are the z halo planes of the z neighbours.
+__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const LoadCtx& L, int p,
+                                            int y, int xp, int t0) {
     const double sv = sent();
-    const int bp = y * 8 + x0;
-    const bool body = p >= 0 && p <= 7;
-    // own pair (or the z-halo plane's pair)
-    const int jz = p < 0 ? C.nb[4] : C.nb[5];
-    const bool zok = !(M.dbg & 4) && jz >= 0;
-    const bool ok = body ? ((C.lm >> (2 * p)) & 3u) != 0 : zok;
-    const int64_t off = body ? (int64_t)C.c * 512 + p * 64 + bp
-                             : (int64_t)(jz < 0 ? 0 : jz) * 512 + (p < 0 ? 448 : 0) + bp;
-    cp16_if(&T.u[t0], M.A.u + off, ok);
-    cp16_if(&T.d[t0], M.deff + off, ok);
+    const bool body = (unsigned)p <= 7u;
+    const uint32_t o = body ? L.own + (uint32_t)p * 64u : (p < 0 ? L.zlo : L.zhi);
+    const bool ok = L.c >= 0 && (body ? ((L.lm >> (2 * p)) & 3u) != 0 : o != kNone);
+    const uint32_t oo = ok ? o : 0u;
+    cp16_if(&T.u[t0], M.A.u + oo, ok);
+    cp16_if(&T.d[t0], M.deff + oo, ok);
     if (!ok) *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
     if (!body) return;  // warp-uniform
-    // x halo (lanes xp == 0 / 3): neighbour's x=7 / x=0 side plane
-    const bool xl = xp == 0 || xp == 3;
+    const bool xl = xp == 0 || xp == 3, yl = y == 0 || y == 7;
     const int side = xp == 0 ? 0 : 1;
-    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? C.nb[0] : C.nb[1]);
-    const int64_t ox = ((int64_t)(jx < 0 ? 0 : jx) * 2 + (1 - side)) * 64 + p * 8 + y;
-    cp8_if(&T.hxu[side][y], M.xfu + ox, xl && jx >= 0);
-    cp8_if(&T.hxd[side][y], M.xfd + ox, xl && jx >= 0);
-    if (xl && jx < 0) T.hxd[side][y] = sv;
-    // y halo (lanes y == 0 / 7): neighbour's row y=7 / y=0
-    const bool yl = y == 0 || y == 7;
-    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? C.nb[2] : C.nb[3]);
+    const bool xok = L.c >= 0 && L.xoff != kNone;
+    const uint32_t ox = xok ? L.xoff + (uint32_t)p * 8u : 0u;
+    cp8_if(&T.hxu[side][y], M.xfu + ox, xok);
+    cp8_if(&T.hxd[side][y], M.xfd + ox, xok);
+    if (xl && !xok) T.hxd[side][y] = sv;
+    const bool yok = L.c >= 0 && L.yoff != kNone;
     const int ty = y == 0 ? t0 - 8 : t0 + 8;
-    const int64_t oy = (int64_t)(jy < 0 ? 0 : jy) * 512 + p * 64 + (y == 0 ? 56 : 0) + x0;
-    cp16_if(&T.u[ty], M.A.u + oy, yl && jy >= 0);
-    cp16_if(&T.d[ty], M.deff + oy, yl && jy >= 0);
-    if (yl && jy < 0) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
+    const uint32_t oy = yok ? L.yoff + (uint32_t)p * 64u : 0u;
+    cp16_if(&T.u[ty], M.A.u + oy, yok);
+    cp16_if(&T.d[ty], M.deff + oy, yok);
+    if (yl && !yok) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
 }
 
 // |x| >= 2^990 or non-finite, from the high word (integer pipe)
@@ -220,18 +245,15 @@ __device__ __forceinline__ bool huge(double x) {
 template <int REACTION>
 __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
                                               const ChunkCtx& C, int z, const Tile& Tm,
-                                              const Tile& T0, const Tile& Tp, int lane) {
-    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
+                                              const Tile& T0, const Tile& Tp, int y, int xp, int x0,
+                                              int t0, int lofs, int rofs) {
     const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
     if (!(a0 | a1)) return;
-    const int t0 = tix(x0, y);
     const double2 uc = *reinterpret_cast<const double2*>(&T0.u[t0]);
     const double2 dc = *reinterpret_cast<const double2*>(&T0.d[t0]);
-    const double* pl = xp == 0 ? &T0.hxu[0][y] : &T0.u[t0 - 1];
-    const double* pr = xp == 3 ? &T0.hxu[1][y] : &T0.u[t0 + 2];
     constexpr int kD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
-    const double uL = pl[0], dL = pl[kD];
-    const double uR = pr[0], dR = pr[kD];
+    const double uL = T0.u[lofs], dL = T0.u[lofs + kD];
+    const double uR = T0.u[rofs], dR = T0.u[rofs + kD];
     const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 8]);
     const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 8]);
     const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 8]);
@@ -362,8 +384,6 @@ __device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
     ChunkCtx C;
     C.c = c;
     C.lm = lm;
-#pragma unroll
-    for (int f = 0; f < 6; ++f) C.nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
     C.key = __shfl_sync(0xffffffffu, dv, 30);
     C.flags = __shfl_sync(0xffffffffu, dv, 31);
     return C;
@@ -401,6 +421,8 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         K.dirichlet = A.dirichlet;
     }
     __syncthreads();
+    const int lofs = xp == 0 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + y : tix(x0, y) - 1;
+    const int rofs = xp == 3 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + 8 + y : tix(x0, y) + 2;
 
     // ---- chunk stream: kBatch-chunk claims from one counter ----
     int* ctr = M.counter;
@@ -429,17 +451,20 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     int dv0, dv1;
     load_ctx(M, c_ld, lane, lm0, dv0);
     ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
+    const int t0 = tix(x0, y);
+    LoadCtx Lld = make_load_ctx(c_ld, lm0, dv0, M, y, xp, x0);
     int c_nx = next_id();
     load_ctx(M, c_nx, lane, lm1, dv1);
     int p_ld = -1;  // next plane of Cld to issue (-1..8)
     int L = 0;      // loads issued
     auto issue_next = [&]() {
-        if (Cld.c >= 0) issue_plane(ring[L & (kRing - 1)], M, Cld, p_ld, y, xp, x0);
+        if (Lld.c >= 0) issue_plane(ring[L & (kRing - 1)], M, Lld, p_ld, y, xp, t0);
         cp_commit();
         ++L;
         if (++p_ld == 9) {  // advance the load side to the next chunk
             p_ld = -1;
             Cld = make_ctx(c_nx, lm1, dv1);
+            Lld = make_load_ctx(c_nx, lm1, dv1, M, y, xp, x0);
             c_nx = Cld.c >= 0 ? next_id() : -1;
             load_ctx(M, c_nx, lane, lm1, dv1);
         }
@@ -459,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
             __syncwarp();
             compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
                                     ring[(base + z + 1) & (kRing - 1)],
-                                    ring[(base + z + 2) & (kRing - 1)], lane);
+                                    ring[(base + z + 2) & (kRing - 1)], y, xp, x0, t0, lofs, rofs);
             __syncwarp();
             issue_next();
             if (z == 7) {  // planes 8 of this chunk and -1 of the next
@@ -576,6 +601,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     if (g->cc[0] > 1024 || g->cc[1] > 1024 || g->cc[2] > 1024) return;  // key packing limit
     const int64_t n_all = g->n_chunks;
     if (n_all == 0 || end <= begin) return;
+    if (n_all * 512 >= (int64_t)0xFFFFFFFF) return;  // 32-bit slot offsets (>16 GB per column)
     PD_CUDA(cudaMalloc(&plan->d_desc, sizeof(int32_t) * 8 * (size_t)n_all));
     desc_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(
         d_nbr, g->d_keys, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
