@@ -1,0 +1,3 @@
+#include <gtest/gtest.h>
+
+int main(int argc, char** argv) { return testing::RunAllTests(argc, argv); }
