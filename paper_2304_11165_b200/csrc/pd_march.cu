@@ -186,6 +186,7 @@ struct LoadCtx {
     uint32_t yoff;  // y-halo pair of plane 0 (face lanes)
 };
 
+template <int XD>
 __device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, const MarchArgs& M, int y,
                                                  int xp, int x0) {
     int nb[6];
@@ -200,8 +201,12 @@ __device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, con
     L.zlo = (zk && nb[4] >= 0) ? (uint32_t)nb[4] * 512u + 448u + bp : kNone;
     L.zhi = (zk && nb[5] >= 0) ? (uint32_t)nb[5] * 512u + bp : kNone;
     const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? nb[0] : nb[1]);
-    L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? ((uint32_t)jx * 2u + (xp == 0 ? 1u : 0u)) * 64u + (uint32_t)y
-                                               : kNone;
+    if (XD)  // x halo straight from the neighbour's slab (x = 7 / x = 0 column)
+        L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? (uint32_t)jx * 512u + (uint32_t)y * 8u + (xp == 0 ? 7u : 0u)
+                                                   : kNone;
+    else
+        L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? ((uint32_t)jx * 2u + (xp == 0 ? 1u : 0u)) * 64u + (uint32_t)y
+                                                   : kNone;
     const int jy = (M.dbg & 2) ? -1 : (y == 0 ? nb[2] : nb[3]);
     L.yoff = ((y == 0 || y == 7) && jy >= 0) ? (uint32_t)jy * 512u + (y == 0 ? 56u : 0u) + (uint32_t)x0 : kNone;
     return L;
@@ -211,6 +216,7 @@ __device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, con
 // copies of its node pair (pairs with no active node are never read; their
 // D_eff cells get the sentinel) and, for chunk-face lanes, the x / y halo
 // cells. p = -1 / 8 are the z halo planes of the z neighbours.
+template <int XD>
 __device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const LoadCtx& L, int p,
                                             int y, int xp, int t0) {
     const double sv = sent();
@@ -225,9 +231,9 @@ __device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const L
     const bool xl = xp == 0 || xp == 3, yl = y == 0 || y == 7;
     const int side = xp == 0 ? 0 : 1;
     const bool xok = L.c >= 0 && L.xoff != kNone;
-    const uint32_t ox = xok ? L.xoff + (uint32_t)p * 8u : 0u;
-    cp8_if(&T.hxu[side][y], M.xfu + ox, xok);
-    cp8_if(&T.hxd[side][y], M.xfd + ox, xok);
+    const uint32_t ox = xok ? L.xoff + (uint32_t)p * (XD ? 64u : 8u) : 0u;
+    cp8_if(&T.hxu[side][y], (XD ? M.A.u : M.xfu) + ox, xok);
+    cp8_if(&T.hxd[side][y], (XD ? M.deff : M.xfd) + ox, xok);
     if (xl && !xok) T.hxd[side][y] = sv;
     const bool yok = L.c >= 0 && L.yoff != kNone;
     const int ty = y == 0 ? t0 - 8 : t0 + 8;
@@ -242,7 +248,7 @@ __device__ __forceinline__ bool huge(double x) {
     return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
 }
 
-template <int REACTION>
+template <int REACTION, int XD>
 __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
                                               const ChunkCtx& C, int z, const Tile& Tm,
                                               const Tile& T0, const Tile& Tp, int y, int xp, int x0,
@@ -368,6 +374,7 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
         if (a1) dst[1] = out1;
     }
     // x-face side planes of u_next for the next step's x halos
+    if (XD) return;
     if (xp == 0 && a0) M.xfun[((int64_t)c * 2 + 0) * 64 + z * 8 + y] = out0;
     if (xp == 3 && a1) M.xfun[((int64_t)c * 2 + 1) * 64 + z * 8 + y] = out1;
 }
@@ -393,7 +400,7 @@ __device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
 // z-halo below, the 8 body planes, z-halo above) form one continuous
 // sequence through a kRing-slot tile ring, kAhead loads ahead of the plane
 // being computed, across chunk boundaries.
-template <int REACTION, int OCC>
+template <int REACTION, int OCC, int XD>
 __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SlowConsts K;
@@ -452,19 +459,19 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     load_ctx(M, c_ld, lane, lm0, dv0);
     ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
     const int t0 = tix(x0, y);
-    LoadCtx Lld = make_load_ctx(c_ld, lm0, dv0, M, y, xp, x0);
+    LoadCtx Lld = make_load_ctx<XD>(c_ld, lm0, dv0, M, y, xp, x0);
     int c_nx = next_id();
     load_ctx(M, c_nx, lane, lm1, dv1);
     int p_ld = -1;  // next plane of Cld to issue (-1..8)
     int L = 0;      // loads issued
     auto issue_next = [&]() {
-        if (Lld.c >= 0) issue_plane(ring[L & (kRing - 1)], M, Lld, p_ld, y, xp, t0);
+        if (Lld.c >= 0) issue_plane<XD>(ring[L & (kRing - 1)], M, Lld, p_ld, y, xp, t0);
         cp_commit();
         ++L;
         if (++p_ld == 9) {  // advance the load side to the next chunk
             p_ld = -1;
             Cld = make_ctx(c_nx, lm1, dv1);
-            Lld = make_load_ctx(c_nx, lm1, dv1, M, y, xp, x0);
+            Lld = make_load_ctx<XD>(c_nx, lm1, dv1, M, y, xp, x0);
             c_nx = Cld.c >= 0 ? next_id() : -1;
             load_ctx(M, c_nx, lane, lm1, dv1);
         }
@@ -482,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
             // are in flight at this point of every iteration
             cp_wait<kAhead>();
             __syncwarp();
-            compute_plane<REACTION>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
+            compute_plane<REACTION, XD>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
                                     ring[(base + z + 1) & (kRing - 1)],
                                     ring[(base + z + 2) & (kRing - 1)], y, xp, x0, t0, lofs, rofs);
             __syncwarp();
@@ -692,26 +699,25 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const bool occ3 = p.grid == sms * 3;
     const size_t bytes = sizeof(Tile) * kRing * kWarps;
+    static const int xd = [] {
+        const char* e = getenv("PD_MARCH_XSIDE");
+        return (e && atoi(e) == 1) ? 0 : 1;
+    }();
+    using KernT = void (*)(MarchArgs);
+    static const KernT table[2][2][3] = {
+        {{ftcs_march_kernel<0, kCtasPerSm, 0>, ftcs_march_kernel<1, kCtasPerSm, 0>, ftcs_march_kernel<2, kCtasPerSm, 0>},
+         {ftcs_march_kernel<0, 3, 0>, ftcs_march_kernel<1, 3, 0>, ftcs_march_kernel<2, 3, 0>}},
+        {{ftcs_march_kernel<0, kCtasPerSm, 1>, ftcs_march_kernel<1, kCtasPerSm, 1>, ftcs_march_kernel<2, kCtasPerSm, 1>},
+         {ftcs_march_kernel<0, 3, 1>, ftcs_march_kernel<1, 3, 1>, ftcs_march_kernel<2, 3, 1>}}};
     static bool attr_set = false;
     if (!attr_set) {
-        void (*kerns[])(MarchArgs) = {ftcs_march_kernel<0, 3>, ftcs_march_kernel<1, 3>, ftcs_march_kernel<2, 3>,
-                                      ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
-                                      ftcs_march_kernel<2, kCtasPerSm>};
-        for (auto k : kerns)
-            PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        for (auto& a : table)
+            for (auto& b : a)
+                for (auto k : b) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         attr_set = true;
     }
-    auto go = [&](void (*kern)(MarchArgs)) { kern<<<p.grid, kThreads, bytes, g->stream>>>(M); };
-    if (reaction == PD_REACTION_SURFACE_SINK) {
-        if (occ3) go(ftcs_march_kernel<1, 3>);
-        else go(ftcs_march_kernel<1, kCtasPerSm>);
-    } else if (reaction == PD_REACTION_VOLUMETRIC) {
-        if (occ3) go(ftcs_march_kernel<2, 3>);
-        else go(ftcs_march_kernel<2, kCtasPerSm>);
-    } else {
-        if (occ3) go(ftcs_march_kernel<0, 3>);
-        else go(ftcs_march_kernel<0, kCtasPerSm>);
-    }
+    const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
+    table[xd][occ3 ? 1 : 0][r]<<<p.grid, kThreads, bytes, g->stream>>>(M);
     PD_CUDA(cudaGetLastError());
     p.cur = 1 - p.cur;
 }
