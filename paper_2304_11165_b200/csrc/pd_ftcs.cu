@@ -301,8 +301,6 @@ struct pd_stepper {
     int64_t begin = 0, end = 0;  // owned ordinal range
     pdb::MarchPlan plan;         // 3-D FP64 column-march fast path
     bool use_march = true;
-    bool xf_valid = false;       // plan.d_xf[plan.cur] mirrors the current u
-    uint64_t xf_gen = 0;         // grid generation the side planes were taken at
 };
 
 namespace {
@@ -387,14 +385,8 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         a.k = k;
         a.ord0 = s->begin;
         if (!diag && s->use_march && s->plan.ready) {
-            if (!s->xf_valid || s->xf_gen != g->generation) {
-                march_extract_xfaces(g, s->plan, u);
-                s->xf_valid = true;
-                s->xf_gen = g->generation;
-            }
             march_launch(g, s->plan, a, s->cfg.reaction_kind);
         } else if (g->dims == 3) {
-            s->xf_valid = false;
             if (diag) ftcs_step_kernel<double, 3, true><<<nb, 512, 0, g->stream>>>(a);
             else ftcs_step_kernel<double, 3, false><<<nb, 512, 0, g->stream>>>(a);
         } else {
@@ -652,7 +644,6 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                 continue;
             }
             const int code = hflags[(size_t)fail_k];
-            s->xf_valid = false;
             const int64_t st = step0 + j + fail_k;
             // undo the swaps of the steps that did not complete: the failing
             // step itself is undone only for a non-finite node (the reference

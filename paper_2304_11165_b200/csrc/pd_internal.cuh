@@ -134,12 +134,9 @@ struct MarchPlan {
     int32_t* d_stream = nullptr;   // owned chunk ordinals in schedule order
     int32_t* d_desc = nullptr;     // 8 ints per chunk: nbr[0..5], packed key, flags
     double* d_deff = nullptr;      // D on fluid nodes, -inf elsewhere (static per run)
-    double* d_xfd = nullptr;       // x=0 / x=7 planes of D_eff [c][2][64]
-    double* d_xf[2] = {nullptr, nullptr};  // x planes of u / u_next (double-buffered)
     int* d_counter = nullptr;      // per-step dynamic batch counters
     uint32_t* d_lm = nullptr;      // per chunk and lane: active / sink bits [c][32]
     int grid = 0;
-    int cur = 0;                   // d_xf[cur] mirrors the current u
     int64_t n = 0;
     bool ready = false;
 };
@@ -147,7 +144,6 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
                  const void* d_dcol, int dirichlet, int64_t begin, int64_t end, MarchPlan* plan);
 int march_counters_per_step();
 void march_free(MarchPlan* plan);
-void march_extract_xfaces(pd_grid* g, MarchPlan& plan, const void* col);
 void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction);
 
 struct DeviceGuard {

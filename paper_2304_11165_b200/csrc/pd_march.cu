@@ -50,9 +50,7 @@ namespace pdb {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kCtasPerSm = 4;  // default occupancy (PD_MARCH_OCC=3 selects 3)
-constexpr int kBatch = 1;  // one chunk per claim: neighbours in the schedule run close in time
-constexpr int kParts = 1;
+constexpr int kCtasPerSm = 3;  // 3 x 4 warps x 10 slots x 1.5 KB = 180 KB of ring per SM
 constexpr int kSeg = 16;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
@@ -72,10 +70,7 @@ struct MarchArgs {
     const int32_t* __restrict__ desc;  // 8 ints per chunk: nbr[6], key, flags
     const uint32_t* __restrict__ lm;   // per chunk and lane: active / sink bits
     const double* __restrict__ deff;
-    const double* __restrict__ xfu;  // x-face planes of u       [c][side][64]
-    const double* __restrict__ xfd;  // x-face planes of D_eff   [c][side][64]
-    double* __restrict__ xfun;       // x-face planes of u_next (written)
-    int* counter;                    // kParts counters of this step
+    int* counter;                    // chunk-claim counter of this step
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
 };
 
@@ -136,111 +131,147 @@ __device__ __forceinline__ double fface(double da, double db, double ua, double 
     return ((da + db) * 0.5) * (ub - ua);
 }
 
-struct ChunkCtx {  // what the compute side needs of a chunk
-    int c, key, flags;
-    uint32_t lm;
-};
-
-// Per-warp ring of plane tiles in shared memory. A tile holds u and D_eff of
-// one z-plane of a chunk: rows y = -1..8 of the 8 body columns (pitch 8, so
-// the lanes' 16-B pair accesses are bank-conflict free) and the x- / x+ halo
-// cells of rows 0..7 in two side columns.
-constexpr int kRing = 8;   // power of two: slot = load index & 7
-constexpr int kAhead = 5;  // kRing - 3 (planes z-1, z, z+1 resident)
+// One plane tile: u and D_eff of one z-plane of a chunk, rows y = -1..8 of
+// the 8 body columns (pitch 8: the lanes' 16-B pair accesses are bank-conflict
+// free) and the x- / x+ halo cells of rows 0..7 in two side columns.
 struct Tile {
     double u[80], hxu[2][8];
     double d[80], hxd[2][8];
 };
-__device__ __forceinline__ int tix(int x, int y) { return x + 8 * (y + 1); }
+constexpr uint32_t kTileBytes = sizeof(Tile);                  // 1536
+constexpr uint32_t kDOff = (uint32_t)offsetof(Tile, d);        // u -> D_eff distance (bytes)
+constexpr uint32_t kHxOff = (uint32_t)offsetof(Tile, hxu);     // x-halo column (bytes)
+// Fixed-slot ring: load i (0..9) of every chunk goes to slot i (i = 0: the
+// z- halo plane, 1..8: body planes 0..7, 9: the z+ halo plane), so every
+// shared-memory address in the unrolled chunk body is a lane base + constant.
+constexpr int kSlots = 10;
 
-__device__ __forceinline__ void cp16_if(void* smem, const void* gmem, bool pred) {
+// ---- predicated asynchronous copies (LDGSTS), one predicate per pair ----
+__device__ __forceinline__ void cp16x2(uint32_t su, const double* gu, uint32_t sd, const double* gd,
+                                       bool pred) {
     asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
-        " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(
-            (unsigned)__cvta_generic_to_shared(smem)),
-        "l"(gmem), "r"((int)pred));
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " @p cp.async.cg.shared.global [%0], [%1], 16;\n"
+        " @p cp.async.cg.shared.global [%2], [%3], 16;\n}\n" ::"r"(su),
+        "l"(gu), "r"(sd), "l"(gd), "r"((int)pred));
 }
-__device__ __forceinline__ void cp8_if(void* smem, const void* gmem, bool pred) {
+__device__ __forceinline__ void cp8x2(uint32_t su, const double* gu, uint32_t sd, const double* gd,
+                                      bool pred) {
     asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
-        " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(
-            (unsigned)__cvta_generic_to_shared(smem)),
-        "l"(gmem), "r"((int)pred));
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " @p cp.async.ca.shared.global [%0], [%1], 8;\n"
+        " @p cp.async.ca.shared.global [%2], [%3], 8;\n}\n" ::"r"(su),
+        "l"(gu), "r"(sd), "l"(gd), "r"((int)pred));
+}
+__device__ __forceinline__ void sts_sent1(uint32_t sa, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n"
+        " @p st.shared.v2.u32 [%0], {%2, %3};\n}\n" ::"r"(sa),
+        "r"((int)pred), "r"(0u), "r"(kSentHi));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Lane-specific source offsets (elements, 32-bit: u holds < 2^32 slots, see
-// march_build) of one chunk, computed once per chunk on the load side.
-constexpr uint32_t kNone = 0xFFFFFFFFu;
+// Load side of one chunk, per lane: global sources of everything the lane
+// copies (plane 0; plane p adds p*64 elements) and their predicates.
 struct LoadCtx {
-    int c;
-    uint32_t lm;
-    uint32_t own;   // the lane's pair in plane 0
-    uint32_t zlo;   // pair in the z- neighbour's plane 7
-    uint32_t zhi;   // pair in the z+ neighbour's plane 0
-    uint32_t xoff;  // x-halo cell of plane 0 in the side planes (face lanes)
-    uint32_t yoff;  // y-halo pair of plane 0 (face lanes)
+    const double *gu, *gd;    // own pair
+    const double *zlu, *zld;  // pair in the z- neighbour's plane 7
+    const double *zhu, *zhd;  // pair in the z+ neighbour's plane 0
+    const double *xu, *xd;    // x-halo cell (x-face lanes)
+    const double *yu, *yd;    // y-halo pair (y-face lanes)
+    uint32_t lm;              // active bits of the lane's pair (0 if no chunk)
+    bool zlok, zhok, xok, yok;
 };
 
-template <int XD>
-__device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, const MarchArgs& M, int y,
-                                                 int xp, int x0) {
+// Per-lane constants of the tile geometry (byte offsets inside a tile).
+struct LaneGeo {
+    int y, xp;
+    bool xface, yface;
+    uint32_t s_c;   // own pair
+    uint32_t s_l;   // left neighbour cell (x-halo column for xp = 0)
+    uint32_t s_r;   // right neighbour cell (x-halo column for xp = 3)
+    uint32_t s_hx;  // x-halo cell this lane fills (x-face lanes)
+    uint32_t s_hy;  // y-halo pair this lane fills (y-face lanes)
+    uint32_t bp;    // own pair offset inside plane 0 (elements)
+};
+
+__device__ __forceinline__ LaneGeo lane_geo(int lane) {
+    LaneGeo G;
+    G.y = lane >> 2;
+    G.xp = lane & 3;
+    const int x0 = 2 * G.xp;
+    G.xface = G.xp == 0 || G.xp == 3;
+    G.yface = G.y == 0 || G.y == 7;
+    G.s_c = (uint32_t)(x0 + 8 * (G.y + 1)) * 8u;
+    G.s_l = G.xp == 0 ? kHxOff + (uint32_t)G.y * 8u : G.s_c - 8u;
+    G.s_r = G.xp == 3 ? kHxOff + (uint32_t)(8 + G.y) * 8u : G.s_c + 16u;
+    G.s_hx = kHxOff + (uint32_t)((G.xp == 3 ? 8 : 0) + G.y) * 8u;
+    G.s_hy = G.y == 0 ? G.s_c - 64u : G.s_c + 64u;
+    G.bp = (uint32_t)(G.y * 8 + x0);
+    return G;
+}
+
+// nb[] comes from lanes 24..29 of the descriptor word dv.
+__device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, const MarchArgs& M,
+                                                 const LaneGeo& G) {
     int nb[6];
 #pragma unroll
     for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
     LoadCtx L;
-    L.c = c;
-    L.lm = lm;
-    const uint32_t bp = (uint32_t)(y * 8 + x0);
-    L.own = (uint32_t)(c < 0 ? 0 : c) * 512u + bp;
-    const bool zk = !(M.dbg & 4);
-    L.zlo = (zk && nb[4] >= 0) ? (uint32_t)nb[4] * 512u + 448u + bp : kNone;
-    L.zhi = (zk && nb[5] >= 0) ? (uint32_t)nb[5] * 512u + bp : kNone;
-    const int jx = (M.dbg & 1) ? -1 : (xp == 0 ? nb[0] : nb[1]);
-    if (XD)  // x halo straight from the neighbour's slab (x = 7 / x = 0 column)
-        L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? (uint32_t)jx * 512u + (uint32_t)y * 8u + (xp == 0 ? 7u : 0u)
-                                                   : kNone;
-    else
-        L.xoff = ((xp == 0 || xp == 3) && jx >= 0) ? ((uint32_t)jx * 2u + (xp == 0 ? 1u : 0u)) * 64u + (uint32_t)y
-                                                   : kNone;
-    const int jy = (M.dbg & 2) ? -1 : (y == 0 ? nb[2] : nb[3]);
-    L.yoff = ((y == 0 || y == 7) && jy >= 0) ? (uint32_t)jy * 512u + (y == 0 ? 56u : 0u) + (uint32_t)x0 : kNone;
+    const double* u = M.A.u;
+    const double* de = M.deff;
+    const bool ok = c >= 0;
+    const int64_t own = ok ? (int64_t)c * 512 + G.bp : 0;
+    L.gu = u + own;
+    L.gd = de + own;
+    L.lm = ok ? lm : 0u;
+    L.zlok = ok && nb[4] >= 0 && !(M.dbg & 4);
+    L.zhok = ok && nb[5] >= 0 && !(M.dbg & 4);
+    const int64_t zl = L.zlok ? (int64_t)nb[4] * 512 + 448 + G.bp : 0;
+    const int64_t zh = L.zhok ? (int64_t)nb[5] * 512 + G.bp : 0;
+    L.zlu = u + zl;
+    L.zld = de + zl;
+    L.zhu = u + zh;
+    L.zhd = de + zh;
+    const int jx = G.xp == 0 ? nb[0] : nb[1];
+    L.xok = ok && G.xface && jx >= 0 && !(M.dbg & 1);
+    const int64_t xo = L.xok ? (int64_t)jx * 512 + G.y * 8 + (G.xp == 0 ? 7 : 0) : 0;
+    L.xu = u + xo;
+    L.xd = de + xo;
+    const int jy = G.y == 0 ? nb[2] : nb[3];
+    L.yok = ok && G.yface && jy >= 0 && !(M.dbg & 2);
+    const int64_t yo = L.yok ? (int64_t)jy * 512 + (G.y == 0 ? 56 : 0) + 2 * G.xp : 0;
+    L.yu = u + yo;
+    L.yd = de + yo;
     return L;
 }
 
-// Issues the lane's share of plane p (-1..8) into tile T: predicated 16-B
-// copies of its node pair (pairs with no active node are never read; their
-// D_eff cells get the sentinel) and, for chunk-face lanes, the x / y halo
-// cells. p = -1 / 8 are the z halo planes of the z neighbours.
-template <int XD>
-__device__ __forceinline__ void issue_plane(Tile& T, const MarchArgs& M, const LoadCtx& L, int p,
-                                            int y, int xp, int t0) {
-    const double sv = sent();
-    const bool body = (unsigned)p <= 7u;
-    const uint32_t o = body ? L.own + (uint32_t)p * 64u : (p < 0 ? L.zlo : L.zhi);
-    const bool ok = L.c >= 0 && (body ? ((L.lm >> (2 * p)) & 3u) != 0 : o != kNone);
-    const uint32_t oo = ok ? o : 0u;
-    cp16_if(&T.u[t0], M.A.u + oo, ok);
-    cp16_if(&T.d[t0], M.deff + oo, ok);
-    if (!ok) *reinterpret_cast<double2*>(&T.d[t0]) = make_double2(sv, sv);
-    if (!body) return;  // warp-uniform
-    const bool xl = xp == 0 || xp == 3, yl = y == 0 || y == 7;
-    const int side = xp == 0 ? 0 : 1;
-    const bool xok = L.c >= 0 && L.xoff != kNone;
-    const uint32_t ox = xok ? L.xoff + (uint32_t)p * (XD ? 64u : 8u) : 0u;
-    cp8_if(&T.hxu[side][y], (XD ? M.A.u : M.xfu) + ox, xok);
-    cp8_if(&T.hxd[side][y], (XD ? M.deff : M.xfd) + ox, xok);
-    if (xl && !xok) T.hxd[side][y] = sv;
-    const bool yok = L.c >= 0 && L.yoff != kNone;
-    const int ty = y == 0 ? t0 - 8 : t0 + 8;
-    const uint32_t oy = yok ? L.yoff + (uint32_t)p * 64u : 0u;
-    cp16_if(&T.u[ty], M.A.u + oy, yok);
-    cp16_if(&T.d[ty], M.deff + oy, yok);
-    if (yl && !yok) *reinterpret_cast<double2*>(&T.d[ty]) = make_double2(sv, sv);
+// Issues load i (0..9) of a chunk into ring slot i (slot base address sb).
+// Pairs without an active node are never read (their D_eff cells get the
+// sentinel), so empty 32-B sectors cost no HBM traffic.
+template <int I>
+__device__ __forceinline__ void issue_load(uint32_t sb, const LoadCtx& L, const LaneGeo& G) {
+    const uint32_t st = sb + (uint32_t)I * kTileBytes;
+    if (I == 0) {
+        cp16x2(st + G.s_c, L.zlu, st + kDOff + G.s_c, L.zld, L.zlok);
+        sts_sent1(st + kDOff + G.s_c, !L.zlok), sts_sent1(st + kDOff + G.s_c + 8, !L.zlok);
+    } else if (I == 9) {
+        cp16x2(st + G.s_c, L.zhu, st + kDOff + G.s_c, L.zhd, L.zhok);
+        sts_sent1(st + kDOff + G.s_c, !L.zhok), sts_sent1(st + kDOff + G.s_c + 8, !L.zhok);
+    } else {
+        constexpr int p = I - 1;
+        const bool ok = ((L.lm >> (2 * p)) & 3u) != 0u;
+        cp16x2(st + G.s_c, L.gu + p * 64, st + kDOff + G.s_c, L.gd + p * 64, ok);
+        sts_sent1(st + kDOff + G.s_c, !ok), sts_sent1(st + kDOff + G.s_c + 8, !ok);
+        cp8x2(st + G.s_hx, L.xu + p * 64, st + kDOff + G.s_hx, L.xd + p * 64, L.xok);
+        sts_sent1(st + kDOff + G.s_hx, G.xface && !L.xok);
+        cp16x2(st + G.s_hy, L.yu + p * 64, st + kDOff + G.s_hy, L.yd + p * 64, L.yok);
+        sts_sent1(st + kDOff + G.s_hy, G.yface && !L.yok), sts_sent1(st + kDOff + G.s_hy + 8, G.yface && !L.yok);
+    }
 }
 
 // |x| >= 2^990 or non-finite, from the high word (integer pipe)
@@ -248,135 +279,172 @@ __device__ __forceinline__ bool huge(double x) {
     return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
 }
 
-template <int REACTION, int XD>
-__device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K,
-                                              const ChunkCtx& C, int z, const Tile& Tm,
-                                              const Tile& T0, const Tile& Tp, int y, int xp, int x0,
-                                              int t0, int lofs, int rofs) {
+struct Consts {
+    double dt, neg_k, src_factor, ix, iy, iz;
+};
+
+struct ChunkCtx {  // compute side of a chunk
+    int c, key, flags;
+    uint32_t lm;
+    double* out;  // u_next + c*512 + bp
+};
+
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds1(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+    return v;
+}
+
+// Rare-path handling of a node pair whose fast result is huge / non-finite,
+// and the Dirichlet-exposed chunks: exact generic update (slow_node) on the
+// staged values, then the reference's non-finite / total-mass flags
+// (solver.hpp:444, 250-260, 514-515).
+template <int REACTION>
+__device__ __noinline__ double2 pair_slow(const MarchArgs& M, const SlowConsts& K, const ChunkCtx& C, int z,
+                                          int xp, int y, const double* nu0, const double* nd0,
+                                          const double* nu1, const double* nd1, double uc0, double uc1,
+                                          double dc0, double dc1, bool s0, bool s1, double src0,
+                                          double src1, double out0, double out1) {
+    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;
+    const int x0 = 2 * xp;
+    const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
+    const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
     const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
-    if (!(a0 | a1)) return;
-    const double2 uc = *reinterpret_cast<const double2*>(&T0.u[t0]);
-    const double2 dc = *reinterpret_cast<const double2*>(&T0.d[t0]);
-    constexpr int kD = (int)(offsetof(Tile, d) / sizeof(double));  // u -> d distance
-    const double uL = T0.u[lofs], dL = T0.u[lofs + kD];
-    const double uR = T0.u[rofs], dR = T0.u[rofs + kD];
-    const double2 uym = *reinterpret_cast<const double2*>(&T0.u[t0 - 8]);
-    const double2 dym = *reinterpret_cast<const double2*>(&T0.d[t0 - 8]);
-    const double2 uyp = *reinterpret_cast<const double2*>(&T0.u[t0 + 8]);
-    const double2 dyp = *reinterpret_cast<const double2*>(&T0.d[t0 + 8]);
-    const double2 uzm = *reinterpret_cast<const double2*>(&Tm.u[t0]);
-    const double2 dzm = *reinterpret_cast<const double2*>(&Tm.d[t0]);
-    const double2 uzp = *reinterpret_cast<const double2*>(&Tp.u[t0]);
-    const double2 dzp = *reinterpret_cast<const double2*>(&Tp.d[t0]);
-    const StepArgs<double>& A = M.A;
-    const int o = z * 64 + y * 8 + x0;
-    const int c = C.c;
-    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
-    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
+    bool h0, h1;
+    if (dirichlet) {  // the whole chunk takes the exact generic update
+        if (!sentinel(dc0)) out0 = slow_node<REACTION>(K, uc0, dc0, nu0, nd0, gx, gy, gz, s0, src0);
+        if (!sentinel(dc1)) out1 = slow_node<REACTION>(K, uc1, dc1, nu1, nd1, gx + 1, gy, gz, s1, src1);
+        h0 = a0 && huge(out0);
+        h1 = a1 && huge(out1);
+    } else {  // a huge fast result: re-derive the non-finite ones exactly
+        h0 = a0 && huge(out0);
+        h1 = a1 && huge(out1);
+        if (h0 && !isfinite(out0) && !sentinel(dc0))
+            out0 = slow_node<REACTION>(K, uc0, dc0, nu0, nd0, gx, gy, gz, s0, src0);
+        if (h1 && !isfinite(out1) && !sentinel(dc1))
+            out1 = slow_node<REACTION>(K, uc1, dc1, nu1, nd1, gx + 1, gy, gz, s1, src1);
+    }
+    if (h0 | h1) {
+        const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
+        const int o = z * 64 + y * 8 + x0;
+        if (bad0 | bad1) {
+            atomicMin(M.A.bad_key, ((unsigned long long)C.c << 10) | (unsigned long long)(o + (bad0 ? 0 : 1)));
+            atomicOr(&M.A.flags[M.A.k], 1);
+        } else {
+            atomicOr(&M.A.flags[M.A.k], 2);
+        }
+    }
+    return make_double2(out0, out1);
+}
+
+// u_next stores: streaming (evict-first) — the values are next read one
+// step later, long after they would have left L2.
+__device__ __forceinline__ void stg_pair(double* p, double a, double b, bool a0, bool a1) {
+    asm volatile(
+        "{\n .reg .pred p, q, r;\n setp.ne.b32 p, %3, 0;\n setp.ne.b32 q, %4, 0;\n"
+        " and.pred r, p, q;\n"
+        " @r st.global.cs.v2.f64 [%0], {%1, %2};\n"
+        " xor.pred p, p, r;\n xor.pred q, q, r;\n"
+        " @p st.global.cs.f64 [%0], %1;\n"
+        " @q st.global.cs.f64 [%0+8], %2;\n}\n" ::"l"(p),
+        "d"(a), "d"(b), "r"((int)a0), "r"((int)a1)
+        : "memory");
+}
+
+// Computes plane Z of chunk C from ring slots Z (z-1), Z+1 (z), Z+2 (z+1)
+// and stores the active nodes of the lane's pair into u_next.
+template <int REACTION, int Z>
+__device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
+                                              const ChunkCtx& C, uint32_t sb, const LaneGeo& G) {
+    const bool a0 = (C.lm >> (2 * Z)) & 1u, a1 = (C.lm >> (2 * Z + 1)) & 1u;
+    const uint32_t t0 = sb + (uint32_t)(Z + 1) * kTileBytes;
+    const uint32_t tm = sb + (uint32_t)Z * kTileBytes;
+    const uint32_t tp = sb + (uint32_t)(Z + 2) * kTileBytes;
+    const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
+    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
+    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
+    const double2 uym = lds2(t0 + G.s_c - 64), dym = lds2(t0 + kDOff + G.s_c - 64);
+    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = lds2(t0 + kDOff + G.s_c + 64);
+    const double2 uzm = lds2(tm + G.s_c), dzm = lds2(tm + kDOff + G.s_c);
+    const double2 uzp = lds2(tp + G.s_c), dzp = lds2(tp + kDOff + G.s_c);
+    // lanes without an active node compute too (results are not stored):
+    // no divergence in the plane body
+    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * Z)) & 1u);
+    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * Z)) & 1u);
     double src0 = 0.0, src1 = 0.0;
     if (REACTION == PD_REACTION_VOLUMETRIC) {
-        src0 = A.src[(int64_t)c * 512 + o];
-        src1 = A.src[(int64_t)c * 512 + o + 1];
+        const double* sp = M.A.src + (int64_t)C.c * 512 + Z * 64 + G.bp;
+        src0 = sp[0];
+        src1 = sp[1];
     }
-    const double ix = K.inv_dx2[0], iy = K.inv_dx2[1], iz = K.inv_dx2[2];
-    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
-    double out0, out1;
-    if (!dirichlet) {
-        double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
-        if ((C.flags >> (8 + z)) & 1) {
-            // interior-fluid plane (warp-uniform): no substitution anywhere
-            fxl = fface(dL, dc.x, uL, uc.x);
-            fxi = fface(dc.x, dc.y, uc.x, uc.y);
-            fxr = fface(dc.y, dR, uc.y, uR);
-            fy0m = fface(dym.x, dc.x, uym.x, uc.x);
-            fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
-            fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
-            fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
-            fy1m = fface(dym.y, dc.y, uym.y, uc.y);
-            fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
-            fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
-            fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
-        } else {
-            fxl = face(dL, dc.x, uL, uc.x);
-            fxi = face(dc.x, dc.y, uc.x, uc.y);
-            fxr = face(dc.y, dR, uc.y, uR);
-            fy0m = face(dym.x, dc.x, uym.x, uc.x);
-            fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
-            fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
-            fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
-            fy1m = face(dym.y, dc.y, uym.y, uc.y);
-            fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
-            fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
-            fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
-        }
-        double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
-        lap0 += (fxi - fxl) * ix;
-        lap0 += (fy0p - fy0m) * iy;
-        lap0 += (fz0p - fz0m) * iz;
-        double lap1 = 0.0;
-        lap1 += (fxr - fxi) * ix;
-        lap1 += (fy1p - fy1m) * iy;
-        lap1 += (fz1p - fz1m) * iz;
-        double r0 = 0.0, r1 = 0.0;
-        if (REACTION == PD_REACTION_SURFACE_SINK) {
-            if (s0) r0 = K.neg_k * uc.x;
-            if (s1) r1 = K.neg_k * uc.y;
-        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-            r0 = src0 * K.src_factor;
-            r1 = src1 * K.src_factor;
-        }
-        out0 = uc.x + K.dt * lap0 + K.dt * r0;
-        out1 = uc.y + K.dt * lap1 + K.dt * r1;
+    double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
+    if ((C.flags >> (8 + Z)) & 1) {
+        // interior-fluid plane (warp-uniform): no substitution anywhere
+        fxl = fface(dL, dc.x, uL, uc.x);
+        fxi = fface(dc.x, dc.y, uc.x, uc.y);
+        fxr = fface(dc.y, dR, uc.y, uR);
+        fy0m = fface(dym.x, dc.x, uym.x, uc.x);
+        fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = fface(dym.y, dc.y, uym.y, uc.y);
+        fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
     } else {
-        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
-        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-        const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
-        const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-        out0 = slow_node<REACTION>(K, uc.x, dc.x, nu0, nd0, gx, gy, gz, s0, src0);
-        const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
-        const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-        out1 = slow_node<REACTION>(K, uc.y, dc.y, nu1, nd1, gx + 1, gy, gz, s1, src1);
+        fxl = face(dL, dc.x, uL, uc.x);
+        fxi = face(dc.x, dc.y, uc.x, uc.y);
+        fxr = face(dc.y, dR, uc.y, uR);
+        fy0m = face(dym.x, dc.x, uym.x, uc.x);
+        fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = face(dym.y, dc.y, uym.y, uc.y);
+        fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
     }
+    double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
+    lap0 += (fxi - fxl) * Q.ix;
+    lap0 += (fy0p - fy0m) * Q.iy;
+    lap0 += (fz0p - fz0m) * Q.iz;
+    double lap1 = 0.0;
+    lap1 += (fxr - fxi) * Q.ix;
+    lap1 += (fy1p - fy1m) * Q.iy;
+    lap1 += (fz1p - fz1m) * Q.iz;
+    double r0 = 0.0, r1 = 0.0;
+    if (REACTION == PD_REACTION_SURFACE_SINK) {
+        r0 = s0 ? Q.neg_k * uc.x : 0.0;
+        r1 = s1 ? Q.neg_k * uc.y : 0.0;
+    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+        r0 = src0 * Q.src_factor;
+        r1 = src1 * Q.src_factor;
+    }
+    double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
+    double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
     // walls (active, not fluid) stay frozen (solver.hpp:413-417)
     if (sentinel(dc.x)) out0 = uc.x;
     if (sentinel(dc.y)) out1 = uc.y;
-    const bool h0 = a0 && huge(out0), h1 = a1 && huge(out1);
-    if (h0 | h1) {
-        // rare: a non-finite fast-path result is re-derived exactly (the
-        // +-0 substitution shortcut needs finite operands), then the
-        // reference's non-finite / total-mass checks are flagged
-        // (solver.hpp:444, 250-260, 514-515)
-        const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
-        const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-        if (h0 && !isfinite(out0) && !sentinel(dc.x) && !dirichlet) {
-            const double nu[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
-            const double nd[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-            out0 = slow_node<REACTION>(K, uc.x, dc.x, nu, nd, gx, gy, gz, s0, src0);
-        }
-        if (h1 && !isfinite(out1) && !sentinel(dc.y) && !dirichlet) {
-            const double nu[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
-            const double nd[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-            out1 = slow_node<REACTION>(K, uc.y, dc.y, nu, nd, gx + 1, gy, gz, s1, src1);
-        }
-        const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
-        if (bad0 | bad1) {
-            atomicMin(A.bad_key, ((unsigned long long)c << 10) | (unsigned long long)(o + (bad0 ? 0 : 1)));
-            atomicOr(&A.flags[A.k], 1);
-        } else {
-            atomicOr(&A.flags[A.k], 2);
-        }
+    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
+    if (dirichlet || ((a0 && huge(out0)) | (a1 && huge(out1)))) {
+        // rare: exact generic path (Dirichlet-exposed chunks; non-finite
+        // fast results, where the +-0 substitution shortcut needs finite
+        // operands), then the error / mass flags
+        const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+        const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+        const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+        const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+        const double2 r = pair_slow<REACTION>(M, K, C, Z, G.xp, G.y, nu0, nd0, nu1, nd1, uc.x, uc.y, dc.x,
+                                              dc.y, s0, s1, src0, src1, out0, out1);
+        out0 = r.x;
+        out1 = r.y;
     }
-    double* dst = A.un + (int64_t)c * 512 + o;
-    if (a0 && a1) {
-        *reinterpret_cast<double2*>(dst) = make_double2(out0, out1);
-    } else {
-        if (a0) dst[0] = out0;
-        if (a1) dst[1] = out1;
-    }
-    // x-face side planes of u_next for the next step's x halos
-    if (XD) return;
-    if (xp == 0 && a0) M.xfun[((int64_t)c * 2 + 0) * 64 + z * 8 + y] = out0;
-    if (xp == 3 && a1) M.xfun[((int64_t)c * 2 + 1) * 64 + z * 8 + y] = out1;
+    stg_pair(C.out + Z * 64, out0, out1, a0, a1);
 }
 
 __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
@@ -387,27 +455,30 @@ __device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, ui
     if (lane >= 24) dv = __ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
 }
 
-__device__ __forceinline__ ChunkCtx make_ctx(int c, uint32_t lm, int dv) {
+__device__ __forceinline__ ChunkCtx make_ctx(const MarchArgs& M, int c, uint32_t lm, int dv, const LaneGeo& G) {
     ChunkCtx C;
     C.c = c;
-    C.lm = lm;
+    C.lm = c >= 0 ? lm : 0u;
     C.key = __shfl_sync(0xffffffffu, dv, 30);
     C.flags = __shfl_sync(0xffffffffu, dv, 31);
+    C.out = M.A.un + (c >= 0 ? (int64_t)c * 512 + G.bp : 0);
     return C;
 }
 
-// One warp streams a sequence of chunks. Its plane loads (10 per chunk:
-// z-halo below, the 8 body planes, z-halo above) form one continuous
-// sequence through a kRing-slot tile ring, kAhead loads ahead of the plane
-// being computed, across chunk boundaries.
-template <int REACTION, int OCC, int XD>
+// One warp streams a sequence of chunks. Each chunk needs 10 plane loads
+// (z- halo, body planes 0..7, z+ halo) into the fixed slots 0..9 of the
+// warp's ring; the body of the chunk loop is unrolled over the 8 planes, and
+// the loads of the next chunk are issued as soon as the slots they overwrite
+// have been consumed:
+//   after plane z: 0 -> load 8, 1 -> load 9, 2 -> next 0+1, 3..6 -> next 2..5,
+//   7 -> next 6+7   (one commit group each)
+// so before plane z at most 4 (z <= 4) or 5 (z >= 5) groups may be pending.
+template <int REACTION, int OCC>
 __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
-    const int y = lane >> 2, xp = lane & 3, x0 = 2 * xp;
-    Tile* ring = reinterpret_cast<Tile*>(smem_raw) + warp * kRing;
     const StepArgs<double>& A = M.A;
     if (A.k > 0) {
         const int prev = A.flags[A.k - 1];
@@ -428,79 +499,127 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         K.dirichlet = A.dirichlet;
     }
     __syncthreads();
-    const int lofs = xp == 0 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + y : tix(x0, y) - 1;
-    const int rofs = xp == 3 ? (int)(offsetof(Tile, hxu) / sizeof(double)) + 8 + y : tix(x0, y) + 2;
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const LaneGeo G = lane_geo(lane);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kSlots * kTileBytes;
 
-    // ---- chunk stream: kBatch-chunk claims from one counter ----
+    // chunk pipeline: claim position (3 ahead) -> schedule id (2 ahead) ->
+    // lane mask + descriptor (1 ahead) -> load context -> compute
     int* ctr = M.counter;
+    const int n = (int)M.n;
     auto claim = [&]() -> int {
         int v = 0;
-        if (lane == 0) v = atomicAdd(ctr, kBatch);
+        if (lane == 0) v = atomicAdd(ctr, 1);
         return __shfl_sync(0xffffffffu, v, 0);
     };
-    int b_cur = claim(), b_nxt = claim();
-    int bi = 0;  // position of the next chunk to fetch inside b_cur
-    const int n = (int)M.n;
-    auto next_id = [&]() -> int {
-        if (bi == kBatch) {
-            b_cur = b_nxt;
-            b_nxt = claim();
-            bi = 0;
-        }
-        const int p = b_cur + bi++;
-        return p < n ? __ldg(&M.sched[p]) : -1;
-    };
+    auto sched = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
+    const int p0 = claim();
+    const int idC = sched(p0);
+    if (idC < 0) return;
+    const int p1 = claim();
+    int idN = sched(p1);
+    int pNN = claim();
+    uint32_t lmC;
+    int dvC;
+    load_ctx(M, idC, lane, lmC, dvC);
+    uint32_t lmN;
+    int dvN;
+    load_ctx(M, idN, lane, lmN, dvN);
+    int idNN = sched(pNN);
+    pNN = claim();
 
-    // loading side: chunk whose planes are being issued, and the next one
-    int c_ld = next_id();
-    if (c_ld < 0) return;
-    uint32_t lm0, lm1;
-    int dv0, dv1;
-    load_ctx(M, c_ld, lane, lm0, dv0);
-    ChunkCtx Cld = make_ctx(c_ld, lm0, dv0);
-    const int t0 = tix(x0, y);
-    LoadCtx Lld = make_load_ctx<XD>(c_ld, lm0, dv0, M, y, xp, x0);
-    int c_nx = next_id();
-    load_ctx(M, c_nx, lane, lm1, dv1);
-    int p_ld = -1;  // next plane of Cld to issue (-1..8)
-    int L = 0;      // loads issued
-    auto issue_next = [&]() {
-        if (Lld.c >= 0) issue_plane<XD>(ring[L & (kRing - 1)], M, Lld, p_ld, y, xp, t0);
-        cp_commit();
-        ++L;
-        if (++p_ld == 9) {  // advance the load side to the next chunk
-            p_ld = -1;
-            Cld = make_ctx(c_nx, lm1, dv1);
-            Lld = make_load_ctx<XD>(c_nx, lm1, dv1, M, y, xp, x0);
-            c_nx = Cld.c >= 0 ? next_id() : -1;
-            load_ctx(M, c_nx, lane, lm1, dv1);
-        }
-    };
-    // compute side: follows the load side, which is never more than one
-    // chunk ahead (kAhead + 3 < 10 loads)
-    ChunkCtx Cc = Cld;
-    int base = 0;  // load index of plane -1 of Cc
-    // prologue: planes -1, 0, 1 needed for z = 0, plus kAhead more
-    for (int k = 0; k < 3 + kAhead; ++k) issue_next();
-    while (Cc.c >= 0) {
+    ChunkCtx C = make_ctx(M, idC, lmC, dvC, G);
+    LoadCtx L = make_load_ctx(idC, lmC, dvC, M, G);
+    // prologue: groups {0,1}, 2, 3, 4, 5, {6,7}
+    issue_load<0>(sb, L, G);
+    issue_load<1>(sb, L, G);
+    cp_commit();
+    issue_load<2>(sb, L, G);
+    cp_commit();
+    issue_load<3>(sb, L, G);
+    cp_commit();
+    issue_load<4>(sb, L, G);
+    cp_commit();
+    issue_load<5>(sb, L, G);
+    cp_commit();
+    issue_load<6>(sb, L, G);
+    issue_load<7>(sb, L, G);
+    cp_commit();
+    LoadCtx LN;
 #pragma unroll 1
-        for (int z = 0; z < 8; ++z) {
-            // loads up to index base+z+2 complete; exactly kAhead newer groups
-            // are in flight at this point of every iteration
-            cp_wait<kAhead>();
-            __syncwarp();
-            compute_plane<REACTION, XD>(M, K, Cc, z, ring[(base + z) & (kRing - 1)],
-                                    ring[(base + z + 1) & (kRing - 1)],
-                                    ring[(base + z + 2) & (kRing - 1)], y, xp, x0, t0, lofs, rofs);
-            __syncwarp();
-            issue_next();
-            if (z == 7) {  // planes 8 of this chunk and -1 of the next
-                issue_next();
-                issue_next();
-            }
-        }
-        base += 10;
-        Cc = Cld;
+    while (C.c >= 0) {
+        cp_wait<4>();
+        __syncwarp();
+        compute_plane<REACTION, 0>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<8>(sb, L, G);
+        cp_commit();
+
+        cp_wait<4>();
+        __syncwarp();
+        compute_plane<REACTION, 1>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<9>(sb, L, G);
+        cp_commit();
+
+        cp_wait<4>();
+        __syncwarp();
+        compute_plane<REACTION, 2>(M, K, Q, C, sb, G);
+        __syncwarp();
+        LN = make_load_ctx(idN, lmN, dvN, M, G);
+        issue_load<0>(sb, LN, G);
+        issue_load<1>(sb, LN, G);
+        cp_commit();
+
+        cp_wait<4>();
+        __syncwarp();
+        compute_plane<REACTION, 3>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<2>(sb, LN, G);
+        cp_commit();
+
+        cp_wait<4>();
+        __syncwarp();
+        compute_plane<REACTION, 4>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<3>(sb, LN, G);
+        cp_commit();
+
+        cp_wait<5>();
+        __syncwarp();
+        compute_plane<REACTION, 5>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<4>(sb, LN, G);
+        cp_commit();
+
+        cp_wait<5>();
+        __syncwarp();
+        compute_plane<REACTION, 6>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<5>(sb, LN, G);
+        cp_commit();
+
+        cp_wait<5>();
+        __syncwarp();
+        compute_plane<REACTION, 7>(M, K, Q, C, sb, G);
+        __syncwarp();
+        issue_load<6>(sb, LN, G);
+        issue_load<7>(sb, LN, G);
+        cp_commit();
+
+        // advance the pipeline by one chunk
+        C = make_ctx(M, idN, lmN, dvN, G);
+        L = LN;
+        idN = idNN;
+        load_ctx(M, idN, lane, lmN, dvN);
+        idNN = sched(pNN);
+        pNN = claim();
     }
     cp_wait<0>();
 }
@@ -571,34 +690,13 @@ __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __r
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
 }
 
-// x=0 / x=7 planes of a column into the side array [c][side][z*8+y].
-__global__ void xface_kernel(const double* __restrict__ col, int64_t n, double* __restrict__ xf) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n * 128) return;
-    const int64_t c = t >> 7;
-    const int side = (int)((t >> 6) & 1), p = (int)(t & 63);
-    const int z = p >> 3, y = p & 7;
-    xf[t] = col[c * 512 + z * 64 + y * 8 + (side ? 7 : 0)];
-}
-
 void march_free(MarchPlan* p) {
     cudaFree(p->d_stream);
     cudaFree(p->d_desc);
     cudaFree(p->d_deff);
-    cudaFree(p->d_xfd);
-    cudaFree(p->d_xf[0]);
-    cudaFree(p->d_xf[1]);
     cudaFree(p->d_counter);
     cudaFree(p->d_lm);
     *p = MarchPlan{};
-}
-
-void march_extract_xfaces(pd_grid* g, MarchPlan& p, const void* col) {
-    const int64_t n = g->n_chunks;
-    if (n == 0 || !p.ready) return;
-    xface_kernel<<<(unsigned)((n * 128 + 255) / 256), 256, 0, g->stream>>>((const double*)col, n,
-                                                                          p.d_xf[p.cur]);
-    PD_CUDA(cudaGetLastError());
 }
 
 void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const uint64_t* d_sink,
@@ -619,18 +717,12 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaGetLastError());
     const int64_t slots = n_all * 512;
     PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)slots));
-    PD_CUDA(cudaMalloc(&plan->d_xfd, sizeof(double) * 128 * (size_t)n_all));
-    PD_CUDA(cudaMalloc(&plan->d_xf[0], sizeof(double) * 128 * (size_t)n_all));
-    PD_CUDA(cudaMalloc(&plan->d_xf[1], sizeof(double) * 128 * (size_t)n_all));
-    PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024 * kParts));
+    PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024));
     unsigned long long* d_bad = nullptr;
     PD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
     PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
     deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>(
         (const double*)d_dcol, d_fluid, slots, plan->d_deff, d_bad);
-    PD_CUDA(cudaGetLastError());
-    xface_kernel<<<(unsigned)((n_all * 128 + 255) / 256), 256, 0, g->stream>>>(plan->d_deff, n_all,
-                                                                              plan->d_xfd);
     PD_CUDA(cudaGetLastError());
     unsigned long long bad = 0;
     PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
@@ -666,17 +758,12 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaStreamSynchronize(g->stream));
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-    static const int occ = [] {
-        const char* e = getenv("PD_MARCH_OCC");
-        return (e && atoi(e) == 3) ? 3 : kCtasPerSm;
-    }();
-    plan->grid = sms * occ;
+    plan->grid = sms * kCtasPerSm;
     plan->n = n;
     plan->ready = true;
-    plan->cur = 0;
 }
 
-int march_counters_per_step() { return kParts; }
+int march_counters_per_step() { return 1; }
 
 void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction) {
     MarchArgs M;
@@ -686,40 +773,24 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     M.desc = p.d_desc;
     M.lm = p.d_lm;
     M.deff = p.d_deff;
-    M.xfu = p.d_xf[p.cur];
-    M.xfd = p.d_xfd;
-    M.xfun = p.d_xf[1 - p.cur];
-    M.counter = p.d_counter + (int64_t)(a.k & 1023) * kParts;
+    M.counter = p.d_counter + (a.k & 1023);
     static const int dbg = [] {
         const char* e = getenv("PD_MARCH_DBG");
         return e ? atoi(e) : 0;
     }();
     M.dbg = dbg;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-    const bool occ3 = p.grid == sms * 3;
-    const size_t bytes = sizeof(Tile) * kRing * kWarps;
-    static const int xd = [] {
-        const char* e = getenv("PD_MARCH_XSIDE");
-        return (e && atoi(e) == 1) ? 0 : 1;
-    }();
+    constexpr size_t bytes = (size_t)kTileBytes * kSlots * kWarps;
     using KernT = void (*)(MarchArgs);
-    static const KernT table[2][2][3] = {
-        {{ftcs_march_kernel<0, kCtasPerSm, 0>, ftcs_march_kernel<1, kCtasPerSm, 0>, ftcs_march_kernel<2, kCtasPerSm, 0>},
-         {ftcs_march_kernel<0, 3, 0>, ftcs_march_kernel<1, 3, 0>, ftcs_march_kernel<2, 3, 0>}},
-        {{ftcs_march_kernel<0, kCtasPerSm, 1>, ftcs_march_kernel<1, kCtasPerSm, 1>, ftcs_march_kernel<2, kCtasPerSm, 1>},
-         {ftcs_march_kernel<0, 3, 1>, ftcs_march_kernel<1, 3, 1>, ftcs_march_kernel<2, 3, 1>}}};
+    static const KernT table[3] = {ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
+                                   ftcs_march_kernel<2, kCtasPerSm>};
     static bool attr_set = false;
     if (!attr_set) {
-        for (auto& a : table)
-            for (auto& b : a)
-                for (auto k : b) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        for (auto k : table) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         attr_set = true;
     }
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
-    table[xd][occ3 ? 1 : 0][r]<<<p.grid, kThreads, bytes, g->stream>>>(M);
+    table[r]<<<p.grid, kThreads, bytes, g->stream>>>(M);
     PD_CUDA(cudaGetLastError());
-    p.cur = 1 - p.cur;
 }
 
 }  // namespace pdb
