@@ -71,6 +71,7 @@ struct MarchArgs {
     const uint32_t* __restrict__ lm;   // per chunk and lane: active / sink bits
     const double* __restrict__ deff;
     int* counter;                    // chunk-claim counter of this step
+    int static_sched;                // 1: static interleaved positions (no atomics)
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
 };
 
@@ -305,16 +306,17 @@ __device__ __forceinline__ double lds1(uint32_t a) {
 // staged values, then the reference's non-finite / total-mass flags
 // (solver.hpp:444, 250-260, 514-515).
 template <int REACTION>
-__device__ __noinline__ double2 pair_slow(const MarchArgs& M, const SlowConsts& K, const ChunkCtx& C, int z,
+__device__ __noinline__ double2 pair_slow(unsigned long long* bad_key, int* flagp, const SlowConsts& K,
+                                          int c, int key, int cflags, uint32_t lm, int z,
                                           int xp, int y, const double* nu0, const double* nd0,
                                           const double* nu1, const double* nd1, double uc0, double uc1,
                                           double dc0, double dc1, bool s0, bool s1, double src0,
                                           double src1, double out0, double out1) {
-    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;
+    const bool dirichlet = (cflags & kFlagDirichlet) != 0;
     const int x0 = 2 * xp;
-    const int kx = C.key & 1023, ky = (C.key >> 10) & 1023, kz = (C.key >> 20) & 1023;
+    const int kx = key & 1023, ky = (key >> 10) & 1023, kz = (key >> 20) & 1023;
     const int64_t gx = (int64_t)kx * 8 + x0, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-    const bool a0 = (C.lm >> (2 * z)) & 1u, a1 = (C.lm >> (2 * z + 1)) & 1u;
+    const bool a0 = (lm >> (2 * z)) & 1u, a1 = (lm >> (2 * z + 1)) & 1u;
     bool h0, h1;
     if (dirichlet) {  // the whole chunk takes the exact generic update
         if (!sentinel(dc0)) out0 = slow_node<REACTION>(K, uc0, dc0, nu0, nd0, gx, gy, gz, s0, src0);
@@ -333,10 +335,10 @@ __device__ __noinline__ double2 pair_slow(const MarchArgs& M, const SlowConsts& 
         const bool bad0 = a0 && !isfinite(out0), bad1 = a1 && !isfinite(out1);
         const int o = z * 64 + y * 8 + x0;
         if (bad0 | bad1) {
-            atomicMin(M.A.bad_key, ((unsigned long long)C.c << 10) | (unsigned long long)(o + (bad0 ? 0 : 1)));
-            atomicOr(&M.A.flags[M.A.k], 1);
+            atomicMin(bad_key, ((unsigned long long)c << 10) | (unsigned long long)(o + (bad0 ? 0 : 1)));
+            atomicOr(flagp, 1);
         } else {
-            atomicOr(&M.A.flags[M.A.k], 2);
+            atomicOr(flagp, 2);
         }
     }
     return make_double2(out0, out1);
@@ -439,7 +441,7 @@ __device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowCons
         const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
         const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
         const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-        const double2 r = pair_slow<REACTION>(M, K, C, Z, G.xp, G.y, nu0, nd0, nu1, nd1, uc.x, uc.y, dc.x,
+        const double2 r = pair_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, C.c, C.key, C.flags, C.lm, Z, G.xp, G.y, nu0, nd0, nu1, nd1, uc.x, uc.y, dc.x,
                                               dc.y, s0, s1, src0, src1, out0, out1);
         out0 = r.x;
         out1 = r.y;
@@ -510,10 +512,20 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kSlots * kTileBytes;
 
     // chunk pipeline: claim position (3 ahead) -> schedule id (2 ahead) ->
-    // lane mask + descriptor (1 ahead) -> load context -> compute
+    // lane mask + descriptor (1 ahead) -> load context -> compute.
+    // Positions are claimed from one atomic counter (dynamic, default) or
+    // statically interleaved over the warps of the grid (PD_MARCH_STATIC=1).
     int* ctr = M.counter;
     const int n = (int)M.n;
+    const bool stat = M.static_sched != 0;
+    const int gw = blockIdx.x * kWarps + warp, gstride = gridDim.x * kWarps;
+    int spos = gw;
     auto claim = [&]() -> int {
+        if (stat) {
+            const int v = spos;
+            spos += gstride;
+            return v;
+        }
         int v = 0;
         if (lane == 0) v = atomicAdd(ctr, 1);
         return __shfl_sync(0xffffffffu, v, 0);
@@ -532,7 +544,6 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     int dvN;
     load_ctx(M, idN, lane, lmN, dvN);
     int idNN = sched(pNN);
-    pNN = claim();
 
     ChunkCtx C = make_ctx(M, idC, lmC, dvC, G);
     LoadCtx L = make_load_ctx(idC, lmC, dvC, M, G);
@@ -618,8 +629,8 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         L = LN;
         idN = idNN;
         load_ctx(M, idN, lane, lmN, dvN);
-        idNN = sched(pNN);
         pNN = claim();
+        idNN = sched(pNN);
     }
     cp_wait<0>();
 }
@@ -779,6 +790,11 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
         return e ? atoi(e) : 0;
     }();
     M.dbg = dbg;
+    static const int stat = [] {
+        const char* e = getenv("PD_MARCH_STATIC");
+        return e ? atoi(e) : 0;
+    }();
+    M.static_sched = stat;
     constexpr size_t bytes = (size_t)kTileBytes * kSlots * kWarps;
     using KernT = void (*)(MarchArgs);
     static const KernT table[3] = {ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
