@@ -72,6 +72,7 @@ struct MarchArgs {
     const double* __restrict__ deff;
     int* counter;                    // chunk-claim counter of this step
     int static_sched;                // 1: static interleaved positions (no atomics)
+    int zero;                        // 0 (opaque to the compiler)
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
 };
 
@@ -520,15 +521,24 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     const bool stat = M.static_sched != 0;
     const int gw = blockIdx.x * kWarps + warp, gstride = gridDim.x * kWarps;
     int spos = gw;
-    auto claim = [&]() -> int {
+    // Dynamic claims are issued one chunk before their result is needed. The
+    // counter address is made opaque (ctr + (lane & zero), zero = 0) so ptxas
+    // does not turn the atomic into a warp-aggregated one, whose immediate
+    // result shuffle would expose the atomic's round trip.
+    int* ctr_l = ctr + ((t >> 5) & M.zero);
+    auto claim_issue = [&](int& r) {
         if (stat) {
-            const int v = spos;
+            r = spos;
             spos += gstride;
-            return v;
+        } else if (lane == 0) {
+            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(ctr_l) : "memory");
         }
-        int v = 0;
-        if (lane == 0) v = atomicAdd(ctr, 1);
-        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto claim_get = [&](int r) -> int { return stat ? r : __shfl_sync(0xffffffffu, r, 0); };
+    auto claim = [&]() -> int {
+        int r = 0;
+        claim_issue(r);
+        return claim_get(r);
     };
     auto sched = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
     const int p0 = claim();
@@ -544,6 +554,8 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
     int dvN;
     load_ctx(M, idN, lane, lmN, dvN);
     int idNN = sched(pNN);
+    int raw = 0;
+    claim_issue(raw);
 
     ChunkCtx C = make_ctx(M, idC, lmC, dvC, G);
     LoadCtx L = make_load_ctx(idC, lmC, dvC, M, G);
@@ -629,8 +641,283 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
         L = LN;
         idN = idNN;
         load_ctx(M, idN, lane, lmN, dvN);
-        pNN = claim();
+        pNN = claim_get(raw);
         idNN = sched(pNN);
+        claim_issue(raw);
+    }
+    cp_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// v14: the same per-node arithmetic with a rolled plane loop over a
+// continuous 8-slot ring (slot = load index & 7, 5 loads ahead), 32-bit
+// element offsets against the uniform column bases, and a rare path that
+// re-reads its operands from the ring: small code (instruction-cache
+// resident) and <= 128 registers, so 16 warps per SM fit (4 CTAs x 4 warps x
+// 8 slots x 1.5 KB = 192 KB of ring per SM).
+// ---------------------------------------------------------------------------
+constexpr int kRing14 = 8;
+constexpr int kAhead14 = 5;  // kRing14 - 3 (planes z-1, z, z+1 resident)
+constexpr int kCtas14 = 4;
+
+struct LoadCtx14 {
+    uint32_t own, zl, zh, xo, yo;  // element offsets of the lane's sources in plane 0
+    uint32_t lm;                   // active bits of the lane's pair (0 if no chunk)
+    bool zlok, zhok, xok, yok;
+};
+
+__device__ __forceinline__ LoadCtx14 make_load_ctx14(int c, uint32_t lm, int dv, int dbg, const LaneGeo& G) {
+    int nb[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
+    LoadCtx14 L;
+    const bool ok = c >= 0;
+    L.own = ok ? (uint32_t)c * 512u + G.bp : 0u;
+    L.lm = ok ? lm : 0u;
+    L.zlok = ok && nb[4] >= 0 && !(dbg & 4);
+    L.zhok = ok && nb[5] >= 0 && !(dbg & 4);
+    L.zl = L.zlok ? (uint32_t)nb[4] * 512u + 448u + G.bp : 0u;
+    L.zh = L.zhok ? (uint32_t)nb[5] * 512u + G.bp : 0u;
+    const int jx = G.xp == 0 ? nb[0] : nb[1];
+    L.xok = ok && G.xface && jx >= 0 && !(dbg & 1);
+    L.xo = L.xok ? (uint32_t)jx * 512u + (uint32_t)G.y * 8u + (G.xp == 0 ? 7u : 0u) : 0u;
+    const int jy = G.y == 0 ? nb[2] : nb[3];
+    L.yok = ok && G.yface && jy >= 0 && !(dbg & 2);
+    L.yo = L.yok ? (uint32_t)jy * 512u + (G.y == 0 ? 56u : 0u) + 2u * (uint32_t)G.xp : 0u;
+    return L;
+}
+
+// Load i (0..9, warp-uniform) of a chunk into the ring slot at st.
+__device__ __forceinline__ void issue14(uint32_t st, const double* __restrict__ u, const double* __restrict__ de,
+                                        const LoadCtx14& L, int i, const LaneGeo& G) {
+    if (i == 0 || i == 9) {
+        const bool ok = i == 0 ? L.zlok : L.zhok;
+        const uint32_t o = i == 0 ? L.zl : L.zh;
+        cp16x2(st + G.s_c, u + o, st + kDOff + G.s_c, de + o, ok);
+        sts_sent1(st + kDOff + G.s_c, !ok), sts_sent1(st + kDOff + G.s_c + 8, !ok);
+        return;
+    }
+    const uint32_t p64 = (uint32_t)(i - 1) * 64u;
+    const bool ok = ((L.lm >> (2 * (i - 1))) & 3u) != 0u;
+    const uint32_t o = L.own + p64;
+    cp16x2(st + G.s_c, u + o, st + kDOff + G.s_c, de + o, ok);
+    sts_sent1(st + kDOff + G.s_c, !ok), sts_sent1(st + kDOff + G.s_c + 8, !ok);
+    const uint32_t ox = L.xo + p64;
+    cp8x2(st + G.s_hx, u + ox, st + kDOff + G.s_hx, de + ox, L.xok);
+    sts_sent1(st + kDOff + G.s_hx, G.xface && !L.xok);
+    const uint32_t oy = L.yo + p64;
+    cp16x2(st + G.s_hy, u + oy, st + kDOff + G.s_hy, de + oy, L.yok);
+    sts_sent1(st + kDOff + G.s_hy, G.yface && !L.yok), sts_sent1(st + kDOff + G.s_hy + 8, G.yface && !L.yok);
+}
+
+struct ChunkCtx14 {
+    int c, key, flags;
+    uint32_t lm;
+};
+
+// Rare path (Dirichlet-exposed chunk, or a huge / non-finite fast result):
+// re-reads the pair's operands from the ring and applies the exact generic
+// update and the error / mass flags (solver.hpp:360-455, 250-260, 514-515).
+template <int REACTION>
+__device__ __noinline__ double2 pair_slow14(const MarchArgs& M, const SlowConsts& K, ChunkCtx14 C, int z,
+                                            uint32_t tm, uint32_t t0, uint32_t tp, LaneGeo G, double out0,
+                                            double out1) {
+    const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
+    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
+    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
+    const double2 uym = lds2(t0 + G.s_c - 64), dym = lds2(t0 + kDOff + G.s_c - 64);
+    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = lds2(t0 + kDOff + G.s_c + 64);
+    const double2 uzm = lds2(tm + G.s_c), dzm = lds2(tm + kDOff + G.s_c);
+    const double2 uzp = lds2(tp + G.s_c), dzp = lds2(tp + kDOff + G.s_c);
+    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
+    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
+    double src0 = 0.0, src1 = 0.0;
+    if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const double* sp = M.A.src + (int64_t)C.c * 512 + z * 64 + G.bp;
+        src0 = sp[0];
+        src1 = sp[1];
+    }
+    const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+    const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+    const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+    const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+    return pair_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, C.c, C.key, C.flags, C.lm, z, G.xp, G.y, nu0,
+                               nd0, nu1, nd1, uc.x, uc.y, dc.x, dc.y, s0, s1, src0, src1, out0, out1);
+}
+
+template <int REACTION>
+__device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
+                                          const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
+                                          const LaneGeo& G, double* __restrict__ un) {
+    const uint32_t lz = C.lm >> (2 * z);
+    const bool a0 = lz & 1u, a1 = (lz >> 1) & 1u;
+    const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
+    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
+    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
+    const double2 uym = lds2(t0 + G.s_c - 64), dym = lds2(t0 + kDOff + G.s_c - 64);
+    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = lds2(t0 + kDOff + G.s_c + 64);
+    const double2 uzm = lds2(tm + G.s_c), dzm = lds2(tm + kDOff + G.s_c);
+    const double2 uzp = lds2(tp + G.s_c), dzp = lds2(tp + kDOff + G.s_c);
+    double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
+    if ((C.flags >> (8 + z)) & 1) {
+        fxl = fface(dL, dc.x, uL, uc.x);
+        fxi = fface(dc.x, dc.y, uc.x, uc.y);
+        fxr = fface(dc.y, dR, uc.y, uR);
+        fy0m = fface(dym.x, dc.x, uym.x, uc.x);
+        fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = fface(dym.y, dc.y, uym.y, uc.y);
+        fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
+    } else {
+        fxl = face(dL, dc.x, uL, uc.x);
+        fxi = face(dc.x, dc.y, uc.x, uc.y);
+        fxr = face(dc.y, dR, uc.y, uR);
+        fy0m = face(dym.x, dc.x, uym.x, uc.x);
+        fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = face(dym.y, dc.y, uym.y, uc.y);
+        fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
+    }
+    double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
+    lap0 += (fxi - fxl) * Q.ix;
+    lap0 += (fy0p - fy0m) * Q.iy;
+    lap0 += (fz0p - fz0m) * Q.iz;
+    double lap1 = 0.0;
+    lap1 += (fxr - fxi) * Q.ix;
+    lap1 += (fy1p - fy1m) * Q.iy;
+    lap1 += (fz1p - fz1m) * Q.iz;
+    double r0 = 0.0, r1 = 0.0;
+    if (REACTION == PD_REACTION_SURFACE_SINK) {
+        r0 = ((lz >> 16) & 1u) ? Q.neg_k * uc.x : 0.0;
+        r1 = ((lz >> 17) & 1u) ? Q.neg_k * uc.y : 0.0;
+    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const double* sp = M.A.src + (int64_t)C.c * 512 + z * 64 + G.bp;
+        r0 = sp[0] * Q.src_factor;
+        r1 = sp[1] * Q.src_factor;
+    }
+    double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
+    double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
+    if (sentinel(dc.x)) out0 = uc.x;  // walls stay frozen (solver.hpp:413-417)
+    if (sentinel(dc.y)) out1 = uc.y;
+    if ((C.flags & kFlagDirichlet) || ((a0 && huge(out0)) | (a1 && huge(out1)))) {
+        const double2 r = pair_slow14<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        out0 = r.x;
+        out1 = r.y;
+    }
+    stg_pair(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, a0, a1);
+}
+
+template <int REACTION>
+__global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchArgs M) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+    }
+    __syncthreads();
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const LaneGeo G = lane_geo(lane);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kRing14 * kTileBytes;
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    double* __restrict__ un = A.un;
+
+    // chunk pipeline (see ftcs_march_kernel): claim -> schedule id ->
+    // lane mask + descriptor -> load side -> compute side
+    int* ctr_l = M.counter + ((t >> 5) & M.zero);
+    const int n = (int)M.n;
+    auto claim_issue = [&](int& r) {
+        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(ctr_l) : "memory");
+    };
+    auto claim_get = [&](int r) -> int { return __shfl_sync(0xffffffffu, r, 0); };
+    auto sched = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
+    int r0 = 0, r1 = 0, r2 = 0;
+    claim_issue(r0);
+    claim_issue(r1);
+    claim_issue(r2);
+    const int idC = sched(claim_get(r0));
+    if (idC < 0) return;
+    int idN = sched(claim_get(r1));
+    int idNN = sched(claim_get(r2));
+    int raw = 0;
+    claim_issue(raw);
+    uint32_t lmC, lmN;
+    int dvC, dvN;
+    load_ctx(M, idC, lane, lmC, dvC);
+    load_ctx(M, idN, lane, lmN, dvN);
+
+    // load side
+    ChunkCtx14 Cld{idC, __shfl_sync(0xffffffffu, dvC, 30), __shfl_sync(0xffffffffu, dvC, 31), lmC};
+    LoadCtx14 Lld = make_load_ctx14(idC, lmC, dvC, M.dbg, G);
+    int p_ld = 0;    // next load index (0..9) of the load-side chunk
+    uint32_t Lc = 0;  // loads issued
+    auto issue_next = [&]() {
+        issue14(sb + (Lc & (kRing14 - 1)) * kTileBytes, u, de, Lld, p_ld, G);
+        cp_commit();
+        ++Lc;
+        if (++p_ld == 10) {  // the load side moves on to the next chunk
+            p_ld = 0;
+            Cld = ChunkCtx14{idN, __shfl_sync(0xffffffffu, dvN, 30), __shfl_sync(0xffffffffu, dvN, 31),
+                             idN >= 0 ? lmN : 0u};
+            Lld = make_load_ctx14(idN, lmN, dvN, M.dbg, G);
+            idN = idNN;
+            load_ctx(M, idN, lane, lmN, dvN);
+            idNN = sched(claim_get(raw));
+            claim_issue(raw);
+        }
+    };
+    ChunkCtx14 Cc = Cld;
+    uint32_t base = 0;  // load index of plane -1 of Cc
+#pragma unroll 1
+    for (int k = 0; k < 3 + kAhead14; ++k) issue_next();
+#pragma unroll 1
+    while (Cc.c >= 0) {
+#pragma unroll 1
+        for (int z = 0; z < 8; ++z) {
+            cp_wait<kAhead14>();
+            __syncwarp();
+            const uint32_t b = base + (uint32_t)z;
+            compute14<REACTION>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes, sb + ((b + 1u) & 7u) * kTileBytes,
+                                sb + ((b + 2u) & 7u) * kTileBytes, G, un);
+            __syncwarp();
+            issue_next();
+            if (z == 7) {  // plane 8 of this chunk and plane -1 of the next
+                issue_next();
+                issue_next();
+            }
+        }
+        base += 10u;
+        Cc = Cld;
     }
     cp_wait<0>();
 }
@@ -795,17 +1082,39 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
         return e ? atoi(e) : 0;
     }();
     M.static_sched = stat;
-    constexpr size_t bytes = (size_t)kTileBytes * kSlots * kWarps;
+    M.zero = 0;
+    static const int ver = [] {
+        const char* e = getenv("PD_MARCH_V");
+        return e ? atoi(e) : 14;
+    }();
     using KernT = void (*)(MarchArgs);
-    static const KernT table[3] = {ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
-                                   ftcs_march_kernel<2, kCtasPerSm>};
-    static bool attr_set = false;
-    if (!attr_set) {
-        for (auto k : table) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        attr_set = true;
-    }
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
-    table[r]<<<p.grid, kThreads, bytes, g->stream>>>(M);
+    if (ver == 13) {
+        constexpr size_t bytes = (size_t)kTileBytes * kSlots * kWarps;
+        static const KernT table[3] = {ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
+                                       ftcs_march_kernel<2, kCtasPerSm>};
+        static bool attr_set = false;
+        if (!attr_set) {
+            for (auto k : table)
+                PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            attr_set = true;
+        }
+        int sms = 148;
+        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        table[r]<<<sms * kCtasPerSm, kThreads, bytes, g->stream>>>(M);
+    } else {
+        constexpr size_t bytes = (size_t)kTileBytes * kRing14 * kWarps;
+        static const KernT table[3] = {ftcs_march14_kernel<0>, ftcs_march14_kernel<1>, ftcs_march14_kernel<2>};
+        static bool attr_set = false;
+        if (!attr_set) {
+            for (auto k : table)
+                PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            attr_set = true;
+        }
+        int sms = 148;
+        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        table[r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);
+    }
     PD_CUDA(cudaGetLastError());
 }
 
