@@ -73,6 +73,7 @@ struct MarchArgs {
     int* counter;                    // chunk-claim counter of this step
     int static_sched;                // 1: static interleaved positions (no atomics)
     int zero;                        // 0 (opaque to the compiler)
+    int64_t n_all;                   // chunks of the grid (D_eff sentinel chunk follows them)
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
 };
 
@@ -659,6 +660,23 @@ __global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) 
 constexpr int kRing14 = 8;
 constexpr int kAhead14 = 5;  // kRing14 - 3 (planes z-1, z, z+1 resident)
 constexpr int kCtas14 = 4;
+constexpr uint32_t kCtxBytes14 = 176;  // lm[32], desc[8], id, pad
+constexpr uint32_t kWarpBytes14 = kRing14 * kTileBytes + 3 * kCtxBytes14;
+
+__device__ __forceinline__ void cp4(uint32_t sa, const void* g, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(sa),
+        "l"(g), "r"((int)pred));
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(a), "r"(v));
+}
 
 struct LoadCtx14 {
     uint32_t own, zl, zh, xo, yo;  // element offsets of the lane's sources in plane 0
@@ -687,27 +705,42 @@ __device__ __forceinline__ LoadCtx14 make_load_ctx14(int c, uint32_t lm, int dv,
     return L;
 }
 
-// Load i (0..9, warp-uniform) of a chunk into the ring slot at st.
+// Load i (0..9, warp-uniform) of a chunk into the ring slot at st. D_eff
+// cells without a source in the grid (inactive pairs, missing neighbours)
+// copy the same cells of the sentinel chunk (-inf, at sent_off); their u is
+// not loaded (never used: the face terms of a sentinel side are zero).
+__device__ __forceinline__ void cp16_ud(uint32_t su, const double* gu, bool pu, uint32_t sd, const double* gd,
+                                        bool pd) {
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.b32 p, %4, 0;\n setp.ne.b32 q, %5, 0;\n"
+        " @p cp.async.cg.shared.global [%0], [%1], 16;\n"
+        " @q cp.async.cg.shared.global [%2], [%3], 16;\n}\n" ::"r"(su),
+        "l"(gu), "r"(sd), "l"(gd), "r"((int)pu), "r"((int)pd));
+}
+__device__ __forceinline__ void cp8_ud(uint32_t su, const double* gu, bool pu, uint32_t sd, const double* gd,
+                                       bool pd) {
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.b32 p, %4, 0;\n setp.ne.b32 q, %5, 0;\n"
+        " @p cp.async.ca.shared.global [%0], [%1], 8;\n"
+        " @q cp.async.ca.shared.global [%2], [%3], 8;\n}\n" ::"r"(su),
+        "l"(gu), "r"(sd), "l"(gd), "r"((int)pu), "r"((int)pd));
+}
 __device__ __forceinline__ void issue14(uint32_t st, const double* __restrict__ u, const double* __restrict__ de,
-                                        const LoadCtx14& L, int i, const LaneGeo& G) {
+                                        const LoadCtx14& L, int i, const LaneGeo& G, uint32_t sent_off) {
     if (i == 0 || i == 9) {
         const bool ok = i == 0 ? L.zlok : L.zhok;
         const uint32_t o = i == 0 ? L.zl : L.zh;
-        cp16x2(st + G.s_c, u + o, st + kDOff + G.s_c, de + o, ok);
-        sts_sent1(st + kDOff + G.s_c, !ok), sts_sent1(st + kDOff + G.s_c + 8, !ok);
+        cp16_ud(st + G.s_c, u + o, ok, st + kDOff + G.s_c, de + (ok ? o : sent_off + G.bp), true);
         return;
     }
     const uint32_t p64 = (uint32_t)(i - 1) * 64u;
     const bool ok = ((L.lm >> (2 * (i - 1))) & 3u) != 0u;
     const uint32_t o = L.own + p64;
-    cp16x2(st + G.s_c, u + o, st + kDOff + G.s_c, de + o, ok);
-    sts_sent1(st + kDOff + G.s_c, !ok), sts_sent1(st + kDOff + G.s_c + 8, !ok);
+    cp16_ud(st + G.s_c, u + o, ok, st + kDOff + G.s_c, de + (ok ? o : sent_off + G.bp + p64), true);
     const uint32_t ox = L.xo + p64;
-    cp8x2(st + G.s_hx, u + ox, st + kDOff + G.s_hx, de + ox, L.xok);
-    sts_sent1(st + kDOff + G.s_hx, G.xface && !L.xok);
+    cp8_ud(st + G.s_hx, u + ox, L.xok, st + kDOff + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64), G.xface);
     const uint32_t oy = L.yo + p64;
-    cp16x2(st + G.s_hy, u + oy, st + kDOff + G.s_hy, de + oy, L.yok);
-    sts_sent1(st + kDOff + G.s_hy, G.yface && !L.yok), sts_sent1(st + kDOff + G.s_hy + 8, G.yface && !L.yok);
+    cp16_ud(st + G.s_hy, u + oy, L.yok, st + kDOff + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64), G.yface);
 }
 
 struct ChunkCtx14 {
@@ -759,7 +792,8 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
     const double2 uzm = lds2(tm + G.s_c), dzm = lds2(tm + kDOff + G.s_c);
     const double2 uzp = lds2(tp + G.s_c), dzp = lds2(tp + kDOff + G.s_c);
     double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
-    if ((C.flags >> (8 + z)) & 1) {
+    const bool interior = (C.flags >> (8 + z)) & 1;  // warp-uniform: no walls, no substitution
+    if (interior) {
         fxl = fface(dL, dc.x, uL, uc.x);
         fxi = fface(dc.x, dc.y, uc.x, uc.y);
         fxr = fface(dc.y, dR, uc.y, uR);
@@ -803,8 +837,10 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
     }
     double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
     double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
-    if (sentinel(dc.x)) out0 = uc.x;  // walls stay frozen (solver.hpp:413-417)
-    if (sentinel(dc.y)) out1 = uc.y;
+    if (!interior) {  // walls stay frozen (solver.hpp:413-417)
+        if (sentinel(dc.x)) out0 = uc.x;
+        if (sentinel(dc.y)) out1 = uc.y;
+    }
     if ((C.flags & kFlagDirichlet) || ((a0 && huge(out0)) | (a1 && huge(out1)))) {
         const double2 r = pair_slow14<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
@@ -847,54 +883,87 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     Q.iy = A.inv_dx2[1];
     Q.iz = A.inv_dx2[2];
     const LaneGeo G = lane_geo(lane);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kRing14 * kTileBytes;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes14;
     const double* __restrict__ u = A.u;
     const double* __restrict__ de = M.deff;
     double* __restrict__ un = A.un;
+    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
 
-    // chunk pipeline (see ftcs_march_kernel): claim -> schedule id ->
-    // lane mask + descriptor -> load side -> compute side
+    // Chunk pipeline, staged through a 3-entry per-warp context ring in shared
+    // memory so no register ever waits on a just-issued load: at the advance
+    // onto chunk k, entry k%3 holds chunk k's lane masks + descriptor + id,
+    // entry (k+1)%3 holds chunk k+1's id, and lane 0 holds the claimed
+    // schedule position of chunk k+2. The advance reads entry k%3, issues the
+    // cp.async of chunk k+1's masks / descriptor and of chunk k+2's id, and
+    // claims the position of chunk k+3 (a plain atomic: the counter address is
+    // opaque, ctr + (warp & zero), so ptxas does not warp-aggregate it and
+    // shuffle the result right away).
     int* ctr_l = M.counter + ((t >> 5) & M.zero);
     const int n = (int)M.n;
-    auto claim_issue = [&](int& r) {
-        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(ctr_l) : "memory");
-    };
-    auto claim_get = [&](int r) -> int { return __shfl_sync(0xffffffffu, r, 0); };
-    auto sched = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
-    int r0 = 0, r1 = 0, r2 = 0;
-    claim_issue(r0);
-    claim_issue(r1);
-    claim_issue(r2);
-    const int idC = sched(claim_get(r0));
-    if (idC < 0) return;
-    int idN = sched(claim_get(r1));
-    int idNN = sched(claim_get(r2));
+    const uint32_t cb = sb + kRing14 * kTileBytes;  // context ring
+    auto cent = [&](int e) -> uint32_t { return cb + (uint32_t)e * kCtxBytes14; };
     int raw = 0;
-    claim_issue(raw);
-    uint32_t lmC, lmN;
-    int dvC, dvN;
-    load_ctx(M, idC, lane, lmC, dvC);
-    load_ctx(M, idN, lane, lmN, dvN);
-
-    // load side
-    ChunkCtx14 Cld{idC, __shfl_sync(0xffffffffu, dvC, 30), __shfl_sync(0xffffffffu, dvC, 31), lmC};
-    LoadCtx14 Lld = make_load_ctx14(idC, lmC, dvC, M.dbg, G);
+    auto claim_issue = [&]() {
+        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(raw) : "l"(ctr_l) : "memory");
+    };
+    auto sched_sync = [&]() -> int {
+        claim_issue();
+        const int p = __shfl_sync(0xffffffffu, raw, 0);
+        return p < n ? __ldg(&M.sched[p]) : -1;
+    };
+    auto fetch_ctx = [&](uint32_t e, int c) {  // masks + descriptor of chunk c into entry e
+        cp4(e + 4u * (uint32_t)lane, M.lm + (int64_t)(c < 0 ? 0 : c) * 32 + lane, c >= 0);
+        cp4(e + 128u + 4u * (uint32_t)(lane & 7), M.desc + (int64_t)(c < 0 ? 0 : c) * 8 + (lane & 7),
+            c >= 0 && lane < 8);
+    };
+    {
+        const int id0 = sched_sync();
+        if (id0 < 0) return;
+        const int id1 = sched_sync();
+        if (lane == 0) {
+            sts_u32(cent(0) + 160u, (uint32_t)id0);
+            sts_u32(cent(1) + 160u, (uint32_t)id1);
+        }
+        fetch_ctx(cent(0), id0);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        claim_issue();
+    }
+    int ek = 0;  // entry of the load-side chunk
+    ChunkCtx14 Cld;
+    LoadCtx14 Lld;
+    auto advance = [&]() {
+        const uint32_t e0 = cent(ek);
+        const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
+        const uint32_t e1 = cent(e1i), e2 = cent(e2i);
+        const int c = (int)lds_u32(e0 + 160u);
+        const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
+        // descriptor word j lives at lane 24 + j (make_load_ctx14 / ChunkCtx14)
+        const int dv = (int)lds_u32(e0 + 128u + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
+        Cld = ChunkCtx14{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm};
+        Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
+        const int c1 = (int)lds_u32(e1 + 160u);
+        fetch_ctx(e1, c1);
+        if (lane == 0) {
+            const bool ok = raw < n;
+            cp4(e2 + 160u, M.sched + (ok ? raw : 0), ok);
+            if (!ok) sts_u32(e2 + 160u, 0xFFFFFFFFu);
+        }
+        claim_issue();
+        ek = e1i;
+    };
+    advance();
     int p_ld = 0;    // next load index (0..9) of the load-side chunk
     uint32_t Lc = 0;  // loads issued
     auto issue_next = [&]() {
-        issue14(sb + (Lc & (kRing14 - 1)) * kTileBytes, u, de, Lld, p_ld, G);
-        cp_commit();
-        ++Lc;
+        issue14(sb + (Lc & (kRing14 - 1)) * kTileBytes, u, de, Lld, p_ld, G, sent_off);
         if (++p_ld == 10) {  // the load side moves on to the next chunk
             p_ld = 0;
-            Cld = ChunkCtx14{idN, __shfl_sync(0xffffffffu, dvN, 30), __shfl_sync(0xffffffffu, dvN, 31),
-                             idN >= 0 ? lmN : 0u};
-            Lld = make_load_ctx14(idN, lmN, dvN, M.dbg, G);
-            idN = idNN;
-            load_ctx(M, idN, lane, lmN, dvN);
-            idNN = sched(claim_get(raw));
-            claim_issue(raw);
+            advance();
         }
+        cp_commit();
+        ++Lc;
     };
     ChunkCtx14 Cc = Cld;
     uint32_t base = 0;  // load index of plane -1 of Cc
@@ -921,6 +990,8 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     }
     cp_wait<0>();
 }
+
+__global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
                             const uint64_t* __restrict__ flu, int64_t n, int64_t s0, int64_t s1,
@@ -1014,7 +1085,12 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
                                                                                 n_all, plan->d_lm);
     PD_CUDA(cudaGetLastError());
     const int64_t slots = n_all * 512;
-    PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)slots));
+    // one extra chunk of sentinels after the last one: the source of every
+    // D_eff cell a plane load does not read from the grid (inactive pairs,
+    // missing neighbours), so the loads need no shared-memory sentinel stores
+    PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)(slots + 512)));
+    PD_CUDA(cudaMemsetAsync(plan->d_deff + slots, 0, sizeof(double) * 512, g->stream));
+    sentinel_fill_kernel<<<1, 512, 0, g->stream>>>(plan->d_deff + slots);
     PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024));
     unsigned long long* d_bad = nullptr;
     PD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
@@ -1083,6 +1159,7 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
     }();
     M.static_sched = stat;
     M.zero = 0;
+    M.n_all = g->n_chunks;
     static const int ver = [] {
         const char* e = getenv("PD_MARCH_V");
         return e ? atoi(e) : 14;
@@ -1103,7 +1180,7 @@ void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int react
         PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
         table[r]<<<sms * kCtasPerSm, kThreads, bytes, g->stream>>>(M);
     } else {
-        constexpr size_t bytes = (size_t)kTileBytes * kRing14 * kWarps;
+        constexpr size_t bytes = (size_t)kWarpBytes14 * kWarps;
         static const KernT table[3] = {ftcs_march14_kernel<0>, ftcs_march14_kernel<1>, ftcs_march14_kernel<2>};
         static bool attr_set = false;
         if (!attr_set) {
