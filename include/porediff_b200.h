@@ -200,6 +200,29 @@ int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed);
 /* Fills a property with a constant on active nodes. */
 int pd_grid_fill_const(pd_grid* g, int prop, double value);
 
+/* ---- FRAP / effective diffusivity support (reference analysis.hpp:147-225)
+ * ------------------------------------------------------------------------ */
+
+/* build_free_box_grid (analysis.hpp:147-153): every node of the box active,
+ * chunks in ascending linear index; prop_phi (>= 0) is set to phi_value on
+ * every node, all other properties zero. */
+int pd_grid_create_full(int dims, int scalar_bytes, const int64_t* size, const double* spacing, int n_props,
+                        int prop_phi, double phi_value, int device, pd_grid** out);
+/* run_frap initial condition (analysis.hpp:179-186): u = (node in [lo, hi)) ?
+ * 0 : 1 and D = T(d_molecular) on every active node; returns the active
+ * counts inside the box (region) and overall (phase). */
+int pd_grid_frap_init(pd_grid* g, int prop_u, int prop_d, const int64_t* lo, const int64_t* hi,
+                      double d_molecular, int64_t* region, int64_t* phase);
+/* The run_frap observer's region mass before the cell-volume factor
+ * (analysis.hpp:211-216): sum of double(value) over the active nodes of
+ * [lo, hi) in lexicographic order (axis 0 fastest), sequential, bit-exact. */
+int pd_grid_box_sum(pd_grid* g, int prop, const int64_t* lo, const int64_t* hi, double* out);
+/* Attaches that observer to a stepper: pd_stepper_run then also evaluates the
+ * box sum of the post-step u at every recorded step; NULL detaches. */
+int pd_stepper_set_region(pd_stepper* s, const int64_t* lo, const int64_t* hi);
+/* Box sums of the rows produced by the last pd_stepper_run (row order). */
+int pd_stepper_region_sums(const pd_stepper* s, double* out, int64_t cap, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

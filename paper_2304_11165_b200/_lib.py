@@ -97,6 +97,11 @@ _SIGNATURES = [
     ("pd_grid_populate_diffusion", C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double]),
     ("pd_grid_fill_hash", C.c_int, [_P, C.c_int, C.c_uint64]),
     ("pd_grid_fill_const", C.c_int, [_P, C.c_int, C.c_double]),
+    ("pd_grid_create_full", C.c_int, [C.c_int, C.c_int, _I64P, _DP, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(_P)]),
+    ("pd_grid_frap_init", C.c_int, [_P, C.c_int, C.c_int, _I64P, _I64P, C.c_double, _I64P, _I64P]),
+    ("pd_grid_box_sum", C.c_int, [_P, C.c_int, _I64P, _I64P, _DP]),
+    ("pd_stepper_set_region", C.c_int, [_P, _I64P, _I64P]),
+    ("pd_stepper_region_sums", C.c_int, [_P, _DP, C.c_int64, _I64P]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

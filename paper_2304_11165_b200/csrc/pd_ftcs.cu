@@ -301,6 +301,12 @@ struct pd_stepper {
     int64_t begin = 0, end = 0;  // owned ordinal range
     pdb::MarchPlan plan;         // 3-D FP64 column-march fast path
     bool use_march = true;
+    // region-mass observer (run_frap, analysis.hpp:211-219): box sum of u at
+    // every recorded step
+    bool has_region = false;
+    int64_t rlo[3] = {0, 0, 0}, rhi[3] = {0, 0, 0};
+    double* d_region = nullptr;  // one per row of the batch
+    std::vector<double> region_out;
 };
 
 namespace {
@@ -456,6 +462,7 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             PD_CUDA(cudaMalloc(&s->d_flags, sizeof(int) * (size_t)kBatch));
             PD_CUDA(cudaMalloc(&s->d_bad, sizeof(unsigned long long)));
             PD_CUDA(cudaMalloc(&s->d_rows, sizeof(double) * 3 * (size_t)kBatch));
+            PD_CUDA(cudaMalloc(&s->d_region, sizeof(double) * (size_t)kBatch));
             PD_CUDA(cudaEventCreate(&s->ev0));
             PD_CUDA(cudaEventCreate(&s->ev1));
             if (g->n_chunks > 0) {
@@ -514,6 +521,7 @@ int pd_stepper_destroy(pd_stepper* s) {
         cudaFree(s->d_flags);
         cudaFree(s->d_bad);
         cudaFree(s->d_rows);
+        cudaFree(s->d_region);
         march_free(&s->plan);
         if (s->ev0) cudaEventDestroy(s->ev0);
         if (s->ev1) cudaEventDestroy(s->ev1);
@@ -586,6 +594,8 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
         std::vector<int> hflags((size_t)kBatch);
         std::vector<double> hrows((size_t)kBatch * 3);
         std::vector<int64_t> row_step((size_t)kBatch);
+        std::vector<double> hregion((size_t)kBatch);
+        s->region_out.clear();
         while (j < n_steps) {
             const int64_t nb = std::min<int64_t>(kBatch, n_steps - j);
             PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)nb, g->stream));
@@ -605,6 +615,7 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                 if (record) {
                     launch_pairwise_finalize(g, s->d_rows + 3 * nr, s->d_flags + k, s->begin,
                                              s->end - s->begin);
+                    if (s->has_region) launch_box_sum(g, g->cols[(size_t)cn], s->rlo, s->rhi, s->d_region + nr);
                     row_step[(size_t)nr] = st + 1;
                     ++nr;
                 }
@@ -616,6 +627,9 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                                     cudaMemcpyDeviceToHost, g->stream));
             if (nr > 0)
                 PD_CUDA(cudaMemcpyAsync(hrows.data(), s->d_rows, sizeof(double) * 3 * (size_t)nr,
+                                        cudaMemcpyDeviceToHost, g->stream));
+            if (nr > 0 && s->has_region)
+                PD_CUDA(cudaMemcpyAsync(hregion.data(), s->d_region, sizeof(double) * (size_t)nr,
                                         cudaMemcpyDeviceToHost, g->stream));
             PD_CUDA(cudaStreamSynchronize(g->stream));
             float ms = 0.f;
@@ -638,6 +652,7 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                 d.total_mass = hrows[(size_t)r * 3];
                 d.min_u = hrows[(size_t)r * 3 + 1];
                 d.max_u = hrows[(size_t)r * 3 + 2];
+                if (s->has_region) s->region_out.push_back(hregion[(size_t)r]);
             }
             if (fail_k < 0) {
                 j += nb;
@@ -677,6 +692,27 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
         }
         s->last_ms = total_ms;
     });
+}
+
+int pd_stepper_set_region(pd_stepper* s, const int64_t* lo, const int64_t* hi) {
+    return guarded([&] {
+        if (!lo || !hi) {
+            s->has_region = false;
+            return;
+        }
+        check_box(s->g, lo, hi);
+        for (int a = 0; a < 3; ++a) {
+            s->rlo[a] = a < s->g->dims ? lo[a] : 0;
+            s->rhi[a] = a < s->g->dims ? hi[a] : 1;
+        }
+        s->has_region = true;
+    });
+}
+
+int pd_stepper_region_sums(const pd_stepper* s, double* out, int64_t cap, int64_t* n) {
+    *n = (int64_t)s->region_out.size();
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n); ++i) out[i] = s->region_out[(size_t)i];
+    return PD_OK;
 }
 
 int pd_stepper_last_ms(const pd_stepper* s, double* ms) {

@@ -146,6 +146,12 @@ int march_counters_per_step();
 void march_free(MarchPlan* plan);
 void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction);
 
+// Sequential lexicographic (axis 0 fastest) double sum of the active nodes of
+// a column inside the box [lo, hi) into *dst (device) — the run_frap region
+// observer (analysis.hpp:211-219), pd_frap.cu.
+void launch_box_sum(pd_grid* g, const void* col, const int64_t* lo, const int64_t* hi, double* dst);
+void check_box(const pd_grid* g, const int64_t* lo, const int64_t* hi);
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

@@ -15,7 +15,7 @@ import ctypes as C
 import math
 import time as _time
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -242,6 +242,8 @@ class StepDiagnostics:
 @dataclass
 class SimulationResult:
     diagnostics: List[StepDiagnostics]
+    # device region-mass observer (run_frap): box sum of u per diagnostics row
+    region_sums: List[float] = field(default_factory=list)
 
 
 scratch_channel = "u_next"
@@ -344,6 +346,19 @@ class SparseBlockGrid:
                 g._data[p] = np.ascontiguousarray(data[p], g.dtype).reshape(-1, g.V).copy()
             else:
                 g._data[p] = np.zeros((len(lin), g.V), g.dtype)
+        return g
+
+    @classmethod
+    def from_device(cls, geometry, properties, dev: "DeviceGrid", dtype=np.float64):
+        """A grid whose state lives on the device (host slabs fetched on first
+        access)."""
+        g = cls(geometry, properties, dtype)
+        keys, masks = dev.layout()
+        g._keys, g._masks, g._lin = keys, masks, g._linear(keys)
+        g._data = {p: None for p in g.props}
+        g._dev = dev
+        g._dev_newer = True
+        g._host_newer = False
         return g
 
     def _linear(self, keys: np.ndarray) -> np.ndarray:
@@ -666,6 +681,36 @@ class DeviceGrid:
     def fill_const(self, prop: int, value: float):
         _check(lib.pd_grid_fill_const(self.h, prop, value))
 
+    @classmethod
+    def full(cls, geom: GridGeometry, n_props: int, prop_phi: int = -1, phi_value: float = 0.0,
+             dtype=np.float64, device=0) -> "DeviceGrid":
+        """Every node active (build_free_box_grid, analysis.hpp:147-153)."""
+        size = (C.c_int64 * 3)(*(list(geom.size) + [1] * (3 - geom.dims)))
+        spacing = (C.c_double * 3)(*(list(geom.spacing) + [1.0] * (3 - geom.dims)))
+        h = C.c_void_p()
+        _check(lib.pd_grid_create_full(geom.dims, np.dtype(dtype).itemsize, size, spacing, n_props, prop_phi,
+                                       phi_value, device, C.byref(h)))
+        n = C.c_int64()
+        lib.pd_grid_info(h, C.byref(n), None)
+        return cls(h, geom, dtype, int(n.value), n_props)
+
+    @staticmethod
+    def _box(lo, hi):
+        return (C.c_int64 * 3)(*(list(lo) + [0] * (3 - len(lo)))), (C.c_int64 * 3)(*(list(hi) + [1] * (3 - len(hi))))
+
+    def box_sum(self, prop: int, lo, hi) -> float:
+        """Lexicographic sequential sum of the active values in [lo, hi)."""
+        a, b = self._box(lo, hi)
+        out = C.c_double()
+        _check(lib.pd_grid_box_sum(self.h, prop, a, b, C.byref(out)))
+        return out.value
+
+    def frap_init(self, prop_u: int, prop_d: int, lo, hi, d_molecular: float):
+        a, b = self._box(lo, hi)
+        region, phase = C.c_int64(), C.c_int64()
+        _check(lib.pd_grid_frap_init(self.h, prop_u, prop_d, a, b, d_molecular, C.byref(region), C.byref(phase)))
+        return int(region.value), int(phase.value)
+
     def close(self):
         if self.h is not None and self.h.value:
             lib.pd_grid_destroy(self.h)
@@ -787,6 +832,20 @@ class FtcsStepper:
         rows = self.run(step_index, 1, step_index + 1)
         return rows[0]
 
+    def set_region(self, lo, hi):
+        a, b = DeviceGrid._box(lo, hi)
+        _check(lib.pd_stepper_set_region(self.h, a, b))
+        self._has_region = True
+
+    def region_sums(self) -> List[float]:
+        if not getattr(self, "_has_region", False):
+            return []
+        n = C.c_int64()
+        lib.pd_stepper_region_sums(self.h, None, 0, C.byref(n))
+        buf = (C.c_double * max(1, n.value))()
+        lib.pd_stepper_region_sums(self.h, buf, n.value, C.byref(n))
+        return list(buf[: n.value])
+
     def last_ms(self) -> float:
         ms = C.c_double()
         lib.pd_stepper_last_ms(self.h, C.byref(ms))
@@ -829,10 +888,15 @@ def total_mass(grid: SparseBlockGrid, channel: str = "u") -> float:
 
 
 def run_simulation(grid: SparseBlockGrid, config: SimulationConfig,
-                   observers: Sequence[Callable[[SparseBlockGrid, StepDiagnostics], None]] = ()
-                   ) -> SimulationResult:
-    """solver.hpp:489-519."""
+                   observers: Sequence[Callable[[SparseBlockGrid, StepDiagnostics], None]] = (),
+                   region: Optional[Tuple[Sequence[int], Sequence[int]]] = None) -> SimulationResult:
+    """solver.hpp:489-519. ``region=(lo, hi)`` attaches the device
+    region-mass observer of run_frap (analysis.hpp:211-219): the result then
+    carries the box sum of u for every diagnostics row."""
     stepper = FtcsStepper(grid, config)
+    sums: List[float] = []
+    if region is not None:
+        stepper.set_region(*region)
     try:
         if config.enforce_stability:
             bound = stepper.stability_bound()
@@ -849,9 +913,12 @@ def run_simulation(grid: SparseBlockGrid, config: SimulationConfig,
                 obs(grid, d)
 
         record(stepper.snapshot_diagnostics())
+        if region is not None:
+            sums.append(stepper.dev.box_sum(grid.property_index("u"), *region))
         n = config.n_steps
         if not observers:
             diags.extend(stepper.run(0, n, n))
+            sums.extend(stepper.region_sums())
         else:
             s = 0
             while s < n:
@@ -859,8 +926,9 @@ def run_simulation(grid: SparseBlockGrid, config: SimulationConfig,
                 nxt = min(n, ((s // config.record_every) + 1) * config.record_every)
                 for d in stepper.run(s, nxt - s, n):
                     record(d)
+                sums.extend(stepper.region_sums())
                 s = nxt
-        return SimulationResult(diags)
+        return SimulationResult(diags, sums)
     finally:
         stepper.close()
 
