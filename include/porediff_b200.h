@@ -223,6 +223,51 @@ int pd_stepper_set_region(pd_stepper* s, const int64_t* lo, const int64_t* hi);
 /* Box sums of the rows produced by the last pd_stepper_run (row order). */
 int pd_stepper_region_sums(const pd_stepper* s, double* out, int64_t cap, int64_t* n);
 
+/* ---- level-set geometry stage (north_star subsystem 2; reference
+ *      levelset.hpp:13-191, geometry.hpp:67-176, dense_field.hpp:12-82) ----- */
+
+/* A dense field on the device: one T array over the box, axis 0 fastest
+ * (DenseField<T,Dims>, dense_field.hpp:12-82; grid_geometry.hpp:73-77). */
+typedef struct pd_field pd_field;
+
+/* porediff::LevelSetOptions (levelset.hpp:13-20). */
+typedef struct pd_levelset_options {
+    int32_t max_iterations;       /* 1000 */
+    double tolerance;             /* 1e-3: stop when max band update < tolerance*h */
+    double pseudo_time_step;      /* 0.5 (units of h) */
+    double band_width_for_error;  /* 4.0 (unused by the sweep) */
+    double residual_band_width;   /* 6.0: |phi| <= width*h nodes monitored */
+    int32_t rescale_initial;      /* 1: start from sign(phi)*h */
+} pd_levelset_options;
+
+/* porediff::RedistanceDiagnostics (levelset.hpp:22-26). */
+typedef struct pd_redistance_diag {
+    int32_t iterations;
+    double final_residual;  /* last max band update, in units of h */
+    int32_t converged;
+} pd_redistance_diag;
+
+int pd_field_create(int dims, int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
+                    int device, pd_field** out);
+int pd_field_destroy(pd_field* f);
+int pd_field_upload(pd_field* f, const void* host_values);
+int pd_field_download(pd_field* f, void* host_values);
+int pd_field_device_ptr(pd_field* f, void** ptr);
+/* mask_to_indicator (geometry.hpp:67-77): bits (one byte per voxel, axis 0
+ * fastest) -> +1 / -1. */
+int pd_field_from_mask(pd_field* f, const uint8_t* host_bits, int64_t n_bits);
+/* filter_thin_features (geometry.hpp:121-142): opening of the positive phase
+ * by a cubic window of min_thickness_cells nodes per axis, in place. */
+int pd_field_filter_thin(pd_field* f, int min_thickness_cells);
+/* sussman_redistance (levelset.hpp:115-191), in place; bit-exact sweeps and
+ * stopping rule. */
+int pd_field_redistance(pd_field* f, const pd_levelset_options* opts, pd_redistance_diag* out);
+/* build_sparse_grid (geometry.hpp:148-176) from a device level set: a node is
+ * active iff T(b_low)+eps < phi < T(b_up)-eps; chunks in ascending linear
+ * index; phi copied into prop_phi, other properties zero. */
+int pd_build_grid_from_field(const pd_field* f, double b_low, double b_up, int n_props, int prop_phi,
+                             pd_grid** out);
+
 #ifdef __cplusplus
 }
 #endif

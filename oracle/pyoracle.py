@@ -117,6 +117,25 @@ class Ref:
         L.ref_worker_count.restype = C.c_int
         L.ref_frap_fit.argtypes = [P, C.c_double, C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_double, P, P, P, P, P, P]
+        L.ref_field_redistance.argtypes = [C.c_int, C.c_int, P, P, P, P, P]
+        L.ref_field_filter_thin.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int]
+
+    def field_redistance(self, size, spacing, values, opts):
+        """sussman_redistance on a dense field (axis 0 fastest); returns
+        (code, message, field, (iterations, final_residual, converged))."""
+        from paper_2304_11165_b200._lib import pd_levelset_options, pd_redistance_diag
+        v = np.ascontiguousarray(values).copy()
+        o = pd_levelset_options(*opts)
+        d = pd_redistance_diag()
+        code = self.L.ref_field_redistance(len(size), v.dtype.itemsize, _p(size, np.int64),
+                                           _p(list(spacing), np.float64), v.ctypes.data, C.byref(o), C.byref(d))
+        return code, self.last_error(), v, (d.iterations, d.final_residual, bool(d.converged))
+
+    def field_filter_thin(self, size, spacing, values, w):
+        v = np.ascontiguousarray(values).copy()
+        code = self.L.ref_field_filter_thin(len(size), v.dtype.itemsize, _p(size, np.int64),
+                                            _p(list(spacing), np.float64), v.ctypes.data, w)
+        return code, self.last_error(), v
 
     def last_error(self):
         return (self.L.ref_last_error() or b"").decode()

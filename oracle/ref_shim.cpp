@@ -24,6 +24,7 @@
 #include "porediff/sparse_block_grid.hpp"
 #include "porediff/synthetic.hpp"
 #include "porediff/config.hpp"
+#include "porediff/levelset.hpp"
 
 #include "porediff_b200.h"  // pd_sim_config / pd_diag layouts only
 
@@ -386,6 +387,57 @@ int ref_frap_fit(void* h, double bleach_fraction, double d_molecular, double t_f
             *tau = fit.tau_d;
             *residual = fit.fit_residual;
         }
+    });
+}
+
+/* ---- level-set stage (levelset.hpp:115-191, geometry.hpp:121-142), dense
+ *      fields in place ------------------------------------------------------- */
+
+}  // extern "C"
+
+namespace {
+template <class T, int D, class F>
+int with_field(const int64_t* size, const double* spacing, void* data, F&& f) {
+    return guarded([&] {
+        auto geom = geom_of<D>(size, spacing, nullptr);
+        pd::DenseField<T, D> field(geom);
+        std::memcpy(field.data(), data, sizeof(T) * (size_t)geom.node_count());
+        f(field);
+        std::memcpy(data, field.data(), sizeof(T) * (size_t)geom.node_count());
+    });
+}
+template <class F>
+int dispatch_field(int dims, int tbytes, const int64_t* size, const double* spacing, void* data, F&& f) {
+    if (dims == 3 && tbytes == 8) return with_field<double, 3>(size, spacing, data, f);
+    if (dims == 2 && tbytes == 8) return with_field<double, 2>(size, spacing, data, f);
+    if (dims == 3) return with_field<float, 3>(size, spacing, data, f);
+    return with_field<float, 2>(size, spacing, data, f);
+}
+}  // namespace
+
+extern "C" {
+
+int ref_field_redistance(int dims, int tbytes, const int64_t* size, const double* spacing, void* data,
+                         const pd_levelset_options* o, pd_redistance_diag* out) {
+    return dispatch_field(dims, tbytes, size, spacing, data, [&](auto& field) {
+        pd::LevelSetOptions opts;
+        opts.max_iterations = o->max_iterations;
+        opts.tolerance = o->tolerance;
+        opts.pseudo_time_step = o->pseudo_time_step;
+        opts.band_width_for_error = o->band_width_for_error;
+        opts.residual_band_width = o->residual_band_width;
+        opts.rescale_initial = o->rescale_initial != 0;
+        const auto d = pd::sussman_redistance(field, opts);
+        out->iterations = d.iterations;
+        out->final_residual = d.final_residual;
+        out->converged = d.converged;
+    });
+}
+
+int ref_field_filter_thin(int dims, int tbytes, const int64_t* size, const double* spacing, void* data,
+                          int min_thickness_cells) {
+    return dispatch_field(dims, tbytes, size, spacing, data, [&](auto& field) {
+        field = pd::filter_thin_features(field, min_thickness_cells);
     });
 }
 

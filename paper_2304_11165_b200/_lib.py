@@ -59,6 +59,21 @@ class pd_diag(C.Structure):
     ]
 
 
+class pd_levelset_options(C.Structure):
+    _fields_ = [
+        ("max_iterations", C.c_int32),
+        ("tolerance", C.c_double),
+        ("pseudo_time_step", C.c_double),
+        ("band_width_for_error", C.c_double),
+        ("residual_band_width", C.c_double),
+        ("rescale_initial", C.c_int32),
+    ]
+
+
+class pd_redistance_diag(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("final_residual", C.c_double), ("converged", C.c_int32)]
+
+
 _P = C.c_void_p
 _I64P = C.POINTER(C.c_int64)
 _DP = C.POINTER(C.c_double)
@@ -102,6 +117,15 @@ _SIGNATURES = [
     ("pd_grid_box_sum", C.c_int, [_P, C.c_int, _I64P, _I64P, _DP]),
     ("pd_stepper_set_region", C.c_int, [_P, _I64P, _I64P]),
     ("pd_stepper_region_sums", C.c_int, [_P, _DP, C.c_int64, _I64P]),
+    ("pd_field_create", C.c_int, [C.c_int, C.c_int, _I64P, _DP, _DP, C.c_int, C.POINTER(_P)]),
+    ("pd_field_destroy", C.c_int, [_P]),
+    ("pd_field_upload", C.c_int, [_P, _P]),
+    ("pd_field_download", C.c_int, [_P, _P]),
+    ("pd_field_device_ptr", C.c_int, [_P, C.POINTER(_P)]),
+    ("pd_field_from_mask", C.c_int, [_P, _P, C.c_int64]),
+    ("pd_field_filter_thin", C.c_int, [_P, C.c_int]),
+    ("pd_field_redistance", C.c_int, [_P, C.POINTER(pd_levelset_options), C.POINTER(pd_redistance_diag)]),
+    ("pd_build_grid_from_field", C.c_int, [_P, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(_P)]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

@@ -146,6 +146,11 @@ int march_counters_per_step();
 void march_free(MarchPlan* plan);
 void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction);
 
+// Grid construction helpers (pd_grid.cu).
+void init_geometry(pd_grid* g, int dims, int tbytes, const int64_t* size, const double* spacing, int device);
+void alloc_columns(pd_grid* g, int n_props);
+void count_active(pd_grid* g);
+
 // Sequential lexicographic (axis 0 fastest) double sum of the active nodes of
 // a column inside the box [lo, hi) into *dst (device) — the run_frap region
 // observer (analysis.hpp:211-219), pd_frap.cu.
