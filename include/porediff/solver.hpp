@@ -255,6 +255,42 @@ class FtcsStepper {
         return s;
     }
 
+    /// Attaches the device region-mass observer (run_frap): every recorded
+    /// step of advance() also yields the lexicographic sum of u over [lo, hi).
+    void set_region(const NodeIndex<Dims>& lo, const NodeIndex<Dims>& hi) {
+        bind();
+        region_ = true;
+        lo_ = lo;
+        hi_ = hi;
+        std::int64_t a[3] = {0, 0, 0}, b[3] = {1, 1, 1};
+        for (int k = 0; k < Dims; ++k) {
+            a[k] = lo[k];
+            b[k] = hi[k];
+        }
+        b200::check(pd_stepper_set_region(st_, a, b));
+    }
+
+    /// Region sums of the rows of the last advance() (row order).
+    std::vector<double> region_sums() const {
+        std::int64_t n = 0;
+        b200::check(pd_stepper_region_sums(st_, nullptr, 0, &n));
+        std::vector<double> out(static_cast<std::size_t>(n));
+        b200::check(pd_stepper_region_sums(st_, out.data(), n, &n));
+        return out;
+    }
+
+    /// Region sum of the current u (the step-0 row).
+    double region_sum_now() const {
+        std::int64_t a[3] = {0, 0, 0}, b[3] = {1, 1, 1};
+        for (int k = 0; k < Dims; ++k) {
+            a[k] = lo_[k];
+            b[k] = hi_[k];
+        }
+        double m = 0.0;
+        b200::check(pd_grid_box_sum(dev_.get(), i_u_, a, b, &m));
+        return m;
+    }
+
     /// Device time of the last advance()'s step kernels (CUDA events).
     double last_device_ms() const {
         double ms = 0.0;
@@ -296,6 +332,7 @@ class FtcsStepper {
         st_ = nullptr;
         dev_ = std::move(dev);
         b200::check(pd_stepper_create(dev_.get(), &c_, i_phi_, i_u_, i_d_, i_next_, &st_));
+        if (region_) set_region(lo_, hi_);
     }
 
     Grid& grid_;
@@ -304,6 +341,8 @@ class FtcsStepper {
     int i_phi_ = -1, i_u_ = -1, i_d_ = -1, i_next_ = -1, i_src_ = -1;
     std::shared_ptr<pd_grid> dev_;
     pd_stepper* st_ = nullptr;
+    bool region_ = false;
+    NodeIndex<Dims> lo_{}, hi_{};
 };
 
 template <typename T, int Dims>
@@ -320,12 +359,14 @@ struct SimulationResult {
     std::vector<StepDiagnostics> diagnostics;  // step 0 plus every recorded step
 };
 
-/// Reference solver.hpp:489-519. Without observers the whole run is one
-/// device call; with observers the run is split at record points so each
-/// observer sees the grid at exactly the recorded step.
+namespace detail {
+
+/// run_simulation core; with `region` (lo, hi) the device region-mass
+/// observer of run_frap is attached and its per-row sums appended to `sums`.
 template <typename T, int Dims>
-SimulationResult run_simulation(SparseBlockGrid<T, Dims>& grid, const SimulationConfig& config,
-                                const std::vector<SimulationObserver<T, Dims>>& observers = {}) {
+SimulationResult run_simulation_impl(SparseBlockGrid<T, Dims>& grid, const SimulationConfig& config,
+                                     const std::vector<SimulationObserver<T, Dims>>& observers,
+                                     const NodeIndex<Dims>* region, std::vector<double>* sums) {
     FtcsStepper<T, Dims> stepper(grid, config);
     if (config.enforce_stability) {
         const double bound = stepper.stability_bound();
@@ -334,23 +375,40 @@ SimulationResult run_simulation(SparseBlockGrid<T, Dims>& grid, const Simulation
                                   format_scalar(bound) + " (dt must be strictly below it; max D = " +
                                   format_scalar(max_diffusivity(grid)) + ")");
     }
+    if (region) stepper.set_region(region[0], region[1]);
     SimulationResult result;
     auto record = [&](const StepDiagnostics& d) {
         result.diagnostics.push_back(d);
         for (const auto& obs : observers) obs(grid, d);
     };
     record(stepper.snapshot_diagnostics());
+    if (region) sums->push_back(stepper.region_sum_now());
     const std::int64_t n = config.n_steps;
     if (observers.empty()) {
         for (const auto& d : stepper.advance(0, n, n)) result.diagnostics.push_back(d);
+        if (region)
+            for (double m : stepper.region_sums()) sums->push_back(m);
         return result;
     }
     for (std::int64_t s = 0; s < n;) {
         const std::int64_t next = std::min(n, (s / config.record_every + 1) * config.record_every);
         for (const auto& d : stepper.advance(s, next - s, n)) record(d);
+        if (region)
+            for (double m : stepper.region_sums()) sums->push_back(m);
         s = next;
     }
     return result;
+}
+
+}  // namespace detail
+
+/// Reference solver.hpp:489-519. Without observers the whole run is one
+/// device call; with observers the run is split at record points so each
+/// observer sees the grid at exactly the recorded step.
+template <typename T, int Dims>
+SimulationResult run_simulation(SparseBlockGrid<T, Dims>& grid, const SimulationConfig& config,
+                                const std::vector<SimulationObserver<T, Dims>>& observers = {}) {
+    return detail::run_simulation_impl(grid, config, observers, nullptr, nullptr);
 }
 
 }  // namespace porediff

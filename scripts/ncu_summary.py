@@ -18,7 +18,7 @@ for k, x in zip(h, v):
 print("-- stalls per issue")
 st = [(k, float(x)) for k, x in zip(h, v) if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")]
 for k, x in sorted(st, key=lambda t: -t[1])[:12]:
-    print(f"  {k[34:-30]:30s} {x:.3f}")
+    print(f"  {k[34:-23]:30s} {x:.3f}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hh = rows[1]
