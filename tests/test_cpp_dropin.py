@@ -1,5 +1,6 @@
-"""The reference's own GoogleTest suites for the FTCS path
-(/root/reference/proj/tests/{solver,grid,geometry}_test.cpp), compiled here by
+"""The reference's own GoogleTest suites for the FTCS path and its geometry /
+analysis layers (/root/reference/proj/tests/{solver,grid,geometry,levelset,
+analysis}_test.cpp), compiled here by
 cpp/Makefile against the drop-in headers in include/porediff (whose solver
 executes on the B200 through libporediff_b200.so), plus cpp/dropin_test.cpp
 (host/device mirror coherence). The binaries are built in this container and
@@ -41,6 +42,21 @@ def test_reference_host_suites(suite):
 @pytest.mark.gpu
 def test_reference_solver_suite_on_b200():
     out = _run("solver_test")
+    assert "[  PASSED  ]" in out
+
+
+@pytest.mark.gpu
+def test_reference_levelset_suite_on_b200():
+    # sussman_redistance runs on the device (pd_field_redistance)
+    out = _run("levelset_test")
+    assert "[  PASSED  ]" in out
+
+
+@pytest.mark.gpu
+def test_reference_analysis_suite_on_b200():
+    # run_frap / fit_effective_D: every FTCS run and the region observer on
+    # the device
+    out = _run("analysis_test")
     assert "[  PASSED  ]" in out
 
 
