@@ -234,6 +234,8 @@ def run_ours(args):
     launches = dom.launches(stepper) - launches0
     if world > 1:
         launches += 4 * args.steps
+    # exact global diagnostics of the final state (all ranks take part)
+    diag = dom.diagnostics(stepper)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     act_t = torch.tensor([dom.owned_active], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -279,6 +281,8 @@ def run_ours(args):
             "roofline_frac_of_step": dom.owned_active * BYTES_PER_UPDATE / (step_ms / 1e3) / 1e9 / peak,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "wall_s_timed_region": wall,
+            "final_diagnostics": {"total_mass": diag[0], "min_u": diag[1], "max_u": diag[2],
+                                  "note": "exact across ranks: rank-ordered per-chunk partials + pairwise_sum"},
         }
         print(json.dumps(line))
     if world > 1:

@@ -148,6 +148,28 @@ int pd_stepper_destroy(pd_stepper* s);
  * [begin, end) — the chunks a rank owns under z-slab sharding; the other
  * chunks of the grid are read-only ghost halos. Default: all chunks. */
 int pd_stepper_set_range(pd_stepper* s, int64_t begin, int64_t end);
+/* Asynchronous stepping for overlapped multi-GPU runs. Enqueues the step
+ * kernel for the owned sub-range [begin, end) on the grid's stream (see
+ * pd_grid_set_stream): reads logical u, writes logical u_next, no swap, no
+ * diagnostics, no host synchronisation. Steps are stream-ordered; a
+ * non-finite node is recorded on the device and reported by
+ * pd_stepper_status. pd_stepper_swap then swaps u / u_next
+ * (solver.hpp:262) once every sub-range of the step has been enqueued. */
+int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t end, double factor);
+int pd_stepper_swap(pd_stepper* s);
+/* Synchronises and reports (then clears) a non-finite node of the enqueued
+ * steps as numeric_error "non-finite value at step <step_number>, node (...)". */
+int pd_stepper_status(pd_stepper* s, int64_t step_number);
+/* Exact diagnostics across ranks: per-chunk sequential mass and
+ * min / max of the current u over the owned range, into caller device arrays
+ * of end-begin doubles (stream-ordered). Ranks own ascending ordinal ranges,
+ * so their arrays concatenated in rank order are the global per-chunk
+ * partials; pd_reduce_partials folds them exactly like total_mass /
+ * snapshot_diagnostics (pairwise_sum over global ordinals, parallel.hpp:68-84;
+ * left-preference min/max) into row = {mass*cell_volume, min, max}. */
+int pd_stepper_partials(pd_stepper* s, double* dev_mass, double* dev_min, double* dev_max);
+int pd_reduce_partials(pd_grid* g, const double* dev_mass, const double* dev_min, const double* dev_max, int64_t n,
+                       double* row);
 /* Strict stability bound for the grid's current D (solver.hpp:220-224). */
 int pd_stepper_stability_bound(pd_stepper* s, double* out);
 /* Step-0 row (snapshot_diagnostics, solver.hpp:282-301). */

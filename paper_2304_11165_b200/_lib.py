@@ -117,6 +117,11 @@ _SIGNATURES = [
     ("pd_grid_box_sum", C.c_int, [_P, C.c_int, _I64P, _I64P, _DP]),
     ("pd_stepper_set_region", C.c_int, [_P, _I64P, _I64P]),
     ("pd_stepper_region_sums", C.c_int, [_P, _DP, C.c_int64, _I64P]),
+    ("pd_stepper_enqueue", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_double]),
+    ("pd_stepper_swap", C.c_int, [_P]),
+    ("pd_stepper_status", C.c_int, [_P, C.c_int64]),
+    ("pd_stepper_partials", C.c_int, [_P, _P, _P, _P]),
+    ("pd_reduce_partials", C.c_int, [_P, _P, _P, _P, C.c_int64, _DP]),
     ("pd_field_create", C.c_int, [C.c_int, C.c_int, _I64P, _DP, _DP, C.c_int, C.POINTER(_P)]),
     ("pd_field_destroy", C.c_int, [_P]),
     ("pd_field_upload", C.c_int, [_P, _P]),

@@ -463,6 +463,8 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             PD_CUDA(cudaMalloc(&s->d_bad, sizeof(unsigned long long)));
             PD_CUDA(cudaMalloc(&s->d_rows, sizeof(double) * 3 * (size_t)kBatch));
             PD_CUDA(cudaMalloc(&s->d_region, sizeof(double) * (size_t)kBatch));
+            PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)kBatch, g->stream));
+            PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
             PD_CUDA(cudaEventCreate(&s->ev0));
             PD_CUDA(cudaEventCreate(&s->ev1));
             if (g->n_chunks > 0) {
@@ -691,6 +693,106 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
             j += fail_k + 1;
         }
         s->last_ms = total_ms;
+    });
+}
+
+int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t end, double factor) {
+    return guarded([&] {
+        pd_grid* g = s->g;
+        if (begin < s->begin || end > s->end || begin > end)
+            fail(PD_E_INPUT, "enqueue range outside the stepper's owned range");
+        if (end == begin) return;
+        DeviceGuard dg(g->device);
+        (void)step_index;  // steps are stream-ordered; errors accumulate in flags[0]
+        const void* u = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
+        void* un = g->cols[(size_t)g->column_of[(size_t)s->prop_next]];
+        const unsigned nb = (unsigned)(end - begin);
+        if (g->tbytes == 8) {
+            StepArgs<double> a;
+            fill_args<double>(s, a, u, un, factor);
+            a.k = 0;
+            a.ord0 = begin;
+            if (s->use_march && s->plan.ready) {
+                auto& sp = march_sub(g, s->plan, begin, end);
+                PD_CUDA(cudaMemsetAsync(sp.d_counter, 0, sizeof(int), g->stream));
+                march_launch_sched(g, s->plan, a, s->cfg.reaction_kind, sp.d_stream, sp.n, sp.d_counter);
+            } else if (g->dims == 3) {
+                ftcs_step_kernel<double, 3, false><<<nb, 512, 0, g->stream>>>(a);
+            } else {
+                ftcs_step_kernel<double, 2, false><<<nb, 64, 0, g->stream>>>(a);
+            }
+        } else {
+            StepArgs<float> a;
+            fill_args<float>(s, a, u, un, factor);
+            a.k = 0;
+            a.ord0 = begin;
+            if (g->dims == 3)
+                ftcs_step_kernel<float, 3, false><<<nb, 512, 0, g->stream>>>(a);
+            else
+                ftcs_step_kernel<float, 2, false><<<nb, 64, 0, g->stream>>>(a);
+        }
+        PD_CUDA(cudaGetLastError());
+        s->launches++;
+    });
+}
+
+int pd_stepper_swap(pd_stepper* s) {
+    std::swap(s->g->column_of[(size_t)s->prop_u], s->g->column_of[(size_t)s->prop_next]);
+    return PD_OK;
+}
+
+int pd_stepper_status(pd_stepper* s, int64_t step_number) {
+    return guarded([&] {
+        pd_grid* g = s->g;
+        DeviceGuard dg(g->device);
+        int f = 0;
+        PD_CUDA(cudaMemcpyAsync(&f, s->d_flags, sizeof f, cudaMemcpyDeviceToHost, g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        if (!(f & 1)) {
+            PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int), g->stream));
+            PD_CUDA(cudaStreamSynchronize(g->stream));
+            return;
+        }
+        unsigned long long key = 0;
+        PD_CUDA(cudaMemcpy(&key, s->d_bad, sizeof key, cudaMemcpyDeviceToHost));
+        PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int), g->stream));
+        PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        fail(PD_E_NUMERIC, node_message(g, step_number, key));
+    });
+}
+
+int pd_stepper_partials(pd_stepper* s, double* dev_mass, double* dev_min, double* dev_max) {
+    return guarded([&] {
+        pd_grid* g = s->g;
+        DeviceGuard dg(g->device);
+        const void* u = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
+        launch_chunk_stats(g, u, g->d_masks);
+        const int64_t n = s->end - s->begin;
+        if (n > 0) {
+            double* dst[3] = {dev_mass, dev_min, dev_max};
+            for (int k = 0; k < 3; ++k)
+                PD_CUDA(cudaMemcpyAsync(dst[k], g->red.part[k] + s->begin, sizeof(double) * (size_t)n,
+                                        cudaMemcpyDeviceToDevice, g->stream));
+        }
+    });
+}
+
+int pd_reduce_partials(pd_grid* g, const double* dev_mass, const double* dev_min, const double* dev_max, int64_t n,
+                       double* row) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const int64_t cap = std::max<int64_t>(1, (n + 1023) / 1024);
+        double* scratch = nullptr;
+        PD_CUDA(cudaMalloc(&scratch, sizeof(double) * (size_t)(6 * cap + 3)));
+        const cudaError_t e0 = [&] {
+            launch_pairwise_arrays(g, dev_mass, dev_min, dev_max, n, scratch + 6 * cap, scratch);
+            return cudaMemcpyAsync(row, scratch + 6 * cap, 3 * sizeof(double), cudaMemcpyDeviceToHost, g->stream);
+        }();
+        const cudaError_t e1 = cudaStreamSynchronize(g->stream);
+        cudaFree(scratch);
+        PD_CUDA(e0);
+        PD_CUDA(e1);
     });
 }
 

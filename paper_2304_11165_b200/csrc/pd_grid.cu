@@ -488,6 +488,32 @@ void launch_pairwise_finalize(pd_grid* g, double* dst, int* flags, int64_t begin
     }
 }
 
+void launch_pairwise_arrays(pd_grid* g, const double* m, const double* a, const double* b, int64_t n,
+                            double* dst, double* scratch) {
+    // scratch: 6 * ceil(n / kPairBlock) doubles (two ping-pong triples)
+    if (n <= 0) {
+        empty_row_kernel<<<1, 1, 0, g->stream>>>(dst);
+        PD_CUDA(cudaGetLastError());
+        return;
+    }
+    const int64_t cap = (n + kPairBlock - 1) / kPairBlock;
+    double* ta[3] = {scratch, scratch + cap, scratch + 2 * cap};
+    double* tb[3] = {scratch + 3 * cap, scratch + 4 * cap, scratch + 5 * cap};
+    const double* in[3] = {m, a, b};
+    bool use_a = true;
+    while (true) {
+        const int64_t nb = (n + kPairBlock - 1) / kPairBlock;
+        double** out = use_a ? ta : tb;
+        pairwise_pass_kernel<<<(unsigned)nb, kPairBlock, 0, g->stream>>>(
+            in[0], in[1], in[2], n, out[0], out[1], out[2], nb == 1 ? dst : nullptr, g->cell_volume, nullptr);
+        PD_CUDA(cudaGetLastError());
+        if (nb == 1) break;
+        for (int k = 0; k < 3; ++k) in[k] = out[k];
+        n = nb;
+        use_a = !use_a;
+    }
+}
+
 void check_prop(const pd_grid* g, int prop) {
     if (prop < 0 || prop >= (int)g->column_of.size())
         fail(PD_E_PROPERTY, "unknown property index " + std::to_string(prop));

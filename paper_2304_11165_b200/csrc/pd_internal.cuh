@@ -139,12 +139,26 @@ struct MarchPlan {
     int grid = 0;
     int64_t n = 0;
     bool ready = false;
+    struct Sub {  // sub-range schedules (overlapped multi-GPU stepping)
+        int64_t begin = 0, end = 0, n = 0;
+        int32_t* d_stream = nullptr;
+        int* d_counter = nullptr;
+    };
+    std::vector<Sub> subs;
 };
 void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const uint64_t* d_sink,
                  const void* d_dcol, int dirichlet, int64_t begin, int64_t end, MarchPlan* plan);
 int march_counters_per_step();
 void march_free(MarchPlan* plan);
 void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction);
+int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end);
+MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end);
+void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
+                        int64_t n, int* counter);
+// pairwise_sum + left-preference min/max fold of caller arrays (n leaves)
+// into dst[0..2] = {sum*cell_volume, min, max} (pd_grid.cu).
+void launch_pairwise_arrays(pd_grid* g, const double* m, const double* a, const double* b, int64_t n,
+                            double* dst, double* scratch);
 
 // Grid construction helpers (pd_grid.cu).
 void init_geometry(pd_grid* g, int dims, int tbytes, const int64_t* size, const double* spacing, int device);

@@ -1060,12 +1060,48 @@ __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __r
 }
 
 void march_free(MarchPlan* p) {
+    for (auto& sp : p->subs) {
+        cudaFree(sp.d_stream);
+        cudaFree(sp.d_counter);
+    }
     cudaFree(p->d_stream);
     cudaFree(p->d_desc);
     cudaFree(p->d_deff);
     cudaFree(p->d_counter);
     cudaFree(p->d_lm);
     *p = MarchPlan{};
+}
+
+// Device schedule of the chunk ordinals [begin, end): (z-block of kSeg
+// layers, 4x4 column tiles, column, z), so the chunks in flight form one
+// short window and neighbour halos hit L2.
+int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end) {
+    const int64_t n = end - begin;
+    std::vector<int32_t> keys((size_t)n * 3);
+    if (n > 0)
+        PD_CUDA(cudaMemcpyAsync(keys.data(), g->d_keys + begin * 3, sizeof(int32_t) * 3 * (size_t)n,
+                                cudaMemcpyDeviceToHost, g->stream));
+    PD_CUDA(cudaStreamSynchronize(g->stream));
+    std::vector<int32_t> order((size_t)n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        const int32_t* ka = &keys[(size_t)a * 3];
+        const int32_t* kb = &keys[(size_t)b * 3];
+        const int za = ka[2] / kSeg, zb = kb[2] / kSeg;
+        if (za != zb) return za < zb;
+        if (ka[1] / 4 != kb[1] / 4) return ka[1] / 4 < kb[1] / 4;
+        if (ka[0] / 4 != kb[0] / 4) return ka[0] / 4 < kb[0] / 4;
+        if (ka[1] != kb[1]) return ka[1] < kb[1];
+        if (ka[0] != kb[0]) return ka[0] < kb[0];
+        return ka[2] < kb[2];
+    });
+    for (auto& o : order) o = (int32_t)(o + begin);
+    int32_t* d = nullptr;
+    PD_CUDA(cudaMalloc(&d, sizeof(int32_t) * std::max<size_t>(1, order.size())));
+    if (n > 0)
+        PD_CUDA(cudaMemcpyAsync(d, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, g->stream));
+    PD_CUDA(cudaStreamSynchronize(g->stream));
+    return d;
 }
 
 void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const uint64_t* d_sink,
@@ -1100,36 +1136,14 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaGetLastError());
     unsigned long long bad = 0;
     PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
-    // schedule of the owned range: (zblock, y, x, z)
-    const int64_t n = end - begin;
-    std::vector<int32_t> keys((size_t)n * 3);
-    PD_CUDA(cudaMemcpyAsync(keys.data(), g->d_keys + begin * 3, sizeof(int32_t) * 3 * (size_t)n,
-                            cudaMemcpyDeviceToHost, g->stream));
     PD_CUDA(cudaStreamSynchronize(g->stream));
     cudaFree(d_bad);
     if (bad) {  // non-finite D on a fluid node: keep the exact tile kernel
         march_free(plan);
         return;
     }
-    std::vector<int32_t> order((size_t)n);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-        const int32_t* ka = &keys[(size_t)a * 3];
-        const int32_t* kb = &keys[(size_t)b * 3];
-        // z-block, then 4x4 column tiles, then columns inside the tile, then z
-        const int za = ka[2] / kSeg, zb = kb[2] / kSeg;
-        if (za != zb) return za < zb;
-        if (ka[1] / 4 != kb[1] / 4) return ka[1] / 4 < kb[1] / 4;
-        if (ka[0] / 4 != kb[0] / 4) return ka[0] / 4 < kb[0] / 4;
-        if (ka[1] != kb[1]) return ka[1] < kb[1];
-        if (ka[0] != kb[0]) return ka[0] < kb[0];
-        return ka[2] < kb[2];
-    });
-    for (auto& o : order) o = (int32_t)(o + begin);
-    PD_CUDA(cudaMalloc(&plan->d_stream, sizeof(int32_t) * order.size()));
-    PD_CUDA(cudaMemcpyAsync(plan->d_stream, order.data(), sizeof(int32_t) * order.size(),
-                            cudaMemcpyHostToDevice, g->stream));
-    PD_CUDA(cudaStreamSynchronize(g->stream));
+    const int64_t n = end - begin;
+    plan->d_stream = march_schedule(g, begin, end);
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
     plan->grid = sms * kCtasPerSm;
@@ -1140,14 +1154,33 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
 int march_counters_per_step() { return 1; }
 
 void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction) {
+    march_launch_sched(g, p, a, reaction, p.d_stream, p.n, p.d_counter + (a.k & 1023));
+}
+
+// Sub-range schedule of the plan (built once per distinct [begin, end)).
+MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end) {
+    for (auto& sp : p.subs)
+        if (sp.begin == begin && sp.end == end) return sp;
+    MarchPlan::Sub sp;
+    sp.begin = begin;
+    sp.end = end;
+    sp.n = end - begin;
+    sp.d_stream = march_schedule(g, begin, end);
+    PD_CUDA(cudaMalloc(&sp.d_counter, sizeof(int)));
+    p.subs.push_back(sp);
+    return p.subs.back();
+}
+
+void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
+                        int64_t n, int* counter) {
     MarchArgs M;
     M.A = a;
-    M.sched = p.d_stream;
-    M.n = p.n;
+    M.sched = sched;
+    M.n = n;
     M.desc = p.d_desc;
     M.lm = p.d_lm;
     M.deff = p.d_deff;
-    M.counter = p.d_counter + (a.k & 1023);
+    M.counter = counter;
     static const int dbg = [] {
         const char* e = getenv("PD_MARCH_DBG");
         return e ? atoi(e) : 0;

@@ -18,6 +18,14 @@ identically on both sides, so they are never exchanged.
 
 The plan functions below are pure host logic (tested with gloo on CPU);
 ``Domain`` binds them to the device grid and torch.distributed NCCL.
+
+Overlap (``Domain.run``): each step enqueues the two boundary chunk layers
+first (pd_stepper_enqueue, no host sync), then the face exchange of their new
+planes runs on a communication stream (pack -> NCCL send/recv -> unpack into
+the ghost layers) while the interior layers are stepped on the compute
+stream; the next step starts after both. Record steps reduce exactly across
+ranks (``Domain.diagnostics``): per-chunk partials are gathered in rank (=
+ordinal) order and folded by the reference's pairwise tree.
 """
 from __future__ import annotations
 
@@ -75,6 +83,17 @@ def exchange_plan(keys: np.ndarray, z0: int, z1: int, rank: int, world: int) -> 
     recv_down = np.nonzero(kz == z0 - 1)[0].astype(np.int32) if rank > 0 else none
     recv_up = np.nonzero(kz == z1)[0].astype(np.int32) if rank < world - 1 else none
     return ExchangePlan(z0, z1, begin, end, send_down, send_up, recv_down, recv_up)
+
+
+def sub_ranges(keys: np.ndarray, plan: ExchangePlan):
+    """Owned ordinal range split into (bottom layer, top layer, interior):
+    only the boundary layers read ghost chunks or are read by neighbours."""
+    kz = np.asarray(keys)[:, 2]
+    b1 = int(np.searchsorted(kz, plan.z0 + 1, side="left"))
+    t0 = int(np.searchsorted(kz, plan.z1 - 1, side="left"))
+    b1 = min(max(b1, plan.begin), plan.end)
+    t0 = min(max(t0, b1), plan.end)
+    return (plan.begin, b1), (t0, plan.end), (b1, t0)
 
 
 def exchange_numpy(plan: ExchangePlan, u: np.ndarray, rank: int, world: int, dist) -> None:
@@ -137,12 +156,15 @@ class Domain:
         self.dev.populate_diffusion(0, 2, pd.DiffusionProfile(0.0, 1.0, 0.0, 4.0 * n))
         self.dev.fill_hash(1, 1)
         keys, masks = self.dev.layout()
+        self.keys = keys
         self.plan = exchange_plan(keys, z0, z1, rank, world)
+        self.ranges = sub_ranges(keys, self.plan)
         act = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).sum(axis=1)
         self.owned_active = int(act[self.plan.begin:self.plan.end].sum())
         self.owned_chunks = self.plan.end - self.plan.begin
         self.torch = torch
         self.stream = torch.cuda.current_stream(device)
+        self.comm = torch.cuda.Stream(device=device)
         lib.pd_grid_set_stream(self.dev.h, C.c_void_p(self.stream.cuda_stream))
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(f"cuda:{device}")
         self.d_send_down, self.d_send_up = t(self.plan.send_down), t(self.plan.send_up)
@@ -181,17 +203,18 @@ class Domain:
         self.cfg = cfg
         return h
 
-    def exchange(self):
-        """Device halo exchange of the logical "u" planes (after a step)."""
+    def exchange(self, prop: int = 1):
+        """Device halo exchange of the face planes of logical property `prop`
+        (1 = u after a completed step; 3 = u_next before the swap)."""
         import torch.distributed as dist
         lib, pd = self.lib, self.pd
         P = lambda t: C.c_void_p(t.data_ptr())
         ops = []
         if self.rank > 0 and len(self.plan.send_down):
-            pd._check(lib.pd_grid_pack_face(self.dev.h, 1, P(self.d_send_down), len(self.plan.send_down),
+            pd._check(lib.pd_grid_pack_face(self.dev.h, prop, P(self.d_send_down), len(self.plan.send_down),
                                             FACE_ZLO, P(self.b_send_down)))
         if self.rank < self.world - 1 and len(self.plan.send_up):
-            pd._check(lib.pd_grid_pack_face(self.dev.h, 1, P(self.d_send_up), len(self.plan.send_up),
+            pd._check(lib.pd_grid_pack_face(self.dev.h, prop, P(self.d_send_up), len(self.plan.send_up),
                                             FACE_ZHI, P(self.b_send_up)))
         if self.rank > 0:
             if len(self.plan.send_down):
@@ -207,40 +230,90 @@ class Domain:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         if self.rank > 0 and len(self.plan.recv_down):
-            pd._check(lib.pd_grid_unpack_face(self.dev.h, 1, P(self.d_recv_down), len(self.plan.recv_down),
+            pd._check(lib.pd_grid_unpack_face(self.dev.h, prop, P(self.d_recv_down), len(self.plan.recv_down),
                                               FACE_ZHI, P(self.b_recv_down)))
         if self.rank < self.world - 1 and len(self.plan.recv_up):
-            pd._check(lib.pd_grid_unpack_face(self.dev.h, 1, P(self.d_recv_up), len(self.plan.recv_up),
+            pd._check(lib.pd_grid_unpack_face(self.dev.h, prop, P(self.d_recv_up), len(self.plan.recv_up),
                                               FACE_ZLO, P(self.b_recv_up)))
 
-    def run(self, stepper, step0: int, n: int) -> float:
+    def run(self, stepper, step0: int, n: int, overlap: Optional[bool] = None) -> float:
         """Advances n steps; returns the device milliseconds (CUDA events on
-        the grid's stream) of the whole sequence."""
+        the compute stream) of the whole sequence. world == 1: one
+        pd_stepper_run call. world > 1: boundary layers, then the exchange on
+        the communication stream overlapped with the interior layers."""
         torch, lib, pd = self.torch, self.lib, self.pd
-        rows = (pd._lib.pd_diag * 1)()
-        nr = C.c_int64()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        kms = 0.0
         e0.record(self.stream)
-        if self.world == 1:
+        if overlap is None:
+            overlap = self.world > 1
+        if not overlap:
+            rows = (pd._lib.pd_diag * 1)()
+            nr = C.c_int64()
             pd._check(lib.pd_stepper_run(stepper, step0, n, 1 << 40, None, rows, C.byref(nr)))
             ms_k = C.c_double()
             lib.pd_stepper_last_ms(stepper, C.byref(ms_k))
             kms = ms_k.value
         else:
+            (b0, b1), (t0, t1), (i0, i1) = self.ranges
+            cs, comm = self.stream, self.comm
             for s in range(n):
-                pd._check(lib.pd_stepper_run(stepper, step0 + s, 1, 1 << 40, None, rows, C.byref(nr)))
-                ms_k = C.c_double()
-                lib.pd_stepper_last_ms(stepper, C.byref(ms_k))
-                kms += ms_k.value
-                self.exchange()
+                st = step0 + s
+                pd._check(lib.pd_stepper_enqueue(stepper, st, b0, b1, 1.0))
+                if (t0, t1) != (b0, b1):
+                    pd._check(lib.pd_stepper_enqueue(stepper, st, t0, t1, 1.0))
+                ev_b = torch.cuda.Event()
+                ev_b.record(cs)
+                comm.wait_event(ev_b)
+                with torch.cuda.stream(comm):
+                    lib.pd_grid_set_stream(self.dev.h, C.c_void_p(comm.cuda_stream))
+                    self.exchange(prop=3)  # new boundary planes, before the swap
+                    lib.pd_grid_set_stream(self.dev.h, C.c_void_p(cs.cuda_stream))
+                ev_c = torch.cuda.Event()
+                ev_c.record(comm)
+                pd._check(lib.pd_stepper_enqueue(stepper, st, i0, i1, 1.0))
+                cs.wait_event(ev_c)
+                pd._check(lib.pd_stepper_swap(stepper))
+            kms = None
         e1.record(self.stream)
         e1.synchronize()
+        if overlap:
+            pd._check(lib.pd_stepper_status(stepper, step0 + n))
+        ms = e0.elapsed_time(e1)
+        kms = ms if kms is None else kms  # overlapped: whole step (kernels + exchange)
         self.last_kernel_ms = kms
         self._kernel_ms += kms
         self._steps += n
-        return e0.elapsed_time(e1)
+        return ms
+
+    def diagnostics(self, stepper):
+        """Exact global (total_mass, min_u, max_u) of the current u: per-chunk
+        partials of every rank gathered in ordinal order, then the
+        reference's pairwise tree and min/max fold (pd_reduce_partials)."""
+        import torch
+        import torch.distributed as dist
+        lib, pd = self.lib, self.pd
+        dev = f"cuda:{self.device}"
+        n_own = self.plan.end - self.plan.begin
+        parts = torch.empty((3, max(1, n_own)), dtype=torch.float64, device=dev)
+        P = lambda t: C.c_void_p(t.data_ptr())
+        pd._check(lib.pd_stepper_partials(stepper, P(parts[0]), P(parts[1]), P(parts[2])))
+        if self.world > 1:
+            cnt = torch.tensor([n_own], dtype=torch.int64, device=dev)
+            cnts = [torch.zeros_like(cnt) for _ in range(self.world)]
+            dist.all_gather(cnts, cnt)
+            cnts = [int(c.item()) for c in cnts]
+            m = max(1, max(cnts))
+            pad = torch.zeros((3, m), dtype=torch.float64, device=dev)
+            pad[:, :n_own] = parts[:, :n_own]
+            allp = [torch.empty_like(pad) for _ in range(self.world)]
+            dist.all_gather(allp, pad)
+            glob = torch.cat([a[:, :c] for a, c in zip(allp, cnts)], dim=1).contiguous()
+        else:
+            glob = parts[:, :n_own].contiguous()
+        row = (C.c_double * 3)()
+        pd._check(lib.pd_reduce_partials(self.dev.h, P(glob[0]), P(glob[1]), P(glob[2]), glob.shape[1], row))
+        return row[0], row[1], row[2]
 
     def kernel_ms(self, stepper) -> float:
         """Average device time of one step kernel launch so far."""

@@ -133,3 +133,118 @@ def test_march_and_tile_kernels_agree(cuda, golden, monkeypatch):
     grid = host_case(name)
     pd.run_simulation(grid, sim_config(spec, float.fromhex(gold["dt"])))
     assert sha(grid.channel_data("u")) == gold["sha_outputs"]["u"]
+
+
+@pytest.mark.parametrize("world,n", [(2, 40), (3, 64)])
+def test_overlapped_enqueue_and_exact_diagnostics(world, n, cuda):
+    """The multi-GPU step as bench.py runs it (shard.Domain.run): boundary
+    layers enqueued first, their new planes exchanged before the swap,
+    interior layers after — emulated for `world` shards on one GPU — equals
+    the unsharded run bit for bit, and the rank-ordered partials folded by
+    pd_reduce_partials give exactly the unsharded step-N diagnostics row."""
+    import torch
+
+    from paper_2304_11165_b200 import porediff as pd
+    from paper_2304_11165_b200 import shard
+    from paper_2304_11165_b200._lib import lib
+    from paper_2304_11165_b200.synthetic import SpherePacking
+
+    geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
+    pk = SpherePacking.random((0, 0, 0), (1, 1, 1), 30, 0.07, 0.15, 5)
+    centers, radii = pk.arrays()
+    cc = (n + 7) // 8
+    full = _build(pd, lib, geom, centers, radii, (0, 0, 0), (cc, cc, cc))
+    dt = 0.45 * pd.stability_dt(geom, full.max_active(2))
+    steps = 9
+    s_full = _stepper(pd, lib, full, dt)
+    rows = (pd._lib.pd_diag * 1)()
+    nr = C.c_int64()
+    pd._check(lib.pd_stepper_run(s_full, 0, steps, 1 << 40, None, rows, C.byref(nr)))
+    want = pd._lib.pd_diag()
+    pd._check(lib.pd_stepper_snapshot_diag(s_full, C.byref(want)))
+    u_full = full.download(1)
+    keys_full, _ = full.layout()
+
+    shards = []
+    for r in range(world):
+        z0, z1 = shard.slab_bounds(cc, world, r)
+        dev = _build(pd, lib, geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)))
+        keys, _ = dev.layout()
+        plan = shard.exchange_plan(keys, z0, z1, r, world)
+        s = _stepper(pd, lib, dev, dt, (plan.begin, plan.end))
+        shards.append((dev, plan, s, keys, shard.sub_ranges(keys, plan)))
+
+    def ords(a):
+        return torch.from_numpy(np.ascontiguousarray(a, np.int32)).cuda()
+
+    for step in range(steps):
+        for dev, plan, s, _, ((b0, b1), (t0, t1), _i) in shards:
+            pd._check(lib.pd_stepper_enqueue(s, step, b0, b1, 1.0))
+            if (t0, t1) != (b0, b1):
+                pd._check(lib.pd_stepper_enqueue(s, step, t0, t1, 1.0))
+        sent = {}
+        for r, (dev, plan, s, _, _rg) in enumerate(shards):
+            for lst, face, to in ((plan.send_down, shard.FACE_ZLO, r - 1), (plan.send_up, shard.FACE_ZHI, r + 1)):
+                if len(lst):
+                    buf = torch.empty((len(lst), 64), dtype=torch.float64, device="cuda")
+                    pd._check(lib.pd_grid_pack_face(dev.h, 3, C.c_void_p(ords(lst).data_ptr()), len(lst), face,
+                                                    C.c_void_p(buf.data_ptr())))
+                    sent[(r, to)] = buf
+        for dev, plan, s, _, (_b, _t, (i0, i1)) in shards:
+            pd._check(lib.pd_stepper_enqueue(s, step, i0, i1, 1.0))
+        torch.cuda.synchronize()
+        for r, (dev, plan, s, _, _rg) in enumerate(shards):
+            for lst, face, frm in ((plan.recv_down, shard.FACE_ZHI, r - 1), (plan.recv_up, shard.FACE_ZLO, r + 1)):
+                if len(lst):
+                    pd._check(lib.pd_grid_unpack_face(dev.h, 3, C.c_void_p(ords(lst).data_ptr()), len(lst), face,
+                                                      C.c_void_p(sent[(frm, r)].data_ptr())))
+            pd._check(lib.pd_stepper_swap(s))
+        torch.cuda.synchronize()
+    for dev, plan, s, _, _rg in shards:
+        pd._check(lib.pd_stepper_status(s, steps))
+
+    lin_full = (keys_full[:, 2].astype(np.int64) * cc + keys_full[:, 1]) * cc + keys_full[:, 0]
+    pos = {int(l): i for i, l in enumerate(lin_full)}
+    parts = []
+    for dev, plan, s, keys, _rg in shards:
+        u = dev.download(1)
+        for i in range(plan.begin, plan.end):
+            j = pos[(int(keys[i, 2]) * cc + int(keys[i, 1])) * cc + int(keys[i, 0])]
+            assert np.array_equal(u[i].view(np.uint64), u_full[j].view(np.uint64)), (i, keys[i])
+        k = plan.end - plan.begin
+        p = torch.empty((3, max(1, k)), dtype=torch.float64, device="cuda")
+        pd._check(lib.pd_stepper_partials(s, C.c_void_p(p[0].data_ptr()), C.c_void_p(p[1].data_ptr()),
+                                          C.c_void_p(p[2].data_ptr())))
+        parts.append(p[:, :k])
+    glob = torch.cat(parts, dim=1).contiguous()
+    assert glob.shape[1] == len(keys_full)
+    row = (C.c_double * 3)()
+    pd._check(lib.pd_reduce_partials(shards[0][0].h, C.c_void_p(glob[0].data_ptr()), C.c_void_p(glob[1].data_ptr()),
+                                     C.c_void_p(glob[2].data_ptr()), glob.shape[1], row))
+    assert (row[0].hex(), row[1].hex(), row[2].hex()) == (want.total_mass.hex(), want.min_u.hex(), want.max_u.hex())
+    for dev, plan, s, _, _rg in shards:
+        lib.pd_stepper_destroy(s)
+        dev.close()
+    lib.pd_stepper_destroy(s_full)
+    full.close()
+
+
+def test_domain_overlapped_path_equals_batched_run(cuda):
+    """shard.Domain.run's overlapped branch (enqueue boundary layers, switch
+    the grid to the communication stream for the exchange, enqueue the
+    interior, swap) gives the same bits as one pd_stepper_run; with one rank
+    the exchange itself is empty, the stream and ordering logic is not."""
+    import torch
+
+    from paper_2304_11165_b200 import shard
+    from paper_2304_11165_b200 import synthetic as sy
+    pack = sy.pack_for_porosity(0.25, 12 / 96, 7)
+    a = shard.build_domain(96, pack, 0, 1, device=0)
+    b = shard.build_domain(96, pack, 0, 1, device=0)
+    sa, sb = a.stepper(), b.stepper()
+    a.run(sa, 0, 7, overlap=False)
+    b.run(sb, 0, 7, overlap=True)
+    torch.cuda.synchronize()
+    ua, ub = a.dev.download(1), b.dev.download(1)
+    assert np.array_equal(ua.view(np.uint64), ub.view(np.uint64))
+    assert a.diagnostics(sa) == b.diagnostics(sb)

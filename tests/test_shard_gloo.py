@@ -123,3 +123,15 @@ def test_slab_bounds_partition_and_balance():
     w = np.array([1, 1, 1, 1, 10, 10, 1, 1], float)
     b = [shard.slab_bounds(8, 2, r, w) for r in range(2)]
     assert b[0][1] == b[1][0] and b[1][1] == 8
+
+
+def test_sub_ranges_split_boundary_layers():
+    from paper_2304_11165_b200 import shard
+    # chunk layers z = 0..5 with 3 chunks each, ascending linear order
+    keys = np.array([(x, 0, z) for z in range(6) for x in range(3)], np.int32)
+    plan = shard.exchange_plan(keys, 1, 5, 1, 3)  # owns layers 1..4
+    (b0, b1), (t0, t1), (i0, i1) = shard.sub_ranges(keys, plan)
+    assert (b0, b1) == (3, 6) and (t0, t1) == (12, 15) and (i0, i1) == (6, 12)
+    one = shard.exchange_plan(keys, 2, 3, 1, 3)  # a single owned layer
+    (b0, b1), (t0, t1), (i0, i1) = shard.sub_ranges(keys, one)
+    assert (b0, b1) == (6, 9) and t0 == t1 and i0 == i1
