@@ -1,43 +1,42 @@
-// Warp-per-chunk, register-marching FTCS step for 3-D FP64 grids — the
-// bandwidth path (BASELINE.json configs C1-C5).
+// Warp-per-chunk plane-marching FTCS step for 3-D FP64 grids — the bandwidth
+// path (BASELINE.json configs C1-C5). Same per-node result, bit for bit, as
+// ftcs_step_kernel (pd_ftcs.cu) and the reference (solver.hpp:360-455).
 //
-// Same per-node result, bit for bit, as ftcs_step_kernel (pd_ftcs.cu) and the
-// reference (solver.hpp:360-455). Design (measured alternatives — a staged
-// 10^3 smem tile with CTA barriers, and a TMA/cp.async producer warp feeding
-// mbarrier-synchronised consumer warps — were latency- or producer-bound, see
-// DESIGN.md):
-//
-// * One warp owns one chunk at a time and marches its 8 z-planes; lane
-//   (y, xp) holds the x-adjacent node pair (2xp, 2xp+1) of row y in every
-//   plane. u and D of the planes z-1, z, z+1 live in registers (the z
-//   stencil), x and y neighbours come from warp shuffles, and only the
-//   chunk-face lanes read halo values from memory. No shared memory, no
-//   barriers; loads for plane z+2 are in flight while plane z is computed, and
-//   20 warps per SM keep enough bytes in flight to cover HBM latency.
-// * Pairs without an active node are never loaded (predicated 16-B loads), so
-//   empty 32-B sectors cost no HBM traffic.
-// * Contiguous halos. x faces are 8-B strided in a chunk slab, so every step
-//   also writes the x=0 / x=7 planes of u_next into a side array (64 doubles
-//   per face, contiguous) and the stepper keeps the same for D_eff; y halos
-//   are 64-B rows and z halos 512-B planes of the neighbour chunks.
-// * Schedule. Chunks are ordered (z-block of kSeg layers, 4x4 tiles of chunk
-//   columns, column, z) and claimed kBatch at a time from one atomic counter,
-//   so the chunks in flight always form one short window of that order: the
-//   z halos were streamed by the same warp a moment ago and the x/y halos by
-//   the warps next to it in the window (L2 hits). (Cutting the order into
-//   several independently claimed parts spreads y neighbours hundreds of
-//   microseconds apart and was measured to miss L2.)
-// * Usability without masks. D_eff = fluid ? D : -inf (static per run); a
+// ftcs_march14_kernel (default):
+// * Persistent, 4 CTAs x 4 warps per SM. One warp owns one chunk at a time and
+//   marches its 8 z-planes; lane (y, xp) owns the x-pair (2xp, 2xp+1) of row y.
+// * Every plane (plus the z-halo planes of the z neighbours) is staged by
+//   cp.async into the warp's continuous 8-slot ring of shared-memory tiles
+//   (rows -1..8 x 8 columns + two x-halo columns; u and D_eff), 5 loads ahead
+//   of the plane being computed, across chunk boundaries: no CTA barriers.
+//   x halos (8 B) and y halos (64-B rows) come straight from the neighbour
+//   chunks' slabs — those chunks are in flight in adjacent warps, so they hit
+//   L2 — and z halos are 512-B planes.
+// * Cells without a source in the grid (inactive pairs, missing neighbours)
+//   copy D_eff from a sentinel chunk (-inf) and never read u, so empty 32-B
+//   sectors cost no HBM traffic.
+// * Usability without masks: D_eff = fluid ? D : -inf (static per run); a
 //   neighbour is usable iff it is fluid (solver.hpp:374,379-381), i.e. iff the
 //   face sum d_a + d_b is not -inf.
-// * Face fluxes. F(a|b) = ((d_a+d_b)*0.5)*(u_b-u_a) is exactly the value both
+// * Face fluxes: F(a|b) = ((d_a+d_b)*0.5)*(u_b-u_a) is exactly what both
 //   endpoints compute in the reference (dh_p*(p.u-u_c) for a, dh_m*(u_c-m.u)
 //   for b). For a substituted face the reference computes
 //   ((d_c+d_c)*0.5)*(u_c-u_c) = +-0 when u_c, d_c are finite, and a +-0 term
 //   leaves lap = 0.0 + ... bitwise unchanged, so the fast path uses 0. Planes
-//   whose nodes and neighbours are all fluid skip the selects entirely. Nodes
-//   whose fast result is non-finite, and chunks that touch a Dirichlet outer
-//   face, take the exact generic path on the same register values.
+//   whose nodes and neighbours are all fluid skip the selects and the wall
+//   override. Non-finite fast results and Dirichlet-exposed chunks take the
+//   exact generic path on operands re-read from the ring.
+// * Schedule: chunks are ordered (z-block of kSeg layers, 4x4 tiles of chunk
+//   columns, column, z) and claimed one at a time from one atomic counter, so
+//   the chunks in flight form one short window of that order and neighbour
+//   halos hit L2 (a static interleave was measured to lose that). The claim ->
+//   schedule id -> lane masks/descriptor pipeline runs ahead through a
+//   per-warp context ring in shared memory.
+//
+// ftcs_march15_kernel<R, 1> ("v16", PD_MARCH_V=16): four nodes per lane (two
+// planes per warp iteration), ten fixed slots, 12 warps per SM, swizzled
+// tile rows. 19 % fewer instructions than v14 but not faster yet (see
+// DESIGN.md); kept for the next round's tuning.
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>
@@ -50,7 +49,7 @@ namespace pdb {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kCtasPerSm = 3;  // 3 x 4 warps x 10 slots x 1.5 KB = 180 KB of ring per SM
+constexpr int kCtasPerSm = 4;  // march v14 (default): 4 CTAs x 4 warps per SM
 constexpr int kSeg = 16;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
@@ -69,6 +68,7 @@ struct MarchArgs {
     int64_t n;
     const int32_t* __restrict__ desc;  // 8 ints per chunk: nbr[6], key, flags
     const uint32_t* __restrict__ lm;   // per chunk and lane: active / sink bits
+    const uint32_t* __restrict__ lq;   // per chunk and lane: v15 compute-side quad bits
     const double* __restrict__ deff;
     int* counter;                    // chunk-claim counter of this step
     int static_sched;                // 1: static interleaved positions (no atomics)
@@ -144,10 +144,6 @@ struct Tile {
 constexpr uint32_t kTileBytes = sizeof(Tile);                  // 1536
 constexpr uint32_t kDOff = (uint32_t)offsetof(Tile, d);        // u -> D_eff distance (bytes)
 constexpr uint32_t kHxOff = (uint32_t)offsetof(Tile, hxu);     // x-halo column (bytes)
-// Fixed-slot ring: load i (0..9) of every chunk goes to slot i (i = 0: the
-// z- halo plane, 1..8: body planes 0..7, 9: the z+ halo plane), so every
-// shared-memory address in the unrolled chunk body is a lane base + constant.
-constexpr int kSlots = 10;
 
 // ---- predicated asynchronous copies (LDGSTS), one predicate per pair ----
 __device__ __forceinline__ void cp16x2(uint32_t su, const double* gu, uint32_t sd, const double* gd,
@@ -178,18 +174,6 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Load side of one chunk, per lane: global sources of everything the lane
-// copies (plane 0; plane p adds p*64 elements) and their predicates.
-struct LoadCtx {
-    const double *gu, *gd;    // own pair
-    const double *zlu, *zld;  // pair in the z- neighbour's plane 7
-    const double *zhu, *zhd;  // pair in the z+ neighbour's plane 0
-    const double *xu, *xd;    // x-halo cell (x-face lanes)
-    const double *yu, *yd;    // y-halo pair (y-face lanes)
-    uint32_t lm;              // active bits of the lane's pair (0 if no chunk)
-    bool zlok, zhok, xok, yok;
-};
-
 // Per-lane constants of the tile geometry (byte offsets inside a tile).
 struct LaneGeo {
     int y, xp;
@@ -218,65 +202,6 @@ __device__ __forceinline__ LaneGeo lane_geo(int lane) {
     return G;
 }
 
-// nb[] comes from lanes 24..29 of the descriptor word dv.
-__device__ __forceinline__ LoadCtx make_load_ctx(int c, uint32_t lm, int dv, const MarchArgs& M,
-                                                 const LaneGeo& G) {
-    int nb[6];
-#pragma unroll
-    for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
-    LoadCtx L;
-    const double* u = M.A.u;
-    const double* de = M.deff;
-    const bool ok = c >= 0;
-    const int64_t own = ok ? (int64_t)c * 512 + G.bp : 0;
-    L.gu = u + own;
-    L.gd = de + own;
-    L.lm = ok ? lm : 0u;
-    L.zlok = ok && nb[4] >= 0 && !(M.dbg & 4);
-    L.zhok = ok && nb[5] >= 0 && !(M.dbg & 4);
-    const int64_t zl = L.zlok ? (int64_t)nb[4] * 512 + 448 + G.bp : 0;
-    const int64_t zh = L.zhok ? (int64_t)nb[5] * 512 + G.bp : 0;
-    L.zlu = u + zl;
-    L.zld = de + zl;
-    L.zhu = u + zh;
-    L.zhd = de + zh;
-    const int jx = G.xp == 0 ? nb[0] : nb[1];
-    L.xok = ok && G.xface && jx >= 0 && !(M.dbg & 1);
-    const int64_t xo = L.xok ? (int64_t)jx * 512 + G.y * 8 + (G.xp == 0 ? 7 : 0) : 0;
-    L.xu = u + xo;
-    L.xd = de + xo;
-    const int jy = G.y == 0 ? nb[2] : nb[3];
-    L.yok = ok && G.yface && jy >= 0 && !(M.dbg & 2);
-    const int64_t yo = L.yok ? (int64_t)jy * 512 + (G.y == 0 ? 56 : 0) + 2 * G.xp : 0;
-    L.yu = u + yo;
-    L.yd = de + yo;
-    return L;
-}
-
-// Issues load i (0..9) of a chunk into ring slot i (slot base address sb).
-// Pairs without an active node are never read (their D_eff cells get the
-// sentinel), so empty 32-B sectors cost no HBM traffic.
-template <int I>
-__device__ __forceinline__ void issue_load(uint32_t sb, const LoadCtx& L, const LaneGeo& G) {
-    const uint32_t st = sb + (uint32_t)I * kTileBytes;
-    if (I == 0) {
-        cp16x2(st + G.s_c, L.zlu, st + kDOff + G.s_c, L.zld, L.zlok);
-        sts_sent1(st + kDOff + G.s_c, !L.zlok), sts_sent1(st + kDOff + G.s_c + 8, !L.zlok);
-    } else if (I == 9) {
-        cp16x2(st + G.s_c, L.zhu, st + kDOff + G.s_c, L.zhd, L.zhok);
-        sts_sent1(st + kDOff + G.s_c, !L.zhok), sts_sent1(st + kDOff + G.s_c + 8, !L.zhok);
-    } else {
-        constexpr int p = I - 1;
-        const bool ok = ((L.lm >> (2 * p)) & 3u) != 0u;
-        cp16x2(st + G.s_c, L.gu + p * 64, st + kDOff + G.s_c, L.gd + p * 64, ok);
-        sts_sent1(st + kDOff + G.s_c, !ok), sts_sent1(st + kDOff + G.s_c + 8, !ok);
-        cp8x2(st + G.s_hx, L.xu + p * 64, st + kDOff + G.s_hx, L.xd + p * 64, L.xok);
-        sts_sent1(st + kDOff + G.s_hx, G.xface && !L.xok);
-        cp16x2(st + G.s_hy, L.yu + p * 64, st + kDOff + G.s_hy, L.yd + p * 64, L.yok);
-        sts_sent1(st + kDOff + G.s_hy, G.yface && !L.yok), sts_sent1(st + kDOff + G.s_hy + 8, G.yface && !L.yok);
-    }
-}
-
 // |x| >= 2^990 or non-finite, from the high word (integer pipe)
 __device__ __forceinline__ bool huge(double x) {
     return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
@@ -284,12 +209,6 @@ __device__ __forceinline__ bool huge(double x) {
 
 struct Consts {
     double dt, neg_k, src_factor, ix, iy, iz;
-};
-
-struct ChunkCtx {  // compute side of a chunk
-    int c, key, flags;
-    uint32_t lm;
-    double* out;  // u_next + c*512 + bp
 };
 
 __device__ __forceinline__ double2 lds2(uint32_t a) {
@@ -358,295 +277,6 @@ __device__ __forceinline__ void stg_pair(double* p, double a, double b, bool a0,
         " @q st.global.cs.f64 [%0+8], %2;\n}\n" ::"l"(p),
         "d"(a), "d"(b), "r"((int)a0), "r"((int)a1)
         : "memory");
-}
-
-// Computes plane Z of chunk C from ring slots Z (z-1), Z+1 (z), Z+2 (z+1)
-// and stores the active nodes of the lane's pair into u_next.
-template <int REACTION, int Z>
-__device__ __forceinline__ void compute_plane(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
-                                              const ChunkCtx& C, uint32_t sb, const LaneGeo& G) {
-    const bool a0 = (C.lm >> (2 * Z)) & 1u, a1 = (C.lm >> (2 * Z + 1)) & 1u;
-    const uint32_t t0 = sb + (uint32_t)(Z + 1) * kTileBytes;
-    const uint32_t tm = sb + (uint32_t)Z * kTileBytes;
-    const uint32_t tp = sb + (uint32_t)(Z + 2) * kTileBytes;
-    const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
-    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
-    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
-    const double2 uym = lds2(t0 + G.s_c - 64), dym = lds2(t0 + kDOff + G.s_c - 64);
-    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = lds2(t0 + kDOff + G.s_c + 64);
-    const double2 uzm = lds2(tm + G.s_c), dzm = lds2(tm + kDOff + G.s_c);
-    const double2 uzp = lds2(tp + G.s_c), dzp = lds2(tp + kDOff + G.s_c);
-    // lanes without an active node compute too (results are not stored):
-    // no divergence in the plane body
-    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * Z)) & 1u);
-    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * Z)) & 1u);
-    double src0 = 0.0, src1 = 0.0;
-    if (REACTION == PD_REACTION_VOLUMETRIC) {
-        const double* sp = M.A.src + (int64_t)C.c * 512 + Z * 64 + G.bp;
-        src0 = sp[0];
-        src1 = sp[1];
-    }
-    double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
-    if ((C.flags >> (8 + Z)) & 1) {
-        // interior-fluid plane (warp-uniform): no substitution anywhere
-        fxl = fface(dL, dc.x, uL, uc.x);
-        fxi = fface(dc.x, dc.y, uc.x, uc.y);
-        fxr = fface(dc.y, dR, uc.y, uR);
-        fy0m = fface(dym.x, dc.x, uym.x, uc.x);
-        fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
-        fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
-        fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
-        fy1m = fface(dym.y, dc.y, uym.y, uc.y);
-        fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
-        fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
-        fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
-    } else {
-        fxl = face(dL, dc.x, uL, uc.x);
-        fxi = face(dc.x, dc.y, uc.x, uc.y);
-        fxr = face(dc.y, dR, uc.y, uR);
-        fy0m = face(dym.x, dc.x, uym.x, uc.x);
-        fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
-        fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
-        fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
-        fy1m = face(dym.y, dc.y, uym.y, uc.y);
-        fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
-        fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
-        fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
-    }
-    double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
-    lap0 += (fxi - fxl) * Q.ix;
-    lap0 += (fy0p - fy0m) * Q.iy;
-    lap0 += (fz0p - fz0m) * Q.iz;
-    double lap1 = 0.0;
-    lap1 += (fxr - fxi) * Q.ix;
-    lap1 += (fy1p - fy1m) * Q.iy;
-    lap1 += (fz1p - fz1m) * Q.iz;
-    double r0 = 0.0, r1 = 0.0;
-    if (REACTION == PD_REACTION_SURFACE_SINK) {
-        r0 = s0 ? Q.neg_k * uc.x : 0.0;
-        r1 = s1 ? Q.neg_k * uc.y : 0.0;
-    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-        r0 = src0 * Q.src_factor;
-        r1 = src1 * Q.src_factor;
-    }
-    double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
-    double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
-    // walls (active, not fluid) stay frozen (solver.hpp:413-417)
-    if (sentinel(dc.x)) out0 = uc.x;
-    if (sentinel(dc.y)) out1 = uc.y;
-    const bool dirichlet = (C.flags & kFlagDirichlet) != 0;  // warp-uniform
-    if (dirichlet || ((a0 && huge(out0)) | (a1 && huge(out1)))) {
-        // rare: exact generic path (Dirichlet-exposed chunks; non-finite
-        // fast results, where the +-0 substitution shortcut needs finite
-        // operands), then the error / mass flags
-        const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
-        const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
-        const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
-        const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
-        const double2 r = pair_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, C.c, C.key, C.flags, C.lm, Z, G.xp, G.y, nu0, nd0, nu1, nd1, uc.x, uc.y, dc.x,
-                                              dc.y, s0, s1, src0, src1, out0, out1);
-        out0 = r.x;
-        out1 = r.y;
-    }
-    stg_pair(C.out + Z * 64, out0, out1, a0, a1);
-}
-
-__device__ __forceinline__ void load_ctx(const MarchArgs& M, int c, int lane, uint32_t& lm, int& dv) {
-    lm = 0u;
-    dv = -1;
-    if (c < 0) return;
-    lm = __ldg(&M.lm[(int64_t)c * 32 + lane]);
-    if (lane >= 24) dv = __ldg(&M.desc[(int64_t)c * 8 + lane - 24]);
-}
-
-__device__ __forceinline__ ChunkCtx make_ctx(const MarchArgs& M, int c, uint32_t lm, int dv, const LaneGeo& G) {
-    ChunkCtx C;
-    C.c = c;
-    C.lm = c >= 0 ? lm : 0u;
-    C.key = __shfl_sync(0xffffffffu, dv, 30);
-    C.flags = __shfl_sync(0xffffffffu, dv, 31);
-    C.out = M.A.un + (c >= 0 ? (int64_t)c * 512 + G.bp : 0);
-    return C;
-}
-
-// One warp streams a sequence of chunks. Each chunk needs 10 plane loads
-// (z- halo, body planes 0..7, z+ halo) into the fixed slots 0..9 of the
-// warp's ring; the body of the chunk loop is unrolled over the 8 planes, and
-// the loads of the next chunk are issued as soon as the slots they overwrite
-// have been consumed:
-//   after plane z: 0 -> load 8, 1 -> load 9, 2 -> next 0+1, 3..6 -> next 2..5,
-//   7 -> next 6+7   (one commit group each)
-// so before plane z at most 4 (z <= 4) or 5 (z >= 5) groups may be pending.
-template <int REACTION, int OCC>
-__global__ void __launch_bounds__(kThreads, OCC) ftcs_march_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ SlowConsts K;
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const StepArgs<double>& A = M.A;
-    if (A.k > 0) {
-        const int prev = A.flags[A.k - 1];
-        if (prev) {
-            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
-            return;
-        }
-    }
-    if (t == 0) {
-        for (int a = 0; a < 3; ++a) {
-            K.size[a] = A.size[a];
-            K.inv_dx2[a] = A.inv_dx2[a];
-        }
-        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
-        K.dt = A.dt;
-        K.neg_k = A.neg_k;
-        K.src_factor = A.src_factor;
-        K.dirichlet = A.dirichlet;
-    }
-    __syncthreads();
-    Consts Q;
-    Q.dt = A.dt;
-    Q.neg_k = A.neg_k;
-    Q.src_factor = A.src_factor;
-    Q.ix = A.inv_dx2[0];
-    Q.iy = A.inv_dx2[1];
-    Q.iz = A.inv_dx2[2];
-    const LaneGeo G = lane_geo(lane);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kSlots * kTileBytes;
-
-    // chunk pipeline: claim position (3 ahead) -> schedule id (2 ahead) ->
-    // lane mask + descriptor (1 ahead) -> load context -> compute.
-    // Positions are claimed from one atomic counter (dynamic, default) or
-    // statically interleaved over the warps of the grid (PD_MARCH_STATIC=1).
-    int* ctr = M.counter;
-    const int n = (int)M.n;
-    const bool stat = M.static_sched != 0;
-    const int gw = blockIdx.x * kWarps + warp, gstride = gridDim.x * kWarps;
-    int spos = gw;
-    // Dynamic claims are issued one chunk before their result is needed. The
-    // counter address is made opaque (ctr + (lane & zero), zero = 0) so ptxas
-    // does not turn the atomic into a warp-aggregated one, whose immediate
-    // result shuffle would expose the atomic's round trip.
-    int* ctr_l = ctr + ((t >> 5) & M.zero);
-    auto claim_issue = [&](int& r) {
-        if (stat) {
-            r = spos;
-            spos += gstride;
-        } else if (lane == 0) {
-            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(ctr_l) : "memory");
-        }
-    };
-    auto claim_get = [&](int r) -> int { return stat ? r : __shfl_sync(0xffffffffu, r, 0); };
-    auto claim = [&]() -> int {
-        int r = 0;
-        claim_issue(r);
-        return claim_get(r);
-    };
-    auto sched = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
-    const int p0 = claim();
-    const int idC = sched(p0);
-    if (idC < 0) return;
-    const int p1 = claim();
-    int idN = sched(p1);
-    int pNN = claim();
-    uint32_t lmC;
-    int dvC;
-    load_ctx(M, idC, lane, lmC, dvC);
-    uint32_t lmN;
-    int dvN;
-    load_ctx(M, idN, lane, lmN, dvN);
-    int idNN = sched(pNN);
-    int raw = 0;
-    claim_issue(raw);
-
-    ChunkCtx C = make_ctx(M, idC, lmC, dvC, G);
-    LoadCtx L = make_load_ctx(idC, lmC, dvC, M, G);
-    // prologue: groups {0,1}, 2, 3, 4, 5, {6,7}
-    issue_load<0>(sb, L, G);
-    issue_load<1>(sb, L, G);
-    cp_commit();
-    issue_load<2>(sb, L, G);
-    cp_commit();
-    issue_load<3>(sb, L, G);
-    cp_commit();
-    issue_load<4>(sb, L, G);
-    cp_commit();
-    issue_load<5>(sb, L, G);
-    cp_commit();
-    issue_load<6>(sb, L, G);
-    issue_load<7>(sb, L, G);
-    cp_commit();
-    LoadCtx LN;
-#pragma unroll 1
-    while (C.c >= 0) {
-        cp_wait<4>();
-        __syncwarp();
-        compute_plane<REACTION, 0>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<8>(sb, L, G);
-        cp_commit();
-
-        cp_wait<4>();
-        __syncwarp();
-        compute_plane<REACTION, 1>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<9>(sb, L, G);
-        cp_commit();
-
-        cp_wait<4>();
-        __syncwarp();
-        compute_plane<REACTION, 2>(M, K, Q, C, sb, G);
-        __syncwarp();
-        LN = make_load_ctx(idN, lmN, dvN, M, G);
-        issue_load<0>(sb, LN, G);
-        issue_load<1>(sb, LN, G);
-        cp_commit();
-
-        cp_wait<4>();
-        __syncwarp();
-        compute_plane<REACTION, 3>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<2>(sb, LN, G);
-        cp_commit();
-
-        cp_wait<4>();
-        __syncwarp();
-        compute_plane<REACTION, 4>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<3>(sb, LN, G);
-        cp_commit();
-
-        cp_wait<5>();
-        __syncwarp();
-        compute_plane<REACTION, 5>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<4>(sb, LN, G);
-        cp_commit();
-
-        cp_wait<5>();
-        __syncwarp();
-        compute_plane<REACTION, 6>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<5>(sb, LN, G);
-        cp_commit();
-
-        cp_wait<5>();
-        __syncwarp();
-        compute_plane<REACTION, 7>(M, K, Q, C, sb, G);
-        __syncwarp();
-        issue_load<6>(sb, LN, G);
-        issue_load<7>(sb, LN, G);
-        cp_commit();
-
-        // advance the pipeline by one chunk
-        C = make_ctx(M, idN, lmN, dvN, G);
-        L = LN;
-        idN = idNN;
-        load_ctx(M, idN, lane, lmN, dvN);
-        pNN = claim_get(raw);
-        idNN = sched(pNN);
-        claim_issue(raw);
-    }
-    cp_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -991,6 +621,414 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     cp_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// v15: four nodes per lane. The load side is v14's (each lane copies its
+// 16-B pair of u and D_eff per plane into the 8-slot ring, face lanes the
+// halo cells), but the compute side gives every lane a row segment of four
+// nodes: lanes 0-15 compute plane 2*it and lanes 16-31 plane 2*it+1 of the
+// same chunk, (y, xq) = ((lane & 15) >> 1, lane & 1), nodes x = 4*xq .. +3.
+// Per-lane fixed costs (slot addresses, predicates, the rare-path test, the
+// loop) are paid once per four nodes, x faces between the four nodes come
+// from registers, and a chunk takes four iterations instead of eight.
+// Ring discipline (one commit group per plane load, load i of chunk k at
+// index 10k+i): before iteration it the loads up to 10k+2it+3 must be done
+// and exactly four newer ones are in flight (wait_group 4); after it the
+// slots of planes 2it-1 and 2it are free, so loads 10k+2it+8 and 10k+2it+9
+// are issued (it = 3: also 10k+16 and 10k+17, the next chunk's planes).
+// ---------------------------------------------------------------------------
+constexpr int kCtas15 = 4;
+constexpr int kAhead15 = 4;
+constexpr uint32_t kCtxLq = 128;    // ctx entry: lm[32] | lq[32] | desc[8] | id
+constexpr uint32_t kCtxDesc = 256;
+constexpr uint32_t kCtxId = 288;
+constexpr uint32_t kCtxBytes15 = 304;
+constexpr uint32_t kWarpBytes15 = kRing14 * kTileBytes + 3 * kCtxBytes15;
+
+// v15 tile rows are swizzled at 16-B granularity: logical granule g of tile
+// row R (R = y + 1, rows -1..8) sits at physical granule g ^ ((R >> 1) & 1).
+// A quad lane reads 16 B at a 32-B stride within a row; the swizzle makes the
+// eight lanes of every LDS.128 phase (four rows, two lanes each) hit eight
+// distinct 16-B bank groups. Pair loads (v14 lanes) stay conflict-free: a
+// row's granules are only permuted.
+__device__ __forceinline__ uint32_t swz(int R, int x) {  // byte offset of node x of tile row R
+    return 64u * (uint32_t)R + 16u * (uint32_t)((x >> 1) ^ ((R >> 1) & 1)) + 8u * (uint32_t)(x & 1);
+}
+
+__device__ __forceinline__ LaneGeo lane_geo_swz(int lane) {
+    LaneGeo G = lane_geo(lane);
+    const int x0 = 2 * G.xp;
+    G.s_c = swz(G.y + 1, x0);
+    G.s_hy = G.y == 0 ? swz(0, x0) : swz(9, x0);
+    return G;
+}
+
+struct QuadGeo {
+    int h, y, xq;
+    uint32_t cA;  // nodes x0, x0+1 of row y (x0+2, x0+3: cA ^ 16, the neighbouring granule)
+    uint32_t mA;  // same columns, row y-1
+    uint32_t pA;  // same columns, row y+1
+    uint32_t s_l, s_r;  // left / right neighbour cells
+    uint32_t bq;        // element offset of node x0 in a plane
+};
+
+__device__ __forceinline__ QuadGeo quad_geo(int lane) {
+    QuadGeo Q;
+    Q.h = lane >> 4;
+    const int r = lane & 15;
+    Q.y = r >> 1;
+    Q.xq = r & 1;
+    const int x0 = 4 * Q.xq, R = Q.y + 1;
+    Q.cA = swz(R, x0);
+    Q.mA = swz(R - 1, x0);
+    Q.pA = swz(R + 1, x0);
+    Q.s_l = Q.xq == 0 ? kHxOff + (uint32_t)Q.y * 8u : swz(R, x0 - 1);
+    Q.s_r = Q.xq == 1 ? kHxOff + (uint32_t)(8 + Q.y) * 8u : swz(R, x0 + 4);
+    Q.bq = (uint32_t)(Q.y * 8 + x0);
+    return Q;
+}
+
+struct ChunkCtx15 {
+    int c, key, flags;
+    uint32_t lq;  // compute-side bits: 4*it+i active, 16+4*it+i sink
+};
+
+// Per chunk and lane: compute-side bits of the lane's quad in planes 2*it+h.
+__global__ void lanemask15_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ snk, int64_t n,
+                                  uint32_t* __restrict__ lq) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * 32) return;
+    const int64_t c = t >> 5;
+    const int lane = (int)(t & 31);
+    const int h = lane >> 4, r = lane & 15;
+    const int bq = (r >> 1) * 8 + 4 * (r & 1);
+    uint32_t v = 0;
+    for (int it = 0; it < 4; ++it) {
+        const int z = 2 * it + h;
+        v |= (uint32_t)((act[c * 8 + z] >> bq) & 15ull) << (4 * it);
+        v |= (uint32_t)((snk[c * 8 + z] >> bq) & 15ull) << (16 + 4 * it);
+    }
+    lq[t] = v;
+}
+
+// Rare path of one quad (a Dirichlet-exposed chunk, or a huge / non-finite
+// fast result): exact generic update per node on operands re-read from the
+// ring, then the reference's non-finite / total-mass flags.
+template <int REACTION>
+__device__ __noinline__ double4 quad_slow(unsigned long long* bad_key, int* flagp, const SlowConsts& K,
+                                          const double* __restrict__ src, int c, int key, int cflags,
+                                          uint32_t bits, int z, uint32_t tm, uint32_t t0, uint32_t tp, QuadGeo G,
+                                          double4 o) {
+    double out[4] = {o.x, o.y, o.z, o.w};
+    double u[6], d[6];  // x0-1 .. x0+4
+    const int R = G.y + 1;
+    u[0] = lds1(t0 + G.s_l);
+    d[0] = lds1(t0 + kDOff + G.s_l);
+    u[5] = lds1(t0 + G.s_r);
+    d[5] = lds1(t0 + kDOff + G.s_r);
+    for (int i = 0; i < 4; ++i) {
+        u[i + 1] = lds1(t0 + swz(R, 4 * G.xq + i));
+        d[i + 1] = lds1(t0 + kDOff + swz(R, 4 * G.xq + i));
+    }
+    const bool dirichlet = (cflags & kFlagDirichlet) != 0;
+    const int kx = key & 1023, ky = (key >> 10) & 1023, kz = (key >> 20) & 1023;
+    const int x0 = 4 * G.xq;
+    bool h[4], any = false;
+    for (int i = 0; i < 4; ++i) {
+        const bool a = (bits >> i) & 1u;
+        const double uc = u[i + 1], dc = d[i + 1];
+        const int x = 4 * G.xq + i;
+        const uint32_t e = swz(R, x), em = swz(R - 1, x), ep = swz(R + 1, x);
+        const double nu[6] = {u[i], u[i + 2], lds1(t0 + em), lds1(t0 + ep), lds1(tm + e), lds1(tp + e)};
+        const double nd[6] = {d[i], d[i + 2], lds1(t0 + kDOff + em), lds1(t0 + kDOff + ep),
+                              lds1(tm + kDOff + e), lds1(tp + kDOff + e)};
+        const bool s = REACTION == PD_REACTION_SURFACE_SINK && ((bits >> (16 + i)) & 1u);
+        const double sv = REACTION == PD_REACTION_VOLUMETRIC ? src[(int64_t)c * 512 + z * 64 + G.bq + i] : 0.0;
+        const int64_t gx = (int64_t)kx * 8 + x0 + i, gy = (int64_t)ky * 8 + G.y, gz = (int64_t)kz * 8 + z;
+        if (dirichlet) {
+            if (!sentinel(dc)) out[i] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
+            h[i] = a && huge(out[i]);
+        } else {
+            h[i] = a && huge(out[i]);
+            if (h[i] && !isfinite(out[i]) && !sentinel(dc))
+                out[i] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
+        }
+        any = any || h[i];
+    }
+    if (any) {
+        int first = -1;
+        for (int i = 3; i >= 0; --i)
+            if (((bits >> i) & 1u) && !isfinite(out[i])) first = i;
+        if (first >= 0) {
+            const int off = z * 64 + (int)G.bq + first;
+            atomicMin(bad_key, ((unsigned long long)c << 10) | (unsigned long long)off);
+            atomicOr(flagp, 1);
+        } else {
+            atomicOr(flagp, 2);
+        }
+    }
+    return make_double4(out[0], out[1], out[2], out[3]);
+}
+
+template <int REACTION, int R10>
+__device__ __forceinline__ void compute15(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
+                                          const ChunkCtx15& C, int it, uint32_t sb, uint32_t base, const QuadGeo& G,
+                                          double* __restrict__ un) {
+    const int z = 2 * it + G.h;
+    // 8-slot continuous ring, or (R10) 10 fixed slots: plane p of every chunk in slot p + 1
+    const uint32_t b = R10 ? (uint32_t)z : base + (uint32_t)z;
+    const uint32_t tm = sb + (R10 ? b : (b & 7u)) * kTileBytes;
+    const uint32_t t0 = sb + (R10 ? b + 1u : ((b + 1u) & 7u)) * kTileBytes;
+    const uint32_t tp = sb + (R10 ? b + 2u : ((b + 2u) & 7u)) * kTileBytes;
+    const uint32_t bits = (C.lq >> (4 * it)) & 0x000F000Fu;
+    const bool interior = ((C.flags >> (8 + 2 * it)) & 3) == 3;  // both planes of the pair (warp-uniform)
+    const double2 ua = lds2(t0 + G.cA), ub = lds2(t0 + (G.cA ^ 16u));
+    const double2 da = lds2(t0 + kDOff + G.cA), db = lds2(t0 + kDOff + (G.cA ^ 16u));
+    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
+    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
+    const double u0 = ua.x, u1 = ua.y, u2 = ub.x, u3 = ub.y;
+    const double d0 = da.x, d1 = da.y, d2 = db.x, d3 = db.y;
+    double l0, l1, l2, l3;  // lap starts at T{0} (solver.hpp:420): lap = 0.0 + x term
+    {
+        double fL, f01, f12, f23, fR;
+        if (interior) {
+            fL = fface(dL, d0, uL, u0);
+            f01 = fface(d0, d1, u0, u1);
+            f12 = fface(d1, d2, u1, u2);
+            f23 = fface(d2, d3, u2, u3);
+            fR = fface(d3, dR, u3, uR);
+        } else {
+            fL = face(dL, d0, uL, u0);
+            f01 = face(d0, d1, u0, u1);
+            f12 = face(d1, d2, u1, u2);
+            f23 = face(d2, d3, u2, u3);
+            fR = face(d3, dR, u3, uR);
+        }
+        l0 = 0.0 + (f01 - fL) * Q.ix;
+        l1 = 0.0 + (f12 - f01) * Q.ix;
+        l2 = 0.0 + (f23 - f12) * Q.ix;
+        l3 = 0.0 + (fR - f23) * Q.ix;
+    }
+    // y then z (solver.hpp:421-433: axes in order)
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+        const uint32_t oM = ax == 0 ? G.mA : G.cA, oP = ax == 0 ? G.pA : G.cA;
+        const uint32_t amA = (ax == 0 ? t0 : tm) + oM, amB = (ax == 0 ? t0 : tm) + (oM ^ 16u);
+        const uint32_t apA = (ax == 0 ? t0 : tp) + oP, apB = (ax == 0 ? t0 : tp) + (oP ^ 16u);
+        const double w = ax == 0 ? Q.iy : Q.iz;
+        const double2 uma = lds2(amA), umb = lds2(amB), dma = lds2(amA + kDOff), dmb = lds2(amB + kDOff);
+        const double2 upa = lds2(apA), upb = lds2(apB), dpa = lds2(apA + kDOff), dpb = lds2(apB + kDOff);
+        double m0, m1, m2, m3, p0, p1, p2, p3;
+        if (interior) {
+            m0 = fface(dma.x, d0, uma.x, u0);
+            m1 = fface(dma.y, d1, uma.y, u1);
+            m2 = fface(dmb.x, d2, umb.x, u2);
+            m3 = fface(dmb.y, d3, umb.y, u3);
+            p0 = fface(d0, dpa.x, u0, upa.x);
+            p1 = fface(d1, dpa.y, u1, upa.y);
+            p2 = fface(d2, dpb.x, u2, upb.x);
+            p3 = fface(d3, dpb.y, u3, upb.y);
+        } else {
+            m0 = face(dma.x, d0, uma.x, u0);
+            m1 = face(dma.y, d1, uma.y, u1);
+            m2 = face(dmb.x, d2, umb.x, u2);
+            m3 = face(dmb.y, d3, umb.y, u3);
+            p0 = face(d0, dpa.x, u0, upa.x);
+            p1 = face(d1, dpa.y, u1, upa.y);
+            p2 = face(d2, dpb.x, u2, upb.x);
+            p3 = face(d3, dpb.y, u3, upb.y);
+        }
+        l0 += (p0 - m0) * w;
+        l1 += (p1 - m1) * w;
+        l2 += (p2 - m2) * w;
+        l3 += (p3 - m3) * w;
+    }
+    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+    if (REACTION == PD_REACTION_SURFACE_SINK) {
+        r0 = ((bits >> 16) & 1u) ? Q.neg_k * u0 : 0.0;
+        r1 = ((bits >> 17) & 1u) ? Q.neg_k * u1 : 0.0;
+        r2 = ((bits >> 18) & 1u) ? Q.neg_k * u2 : 0.0;
+        r3 = ((bits >> 19) & 1u) ? Q.neg_k * u3 : 0.0;
+    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const double* sp = M.A.src + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bq);
+        r0 = sp[0] * Q.src_factor;
+        r1 = sp[1] * Q.src_factor;
+        r2 = sp[2] * Q.src_factor;
+        r3 = sp[3] * Q.src_factor;
+    }
+    double o0 = u0 + Q.dt * l0 + Q.dt * r0;
+    double o1 = u1 + Q.dt * l1 + Q.dt * r1;
+    double o2 = u2 + Q.dt * l2 + Q.dt * r2;
+    double o3 = u3 + Q.dt * l3 + Q.dt * r3;
+    if (!interior) {  // walls stay frozen (solver.hpp:413-417)
+        if (sentinel(d0)) o0 = u0;
+        if (sentinel(d1)) o1 = u1;
+        if (sentinel(d2)) o2 = u2;
+        if (sentinel(d3)) o3 = u3;
+    }
+    const bool a0 = bits & 1u, a1 = (bits >> 1) & 1u, a2 = (bits >> 2) & 1u, a3 = (bits >> 3) & 1u;
+    const bool hot = (a0 && huge(o0)) | (a1 && huge(o1)) | (a2 && huge(o2)) | (a3 && huge(o3));
+    if ((C.flags & kFlagDirichlet) || hot) {
+        const double4 r = quad_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, M.A.src, C.c, C.key, C.flags, bits,
+                                              z, tm, t0, tp, G, make_double4(o0, o1, o2, o3));
+        o0 = r.x;
+        o1 = r.y;
+        o2 = r.z;
+        o3 = r.w;
+    }
+    double* dst = un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bq);
+    stg_pair(dst, o0, o1, a0, a1);
+    stg_pair(dst + 2, o2, o3, a2, a3);
+}
+
+// R10 = 1 (v16): ten fixed slots per warp (plane p of every chunk in slot
+// p + 1), 12 warps per SM; the next chunk's loads i, i+1 go out as soon as
+// slots i, i+1 are consumed, which keeps six loads in flight (wait_group 6).
+template <int REACTION, int R10>
+__global__ void __launch_bounds__(kThreads, R10 ? 3 : kCtas15) ftcs_march15_kernel(MarchArgs M) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+    }
+    __syncthreads();
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const LaneGeo G = lane_geo_swz(lane);
+    const QuadGeo GQ = quad_geo(lane);
+    constexpr int kSlotsQ = R10 ? 10 : kRing14;
+    constexpr uint32_t kWarpBytesQ = kSlotsQ * kTileBytes + 3 * kCtxBytes15;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytesQ;
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    double* __restrict__ un = A.un;
+    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
+
+    // chunk pipeline as in ftcs_march14_kernel (context ring in shared memory)
+    int* ctr_l = M.counter + ((t >> 5) & M.zero);
+    const int n = (int)M.n;
+    const uint32_t cb = sb + kSlotsQ * kTileBytes;
+    auto cent = [&](int e) -> uint32_t { return cb + (uint32_t)e * kCtxBytes15; };
+    int raw = 0;
+    auto claim_issue = [&]() {
+        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(raw) : "l"(ctr_l) : "memory");
+    };
+    auto sched_sync = [&]() -> int {
+        claim_issue();
+        const int p = __shfl_sync(0xffffffffu, raw, 0);
+        return p < n ? __ldg(&M.sched[p]) : -1;
+    };
+    auto fetch_ctx = [&](uint32_t e, int c) {
+        const int64_t cc = c < 0 ? 0 : c;
+        cp4(e + 4u * (uint32_t)lane, M.lm + cc * 32 + lane, c >= 0);
+        cp4(e + kCtxLq + 4u * (uint32_t)lane, M.lq + cc * 32 + lane, c >= 0);
+        cp4(e + kCtxDesc + 4u * (uint32_t)(lane & 7), M.desc + cc * 8 + (lane & 7), c >= 0 && lane < 8);
+    };
+    {
+        const int id0 = sched_sync();
+        if (id0 < 0) return;
+        const int id1 = sched_sync();
+        if (lane == 0) {
+            sts_u32(cent(0) + kCtxId, (uint32_t)id0);
+            sts_u32(cent(1) + kCtxId, (uint32_t)id1);
+        }
+        fetch_ctx(cent(0), id0);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        claim_issue();
+    }
+    int ek = 0;
+    ChunkCtx15 Cld, Cprev;
+    LoadCtx14 Lld;
+    auto advance = [&]() {
+        Cprev = Cld;  // R10: the chunk whose planes the slots now hold completely
+        const uint32_t e0 = cent(ek);
+        const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
+        const uint32_t e1 = cent(e1i), e2 = cent(e2i);
+        const int c = (int)lds_u32(e0 + kCtxId);
+        const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
+        const uint32_t lq = c >= 0 ? lds_u32(e0 + kCtxLq + 4u * (uint32_t)lane) : 0u;
+        const int dv = (int)lds_u32(e0 + kCtxDesc + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
+        Cld = ChunkCtx15{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lq};
+        Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
+        const int c1 = (int)lds_u32(e1 + kCtxId);
+        fetch_ctx(e1, c1);
+        if (lane == 0) {
+            const bool ok = raw < n;
+            cp4(e2 + kCtxId, M.sched + (ok ? raw : 0), ok);
+            if (!ok) sts_u32(e2 + kCtxId, 0xFFFFFFFFu);
+        }
+        claim_issue();
+        ek = e1i;
+    };
+    advance();
+    // the first advance's copies (chunk 1's context, chunk 2's id) must land
+    // before the prologue's tenth load advances onto chunk 1 (R10)
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+    int p_ld = 0;
+    uint32_t Lc = 0;
+    auto issue_next = [&]() {
+        const uint32_t slot = R10 ? (uint32_t)p_ld : (Lc & (kRing14 - 1));
+        issue14(sb + slot * kTileBytes, u, de, Lld, p_ld, G, sent_off);
+        if (++p_ld == 10) {
+            p_ld = 0;
+            advance();
+        }
+        cp_commit();
+        ++Lc;
+    };
+    ChunkCtx15 Cc = Cld;  // before the prologue: with R10 its tenth load advances the load side
+    uint32_t base = 0;
+#pragma unroll 1
+    for (int k = 0; k < (R10 ? 10 : 4 + kAhead15); ++k) issue_next();
+#pragma unroll 1
+    while (Cc.c >= 0) {
+#pragma unroll 1
+        for (int it = 0; it < 4; ++it) {
+            cp_wait<R10 ? 6 : kAhead15>();
+            __syncwarp();
+            compute15<REACTION, R10>(M, K, Q, Cc, it, sb, base, GQ, un);
+            __syncwarp();
+            issue_next();
+            issue_next();
+            if (it == 3) {
+                issue_next();
+                issue_next();
+            }
+        }
+        base += 10u;
+        // the load side is one chunk ahead with the 8-slot ring, two with R10
+        // (its tenth load of the next chunk already advanced it)
+        Cc = R10 ? Cprev : Cld;
+    }
+    cp_wait<0>();
+}
+
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
@@ -1069,6 +1107,7 @@ void march_free(MarchPlan* p) {
     cudaFree(p->d_deff);
     cudaFree(p->d_counter);
     cudaFree(p->d_lm);
+    cudaFree(p->d_lq);
     *p = MarchPlan{};
 }
 
@@ -1117,6 +1156,9 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
         d_nbr, g->d_keys, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
     PD_CUDA(cudaGetLastError());
     PD_CUDA(cudaMalloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
+    PD_CUDA(cudaMalloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
+    lanemask15_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
+                                                                                  plan->d_lq);
     lanemask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink,
                                                                                 n_all, plan->d_lm);
     PD_CUDA(cudaGetLastError());
@@ -1179,6 +1221,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.n = n;
     M.desc = p.d_desc;
     M.lm = p.d_lm;
+    M.lq = p.d_lq;
     M.deff = p.d_deff;
     M.counter = counter;
     static const int dbg = [] {
@@ -1199,19 +1242,24 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
-    if (ver == 13) {
-        constexpr size_t bytes = (size_t)kTileBytes * kSlots * kWarps;
-        static const KernT table[3] = {ftcs_march_kernel<0, kCtasPerSm>, ftcs_march_kernel<1, kCtasPerSm>,
-                                       ftcs_march_kernel<2, kCtasPerSm>};
+    if (ver == 15 || ver == 16) {
+        const bool r10 = ver == 16;
+        const size_t bytes = (size_t)((r10 ? 10 : kRing14) * kTileBytes + 3 * kCtxBytes15) * kWarps;
+        static const KernT table[2][3] = {
+            {ftcs_march15_kernel<0, 0>, ftcs_march15_kernel<1, 0>, ftcs_march15_kernel<2, 0>},
+            {ftcs_march15_kernel<0, 1>, ftcs_march15_kernel<1, 1>, ftcs_march15_kernel<2, 1>}};
         static bool attr_set = false;
         if (!attr_set) {
-            for (auto k : table)
-                PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            for (int v = 0; v < 2; ++v)
+                for (auto k : table[v])
+                    PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)((size_t)((v ? 10 : kRing14) * kTileBytes + 3 * kCtxBytes15) *
+                                                       kWarps)));
             attr_set = true;
         }
         int sms = 148;
         PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        table[r]<<<sms * kCtasPerSm, kThreads, bytes, g->stream>>>(M);
+        table[r10 ? 1 : 0][r]<<<sms * (r10 ? 3 : kCtas15), kThreads, bytes, g->stream>>>(M);
     } else {
         constexpr size_t bytes = (size_t)kWarpBytes14 * kWarps;
         static const KernT table[3] = {ftcs_march14_kernel<0>, ftcs_march14_kernel<1>, ftcs_march14_kernel<2>};

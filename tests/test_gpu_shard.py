@@ -186,18 +186,25 @@ def test_overlapped_enqueue_and_exact_diagnostics(world, n, cuda):
         for r, (dev, plan, s, _, _rg) in enumerate(shards):
             for lst, face, to in ((plan.send_down, shard.FACE_ZLO, r - 1), (plan.send_up, shard.FACE_ZHI, r + 1)):
                 if len(lst):
+                    # keep the ordinal tensor alive: the pack runs on the shard
+                    # grid's own stream, not torch's
                     buf = torch.empty((len(lst), 64), dtype=torch.float64, device="cuda")
-                    pd._check(lib.pd_grid_pack_face(dev.h, 3, C.c_void_p(ords(lst).data_ptr()), len(lst), face,
+                    o = ords(lst)
+                    torch.cuda.synchronize()
+                    pd._check(lib.pd_grid_pack_face(dev.h, 3, C.c_void_p(o.data_ptr()), len(lst), face,
                                                     C.c_void_p(buf.data_ptr())))
-                    sent[(r, to)] = buf
+                    sent[(r, to)] = (buf, o)
         for dev, plan, s, _, (_b, _t, (i0, i1)) in shards:
             pd._check(lib.pd_stepper_enqueue(s, step, i0, i1, 1.0))
         torch.cuda.synchronize()
         for r, (dev, plan, s, _, _rg) in enumerate(shards):
             for lst, face, frm in ((plan.recv_down, shard.FACE_ZHI, r - 1), (plan.recv_up, shard.FACE_ZLO, r + 1)):
                 if len(lst):
-                    pd._check(lib.pd_grid_unpack_face(dev.h, 3, C.c_void_p(ords(lst).data_ptr()), len(lst), face,
-                                                      C.c_void_p(sent[(frm, r)].data_ptr())))
+                    o = ords(lst)
+                    torch.cuda.synchronize()
+                    pd._check(lib.pd_grid_unpack_face(dev.h, 3, C.c_void_p(o.data_ptr()), len(lst), face,
+                                                      C.c_void_p(sent[(frm, r)][0].data_ptr())))
+                    torch.cuda.synchronize()
             pd._check(lib.pd_stepper_swap(s))
         torch.cuda.synchronize()
     for dev, plan, s, _, _rg in shards:
