@@ -137,7 +137,7 @@ def run_frap(grid: pd.SparseBlockGrid, bleach: IndexBox, d_molecular: float,
     pu, pdd = grid.property_index("u"), grid.property_index("D")
     dev = grid.device()
     region, phase = dev.frap_init(pu, pdd, bleach.lo, bleach.hi, d_molecular)
-    grid._mark_device_newer()
+    grid._mark_device_newer(["u", "D"])
     if region == 0:
         raise InputError("bleach region contains no active nodes")
     if region == phase:

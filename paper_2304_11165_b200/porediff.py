@@ -325,7 +325,7 @@ class SparseBlockGrid:
         self._lin = np.zeros(0, np.int64)
         self._pending = {}  # linear index -> chunk being built by insert()
         self._dev = None  # DeviceGrid mirror
-        self._dev_newer = False  # device holds state the host has not fetched
+        self._dev_newer = set()  # properties whose device copy the host has not fetched
         self._host_newer = True
 
     # -- construction ------------------------------------------------------
@@ -357,7 +357,7 @@ class SparseBlockGrid:
         g._keys, g._masks, g._lin = keys, masks, g._linear(keys)
         g._data = {p: None for p in g.props}
         g._dev = dev
-        g._dev_newer = True
+        g._dev_newer = set(g.props)
         g._host_newer = False
         return g
 
@@ -385,8 +385,15 @@ class SparseBlockGrid:
         self._flush_pending()
         if self._dev is not None and self._dev_newer:
             for p in self.props:
-                self._data[p] = self._dev.download(self.property_index(p))
-            self._dev_newer = False
+                if p not in self._dev_newer:
+                    continue
+                cur = self._data.get(p)
+                if (isinstance(cur, np.ndarray) and cur.shape == (self._dev.n_chunks, self.V)
+                        and cur.dtype == self.dtype and cur.flags.c_contiguous and cur.flags.writeable):
+                    self._dev.download_into(self.property_index(p), cur)  # reuse (possibly pinned) buffer
+                else:
+                    self._data[p] = self._dev.download(self.property_index(p))
+            self._dev_newer = set()
 
     def _touch_host(self):
         self._sync_host()
@@ -408,8 +415,9 @@ class SparseBlockGrid:
             self._host_newer = False
         return self._dev
 
-    def _mark_device_newer(self):
-        self._dev_newer = True
+    def _mark_device_newer(self, props=None):
+        """The device advanced these properties (default: all)."""
+        self._dev_newer |= set(self.props if props is None else props)
 
     # -- insertion (sparse_block_grid.hpp:117-132) ---------------------------
     def _check_bounds(self, idx):
@@ -656,6 +664,10 @@ class DeviceGrid:
         _check(lib.pd_grid_download(self.h, prop, out.ctypes.data))
         return out
 
+    def download_into(self, prop: int, out: np.ndarray) -> None:
+        assert out.shape == (self.n_chunks, self.V) and out.dtype == self.dtype and out.flags.c_contiguous
+        _check(lib.pd_grid_download(self.h, prop, out.ctypes.data))
+
     def device_ptr(self, prop: int) -> int:
         p = C.c_void_p()
         _check(lib.pd_grid_device_ptr(self.h, prop, C.byref(p)))
@@ -821,7 +833,7 @@ class FtcsStepper:
         fac = self._factors(step0, n_steps)
         t0 = _time.perf_counter()
         rc = lib.pd_stepper_run(self.h, step0, n_steps, final_step, fac, rows, C.byref(nr))
-        self.grid._mark_device_newer()
+        self.grid._mark_device_newer(["u", scratch_channel])
         _check(rc)
         wall = _time.perf_counter() - t0
         return [StepDiagnostics(r.step, r.time, r.total_mass, r.min_u, r.max_u, wall)
