@@ -118,3 +118,30 @@ def pack_for_porosity(psi: float, radius: float, seed: int, lo=(0.0, 0.0, 0.0), 
     vol = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2])
     count = int(round(math.log(1.0 / psi) * vol / (4.0 / 3.0 * math.pi * radius ** 3)))
     return SpherePacking.random(lo, hi, count, radius, radius, seed)
+
+
+def grf_mask(size, porosity: float, n_modes: int = 48, k_max: float = 6.0, seed: int = 0, device=None) -> np.ndarray:
+    """Soil-CT-like binary volume for config C3 (not in the reference): a
+    Gaussian random field sum_m cos(2 pi k_m . x / L + phi_m) with n_modes
+    random wave vectors |k| <= k_max (per box length), thresholded at the
+    porosity quantile (pore = 1). Returns uint8 bits, axis 0 fastest. Built
+    with torch on `device` (an input generator, not the simulated path); feed
+    the same mask to both sides of a comparison."""
+    import torch
+    dev = torch.device(device) if device is not None else torch.device("cuda" if torch.cuda.is_available() else "cpu")
+    g = torch.Generator().manual_seed(int(seed))
+    k = (torch.rand((n_modes, 3), generator=g, dtype=torch.float64) * 2 - 1) * k_max
+    ph = torch.rand(n_modes, generator=g, dtype=torch.float64) * 2 * math.pi
+    nx, ny, nz = (int(s) for s in size)
+    xs = [torch.arange(s, dtype=torch.float64, device=dev) / s for s in (nx, ny, nz)]
+    field_ = torch.zeros((nz, ny, nx), dtype=torch.float64, device=dev)
+    for m in range(n_modes):
+        a = 2 * math.pi * k[m].to(dev)
+        field_ += torch.cos(a[0] * xs[0][None, None, :] + a[1] * xs[1][None, :, None] + a[2] * xs[2][:, None, None]
+                            + float(ph[m]))
+    flat = field_.reshape(-1)
+    # pore = the `porosity` fraction of largest values
+    kth = int(round((1.0 - porosity) * flat.numel()))
+    kth = min(max(kth, 1), flat.numel())
+    thr = torch.kthvalue(flat.cpu() if flat.numel() > (1 << 27) else flat, kth).values.to(dev)
+    return (flat > thr).to(torch.uint8).cpu().numpy()
