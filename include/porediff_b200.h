@@ -273,6 +273,8 @@ int pd_field_create(int dims, int scalar_bytes, const int64_t* size, const doubl
                     int device, pd_field** out);
 int pd_field_destroy(pd_field* f);
 int pd_field_upload(pd_field* f, const void* host_values);
+/* Same from device memory (e.g. a level set computed by another library). */
+int pd_field_upload_device(pd_field* f, const void* dev_values);
 int pd_field_download(pd_field* f, void* host_values);
 int pd_field_device_ptr(pd_field* f, void** ptr);
 /* mask_to_indicator (geometry.hpp:67-77): bits (one byte per voxel, axis 0

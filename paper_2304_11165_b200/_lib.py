@@ -125,6 +125,7 @@ _SIGNATURES = [
     ("pd_field_create", C.c_int, [C.c_int, C.c_int, _I64P, _DP, _DP, C.c_int, C.POINTER(_P)]),
     ("pd_field_destroy", C.c_int, [_P]),
     ("pd_field_upload", C.c_int, [_P, _P]),
+    ("pd_field_upload_device", C.c_int, [_P, _P]),
     ("pd_field_download", C.c_int, [_P, _P]),
     ("pd_field_device_ptr", C.c_int, [_P, C.POINTER(_P)]),
     ("pd_field_from_mask", C.c_int, [_P, _P, C.c_int64]),

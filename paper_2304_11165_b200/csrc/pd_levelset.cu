@@ -68,10 +68,11 @@ __global__ void cells_from_indicator(const T* __restrict__ v, int64_t n, uint8_t
 // erode: AND of in[i .. i+w-1]; dilate: OR of in[i-w+1 .. i]; outside = false
 __global__ void box_filter_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, FieldGeo g,
                                   int axis, int w, int erode) {
-    const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (f >= g.total) return;
+    const int64_t x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    if (x >= g.n[0] || y >= g.n[1]) return;
+    const int64_t f = x + y * g.s1 + z * g.s2;
     const int64_t stride = axis == 0 ? 1 : (axis == 1 ? g.s1 : g.s2);
-    const int64_t i = axis == 0 ? f % g.n[0] : (axis == 1 ? (f / g.s1) % g.n[1] : f / g.s2);
+    const int64_t i = axis == 0 ? x : (axis == 1 ? y : z);
     const int64_t na = g.n[axis];
     bool v = erode;
     for (int k = 0; k < w; ++k) {
@@ -166,11 +167,13 @@ __global__ void __launch_bounds__(256)
     sussman_sweep_kernel(const T* __restrict__ phi, T* __restrict__ next, FieldGeo g, SweepConsts<T> K,
                          typename Bits<T>::U* __restrict__ res, const int* __restrict__ done) {
     if (*done) return;
-    const int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // 3-D launch: x = blockIdx.x*32 + tx, y = blockIdx.y*8 + ty, z = blockIdx.z
+    const int64_t x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, z = blockIdx.z;
+    const int64_t f = x + y * g.s1 + z * g.s2;
     T local = T(0);
-    if (f < g.total) {
+    if (x < g.n[0] && y < g.n[1]) {
         const T c = phi[f];
-        const int64_t idx[3] = {f % g.n[0], (f / g.s1) % g.n[1], f / g.s2};
+        const int64_t idx[3] = {x, y, z};
         const int64_t stride[3] = {1, g.s1, g.s2};
         const bool pos = !(c < T(0));
         T sum = T(0);
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(256)
         const typename Bits<T>::U other = __shfl_xor_sync(0xffffffffu, b, o);
         b = other > b ? other : b;
     }
-    if ((threadIdx.x & 31) == 0 && b) atomicMax(res, b);
+    if (threadIdx.x == 0 && b) atomicMax(res, b);
 }
 
 // After sweep it (1-based): converged when residual < tol (levelset.hpp:183-187).
@@ -212,6 +215,11 @@ __global__ void sussman_check_kernel(const typename Bits<T>::U* __restrict__ res
 
 constexpr int kFieldThreads = 256;
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + kFieldThreads - 1) / kFieldThreads); }
+// 3-D launch over a field: 32 x 8 thread tiles of (x, y), one z per block row
+inline dim3 grid3(const pd_field* f) {
+    return dim3((unsigned)((f->size[0] + 31) / 32), (unsigned)((f->size[1] + 7) / 8), (unsigned)f->size[2]);
+}
+const dim3 kBlock3(32, 8, 1);
 
 void check_field(const pd_field* f) {
     if (!f || !f->d) fail(PD_E_INPUT, "null field");
@@ -350,10 +358,10 @@ void redistance(pd_field* f, const pd_levelset_options* o, pd_redistance_diag* o
             const T* src = bufs[(it - 1) & 1];
             T* dst = bufs[it & 1];
             if (f->dims == 3)
-                sussman_sweep_kernel<T, 3><<<blocks_for(f->n), 256, 0, f->stream>>>(src, dst, g, K, d_res + it,
+                sussman_sweep_kernel<T, 3><<<grid3(f), kBlock3, 0, f->stream>>>(src, dst, g, K, d_res + it,
                                                                                    d_state);
             else
-                sussman_sweep_kernel<T, 2><<<blocks_for(f->n), 256, 0, f->stream>>>(src, dst, g, K, d_res + it,
+                sussman_sweep_kernel<T, 2><<<grid3(f), kBlock3, 0, f->stream>>>(src, dst, g, K, d_res + it,
                                                                                    d_state);
             sussman_check_kernel<T><<<1, 1, 0, f->stream>>>(d_res + it, it, K.tol, d_state, d_state + 1);
             if (it % kSync == 0 || it == o->max_iterations) {
@@ -448,6 +456,15 @@ int pd_field_upload(pd_field* f, const void* host) {
     });
 }
 
+int pd_field_upload_device(pd_field* f, const void* dev) {
+    return guarded([&] {
+        check_field(f);
+        DeviceGuard dg(f->device);
+        PD_CUDA(cudaMemcpyAsync(f->d, dev, (size_t)f->n * (size_t)f->tbytes, cudaMemcpyDeviceToDevice, f->stream));
+        PD_CUDA(cudaStreamSynchronize(f->stream));
+    });
+}
+
 int pd_field_download(pd_field* f, void* host) {
     return guarded([&] {
         check_field(f);
@@ -506,7 +523,7 @@ int pd_field_filter_thin(pd_field* f, int min_thickness_cells) {
             // erode along every axis, then dilate along every axis (geometry.hpp:137-138)
             for (int pass = 0; pass < 2; ++pass)
                 for (int ax = 0; ax < f->dims; ++ax) {
-                    box_filter_kernel<<<blocks_for(f->n), kFieldThreads, 0, f->stream>>>(a, b, g, ax,
+                    box_filter_kernel<<<grid3(f), kBlock3, 0, f->stream>>>(a, b, g, ax,
                                                                                        min_thickness_cells,
                                                                                        pass == 0);
                     std::swap(a, b);

@@ -88,6 +88,10 @@ class DeviceField:
             raise InputError("field value count does not match the geometry")
         _check(lib.pd_field_upload(self.h, a.ctypes.data))
 
+    def upload_device(self, ptr: int):
+        """Values from device memory (nodes x itemsize bytes at ptr)."""
+        _check(lib.pd_field_upload_device(self.h, C.c_void_p(ptr)))
+
     def download(self) -> np.ndarray:
         out = np.empty(self.node_count(), self.dtype)
         _check(lib.pd_field_download(self.h, out.ctypes.data))
