@@ -292,6 +292,35 @@ int pd_field_redistance(pd_field* f, const pd_levelset_options* opts, pd_redista
 int pd_build_grid_from_field(const pd_field* f, double b_low, double b_up, int n_props, int prop_phi,
                              pd_grid** out);
 
+/* ---- snapshots (reference snapshot.hpp:195-348) --------
+ * Byte-identical "SBGR" (sparse grid) and "SBGD" (dense field) containers,
+ * streamed from / to the device in batches through pinned staging buffers.
+ * I/O failures are PD_E_IO with the reference's messages. */
+
+/* SnapshotInfo (snapshot.hpp:41-50); property names come back as
+ * consecutive NUL-terminated strings in names_buf. */
+typedef struct pd_snapshot_info {
+    char magic[5];  /* "SBGD" or "SBGR" */
+    uint32_t version, scalar_bits, dims;
+    uint64_t size[3];
+    double spacing[3], origin[3];
+    uint32_t n_properties;
+} pd_snapshot_info;
+
+/* write_sparse_snapshot: names in registration order (one per property),
+ * origin[dims] (the device grid keeps no origin). Payloads are written in
+ * registration order regardless of u/u_next swaps. */
+int pd_grid_write_snapshot(pd_grid* g, const char* path, const char* const* names, int n_names,
+                           const double* origin);
+/* read_sparse_snapshot for the given rank and scalar width: creates the
+ * device grid; origin[dims] and the names are returned. */
+int pd_grid_read_snapshot(const char* path, int dims, int scalar_bytes, int device, pd_grid** out, double* origin,
+                          char* names_buf, size_t names_cap, int* n_names);
+int pd_field_write_snapshot(pd_field* f, const char* path);
+int pd_field_read_snapshot(const char* path, int dims, int scalar_bytes, int device, pd_field** out);
+/* peek_snapshot: header only. */
+int pd_peek_snapshot(const char* path, pd_snapshot_info* info, char* names_buf, size_t names_cap);
+
 #ifdef __cplusplus
 }
 #endif

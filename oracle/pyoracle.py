@@ -119,6 +119,10 @@ class Ref:
                                    C.c_double, C.c_double, P, P, P, P, P, P]
         L.ref_field_redistance.argtypes = [C.c_int, C.c_int, P, P, P, P, P]
         L.ref_field_filter_thin.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int]
+        L.ref_grid_write_snapshot.argtypes = [P, C.c_char_p]
+        L.ref_grid_read_snapshot.restype = P
+        L.ref_grid_read_snapshot.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
+        L.ref_field_write_snapshot.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_char_p]
 
     def field_redistance(self, size, spacing, values, opts):
         """sussman_redistance on a dense field (axis 0 fastest); returns
@@ -130,6 +134,19 @@ class Ref:
         code = self.L.ref_field_redistance(len(size), v.dtype.itemsize, _p(size, np.int64),
                                            _p(list(spacing), np.float64), v.ctypes.data, C.byref(o), C.byref(d))
         return code, self.last_error(), v, (d.iterations, d.final_residual, bool(d.converged))
+
+    def write_dense_snapshot(self, size, spacing, origin, values, path):
+        v = np.ascontiguousarray(values)
+        code = self.L.ref_field_write_snapshot(len(size), v.dtype.itemsize, _p(size, np.int64), _p(list(spacing), np.float64),
+                                               _p(list(origin), np.float64), v.ctypes.data, str(path).encode())
+        return code, self.last_error()
+
+    def read_sparse_snapshot(self, path):
+        code = C.c_int()
+        h = self.L.ref_grid_read_snapshot(str(path).encode(), C.byref(code))
+        if code.value:
+            return code.value, self.last_error(), None
+        return 0, "", RefGrid(self, h, 3, 8, ["phi", "u", "D", "u_next"])
 
     def field_filter_thin(self, size, spacing, values, w):
         v = np.ascontiguousarray(values).copy()
@@ -207,6 +224,9 @@ class RefGrid:
             self.ref.L.ref_grid_free(self.h)
         except Exception:
             pass
+
+    def write_snapshot(self, path):
+        return self.ref.L.ref_grid_write_snapshot(self.h, str(path).encode()), self.ref.last_error()
 
     def chunk_count(self):
         return self.ref.L.ref_grid_chunk_count(self.h)

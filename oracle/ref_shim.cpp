@@ -25,6 +25,7 @@
 #include "porediff/synthetic.hpp"
 #include "porediff/config.hpp"
 #include "porediff/levelset.hpp"
+#include "porediff/snapshot.hpp"
 
 #include "porediff_b200.h"  // pd_sim_config / pd_diag layouts only
 
@@ -71,6 +72,7 @@ struct RefGridBase {
                      int64_t* n_rows) = 0;
     virtual double total_mass(int prop) const = 0;
     virtual double max_diffusivity(int prop) const = 0;
+    virtual void write_snapshot(const char* path) const = 0;
 };
 
 template <typename T, int D>
@@ -83,6 +85,7 @@ struct RefGrid : RefGridBase {
 
     int64_t chunk_count() const override { return g.chunk_count(); }
     int64_t active_count() const override { return g.active_node_count(); }
+    void write_snapshot(const char* path) const override { pd::write_sparse_snapshot(g, path); }
 
     void export_layout(int32_t* keys, uint64_t* masks) const override {
         int64_t i = 0;
@@ -438,6 +441,36 @@ int ref_field_filter_thin(int dims, int tbytes, const int64_t* size, const doubl
                           int min_thickness_cells) {
     return dispatch_field(dims, tbytes, size, spacing, data, [&](auto& field) {
         field = pd::filter_thin_features(field, min_thickness_cells);
+    });
+}
+
+/* ---- snapshots (snapshot.hpp) -------------------------------------------- */
+
+int ref_grid_write_snapshot(void* h, const char* path) {
+    return guarded([&] { static_cast<RefGridBase*>(h)->write_snapshot(path); });
+}
+
+/* read_sparse_snapshot into a reference grid handle (3-D double only). */
+void* ref_grid_read_snapshot(const char* path, int* code) {
+    void* out = nullptr;
+    *code = guarded([&] { out = new RefGrid<double, 3>(pd::read_sparse_snapshot<double, 3>(path)); });
+    return out;
+}
+
+int ref_field_write_snapshot(int dims, int tbytes, const int64_t* size, const double* spacing, const double* origin,
+                             const void* data, const char* path) {
+    return guarded([&] {
+        auto go = [&](auto tag, auto dc) {
+            using T = decltype(tag);
+            constexpr int D = decltype(dc)::value;
+            pd::DenseField<T, D> f(geom_of<D>(size, spacing, origin));
+            std::memcpy(f.data(), data, sizeof(T) * (size_t)f.node_count());
+            pd::write_dense_snapshot(f, path);
+        };
+        if (dims == 3 && tbytes == 8) go(double{}, std::integral_constant<int, 3>{});
+        else if (dims == 2 && tbytes == 8) go(double{}, std::integral_constant<int, 2>{});
+        else if (dims == 3) go(float{}, std::integral_constant<int, 3>{});
+        else go(float{}, std::integral_constant<int, 2>{});
     });
 }
 

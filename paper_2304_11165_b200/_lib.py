@@ -74,6 +74,19 @@ class pd_redistance_diag(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("final_residual", C.c_double), ("converged", C.c_int32)]
 
 
+class pd_snapshot_info(C.Structure):
+    _fields_ = [
+        ("magic", C.c_char * 5),
+        ("version", C.c_uint32),
+        ("scalar_bits", C.c_uint32),
+        ("dims", C.c_uint32),
+        ("size", C.c_uint64 * 3),
+        ("spacing", C.c_double * 3),
+        ("origin", C.c_double * 3),
+        ("n_properties", C.c_uint32),
+    ]
+
+
 _P = C.c_void_p
 _I64P = C.POINTER(C.c_int64)
 _DP = C.POINTER(C.c_double)
@@ -132,6 +145,12 @@ _SIGNATURES = [
     ("pd_field_filter_thin", C.c_int, [_P, C.c_int]),
     ("pd_field_redistance", C.c_int, [_P, C.POINTER(pd_levelset_options), C.POINTER(pd_redistance_diag)]),
     ("pd_build_grid_from_field", C.c_int, [_P, C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("pd_grid_write_snapshot", C.c_int, [_P, C.c_char_p, C.POINTER(C.c_char_p), C.c_int, _DP]),
+    ("pd_grid_read_snapshot", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P), _DP, C.c_char_p,
+                                        C.c_size_t, C.POINTER(C.c_int)]),
+    ("pd_field_write_snapshot", C.c_int, [_P, C.c_char_p]),
+    ("pd_field_read_snapshot", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("pd_peek_snapshot", C.c_int, [C.c_char_p, C.POINTER(pd_snapshot_info), C.c_char_p, C.c_size_t]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

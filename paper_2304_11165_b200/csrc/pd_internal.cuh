@@ -84,6 +84,16 @@ struct pd_grid {
     uint64_t generation = 0;  // bumped by every host-visible write to a column
 };
 
+// A dense field on the device (pd_levelset.cu, pd_snapshot.cu).
+struct pd_field {
+    int dims = 3, tbytes = 8, device = 0;
+    int64_t size[3] = {1, 1, 1};
+    double spacing[3] = {1, 1, 1}, origin[3] = {0, 0, 0};
+    int64_t n = 0;
+    void* d = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
 namespace pdb {
 
 // Chunk-level reductions (pd_grid.cu).

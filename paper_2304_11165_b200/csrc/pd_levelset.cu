@@ -21,15 +21,6 @@
 
 #include "pd_internal.cuh"
 
-struct pd_field {
-    int dims = 3, tbytes = 8, device = 0;
-    int64_t size[3] = {1, 1, 1};
-    double spacing[3] = {1, 1, 1}, origin[3] = {0, 0, 0};
-    int64_t n = 0;
-    void* d = nullptr;
-    cudaStream_t stream = nullptr;
-};
-
 namespace pdb {
 
 struct FieldGeo {
