@@ -313,6 +313,18 @@ namespace {
 
 constexpr int64_t kBatch = 512;
 
+// Below this many chunks per launch the one-CTA-per-chunk tile kernel is
+// faster than the persistent march kernel (its pipeline fill / drain and
+// per-warp claims dominate): measured crossover between 4 k and 14 k chunks
+// (128^3 / 192^3 free boxes); PD_MARCH_MIN_CHUNKS overrides.
+int64_t march_min_chunks() {
+    static const int64_t v = [] {
+        const char* e = getenv("PD_MARCH_MIN_CHUNKS");
+        return e ? (int64_t)atoll(e) : (int64_t)6144;
+    }();
+    return v;
+}
+
 void march_build_for(pd_stepper* s, int64_t begin, int64_t end) {
     pd_grid* g = s->g;
     int dir = 0;
@@ -390,7 +402,7 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         fill_args<double>(s, a, u, un, factor);
         a.k = k;
         a.ord0 = s->begin;
-        if (!diag && s->use_march && s->plan.ready) {
+        if (!diag && s->use_march && s->plan.ready && s->end - s->begin >= march_min_chunks()) {
             march_launch(g, s->plan, a, s->cfg.reaction_kind);
         } else if (g->dims == 3) {
             if (diag) ftcs_step_kernel<double, 3, true><<<nb, 512, 0, g->stream>>>(a);
@@ -712,7 +724,7 @@ int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t
             fill_args<double>(s, a, u, un, factor);
             a.k = 0;
             a.ord0 = begin;
-            if (s->use_march && s->plan.ready) {
+            if (s->use_march && s->plan.ready && end - begin >= march_min_chunks()) {
                 auto& sp = march_sub(g, s->plan, begin, end);
                 PD_CUDA(cudaMemsetAsync(sp.d_counter, 0, sizeof(int), g->stream));
                 march_launch_sched(g, s->plan, a, s->cfg.reaction_kind, sp.d_stream, sp.n, sp.d_counter);

@@ -1,5 +1,13 @@
+import os
 import sys
 from pathlib import Path
+
+# The library picks the one-CTA-per-chunk tile kernel for small grids (fewer
+# than PD_MARCH_MIN_CHUNKS chunks per launch) and the march kernel for large
+# ones. The parity cases are small, so the suite forces the march kernel (the
+# bench path) everywhere; the tile kernel is covered by the 2-D, FP32, record
+# and PD_NO_MARCH cases.
+os.environ.setdefault("PD_MARCH_MIN_CHUNKS", "0")
 
 import pytest
 
