@@ -165,7 +165,7 @@ int pd_grid_frap_init(pd_grid* g, int prop_u, int prop_d, const int64_t* lo, con
             if (p < 0 || p >= (int)g->column_of.size()) fail(PD_E_PROPERTY, "unknown property index");
         DeviceGuard dg(g->device);
         unsigned long long* d_counts = nullptr;
-        PD_CUDA(cudaMalloc(&d_counts, 2 * sizeof(unsigned long long)));
+        PD_CUDA(pd_malloc(&d_counts, 2 * sizeof(unsigned long long)));
         try {
             PD_CUDA(cudaMemsetAsync(d_counts, 0, 2 * sizeof(unsigned long long), g->stream));
             const BoxArgs b = box_args(g, lo, hi);
@@ -196,10 +196,10 @@ int pd_grid_frap_init(pd_grid* g, int prop_u, int prop_d, const int64_t* lo, con
             *phase = (int64_t)h[1];
             g->generation++;
         } catch (...) {
-            cudaFree(d_counts);
+            pd_free(d_counts);
             throw;
         }
-        cudaFree(d_counts);
+        pd_free(d_counts);
     });
 }
 

@@ -468,13 +468,13 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             s->hmin = g->spacing[0];
             for (int a = 1; a < g->dims; ++a) s->hmin = std::min(s->hmin, g->spacing[a]);
             const int64_t n = std::max<int64_t>(1, g->n_chunks);
-            PD_CUDA(cudaMalloc(&s->d_fluid, sizeof(uint64_t) * (size_t)(n * g->W)));
-            PD_CUDA(cudaMalloc(&s->d_sink, sizeof(uint64_t) * (size_t)(n * g->W)));
-            PD_CUDA(cudaMalloc(&s->d_nbr, sizeof(int32_t) * (size_t)(n * 2 * g->dims)));
-            PD_CUDA(cudaMalloc(&s->d_flags, sizeof(int) * (size_t)kBatch));
-            PD_CUDA(cudaMalloc(&s->d_bad, sizeof(unsigned long long)));
-            PD_CUDA(cudaMalloc(&s->d_rows, sizeof(double) * 3 * (size_t)kBatch));
-            PD_CUDA(cudaMalloc(&s->d_region, sizeof(double) * (size_t)kBatch));
+            PD_CUDA(pd_malloc(&s->d_fluid, sizeof(uint64_t) * (size_t)(n * g->W)));
+            PD_CUDA(pd_malloc(&s->d_sink, sizeof(uint64_t) * (size_t)(n * g->W)));
+            PD_CUDA(pd_malloc(&s->d_nbr, sizeof(int32_t) * (size_t)(n * 2 * g->dims)));
+            PD_CUDA(pd_malloc(&s->d_flags, sizeof(int) * (size_t)kBatch));
+            PD_CUDA(pd_malloc(&s->d_bad, sizeof(unsigned long long)));
+            PD_CUDA(pd_malloc(&s->d_rows, sizeof(double) * 3 * (size_t)kBatch));
+            PD_CUDA(pd_malloc(&s->d_region, sizeof(double) * (size_t)kBatch));
             PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)kBatch, g->stream));
             PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
             PD_CUDA(cudaEventCreate(&s->ev0));
@@ -529,13 +529,13 @@ int pd_stepper_destroy(pd_stepper* s) {
     {
         DeviceGuard dg(s->g->device);
         cudaStreamSynchronize(s->g->stream);
-        cudaFree(s->d_fluid);
-        cudaFree(s->d_sink);
-        cudaFree(s->d_nbr);
-        cudaFree(s->d_flags);
-        cudaFree(s->d_bad);
-        cudaFree(s->d_rows);
-        cudaFree(s->d_region);
+        pd_free(s->d_fluid);
+        pd_free(s->d_sink);
+        pd_free(s->d_nbr);
+        pd_free(s->d_flags);
+        pd_free(s->d_bad);
+        pd_free(s->d_rows);
+        pd_free(s->d_region);
         march_free(&s->plan);
         if (s->ev0) cudaEventDestroy(s->ev0);
         if (s->ev1) cudaEventDestroy(s->ev1);
@@ -796,13 +796,13 @@ int pd_reduce_partials(pd_grid* g, const double* dev_mass, const double* dev_min
         DeviceGuard dg(g->device);
         const int64_t cap = std::max<int64_t>(1, (n + 1023) / 1024);
         double* scratch = nullptr;
-        PD_CUDA(cudaMalloc(&scratch, sizeof(double) * (size_t)(6 * cap + 3)));
+        PD_CUDA(pd_malloc(&scratch, sizeof(double) * (size_t)(6 * cap + 3)));
         const cudaError_t e0 = [&] {
             launch_pairwise_arrays(g, dev_mass, dev_min, dev_max, n, scratch + 6 * cap, scratch);
             return cudaMemcpyAsync(row, scratch + 6 * cap, 3 * sizeof(double), cudaMemcpyDeviceToHost, g->stream);
         }();
         const cudaError_t e1 = cudaStreamSynchronize(g->stream);
-        cudaFree(scratch);
+        pd_free(scratch);
         PD_CUDA(e0);
         PD_CUDA(e1);
     });

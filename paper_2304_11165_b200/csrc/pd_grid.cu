@@ -428,13 +428,13 @@ void ensure_scratch(pd_grid* g) {
     const int64_t need = g->n_chunks > 0 ? g->n_chunks : 1;
     if (g->red.cap >= need) return;
     for (int k = 0; k < 3; ++k) {
-        if (g->red.part[k]) cudaFree(g->red.part[k]);
-        if (g->red.tmp_a[k]) cudaFree(g->red.tmp_a[k]);
-        if (g->red.tmp_b[k]) cudaFree(g->red.tmp_b[k]);
+        if (g->red.part[k]) pd_free(g->red.part[k]);
+        if (g->red.tmp_a[k]) pd_free(g->red.tmp_a[k]);
+        if (g->red.tmp_b[k]) pd_free(g->red.tmp_b[k]);
         const int64_t nb = (need + kPairBlock - 1) / kPairBlock;
-        PD_CUDA(cudaMalloc(&g->red.part[k], sizeof(double) * need));
-        PD_CUDA(cudaMalloc(&g->red.tmp_a[k], sizeof(double) * nb));
-        PD_CUDA(cudaMalloc(&g->red.tmp_b[k], sizeof(double) * nb));
+        PD_CUDA(pd_malloc(&g->red.part[k], sizeof(double) * need));
+        PD_CUDA(pd_malloc(&g->red.tmp_a[k], sizeof(double) * nb));
+        PD_CUDA(pd_malloc(&g->red.tmp_b[k], sizeof(double) * nb));
     }
     g->red.cap = need;
 }
@@ -534,7 +534,7 @@ void alloc_columns(pd_grid* g, int n_props) {
     for (int p = 0; p < n_props; ++p) {
         g->column_of[(size_t)p] = p;
         if (g->n_chunks > 0) {
-            PD_CUDA(cudaMalloc(&g->cols[(size_t)p], slab_bytes(g)));
+            PD_CUDA(pd_malloc(&g->cols[(size_t)p], slab_bytes(g)));
             PD_CUDA(cudaMemsetAsync(g->cols[(size_t)p], 0, slab_bytes(g), g->stream));
         }
     }
@@ -564,7 +564,7 @@ void init_geometry(pd_grid* g, int dims, int tbytes, const int64_t* size, const 
 
 void count_active(pd_grid* g) {
     unsigned long long* d_cnt = nullptr;
-    PD_CUDA(cudaMalloc(&d_cnt, sizeof(unsigned long long)));
+    PD_CUDA(pd_malloc(&d_cnt, sizeof(unsigned long long)));
     PD_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), g->stream));
     const int64_t words = g->n_chunks * g->W;
     if (words > 0) {
@@ -575,7 +575,7 @@ void count_active(pd_grid* g) {
     unsigned long long h = 0;
     PD_CUDA(cudaMemcpyAsync(&h, d_cnt, sizeof h, cudaMemcpyDeviceToHost, g->stream));
     PD_CUDA(cudaStreamSynchronize(g->stream));
-    cudaFree(d_cnt);
+    pd_free(d_cnt);
     g->active = (int64_t)h;
 }
 
@@ -629,13 +629,13 @@ int pd_grid_create(int dims, int scalar_bytes, const int64_t* size, const double
             PD_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
             g->stream = g->own_stream;
             g->n_chunks = n_chunks;
-            PD_CUDA(cudaMalloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
+            PD_CUDA(pd_malloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
             PD_CUDA(cudaMemsetAsync(g->d_table, 0xff, sizeof(int32_t) * (size_t)g->table_size,
                                     g->stream));
-            PD_CUDA(cudaMalloc(&g->d_row, sizeof(double) * 4));
+            PD_CUDA(pd_malloc(&g->d_row, sizeof(double) * 4));
             if (n_chunks > 0) {
-                PD_CUDA(cudaMalloc(&g->d_keys, sizeof(int32_t) * (size_t)(n_chunks * dims)));
-                PD_CUDA(cudaMalloc(&g->d_masks, sizeof(uint64_t) * (size_t)(n_chunks * g->W)));
+                PD_CUDA(pd_malloc(&g->d_keys, sizeof(int32_t) * (size_t)(n_chunks * dims)));
+                PD_CUDA(pd_malloc(&g->d_masks, sizeof(uint64_t) * (size_t)(n_chunks * g->W)));
                 PD_CUDA(cudaMemcpyAsync(g->d_keys, keys, sizeof(int32_t) * (size_t)(n_chunks * dims),
                                         cudaMemcpyHostToDevice, g->stream));
                 PD_CUDA(cudaMemcpyAsync(g->d_masks, masks,
@@ -667,15 +667,15 @@ int pd_grid_destroy(pd_grid* g) {
         DeviceGuard dg(g->device);
         if (g->stream) cudaStreamSynchronize(g->stream);
         if (g->own_stream) cudaStreamSynchronize(g->own_stream);
-        for (void* c : g->cols) cudaFree(c);
-        cudaFree(g->d_keys);
-        cudaFree(g->d_masks);
-        cudaFree(g->d_table);
-        cudaFree(g->d_row);
+        for (void* c : g->cols) pd_free(c);
+        pd_free(g->d_keys);
+        pd_free(g->d_masks);
+        pd_free(g->d_table);
+        pd_free(g->d_row);
         for (int k = 0; k < 3; ++k) {
-            cudaFree(g->red.part[k]);
-            cudaFree(g->red.tmp_a[k]);
-            cudaFree(g->red.tmp_b[k]);
+            pd_free(g->red.part[k]);
+            pd_free(g->red.tmp_a[k]);
+            pd_free(g->red.tmp_b[k]);
         }
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
     }
@@ -917,7 +917,7 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
             DeviceGuard dg(device);
             PD_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
             g->stream = g->own_stream;
-            PD_CUDA(cudaMalloc(&g->d_row, sizeof(double) * 4));
+            PD_CUDA(pd_malloc(&g->d_row, sizeof(double) * 4));
             PackArgs p;
             int64_t slots = 1;
             for (int a = 0; a < 3; ++a) {
@@ -932,8 +932,8 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
                 slots *= p.rext[a];
             }
             p.n_spheres = n_spheres;
-            PD_CUDA(cudaMalloc(&d_centers, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres * 3)));
-            PD_CUDA(cudaMalloc(&d_radii, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres)));
+            PD_CUDA(pd_malloc(&d_centers, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres * 3)));
+            PD_CUDA(pd_malloc(&d_radii, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres)));
             if (n_spheres > 0) {
                 PD_CUDA(cudaMemcpyAsync(d_centers, centers, sizeof(double) * (size_t)(n_spheres * 3),
                                         cudaMemcpyHostToDevice, g->stream));
@@ -942,7 +942,7 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
             }
             p.centers = (const double*)d_centers;
             p.radii = (const double*)d_radii;
-            PD_CUDA(cudaMalloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
+            PD_CUDA(pd_malloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
             PD_CUDA(cudaMemsetAsync(g->d_table, 0xff, sizeof(int32_t) * (size_t)g->table_size, g->stream));
             if (slots == 0) {
                 if (chunk_lo == nullptr)
@@ -950,14 +950,14 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
                 alloc_columns(g, n_props);
                 ensure_scratch(g);
                 PD_CUDA(cudaStreamSynchronize(g->stream));
-                cudaFree(d_centers);
-                cudaFree(d_radii);
+                pd_free(d_centers);
+                pd_free(d_radii);
                 *out = g;
                 return;
             }
-            PD_CUDA(cudaMalloc(&slot_masks, sizeof(uint64_t) * (size_t)slots * 8));
-            PD_CUDA(cudaMalloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
-            PD_CUDA(cudaMalloc(&ordinal, sizeof(int32_t) * (size_t)slots));
+            PD_CUDA(pd_malloc(&slot_masks, sizeof(uint64_t) * (size_t)slots * 8));
+            PD_CUDA(pd_malloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
+            PD_CUDA(pd_malloc(&ordinal, sizeof(int32_t) * (size_t)slots));
             if (scalar_bytes == 8) {
                 const double eps = std::numeric_limits<double>::epsilon();
                 pack_mask_kernel<double><<<(unsigned)slots, 512, 0, g->stream>>>(
@@ -971,7 +971,7 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
             size_t tmp_bytes = 0;
             PD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, slot_flag, ordinal,
                                                   (int)slots, g->stream));
-            PD_CUDA(cudaMalloc(&cub_tmp, tmp_bytes));
+            PD_CUDA(pd_malloc(&cub_tmp, tmp_bytes));
             PD_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, tmp_bytes, slot_flag, ordinal,
                                                   (int)slots, g->stream));
             int32_t last_ord = 0, last_flag = 0;
@@ -983,8 +983,8 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
             g->n_chunks = (int64_t)last_ord + last_flag;
             if (g->n_chunks == 0 && chunk_lo == nullptr)
                 fail(PD_E_INPUT, "no node lies inside the phase band: the grid would be empty");
-            PD_CUDA(cudaMalloc(&g->d_keys, sizeof(int32_t) * (size_t)(g->n_chunks * 3)));
-            PD_CUDA(cudaMalloc(&g->d_masks, sizeof(uint64_t) * (size_t)(g->n_chunks * 8)));
+            PD_CUDA(pd_malloc(&g->d_keys, sizeof(int32_t) * (size_t)(g->n_chunks * 3)));
+            PD_CUDA(pd_malloc(&g->d_masks, sizeof(uint64_t) * (size_t)(g->n_chunks * 8)));
             alloc_columns(g, n_props);
             if (scalar_bytes == 8)
                 pack_fill_kernel<double><<<(unsigned)slots, 512, 0, g->stream>>>(
@@ -999,21 +999,21 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
             count_active(g);
             ensure_scratch(g);
         } catch (...) {
-            cudaFree(d_centers);
-            cudaFree(d_radii);
-            cudaFree(slot_masks);
-            cudaFree(slot_flag);
-            cudaFree(ordinal);
-            cudaFree(cub_tmp);
+            pd_free(d_centers);
+            pd_free(d_radii);
+            pd_free(slot_masks);
+            pd_free(slot_flag);
+            pd_free(ordinal);
+            pd_free(cub_tmp);
             pd_grid_destroy(g);
             throw;
         }
-        cudaFree(d_centers);
-        cudaFree(d_radii);
-        cudaFree(slot_masks);
-        cudaFree(slot_flag);
-        cudaFree(ordinal);
-        cudaFree(cub_tmp);
+        pd_free(d_centers);
+        pd_free(d_radii);
+        pd_free(slot_masks);
+        pd_free(slot_flag);
+        pd_free(ordinal);
+        pd_free(cub_tmp);
         *out = g;
     });
 }

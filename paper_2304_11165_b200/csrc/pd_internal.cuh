@@ -12,6 +12,42 @@
 
 namespace pdb {
 
+// Device allocations come from the device's stream-ordered memory pool with
+// an unlimited release threshold, so memory freed by one grid / stepper /
+// temporary is reused by the next without returning to the driver (grids are
+// created and destroyed per FRAP probe and per run_simulation call; plain
+// cudaMalloc/cudaFree cost tens of milliseconds at these sizes and synchronise
+// the device). The allocation is complete before pd_malloc returns; pd_free
+// waits for outstanding device work first, as cudaFree does.
+inline void pool_init_once() {
+    static thread_local int done_for = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (done_for == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_for = dev;
+}
+template <class T>
+inline cudaError_t pd_malloc(T** p, size_t n) {
+    pool_init_once();
+    void* v = nullptr;
+    cudaError_t e = cudaMallocAsync(&v, n, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    *p = static_cast<T*>(v);
+    return e;
+}
+inline cudaError_t pd_free(void* p) {
+    if (!p) return cudaSuccess;
+    cudaDeviceSynchronize();
+    const cudaError_t e = cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
+    return e;
+}
+
 struct Error {
     int code;
     std::string msg;

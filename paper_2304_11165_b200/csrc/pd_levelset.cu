@@ -278,9 +278,9 @@ void build_from_field(const pd_field* f, double b_low, double b_up, int n_props,
     int32_t *slot_flag = nullptr, *ordinal = nullptr;
     void* tmp = nullptr;
     try {
-        PD_CUDA(cudaMalloc(&slot_masks, sizeof(uint64_t) * (size_t)(slots * W)));
-        PD_CUDA(cudaMalloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
-        PD_CUDA(cudaMalloc(&ordinal, sizeof(int32_t) * (size_t)slots));
+        PD_CUDA(pd_malloc(&slot_masks, sizeof(uint64_t) * (size_t)(slots * W)));
+        PD_CUDA(pd_malloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
+        PD_CUDA(pd_malloc(&ordinal, sizeof(int32_t) * (size_t)slots));
         // eps = numeric_limits<T>::epsilon(); lo = T(b_low) + eps, hi = T(b_up) - eps
         const T eps = std::numeric_limits<T>::epsilon();
         const T lo = static_cast<T>(b_low) + eps;
@@ -290,7 +290,7 @@ void build_from_field(const pd_field* f, double b_low, double b_up, int n_props,
         PD_CUDA(cudaGetLastError());
         size_t tb = 0;
         PD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, slot_flag, ordinal, (int)slots, g->stream));
-        PD_CUDA(cudaMalloc(&tmp, tb));
+        PD_CUDA(pd_malloc(&tmp, tb));
         PD_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, slot_flag, ordinal, (int)slots, g->stream));
         int32_t last_ord = 0, last_flag = 0;
         PD_CUDA(cudaMemcpyAsync(&last_ord, ordinal + slots - 1, 4, cudaMemcpyDeviceToHost, g->stream));
@@ -298,8 +298,8 @@ void build_from_field(const pd_field* f, double b_low, double b_up, int n_props,
         PD_CUDA(cudaStreamSynchronize(g->stream));
         g->n_chunks = (int64_t)last_ord + last_flag;
         if (g->n_chunks == 0) fail(PD_E_INPUT, "no node lies inside the phase band: the grid would be empty");
-        PD_CUDA(cudaMalloc(&g->d_keys, sizeof(int32_t) * (size_t)(g->n_chunks * D)));
-        PD_CUDA(cudaMalloc(&g->d_masks, sizeof(uint64_t) * (size_t)(g->n_chunks * W)));
+        PD_CUDA(pd_malloc(&g->d_keys, sizeof(int32_t) * (size_t)(g->n_chunks * D)));
+        PD_CUDA(pd_malloc(&g->d_masks, sizeof(uint64_t) * (size_t)(g->n_chunks * W)));
         alloc_columns(g, n_props);
         field_fill_kernel<T, D><<<(unsigned)slots, V, 0, g->stream>>>(
             (const T*)f->d, fg, g->cc[0], g->cc[1], slot_masks, slot_flag, ordinal, g->d_keys, g->d_masks,
@@ -307,16 +307,16 @@ void build_from_field(const pd_field* f, double b_low, double b_up, int n_props,
         PD_CUDA(cudaGetLastError());
         PD_CUDA(cudaStreamSynchronize(g->stream));
     } catch (...) {
-        cudaFree(slot_masks);
-        cudaFree(slot_flag);
-        cudaFree(ordinal);
-        cudaFree(tmp);
+        pd_free(slot_masks);
+        pd_free(slot_flag);
+        pd_free(ordinal);
+        pd_free(tmp);
         throw;
     }
-    cudaFree(slot_masks);
-    cudaFree(slot_flag);
-    cudaFree(ordinal);
-    cudaFree(tmp);
+    pd_free(slot_masks);
+    pd_free(slot_flag);
+    pd_free(ordinal);
+    pd_free(tmp);
 }
 
 template <class T>
@@ -338,10 +338,10 @@ void redistance(pd_field* f, const pd_levelset_options* o, pd_redistance_diag* o
     int* d_state = nullptr;  // done, iters
     const int kSync = 32;    // sweeps per host check
     try {
-        PD_CUDA(cudaMalloc(&next, sizeof(T) * (size_t)f->n));
-        PD_CUDA(cudaMalloc(&d_res, sizeof(typename Bits<T>::U) * (size_t)(o->max_iterations + 1)));
+        PD_CUDA(pd_malloc(&next, sizeof(T) * (size_t)f->n));
+        PD_CUDA(pd_malloc(&d_res, sizeof(typename Bits<T>::U) * (size_t)(o->max_iterations + 1)));
         PD_CUDA(cudaMemsetAsync(d_res, 0, sizeof(typename Bits<T>::U) * (size_t)(o->max_iterations + 1), f->stream));
-        PD_CUDA(cudaMalloc(&d_state, 2 * sizeof(int)));
+        PD_CUDA(pd_malloc(&d_state, 2 * sizeof(int)));
         PD_CUDA(cudaMemsetAsync(d_state, 0, 2 * sizeof(int), f->stream));
         T* bufs[2] = {(T*)f->d, next};
         int h_state[2] = {0, 0};
@@ -377,14 +377,14 @@ void redistance(pd_field* f, const pd_levelset_options* o, pd_redistance_diag* o
         out->final_residual = static_cast<double>(resid) / static_cast<double>(K.h);
         out->converged = h_state[0];
     } catch (...) {
-        cudaFree(next);
-        cudaFree(d_res);
-        cudaFree(d_state);
+        pd_free(next);
+        pd_free(d_res);
+        pd_free(d_state);
         throw;
     }
-    cudaFree(next);
-    cudaFree(d_res);
-    cudaFree(d_state);
+    pd_free(next);
+    pd_free(d_res);
+    pd_free(d_state);
 }
 
 }  // namespace pdb
@@ -415,7 +415,7 @@ int pd_field_create(int dims, int scalar_bytes, const int64_t* size, const doubl
             }
             DeviceGuard dg(device);
             PD_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
-            PD_CUDA(cudaMalloc(&f->d, (size_t)f->n * (size_t)scalar_bytes));
+            PD_CUDA(pd_malloc(&f->d, (size_t)f->n * (size_t)scalar_bytes));
             PD_CUDA(cudaMemsetAsync(f->d, 0, (size_t)f->n * (size_t)scalar_bytes, f->stream));
             PD_CUDA(cudaStreamSynchronize(f->stream));
         } catch (...) {
@@ -431,7 +431,7 @@ int pd_field_destroy(pd_field* f) {
     {
         DeviceGuard dg(f->device);
         if (f->stream) cudaStreamSynchronize(f->stream);
-        cudaFree(f->d);
+        pd_free(f->d);
         if (f->stream) cudaStreamDestroy(f->stream);
     }
     delete f;
@@ -476,14 +476,14 @@ int pd_field_from_mask(pd_field* f, const uint8_t* host_bits, int64_t n_bits) {
         if (n_bits != f->n) fail(PD_E_INPUT, "mask bit count does not match voxel count");
         DeviceGuard dg(f->device);
         uint8_t* d_bits = nullptr;
-        PD_CUDA(cudaMalloc(&d_bits, (size_t)f->n));
+        PD_CUDA(pd_malloc(&d_bits, (size_t)f->n));
         PD_CUDA(cudaMemcpyAsync(d_bits, host_bits, (size_t)f->n, cudaMemcpyHostToDevice, f->stream));
         if (f->tbytes == 8)
             indicator_kernel<double><<<blocks_for(f->n), kFieldThreads, 0, f->stream>>>(d_bits, f->n, (double*)f->d);
         else
             indicator_kernel<float><<<blocks_for(f->n), kFieldThreads, 0, f->stream>>>(d_bits, f->n, (float*)f->d);
         const cudaError_t e = cudaStreamSynchronize(f->stream);
-        cudaFree(d_bits);
+        pd_free(d_bits);
         PD_CUDA(e);
     });
 }
@@ -497,9 +497,9 @@ int pd_field_filter_thin(pd_field* f, int min_thickness_cells) {
         uint8_t *a = nullptr, *b = nullptr;
         int* bad = nullptr;
         try {
-            PD_CUDA(cudaMalloc(&a, (size_t)f->n));
-            PD_CUDA(cudaMalloc(&b, (size_t)f->n));
-            PD_CUDA(cudaMalloc(&bad, sizeof(int)));
+            PD_CUDA(pd_malloc(&a, (size_t)f->n));
+            PD_CUDA(pd_malloc(&b, (size_t)f->n));
+            PD_CUDA(pd_malloc(&bad, sizeof(int)));
             PD_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), f->stream));
             if (f->tbytes == 8)
                 cells_from_indicator<double><<<blocks_for(f->n), kFieldThreads, 0, f->stream>>>((const double*)f->d,
@@ -528,14 +528,14 @@ int pd_field_filter_thin(pd_field* f, int min_thickness_cells) {
             PD_CUDA(cudaGetLastError());
             PD_CUDA(cudaStreamSynchronize(f->stream));
         } catch (...) {
-            cudaFree(a);
-            cudaFree(b);
-            cudaFree(bad);
+            pd_free(a);
+            pd_free(b);
+            pd_free(bad);
             throw;
         }
-        cudaFree(a);
-        cudaFree(b);
-        cudaFree(bad);
+        pd_free(a);
+        pd_free(b);
+        pd_free(bad);
     });
 }
 
@@ -549,7 +549,7 @@ int pd_field_redistance(pd_field* f, const pd_levelset_options* o, pd_redistance
             fail(PD_E_INPUT, "pseudo_time_step must lie in (0, 1] (units of h)");
         DeviceGuard dg(f->device);
         int* flags = nullptr;
-        PD_CUDA(cudaMalloc(&flags, 2 * sizeof(int)));
+        PD_CUDA(pd_malloc(&flags, 2 * sizeof(int)));
         int h[2] = {0, 0};
         try {
             PD_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), f->stream));
@@ -563,10 +563,10 @@ int pd_field_redistance(pd_field* f, const pd_levelset_options* o, pd_redistance
             PD_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, f->stream));
             PD_CUDA(cudaStreamSynchronize(f->stream));
         } catch (...) {
-            cudaFree(flags);
+            pd_free(flags);
             throw;
         }
-        cudaFree(flags);
+        pd_free(flags);
         if (h[0]) fail(PD_E_INPUT, "redistancing input contains non-finite values");
         if (!h[1]) fail(PD_E_INPUT, "no interface found: the field never changes sign");
         if (f->tbytes == 8)
@@ -587,7 +587,7 @@ int pd_build_grid_from_field(const pd_field* f, double b_low, double b_up, int n
         DeviceGuard dg(f->device);
         {  // all_finite (geometry.hpp:158)
             int* flags = nullptr;
-            PD_CUDA(cudaMalloc(&flags, 2 * sizeof(int)));
+            PD_CUDA(pd_malloc(&flags, 2 * sizeof(int)));
             int h[2] = {0, 0};
             PD_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), f->stream));
             const FieldGeo g = field_geo(f);
@@ -599,7 +599,7 @@ int pd_build_grid_from_field(const pd_field* f, double b_low, double b_up, int n
                     (const float*)f->d, g, f->dims, flags);
             const cudaError_t e1 = cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, f->stream);
             const cudaError_t e2 = cudaStreamSynchronize(f->stream);
-            cudaFree(flags);
+            pd_free(flags);
             PD_CUDA(e1);
             PD_CUDA(e2);
             if (h[0]) fail(PD_E_INPUT, "level-set field contains non-finite values");
@@ -609,8 +609,8 @@ int pd_build_grid_from_field(const pd_field* f, double b_low, double b_up, int n
             init_geometry(g, f->dims, f->tbytes, f->size, f->spacing, f->device);
             g->stream = f->stream;  // temporarily share the field's stream
             PD_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
-            PD_CUDA(cudaMalloc(&g->d_row, sizeof(double) * 4));
-            PD_CUDA(cudaMalloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
+            PD_CUDA(pd_malloc(&g->d_row, sizeof(double) * 4));
+            PD_CUDA(pd_malloc(&g->d_table, sizeof(int32_t) * (size_t)g->table_size));
             PD_CUDA(cudaMemsetAsync(g->d_table, 0xff, sizeof(int32_t) * (size_t)g->table_size, g->stream));
             if (f->tbytes == 8 && f->dims == 3)
                 build_from_field<double, 3>(f, b_low, b_up, n_props, prop_phi, g);

@@ -37,6 +37,8 @@
 // planes per warp iteration), ten fixed slots, 12 warps per SM, swizzled
 // tile rows. 19 % fewer instructions than v14 but not faster yet (see
 // DESIGN.md); kept for the next round's tuning.
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>
@@ -1099,47 +1101,65 @@ __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __r
 
 void march_free(MarchPlan* p) {
     for (auto& sp : p->subs) {
-        cudaFree(sp.d_stream);
-        cudaFree(sp.d_counter);
+        pd_free(sp.d_stream);
+        pd_free(sp.d_counter);
     }
-    cudaFree(p->d_stream);
-    cudaFree(p->d_desc);
-    cudaFree(p->d_deff);
-    cudaFree(p->d_counter);
-    cudaFree(p->d_lm);
-    cudaFree(p->d_lq);
+    pd_free(p->d_stream);
+    pd_free(p->d_desc);
+    pd_free(p->d_deff);
+    pd_free(p->d_counter);
+    pd_free(p->d_lm);
+    pd_free(p->d_lq);
     *p = MarchPlan{};
 }
 
 // Device schedule of the chunk ordinals [begin, end): (z-block of kSeg
 // layers, 4x4 column tiles, column, z), so the chunks in flight form one
 // short window and neighbour halos hit L2.
+__global__ void sched_key_kernel(const int32_t* __restrict__ keys, int64_t begin, int64_t n,
+                                 unsigned long long* __restrict__ sk, int32_t* __restrict__ ord) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t* k = keys + (begin + i) * 3;
+    const unsigned long long x = (unsigned)k[0], y = (unsigned)k[1], z = (unsigned)k[2];
+    // (z-block of kSeg layers, 4x4 column tile, column, z); keys < 1024 per axis
+    sk[i] = ((z / kSeg) << 50) | ((y >> 2) << 42) | ((x >> 2) << 34) | (y << 20) | (x << 10) | z;
+    ord[i] = (int32_t)(begin + i);
+}
+
 int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end) {
+    // device radix sort of per-chunk schedule keys (the host sort cost ~20 ms
+    // at 10^5 chunks)
     const int64_t n = end - begin;
-    std::vector<int32_t> keys((size_t)n * 3);
-    if (n > 0)
-        PD_CUDA(cudaMemcpyAsync(keys.data(), g->d_keys + begin * 3, sizeof(int32_t) * 3 * (size_t)n,
-                                cudaMemcpyDeviceToHost, g->stream));
-    PD_CUDA(cudaStreamSynchronize(g->stream));
-    std::vector<int32_t> order((size_t)n);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-        const int32_t* ka = &keys[(size_t)a * 3];
-        const int32_t* kb = &keys[(size_t)b * 3];
-        const int za = ka[2] / kSeg, zb = kb[2] / kSeg;
-        if (za != zb) return za < zb;
-        if (ka[1] / 4 != kb[1] / 4) return ka[1] / 4 < kb[1] / 4;
-        if (ka[0] / 4 != kb[0] / 4) return ka[0] / 4 < kb[0] / 4;
-        if (ka[1] != kb[1]) return ka[1] < kb[1];
-        if (ka[0] != kb[0]) return ka[0] < kb[0];
-        return ka[2] < kb[2];
-    });
-    for (auto& o : order) o = (int32_t)(o + begin);
     int32_t* d = nullptr;
-    PD_CUDA(cudaMalloc(&d, sizeof(int32_t) * std::max<size_t>(1, order.size())));
-    if (n > 0)
-        PD_CUDA(cudaMemcpyAsync(d, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, g->stream));
-    PD_CUDA(cudaStreamSynchronize(g->stream));
+    PD_CUDA(pd_malloc(&d, sizeof(int32_t) * (size_t)std::max<int64_t>(1, n)));
+    if (n == 0) return d;
+    unsigned long long *k_in = nullptr, *k_out = nullptr;
+    int32_t* o_in = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    try {
+        PD_CUDA(pd_malloc(&k_in, sizeof(unsigned long long) * (size_t)n));
+        PD_CUDA(pd_malloc(&k_out, sizeof(unsigned long long) * (size_t)n));
+        PD_CUDA(pd_malloc(&o_in, sizeof(int32_t) * (size_t)n));
+        sched_key_kernel<<<(unsigned)((n + 255) / 256), 256, 0, g->stream>>>(g->d_keys, begin, n, k_in, o_in);
+        PD_CUDA(cudaGetLastError());
+        PD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, o_in, d, (int)n, 0, 60, g->stream));
+        PD_CUDA(pd_malloc(&tmp, tb));
+        PD_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, o_in, d, (int)n, 0, 60, g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+    } catch (...) {
+        pd_free(k_in);
+        pd_free(k_out);
+        pd_free(o_in);
+        pd_free(tmp);
+        pd_free(d);
+        throw;
+    }
+    pd_free(k_in);
+    pd_free(k_out);
+    pd_free(o_in);
+    pd_free(tmp);
     return d;
 }
 
@@ -1151,14 +1171,17 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     const int64_t n_all = g->n_chunks;
     if (n_all == 0 || end <= begin) return;
     if (n_all * 512 >= (int64_t)0xFFFFFFFF) return;  // 32-bit slot offsets (>16 GB per column)
-    PD_CUDA(cudaMalloc(&plan->d_desc, sizeof(int32_t) * 8 * (size_t)n_all));
+    PD_CUDA(pd_malloc(&plan->d_desc, sizeof(int32_t) * 8 * (size_t)n_all));
     desc_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(
         d_nbr, g->d_keys, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
     PD_CUDA(cudaGetLastError());
-    PD_CUDA(cudaMalloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
-    PD_CUDA(cudaMalloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
-    lanemask15_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
-                                                                                  plan->d_lq);
+    PD_CUDA(pd_malloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
+    const char* ver_env = getenv("PD_MARCH_V");
+    if (ver_env && atoi(ver_env) >= 15) {  // quad lane masks only for the v15/v16 variants
+        PD_CUDA(pd_malloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
+        lanemask15_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
+                                                                                      plan->d_lq);
+    }
     lanemask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink,
                                                                                 n_all, plan->d_lm);
     PD_CUDA(cudaGetLastError());
@@ -1166,12 +1189,12 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     // one extra chunk of sentinels after the last one: the source of every
     // D_eff cell a plane load does not read from the grid (inactive pairs,
     // missing neighbours), so the loads need no shared-memory sentinel stores
-    PD_CUDA(cudaMalloc(&plan->d_deff, sizeof(double) * (size_t)(slots + 512)));
+    PD_CUDA(pd_malloc(&plan->d_deff, sizeof(double) * (size_t)(slots + 512)));
     PD_CUDA(cudaMemsetAsync(plan->d_deff + slots, 0, sizeof(double) * 512, g->stream));
     sentinel_fill_kernel<<<1, 512, 0, g->stream>>>(plan->d_deff + slots);
-    PD_CUDA(cudaMalloc(&plan->d_counter, sizeof(int) * 1024));
+    PD_CUDA(pd_malloc(&plan->d_counter, sizeof(int) * 1024));
     unsigned long long* d_bad = nullptr;
-    PD_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+    PD_CUDA(pd_malloc(&d_bad, sizeof(unsigned long long)));
     PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
     deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>(
         (const double*)d_dcol, d_fluid, slots, plan->d_deff, d_bad);
@@ -1179,7 +1202,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     unsigned long long bad = 0;
     PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
     PD_CUDA(cudaStreamSynchronize(g->stream));
-    cudaFree(d_bad);
+    pd_free(d_bad);
     if (bad) {  // non-finite D on a fluid node: keep the exact tile kernel
         march_free(plan);
         return;
@@ -1208,7 +1231,7 @@ MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end) 
     sp.end = end;
     sp.n = end - begin;
     sp.d_stream = march_schedule(g, begin, end);
-    PD_CUDA(cudaMalloc(&sp.d_counter, sizeof(int)));
+    PD_CUDA(pd_malloc(&sp.d_counter, sizeof(int)));
     p.subs.push_back(sp);
     return p.subs.back();
 }

@@ -142,9 +142,9 @@ struct Pinned {
 };
 struct DevBuf {
     unsigned char* p = nullptr;
-    explicit DevBuf(size_t n) { PD_CUDA(cudaMalloc(&p, n)); }
+    explicit DevBuf(size_t n) { PD_CUDA(pd_malloc(&p, n)); }
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) pd_free(p);
     }
 };
 
