@@ -402,8 +402,12 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         fill_args<double>(s, a, u, un, factor);
         a.k = k;
         a.ord0 = s->begin;
-        if (!diag && s->use_march && s->plan.ready && s->end - s->begin >= march_min_chunks()) {
+        if (s->use_march && s->plan.ready && s->end - s->begin >= march_min_chunks()) {
             march_launch(g, s->plan, a, s->cfg.reaction_kind);
+            // record step: per-chunk sequential mass / min / max of the new u
+            // in the reference's order (solver.hpp:264-278), a second pass
+            // (8 B/node) instead of the slower generic diagnostics kernel
+            if (diag) launch_chunk_stats(g, un, g->d_masks);
         } else if (g->dims == 3) {
             if (diag) ftcs_step_kernel<double, 3, true><<<nb, 512, 0, g->stream>>>(a);
             else ftcs_step_kernel<double, 3, false><<<nb, 512, 0, g->stream>>>(a);

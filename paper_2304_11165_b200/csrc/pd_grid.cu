@@ -49,45 +49,35 @@ __global__ void build_table_kernel(const int32_t* __restrict__ keys, int64_t n,
 __device__ __forceinline__ double min_left(double l, double r) { return (r < l) ? r : l; }
 __device__ __forceinline__ double max_left(double l, double r) { return (l < r) ? r : l; }
 
+// One thread per chunk: the reference's sequential per-chunk mass over the
+// active offsets in ascending order, and the std::min / std::max folds in the
+// same order (the first of equal values is kept; NaN never enters the fold).
+// A thread walks its own slab; consecutive offsets share L1 lines.
 template <class T, int D>
-__global__ void __launch_bounds__(Geo<D>::V)
-    chunk_stats_kernel(const T* __restrict__ x, const uint64_t* __restrict__ masks,
-                       double* __restrict__ mass, double* __restrict__ mn,
-                       double* __restrict__ mx) {
+__global__ void __launch_bounds__(128)
+    chunk_stats_kernel(const T* __restrict__ x, const uint64_t* __restrict__ masks, int64_t n,
+                       double* __restrict__ mass, double* __restrict__ mn, double* __restrict__ mx) {
     constexpr int V = Geo<D>::V, W = Geo<D>::W;
-    __shared__ double sv[V], smn[V], smx[V];
-    __shared__ uint64_t sm[W];
-    const int64_t i = blockIdx.x;
-    const int off = threadIdx.x;
-    if (off < W) sm[off] = masks[i * W + off];
-    const bool act = (masks[i * W + (off >> 6)] >> (off & 63)) & 1u;
-    const double v = act ? (double)x[i * V + off] : 0.0;
-    sv[off] = v;
-    const bool ok = act && !isnan(v);
-    smn[off] = ok ? v : INFINITY;
-    smx[off] = ok ? v : -INFINITY;
-    __syncthreads();
-    for (int s = 1; s < V; s <<= 1) {
-        if ((off & (2 * s - 1)) == 0) {
-            smn[off] = min_left(smn[off], smn[off + s]);
-            smx[off] = max_left(smx[off], smx[off + s]);
-        }
-        __syncthreads();
-    }
-    if (off == 0) {
-        double acc = 0.0;
-        for (int w = 0; w < W; ++w) {
-            uint64_t bits = sm[w];
-            while (bits) {
-                const int b = __ffsll((long long)bits) - 1;
-                acc += sv[w * 64 + b];
-                bits &= bits - 1;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const T* xs = x + i * V;
+    double acc = 0.0, lo = INFINITY, hi = -INFINITY;
+    for (int w = 0; w < W; ++w) {
+        uint64_t bits = __ldg(&masks[i * W + w]);
+        while (bits) {
+            const int b = __ffsll((long long)bits) - 1;
+            bits &= bits - 1;
+            const double v = (double)__ldg(&xs[w * 64 + b]);
+            acc += v;
+            if (!isnan(v)) {
+                lo = min_left(lo, v);
+                hi = max_left(hi, v);
             }
         }
-        mass[i] = acc;
-        mn[i] = smn[0];
-        mx[i] = smx[0];
     }
+    mass[i] = acc;
+    mn[i] = lo;
+    mx[i] = hi;
 }
 
 // pairwise_sum (parallel.hpp:68-84): element j of level L covers leaves
@@ -445,8 +435,8 @@ void launch_chunk_stats(pd_grid* g, const void* col, const uint64_t* masks) {
     dispatch(g, [&](auto tp, auto dc) {
         using T = std::remove_pointer_t<decltype(tp)>;
         constexpr int D = decltype(dc)::value;
-        chunk_stats_kernel<T, D><<<(unsigned)g->n_chunks, Geo<D>::V, 0, g->stream>>>(
-            (const T*)col, masks, g->red.part[0], g->red.part[1], g->red.part[2]);
+        chunk_stats_kernel<T, D><<<(unsigned)((g->n_chunks + 127) / 128), 128, 0, g->stream>>>(
+            (const T*)col, masks, g->n_chunks, g->red.part[0], g->red.part[1], g->red.part[2]);
     });
     PD_CUDA(cudaGetLastError());
 }

@@ -223,7 +223,9 @@ def test_overlapped_enqueue_and_exact_diagnostics(world, n, cuda):
         pd._check(lib.pd_stepper_partials(s, C.c_void_p(p[0].data_ptr()), C.c_void_p(p[1].data_ptr()),
                                           C.c_void_p(p[2].data_ptr())))
         parts.append(p[:, :k])
+    torch.cuda.synchronize()  # partials were written on the shard grids' own streams
     glob = torch.cat(parts, dim=1).contiguous()
+    torch.cuda.synchronize()
     assert glob.shape[1] == len(keys_full)
     row = (C.c_double * 3)()
     pd._check(lib.pd_reduce_partials(shards[0][0].h, C.c_void_p(glob[0].data_ptr()), C.c_void_p(glob[1].data_ptr()),
