@@ -1031,6 +1031,352 @@ __global__ void __launch_bounds__(kThreads, R10 ? 3 : kCtas15) ftcs_march15_kern
     cp_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// v17 "row march": every lane computes a whole x-row (8 nodes) of one plane —
+// lane (y, zq) = (lane & 7, lane >> 3) takes row y of plane 4*it + zq, so a
+// warp covers half a chunk per iteration. x faces come from registers; the
+// y / z neighbour rows are read as four 16-B granules per array. Tile rows
+// have an 80-B pitch (8 doubles + the row's two x-halo cells), which makes the
+// eight lanes of every LDS.128 phase (eight rows, same granule) hit eight
+// distinct 16-B bank groups. Continuous 16-slot ring per warp (slot = load
+// index & 15), 8 warps per SM; loads run 1-1.5 iterations ahead.
+// ---------------------------------------------------------------------------
+constexpr int kRing17 = 16;
+constexpr int kCtas17 = 2;
+constexpr uint32_t kRow17 = 80;                    // row pitch (bytes)
+constexpr uint32_t kArr17 = 10 * kRow17;           // one array (rows -1..8)
+constexpr uint32_t kTile17 = 2 * kArr17;           // u then D_eff
+constexpr uint32_t kWarpBytes17 = kRing17 * kTile17 + 3 * kCtxBytes15;
+
+__device__ __forceinline__ LaneGeo lane_geo17(int lane) {  // load side in the v17 tile layout
+    LaneGeo G = lane_geo(lane);
+    const uint32_t R = (uint32_t)G.y + 1;
+    G.s_c = kRow17 * R + 16u * (uint32_t)G.xp;
+    G.s_hx = kRow17 * R + 64u + (G.xp == 3 ? 8u : 0u);
+    G.s_hy = (G.y == 0 ? 0u : 9u * kRow17) + 16u * (uint32_t)G.xp;
+    return G;
+}
+
+__device__ __forceinline__ void issue17(uint32_t st, const double* __restrict__ u, const double* __restrict__ de,
+                                        const LoadCtx14& L, int i, const LaneGeo& G, uint32_t sent_off) {
+    if (i == 0 || i == 9) {
+        const bool ok = i == 0 ? L.zlok : L.zhok;
+        const uint32_t o = i == 0 ? L.zl : L.zh;
+        cp16_ud(st + G.s_c, u + o, ok, st + kArr17 + G.s_c, de + (ok ? o : sent_off + G.bp), true);
+        return;
+    }
+    const uint32_t p64 = (uint32_t)(i - 1) * 64u;
+    const bool ok = ((L.lm >> (2 * (i - 1))) & 3u) != 0u;
+    const uint32_t o = L.own + p64;
+    cp16_ud(st + G.s_c, u + o, ok, st + kArr17 + G.s_c, de + (ok ? o : sent_off + G.bp + p64), true);
+    const uint32_t ox = L.xo + p64;
+    cp8_ud(st + G.s_hx, u + ox, L.xok, st + kArr17 + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64), G.xface);
+    const uint32_t oy = L.yo + p64;
+    cp16_ud(st + G.s_hy, u + oy, L.yok, st + kArr17 + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64), G.yface);
+}
+
+struct ChunkCtx17 {
+    int c, key, flags;
+    uint32_t lr;  // bit 8*it + x: node x of the lane's row in plane 4*it + zq active; +16: sink
+};
+
+__global__ void lanemask17_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ snk, int64_t n,
+                                  uint32_t* __restrict__ lr) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * 32) return;
+    const int64_t c = t >> 5;
+    const int lane = (int)(t & 31);
+    const int y = lane & 7, zq = lane >> 3;
+    uint32_t v = 0;
+    for (int it = 0; it < 2; ++it) {
+        const int z = 4 * it + zq;
+        v |= (uint32_t)((act[c * 8 + z] >> (8 * y)) & 0xFFull) << (8 * it);
+        v |= (uint32_t)((snk[c * 8 + z] >> (8 * y)) & 0xFFull) << (16 + 8 * it);
+    }
+    lr[t] = v;
+}
+
+// Rare path of one row: exact generic update per node from the ring.
+template <int REACTION>
+__device__ __noinline__ void row_slow(unsigned long long* bad_key, int* flagp, const SlowConsts& K,
+                                      const double* __restrict__ src, int c, int key, int cflags, uint32_t bits, int z,
+                                      int y, uint32_t tm, uint32_t t0, uint32_t tp, double* out) {
+    const uint32_t o = kRow17 * (uint32_t)(y + 1);
+    double u[10], d[10];  // x = -1..8
+    u[0] = lds1(t0 + o + 64);
+    d[0] = lds1(t0 + kArr17 + o + 64);
+    u[9] = lds1(t0 + o + 72);
+    d[9] = lds1(t0 + kArr17 + o + 72);
+    for (int x = 0; x < 8; ++x) {
+        u[x + 1] = lds1(t0 + o + 8u * x);
+        d[x + 1] = lds1(t0 + kArr17 + o + 8u * x);
+    }
+    const bool dirichlet = (cflags & kFlagDirichlet) != 0;
+    const int kx = key & 1023, ky = (key >> 10) & 1023, kz = (key >> 20) & 1023;
+    bool any = false;
+    bool h[8];
+    for (int x = 0; x < 8; ++x) {
+        const bool a = (bits >> x) & 1u;
+        const double uc = u[x + 1], dc = d[x + 1];
+        const uint32_t e = o + 8u * x;
+        const double nu[6] = {u[x], u[x + 2], lds1(t0 + e - kRow17), lds1(t0 + e + kRow17), lds1(tm + e), lds1(tp + e)};
+        const double nd[6] = {d[x], d[x + 2], lds1(t0 + kArr17 + e - kRow17), lds1(t0 + kArr17 + e + kRow17),
+                              lds1(tm + kArr17 + e), lds1(tp + kArr17 + e)};
+        const bool s = REACTION == PD_REACTION_SURFACE_SINK && ((bits >> (16 + x)) & 1u);
+        const double sv = REACTION == PD_REACTION_VOLUMETRIC ? src[(int64_t)c * 512 + z * 64 + y * 8 + x] : 0.0;
+        const int64_t gx = (int64_t)kx * 8 + x, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
+        if (dirichlet) {
+            if (!sentinel(dc)) out[x] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
+            h[x] = a && huge(out[x]);
+        } else {
+            h[x] = a && huge(out[x]);
+            if (h[x] && !isfinite(out[x]) && !sentinel(dc))
+                out[x] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
+        }
+        any = any || h[x];
+    }
+    if (any) {
+        int first = -1;
+        for (int x = 7; x >= 0; --x)
+            if (((bits >> x) & 1u) && !isfinite(out[x])) first = x;
+        if (first >= 0) {
+            atomicMin(bad_key, ((unsigned long long)c << 10) | (unsigned long long)(z * 64 + y * 8 + first));
+            atomicOr(flagp, 1);
+        } else {
+            atomicOr(flagp, 2);
+        }
+    }
+}
+
+template <int INTERIOR>
+__device__ __forceinline__ double rface(double da, double db, double ua, double ub) {
+    return INTERIOR ? fface(da, db, ua, ub) : face(da, db, ua, ub);
+}
+
+// One row of 8 nodes: lap = 0 + x, += y, += z (solver.hpp:420-433, axes in order).
+template <int INTERIOR>
+__device__ __forceinline__ void row_lap(const Consts& Q, uint32_t t0, uint32_t tm, uint32_t tp, uint32_t o,
+                                        const double* u, const double* d, double* lap) {
+    const double2 hu = lds2(t0 + o + 64), hd = lds2(t0 + kArr17 + o + 64);  // x = -1, x = 8
+    double fprev = rface<INTERIOR>(hd.x, d[0], hu.x, u[0]);
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+        const double fnext = x < 7 ? rface<INTERIOR>(d[x], d[x + 1], u[x], u[x + 1]) : rface<INTERIOR>(d[7], hd.y, u[7], hu.y);
+        lap[x] = 0.0 + (fnext - fprev) * Q.ix;
+        fprev = fnext;
+    }
+#pragma unroll
+    for (int ax = 0; ax < 2; ++ax) {
+        const uint32_t om = ax == 0 ? t0 + o - kRow17 : tm + o;
+        const uint32_t op = ax == 0 ? t0 + o + kRow17 : tp + o;
+        const double w = ax == 0 ? Q.iy : Q.iz;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const double2 um = lds2(om + 16u * g), dm = lds2(om + kArr17 + 16u * g);
+            const double2 up = lds2(op + 16u * g), dp = lds2(op + kArr17 + 16u * g);
+            const int x = 2 * g;
+            const double m0 = rface<INTERIOR>(dm.x, d[x], um.x, u[x]);
+            const double p0 = rface<INTERIOR>(d[x], dp.x, u[x], up.x);
+            const double m1 = rface<INTERIOR>(dm.y, d[x + 1], um.y, u[x + 1]);
+            const double p1 = rface<INTERIOR>(d[x + 1], dp.y, u[x + 1], up.y);
+            lap[x] += (p0 - m0) * w;
+            lap[x + 1] += (p1 - m1) * w;
+        }
+    }
+}
+
+template <int REACTION>
+__device__ __forceinline__ void compute17(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
+                                          const ChunkCtx17& C, int it, uint32_t sb, uint32_t base, int y, int zq,
+                                          double* __restrict__ un) {
+    const int z = 4 * it + zq;
+    const uint32_t b = base + (uint32_t)z;
+    const uint32_t tm = sb + (b & 15u) * kTile17;
+    const uint32_t t0 = sb + ((b + 1u) & 15u) * kTile17;
+    const uint32_t tp = sb + ((b + 2u) & 15u) * kTile17;
+    const uint32_t bits = (C.lr >> (8 * it)) & 0x00FF00FFu;
+    const uint32_t o = kRow17 * (uint32_t)(y + 1);
+    double u[8], d[8], lap[8];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const double2 a = lds2(t0 + o + 16u * g), e = lds2(t0 + kArr17 + o + 16u * g);
+        u[2 * g] = a.x;
+        u[2 * g + 1] = a.y;
+        d[2 * g] = e.x;
+        d[2 * g + 1] = e.y;
+    }
+    const bool interior = ((C.flags >> (8 + 4 * it)) & 15) == 15;  // all four planes (warp-uniform)
+    if (interior)
+        row_lap<1>(Q, t0, tm, tp, o, u, d, lap);
+    else
+        row_lap<0>(Q, t0, tm, tp, o, u, d, lap);
+    double out[8];
+    bool hot = false;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+        double r = 0.0;
+        if (REACTION == PD_REACTION_SURFACE_SINK) {
+            r = ((bits >> (16 + x)) & 1u) ? Q.neg_k * u[x] : 0.0;
+        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+            r = M.A.src[(uint32_t)C.c * 512u + (uint32_t)z * 64u + (uint32_t)y * 8u + x] * Q.src_factor;
+        }
+        out[x] = u[x] + Q.dt * lap[x] + Q.dt * r;
+        if (!interior && sentinel(d[x])) out[x] = u[x];  // walls stay frozen (solver.hpp:413-417)
+        hot = hot || (((bits >> x) & 1u) && huge(out[x]));
+    }
+    if ((C.flags & kFlagDirichlet) || hot)
+        row_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, M.A.src, C.c, C.key, C.flags, bits, z, y, tm, t0, tp,
+                           out);
+    double* dst = un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + (uint32_t)y * 8u);
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+        stg_pair(dst + 2 * g, out[2 * g], out[2 * g + 1], (bits >> (2 * g)) & 1u, (bits >> (2 * g + 1)) & 1u);
+}
+
+template <int REACTION>
+__global__ void __launch_bounds__(kThreads, kCtas17) ftcs_march17_kernel(MarchArgs M) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+    }
+    __syncthreads();
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const LaneGeo G = lane_geo17(lane);
+    const int ry = lane & 7, rzq = lane >> 3;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes17;
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    double* __restrict__ un = A.un;
+    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
+
+    // chunk pipeline (see ftcs_march14_kernel), compute-side masks in lr
+    int* ctr_l = M.counter + ((t >> 5) & M.zero);
+    const int n = (int)M.n;
+    const uint32_t cb = sb + kRing17 * kTile17;
+    auto cent = [&](int e) -> uint32_t { return cb + (uint32_t)e * kCtxBytes15; };
+    int raw = 0;
+    auto claim_issue = [&]() {
+        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(raw) : "l"(ctr_l) : "memory");
+    };
+    auto sched_sync = [&]() -> int {
+        claim_issue();
+        const int p = __shfl_sync(0xffffffffu, raw, 0);
+        return p < n ? __ldg(&M.sched[p]) : -1;
+    };
+    auto fetch_ctx = [&](uint32_t e, int c) {
+        const int64_t cc = c < 0 ? 0 : c;
+        cp4(e + 4u * (uint32_t)lane, M.lm + cc * 32 + lane, c >= 0);
+        cp4(e + kCtxLq + 4u * (uint32_t)lane, M.lq + cc * 32 + lane, c >= 0);
+        cp4(e + kCtxDesc + 4u * (uint32_t)(lane & 7), M.desc + cc * 8 + (lane & 7), c >= 0 && lane < 8);
+    };
+    {
+        const int id0 = sched_sync();
+        if (id0 < 0) return;
+        const int id1 = sched_sync();
+        if (lane == 0) {
+            sts_u32(cent(0) + kCtxId, (uint32_t)id0);
+            sts_u32(cent(1) + kCtxId, (uint32_t)id1);
+        }
+        fetch_ctx(cent(0), id0);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        claim_issue();
+    }
+    int ek = 0;
+    ChunkCtx17 Cld, Cprev;
+    LoadCtx14 Lld;
+    auto advance = [&]() {
+        Cprev = Cld;
+        const uint32_t e0 = cent(ek);
+        const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
+        const uint32_t e1 = cent(e1i), e2 = cent(e2i);
+        const int c = (int)lds_u32(e0 + kCtxId);
+        const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
+        const uint32_t lr = c >= 0 ? lds_u32(e0 + kCtxLq + 4u * (uint32_t)lane) : 0u;
+        const int dv = (int)lds_u32(e0 + kCtxDesc + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
+        Cld = ChunkCtx17{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lr};
+        Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
+        const int c1 = (int)lds_u32(e1 + kCtxId);
+        fetch_ctx(e1, c1);
+        if (lane == 0) {
+            const bool ok = raw < n;
+            cp4(e2 + kCtxId, M.sched + (ok ? raw : 0), ok);
+            if (!ok) sts_u32(e2 + kCtxId, 0xFFFFFFFFu);
+        }
+        claim_issue();
+        ek = e1i;
+    };
+    advance();
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+    int p_ld = 0;
+    uint32_t Lc = 0;
+    auto issue_next = [&]() {
+        issue17(sb + (Lc & (kRing17 - 1)) * kTile17, u, de, Lld, p_ld, G, sent_off);
+        if (++p_ld == 10) {
+            p_ld = 0;
+            // the context fetched at the previous advance (ten loads ago) must
+            // have landed: at most the nine newest groups may still be pending
+            cp_wait<9>();
+            __syncwarp();
+            advance();
+        }
+        cp_commit();
+        ++Lc;
+    };
+    ChunkCtx17 Cc = Cld;
+    uint32_t base = 0;  // load index of plane -1 of Cc
+    // prologue: this chunk's 10 loads and the next chunk's loads 0..5
+#pragma unroll 1
+    for (int k = 0; k < 16; ++k) issue_next();
+#pragma unroll 1
+    while (Cc.c >= 0) {
+        // before each half: the loads it needs are done, ten newer ones in flight
+        cp_wait<10>();
+        __syncwarp();
+        compute17<REACTION>(M, K, Q, Cc, 0, sb, base, ry, rzq, un);
+        __syncwarp();
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) issue_next();  // next chunk's loads 6..9 (slots of planes -1..2)
+        cp_wait<10>();
+        __syncwarp();
+        compute17<REACTION>(M, K, Q, Cc, 1, sb, base, ry, rzq, un);
+        __syncwarp();
+#pragma unroll 1
+        for (int k = 0; k < 6; ++k) issue_next();  // the chunk after's loads 0..5
+        base += 10u;
+        Cc = Cprev;
+    }
+    cp_wait<0>();
+}
+
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
@@ -1177,9 +1523,14 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaGetLastError());
     PD_CUDA(pd_malloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
     const char* ver_env = getenv("PD_MARCH_V");
-    if (ver_env && atoi(ver_env) >= 15) {  // quad lane masks only for the v15/v16 variants
+    const int ver = ver_env ? atoi(ver_env) : 14;
+    if (ver == 15 || ver == 16) {  // quad lane masks
         PD_CUDA(pd_malloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
         lanemask15_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
+                                                                                      plan->d_lq);
+    } else if (ver == 17) {  // row lane masks
+        PD_CUDA(pd_malloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
+        lanemask17_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
                                                                                       plan->d_lq);
     }
     lanemask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink,
@@ -1265,7 +1616,19 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
-    if (ver == 15 || ver == 16) {
+    if (ver == 17) {
+        constexpr size_t bytes = (size_t)kWarpBytes17 * kWarps;
+        static const KernT table[3] = {ftcs_march17_kernel<0>, ftcs_march17_kernel<1>, ftcs_march17_kernel<2>};
+        static bool attr_set = false;
+        if (!attr_set) {
+            for (auto k : table)
+                PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            attr_set = true;
+        }
+        int sms = 148;
+        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+        table[r]<<<sms * kCtas17, kThreads, bytes, g->stream>>>(M);
+    } else if (ver == 15 || ver == 16) {
         const bool r10 = ver == 16;
         const size_t bytes = (size_t)((r10 ? 10 : kRing14) * kTileBytes + 3 * kCtxBytes15) * kWarps;
         static const KernT table[2][3] = {
