@@ -321,6 +321,35 @@ int pd_field_read_snapshot(const char* path, int dims, int scalar_bytes, int dev
 /* peek_snapshot: header only. */
 int pd_peek_snapshot(const char* path, pd_snapshot_info* info, char* names_buf, size_t names_cap);
 
+/* ---- VTK export (reference vtk.hpp:57-143, scalar_text.hpp:20-28; SURVEY
+ * §8f row 4) ---------------------------------------------------------------
+ * Legacy ASCII STRUCTURED_POINTS files, byte-identical to the reference's
+ * write_vtk: the text of every node is produced on the device by an exact
+ * "%.17g" / "%.9g" formatter and streamed to the file in batches. */
+
+/* format_scalar (scalar_text.hpp:20-28): the text the device formatter
+ * produces for v ("%.17g" when scalar_bytes is 8, "%.9g" of the float value
+ * when 4, "nan" for any NaN), NUL-terminated; cap >= 26 always suffices. */
+int pd_format_scalar(double v, int scalar_bytes, char* buf, size_t cap, int* len);
+/* write_vtk (vtk.hpp:57-111) of a dense dataset: n_arrays scalar arrays of
+ * node_count values (scalar_bytes each; host or device pointers) and an
+ * optional int32 mask array (same residency), lattice size/spacing/origin of
+ * `dims` entries (2-D lattices get a third extent of 1). Names are checked
+ * like the reference (empty, whitespace, duplicates; PD_E_INPUT). */
+int pd_write_vtk(const char* path, const char* title, int dims, const int64_t* size, const double* spacing,
+                 const double* origin, int scalar_bytes, int n_arrays, const char* const* names,
+                 const void* const* values, int values_on_device, const int32_t* mask, int device);
+/* write_vtk(vtk_from_sparse(grid, channels, blank)) (vtk.hpp:115-143) fused on
+ * the device: logical properties props[0..n_sel) written under `names`,
+ * inactive nodes print `blank` (cast to the grid scalar), then the mask array
+ * (1 = active). */
+int pd_grid_write_vtk(pd_grid* g, const char* path, const char* title, const int* props, const char* const* names,
+                      int n_sel, double blank, const double* origin);
+/* vtk_from_sparse (vtk.hpp:115-143) arrays: property `prop` densified onto
+ * the full lattice (x fastest; inactive = blank) and/or the int32 mask, into
+ * host buffers (either may be NULL). */
+int pd_grid_densify(pd_grid* g, int prop, double blank, void* host_values, int32_t* host_mask);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,9 @@ class Ref:
         L.ref_grid_read_snapshot.restype = P
         L.ref_grid_read_snapshot.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
         L.ref_field_write_snapshot.argtypes = [C.c_int, C.c_int, P, P, P, P, C.c_char_p]
+        L.ref_grid_write_vtk.argtypes = [P, C.c_char_p, C.c_char_p, C.c_double, P]
+        L.ref_write_vtk.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, P, P, P, C.c_int, C.c_char_p, P, P,
+                                    C.c_int64]
 
     def field_redistance(self, size, spacing, values, opts):
         """sussman_redistance on a dense field (axis 0 fastest); returns
@@ -139,6 +142,19 @@ class Ref:
         v = np.ascontiguousarray(values)
         code = self.L.ref_field_write_snapshot(len(size), v.dtype.itemsize, _p(size, np.int64), _p(list(spacing), np.float64),
                                                _p(list(origin), np.float64), v.ctypes.data, str(path).encode())
+        return code, self.last_error()
+
+    def write_vtk(self, path, size, spacing, origin, arrays, mask=None, title="porediff field export"):
+        """write_vtk (vtk.hpp:57-111) of a dense dataset: arrays = [(name, values)]
+        (one dtype), mask = int32 values or None."""
+        vals = [np.ascontiguousarray(v) for _, v in arrays]
+        tb = vals[0].dtype.itemsize if vals else 8
+        ptrs = (C.c_void_p * max(1, len(vals)))(*[v.ctypes.data for v in vals])
+        m = None if mask is None else np.ascontiguousarray(mask, np.int32)
+        code = self.L.ref_write_vtk(str(path).encode(), title.encode(), len(size), tb, _p(size, np.int64),
+                                    _p(list(spacing), np.float64), _p(list(origin), np.float64), len(vals),
+                                    "\n".join(nm for nm, _ in arrays).encode(), ptrs,
+                                    None if m is None else m.ctypes.data, 0 if m is None else len(m))
         return code, self.last_error()
 
     def read_sparse_snapshot(self, path):
@@ -227,6 +243,12 @@ class RefGrid:
 
     def write_snapshot(self, path):
         return self.ref.L.ref_grid_write_snapshot(self.h, str(path).encode()), self.ref.last_error()
+
+    def write_vtk(self, path, channels=(), blank=float("nan"), origin=None):
+        """write_vtk(vtk_from_sparse(grid, channels, blank))."""
+        o = None if origin is None else _p(list(origin), np.float64)
+        code = self.ref.L.ref_grid_write_vtk(self.h, str(path).encode(), "\n".join(channels).encode(), blank, o)
+        return code, self.ref.last_error()
 
     def chunk_count(self):
         return self.ref.L.ref_grid_chunk_count(self.h)

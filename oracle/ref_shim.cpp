@@ -26,6 +26,7 @@
 #include "porediff/config.hpp"
 #include "porediff/levelset.hpp"
 #include "porediff/snapshot.hpp"
+#include "porediff/vtk.hpp"
 
 #include "porediff_b200.h"  // pd_sim_config / pd_diag layouts only
 
@@ -73,6 +74,7 @@ struct RefGridBase {
     virtual double total_mass(int prop) const = 0;
     virtual double max_diffusivity(int prop) const = 0;
     virtual void write_snapshot(const char* path) const = 0;
+    virtual void write_vtk(const char* path, const char* channels, double blank, const double* origin) const = 0;
 };
 
 template <typename T, int D>
@@ -86,6 +88,25 @@ struct RefGrid : RefGridBase {
     int64_t chunk_count() const override { return g.chunk_count(); }
     int64_t active_count() const override { return g.active_node_count(); }
     void write_snapshot(const char* path) const override { pd::write_sparse_snapshot(g, path); }
+    // write_vtk(vtk_from_sparse(g, channels, blank)); channels: '\n'-joined,
+    // empty = every property; origin overrides the grid's when non-null
+    void write_vtk(const char* path, const char* channels, double blank, const double* origin) const override {
+        std::vector<std::string> ch;
+        std::string cur;
+        for (const char* c = channels; *c; ++c) {
+            if (*c == '\n') {
+                ch.push_back(cur);
+                cur.clear();
+            } else {
+                cur.push_back(*c);
+            }
+        }
+        if (!cur.empty()) ch.push_back(cur);
+        auto ds = pd::vtk_from_sparse(g, ch, static_cast<T>(blank));
+        if (origin)
+            for (int a = 0; a < D; ++a) ds.geometry.origin[a] = origin[a];
+        pd::write_vtk(ds, path);
+    }
 
     void export_layout(int32_t* keys, uint64_t* masks) const override {
         int64_t i = 0;
@@ -466,6 +487,49 @@ int ref_field_write_snapshot(int dims, int tbytes, const int64_t* size, const do
             pd::DenseField<T, D> f(geom_of<D>(size, spacing, origin));
             std::memcpy(f.data(), data, sizeof(T) * (size_t)f.node_count());
             pd::write_dense_snapshot(f, path);
+        };
+        if (dims == 3 && tbytes == 8) go(double{}, std::integral_constant<int, 3>{});
+        else if (dims == 2 && tbytes == 8) go(double{}, std::integral_constant<int, 2>{});
+        else if (dims == 3) go(float{}, std::integral_constant<int, 3>{});
+        else go(float{}, std::integral_constant<int, 2>{});
+    });
+}
+
+/* ---- VTK (vtk.hpp) ------------------------------------------------------- */
+
+int ref_grid_write_vtk(void* h, const char* path, const char* channels, double blank, const double* origin) {
+    return guarded([&] { static_cast<RefGridBase*>(h)->write_vtk(path, channels, blank, origin); });
+}
+
+/* write_vtk of a dense dataset: n_arrays arrays (names '\n'-joined), optional
+ * int32 mask (NULL = none). */
+int ref_write_vtk(const char* path, const char* title, int dims, int tbytes, const int64_t* size,
+                  const double* spacing, const double* origin, int n_arrays, const char* names,
+                  const void* const* values, const int32_t* mask, int64_t mask_len) {
+    return guarded([&] {
+        std::vector<std::string> nm;
+        std::string cur;
+        for (const char* c = names; *c; ++c) {
+            if (*c == '\n') {
+                nm.push_back(cur);
+                cur.clear();
+            } else {
+                cur.push_back(*c);
+            }
+        }
+        nm.push_back(cur);
+        auto go = [&](auto tag, auto dc) {
+            using T = decltype(tag);
+            constexpr int D = decltype(dc)::value;
+            pd::VtkDataset<T, D> ds;
+            ds.geometry = geom_of<D>(size, spacing, origin);
+            const size_t n = (size_t)ds.geometry.node_count();
+            for (int i = 0; i < n_arrays; ++i) {
+                const T* v = static_cast<const T*>(values[i]);
+                ds.add_scalar(nm[(size_t)i], std::vector<T>(v, v + n));
+            }
+            if (mask) ds.mask.assign(mask, mask + mask_len);
+            pd::write_vtk(ds, path, title);
         };
         if (dims == 3 && tbytes == 8) go(double{}, std::integral_constant<int, 3>{});
         else if (dims == 2 && tbytes == 8) go(double{}, std::integral_constant<int, 2>{});

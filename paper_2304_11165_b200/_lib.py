@@ -151,6 +151,12 @@ _SIGNATURES = [
     ("pd_field_write_snapshot", C.c_int, [_P, C.c_char_p]),
     ("pd_field_read_snapshot", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     ("pd_peek_snapshot", C.c_int, [C.c_char_p, C.POINTER(pd_snapshot_info), C.c_char_p, C.c_size_t]),
+    ("pd_format_scalar", C.c_int, [C.c_double, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]),
+    ("pd_write_vtk", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int64), _DP, _DP, C.c_int, C.c_int,
+                               C.POINTER(C.c_char_p), C.POINTER(C.c_void_p), C.c_int, _P, C.c_int]),
+    ("pd_grid_write_vtk", C.c_int, [_P, C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_char_p), C.c_int,
+                                    C.c_double, _DP]),
+    ("pd_grid_densify", C.c_int, [_P, C.c_int, C.c_double, _P, _P]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

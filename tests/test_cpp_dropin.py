@@ -63,3 +63,11 @@ def test_reference_analysis_suite_on_b200():
 @pytest.mark.gpu
 def test_dropin_mirror_coherence():
     _run("dropin_test")
+
+
+@pytest.mark.gpu
+def test_reference_io_suite_on_b200():
+    # scalar text, SBGD/SBGR snapshots (device-assembled records), mask files,
+    # VTK (node texts formatted on the device) through the drop-in headers
+    out = _run("io_test")
+    assert "[  PASSED  ]" in out
