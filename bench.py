@@ -253,10 +253,10 @@ def run_ours(args):
         ms = dom.run(stepper, args.warmup, args.steps)
         sync()
         wall = time.perf_counter() - t0
-    # step kernels + (N>1) two face packs and two unpacks per step
+    # step kernels + (N>1) the exchange's own kernels: peer wait + signal per
+    # step (fused push), or two face packs and two unpacks (NCCL transport)
     launches = dom.launches(stepper) - launches0
-    if world > 1:
-        launches += 4 * args.steps
+    launches += dom.extra_launches_per_step * args.steps
     # exact global diagnostics of the final state (all ranks take part)
     diag = dom.diagnostics(stepper)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")

@@ -321,6 +321,38 @@ int pd_field_read_snapshot(const char* path, int dims, int scalar_bytes, int dev
 /* peek_snapshot: header only. */
 int pd_peek_snapshot(const char* path, pd_snapshot_info* info, char* names_buf, size_t names_cap);
 
+/* ---- fused multi-GPU halo exchange over peer memory (
+ * pd_peer.cu) ---------------------------------------------------------------
+ * Replaces the pack -> NCCL send/recv -> unpack exchange (pd_grid_pack_face /
+ * pd_grid_unpack_face) for 3-D FP64 z-slab shards: the step kernel stores
+ * each boundary chunk's new z=0 (side 0, lower neighbour) or z=7 (side 1,
+ * upper neighbour) plane straight into the neighbour's ghost chunk, and
+ * per-neighbour step counters in peer memory order the steps (wait before a
+ * step, signal after it). Across processes the neighbour's columns and
+ * counters are mapped with CUDA IPC (pd_grid_make_shareable,
+ * pd_grid_ipc_handles, pd_stepper_sync_ipc_handle, pd_ipc_open); within one
+ * process the raw pointers are passed. */
+int pd_grid_make_shareable(pd_grid* g);            /* columns -> cudaMalloc (IPC-exportable) */
+int pd_grid_ipc_handles(pd_grid* g, void* out);    /* n_props handles of pd_ipc_handle_size() bytes */
+int pd_grid_column_ptrs(pd_grid* g, void** out);   /* n_props physical column pointers */
+int pd_ipc_handle_size(void);
+int pd_ipc_open(const void* handle, int device, void** ptr);
+int pd_ipc_close(void* ptr, int device);
+/* the stepper's two step-counter words ([0] raised by the lower neighbour,
+ * [1] by the upper one), created on first use */
+int pd_stepper_sync_words(pd_stepper* s, void** ptr);
+int pd_stepper_sync_ipc_handle(pd_stepper* s, void* out);
+/* side 0 = lower, 1 = upper neighbour: its physical column pointers (n_cols =
+ * n_props, same property order), its counter words, and the n pairs (own
+ * boundary chunk ordinal -> neighbour's ghost chunk ordinal). From then on
+ * every step of pd_stepper_run / pd_stepper_enqueue (whole owned range) waits,
+ * pushes and signals. peer_sync NULL removes the side. */
+int pd_stepper_set_peer(pd_stepper* s, int side, void* const* peer_cols, int n_cols, void* peer_sync,
+                        const int32_t* src_ords, const int32_t* dst_ords, int64_t n);
+/* zero the own counters and the step epoch (all ranks, then a host barrier,
+ * before the first exchanged step) */
+int pd_stepper_peer_reset(pd_stepper* s);
+
 /* ---- VTK export (reference vtk.hpp:57-143, scalar_text.hpp:20-28; SURVEY
  * §8f row 4) ---------------------------------------------------------------
  * Legacy ASCII STRUCTURED_POINTS files, byte-identical to the reference's

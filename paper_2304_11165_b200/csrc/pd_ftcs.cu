@@ -24,6 +24,8 @@
 #include <initializer_list>
 #include <limits>
 
+#include <cstring>
+
 #include "pd_internal.cuh"
 
 namespace pdb {
@@ -307,6 +309,7 @@ struct pd_stepper {
     int64_t rlo[3] = {0, 0, 0}, rhi[3] = {0, 0, 0};
     double* d_region = nullptr;  // one per row of the batch
     std::vector<double> region_out;
+    pdb::PeerState peer;  // fused multi-GPU halo push (pd_peer.cu)
 };
 
 namespace {
@@ -393,6 +396,27 @@ void fill_args(const pd_stepper* s, StepArgs<T>& a, const void* u, void* un, dou
     a.flags = s->d_flags;
 }
 
+// One step of the owned range with the fused halo push: wait for the
+// neighbours' previous step, march (boundary planes stored into their ghost
+// chunks as they are computed), raise their counters.
+void launch_peer_step(pd_stepper* s, const StepArgs<double>& a) {
+    pd_grid* g = s->g;
+    if (!s->plan.ready) fail(PD_E_INPUT, "the fused peer halo push needs the march path (3-D FP64 grid)");
+    if (s->peer.flags_dirty) {
+        march_push_flags(g, s->plan, s->peer.d_ord);
+        s->peer.flags_dirty = false;
+    }
+    PeerLaunch pl;
+    const int cn = g->column_of[(size_t)s->prop_next];
+    for (int side = 0; side < 2; ++side)
+        pl.un[side] = s->peer.side[side] ? static_cast<double*>(s->peer.cols[side][cn]) : nullptr;
+    pl.ord = s->peer.d_ord;
+    peer_wait(g->stream, s->peer);
+    march_launch(g, s->plan, a, s->cfg.reaction_kind, &pl);
+    peer_signal(g->stream, s->peer);
+    s->peer.epoch++;
+}
+
 void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool diag, int k) {
     pd_grid* g = s->g;
     if (s->end <= s->begin) return;
@@ -402,7 +426,10 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         fill_args<double>(s, a, u, un, factor);
         a.k = k;
         a.ord0 = s->begin;
-        if (s->use_march && s->plan.ready && s->end - s->begin >= march_min_chunks()) {
+        if (s->peer.on) {
+            launch_peer_step(s, a);
+            if (diag) launch_chunk_stats(g, un, g->d_masks);
+        } else if (s->use_march && s->plan.ready && s->end - s->begin >= march_min_chunks()) {
             march_launch(g, s->plan, a, s->cfg.reaction_kind);
             // record step: per-chunk sequential mass / min / max of the new u
             // in the reference's order (solver.hpp:264-278), a second pass
@@ -540,6 +567,9 @@ int pd_stepper_destroy(pd_stepper* s) {
         pd_free(s->d_bad);
         pd_free(s->d_rows);
         pd_free(s->d_region);
+        pd_free(s->peer.d_ord);
+        pd_free(s->peer.d_err);
+        if (s->peer.d_sync) cudaFree(s->peer.d_sync);
         march_free(&s->plan);
         if (s->ev0) cudaEventDestroy(s->ev0);
         if (s->ev1) cudaEventDestroy(s->ev1);
@@ -723,6 +753,19 @@ int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t
         const void* u = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
         void* un = g->cols[(size_t)g->column_of[(size_t)s->prop_next]];
         const unsigned nb = (unsigned)(end - begin);
+        if (s->peer.on) {
+            if (begin != s->begin || end != s->end)
+                fail(PD_E_INPUT, "with the fused peer exchange a step covers the whole owned range");
+            StepArgs<double> a;
+            fill_args<double>(s, a, u, un, factor);
+            a.k = 0;
+            a.ord0 = begin;
+            PD_CUDA(cudaMemsetAsync(s->plan.d_counter, 0, sizeof(int), g->stream));
+            launch_peer_step(s, a);
+            PD_CUDA(cudaGetLastError());
+            s->launches++;
+            return;
+        }
         if (g->tbytes == 8) {
             StepArgs<double> a;
             fill_args<double>(s, a, u, un, factor);
@@ -752,6 +795,79 @@ int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t
     });
 }
 
+int pd_stepper_sync_words(pd_stepper* s, void** ptr) {
+    return guarded([&] {
+        DeviceGuard dg(s->g->device);
+        if (!s->peer.d_sync) {  // cudaMalloc: exportable through CUDA IPC
+            PD_CUDA(cudaMalloc(&s->peer.d_sync, 64));
+            PD_CUDA(cudaMemset(s->peer.d_sync, 0, 64));
+        }
+        *ptr = s->peer.d_sync;
+    });
+}
+
+int pd_stepper_sync_ipc_handle(pd_stepper* s, void* out) {
+    return guarded([&] {
+        void* p = nullptr;
+        int rc = pd_stepper_sync_words(s, &p);
+        if (rc != PD_OK) fail(rc, pd_last_error());
+        DeviceGuard dg(s->g->device);
+        cudaIpcMemHandle_t h;
+        PD_CUDA(cudaIpcGetMemHandle(&h, p));
+        std::memcpy(out, &h, sizeof h);
+    });
+}
+
+int pd_stepper_set_peer(pd_stepper* s, int side, void* const* peer_cols, int n_cols, void* peer_sync,
+                        const int32_t* src_ords, const int32_t* dst_ords, int64_t n) {
+    return guarded([&] {
+        pd_grid* g = s->g;
+        if (side != 0 && side != 1) fail(PD_E_INPUT, "side must be 0 (lower) or 1 (upper)");
+        if (n_cols != (int)g->cols.size() || n_cols > 16) fail(PD_E_INPUT, "one peer column per grid property");
+        if (g->dims != 3 || g->tbytes != 8 || !s->plan.ready)
+            fail(PD_E_INPUT, "the fused peer halo push needs the march path (3-D FP64 grid)");
+        DeviceGuard dg(g->device);
+        void* own = nullptr;
+        int rc = pd_stepper_sync_words(s, &own);
+        if (rc != PD_OK) fail(rc, pd_last_error());
+        if (!s->peer.d_ord) {
+            PD_CUDA(pd_malloc(&s->peer.d_ord, sizeof(int32_t) * 2 * (size_t)std::max<int64_t>(1, g->n_chunks)));
+            PD_CUDA(cudaMemsetAsync(s->peer.d_ord, 0xff, sizeof(int32_t) * 2 * (size_t)std::max<int64_t>(1, g->n_chunks),
+                                    g->stream));
+            PD_CUDA(pd_malloc(&s->peer.d_err, sizeof(int)));
+            PD_CUDA(cudaMemsetAsync(s->peer.d_err, 0, sizeof(int), g->stream));
+        }
+        std::vector<int32_t> ord((size_t)g->n_chunks * 2);
+        PD_CUDA(cudaMemcpyAsync(ord.data(), s->peer.d_ord, sizeof(int32_t) * ord.size(), cudaMemcpyDeviceToHost,
+                                g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        for (int64_t c = 0; c < g->n_chunks; ++c) ord[(size_t)(2 * c + side)] = -1;
+        for (int64_t i = 0; i < n; ++i) {
+            if (src_ords[i] < s->begin || src_ords[i] >= s->end)
+                fail(PD_E_INPUT, "push source chunk outside the stepper's owned range");
+            ord[(size_t)(2 * src_ords[i] + side)] = dst_ords[i];
+        }
+        PD_CUDA(cudaMemcpyAsync(s->peer.d_ord, ord.data(), sizeof(int32_t) * ord.size(), cudaMemcpyHostToDevice,
+                                g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        for (int c = 0; c < n_cols; ++c) s->peer.cols[side][c] = peer_cols[c];
+        s->peer.sync[side] = static_cast<unsigned*>(peer_sync);
+        s->peer.side[side] = peer_sync != nullptr;
+        s->peer.on = s->peer.side[0] || s->peer.side[1];
+        s->peer.flags_dirty = true;
+    });
+}
+
+int pd_stepper_peer_reset(pd_stepper* s) {
+    return guarded([&] {
+        DeviceGuard dg(s->g->device);
+        if (s->peer.d_sync) PD_CUDA(cudaMemset(s->peer.d_sync, 0, 64));
+        if (s->peer.d_err) PD_CUDA(cudaMemset(s->peer.d_err, 0, sizeof(int)));
+        s->peer.epoch = 0;
+        PD_CUDA(cudaDeviceSynchronize());
+    });
+}
+
 int pd_stepper_swap(pd_stepper* s) {
     std::swap(s->g->column_of[(size_t)s->prop_u], s->g->column_of[(size_t)s->prop_next]);
     return PD_OK;
@@ -764,6 +880,11 @@ int pd_stepper_status(pd_stepper* s, int64_t step_number) {
         int f = 0;
         PD_CUDA(cudaMemcpyAsync(&f, s->d_flags, sizeof f, cudaMemcpyDeviceToHost, g->stream));
         PD_CUDA(cudaStreamSynchronize(g->stream));
+        if (s->peer.d_err) {
+            int e = 0;
+            PD_CUDA(cudaMemcpy(&e, s->peer.d_err, sizeof e, cudaMemcpyDeviceToHost));
+            if (e) fail(PD_E_CUDA, "peer halo exchange: a neighbour's step counter did not advance within 30 s");
+        }
         if (!(f & 1)) {
             PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int), g->stream));
             PD_CUDA(cudaStreamSynchronize(g->stream));

@@ -657,7 +657,12 @@ int pd_grid_destroy(pd_grid* g) {
         DeviceGuard dg(g->device);
         if (g->stream) cudaStreamSynchronize(g->stream);
         if (g->own_stream) cudaStreamSynchronize(g->own_stream);
-        for (void* c : g->cols) pd_free(c);
+        for (size_t i = 0; i < g->cols.size(); ++i) {
+            if (i < g->col_ipc.size() && g->col_ipc[i])
+                cudaFree(g->cols[i]);
+            else
+                pd_free(g->cols[i]);
+        }
         pd_free(g->d_keys);
         pd_free(g->d_masks);
         pd_free(g->d_table);

@@ -112,6 +112,7 @@ struct pd_grid {
     uint64_t* d_masks = nullptr;
     int32_t* d_table = nullptr;  // chunk linear index -> ordinal, -1 absent
     std::vector<void*> cols;     // physical columns
+    std::vector<char> col_ipc;   // column allocated with cudaMalloc (IPC-exportable)
     std::vector<int> column_of;  // logical property -> physical column
     cudaStream_t stream = nullptr;      // stream all work is issued on
     cudaStream_t own_stream = nullptr;  // the grid's own stream
@@ -197,11 +198,35 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
                  const void* d_dcol, int dirichlet, int64_t begin, int64_t end, MarchPlan* plan);
 int march_counters_per_step();
 void march_free(MarchPlan* plan);
-void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction);
+// fused halo push targets of one launch (pd_peer.cu)
+struct PeerLaunch {
+    double* un[2];         // lower / upper peer's u_next column base (null: none)
+    const int32_t* ord;    // [n_chunks][2] peer ghost ordinal, -1 none
+};
+void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction,
+                  const PeerLaunch* pl = nullptr);
+void march_push_flags(pd_grid* g, MarchPlan& p, const int32_t* d_ord);
 int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end);
 MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end);
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
-                        int64_t n, int* counter);
+                        int64_t n, int* counter, const PeerLaunch* pl = nullptr);
+
+// Multi-GPU peer exchange state of a stepper (pd_peer.cu, pd_ftcs.cu): the
+// step kernel pushes the boundary planes straight into the neighbours' ghost
+// chunks; per-neighbour step counters in peer memory order the steps.
+struct PeerState {
+    bool on = false;
+    bool side[2] = {false, false};   // lower / upper neighbour present
+    void* cols[2][16] = {};          // neighbour's physical column bases
+    unsigned* sync[2] = {};          // neighbour's counter words
+    unsigned* d_sync = nullptr;      // own counters: [0] written by the lower, [1] by the upper neighbour
+    int* d_err = nullptr;            // wait timed out
+    int32_t* d_ord = nullptr;        // [n_chunks][2] neighbour ghost ordinal, -1 none
+    uint32_t epoch = 0;              // steps taken since the handshake
+    bool flags_dirty = false;
+};
+void peer_wait(cudaStream_t st, const PeerState& p);
+void peer_signal(cudaStream_t st, const PeerState& p);
 // pairwise_sum + left-preference min/max fold of caller arrays (n leaves)
 // into dst[0..2] = {sum*cell_volume, min, max} (pd_grid.cu).
 void launch_pairwise_arrays(pd_grid* g, const double* m, const double* a, const double* b, int64_t n,

@@ -55,6 +55,8 @@ constexpr int kCtasPerSm = 4;  // march v14 (default): 4 CTAs x 4 warps per SM
 constexpr int kSeg = 16;
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
+constexpr int kFlagPushLo = 1 << 16;  // push the new z=0 plane to the lower peer's ghost chunk
+constexpr int kFlagPushHi = 1 << 17;  // push the new z=7 plane to the upper peer's ghost chunk
 // desc flag bits 8..15: plane z is interior-fluid (every node and every face
 // neighbour fluid) -> select-free path
 
@@ -77,6 +79,11 @@ struct MarchArgs {
     int zero;                        // 0 (opaque to the compiler)
     int64_t n_all;                   // chunks of the grid (D_eff sentinel chunk follows them)
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
+    // fused halo push (multi-GPU, pd_peer.cu): chunks flagged kFlagPushLo /
+    // kFlagPushHi also store their new z=0 / z=7 plane into the lower / upper
+    // peer's ghost chunk peer_ord[2c+side] of the peer's u_next column
+    double* peer_un[2];
+    const int32_t* __restrict__ peer_ord;
 };
 
 
@@ -410,10 +417,22 @@ __device__ __noinline__ double2 pair_slow14(const MarchArgs& M, const SlowConsts
                                nd0, nu1, nd1, uc.x, uc.y, dc.x, dc.y, s0, s1, src0, src1, out0, out1);
 }
 
+// Remote store of a node pair into the peer's ghost chunk (NVLink P2P / same
+// device); active nodes only, like the local store.
+__device__ __noinline__ void push_pair14(const MarchArgs& M, const ChunkCtx14& C, int z, uint32_t bp, double out0,
+                                         double out1, bool a0, bool a1) {
+    const int side = z == 0 ? 0 : 1;
+    if (!(C.flags & (side ? kFlagPushHi : kFlagPushLo))) return;
+    const int32_t o = __ldg(M.peer_ord + 2 * (int64_t)C.c + side);
+    double* p = M.peer_un[side] + (int64_t)o * 512 + z * 64 + bp;
+    if (a0) p[0] = out0;
+    if (a1) p[1] = out1;
+}
+
 template <int REACTION>
 __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
                                           const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
-                                          const LaneGeo& G, double* __restrict__ un) {
+                                          const LaneGeo& G, double* __restrict__ un, bool& pushed) {
     const uint32_t lz = C.lm >> (2 * z);
     const bool a0 = lz & 1u, a1 = (lz >> 1) & 1u;
     const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
@@ -479,6 +498,10 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
         out1 = r.y;
     }
     stg_pair(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, a0, a1);
+    if ((C.flags & (kFlagPushLo | kFlagPushHi)) && (z == 0 || z == 7)) {
+        push_pair14(M, C, z, G.bp, out0, out1, a0, a1);
+        pushed = true;
+    }
 }
 
 template <int REACTION>
@@ -599,6 +622,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     };
     ChunkCtx14 Cc = Cld;
     uint32_t base = 0;  // load index of plane -1 of Cc
+    bool pushed = false;
 #pragma unroll 1
     for (int k = 0; k < 3 + kAhead14; ++k) issue_next();
 #pragma unroll 1
@@ -609,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
             __syncwarp();
             const uint32_t b = base + (uint32_t)z;
             compute14<REACTION>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes, sb + ((b + 1u) & 7u) * kTileBytes,
-                                sb + ((b + 2u) & 7u) * kTileBytes, G, un);
+                                sb + ((b + 2u) & 7u) * kTileBytes, G, un, pushed);
             __syncwarp();
             issue_next();
             if (z == 7) {  // plane 8 of this chunk and plane -1 of the next
@@ -621,6 +645,9 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
         Cc = Cld;
     }
     cp_wait<0>();
+    // the pushed planes are visible system-wide before this kernel completes
+    // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
+    if (pushed) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1379,6 +1406,22 @@ __global__ void __launch_bounds__(kThreads, kCtas17) ftcs_march17_kernel(MarchAr
 
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
+// desc flags of the fused halo push: bit set iff the chunk has a peer ghost
+__global__ void push_flags_kernel(int32_t* __restrict__ desc, const int32_t* __restrict__ ord, int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int f = desc[i * 8 + 7] & ~(kFlagPushLo | kFlagPushHi);
+    if (ord[2 * i] >= 0) f |= kFlagPushLo;
+    if (ord[2 * i + 1] >= 0) f |= kFlagPushHi;
+    desc[i * 8 + 7] = f;
+}
+
+void march_push_flags(pd_grid* g, MarchPlan& p, const int32_t* d_ord) {
+    if (!p.ready || g->n_chunks == 0) return;
+    push_flags_kernel<<<(unsigned)((g->n_chunks + 255) / 256), 256, 0, g->stream>>>(p.d_desc, d_ord, g->n_chunks);
+    PD_CUDA(cudaGetLastError());
+}
+
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
                             const uint64_t* __restrict__ flu, int64_t n, int64_t s0, int64_t s1,
                             int64_t s2, int dirichlet, int32_t* __restrict__ desc) {
@@ -1569,8 +1612,8 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
 
 int march_counters_per_step() { return 1; }
 
-void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction) {
-    march_launch_sched(g, p, a, reaction, p.d_stream, p.n, p.d_counter + (a.k & 1023));
+void march_launch(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const PeerLaunch* pl) {
+    march_launch_sched(g, p, a, reaction, p.d_stream, p.n, p.d_counter + (a.k & 1023), pl);
 }
 
 // Sub-range schedule of the plan (built once per distinct [begin, end)).
@@ -1588,8 +1631,11 @@ MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end) 
 }
 
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
-                        int64_t n, int* counter) {
+                        int64_t n, int* counter, const PeerLaunch* pl) {
     MarchArgs M;
+    M.peer_un[0] = pl ? pl->un[0] : nullptr;
+    M.peer_un[1] = pl ? pl->un[1] : nullptr;
+    M.peer_ord = pl ? pl->ord : nullptr;
     M.A = a;
     M.sched = sched;
     M.n = n;
@@ -1616,6 +1662,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
+    if (pl && ver != 14) fail(PD_E_INPUT, "the fused peer halo push needs march v14 (PD_MARCH_V unset)");
     if (ver == 17) {
         constexpr size_t bytes = (size_t)kWarpBytes17 * kWarps;
         static const KernT table[3] = {ftcs_march17_kernel<0>, ftcs_march17_kernel<1>, ftcs_march17_kernel<2>};

@@ -19,18 +19,30 @@ identically on both sides, so they are never exchanged.
 The plan functions below are pure host logic (tested with gloo on CPU);
 ``Domain`` binds them to the device grid and torch.distributed NCCL.
 
-Overlap (``Domain.run``): each step enqueues the two boundary chunk layers
-first (pd_stepper_enqueue, no host sync), then the face exchange of their new
-planes runs on a communication stream (pack -> NCCL send/recv -> unpack into
-the ghost layers) while the interior layers are stepped on the compute
-stream; the next step starts after both. Record steps reduce exactly across
-ranks (``Domain.diagnostics``): per-chunk partials are gathered in rank (=
-ordinal) order and folded by the reference's pairwise tree.
+Two exchange transports:
+
+* "peer" (default for 3-D FP64 with world > 1): the exchange is fused into
+  the step kernel. Each rank maps its neighbours' u / u_next columns and step
+  counters through CUDA IPC (NVLink peer memory); the march kernel stores
+  every boundary chunk's new z=0 / z=7 plane straight into the neighbour's
+  ghost chunk while it computes the slab, and one-word step counters in the
+  neighbours' memory order consecutive steps (pd_peer.cu). A step is one
+  kernel plus a 1-thread wait and signal; no pack, no NCCL, no host sync.
+* "nccl" (PD_EXCHANGE=nccl, and FP32 / 2-D): each step enqueues the two
+  boundary chunk layers first (pd_stepper_enqueue, no host sync), then the
+  face exchange of their new planes runs on a communication stream (pack ->
+  NCCL send/recv -> unpack into the ghost layers) while the interior layers
+  are stepped on the compute stream; the next step starts after both.
+
+Record steps reduce exactly across ranks (``Domain.diagnostics``): per-chunk
+partials are gathered in rank (= ordinal) order and folded by the
+reference's pairwise tree.
 """
 from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -126,7 +138,7 @@ def exchange_numpy(plan: ExchangePlan, u: np.ndarray, rank: int, world: int, dis
 class Domain:
     """One rank's shard of a sphere-pack domain on its GPU."""
 
-    def __init__(self, n, pack, rank, world, device, dtype=np.float64):
+    def __init__(self, n, pack, rank, world, device, dtype=np.float64, exchange=None):
         import torch
 
         from . import porediff as pd
@@ -175,24 +187,32 @@ class Domain:
         self.b_recv_down, self.b_recv_up = mk(len(self.plan.recv_down)), mk(len(self.plan.recv_up))
         self._kernel_ms = 0.0
         self._steps = 0
+        if exchange is None:
+            exchange = os.environ.get("PD_EXCHANGE", "peer")
+        if np.dtype(dtype) != np.float64:
+            exchange = "nccl"  # the fused push lives in the 3-D FP64 march kernel
+        self.exchange_mode = exchange if world > 1 else "none"
+        self._ipc = []
+        # own kernels per step besides the step kernel: peer wait + signal, or
+        # two face packs and two unpacks
+        self.extra_launches_per_step = {"peer": 2, "nccl": 4}.get(self.exchange_mode, 0)
+
+    def _allreduce(self, v: float, op: str = "sum") -> float:
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return v
+        dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{self.device}"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
 
     def total_chunks(self, world):
-        import torch
-        import torch.distributed as dist
-        t = torch.tensor([self.owned_chunks], dtype=torch.float64, device=f"cuda:{self.device}")
-        if world > 1:
-            dist.all_reduce(t)
-        return int(t.item())
+        return int(self._allreduce(float(self.owned_chunks)))
 
     def stepper(self, dt_frac=0.4, sink_rate=1.0, sink_width=1.0):
-        import torch
-        import torch.distributed as dist
         pd = self.pd
-        dmax = self.dev.max_active(2)
-        t = torch.tensor([dmax], dtype=torch.float64, device=f"cuda:{self.device}")
-        if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dmax = float(t.item())
+        dmax = self._allreduce(self.dev.max_active(2), "max")
         cfg = pd.SimulationConfig(dt=dt_frac * pd.stability_dt(self.geom, dmax), n_steps=1 << 40,
                                   record_every=1 << 40)
         cfg.reaction = pd.ReactionSpec.surface_sink(sink_rate, sink_width)
@@ -201,7 +221,54 @@ class Domain:
         pd._check(self.lib.pd_stepper_create(self.dev.h, C.byref(ccfg), 0, 1, 2, 3, C.byref(h)))
         pd._check(self.lib.pd_stepper_set_range(h, self.plan.begin, self.plan.end))
         self.cfg = cfg
+        if self.exchange_mode == "peer":
+            self.setup_peer(h)
         return h
+
+    def setup_peer(self, stepper):
+        """Map the neighbours' columns and step counters (CUDA IPC) and bind
+        the fused push: my bottom layer -> lower neighbour's upper ghost
+        layer, my top layer -> upper neighbour's lower ghost layer."""
+        import torch.distributed as dist
+        lib, pd = self.lib, self.pd
+        hs = lib.pd_ipc_handle_size()
+        n_cols = 4
+        pd._check(lib.pd_grid_make_shareable(self.dev.h))
+        cols = C.create_string_buffer(hs * n_cols)
+        pd._check(lib.pd_grid_ipc_handles(self.dev.h, cols))
+        sy = C.create_string_buffer(hs)
+        pd._check(lib.pd_stepper_sync_ipc_handle(stepper, sy))
+        mine = {"cols": cols.raw, "sync": sy.raw, "recv_down": self.plan.recv_down.tolist(),
+                "recv_up": self.plan.recv_up.tolist()}
+        every = [None] * self.world
+        dist.all_gather_object(every, mine)
+
+        def opened(handle: bytes) -> int:
+            p = C.c_void_p()
+            pd._check(lib.pd_ipc_open(handle, self.device, C.byref(p)))
+            self._ipc.append(p.value)
+            return p.value
+
+        for side, nb, src in ((0, self.rank - 1, self.plan.send_down), (1, self.rank + 1, self.plan.send_up)):
+            if nb < 0 or nb >= self.world:
+                continue
+            o = every[nb]
+            dst = np.asarray(o["recv_up"] if side == 0 else o["recv_down"], np.int32)
+            src = np.ascontiguousarray(src, np.int32)
+            if len(dst) != len(src):
+                raise RuntimeError(f"rank {self.rank}: boundary layer has {len(src)} chunks, "
+                                   f"neighbour ghost layer {len(dst)}")
+            ptrs = (C.c_void_p * n_cols)(*[opened(o["cols"][c * hs:(c + 1) * hs]) for c in range(n_cols)])
+            sp = opened(o["sync"])
+            pd._check(lib.pd_stepper_set_peer(stepper, side, ptrs, n_cols, C.c_void_p(sp), src.ctypes.data,
+                                              dst.ctypes.data, len(src)))
+        pd._check(lib.pd_stepper_peer_reset(stepper))
+        dist.barrier()
+
+    def close_peer(self):
+        for p in self._ipc:
+            self.lib.pd_ipc_close(C.c_void_p(p), self.device)
+        self._ipc = []
 
     def exchange(self, prop: int = 1):
         """Device halo exchange of the face planes of logical property `prop`
@@ -246,8 +313,8 @@ class Domain:
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(self.stream)
         if overlap is None:
-            overlap = self.world > 1
-        if not overlap:
+            overlap = self.exchange_mode == "nccl"
+        if not overlap:  # one device call; with "peer" every step waits, pushes, signals
             rows = (pd._lib.pd_diag * 1)()
             nr = C.c_int64()
             pd._check(lib.pd_stepper_run(stepper, step0, n, 1 << 40, None, rows, C.byref(nr)))
@@ -277,7 +344,7 @@ class Domain:
             kms = None
         e1.record(self.stream)
         e1.synchronize()
-        if overlap:
+        if overlap or self.exchange_mode == "peer":
             pd._check(lib.pd_stepper_status(stepper, step0 + n))
         ms = e0.elapsed_time(e1)
         kms = ms if kms is None else kms  # overlapped: whole step (kernels + exchange)
@@ -299,16 +366,18 @@ class Domain:
         P = lambda t: C.c_void_p(t.data_ptr())
         pd._check(lib.pd_stepper_partials(stepper, P(parts[0]), P(parts[1]), P(parts[2])))
         if self.world > 1:
-            cnt = torch.tensor([n_own], dtype=torch.int64, device=dev)
+            cdev = "cpu" if dist.get_backend() == "gloo" else dev
+            torch.cuda.synchronize(self.device)
+            cnt = torch.tensor([n_own], dtype=torch.int64, device=cdev)
             cnts = [torch.zeros_like(cnt) for _ in range(self.world)]
             dist.all_gather(cnts, cnt)
             cnts = [int(c.item()) for c in cnts]
             m = max(1, max(cnts))
-            pad = torch.zeros((3, m), dtype=torch.float64, device=dev)
-            pad[:, :n_own] = parts[:, :n_own]
+            pad = torch.zeros((3, m), dtype=torch.float64, device=cdev)
+            pad[:, :n_own] = parts[:, :n_own].to(cdev)
             allp = [torch.empty_like(pad) for _ in range(self.world)]
             dist.all_gather(allp, pad)
-            glob = torch.cat([a[:, :c] for a, c in zip(allp, cnts)], dim=1).contiguous()
+            glob = torch.cat([a[:, :c] for a, c in zip(allp, cnts)], dim=1).to(dev).contiguous()
         else:
             glob = parts[:, :n_own].contiguous()
         row = (C.c_double * 3)()

@@ -257,3 +257,77 @@ def test_domain_overlapped_path_equals_batched_run(cuda):
     ua, ub = a.dev.download(1), b.dev.download(1)
     assert np.array_equal(ua.view(np.uint64), ub.view(np.uint64))
     assert a.diagnostics(sa) == b.diagnostics(sb)
+
+
+@pytest.mark.parametrize("world,n", [(2, 48), (3, 64)])
+def test_fused_peer_push_equals_unsharded(world, n, cuda):
+    """The fused exchange (pd_stepper_set_peer): the march kernel stores each
+    boundary chunk's new z=0 / z=7 plane straight into the neighbour shard's
+    ghost chunk and per-neighbour step counters order the steps — `world`
+    shards on one GPU, each on its own stream, all steps enqueued without a
+    host sync — equals the unsharded run bit for bit."""
+    from paper_2304_11165_b200 import porediff as pd
+    from paper_2304_11165_b200 import shard
+    from paper_2304_11165_b200._lib import lib
+    from paper_2304_11165_b200.synthetic import SpherePacking
+
+    geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
+    pk = SpherePacking.random((0, 0, 0), (1, 1, 1), 36, 0.06, 0.14, 17)
+    centers, radii = pk.arrays()
+    cc = (n + 7) // 8
+    full = _build(pd, lib, geom, centers, radii, (0, 0, 0), (cc, cc, cc))
+    dt = 0.45 * pd.stability_dt(geom, full.max_active(2))
+    steps = 11
+    s_full = _stepper(pd, lib, full, dt)
+    rows = (pd._lib.pd_diag * 1)()
+    nr = C.c_int64()
+    pd._check(lib.pd_stepper_run(s_full, 0, steps, 1 << 40, None, rows, C.byref(nr)))
+    u_full = full.download(1)
+    keys_full, _ = full.layout()
+
+    shards = []
+    for r in range(world):
+        z0, z1 = shard.slab_bounds(cc, world, r)
+        dev = _build(pd, lib, geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)))
+        keys, _ = dev.layout()
+        plan = shard.exchange_plan(keys, z0, z1, r, world)
+        s = _stepper(pd, lib, dev, dt, (plan.begin, plan.end))
+        cols = (C.c_void_p * 4)()
+        pd._check(lib.pd_grid_column_ptrs(dev.h, cols))
+        sync = C.c_void_p()
+        pd._check(lib.pd_stepper_sync_words(s, C.byref(sync)))
+        shards.append((dev, plan, s, keys, cols, sync))
+    for r, (dev, plan, s, keys, cols, sync) in enumerate(shards):
+        for side, nb, src in ((0, r - 1, plan.send_down), (1, r + 1, plan.send_up)):
+            if nb < 0 or nb >= world:
+                continue
+            o = shards[nb]
+            dst = np.ascontiguousarray(o[1].recv_up if side == 0 else o[1].recv_down, np.int32)
+            src = np.ascontiguousarray(src, np.int32)
+            assert len(dst) == len(src)
+            pd._check(lib.pd_stepper_set_peer(s, side, o[4], 4, o[5], src.ctypes.data, dst.ctypes.data, len(src)))
+    for sh in shards:
+        pd._check(lib.pd_stepper_peer_reset(sh[2]))
+    for step in range(steps):
+        for dev, plan, s, *_ in shards:
+            pd._check(lib.pd_stepper_enqueue(s, step, plan.begin, plan.end, 1.0))
+        for sh in shards:
+            pd._check(lib.pd_stepper_swap(sh[2]))
+    for dev, plan, s, *_ in shards:
+        pd._check(lib.pd_stepper_status(s, steps))
+
+    lin_full = (keys_full[:, 2].astype(np.int64) * cc + keys_full[:, 1]) * cc + keys_full[:, 0]
+    pos = {int(l): i for i, l in enumerate(lin_full)}
+    covered = 0
+    for dev, plan, s, keys, *_ in shards:
+        u = dev.download(1)
+        for i in range(plan.begin, plan.end):
+            j = pos[(int(keys[i, 2]) * cc + int(keys[i, 1])) * cc + int(keys[i, 0])]
+            assert np.array_equal(u[i].view(np.uint64), u_full[j].view(np.uint64)), (i, keys[i])
+            covered += 1
+    assert covered == len(keys_full)
+    for dev, plan, s, *_ in shards:
+        lib.pd_stepper_destroy(s)
+        dev.close()
+    lib.pd_stepper_destroy(s_full)
+    full.close()
