@@ -429,7 +429,7 @@ __device__ __noinline__ void push_pair14(const MarchArgs& M, const ChunkCtx14& C
     if (a1) p[1] = out1;
 }
 
-template <int REACTION>
+template <int REACTION, bool PUSH>
 __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
                                           const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
                                           const LaneGeo& G, double* __restrict__ un, bool& pushed) {
@@ -498,13 +498,13 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
         out1 = r.y;
     }
     stg_pair(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, a0, a1);
-    if ((C.flags & (kFlagPushLo | kFlagPushHi)) && (z == 0 || z == 7)) {
+    if (PUSH && (C.flags & (kFlagPushLo | kFlagPushHi)) && (z == 0 || z == 7)) {
         push_pair14(M, C, z, G.bp, out0, out1, a0, a1);
         pushed = true;
     }
 }
 
-template <int REACTION>
+template <int REACTION, bool PUSH>
 __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchArgs M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SlowConsts K;
@@ -632,8 +632,8 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
             cp_wait<kAhead14>();
             __syncwarp();
             const uint32_t b = base + (uint32_t)z;
-            compute14<REACTION>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes, sb + ((b + 1u) & 7u) * kTileBytes,
-                                sb + ((b + 2u) & 7u) * kTileBytes, G, un, pushed);
+            compute14<REACTION, PUSH>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes, sb + ((b + 1u) & 7u) * kTileBytes,
+                                      sb + ((b + 2u) & 7u) * kTileBytes, G, un, pushed);
             __syncwarp();
             issue_next();
             if (z == 7) {  // plane 8 of this chunk and plane -1 of the next
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     cp_wait<0>();
     // the pushed planes are visible system-wide before this kernel completes
     // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
-    if (pushed) __threadfence_system();
+    if (PUSH && pushed) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -1695,16 +1695,19 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
         table[r10 ? 1 : 0][r]<<<sms * (r10 ? 3 : kCtas15), kThreads, bytes, g->stream>>>(M);
     } else {
         constexpr size_t bytes = (size_t)kWarpBytes14 * kWarps;
-        static const KernT table[3] = {ftcs_march14_kernel<0>, ftcs_march14_kernel<1>, ftcs_march14_kernel<2>};
+        static const KernT table[2][3] = {
+            {ftcs_march14_kernel<0, false>, ftcs_march14_kernel<1, false>, ftcs_march14_kernel<2, false>},
+            {ftcs_march14_kernel<0, true>, ftcs_march14_kernel<1, true>, ftcs_march14_kernel<2, true>}};
         static bool attr_set = false;
         if (!attr_set) {
-            for (auto k : table)
-                PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            for (auto& row : table)
+                for (auto k : row)
+                    PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
             attr_set = true;
         }
         int sms = 148;
         PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        table[r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);
+        table[pl ? 1 : 0][r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);  // [push][reaction]
     }
     PD_CUDA(cudaGetLastError());
 }
