@@ -362,7 +362,9 @@ def run_e2e(args, pack):
     active = int(host["phi"][1].size and sum(bin(int(w)).count("1") for w in masks.ravel()))
     slab = nch * 512 * 8
     return {"value": active * args.e2e_steps / secs / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": 4 * slab,
-            "d2h_bytes_per_step": 4 * slab + 40 * len(res.diagnostics),
+            # run_simulation leaves u and u_next device-newer; the reads of
+            # both pull exactly those two slabs (phi and D never change)
+            "d2h_bytes_per_step": 2 * slab + 40 * len(res.diagnostics),
             "workload": f"run_simulation on a host grid, [0,{n})^3 crop of the same geometry, "
                         f"{args.e2e_steps} steps per call (one call = one e2e step)",
             "active_nodes": active, "seconds": secs}
