@@ -13,6 +13,9 @@ import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libporediff_b200.so"
+# kernel A/B experiments load an alternative in-tree build (scripts/gpu_ab_lib.sh)
+if os.environ.get("PD_LIB_VARIANT"):
+    LIB_PATH = Path(__file__).resolve().parent / "lib" / "variants" / f"{os.environ['PD_LIB_VARIANT']}.so"
 
 PD_OK = 0
 PD_E_INPUT = 1
