@@ -135,3 +135,43 @@ def test_sub_ranges_split_boundary_layers():
     one = shard.exchange_plan(keys, 2, 3, 1, 3)  # a single owned layer
     (b0, b1), (t0, t1), (i0, i1) = shard.sub_ranges(keys, one)
     assert (b0, b1) == (6, 9) and t0 == t1 and i0 == i1
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_peer_push_pairing_maps_identical_chunks(world):
+    """Host logic of the fused exchange's pairing (shard.Domain.setup_peer):
+    rank r pushes its bottom layer into rank r-1's upper ghost layer and its
+    top layer into rank r+1's lower ghost layer, ordinal by ordinal. Every
+    pair must name the same global chunk on both sides, and every ghost chunk
+    must receive exactly one push."""
+    from paper_2304_11165_b200 import shard
+    grid, geom = _case()
+    keys = grid.keys()
+    cc = (geom.size[2] + 7) // 8
+    plans, lkeys = [], []
+    for r in range(world):
+        z0, z1 = shard.slab_bounds(cc, world, r)
+        sel = np.nonzero((keys[:, 2] >= z0 - 1) & (keys[:, 2] <= z1))[0]
+        lkeys.append(keys[sel])
+        plans.append(shard.exchange_plan(keys[sel], z0, z1, r, world))
+    for r in range(world):
+        got = {}
+        for side, nb, src in ((0, r - 1, plans[r].send_down), (1, r + 1, plans[r].send_up)):
+            if not 0 <= nb < world:
+                assert len(src) == 0
+                continue
+            dst = plans[nb].recv_up if side == 0 else plans[nb].recv_down
+            assert len(dst) == len(src)
+            for a, b in zip(src, dst):
+                assert tuple(lkeys[r][a]) == tuple(lkeys[nb][b])
+                got[(nb, int(b))] = got.get((nb, int(b)), 0) + 1
+        for (nb, b), k in got.items():
+            assert k == 1
+    for r in range(world):  # each ghost chunk is fed by exactly its owner
+        fed = set()
+        for q in (r - 1, r + 1):
+            if 0 <= q < world:
+                src = plans[q].send_up if q == r - 1 else plans[q].send_down
+                fed |= {tuple(lkeys[q][a]) for a in src}
+        ghosts = {tuple(lkeys[r][b]) for b in list(plans[r].recv_down) + list(plans[r].recv_up)}
+        assert ghosts == fed
