@@ -447,7 +447,10 @@ void launch_step(pd_stepper* s, const void* u, void* un, double factor, bool dia
         fill_args<float>(s, a, u, un, factor);
         a.k = k;
         a.ord0 = s->begin;
-        if (g->dims == 3) {
+        if (s->use_march && s->plan.ready && s->end - s->begin >= march_min_chunks()) {
+            march32_launch(g, s->plan, a, s->cfg.reaction_kind);
+            if (diag) launch_chunk_stats(g, un, g->d_masks);
+        } else if (g->dims == 3) {
             if (diag) ftcs_step_kernel<float, 3, true><<<nb, 512, 0, g->stream>>>(a);
             else ftcs_step_kernel<float, 3, false><<<nb, 512, 0, g->stream>>>(a);
         } else {
@@ -584,7 +587,7 @@ int pd_stepper_set_range(pd_stepper* s, int64_t begin, int64_t end) {
             fail(PD_E_INPUT, "stepper ordinal range outside the grid");
         s->begin = begin;
         s->end = end;
-        if (s->use_march && s->g->dims == 3 && s->g->tbytes == 8) {
+        if (s->use_march && s->g->dims == 3) {
             DeviceGuard dg(s->g->device);
             march_build_for(s, begin, end);
         }
@@ -785,7 +788,11 @@ int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t
             fill_args<float>(s, a, u, un, factor);
             a.k = 0;
             a.ord0 = begin;
-            if (g->dims == 3)
+            if (s->use_march && s->plan.ready && end - begin >= march_min_chunks()) {
+                auto& sp = march_sub(g, s->plan, begin, end);
+                PD_CUDA(cudaMemsetAsync(sp.d_counter, 0, sizeof(int), g->stream));
+                march32_launch_sched(g, s->plan, a, s->cfg.reaction_kind, sp.d_stream, sp.n, sp.d_counter);
+            } else if (g->dims == 3)
                 ftcs_step_kernel<float, 3, false><<<nb, 512, 0, g->stream>>>(a);
             else
                 ftcs_step_kernel<float, 2, false><<<nb, 64, 0, g->stream>>>(a);

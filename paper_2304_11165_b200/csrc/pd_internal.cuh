@@ -180,7 +180,7 @@ struct StepArgs {
 struct MarchPlan {
     int32_t* d_stream = nullptr;   // owned chunk ordinals in schedule order
     int32_t* d_desc = nullptr;     // 8 ints per chunk: nbr[0..5], packed key, flags
-    double* d_deff = nullptr;      // D on fluid nodes, -inf elsewhere (static per run)
+    void* d_deff = nullptr;        // D (grid scalar type) on fluid nodes, -inf elsewhere (static per run)
     int* d_counter = nullptr;      // per-step dynamic batch counters
     uint32_t* d_lm = nullptr;      // per chunk and lane: active / sink bits [c][32]
     uint32_t* d_lq = nullptr;      // per chunk and lane: quad (4-node) bits for march v15 [c][32]
@@ -206,6 +206,11 @@ struct PeerLaunch {
 void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int reaction,
                   const PeerLaunch* pl = nullptr);
 void march_push_flags(pd_grid* g, MarchPlan& p, const int32_t* d_ord);
+// 3-D FP32 grids (pd_march32.cu)
+bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void** out);
+void march32_launch(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction);
+void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction, const int32_t* sched,
+                          int64_t n, int* counter);
 int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end);
 MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end);
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,

@@ -1555,7 +1555,7 @@ int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end) {
 void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, const uint64_t* d_sink,
                  const void* d_dcol, int dirichlet, int64_t begin, int64_t end, MarchPlan* plan) {
     march_free(plan);
-    if (g->dims != 3 || g->tbytes != 8) return;
+    if (g->dims != 3) return;
     if (g->cc[0] > 1024 || g->cc[1] > 1024 || g->cc[2] > 1024) return;  // key packing limit
     const int64_t n_all = g->n_chunks;
     if (n_all == 0 || end <= begin) return;
@@ -1566,7 +1566,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     PD_CUDA(cudaGetLastError());
     PD_CUDA(pd_malloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
     const char* ver_env = getenv("PD_MARCH_V");
-    const int ver = ver_env ? atoi(ver_env) : 14;
+    const int ver = g->tbytes == 4 ? 14 : (ver_env ? atoi(ver_env) : 14);  // FP32: pd_march32.cu
     if (ver == 15 || ver == 16) {  // quad lane masks
         PD_CUDA(pd_malloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
         lanemask15_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
@@ -1580,26 +1580,34 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
                                                                                 n_all, plan->d_lm);
     PD_CUDA(cudaGetLastError());
     const int64_t slots = n_all * 512;
-    // one extra chunk of sentinels after the last one: the source of every
-    // D_eff cell a plane load does not read from the grid (inactive pairs,
-    // missing neighbours), so the loads need no shared-memory sentinel stores
-    PD_CUDA(pd_malloc(&plan->d_deff, sizeof(double) * (size_t)(slots + 512)));
-    PD_CUDA(cudaMemsetAsync(plan->d_deff + slots, 0, sizeof(double) * 512, g->stream));
-    sentinel_fill_kernel<<<1, 512, 0, g->stream>>>(plan->d_deff + slots);
     PD_CUDA(pd_malloc(&plan->d_counter, sizeof(int) * 1024));
-    unsigned long long* d_bad = nullptr;
-    PD_CUDA(pd_malloc(&d_bad, sizeof(unsigned long long)));
-    PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
-    deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>(
-        (const double*)d_dcol, d_fluid, slots, plan->d_deff, d_bad);
-    PD_CUDA(cudaGetLastError());
-    unsigned long long bad = 0;
-    PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
-    PD_CUDA(cudaStreamSynchronize(g->stream));
-    pd_free(d_bad);
-    if (bad) {  // non-finite D on a fluid node: keep the exact tile kernel
-        march_free(plan);
-        return;
+    if (g->tbytes == 4) {
+        if (!march32_deff(g, d_dcol, d_fluid, &plan->d_deff)) {
+            march_free(plan);  // non-finite D on a fluid node: keep the exact tile kernel
+            return;
+        }
+    } else {
+        // one extra chunk of sentinels after the last one: the source of every
+        // D_eff cell a plane load does not read from the grid (inactive pairs,
+        // missing neighbours), so the loads need no shared-memory sentinel stores
+        double* deff = nullptr;
+        PD_CUDA(pd_malloc(&deff, sizeof(double) * (size_t)(slots + 512)));
+        plan->d_deff = deff;
+        sentinel_fill_kernel<<<1, 512, 0, g->stream>>>(deff + slots);
+        unsigned long long* d_bad = nullptr;
+        PD_CUDA(pd_malloc(&d_bad, sizeof(unsigned long long)));
+        PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
+        deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>((const double*)d_dcol, d_fluid, slots,
+                                                                            deff, d_bad);
+        PD_CUDA(cudaGetLastError());
+        unsigned long long bad = 0;
+        PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        pd_free(d_bad);
+        if (bad) {  // non-finite D on a fluid node: keep the exact tile kernel
+            march_free(plan);
+            return;
+        }
     }
     const int64_t n = end - begin;
     plan->d_stream = march_schedule(g, begin, end);
@@ -1642,7 +1650,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.desc = p.d_desc;
     M.lm = p.d_lm;
     M.lq = p.d_lq;
-    M.deff = p.d_deff;
+    M.deff = static_cast<const double*>(p.d_deff);
     M.counter = counter;
     static const int dbg = [] {
         const char* e = getenv("PD_MARCH_DBG");

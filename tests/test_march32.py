@@ -1,0 +1,89 @@
+"""The FP32 march kernel (pd_march32.cu; the reference's T = float path,
+solver.hpp:385-455 in float) against the reference run in-process on the same
+inputs: u, u_next and every diagnostics row bit for bit, on grids with many
+chunks per warp — sink band, volumetric source with a time factor, walls,
+Dirichlet faces — and the non-finite error path (message and post-error
+state). conftest.py sets PD_MARCH_MIN_CHUNKS=0, so every 3-D FP32 step here
+runs the march kernel."""
+import numpy as np
+import pytest
+
+import cases
+from cases import dt_of, oracle_config, sim_config, time_factor
+
+pytestmark = pytest.mark.gpu
+
+SPECS = {
+    "pack61_fp32_vol": dict(dims=3, n=61, box=(0.0, 1.0), geom="pack", pack=(40, 0.06, 0.14, 91),
+                            channels=["phi", "u", "D", "u_next", "f"], profile=(0.05, 1.0, 0.0, 60.0),
+                            u0=("hash_unit", 4), fp32=True, reaction=("volumetric", "f", "exp"), dt_frac=0.45,
+                            steps=40, record=8),
+    "pack56_fp32_walls": dict(dims=3, n=56, box=(0.0, 1.0), geom="pack", pack=(30, 0.07, 0.15, 12),
+                              channels=["phi", "u", "D", "u_next"], profile=("anchored", 0.05, 0.95, 200.0, 0.02),
+                              u0=("hash_unit", 6), fp32=True, eps=0.5 / 56, reaction=("surface_sink", 2.0, 1.0),
+                              dirichlet={0: 1.0, 5: 0.25}, dt_frac=0.45, steps=60, record=60),
+}
+
+
+@pytest.fixture
+def spec_cases(monkeypatch):
+    for k, v in SPECS.items():
+        monkeypatch.setitem(cases.CASES, k, v)
+    return cases.CASES
+
+
+def _compare(ours, g, res, rows):
+    assert [tuple(r) for r in rows] == [(d.step, d.time, d.total_mass, d.min_u, d.max_u) for d in res.diagnostics]
+    for c in ("u", "u_next"):
+        a, b = ours.channel_data(c), g.prop(c)
+        assert a.dtype == np.float32
+        diff = np.nonzero(a.view(np.uint32) != b.view(np.uint32))
+        assert diff[0].size == 0, (c, diff[0][:5], diff[1][:5], a[diff][:5], b[diff][:5])
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_fp32_march_equals_reference(name, spec_cases, ref, cuda):
+    from paper_2304_11165_b200 import porediff as pd
+    spec = spec_cases[name]
+    g = cases.ref_case(name, ref)
+    keys, masks = g.layout()
+    assert len(keys) > 200  # many chunks per launch
+    data = {c: g.prop(c) for c in spec["channels"]}
+    dt = dt_of(spec, g.max_diffusivity())
+    geom = pd.GridGeometry.cell_centered_box(spec["n"], *spec["box"], spec["dims"])
+    ours = pd.SparseBlockGrid.from_layout(geom, spec["channels"], keys, masks, data, np.float32)
+    code, msg, rows = g.run(oracle_config(spec, dt), time_factor(spec))
+    assert code == 0, msg
+    res = pd.run_simulation(ours, sim_config(spec, dt))
+    _compare(ours, g, res, rows)
+
+
+def test_fp32_march_nonfinite_error_and_state(spec_cases, ref, cuda):
+    """An overflow mid-run: same numeric_error text (first step, lowest
+    ordinal node) and the same post-error u / u_next as the reference."""
+    from paper_2304_11165_b200 import porediff as pd
+    name = "pack56_fp32_walls"
+    spec = dict(spec_cases[name])
+    g = cases.ref_case(name, ref)
+    keys, masks = g.layout()
+    u = g.prop("u")
+    act = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).astype(bool)
+    j, off = [int(v[len(v) // 2]) for v in np.nonzero(act)]
+    u[j, off] = np.float32(3e38)
+    g.set_prop("u", u)
+    data = {c: g.prop(c) for c in spec["channels"]}
+    dt = 3.0 * dt_of(spec, g.max_diffusivity())
+    spec["steps"] = 30
+    ocfg = oracle_config(spec, dt)
+    ocfg.enforce_stability = 0
+    code, msg, _ = g.run(ocfg, None)
+    assert code == 6, msg
+    geom = pd.GridGeometry.cell_centered_box(spec["n"], *spec["box"], spec["dims"])
+    ours = pd.SparseBlockGrid.from_layout(geom, spec["channels"], keys, masks, data, np.float32)
+    cfg = sim_config(spec, dt)
+    cfg.enforce_stability = False
+    with pytest.raises(pd.NumericError) as ei:
+        pd.run_simulation(ours, cfg)
+    assert str(ei.value) == msg
+    for c in ("u", "u_next"):
+        assert np.array_equal(ours.channel_data(c).view(np.uint32), g.prop(c).view(np.uint32)), c
