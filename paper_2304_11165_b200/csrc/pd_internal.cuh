@@ -183,7 +183,6 @@ struct MarchPlan {
     void* d_deff = nullptr;        // D (grid scalar type) on fluid nodes, -inf elsewhere (static per run)
     int* d_counter = nullptr;      // per-step dynamic batch counters
     uint32_t* d_lm = nullptr;      // per chunk and lane: active / sink bits [c][32]
-    uint32_t* d_lq = nullptr;      // per chunk and lane: quad (4-node) bits for march v15 [c][32]
     int grid = 0;
     int64_t n = 0;
     bool ready = false;

@@ -33,10 +33,8 @@
 //   schedule id -> lane masks/descriptor pipeline runs ahead through a
 //   per-warp context ring in shared memory.
 //
-// ftcs_march15_kernel<R, 1> ("v16", PD_MARCH_V=16): four nodes per lane (two
-// planes per warp iteration), ten fixed slots, 12 warps per SM, swizzled
-// tile rows. 19 % fewer instructions than v14 but not faster yet (see
-// DESIGN.md); kept for the next round's tuning.
+// Earlier layouts (four nodes per lane "v15/v16", a whole x-row per lane
+// "v17") were measured and retired; see DESIGN.md section 4 and commit d37e7fc.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -72,10 +70,8 @@ struct MarchArgs {
     int64_t n;
     const int32_t* __restrict__ desc;  // 8 ints per chunk: nbr[6], key, flags
     const uint32_t* __restrict__ lm;   // per chunk and lane: active / sink bits
-    const uint32_t* __restrict__ lq;   // per chunk and lane: v15 compute-side quad bits
     const double* __restrict__ deff;
     int* counter;                    // chunk-claim counter of this step
-    int static_sched;                // 1: static interleaved positions (no atomics)
     int zero;                        // 0 (opaque to the compiler)
     int64_t n_all;                   // chunks of the grid (D_eff sentinel chunk follows them)
     int dbg;                         // measurement-only halo skip mask (PD_MARCH_DBG)
@@ -155,28 +151,6 @@ constexpr uint32_t kDOff = (uint32_t)offsetof(Tile, d);        // u -> D_eff dis
 constexpr uint32_t kHxOff = (uint32_t)offsetof(Tile, hxu);     // x-halo column (bytes)
 
 // ---- predicated asynchronous copies (LDGSTS), one predicate per pair ----
-__device__ __forceinline__ void cp16x2(uint32_t su, const double* gu, uint32_t sd, const double* gd,
-                                       bool pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " @p cp.async.cg.shared.global [%0], [%1], 16;\n"
-        " @p cp.async.cg.shared.global [%2], [%3], 16;\n}\n" ::"r"(su),
-        "l"(gu), "r"(sd), "l"(gd), "r"((int)pred));
-}
-__device__ __forceinline__ void cp8x2(uint32_t su, const double* gu, uint32_t sd, const double* gd,
-                                      bool pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " @p cp.async.ca.shared.global [%0], [%1], 8;\n"
-        " @p cp.async.ca.shared.global [%2], [%3], 8;\n}\n" ::"r"(su),
-        "l"(gu), "r"(sd), "l"(gd), "r"((int)pred));
-}
-__device__ __forceinline__ void sts_sent1(uint32_t sa, bool pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n"
-        " @p st.shared.v2.u32 [%0], {%2, %3};\n}\n" ::"r"(sa),
-        "r"((int)pred), "r"(0u), "r"(kSentHi));
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -650,760 +624,6 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     if (PUSH && pushed) __threadfence_system();
 }
 
-// ---------------------------------------------------------------------------
-// v15: four nodes per lane. The load side is v14's (each lane copies its
-// 16-B pair of u and D_eff per plane into the 8-slot ring, face lanes the
-// halo cells), but the compute side gives every lane a row segment of four
-// nodes: lanes 0-15 compute plane 2*it and lanes 16-31 plane 2*it+1 of the
-// same chunk, (y, xq) = ((lane & 15) >> 1, lane & 1), nodes x = 4*xq .. +3.
-// Per-lane fixed costs (slot addresses, predicates, the rare-path test, the
-// loop) are paid once per four nodes, x faces between the four nodes come
-// from registers, and a chunk takes four iterations instead of eight.
-// Ring discipline (one commit group per plane load, load i of chunk k at
-// index 10k+i): before iteration it the loads up to 10k+2it+3 must be done
-// and exactly four newer ones are in flight (wait_group 4); after it the
-// slots of planes 2it-1 and 2it are free, so loads 10k+2it+8 and 10k+2it+9
-// are issued (it = 3: also 10k+16 and 10k+17, the next chunk's planes).
-// ---------------------------------------------------------------------------
-constexpr int kCtas15 = 4;
-constexpr int kAhead15 = 4;
-constexpr uint32_t kCtxLq = 128;    // ctx entry: lm[32] | lq[32] | desc[8] | id
-constexpr uint32_t kCtxDesc = 256;
-constexpr uint32_t kCtxId = 288;
-constexpr uint32_t kCtxBytes15 = 304;
-constexpr uint32_t kWarpBytes15 = kRing14 * kTileBytes + 3 * kCtxBytes15;
-
-// v15 tile rows are swizzled at 16-B granularity: logical granule g of tile
-// row R (R = y + 1, rows -1..8) sits at physical granule g ^ ((R >> 1) & 1).
-// A quad lane reads 16 B at a 32-B stride within a row; the swizzle makes the
-// eight lanes of every LDS.128 phase (four rows, two lanes each) hit eight
-// distinct 16-B bank groups. Pair loads (v14 lanes) stay conflict-free: a
-// row's granules are only permuted.
-__device__ __forceinline__ uint32_t swz(int R, int x) {  // byte offset of node x of tile row R
-    return 64u * (uint32_t)R + 16u * (uint32_t)((x >> 1) ^ ((R >> 1) & 1)) + 8u * (uint32_t)(x & 1);
-}
-
-__device__ __forceinline__ LaneGeo lane_geo_swz(int lane) {
-    LaneGeo G = lane_geo(lane);
-    const int x0 = 2 * G.xp;
-    G.s_c = swz(G.y + 1, x0);
-    G.s_hy = G.y == 0 ? swz(0, x0) : swz(9, x0);
-    return G;
-}
-
-struct QuadGeo {
-    int h, y, xq;
-    uint32_t cA;  // nodes x0, x0+1 of row y (x0+2, x0+3: cA ^ 16, the neighbouring granule)
-    uint32_t mA;  // same columns, row y-1
-    uint32_t pA;  // same columns, row y+1
-    uint32_t s_l, s_r;  // left / right neighbour cells
-    uint32_t bq;        // element offset of node x0 in a plane
-};
-
-__device__ __forceinline__ QuadGeo quad_geo(int lane) {
-    QuadGeo Q;
-    Q.h = lane >> 4;
-    const int r = lane & 15;
-    Q.y = r >> 1;
-    Q.xq = r & 1;
-    const int x0 = 4 * Q.xq, R = Q.y + 1;
-    Q.cA = swz(R, x0);
-    Q.mA = swz(R - 1, x0);
-    Q.pA = swz(R + 1, x0);
-    Q.s_l = Q.xq == 0 ? kHxOff + (uint32_t)Q.y * 8u : swz(R, x0 - 1);
-    Q.s_r = Q.xq == 1 ? kHxOff + (uint32_t)(8 + Q.y) * 8u : swz(R, x0 + 4);
-    Q.bq = (uint32_t)(Q.y * 8 + x0);
-    return Q;
-}
-
-struct ChunkCtx15 {
-    int c, key, flags;
-    uint32_t lq;  // compute-side bits: 4*it+i active, 16+4*it+i sink
-};
-
-// Per chunk and lane: compute-side bits of the lane's quad in planes 2*it+h.
-__global__ void lanemask15_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ snk, int64_t n,
-                                  uint32_t* __restrict__ lq) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n * 32) return;
-    const int64_t c = t >> 5;
-    const int lane = (int)(t & 31);
-    const int h = lane >> 4, r = lane & 15;
-    const int bq = (r >> 1) * 8 + 4 * (r & 1);
-    uint32_t v = 0;
-    for (int it = 0; it < 4; ++it) {
-        const int z = 2 * it + h;
-        v |= (uint32_t)((act[c * 8 + z] >> bq) & 15ull) << (4 * it);
-        v |= (uint32_t)((snk[c * 8 + z] >> bq) & 15ull) << (16 + 4 * it);
-    }
-    lq[t] = v;
-}
-
-// Rare path of one quad (a Dirichlet-exposed chunk, or a huge / non-finite
-// fast result): exact generic update per node on operands re-read from the
-// ring, then the reference's non-finite / total-mass flags.
-template <int REACTION>
-__device__ __noinline__ double4 quad_slow(unsigned long long* bad_key, int* flagp, const SlowConsts& K,
-                                          const double* __restrict__ src, int c, int key, int cflags,
-                                          uint32_t bits, int z, uint32_t tm, uint32_t t0, uint32_t tp, QuadGeo G,
-                                          double4 o) {
-    double out[4] = {o.x, o.y, o.z, o.w};
-    double u[6], d[6];  // x0-1 .. x0+4
-    const int R = G.y + 1;
-    u[0] = lds1(t0 + G.s_l);
-    d[0] = lds1(t0 + kDOff + G.s_l);
-    u[5] = lds1(t0 + G.s_r);
-    d[5] = lds1(t0 + kDOff + G.s_r);
-    for (int i = 0; i < 4; ++i) {
-        u[i + 1] = lds1(t0 + swz(R, 4 * G.xq + i));
-        d[i + 1] = lds1(t0 + kDOff + swz(R, 4 * G.xq + i));
-    }
-    const bool dirichlet = (cflags & kFlagDirichlet) != 0;
-    const int kx = key & 1023, ky = (key >> 10) & 1023, kz = (key >> 20) & 1023;
-    const int x0 = 4 * G.xq;
-    bool h[4], any = false;
-    for (int i = 0; i < 4; ++i) {
-        const bool a = (bits >> i) & 1u;
-        const double uc = u[i + 1], dc = d[i + 1];
-        const int x = 4 * G.xq + i;
-        const uint32_t e = swz(R, x), em = swz(R - 1, x), ep = swz(R + 1, x);
-        const double nu[6] = {u[i], u[i + 2], lds1(t0 + em), lds1(t0 + ep), lds1(tm + e), lds1(tp + e)};
-        const double nd[6] = {d[i], d[i + 2], lds1(t0 + kDOff + em), lds1(t0 + kDOff + ep),
-                              lds1(tm + kDOff + e), lds1(tp + kDOff + e)};
-        const bool s = REACTION == PD_REACTION_SURFACE_SINK && ((bits >> (16 + i)) & 1u);
-        const double sv = REACTION == PD_REACTION_VOLUMETRIC ? src[(int64_t)c * 512 + z * 64 + G.bq + i] : 0.0;
-        const int64_t gx = (int64_t)kx * 8 + x0 + i, gy = (int64_t)ky * 8 + G.y, gz = (int64_t)kz * 8 + z;
-        if (dirichlet) {
-            if (!sentinel(dc)) out[i] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
-            h[i] = a && huge(out[i]);
-        } else {
-            h[i] = a && huge(out[i]);
-            if (h[i] && !isfinite(out[i]) && !sentinel(dc))
-                out[i] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
-        }
-        any = any || h[i];
-    }
-    if (any) {
-        int first = -1;
-        for (int i = 3; i >= 0; --i)
-            if (((bits >> i) & 1u) && !isfinite(out[i])) first = i;
-        if (first >= 0) {
-            const int off = z * 64 + (int)G.bq + first;
-            atomicMin(bad_key, ((unsigned long long)c << 10) | (unsigned long long)off);
-            atomicOr(flagp, 1);
-        } else {
-            atomicOr(flagp, 2);
-        }
-    }
-    return make_double4(out[0], out[1], out[2], out[3]);
-}
-
-template <int REACTION, int R10>
-__device__ __forceinline__ void compute15(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
-                                          const ChunkCtx15& C, int it, uint32_t sb, uint32_t base, const QuadGeo& G,
-                                          double* __restrict__ un) {
-    const int z = 2 * it + G.h;
-    // 8-slot continuous ring, or (R10) 10 fixed slots: plane p of every chunk in slot p + 1
-    const uint32_t b = R10 ? (uint32_t)z : base + (uint32_t)z;
-    const uint32_t tm = sb + (R10 ? b : (b & 7u)) * kTileBytes;
-    const uint32_t t0 = sb + (R10 ? b + 1u : ((b + 1u) & 7u)) * kTileBytes;
-    const uint32_t tp = sb + (R10 ? b + 2u : ((b + 2u) & 7u)) * kTileBytes;
-    const uint32_t bits = (C.lq >> (4 * it)) & 0x000F000Fu;
-    const bool interior = ((C.flags >> (8 + 2 * it)) & 3) == 3;  // both planes of the pair (warp-uniform)
-    const double2 ua = lds2(t0 + G.cA), ub = lds2(t0 + (G.cA ^ 16u));
-    const double2 da = lds2(t0 + kDOff + G.cA), db = lds2(t0 + kDOff + (G.cA ^ 16u));
-    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
-    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
-    const double u0 = ua.x, u1 = ua.y, u2 = ub.x, u3 = ub.y;
-    const double d0 = da.x, d1 = da.y, d2 = db.x, d3 = db.y;
-    double l0, l1, l2, l3;  // lap starts at T{0} (solver.hpp:420): lap = 0.0 + x term
-    {
-        double fL, f01, f12, f23, fR;
-        if (interior) {
-            fL = fface(dL, d0, uL, u0);
-            f01 = fface(d0, d1, u0, u1);
-            f12 = fface(d1, d2, u1, u2);
-            f23 = fface(d2, d3, u2, u3);
-            fR = fface(d3, dR, u3, uR);
-        } else {
-            fL = face(dL, d0, uL, u0);
-            f01 = face(d0, d1, u0, u1);
-            f12 = face(d1, d2, u1, u2);
-            f23 = face(d2, d3, u2, u3);
-            fR = face(d3, dR, u3, uR);
-        }
-        l0 = 0.0 + (f01 - fL) * Q.ix;
-        l1 = 0.0 + (f12 - f01) * Q.ix;
-        l2 = 0.0 + (f23 - f12) * Q.ix;
-        l3 = 0.0 + (fR - f23) * Q.ix;
-    }
-    // y then z (solver.hpp:421-433: axes in order)
-#pragma unroll
-    for (int ax = 0; ax < 2; ++ax) {
-        const uint32_t oM = ax == 0 ? G.mA : G.cA, oP = ax == 0 ? G.pA : G.cA;
-        const uint32_t amA = (ax == 0 ? t0 : tm) + oM, amB = (ax == 0 ? t0 : tm) + (oM ^ 16u);
-        const uint32_t apA = (ax == 0 ? t0 : tp) + oP, apB = (ax == 0 ? t0 : tp) + (oP ^ 16u);
-        const double w = ax == 0 ? Q.iy : Q.iz;
-        const double2 uma = lds2(amA), umb = lds2(amB), dma = lds2(amA + kDOff), dmb = lds2(amB + kDOff);
-        const double2 upa = lds2(apA), upb = lds2(apB), dpa = lds2(apA + kDOff), dpb = lds2(apB + kDOff);
-        double m0, m1, m2, m3, p0, p1, p2, p3;
-        if (interior) {
-            m0 = fface(dma.x, d0, uma.x, u0);
-            m1 = fface(dma.y, d1, uma.y, u1);
-            m2 = fface(dmb.x, d2, umb.x, u2);
-            m3 = fface(dmb.y, d3, umb.y, u3);
-            p0 = fface(d0, dpa.x, u0, upa.x);
-            p1 = fface(d1, dpa.y, u1, upa.y);
-            p2 = fface(d2, dpb.x, u2, upb.x);
-            p3 = fface(d3, dpb.y, u3, upb.y);
-        } else {
-            m0 = face(dma.x, d0, uma.x, u0);
-            m1 = face(dma.y, d1, uma.y, u1);
-            m2 = face(dmb.x, d2, umb.x, u2);
-            m3 = face(dmb.y, d3, umb.y, u3);
-            p0 = face(d0, dpa.x, u0, upa.x);
-            p1 = face(d1, dpa.y, u1, upa.y);
-            p2 = face(d2, dpb.x, u2, upb.x);
-            p3 = face(d3, dpb.y, u3, upb.y);
-        }
-        l0 += (p0 - m0) * w;
-        l1 += (p1 - m1) * w;
-        l2 += (p2 - m2) * w;
-        l3 += (p3 - m3) * w;
-    }
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-    if (REACTION == PD_REACTION_SURFACE_SINK) {
-        r0 = ((bits >> 16) & 1u) ? Q.neg_k * u0 : 0.0;
-        r1 = ((bits >> 17) & 1u) ? Q.neg_k * u1 : 0.0;
-        r2 = ((bits >> 18) & 1u) ? Q.neg_k * u2 : 0.0;
-        r3 = ((bits >> 19) & 1u) ? Q.neg_k * u3 : 0.0;
-    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-        const double* sp = M.A.src + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bq);
-        r0 = sp[0] * Q.src_factor;
-        r1 = sp[1] * Q.src_factor;
-        r2 = sp[2] * Q.src_factor;
-        r3 = sp[3] * Q.src_factor;
-    }
-    double o0 = u0 + Q.dt * l0 + Q.dt * r0;
-    double o1 = u1 + Q.dt * l1 + Q.dt * r1;
-    double o2 = u2 + Q.dt * l2 + Q.dt * r2;
-    double o3 = u3 + Q.dt * l3 + Q.dt * r3;
-    if (!interior) {  // walls stay frozen (solver.hpp:413-417)
-        if (sentinel(d0)) o0 = u0;
-        if (sentinel(d1)) o1 = u1;
-        if (sentinel(d2)) o2 = u2;
-        if (sentinel(d3)) o3 = u3;
-    }
-    const bool a0 = bits & 1u, a1 = (bits >> 1) & 1u, a2 = (bits >> 2) & 1u, a3 = (bits >> 3) & 1u;
-    const bool hot = (a0 && huge(o0)) | (a1 && huge(o1)) | (a2 && huge(o2)) | (a3 && huge(o3));
-    if ((C.flags & kFlagDirichlet) || hot) {
-        const double4 r = quad_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, M.A.src, C.c, C.key, C.flags, bits,
-                                              z, tm, t0, tp, G, make_double4(o0, o1, o2, o3));
-        o0 = r.x;
-        o1 = r.y;
-        o2 = r.z;
-        o3 = r.w;
-    }
-    double* dst = un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bq);
-    stg_pair(dst, o0, o1, a0, a1);
-    stg_pair(dst + 2, o2, o3, a2, a3);
-}
-
-// R10 = 1 (v16): ten fixed slots per warp (plane p of every chunk in slot
-// p + 1), 12 warps per SM; the next chunk's loads i, i+1 go out as soon as
-// slots i, i+1 are consumed, which keeps six loads in flight (wait_group 6).
-template <int REACTION, int R10>
-__global__ void __launch_bounds__(kThreads, R10 ? 3 : kCtas15) ftcs_march15_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ SlowConsts K;
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const StepArgs<double>& A = M.A;
-    if (A.k > 0) {
-        const int prev = A.flags[A.k - 1];
-        if (prev) {
-            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
-            return;
-        }
-    }
-    if (t == 0) {
-        for (int a = 0; a < 3; ++a) {
-            K.size[a] = A.size[a];
-            K.inv_dx2[a] = A.inv_dx2[a];
-        }
-        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
-        K.dt = A.dt;
-        K.neg_k = A.neg_k;
-        K.src_factor = A.src_factor;
-        K.dirichlet = A.dirichlet;
-    }
-    __syncthreads();
-    Consts Q;
-    Q.dt = A.dt;
-    Q.neg_k = A.neg_k;
-    Q.src_factor = A.src_factor;
-    Q.ix = A.inv_dx2[0];
-    Q.iy = A.inv_dx2[1];
-    Q.iz = A.inv_dx2[2];
-    const LaneGeo G = lane_geo_swz(lane);
-    const QuadGeo GQ = quad_geo(lane);
-    constexpr int kSlotsQ = R10 ? 10 : kRing14;
-    constexpr uint32_t kWarpBytesQ = kSlotsQ * kTileBytes + 3 * kCtxBytes15;
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytesQ;
-    const double* __restrict__ u = A.u;
-    const double* __restrict__ de = M.deff;
-    double* __restrict__ un = A.un;
-    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
-
-    // chunk pipeline as in ftcs_march14_kernel (context ring in shared memory)
-    int* ctr_l = M.counter + ((t >> 5) & M.zero);
-    const int n = (int)M.n;
-    const uint32_t cb = sb + kSlotsQ * kTileBytes;
-    auto cent = [&](int e) -> uint32_t { return cb + (uint32_t)e * kCtxBytes15; };
-    int raw = 0;
-    auto claim_issue = [&]() {
-        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(raw) : "l"(ctr_l) : "memory");
-    };
-    auto sched_sync = [&]() -> int {
-        claim_issue();
-        const int p = __shfl_sync(0xffffffffu, raw, 0);
-        return p < n ? __ldg(&M.sched[p]) : -1;
-    };
-    auto fetch_ctx = [&](uint32_t e, int c) {
-        const int64_t cc = c < 0 ? 0 : c;
-        cp4(e + 4u * (uint32_t)lane, M.lm + cc * 32 + lane, c >= 0);
-        cp4(e + kCtxLq + 4u * (uint32_t)lane, M.lq + cc * 32 + lane, c >= 0);
-        cp4(e + kCtxDesc + 4u * (uint32_t)(lane & 7), M.desc + cc * 8 + (lane & 7), c >= 0 && lane < 8);
-    };
-    {
-        const int id0 = sched_sync();
-        if (id0 < 0) return;
-        const int id1 = sched_sync();
-        if (lane == 0) {
-            sts_u32(cent(0) + kCtxId, (uint32_t)id0);
-            sts_u32(cent(1) + kCtxId, (uint32_t)id1);
-        }
-        fetch_ctx(cent(0), id0);
-        cp_commit();
-        cp_wait<0>();
-        __syncwarp();
-        claim_issue();
-    }
-    int ek = 0;
-    ChunkCtx15 Cld, Cprev;
-    LoadCtx14 Lld;
-    auto advance = [&]() {
-        Cprev = Cld;  // R10: the chunk whose planes the slots now hold completely
-        const uint32_t e0 = cent(ek);
-        const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
-        const uint32_t e1 = cent(e1i), e2 = cent(e2i);
-        const int c = (int)lds_u32(e0 + kCtxId);
-        const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
-        const uint32_t lq = c >= 0 ? lds_u32(e0 + kCtxLq + 4u * (uint32_t)lane) : 0u;
-        const int dv = (int)lds_u32(e0 + kCtxDesc + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
-        Cld = ChunkCtx15{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lq};
-        Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
-        const int c1 = (int)lds_u32(e1 + kCtxId);
-        fetch_ctx(e1, c1);
-        if (lane == 0) {
-            const bool ok = raw < n;
-            cp4(e2 + kCtxId, M.sched + (ok ? raw : 0), ok);
-            if (!ok) sts_u32(e2 + kCtxId, 0xFFFFFFFFu);
-        }
-        claim_issue();
-        ek = e1i;
-    };
-    advance();
-    // the first advance's copies (chunk 1's context, chunk 2's id) must land
-    // before the prologue's tenth load advances onto chunk 1 (R10)
-    cp_commit();
-    cp_wait<0>();
-    __syncwarp();
-    int p_ld = 0;
-    uint32_t Lc = 0;
-    auto issue_next = [&]() {
-        const uint32_t slot = R10 ? (uint32_t)p_ld : (Lc & (kRing14 - 1));
-        issue14(sb + slot * kTileBytes, u, de, Lld, p_ld, G, sent_off);
-        if (++p_ld == 10) {
-            p_ld = 0;
-            advance();
-        }
-        cp_commit();
-        ++Lc;
-    };
-    ChunkCtx15 Cc = Cld;  // before the prologue: with R10 its tenth load advances the load side
-    uint32_t base = 0;
-#pragma unroll 1
-    for (int k = 0; k < (R10 ? 10 : 4 + kAhead15); ++k) issue_next();
-#pragma unroll 1
-    while (Cc.c >= 0) {
-#pragma unroll 1
-        for (int it = 0; it < 4; ++it) {
-            cp_wait<R10 ? 6 : kAhead15>();
-            __syncwarp();
-            compute15<REACTION, R10>(M, K, Q, Cc, it, sb, base, GQ, un);
-            __syncwarp();
-            issue_next();
-            issue_next();
-            if (it == 3) {
-                issue_next();
-                issue_next();
-            }
-        }
-        base += 10u;
-        // the load side is one chunk ahead with the 8-slot ring, two with R10
-        // (its tenth load of the next chunk already advanced it)
-        Cc = R10 ? Cprev : Cld;
-    }
-    cp_wait<0>();
-}
-
-// ---------------------------------------------------------------------------
-// v17 "row march": every lane computes a whole x-row (8 nodes) of one plane —
-// lane (y, zq) = (lane & 7, lane >> 3) takes row y of plane 4*it + zq, so a
-// warp covers half a chunk per iteration. x faces come from registers; the
-// y / z neighbour rows are read as four 16-B granules per array. Tile rows
-// have an 80-B pitch (8 doubles + the row's two x-halo cells), which makes the
-// eight lanes of every LDS.128 phase (eight rows, same granule) hit eight
-// distinct 16-B bank groups. Continuous 16-slot ring per warp (slot = load
-// index & 15), 8 warps per SM; loads run 1-1.5 iterations ahead.
-// ---------------------------------------------------------------------------
-constexpr int kRing17 = 16;
-constexpr int kCtas17 = 2;
-constexpr uint32_t kRow17 = 80;                    // row pitch (bytes)
-constexpr uint32_t kArr17 = 10 * kRow17;           // one array (rows -1..8)
-constexpr uint32_t kTile17 = 2 * kArr17;           // u then D_eff
-constexpr uint32_t kWarpBytes17 = kRing17 * kTile17 + 3 * kCtxBytes15;
-
-__device__ __forceinline__ LaneGeo lane_geo17(int lane) {  // load side in the v17 tile layout
-    LaneGeo G = lane_geo(lane);
-    const uint32_t R = (uint32_t)G.y + 1;
-    G.s_c = kRow17 * R + 16u * (uint32_t)G.xp;
-    G.s_hx = kRow17 * R + 64u + (G.xp == 3 ? 8u : 0u);
-    G.s_hy = (G.y == 0 ? 0u : 9u * kRow17) + 16u * (uint32_t)G.xp;
-    return G;
-}
-
-__device__ __forceinline__ void issue17(uint32_t st, const double* __restrict__ u, const double* __restrict__ de,
-                                        const LoadCtx14& L, int i, const LaneGeo& G, uint32_t sent_off) {
-    if (i == 0 || i == 9) {
-        const bool ok = i == 0 ? L.zlok : L.zhok;
-        const uint32_t o = i == 0 ? L.zl : L.zh;
-        cp16_ud(st + G.s_c, u + o, ok, st + kArr17 + G.s_c, de + (ok ? o : sent_off + G.bp), true);
-        return;
-    }
-    const uint32_t p64 = (uint32_t)(i - 1) * 64u;
-    const bool ok = ((L.lm >> (2 * (i - 1))) & 3u) != 0u;
-    const uint32_t o = L.own + p64;
-    cp16_ud(st + G.s_c, u + o, ok, st + kArr17 + G.s_c, de + (ok ? o : sent_off + G.bp + p64), true);
-    const uint32_t ox = L.xo + p64;
-    cp8_ud(st + G.s_hx, u + ox, L.xok, st + kArr17 + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64), G.xface);
-    const uint32_t oy = L.yo + p64;
-    cp16_ud(st + G.s_hy, u + oy, L.yok, st + kArr17 + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64), G.yface);
-}
-
-struct ChunkCtx17 {
-    int c, key, flags;
-    uint32_t lr;  // bit 8*it + x: node x of the lane's row in plane 4*it + zq active; +16: sink
-};
-
-__global__ void lanemask17_kernel(const uint64_t* __restrict__ act, const uint64_t* __restrict__ snk, int64_t n,
-                                  uint32_t* __restrict__ lr) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n * 32) return;
-    const int64_t c = t >> 5;
-    const int lane = (int)(t & 31);
-    const int y = lane & 7, zq = lane >> 3;
-    uint32_t v = 0;
-    for (int it = 0; it < 2; ++it) {
-        const int z = 4 * it + zq;
-        v |= (uint32_t)((act[c * 8 + z] >> (8 * y)) & 0xFFull) << (8 * it);
-        v |= (uint32_t)((snk[c * 8 + z] >> (8 * y)) & 0xFFull) << (16 + 8 * it);
-    }
-    lr[t] = v;
-}
-
-// Rare path of one row: exact generic update per node from the ring.
-template <int REACTION>
-__device__ __noinline__ void row_slow(unsigned long long* bad_key, int* flagp, const SlowConsts& K,
-                                      const double* __restrict__ src, int c, int key, int cflags, uint32_t bits, int z,
-                                      int y, uint32_t tm, uint32_t t0, uint32_t tp, double* out) {
-    const uint32_t o = kRow17 * (uint32_t)(y + 1);
-    double u[10], d[10];  // x = -1..8
-    u[0] = lds1(t0 + o + 64);
-    d[0] = lds1(t0 + kArr17 + o + 64);
-    u[9] = lds1(t0 + o + 72);
-    d[9] = lds1(t0 + kArr17 + o + 72);
-    for (int x = 0; x < 8; ++x) {
-        u[x + 1] = lds1(t0 + o + 8u * x);
-        d[x + 1] = lds1(t0 + kArr17 + o + 8u * x);
-    }
-    const bool dirichlet = (cflags & kFlagDirichlet) != 0;
-    const int kx = key & 1023, ky = (key >> 10) & 1023, kz = (key >> 20) & 1023;
-    bool any = false;
-    bool h[8];
-    for (int x = 0; x < 8; ++x) {
-        const bool a = (bits >> x) & 1u;
-        const double uc = u[x + 1], dc = d[x + 1];
-        const uint32_t e = o + 8u * x;
-        const double nu[6] = {u[x], u[x + 2], lds1(t0 + e - kRow17), lds1(t0 + e + kRow17), lds1(tm + e), lds1(tp + e)};
-        const double nd[6] = {d[x], d[x + 2], lds1(t0 + kArr17 + e - kRow17), lds1(t0 + kArr17 + e + kRow17),
-                              lds1(tm + kArr17 + e), lds1(tp + kArr17 + e)};
-        const bool s = REACTION == PD_REACTION_SURFACE_SINK && ((bits >> (16 + x)) & 1u);
-        const double sv = REACTION == PD_REACTION_VOLUMETRIC ? src[(int64_t)c * 512 + z * 64 + y * 8 + x] : 0.0;
-        const int64_t gx = (int64_t)kx * 8 + x, gy = (int64_t)ky * 8 + y, gz = (int64_t)kz * 8 + z;
-        if (dirichlet) {
-            if (!sentinel(dc)) out[x] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
-            h[x] = a && huge(out[x]);
-        } else {
-            h[x] = a && huge(out[x]);
-            if (h[x] && !isfinite(out[x]) && !sentinel(dc))
-                out[x] = slow_node<REACTION>(K, uc, dc, nu, nd, gx, gy, gz, s, sv);
-        }
-        any = any || h[x];
-    }
-    if (any) {
-        int first = -1;
-        for (int x = 7; x >= 0; --x)
-            if (((bits >> x) & 1u) && !isfinite(out[x])) first = x;
-        if (first >= 0) {
-            atomicMin(bad_key, ((unsigned long long)c << 10) | (unsigned long long)(z * 64 + y * 8 + first));
-            atomicOr(flagp, 1);
-        } else {
-            atomicOr(flagp, 2);
-        }
-    }
-}
-
-template <int INTERIOR>
-__device__ __forceinline__ double rface(double da, double db, double ua, double ub) {
-    return INTERIOR ? fface(da, db, ua, ub) : face(da, db, ua, ub);
-}
-
-// One row of 8 nodes: lap = 0 + x, += y, += z (solver.hpp:420-433, axes in order).
-template <int INTERIOR>
-__device__ __forceinline__ void row_lap(const Consts& Q, uint32_t t0, uint32_t tm, uint32_t tp, uint32_t o,
-                                        const double* u, const double* d, double* lap) {
-    const double2 hu = lds2(t0 + o + 64), hd = lds2(t0 + kArr17 + o + 64);  // x = -1, x = 8
-    double fprev = rface<INTERIOR>(hd.x, d[0], hu.x, u[0]);
-#pragma unroll
-    for (int x = 0; x < 8; ++x) {
-        const double fnext = x < 7 ? rface<INTERIOR>(d[x], d[x + 1], u[x], u[x + 1]) : rface<INTERIOR>(d[7], hd.y, u[7], hu.y);
-        lap[x] = 0.0 + (fnext - fprev) * Q.ix;
-        fprev = fnext;
-    }
-#pragma unroll
-    for (int ax = 0; ax < 2; ++ax) {
-        const uint32_t om = ax == 0 ? t0 + o - kRow17 : tm + o;
-        const uint32_t op = ax == 0 ? t0 + o + kRow17 : tp + o;
-        const double w = ax == 0 ? Q.iy : Q.iz;
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const double2 um = lds2(om + 16u * g), dm = lds2(om + kArr17 + 16u * g);
-            const double2 up = lds2(op + 16u * g), dp = lds2(op + kArr17 + 16u * g);
-            const int x = 2 * g;
-            const double m0 = rface<INTERIOR>(dm.x, d[x], um.x, u[x]);
-            const double p0 = rface<INTERIOR>(d[x], dp.x, u[x], up.x);
-            const double m1 = rface<INTERIOR>(dm.y, d[x + 1], um.y, u[x + 1]);
-            const double p1 = rface<INTERIOR>(d[x + 1], dp.y, u[x + 1], up.y);
-            lap[x] += (p0 - m0) * w;
-            lap[x + 1] += (p1 - m1) * w;
-        }
-    }
-}
-
-template <int REACTION>
-__device__ __forceinline__ void compute17(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
-                                          const ChunkCtx17& C, int it, uint32_t sb, uint32_t base, int y, int zq,
-                                          double* __restrict__ un) {
-    const int z = 4 * it + zq;
-    const uint32_t b = base + (uint32_t)z;
-    const uint32_t tm = sb + (b & 15u) * kTile17;
-    const uint32_t t0 = sb + ((b + 1u) & 15u) * kTile17;
-    const uint32_t tp = sb + ((b + 2u) & 15u) * kTile17;
-    const uint32_t bits = (C.lr >> (8 * it)) & 0x00FF00FFu;
-    const uint32_t o = kRow17 * (uint32_t)(y + 1);
-    double u[8], d[8], lap[8];
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-        const double2 a = lds2(t0 + o + 16u * g), e = lds2(t0 + kArr17 + o + 16u * g);
-        u[2 * g] = a.x;
-        u[2 * g + 1] = a.y;
-        d[2 * g] = e.x;
-        d[2 * g + 1] = e.y;
-    }
-    const bool interior = ((C.flags >> (8 + 4 * it)) & 15) == 15;  // all four planes (warp-uniform)
-    if (interior)
-        row_lap<1>(Q, t0, tm, tp, o, u, d, lap);
-    else
-        row_lap<0>(Q, t0, tm, tp, o, u, d, lap);
-    double out[8];
-    bool hot = false;
-#pragma unroll
-    for (int x = 0; x < 8; ++x) {
-        double r = 0.0;
-        if (REACTION == PD_REACTION_SURFACE_SINK) {
-            r = ((bits >> (16 + x)) & 1u) ? Q.neg_k * u[x] : 0.0;
-        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-            r = M.A.src[(uint32_t)C.c * 512u + (uint32_t)z * 64u + (uint32_t)y * 8u + x] * Q.src_factor;
-        }
-        out[x] = u[x] + Q.dt * lap[x] + Q.dt * r;
-        if (!interior && sentinel(d[x])) out[x] = u[x];  // walls stay frozen (solver.hpp:413-417)
-        hot = hot || (((bits >> x) & 1u) && huge(out[x]));
-    }
-    if ((C.flags & kFlagDirichlet) || hot)
-        row_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, M.A.src, C.c, C.key, C.flags, bits, z, y, tm, t0, tp,
-                           out);
-    double* dst = un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + (uint32_t)y * 8u);
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-        stg_pair(dst + 2 * g, out[2 * g], out[2 * g + 1], (bits >> (2 * g)) & 1u, (bits >> (2 * g + 1)) & 1u);
-}
-
-template <int REACTION>
-__global__ void __launch_bounds__(kThreads, kCtas17) ftcs_march17_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ SlowConsts K;
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const StepArgs<double>& A = M.A;
-    if (A.k > 0) {
-        const int prev = A.flags[A.k - 1];
-        if (prev) {
-            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
-            return;
-        }
-    }
-    if (t == 0) {
-        for (int a = 0; a < 3; ++a) {
-            K.size[a] = A.size[a];
-            K.inv_dx2[a] = A.inv_dx2[a];
-        }
-        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
-        K.dt = A.dt;
-        K.neg_k = A.neg_k;
-        K.src_factor = A.src_factor;
-        K.dirichlet = A.dirichlet;
-    }
-    __syncthreads();
-    Consts Q;
-    Q.dt = A.dt;
-    Q.neg_k = A.neg_k;
-    Q.src_factor = A.src_factor;
-    Q.ix = A.inv_dx2[0];
-    Q.iy = A.inv_dx2[1];
-    Q.iz = A.inv_dx2[2];
-    const LaneGeo G = lane_geo17(lane);
-    const int ry = lane & 7, rzq = lane >> 3;
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes17;
-    const double* __restrict__ u = A.u;
-    const double* __restrict__ de = M.deff;
-    double* __restrict__ un = A.un;
-    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
-
-    // chunk pipeline (see ftcs_march14_kernel), compute-side masks in lr
-    int* ctr_l = M.counter + ((t >> 5) & M.zero);
-    const int n = (int)M.n;
-    const uint32_t cb = sb + kRing17 * kTile17;
-    auto cent = [&](int e) -> uint32_t { return cb + (uint32_t)e * kCtxBytes15; };
-    int raw = 0;
-    auto claim_issue = [&]() {
-        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(raw) : "l"(ctr_l) : "memory");
-    };
-    auto sched_sync = [&]() -> int {
-        claim_issue();
-        const int p = __shfl_sync(0xffffffffu, raw, 0);
-        return p < n ? __ldg(&M.sched[p]) : -1;
-    };
-    auto fetch_ctx = [&](uint32_t e, int c) {
-        const int64_t cc = c < 0 ? 0 : c;
-        cp4(e + 4u * (uint32_t)lane, M.lm + cc * 32 + lane, c >= 0);
-        cp4(e + kCtxLq + 4u * (uint32_t)lane, M.lq + cc * 32 + lane, c >= 0);
-        cp4(e + kCtxDesc + 4u * (uint32_t)(lane & 7), M.desc + cc * 8 + (lane & 7), c >= 0 && lane < 8);
-    };
-    {
-        const int id0 = sched_sync();
-        if (id0 < 0) return;
-        const int id1 = sched_sync();
-        if (lane == 0) {
-            sts_u32(cent(0) + kCtxId, (uint32_t)id0);
-            sts_u32(cent(1) + kCtxId, (uint32_t)id1);
-        }
-        fetch_ctx(cent(0), id0);
-        cp_commit();
-        cp_wait<0>();
-        __syncwarp();
-        claim_issue();
-    }
-    int ek = 0;
-    ChunkCtx17 Cld, Cprev;
-    LoadCtx14 Lld;
-    auto advance = [&]() {
-        Cprev = Cld;
-        const uint32_t e0 = cent(ek);
-        const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
-        const uint32_t e1 = cent(e1i), e2 = cent(e2i);
-        const int c = (int)lds_u32(e0 + kCtxId);
-        const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
-        const uint32_t lr = c >= 0 ? lds_u32(e0 + kCtxLq + 4u * (uint32_t)lane) : 0u;
-        const int dv = (int)lds_u32(e0 + kCtxDesc + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
-        Cld = ChunkCtx17{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lr};
-        Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
-        const int c1 = (int)lds_u32(e1 + kCtxId);
-        fetch_ctx(e1, c1);
-        if (lane == 0) {
-            const bool ok = raw < n;
-            cp4(e2 + kCtxId, M.sched + (ok ? raw : 0), ok);
-            if (!ok) sts_u32(e2 + kCtxId, 0xFFFFFFFFu);
-        }
-        claim_issue();
-        ek = e1i;
-    };
-    advance();
-    cp_commit();
-    cp_wait<0>();
-    __syncwarp();
-    int p_ld = 0;
-    uint32_t Lc = 0;
-    auto issue_next = [&]() {
-        issue17(sb + (Lc & (kRing17 - 1)) * kTile17, u, de, Lld, p_ld, G, sent_off);
-        if (++p_ld == 10) {
-            p_ld = 0;
-            // the context fetched at the previous advance (ten loads ago) must
-            // have landed: at most the nine newest groups may still be pending
-            cp_wait<9>();
-            __syncwarp();
-            advance();
-        }
-        cp_commit();
-        ++Lc;
-    };
-    ChunkCtx17 Cc = Cld;
-    uint32_t base = 0;  // load index of plane -1 of Cc
-    // prologue: this chunk's 10 loads and the next chunk's loads 0..5
-#pragma unroll 1
-    for (int k = 0; k < 16; ++k) issue_next();
-#pragma unroll 1
-    while (Cc.c >= 0) {
-        // before each half: the loads it needs are done, ten newer ones in flight
-        cp_wait<10>();
-        __syncwarp();
-        compute17<REACTION>(M, K, Q, Cc, 0, sb, base, ry, rzq, un);
-        __syncwarp();
-#pragma unroll 1
-        for (int k = 0; k < 4; ++k) issue_next();  // next chunk's loads 6..9 (slots of planes -1..2)
-        cp_wait<10>();
-        __syncwarp();
-        compute17<REACTION>(M, K, Q, Cc, 1, sb, base, ry, rzq, un);
-        __syncwarp();
-#pragma unroll 1
-        for (int k = 0; k < 6; ++k) issue_next();  // the chunk after's loads 0..5
-        base += 10u;
-        Cc = Cprev;
-    }
-    cp_wait<0>();
-}
-
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 // desc flags of the fused halo push: bit set iff the chunk has a peer ghost
@@ -1498,7 +718,6 @@ void march_free(MarchPlan* p) {
     pd_free(p->d_deff);
     pd_free(p->d_counter);
     pd_free(p->d_lm);
-    pd_free(p->d_lq);
     *p = MarchPlan{};
 }
 
@@ -1565,17 +784,6 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
         d_nbr, g->d_keys, d_fluid, n_all, g->size[0], g->size[1], g->size[2], dirichlet, plan->d_desc);
     PD_CUDA(cudaGetLastError());
     PD_CUDA(pd_malloc(&plan->d_lm, sizeof(uint32_t) * 32 * (size_t)n_all));
-    const char* ver_env = getenv("PD_MARCH_V");
-    const int ver = g->tbytes == 4 ? 14 : (ver_env ? atoi(ver_env) : 14);  // FP32: pd_march32.cu
-    if (ver == 15 || ver == 16) {  // quad lane masks
-        PD_CUDA(pd_malloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
-        lanemask15_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
-                                                                                      plan->d_lq);
-    } else if (ver == 17) {  // row lane masks
-        PD_CUDA(pd_malloc(&plan->d_lq, sizeof(uint32_t) * 32 * (size_t)n_all));
-        lanemask17_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink, n_all,
-                                                                                      plan->d_lq);
-    }
     lanemask_kernel<<<(unsigned)((n_all * 32 + 255) / 256), 256, 0, g->stream>>>(g->d_masks, d_sink,
                                                                                 n_all, plan->d_lm);
     PD_CUDA(cudaGetLastError());
@@ -1649,7 +857,6 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.n = n;
     M.desc = p.d_desc;
     M.lm = p.d_lm;
-    M.lq = p.d_lq;
     M.deff = static_cast<const double*>(p.d_deff);
     M.counter = counter;
     static const int dbg = [] {
@@ -1657,11 +864,6 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
         return e ? atoi(e) : 0;
     }();
     M.dbg = dbg;
-    static const int stat = [] {
-        const char* e = getenv("PD_MARCH_STATIC");
-        return e ? atoi(e) : 0;
-    }();
-    M.static_sched = stat;
     M.zero = 0;
     M.n_all = g->n_chunks;
     static const int ver = [] {
@@ -1671,37 +873,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
     if (pl && ver != 14) fail(PD_E_INPUT, "the fused peer halo push needs march v14 (PD_MARCH_V unset)");
-    if (ver == 17) {
-        constexpr size_t bytes = (size_t)kWarpBytes17 * kWarps;
-        static const KernT table[3] = {ftcs_march17_kernel<0>, ftcs_march17_kernel<1>, ftcs_march17_kernel<2>};
-        static bool attr_set = false;
-        if (!attr_set) {
-            for (auto k : table)
-                PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-            attr_set = true;
-        }
-        int sms = 148;
-        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        table[r]<<<sms * kCtas17, kThreads, bytes, g->stream>>>(M);
-    } else if (ver == 15 || ver == 16) {
-        const bool r10 = ver == 16;
-        const size_t bytes = (size_t)((r10 ? 10 : kRing14) * kTileBytes + 3 * kCtxBytes15) * kWarps;
-        static const KernT table[2][3] = {
-            {ftcs_march15_kernel<0, 0>, ftcs_march15_kernel<1, 0>, ftcs_march15_kernel<2, 0>},
-            {ftcs_march15_kernel<0, 1>, ftcs_march15_kernel<1, 1>, ftcs_march15_kernel<2, 1>}};
-        static bool attr_set = false;
-        if (!attr_set) {
-            for (int v = 0; v < 2; ++v)
-                for (auto k : table[v])
-                    PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)((size_t)((v ? 10 : kRing14) * kTileBytes + 3 * kCtxBytes15) *
-                                                       kWarps)));
-            attr_set = true;
-        }
-        int sms = 148;
-        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        table[r10 ? 1 : 0][r]<<<sms * (r10 ? 3 : kCtas15), kThreads, bytes, g->stream>>>(M);
-    } else {
+    {
         constexpr size_t bytes = (size_t)kWarpBytes14 * kWarps;
         static const KernT table[2][3] = {
             {ftcs_march14_kernel<0, false>, ftcs_march14_kernel<1, false>, ftcs_march14_kernel<2, false>},
