@@ -19,6 +19,8 @@
 #include <limits>
 #include <vector>
 
+#include <cstdlib>
+
 #include "pd_internal.cuh"
 
 namespace pdb {
@@ -179,7 +181,8 @@ __global__ void __launch_bounds__(256)
             if (!has_p) dp = dm;
             sum += godunov_sq(dm, dp, pos);
         }
-        const T grad = sqrt(sum);
+        // sqrt(+0) = +0: skip the library sqrt's special-case path (same bits)
+        const T grad = sum == T(0) ? T(0) : sqrt(sum);
         // smoothed_sign (levelset.hpp:30-34): phi / sqrt(phi^2 + |g|^2 h^2)
         const T ss = (c == T(0)) ? T(0) : c / sqrt(c * c + grad * grad * K.h * K.h);
         const T update = K.dt * ss * (T(1) - grad);
@@ -193,6 +196,130 @@ __global__ void __launch_bounds__(256)
         b = other > b ? other : b;
     }
     if (threadIdx.x == 0 && b) atomicMax(res, b);
+}
+
+// 3-D sweep as a z-march (same per-node expression tree as
+// sussman_sweep_kernel, so the same bits): a 32 x 8 block owns an (x, y) tile
+// and walks a segment of z; its own column values come through a register
+// pipeline issued kAheadZ planes ahead, the tile's x / y neighbours through a
+// shared-memory copy of the current plane (+ one halo cell per side, also
+// prefetched), so every phi value is read from DRAM about once per sweep
+// instead of once per neighbour use, and the loads are in flight while the
+// previous planes compute. The band residual is folded per thread over the
+// segment and reduced once per warp.
+constexpr int kAheadZ = 3;
+
+template <class T>
+__device__ __forceinline__ T ld_or0(const T* __restrict__ p, int64_t i, bool ok) {
+    return ok ? __ldg(p + i) : T(0);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+    sussman_zmarch_kernel(const T* __restrict__ phi, T* __restrict__ next, FieldGeo g, SweepConsts<T> K,
+                          typename Bits<T>::U* __restrict__ res, const int* __restrict__ done, int zseg) {
+    if (*done) return;
+    __shared__ T tile[10][34];  // rows y-1..y+8 of the block, columns x-1..x+32
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t x = blockIdx.x * 32 + tx, y = blockIdx.y * 8 + ty;
+    const int64_t nz = g.n[2];
+    const int64_t z0 = (int64_t)blockIdx.z * zseg;
+    const int64_t z1 = z0 + zseg < nz ? z0 + zseg : nz;
+    const bool inb = x < g.n[0] && y < g.n[1];
+    const int64_t col = x + y * g.s1;  // plane-0 index of the thread's own column
+    // halo cell this thread stages (x halo for tx = 0 / 31, y halo for ty = 0 / 7)
+    const bool hx = tx == 0 || tx == 31, hy = ty == 0 || ty == 7;
+    const int64_t xh = tx == 0 ? x - 1 : x + 1, yh = ty == 0 ? y - 1 : y + 1;
+    const bool hx_ok = hx && xh >= 0 && xh < g.n[0] && y < g.n[1];
+    const bool hy_ok = hy && yh >= 0 && yh < g.n[1] && x < g.n[0];
+    const int64_t hx_col = xh + y * g.s1, hy_col = x + yh * g.s1;
+    // pipelines: q[k] = own value of plane z+k (k = -1 .. kAheadZ); hxq / hyq =
+    // halo values of planes z .. z+kAheadZ-1
+    T q[kAheadZ + 2];
+    T hxq[kAheadZ], hyq[kAheadZ];
+#pragma unroll
+    for (int k = 0; k < kAheadZ + 2; ++k) {
+        const int64_t z = z0 - 1 + k;
+        q[k] = ld_or0(phi, col + z * g.s2, inb && z >= 0 && z < nz);
+    }
+#pragma unroll
+    for (int k = 0; k < kAheadZ; ++k) {
+        const int64_t z = z0 + k;
+        hxq[k] = ld_or0(phi, hx_col + z * g.s2, hx_ok && z < nz);
+        hyq[k] = ld_or0(phi, hy_col + z * g.s2, hy_ok && z < nz);
+    }
+    // residual as a max over bit patterns, like sussman_sweep_kernel (a NaN
+    // update wins, exactly as there)
+    typename Bits<T>::U lb = 0;
+    const bool pos_x_m = x > 0, pos_x_p = x + 1 < g.n[0];
+    const bool pos_y_m = y > 0, pos_y_p = y + 1 < g.n[1];
+    for (int64_t z = z0; z < z1; ++z) {
+        const T c = q[1];
+        __syncthreads();  // the previous plane's readers are done
+        tile[ty + 1][tx + 1] = c;
+        if (hx) tile[ty + 1][tx == 0 ? 0 : 33] = hxq[0];
+        if (hy) tile[ty == 0 ? 0 : 9][tx + 1] = hyq[0];
+        __syncthreads();
+        // refill the pipelines (plane z+kAheadZ+1 own, z+kAheadZ halos)
+        const T nq = ld_or0(phi, col + (z + kAheadZ + 1) * g.s2, inb && z + kAheadZ + 1 < nz);
+        const T nhx = ld_or0(phi, hx_col + (z + kAheadZ) * g.s2, hx_ok && z + kAheadZ < nz);
+        const T nhy = ld_or0(phi, hy_col + (z + kAheadZ) * g.s2, hy_ok && z + kAheadZ < nz);
+        if (inb) {
+            const bool pos = !(c < T(0));
+            T sum = T(0);
+            {  // axis 0
+                T dm = T(0), dp = T(0);
+                if (pos_x_m) dm = (c - tile[ty + 1][tx]) * K.inv_h[0];
+                if (pos_x_p) dp = (tile[ty + 1][tx + 2] - c) * K.inv_h[0];
+                if (!pos_x_m) dm = dp;
+                if (!pos_x_p) dp = dm;
+                sum += godunov_sq(dm, dp, pos);
+            }
+            {  // axis 1
+                T dm = T(0), dp = T(0);
+                if (pos_y_m) dm = (c - tile[ty][tx + 1]) * K.inv_h[1];
+                if (pos_y_p) dp = (tile[ty + 2][tx + 1] - c) * K.inv_h[1];
+                if (!pos_y_m) dm = dp;
+                if (!pos_y_p) dp = dm;
+                sum += godunov_sq(dm, dp, pos);
+            }
+            {  // axis 2
+                const bool has_m = z > 0, has_p = z + 1 < nz;
+                T dm = T(0), dp = T(0);
+                if (has_m) dm = (c - q[0]) * K.inv_h[2];
+                if (has_p) dp = (q[2] - c) * K.inv_h[2];
+                if (!has_m) dm = dp;
+                if (!has_p) dp = dm;
+                sum += godunov_sq(dm, dp, pos);
+            }
+            // sqrt(+0) = +0: skip the library sqrt's special-case path (same bits)
+            const T grad = sum == T(0) ? T(0) : sqrt(sum);
+            // smoothed_sign (levelset.hpp:30-34): phi / sqrt(phi^2 + |g|^2 h^2)
+            const T ss = (c == T(0)) ? T(0) : c / sqrt(c * c + grad * grad * K.h * K.h);
+            const T update = K.dt * ss * (T(1) - grad);
+            next[col + z * g.s2] = c + update;
+            if (fabs(c) <= K.band) {
+                const typename Bits<T>::U ub = Bits<T>::of(fabs(update));
+                lb = ub > lb ? ub : lb;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kAheadZ + 1; ++k) q[k] = q[k + 1];
+        q[kAheadZ + 1] = nq;
+#pragma unroll
+        for (int k = 0; k < kAheadZ - 1; ++k) {
+            hxq[k] = hxq[k + 1];
+            hyq[k] = hyq[k + 1];
+        }
+        hxq[kAheadZ - 1] = nhx;
+        hyq[kAheadZ - 1] = nhy;
+    }
+    typename Bits<T>::U b = lb;
+    for (int o = 16; o; o >>= 1) {
+        const typename Bits<T>::U other = __shfl_xor_sync(0xffffffffu, b, o);
+        b = other > b ? other : b;
+    }
+    if (tx == 0 && b) atomicMax(res, b);
 }
 
 // After sweep it (1-based): converged when residual < tol (levelset.hpp:183-187).
@@ -345,10 +472,26 @@ void redistance(pd_field* f, const pd_levelset_options* o, pd_redistance_diag* o
         PD_CUDA(cudaMemsetAsync(d_state, 0, 2 * sizeof(int), f->stream));
         T* bufs[2] = {(T*)f->d, next};
         int h_state[2] = {0, 0};
+        // z-march segments: enough blocks for ~4 waves of the (x, y) tiles
+        static const int zmarch = [] {
+            const char* e = getenv("PD_SUSSMAN_ZMARCH");
+            return e ? atoi(e) : 1;
+        }();
+        int sms = 148;
+        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device));
+        const int64_t tiles = ((f->size[0] + 31) / 32) * ((f->size[1] + 7) / 8);
+        int64_t nseg = (int64_t)sms * 8 * 4 / (tiles > 0 ? tiles : 1);
+        if (nseg < 1) nseg = 1;
+        if (nseg > f->size[2]) nseg = f->size[2];
+        const int zseg = (int)((f->size[2] + nseg - 1) / nseg);
         for (int it = 1; it <= o->max_iterations; ++it) {
             const T* src = bufs[(it - 1) & 1];
             T* dst = bufs[it & 1];
-            if (f->dims == 3)
+            if (f->dims == 3 && zmarch) {
+                const dim3 gz((unsigned)((f->size[0] + 31) / 32), (unsigned)((f->size[1] + 7) / 8),
+                              (unsigned)((f->size[2] + zseg - 1) / zseg));
+                sussman_zmarch_kernel<T><<<gz, kBlock3, 0, f->stream>>>(src, dst, g, K, d_res + it, d_state, zseg);
+            } else if (f->dims == 3)
                 sussman_sweep_kernel<T, 3><<<grid3(f), kBlock3, 0, f->stream>>>(src, dst, g, K, d_res + it,
                                                                                    d_state);
             else

@@ -66,6 +66,7 @@ class DeviceField:
     def __init__(self, geometry: pd.GridGeometry, dtype=np.float64, device: int = 0):
         self.geom = geometry
         self.dtype = np.dtype(dtype)
+        self.device = device
         dims = geometry.dims
         size = (C.c_int64 * 3)(*(list(geometry.size) + [1] * (3 - dims)))
         spacing = (C.c_double * 3)(*(list(geometry.spacing) + [1.0] * (3 - dims)))
@@ -98,7 +99,12 @@ class DeviceField:
         return out
 
     def copy(self) -> "DeviceField":
-        return DeviceField.from_host(self.geom, self.download(), self.dtype)
+        """Device-to-device copy (same geometry and scalar type)."""
+        out = DeviceField(self.geom, self.dtype, self.device)
+        ptr = C.c_void_p()
+        _check(lib.pd_field_device_ptr(self.h, C.byref(ptr)))
+        out.upload_device(ptr.value)
+        return out
 
     def close(self):
         if self.h is not None and self.h.value:

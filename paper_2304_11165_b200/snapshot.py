@@ -63,7 +63,7 @@ def read_dense_snapshot(path: str, dtype=np.float64, dims: int = 3, device: int 
     info = peek_snapshot(path)
     geom = pd.GridGeometry.make(tuple(info.size), tuple(info.spacing), tuple(info.origin))
     f = DeviceField.__new__(DeviceField)
-    f.geom, f.dtype, f.h = geom, np.dtype(dtype), C.c_void_p()
+    f.geom, f.dtype, f.h, f.device = geom, np.dtype(dtype), C.c_void_p(), device
     _check(lib.pd_field_read_snapshot(str(path).encode(), dims, np.dtype(dtype).itemsize, device, C.byref(f.h)))
     return f
 
