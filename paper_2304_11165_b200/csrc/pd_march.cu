@@ -55,6 +55,11 @@ constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
 constexpr int kFlagPushLo = 1 << 16;  // push the new z=0 plane to the lower peer's ghost chunk
 constexpr int kFlagPushHi = 1 << 17;  // push the new z=7 plane to the upper peer's ghost chunk
+// uniform chunk: it and its six face neighbours exist, every node is fluid and
+// D_eff is one value dv (bit pattern) throughout, so every face coefficient
+// the reference forms, (d_c + d_n) * 0.5, is (dv + dv) * 0.5: the chunk loads
+// no D_eff at all (march v14, compute14u)
+constexpr int kFlagUnif = 1 << 18;
 // desc flag bits 8..15: plane z is interior-fluid (every node and every face
 // neighbour fluid) -> select-free path
 
@@ -80,6 +85,7 @@ struct MarchArgs {
     // peer's ghost chunk peer_ord[2c+side] of the peer's u_next column
     double* peer_un[2];
     const int32_t* __restrict__ peer_ord;
+    const double* __restrict__ dv;     // per chunk: the uniform D_eff of kFlagUnif chunks
 };
 
 
@@ -273,7 +279,7 @@ __device__ __forceinline__ void stg_pair(double* p, double a, double b, bool a0,
 constexpr int kRing14 = 8;
 constexpr int kAhead14 = 5;  // kRing14 - 3 (planes z-1, z, z+1 resident)
 constexpr int kCtas14 = 4;
-constexpr uint32_t kCtxBytes14 = 176;  // lm[32], desc[8], id, pad
+constexpr uint32_t kCtxBytes14 = 176;  // lm[32] | desc[8] | id, pad | uniform D (at 168)
 constexpr uint32_t kWarpBytes14 = kRing14 * kTileBytes + 3 * kCtxBytes14;
 
 __device__ __forceinline__ void cp4(uint32_t sa, const void* g, bool pred) {
@@ -295,6 +301,7 @@ struct LoadCtx14 {
     uint32_t own, zl, zh, xo, yo;  // element offsets of the lane's sources in plane 0
     uint32_t lm;                   // active bits of the lane's pair (0 if no chunk)
     bool zlok, zhok, xok, yok;
+    bool dl;                       // load D_eff (false for kFlagUnif chunks)
 };
 
 __device__ __forceinline__ LoadCtx14 make_load_ctx14(int c, uint32_t lm, int dv, int dbg, const LaneGeo& G) {
@@ -303,6 +310,7 @@ __device__ __forceinline__ LoadCtx14 make_load_ctx14(int c, uint32_t lm, int dv,
     for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
     LoadCtx14 L;
     const bool ok = c >= 0;
+    L.dl = !(__shfl_sync(0xffffffffu, dv, 31) & kFlagUnif);
     L.own = ok ? (uint32_t)c * 512u + G.bp : 0u;
     L.lm = ok ? lm : 0u;
     L.zlok = ok && nb[4] >= 0 && !(dbg & 4);
@@ -343,22 +351,25 @@ __device__ __forceinline__ void issue14(uint32_t st, const double* __restrict__ 
     if (i == 0 || i == 9) {
         const bool ok = i == 0 ? L.zlok : L.zhok;
         const uint32_t o = i == 0 ? L.zl : L.zh;
-        cp16_ud(st + G.s_c, u + o, ok, st + kDOff + G.s_c, de + (ok ? o : sent_off + G.bp), true);
+        cp16_ud(st + G.s_c, u + o, ok, st + kDOff + G.s_c, de + (ok ? o : sent_off + G.bp), L.dl);
         return;
     }
     const uint32_t p64 = (uint32_t)(i - 1) * 64u;
     const bool ok = ((L.lm >> (2 * (i - 1))) & 3u) != 0u;
     const uint32_t o = L.own + p64;
-    cp16_ud(st + G.s_c, u + o, ok, st + kDOff + G.s_c, de + (ok ? o : sent_off + G.bp + p64), true);
+    cp16_ud(st + G.s_c, u + o, ok, st + kDOff + G.s_c, de + (ok ? o : sent_off + G.bp + p64), L.dl);
     const uint32_t ox = L.xo + p64;
-    cp8_ud(st + G.s_hx, u + ox, L.xok, st + kDOff + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64), G.xface);
+    cp8_ud(st + G.s_hx, u + ox, L.xok, st + kDOff + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64),
+           G.xface && L.dl);
     const uint32_t oy = L.yo + p64;
-    cp16_ud(st + G.s_hy, u + oy, L.yok, st + kDOff + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64), G.yface);
+    cp16_ud(st + G.s_hy, u + oy, L.yok, st + kDOff + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64),
+            G.yface && L.dl);
 }
 
 struct ChunkCtx14 {
     int c, key, flags;
     uint32_t lm;
+    double dv;  // uniform D_eff (kFlagUnif chunks)
 };
 
 // Rare path (Dirichlet-exposed chunk, or a huge / non-finite fast result):
@@ -368,13 +379,15 @@ template <int REACTION>
 __device__ __noinline__ double2 pair_slow14(const MarchArgs& M, const SlowConsts& K, ChunkCtx14 C, int z,
                                             uint32_t tm, uint32_t t0, uint32_t tp, LaneGeo G, double out0,
                                             double out1) {
-    const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
-    const double uL = lds1(t0 + G.s_l), dL = lds1(t0 + kDOff + G.s_l);
-    const double uR = lds1(t0 + G.s_r), dR = lds1(t0 + kDOff + G.s_r);
-    const double2 uym = lds2(t0 + G.s_c - 64), dym = lds2(t0 + kDOff + G.s_c - 64);
-    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = lds2(t0 + kDOff + G.s_c + 64);
-    const double2 uzm = lds2(tm + G.s_c), dzm = lds2(tm + kDOff + G.s_c);
-    const double2 uzp = lds2(tp + G.s_c), dzp = lds2(tp + kDOff + G.s_c);
+    const bool un = (C.flags & kFlagUnif) != 0;  // no D_eff in the ring: every d is dv
+    const double2 vv = make_double2(C.dv, C.dv);
+    const double2 uc = lds2(t0 + G.s_c), dc = un ? vv : lds2(t0 + kDOff + G.s_c);
+    const double uL = lds1(t0 + G.s_l), dL = un ? C.dv : lds1(t0 + kDOff + G.s_l);
+    const double uR = lds1(t0 + G.s_r), dR = un ? C.dv : lds1(t0 + kDOff + G.s_r);
+    const double2 uym = lds2(t0 + G.s_c - 64), dym = un ? vv : lds2(t0 + kDOff + G.s_c - 64);
+    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = un ? vv : lds2(t0 + kDOff + G.s_c + 64);
+    const double2 uzm = lds2(tm + G.s_c), dzm = un ? vv : lds2(tm + kDOff + G.s_c);
+    const double2 uzp = lds2(tp + G.s_c), dzp = un ? vv : lds2(tp + kDOff + G.s_c);
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
     const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
     double src0 = 0.0, src1 = 0.0;
@@ -403,10 +416,64 @@ __device__ __noinline__ void push_pair14(const MarchArgs& M, const ChunkCtx14& C
     if (a1) p[1] = out1;
 }
 
+// Uniform chunk (kFlagUnif): every node active and fluid, every face
+// coefficient (dv + dv) * 0.5 — the reference's (d_c + d_n) * 0.5 with both
+// sides dv — so only u comes from the ring. Same expression order as the
+// interior path of compute14.
+template <int REACTION, bool PUSH>
+__device__ __forceinline__ void compute14u(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
+                                           const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
+                                           const LaneGeo& G, double* __restrict__ un, bool& pushed) {
+    const uint32_t lz = C.lm >> (2 * z);
+    const double2 uc = lds2(t0 + G.s_c);
+    const double uL = lds1(t0 + G.s_l), uR = lds1(t0 + G.s_r);
+    const double2 uym = lds2(t0 + G.s_c - 64), uyp = lds2(t0 + G.s_c + 64);
+    const double2 uzm = lds2(tm + G.s_c), uzp = lds2(tp + G.s_c);
+    const double dh = (C.dv + C.dv) * 0.5;
+    const double fxl = dh * (uc.x - uL), fxi = dh * (uc.y - uc.x), fxr = dh * (uR - uc.y);
+    const double fy0m = dh * (uc.x - uym.x), fy0p = dh * (uyp.x - uc.x);
+    const double fz0m = dh * (uc.x - uzm.x), fz0p = dh * (uzp.x - uc.x);
+    const double fy1m = dh * (uc.y - uym.y), fy1p = dh * (uyp.y - uc.y);
+    const double fz1m = dh * (uc.y - uzm.y), fz1p = dh * (uzp.y - uc.y);
+    double lap0 = 0.0;
+    lap0 += (fxi - fxl) * Q.ix;
+    lap0 += (fy0p - fy0m) * Q.iy;
+    lap0 += (fz0p - fz0m) * Q.iz;
+    double lap1 = 0.0;
+    lap1 += (fxr - fxi) * Q.ix;
+    lap1 += (fy1p - fy1m) * Q.iy;
+    lap1 += (fz1p - fz1m) * Q.iz;
+    double r0 = 0.0, r1 = 0.0;
+    if (REACTION == PD_REACTION_SURFACE_SINK) {
+        r0 = ((lz >> 16) & 1u) ? Q.neg_k * uc.x : 0.0;
+        r1 = ((lz >> 17) & 1u) ? Q.neg_k * uc.y : 0.0;
+    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const double* sp = M.A.src + (int64_t)C.c * 512 + z * 64 + G.bp;
+        r0 = sp[0] * Q.src_factor;
+        r1 = sp[1] * Q.src_factor;
+    }
+    double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
+    double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
+    if (huge(out0) | huge(out1)) {
+        const double2 r = pair_slow14<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        out0 = r.x;
+        out1 = r.y;
+    }
+    stg_pair(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, true, true);
+    if (PUSH && (C.flags & (kFlagPushLo | kFlagPushHi)) && (z == 0 || z == 7)) {
+        push_pair14(M, C, z, G.bp, out0, out1, true, true);
+        pushed = true;
+    }
+}
+
 template <int REACTION, bool PUSH>
 __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
                                           const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
                                           const LaneGeo& G, double* __restrict__ un, bool& pushed) {
+    if (C.flags & kFlagUnif) {  // warp-uniform
+        compute14u<REACTION, PUSH>(M, K, Q, C, z, tm, t0, tp, G, un, pushed);
+        return;
+    }
     const uint32_t lz = C.lm >> (2 * z);
     const bool a0 = lz & 1u, a1 = (lz >> 1) & 1u;
     const double2 uc = lds2(t0 + G.s_c), dc = lds2(t0 + kDOff + G.s_c);
@@ -540,10 +607,12 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
         const int p = __shfl_sync(0xffffffffu, raw, 0);
         return p < n ? __ldg(&M.sched[p]) : -1;
     };
-    auto fetch_ctx = [&](uint32_t e, int c) {  // masks + descriptor of chunk c into entry e
+    auto fetch_ctx = [&](uint32_t e, int c) {  // masks + descriptor + uniform D of chunk c into entry e
         cp4(e + 4u * (uint32_t)lane, M.lm + (int64_t)(c < 0 ? 0 : c) * 32 + lane, c >= 0);
         cp4(e + 128u + 4u * (uint32_t)(lane & 7), M.desc + (int64_t)(c < 0 ? 0 : c) * 8 + (lane & 7),
             c >= 0 && lane < 8);
+        cp4(e + 168u + 4u * (uint32_t)(lane & 1),
+            reinterpret_cast<const uint32_t*>(M.dv + (c < 0 ? 0 : c)) + (lane & 1), c >= 0 && lane < 2);
     };
     {
         const int id0 = sched_sync();
@@ -570,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
         const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
         // descriptor word j lives at lane 24 + j (make_load_ctx14 / ChunkCtx14)
         const int dv = (int)lds_u32(e0 + 128u + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
-        Cld = ChunkCtx14{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm};
+        Cld = ChunkCtx14{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm,
+                         lds1(e0 + 168u)};
         Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
         const int c1 = (int)lds_u32(e1 + 160u);
         fetch_ctx(e1, c1);
@@ -698,6 +768,33 @@ __global__ void lanemask_kernel(const uint64_t* __restrict__ act, const uint64_t
 
 // D_eff = fluid ? D : -inf over every slot; counts fluid nodes whose D is not
 // finite (then the fast path is disabled: its sentinel logic assumes finite D).
+// Uniform chunks (kFlagUnif): per chunk the common D_eff bit pattern of its
+// 512 slots (all fluid), else the marker ~0 (a NaN, never a valid D_eff).
+constexpr unsigned long long kNotUnif = ~0ull;
+__global__ void unif_dv_kernel(const double* __restrict__ deff, int64_t n, double* __restrict__ dv) {
+    const int64_t c = blockIdx.x;
+    const int lane = threadIdx.x;
+    if (c >= n) return;
+    const unsigned long long* d = reinterpret_cast<const unsigned long long*>(deff) + c * 512;
+    const unsigned long long v0 = d[0];
+    bool same = (unsigned)(v0 >> 32) != kSentHi;
+    for (int i = lane; i < 512; i += 32) same = same && d[i] == v0;
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) reinterpret_cast<unsigned long long*>(dv)[c] = same ? v0 : kNotUnif;
+}
+__global__ void unif_flag_kernel(int32_t* __restrict__ desc, const double* __restrict__ dv, int64_t n) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const unsigned long long* b = reinterpret_cast<const unsigned long long*>(dv);
+    const unsigned long long v = b[c];
+    bool ok = v != kNotUnif;
+    for (int f = 0; f < 6 && ok; ++f) {
+        const int j = desc[c * 8 + f];
+        ok = j >= 0 && b[j] == v;
+    }
+    if (ok) desc[c * 8 + 7] |= kFlagUnif;
+}
+
 __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __restrict__ fluid,
                             int64_t n_slots, double* __restrict__ deff, unsigned long long* bad) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -715,6 +812,7 @@ void march_free(MarchPlan* p) {
     }
     pd_free(p->d_stream);
     pd_free(p->d_desc);
+    pd_free(p->d_dv);
     pd_free(p->d_deff);
     pd_free(p->d_counter);
     pd_free(p->d_lm);
@@ -816,6 +914,10 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
             march_free(plan);
             return;
         }
+        PD_CUDA(pd_malloc(&plan->d_dv, sizeof(double) * (size_t)n_all));
+        unif_dv_kernel<<<(unsigned)n_all, 32, 0, g->stream>>>(deff, n_all, plan->d_dv);
+        unif_flag_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(plan->d_desc, plan->d_dv, n_all);
+        PD_CUDA(cudaGetLastError());
     }
     const int64_t n = end - begin;
     plan->d_stream = march_schedule(g, begin, end);
@@ -858,6 +960,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.desc = p.d_desc;
     M.lm = p.d_lm;
     M.deff = static_cast<const double*>(p.d_deff);
+    M.dv = p.d_dv;
     M.counter = counter;
     static const int dbg = [] {
         const char* e = getenv("PD_MARCH_DBG");

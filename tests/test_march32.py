@@ -1,6 +1,6 @@
 """The FP32 march kernel (pd_march32.cu; the reference's T = float path,
-solver.hpp:385-455 in float) against the reference run in-process on the same
-inputs: u, u_next and every diagnostics row bit for bit, on grids with many
+solver.hpp:385-455 in float) and the FP64 march kernel's uniform-chunk path
+against the reference run in-process on the same inputs: u, u_next and every diagnostics row bit for bit, on grids with many
 chunks per warp — sink band, volumetric source with a time factor, walls,
 Dirichlet faces — and the non-finite error path (message and post-error
 state). conftest.py sets PD_MARCH_MIN_CHUNKS=0, so every 3-D FP32 step here
@@ -87,3 +87,44 @@ def test_fp32_march_nonfinite_error_and_state(spec_cases, ref, cuda):
     assert str(ei.value) == msg
     for c in ("u", "u_next"):
         assert np.array_equal(ours.channel_data(c).view(np.uint32), g.prop(c).view(np.uint32)), c
+
+
+# FP64 march: uniform chunks (kFlagUnif — every node fluid, one D_eff value in
+# the chunk and its six neighbours) load no D_eff and use (dv + dv) * 0.5 for
+# every face. A steep sigmoid saturates D to exactly d_min + d_max a few cells
+# from the interface, so most chunks of a coarse-grained pack are uniform.
+SPECS64 = {
+    "pack64_unif_sink": dict(dims=3, n=64, box=(0.0, 1.0), geom="pack", pack=(6, 0.05, 0.09, 3),
+                             channels=["phi", "u", "D", "u_next"], profile=(0.05, 1.0, 0.0, 4000.0),
+                             u0=("hash_unit", 2), reaction=("surface_sink", 1.5, 1.0), dt_frac=0.45,
+                             steps=40, record=10),
+    "pack64_unif_vol": dict(dims=3, n=64, box=(0.0, 1.0), geom="pack", pack=(6, 0.05, 0.09, 5),
+                            channels=["phi", "u", "D", "u_next", "f"], profile=(0.1, 2.0, 0.0, 4000.0),
+                            u0=("hash_unit", 8), reaction=("volumetric", "f", "exp"), dirichlet={1: 0.5},
+                            dt_frac=0.45, steps=30, record=30),
+}
+
+
+@pytest.mark.parametrize("name", list(SPECS64))
+def test_fp64_uniform_chunks_equal_reference(name, monkeypatch, ref, cuda):
+    from paper_2304_11165_b200 import porediff as pd
+    for k, v in SPECS64.items():
+        monkeypatch.setitem(cases.CASES, k, v)
+    spec = cases.CASES[name]
+    g = cases.ref_case(name, ref)
+    keys, masks = g.layout()
+    D = g.prop("D")
+    full = np.all(masks == np.uint64(0xFFFFFFFFFFFFFFFF), axis=1)
+    assert (full & (D.min(axis=1) == D.max(axis=1))).mean() > 0.3  # plenty of uniform chunks
+    data = {c: g.prop(c) for c in spec["channels"]}
+    dt = dt_of(spec, g.max_diffusivity())
+    geom = pd.GridGeometry.cell_centered_box(spec["n"], *spec["box"], spec["dims"])
+    ours = pd.SparseBlockGrid.from_layout(geom, spec["channels"], keys, masks, data)
+    code, msg, rows = g.run(oracle_config(spec, dt), time_factor(spec))
+    assert code == 0, msg
+    res = pd.run_simulation(ours, sim_config(spec, dt))
+    assert [tuple(r) for r in rows] == [(d.step, d.time, d.total_mass, d.min_u, d.max_u) for d in res.diagnostics]
+    for c in ("u", "u_next"):
+        a, b = ours.channel_data(c), g.prop(c)
+        diff = np.nonzero(a.view(np.uint64) != b.view(np.uint64))
+        assert diff[0].size == 0, (c, diff[0][:5], diff[1][:5], a[diff][:5], b[diff][:5])
