@@ -55,10 +55,10 @@ constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
 constexpr int kFlagPushLo = 1 << 16;  // push the new z=0 plane to the lower peer's ghost chunk
 constexpr int kFlagPushHi = 1 << 17;  // push the new z=7 plane to the upper peer's ghost chunk
-// uniform chunk: it and its six face neighbours exist, every node is fluid and
-// D_eff is one value dv (bit pattern) throughout, so every face coefficient
-// the reference forms, (d_c + d_n) * 0.5, is (dv + dv) * 0.5: the chunk loads
-// no D_eff at all (march v14, compute14u)
+// uniform chunk: its six face neighbours exist, every node is fluid with one
+// D_eff bit pattern dv, and so is the facing layer of every neighbour, so each
+// face coefficient the reference forms, (d_c + d_n) * 0.5, is (dv + dv) * 0.5:
+// the chunk loads no D_eff at all (march v14, compute14u)
 constexpr int kFlagUnif = 1 << 18;
 // desc flag bits 8..15: plane z is interior-fluid (every node and every face
 // neighbour fluid) -> select-free path
@@ -782,17 +782,41 @@ __global__ void unif_dv_kernel(const double* __restrict__ deff, int64_t n, doubl
     same = __all_sync(0xffffffffu, same);
     if (lane == 0) reinterpret_cast<unsigned long long*>(dv)[c] = same ? v0 : kNotUnif;
 }
-__global__ void unif_flag_kernel(int32_t* __restrict__ desc, const double* __restrict__ dv, int64_t n) {
-    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// A chunk is uniform when its own slots share one D_eff value dv (all fluid)
+// and the facing layer of each of its six neighbours (the only cells its
+// faces read) holds dv too: one warp per chunk, lane pairs per face cell.
+__global__ void unif_flag_kernel(int32_t* __restrict__ desc, const double* __restrict__ deff,
+                                 const double* __restrict__ dv, int64_t n) {
+    const int64_t c = blockIdx.x;
+    const int lane = threadIdx.x;
     if (c >= n) return;
-    const unsigned long long* b = reinterpret_cast<const unsigned long long*>(dv);
-    const unsigned long long v = b[c];
-    bool ok = v != kNotUnif;
-    for (int f = 0; f < 6 && ok; ++f) {
+    const unsigned long long v = reinterpret_cast<const unsigned long long*>(dv)[c];
+    if (v == kNotUnif) return;
+    const unsigned long long* d = reinterpret_cast<const unsigned long long*>(deff);
+    bool ok = true;
+    for (int f = 0; f < 6; ++f) {
         const int j = desc[c * 8 + f];
-        ok = j >= 0 && b[j] == v;
+        if (j < 0) {
+            ok = false;
+            break;
+        }
+        for (int k = lane; k < 64; k += 32) {  // facing layer of neighbour j
+            const int a = k & 7, b = k >> 3;
+            int off;
+            switch (f) {
+                case 0: off = (b << 6) | (a << 3) | 7; break;  // x- neighbour: its x = 7 column
+                case 1: off = (b << 6) | (a << 3); break;      // x+ : x = 0
+                case 2: off = (b << 6) | (7 << 3) | a; break;  // y- : y = 7 row
+                case 3: off = (b << 6) | a; break;             // y+ : y = 0
+                case 4: off = (7 << 6) | (b << 3) | a; break;  // z- : z = 7 plane
+                default: off = (b << 3) | a; break;            // z+ : z = 0
+            }
+            ok = ok && d[(int64_t)j * 512 + off] == v;
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok) break;
     }
-    if (ok) desc[c * 8 + 7] |= kFlagUnif;
+    if (lane == 0 && ok) desc[c * 8 + 7] |= kFlagUnif;
 }
 
 __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __restrict__ fluid,
@@ -916,7 +940,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
         }
         PD_CUDA(pd_malloc(&plan->d_dv, sizeof(double) * (size_t)n_all));
         unif_dv_kernel<<<(unsigned)n_all, 32, 0, g->stream>>>(deff, n_all, plan->d_dv);
-        unif_flag_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, g->stream>>>(plan->d_desc, plan->d_dv, n_all);
+        unif_flag_kernel<<<(unsigned)n_all, 32, 0, g->stream>>>(plan->d_desc, deff, plan->d_dv, n_all);
         PD_CUDA(cudaGetLastError());
     }
     const int64_t n = end - begin;
