@@ -181,7 +181,7 @@ struct MarchPlan {
     int32_t* d_stream = nullptr;   // owned chunk ordinals in schedule order
     int32_t* d_desc = nullptr;     // 8 ints per chunk: nbr[0..5], packed key, flags
     void* d_deff = nullptr;        // D (grid scalar type) on fluid nodes, -inf elsewhere (static per run)
-    double* d_dv = nullptr;        // per chunk: uniform D_eff of kFlagUnif chunks (FP64 march)
+    void* d_dv = nullptr;          // per chunk: uniform D_eff of kFlagUnif chunks (grid scalar type)
     int* d_counter = nullptr;      // per-step dynamic batch counters
     uint32_t* d_lm = nullptr;      // per chunk and lane: active / sink bits [c][32]
     int grid = 0;

@@ -769,30 +769,32 @@ __global__ void lanemask_kernel(const uint64_t* __restrict__ act, const uint64_t
 // D_eff = fluid ? D : -inf over every slot; counts fluid nodes whose D is not
 // finite (then the fast path is disabled: its sentinel logic assumes finite D).
 // Uniform chunks (kFlagUnif): per chunk the common D_eff bit pattern of its
-// 512 slots (all fluid), else the marker ~0 (a NaN, never a valid D_eff).
-constexpr unsigned long long kNotUnif = ~0ull;
-__global__ void unif_dv_kernel(const double* __restrict__ deff, int64_t n, double* __restrict__ dv) {
+// 512 slots (all fluid), else the marker ~0 (a NaN, never a valid D_eff). B
+// is the scalar's bit type (uint64 for FP64, uint32 for FP32 grids).
+template <class B>
+__global__ void unif_dv_kernel(const B* __restrict__ deff, int64_t n, B* __restrict__ dv, B sent_bits) {
     const int64_t c = blockIdx.x;
     const int lane = threadIdx.x;
     if (c >= n) return;
-    const unsigned long long* d = reinterpret_cast<const unsigned long long*>(deff) + c * 512;
-    const unsigned long long v0 = d[0];
-    bool same = (unsigned)(v0 >> 32) != kSentHi;
+    const B* d = deff + c * 512;
+    const B v0 = d[0];
+    bool same = v0 != sent_bits;
     for (int i = lane; i < 512; i += 32) same = same && d[i] == v0;
     same = __all_sync(0xffffffffu, same);
-    if (lane == 0) reinterpret_cast<unsigned long long*>(dv)[c] = same ? v0 : kNotUnif;
+    if (lane == 0) dv[c] = same ? v0 : (B)~(B)0;
 }
+
 // A chunk is uniform when its own slots share one D_eff value dv (all fluid)
 // and the facing layer of each of its six neighbours (the only cells its
-// faces read) holds dv too: one warp per chunk, lane pairs per face cell.
-__global__ void unif_flag_kernel(int32_t* __restrict__ desc, const double* __restrict__ deff,
-                                 const double* __restrict__ dv, int64_t n) {
+// faces read) holds dv too: one warp per chunk.
+template <class B>
+__global__ void unif_flag_kernel(int32_t* __restrict__ desc, const B* __restrict__ d, const B* __restrict__ dv,
+                                 int64_t n) {
     const int64_t c = blockIdx.x;
     const int lane = threadIdx.x;
     if (c >= n) return;
-    const unsigned long long v = reinterpret_cast<const unsigned long long*>(dv)[c];
-    if (v == kNotUnif) return;
-    const unsigned long long* d = reinterpret_cast<const unsigned long long*>(deff);
+    const B v = dv[c];
+    if (v == (B)~(B)0) return;
     bool ok = true;
     for (int f = 0; f < 6; ++f) {
         const int j = desc[c * 8 + f];
@@ -817,6 +819,18 @@ __global__ void unif_flag_kernel(int32_t* __restrict__ desc, const double* __res
         if (!ok) break;
     }
     if (lane == 0 && ok) desc[c * 8 + 7] |= kFlagUnif;
+}
+
+template <class B>
+void mark_uniform(pd_grid* g, MarchPlan* plan, B sent_bits) {
+    const int64_t n_all = g->n_chunks;
+    B* dv = nullptr;
+    PD_CUDA(pd_malloc(&dv, sizeof(B) * (size_t)n_all));
+    plan->d_dv = dv;
+    const B* deff = static_cast<const B*>(plan->d_deff);
+    unif_dv_kernel<B><<<(unsigned)n_all, 32, 0, g->stream>>>(deff, n_all, dv, sent_bits);
+    unif_flag_kernel<B><<<(unsigned)n_all, 32, 0, g->stream>>>(plan->d_desc, deff, dv, n_all);
+    PD_CUDA(cudaGetLastError());
 }
 
 __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __restrict__ fluid,
@@ -916,6 +930,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
             march_free(plan);  // non-finite D on a fluid node: keep the exact tile kernel
             return;
         }
+        mark_uniform<unsigned>(g, plan, 0xFF800000u);
     } else {
         // one extra chunk of sentinels after the last one: the source of every
         // D_eff cell a plane load does not read from the grid (inactive pairs,
@@ -938,10 +953,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
             march_free(plan);
             return;
         }
-        PD_CUDA(pd_malloc(&plan->d_dv, sizeof(double) * (size_t)n_all));
-        unif_dv_kernel<<<(unsigned)n_all, 32, 0, g->stream>>>(deff, n_all, plan->d_dv);
-        unif_flag_kernel<<<(unsigned)n_all, 32, 0, g->stream>>>(plan->d_desc, deff, plan->d_dv, n_all);
-        PD_CUDA(cudaGetLastError());
+        mark_uniform<unsigned long long>(g, plan, 0xFFF0000000000000ull);
     }
     const int64_t n = end - begin;
     plan->d_stream = march_schedule(g, begin, end);
@@ -984,7 +996,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.desc = p.d_desc;
     M.lm = p.d_lm;
     M.deff = static_cast<const double*>(p.d_deff);
-    M.dv = p.d_dv;
+    M.dv = static_cast<const double*>(p.d_dv);
     M.counter = counter;
     static const int dbg = [] {
         const char* e = getenv("PD_MARCH_DBG");

@@ -24,7 +24,8 @@ constexpr int kRing32 = 8;
 constexpr int kAhead32 = kRing32 - 3;   // planes z-1, z, z+1 resident
 constexpr unsigned kSent32 = 0xFF800000u;  // -inf
 constexpr int kFlagDir32 = 2;           // desc flags (pd_march.cu desc_kernel)
-constexpr uint32_t kCtx32 = 176;        // lm[32], desc[8], id, pad
+constexpr int kFlagUnif32 = 1 << 18;    // uniform chunk (pd_march.cu mark_uniform): no D_eff loads
+constexpr uint32_t kCtx32 = 176;        // lm[32] | desc[8] | id | uniform D (at 164)
 
 __device__ __forceinline__ bool sent32(float d) { return __float_as_uint(d) == kSent32; }
 // non-finite (exponent all ones): the fast result needs the exact re-derivation
@@ -46,6 +47,7 @@ struct Args32 {
     const int32_t* __restrict__ desc;
     const uint32_t* __restrict__ lm;
     const float* __restrict__ deff;
+    const float* __restrict__ dv;  // per chunk: uniform D_eff of kFlagUnif32 chunks
     int* counter;
     int zero;
     int64_t n_all;
@@ -173,11 +175,13 @@ __device__ __noinline__ float slow_node32(const Slow32& K, float u_c, float d_c,
 struct Ctx32 {
     int c, key, flags;
     uint32_t lm;
+    float dv;
 };
 
 struct Load32 {
     uint32_t own, zl, zh, xo, yo, lm;
     bool zlok, zhok, xok, yok;
+    bool dl;  // load D_eff (false for uniform chunks)
 };
 
 __device__ __forceinline__ Load32 load_ctx32(int c, uint32_t lm, int dv, const Geo32& G) {
@@ -186,6 +190,7 @@ __device__ __forceinline__ Load32 load_ctx32(int c, uint32_t lm, int dv, const G
     for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
     Load32 L;
     const bool ok = c >= 0;
+    L.dl = !(__shfl_sync(0xffffffffu, dv, 31) & kFlagUnif32);
     L.own = ok ? (uint32_t)c * 512u + G.bp : 0u;
     L.lm = ok ? lm : 0u;
     L.zlok = ok && nb[4] >= 0;
@@ -208,20 +213,20 @@ __device__ __forceinline__ void issue32(uint32_t st, const float* __restrict__ u
         const bool ok = i == 0 ? L.zlok : L.zhok;
         const uint32_t o = i == 0 ? L.zl : L.zh;
         cpa(st + G.s_c, u + o, 1, ok);
-        cpa(st + kDOff32 + G.s_c, de + (ok ? o : sent_off + G.bp), 1, true);
+        cpa(st + kDOff32 + G.s_c, de + (ok ? o : sent_off + G.bp), 1, L.dl);
         return;
     }
     const uint32_t p64 = (uint32_t)(i - 1) * 64u;
     const bool ok = ((L.lm >> (2 * (i - 1))) & 3u) != 0u;
     const uint32_t o = L.own + p64;
     cpa(st + G.s_c, u + o, 1, ok);
-    cpa(st + kDOff32 + G.s_c, de + (ok ? o : sent_off + G.bp + p64), 1, true);
+    cpa(st + kDOff32 + G.s_c, de + (ok ? o : sent_off + G.bp + p64), 1, L.dl);
     const uint32_t ox = L.xo + p64;
     cpa(st + G.s_hx, u + ox, 0, L.xok);
-    cpa(st + kDOff32 + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64), 0, G.xface);
+    cpa(st + kDOff32 + G.s_hx, de + (L.xok ? ox : sent_off + G.bp + p64), 0, G.xface && L.dl);
     const uint32_t oy = L.yo + p64;
     cpa(st + G.s_hy, u + oy, 1, L.yok);
-    cpa(st + kDOff32 + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64), 1, G.yface);
+    cpa(st + kDOff32 + G.s_hy, de + (L.yok ? oy : sent_off + G.bp + p64), 1, G.yface && L.dl);
 }
 
 // Rare path: Dirichlet-exposed chunk (whole chunk exact) or a non-finite fast
@@ -229,13 +234,15 @@ __device__ __forceinline__ void issue32(uint32_t st, const float* __restrict__ u
 template <int REACTION>
 __device__ __noinline__ float2 slow_pair32(const Args32& M, const Slow32& K, Ctx32 C, int z, uint32_t tm, uint32_t t0,
                                            uint32_t tp, Geo32 G, float out0, float out1) {
-    const float2 uc = lds2f(t0 + G.s_c), dc = lds2f(t0 + kDOff32 + G.s_c);
-    const float uL = lds1f(t0 + G.s_l), dL = lds1f(t0 + kDOff32 + G.s_l);
-    const float uR = lds1f(t0 + G.s_r), dR = lds1f(t0 + kDOff32 + G.s_r);
-    const float2 uym = lds2f(t0 + G.s_c - 32), dym = lds2f(t0 + kDOff32 + G.s_c - 32);
-    const float2 uyp = lds2f(t0 + G.s_c + 32), dyp = lds2f(t0 + kDOff32 + G.s_c + 32);
-    const float2 uzm = lds2f(tm + G.s_c), dzm = lds2f(tm + kDOff32 + G.s_c);
-    const float2 uzp = lds2f(tp + G.s_c), dzp = lds2f(tp + kDOff32 + G.s_c);
+    const bool un = (C.flags & kFlagUnif32) != 0;  // no D_eff in the ring: every d is dv
+    const float2 vv = make_float2(C.dv, C.dv);
+    const float2 uc = lds2f(t0 + G.s_c), dc = un ? vv : lds2f(t0 + kDOff32 + G.s_c);
+    const float uL = lds1f(t0 + G.s_l), dL = un ? C.dv : lds1f(t0 + kDOff32 + G.s_l);
+    const float uR = lds1f(t0 + G.s_r), dR = un ? C.dv : lds1f(t0 + kDOff32 + G.s_r);
+    const float2 uym = lds2f(t0 + G.s_c - 32), dym = un ? vv : lds2f(t0 + kDOff32 + G.s_c - 32);
+    const float2 uyp = lds2f(t0 + G.s_c + 32), dyp = un ? vv : lds2f(t0 + kDOff32 + G.s_c + 32);
+    const float2 uzm = lds2f(tm + G.s_c), dzm = un ? vv : lds2f(tm + kDOff32 + G.s_c);
+    const float2 uzp = lds2f(tp + G.s_c), dzp = un ? vv : lds2f(tp + kDOff32 + G.s_c);
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
     const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
     float src0 = 0.0f, src1 = 0.0f;
@@ -271,9 +278,58 @@ __device__ __noinline__ float2 slow_pair32(const Args32& M, const Slow32& K, Ctx
     return make_float2(out0, out1);
 }
 
+// Uniform chunk: every face coefficient is (dv + dv) * 0.5f (compute14u in
+// pd_march.cu, in float).
+template <int REACTION>
+__device__ __forceinline__ void compute32u(const Args32& M, const Slow32& K, const Ctx32& C, int z, uint32_t tm,
+                                           uint32_t t0, uint32_t tp, const Geo32& G, float* __restrict__ un) {
+    const uint32_t lz = C.lm >> (2 * z);
+    const float2 uc = lds2f(t0 + G.s_c);
+    const float uL = lds1f(t0 + G.s_l), uR = lds1f(t0 + G.s_r);
+    const float2 uym = lds2f(t0 + G.s_c - 32), uyp = lds2f(t0 + G.s_c + 32);
+    const float2 uzm = lds2f(tm + G.s_c), uzp = lds2f(tp + G.s_c);
+    const float dh = (C.dv + C.dv) * 0.5f;
+    const float fxl = dh * (uc.x - uL), fxi = dh * (uc.y - uc.x), fxr = dh * (uR - uc.y);
+    const float fy0m = dh * (uc.x - uym.x), fy0p = dh * (uyp.x - uc.x);
+    const float fz0m = dh * (uc.x - uzm.x), fz0p = dh * (uzp.x - uc.x);
+    const float fy1m = dh * (uc.y - uym.y), fy1p = dh * (uyp.y - uc.y);
+    const float fz1m = dh * (uc.y - uzm.y), fz1p = dh * (uzp.y - uc.y);
+    const float ix = M.A.inv_dx2[0], iy = M.A.inv_dx2[1], iz = M.A.inv_dx2[2];
+    float lap0 = 0.0f;
+    lap0 += (fxi - fxl) * ix;
+    lap0 += (fy0p - fy0m) * iy;
+    lap0 += (fz0p - fz0m) * iz;
+    float lap1 = 0.0f;
+    lap1 += (fxr - fxi) * ix;
+    lap1 += (fy1p - fy1m) * iy;
+    lap1 += (fz1p - fz1m) * iz;
+    float r0 = 0.0f, r1 = 0.0f;
+    if (REACTION == PD_REACTION_SURFACE_SINK) {
+        r0 = ((lz >> 16) & 1u) ? M.A.neg_k * uc.x : 0.0f;
+        r1 = ((lz >> 17) & 1u) ? M.A.neg_k * uc.y : 0.0f;
+    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const float* sp = M.A.src + (int64_t)C.c * 512 + z * 64 + G.bp;
+        r0 = sp[0] * M.A.src_factor;
+        r1 = sp[1] * M.A.src_factor;
+    }
+    const float dt = M.A.dt;
+    float out0 = uc.x + dt * lap0 + dt * r0;
+    float out1 = uc.y + dt * lap1 + dt * r1;
+    if (nonfinite32(out0) | nonfinite32(out1)) {
+        const float2 r = slow_pair32<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        out0 = r.x;
+        out1 = r.y;
+    }
+    stg2f(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, true, true);
+}
+
 template <int REACTION>
 __device__ __forceinline__ void compute32(const Args32& M, const Slow32& K, const Ctx32& C, int z, uint32_t tm,
                                           uint32_t t0, uint32_t tp, const Geo32& G, float* __restrict__ un) {
+    if (C.flags & kFlagUnif32) {  // warp-uniform
+        compute32u<REACTION>(M, K, C, z, tm, t0, tp, G, un);
+        return;
+    }
     const uint32_t lz = C.lm >> (2 * z);
     const bool a0 = lz & 1u, a1 = (lz >> 1) & 1u;
     const float2 uc = lds2f(t0 + G.s_c), dc = lds2f(t0 + kDOff32 + G.s_c);
@@ -401,6 +457,10 @@ __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
             "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(
                 e + 128u + 4u * (uint32_t)(lane & 7)),
             "l"(M.desc + cc * 8 + (lane & 7)), "r"((int)(c >= 0 && lane < 8)));
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(
+                e + 164u),
+            "l"(M.dv + cc), "r"((int)(c >= 0 && lane == 0)));
     };
     {
         const int id0 = sched_sync();
@@ -426,7 +486,7 @@ __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
         const int c = (int)ldsu(e0 + 160u);
         const uint32_t lm = c >= 0 ? ldsu(e0 + 4u * (uint32_t)lane) : 0u;
         const int dv = (int)ldsu(e0 + 128u + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
-        Cld = Ctx32{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm};
+        Cld = Ctx32{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm, lds1f(e0 + 164u)};
         Lld = load_ctx32(c, lm, c >= 0 ? dv : -1, G);
         fetch(e1, (int)ldsu(e1 + 160u));
         if (lane == 0) {
@@ -527,6 +587,7 @@ void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, in
     M.desc = p.d_desc;
     M.lm = p.d_lm;
     M.deff = static_cast<const float*>(p.d_deff);
+    M.dv = static_cast<const float*>(p.d_dv);
     M.counter = counter;
     M.zero = 0;
     M.n_all = g->n_chunks;

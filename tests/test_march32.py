@@ -18,6 +18,11 @@ SPECS = {
                             channels=["phi", "u", "D", "u_next", "f"], profile=(0.05, 1.0, 0.0, 60.0),
                             u0=("hash_unit", 4), fp32=True, reaction=("volumetric", "f", "exp"), dt_frac=0.45,
                             steps=40, record=8),
+    # steep sigmoid: D saturates exactly, most chunks take the uniform path
+    "pack64_fp32_unif": dict(dims=3, n=64, box=(0.0, 1.0), geom="pack", pack=(6, 0.05, 0.09, 3),
+                             channels=["phi", "u", "D", "u_next"], profile=(0.05, 1.0, 0.0, 4000.0),
+                             u0=("hash_unit", 2), fp32=True, reaction=("surface_sink", 1.5, 1.0), dt_frac=0.45,
+                             steps=40, record=10),
     "pack56_fp32_walls": dict(dims=3, n=56, box=(0.0, 1.0), geom="pack", pack=(30, 0.07, 0.15, 12),
                               channels=["phi", "u", "D", "u_next"], profile=("anchored", 0.05, 0.95, 200.0, 0.02),
                               u0=("hash_unit", 6), fp32=True, eps=0.5 / 56, reaction=("surface_sink", 2.0, 1.0),
