@@ -133,3 +133,40 @@ def test_fp64_uniform_chunks_equal_reference(name, monkeypatch, ref, cuda):
         a, b = ours.channel_data(c), g.prop(c)
         diff = np.nonzero(a.view(np.uint64) != b.view(np.uint64))
         assert diff[0].size == 0, (c, diff[0][:5], diff[1][:5], a[diff][:5], b[diff][:5])
+
+
+def test_fp64_uniform_chunk_nonfinite_error_and_state(monkeypatch, ref, cuda):
+    """An overflow that starts inside a uniform chunk (the rare path runs with
+    the chunk's dv instead of D_eff from the ring): same numeric_error text
+    and post-error u / u_next as the reference."""
+    from paper_2304_11165_b200 import porediff as pd
+    for k, v in SPECS64.items():
+        monkeypatch.setitem(cases.CASES, k, v)
+    name = "pack64_unif_sink"
+    spec = dict(cases.CASES[name])
+    g = cases.ref_case(name, ref)
+    keys, masks = g.layout()
+    D = g.prop("D")
+    full = np.all(masks == np.uint64(0xFFFFFFFFFFFFFFFF), axis=1)
+    uni = np.nonzero(full & (D.min(axis=1) == D.max(axis=1)) & np.all(keys > 0, axis=1)
+                     & np.all(keys < 7, axis=1))[0]
+    j = int(uni[len(uni) // 2])
+    u = g.prop("u")
+    u[j, 9 * 64 // 2 + 3] = 1e300
+    g.set_prop("u", u)
+    data = {c: g.prop(c) for c in spec["channels"]}
+    dt = 3.0 * dt_of(spec, g.max_diffusivity())
+    spec["steps"] = 40
+    ocfg = oracle_config(spec, dt)
+    ocfg.enforce_stability = 0
+    code, msg, _ = g.run(ocfg, None)
+    assert code == 6, msg
+    geom = pd.GridGeometry.cell_centered_box(spec["n"], *spec["box"], spec["dims"])
+    ours = pd.SparseBlockGrid.from_layout(geom, spec["channels"], keys, masks, data)
+    cfg = sim_config(spec, dt)
+    cfg.enforce_stability = False
+    with pytest.raises(pd.NumericError) as ei:
+        pd.run_simulation(ours, cfg)
+    assert str(ei.value) == msg
+    for c in ("u", "u_next"):
+        assert np.array_equal(ours.channel_data(c).view(np.uint64), g.prop(c).view(np.uint64)), c
