@@ -321,6 +321,13 @@ int pd_field_read_snapshot(const char* path, int dims, int scalar_bytes, int dev
 /* peek_snapshot: header only. */
 int pd_peek_snapshot(const char* path, pd_snapshot_info* info, char* names_buf, size_t names_cap);
 
+/* Work per z chunk layer of a sphere-pack domain without building it
+ * (allocated chunks and active nodes per layer, cc[2] entries each; either
+ * output may be NULL): for work-balanced z-slab cuts. */
+int pd_sphere_pack_layer_work(int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
+                              int64_t n_spheres, const double* centers, const double* radii, double b_low,
+                              double b_up, int device, int64_t* chunks_per_layer, int64_t* active_per_layer);
+
 /* ---- fused multi-GPU halo exchange over peer memory (
  * pd_peer.cu) ---------------------------------------------------------------
  * Replaces the pack -> NCCL send/recv -> unpack exchange (pd_grid_pack_face /

@@ -154,6 +154,8 @@ _SIGNATURES = [
     ("pd_field_write_snapshot", C.c_int, [_P, C.c_char_p]),
     ("pd_field_read_snapshot", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     ("pd_peek_snapshot", C.c_int, [C.c_char_p, C.POINTER(pd_snapshot_info), C.c_char_p, C.c_size_t]),
+    ("pd_sphere_pack_layer_work", C.c_int, [C.c_int, C.POINTER(C.c_int64), _DP, _DP, C.c_int64, _DP, _DP, C.c_double,
+                                            C.c_double, C.c_int, _P, _P]),
     ("pd_grid_make_shareable", C.c_int, [_P]),
     ("pd_grid_ipc_handles", C.c_int, [_P, _P]),
     ("pd_grid_column_ptrs", C.c_int, [_P, C.POINTER(C.c_void_p)]),

@@ -573,6 +573,23 @@ void count_active(pd_grid* g) {
 
 using namespace pdb;
 
+
+namespace pdb {
+// per chunk layer (z): allocated chunks and active nodes of a slot-mask pass
+__global__ void layer_work_kernel(const uint64_t* __restrict__ slot_masks, const int32_t* __restrict__ slot_flag,
+                                  int64_t per_layer, int64_t layers, unsigned long long* __restrict__ chunks,
+                                  unsigned long long* __restrict__ active) {
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (slot >= per_layer * layers) return;
+    if (!slot_flag[slot]) return;
+    const int64_t z = slot / per_layer;
+    unsigned long long a = 0;
+    for (int w = 0; w < 8; ++w) a += (unsigned long long)__popcll(slot_masks[slot * 8 + w]);
+    atomicAdd(chunks + z, 1ull);
+    atomicAdd(active + z, a);
+}
+}  // namespace pdb
+
 extern "C" {
 
 const char* pd_last_error(void) { return t_err.c_str(); }
@@ -888,6 +905,84 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
                               int prop_phi, int device, pd_grid** out) {
     return pd_build_sphere_pack_region(scalar_bytes, size, spacing, origin, n_spheres, centers, radii,
                                        b_low, b_up, nullptr, nullptr, n_props, prop_phi, device, out);
+}
+
+/* Work per chunk layer of a sphere-pack domain without building it: the
+ * band test of build_sparse_grid (same mask pass as the builder), reduced
+ * to allocated chunks and active nodes per z chunk layer (cc[2] entries
+ * each), for work-balanced z-slab cuts. */
+int pd_sphere_pack_layer_work(int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
+                              int64_t n_spheres, const double* centers, const double* radii, double b_low,
+                              double b_up, int device, int64_t* chunks_per_layer, int64_t* active_per_layer) {
+    return guarded([&] {
+        pd_grid tmp;
+        init_geometry(&tmp, 3, scalar_bytes, size, spacing, device);
+        DeviceGuard dg(device);
+        cudaStream_t st = nullptr;
+        PD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        void *d_centers = nullptr, *d_radii = nullptr, *d_cnt = nullptr;
+        uint64_t* slot_masks = nullptr;
+        int32_t* slot_flag = nullptr;
+        struct Free {
+            std::vector<void*> p;
+            cudaStream_t s;
+            ~Free() {
+                for (void* q : p) pd_free(q);
+                if (s) cudaStreamDestroy(s);
+            }
+        } fr{{}, st};
+        PackArgs p;
+        int64_t slots = 1;
+        for (int a = 0; a < 3; ++a) {
+            p.size[a] = size[a];
+            p.spacing[a] = spacing[a];
+            p.origin[a] = origin[a];
+            p.cc[a] = tmp.cc[a];
+            p.rlo[a] = 0;
+            p.rext[a] = tmp.cc[a];
+            slots *= tmp.cc[a];
+        }
+        p.n_spheres = n_spheres;
+        PD_CUDA(pd_malloc(&d_centers, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres * 3)));
+        fr.p.push_back(d_centers);
+        PD_CUDA(pd_malloc(&d_radii, sizeof(double) * (size_t)std::max<int64_t>(1, n_spheres)));
+        fr.p.push_back(d_radii);
+        if (n_spheres > 0) {
+            PD_CUDA(cudaMemcpyAsync(d_centers, centers, sizeof(double) * (size_t)(n_spheres * 3),
+                                    cudaMemcpyHostToDevice, st));
+            PD_CUDA(cudaMemcpyAsync(d_radii, radii, sizeof(double) * (size_t)n_spheres, cudaMemcpyHostToDevice, st));
+        }
+        p.centers = (const double*)d_centers;
+        p.radii = (const double*)d_radii;
+        PD_CUDA(pd_malloc(&slot_masks, sizeof(uint64_t) * (size_t)slots * 8));
+        fr.p.push_back(slot_masks);
+        PD_CUDA(pd_malloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
+        fr.p.push_back(slot_flag);
+        const int64_t layers = tmp.cc[2];
+        PD_CUDA(pd_malloc(&d_cnt, sizeof(unsigned long long) * 2 * (size_t)layers));
+        fr.p.push_back(d_cnt);
+        PD_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 2 * (size_t)layers, st));
+        if (scalar_bytes == 8) {
+            const double eps = std::numeric_limits<double>::epsilon();
+            pack_mask_kernel<double><<<(unsigned)slots, 512, 0, st>>>(p, b_low + eps, b_up - eps, slot_masks,
+                                                                      slot_flag);
+        } else {
+            const float eps = std::numeric_limits<float>::epsilon();
+            pack_mask_kernel<float><<<(unsigned)slots, 512, 0, st>>>(p, (float)b_low + eps, (float)b_up - eps,
+                                                                     slot_masks, slot_flag);
+        }
+        auto* cnt = static_cast<unsigned long long*>(d_cnt);
+        layer_work_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(slot_masks, slot_flag, tmp.cc[0] * tmp.cc[1],
+                                                                           layers, cnt, cnt + layers);
+        PD_CUDA(cudaGetLastError());
+        std::vector<unsigned long long> h((size_t)(2 * layers));
+        PD_CUDA(cudaMemcpyAsync(h.data(), d_cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        PD_CUDA(cudaStreamSynchronize(st));
+        for (int64_t z = 0; z < layers; ++z) {
+            if (chunks_per_layer) chunks_per_layer[z] = (int64_t)h[(size_t)z];
+            if (active_per_layer) active_per_layer[z] = (int64_t)h[(size_t)(layers + z)];
+        }
+    });
 }
 
 int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const double* spacing,

@@ -138,7 +138,7 @@ def exchange_numpy(plan: ExchangePlan, u: np.ndarray, rank: int, world: int, dis
 class Domain:
     """One rank's shard of a sphere-pack domain on its GPU."""
 
-    def __init__(self, n, pack, rank, world, device, dtype=np.float64, exchange=None):
+    def __init__(self, n, pack, rank, world, device, dtype=np.float64, exchange=None, balance=None):
         import torch
 
         from . import porediff as pd
@@ -149,7 +149,15 @@ class Domain:
         self.geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
         cc = [(n + 7) // 8] * 3
         self.cc = cc
-        z0, z1 = slab_bounds(cc[2], world, rank)
+        # cut the z chunk layers at equal prefix sums of work (allocated chunks
+        # per layer; the step costs per chunk), not at equal layer counts
+        if balance is None:
+            balance = os.environ.get("PD_BALANCE", "chunks") if world > 1 else "layers"
+        weights = None
+        if balance in ("chunks", "active"):
+            weights = layer_work(self.geom, pack, dtype, device)[0 if balance == "chunks" else 1]
+        self.balance = balance
+        z0, z1 = slab_bounds(cc[2], world, rank, weights)
         lo = (C.c_int64 * 3)(0, 0, max(0, z0 - 1))
         hi = (C.c_int64 * 3)(cc[0], cc[1], min(cc[2], z1 + 1))
         centers, radii = pack.arrays()
@@ -392,6 +400,23 @@ class Domain:
         n = C.c_int64()
         self.lib.pd_stepper_launch_count(stepper, C.byref(n))
         return int(n.value)
+
+
+def layer_work(geom, pack, dtype=np.float64, device: int = 0):
+    """(allocated chunks, active nodes) per z chunk layer of the sphere-pack
+    domain, from the builder's mask pass without building the grid
+    (pd_sphere_pack_layer_work)."""
+    from . import porediff as pd
+    from ._lib import lib
+    centers, radii = pack.arrays()
+    layers = (geom.size[2] + 7) // 8
+    chunks = np.zeros(layers, np.int64)
+    active = np.zeros(layers, np.int64)
+    pd._check(lib.pd_sphere_pack_layer_work(
+        np.dtype(dtype).itemsize, (C.c_int64 * 3)(*geom.size), (C.c_double * 3)(*geom.spacing),
+        (C.c_double * 3)(*geom.origin), len(radii), centers.ctypes.data_as(C.POINTER(C.c_double)),
+        radii.ctypes.data_as(C.POINTER(C.c_double)), 0.0, math.inf, device, chunks.ctypes.data, active.ctypes.data))
+    return chunks, active
 
 
 def build_domain(n, pack, rank, world, device=0, dtype=np.float64) -> Domain:

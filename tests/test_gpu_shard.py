@@ -331,3 +331,30 @@ def test_fused_peer_push_equals_unsharded(world, n, cuda):
         dev.close()
     lib.pd_stepper_destroy(s_full)
     full.close()
+
+
+def test_layer_work_matches_built_grid_and_balances(cuda):
+    """pd_sphere_pack_layer_work (the builder's mask pass, no grid) gives the
+    built grid's chunks and active nodes per z layer exactly; work-balanced
+    cuts cover every layer once and even out the chunk counts."""
+    from paper_2304_11165_b200 import porediff as pd
+    from paper_2304_11165_b200 import shard
+    from paper_2304_11165_b200 import synthetic as sy
+    n = 96
+    geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
+    pack = sy.SpherePacking.random((0, 0, 0), (1, 1, 1), 50, 0.05, 0.2, 77)
+    chunks, active = shard.layer_work(geom, pack)
+    c, r = pack.arrays()
+    dev = pd.DeviceGrid.sphere_pack(geom, c, r)
+    keys, masks = dev.layout()
+    cc = (n + 7) // 8
+    want_c = np.bincount(keys[:, 2], minlength=cc)
+    pop = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).sum(axis=1)
+    want_a = np.bincount(keys[:, 2], weights=pop, minlength=cc).astype(np.int64)
+    assert np.array_equal(chunks, want_c) and np.array_equal(active, want_a)
+    dev.close()
+    for world in (2, 3, 5):
+        b = [shard.slab_bounds(cc, world, r, chunks) for r in range(world)]
+        assert b[0][0] == 0 and b[-1][1] == cc and all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+        per = [int(chunks[z0:z1].sum()) for z0, z1 in b]
+        assert max(per) - min(per) <= 2 * int(chunks.max())
