@@ -13,15 +13,15 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _build(pd, lib, geom, centers, radii, lo, hi):
+def _build(pd, lib, geom, centers, radii, lo, hi, dtype=np.float64):
     h = C.c_void_p()
     pd._check(lib.pd_build_sphere_pack_region(
-        8, (C.c_int64 * 3)(*geom.size), (C.c_double * 3)(*geom.spacing), (C.c_double * 3)(*geom.origin),
+        np.dtype(dtype).itemsize, (C.c_int64 * 3)(*geom.size), (C.c_double * 3)(*geom.spacing), (C.c_double * 3)(*geom.origin),
         len(radii), centers.ctypes.data_as(C.POINTER(C.c_double)), radii.ctypes.data_as(C.POINTER(C.c_double)),
         0.0, math.inf, (C.c_int64 * 3)(*lo), (C.c_int64 * 3)(*hi), 4, 0, 0, C.byref(h)))
     n = C.c_int64()
     lib.pd_grid_info(h, C.byref(n), None)
-    dev = pd.DeviceGrid(h, geom, np.float64, int(n.value), 4)
+    dev = pd.DeviceGrid(h, geom, dtype, int(n.value), 4)
     dev.populate_diffusion(0, 2, pd.DiffusionProfile(0.02, 1.0, 0.0, 4.0 * geom.size[0]))
     dev.fill_hash(1, 11)
     return dev
@@ -39,8 +39,8 @@ def _stepper(pd, lib, dev, dt, rng=None):
     return h
 
 
-@pytest.mark.parametrize("world,n", [(2, 48), (3, 61)])
-def test_sharded_run_equals_unsharded(world, n, cuda):
+@pytest.mark.parametrize("world,n,dtype", [(2, 48, np.float64), (3, 61, np.float64), (2, 56, np.float32)])
+def test_sharded_run_equals_unsharded(world, n, dtype, cuda):
     import torch
 
     from paper_2304_11165_b200 import porediff as pd
@@ -52,7 +52,7 @@ def test_sharded_run_equals_unsharded(world, n, cuda):
     pk = SpherePacking.random((0, 0, 0), (1, 1, 1), 40, 0.06, 0.14, 99)
     centers, radii = pk.arrays()
     cc = (n + 7) // 8
-    full = _build(pd, lib, geom, centers, radii, (0, 0, 0), (cc, cc, cc))
+    full = _build(pd, lib, geom, centers, radii, (0, 0, 0), (cc, cc, cc), dtype)
     dmax = full.max_active(2)
     dt = 0.45 * pd.stability_dt(geom, dmax)
     steps = 12
@@ -67,7 +67,7 @@ def test_sharded_run_equals_unsharded(world, n, cuda):
     shards = []
     for r in range(world):
         z0, z1 = shard.slab_bounds(cc, world, r)
-        dev = _build(pd, lib, geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)))
+        dev = _build(pd, lib, geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)), dtype)
         keys, _ = dev.layout()
         plan = shard.exchange_plan(keys, z0, z1, r, world)
         s = _stepper(pd, lib, dev, dt, (plan.begin, plan.end))
@@ -87,7 +87,7 @@ def test_sharded_run_equals_unsharded(world, n, cuda):
             for lst, face, to in ((plan.send_down, shard.FACE_ZLO, r - 1), (plan.send_up, shard.FACE_ZHI, r + 1)):
                 if len(lst) == 0:
                     continue
-                buf = torch.empty((len(lst), 64), dtype=torch.float64, device="cuda")
+                buf = torch.empty((len(lst), 64), dtype=torch.float64 if dtype == np.float64 else torch.float32, device="cuda")
                 o = ords(lst)
                 pd._check(lib.pd_grid_pack_face(dev.h, 1, C.c_void_p(o.data_ptr()), len(lst), face,
                                                 C.c_void_p(buf.data_ptr())))
@@ -112,7 +112,7 @@ def test_sharded_run_equals_unsharded(world, n, cuda):
         for i in range(plan.begin, plan.end):
             l = (int(keys[i, 2]) * cc + int(keys[i, 1])) * cc + int(keys[i, 0])
             j = pos[l]
-            assert np.array_equal(u[i].view(np.uint64), u_full[j].view(np.uint64)), (i, keys[i])
+            assert np.array_equal(u[i], u_full[j]) and np.array_equal(u[i].view(np.uint8), u_full[j].view(np.uint8)), (i, keys[i])
             covered += 1
     assert covered == len(keys_full)
     for dev, plan, s, _ in shards:
