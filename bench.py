@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=2048, help="box edge in nodes")
+    ap.add_argument("--n", "--box", dest="n", type=int, default=2048, help="box edge in nodes")
     ap.add_argument("--psi", type=float, default=0.2, help="target porosity")
     ap.add_argument("--radius-vox", type=float, default=128.0)
     ap.add_argument("--seed", type=int, default=12345)
@@ -230,9 +230,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for exercising the N > 1 path on a one-GPU box: every rank on
+    # cuda:0 (PD_BENCH_SAME_GPU=1) with a gloo control plane
+    # (PD_DIST_BACKEND=gloo); the peer exchange itself is CUDA IPC either way
+    if os.environ.get("PD_BENCH_SAME_GPU") == "1":
+        local = 0
+    backend = os.environ.get("PD_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     pack = workload(args)
     dom = shard.build_domain(args.n, pack, rank, world, device=local)
@@ -259,8 +269,8 @@ def run_ours(args):
     launches += dom.extra_launches_per_step * args.steps
     # exact global diagnostics of the final state (all ranks take part)
     diag = dom.diagnostics(stepper)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    act_t = torch.tensor([dom.owned_active], dtype=torch.float64, device="cuda")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    act_t = torch.tensor([dom.owned_active], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.all_reduce(act_t, op=dist.ReduceOp.SUM)
@@ -275,6 +285,7 @@ def run_ours(args):
     achieved = dom.owned_active * BYTES_PER_UPDATE / (kern_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic(args.n)
 
+    chunks_total = int(dom.total_chunks(world))  # a collective: every rank takes part
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = run_e2e(args, pack)
@@ -295,7 +306,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (device-built sphere pack)",
             "config": config_dict(args, world),
-            "active_nodes": int(active), "chunks": int(dom.total_chunks(world)),
+            "active_nodes": int(active), "chunks": chunks_total,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
                          "algorithmic_bytes_per_launch": dom.owned_active * BYTES_PER_UPDATE,
