@@ -170,3 +170,27 @@ def test_fp64_uniform_chunk_nonfinite_error_and_state(monkeypatch, ref, cuda):
     assert str(ei.value) == msg
     for c in ("u", "u_next"):
         assert np.array_equal(ours.channel_data(c).view(np.uint64), g.prop(c).view(np.uint64)), c
+
+
+def test_fp64_march_128_pack_equals_reference(monkeypatch, ref, cuda):
+    """A C5-shaped case at 128^3 (overlapping spheres, sigmoid D with exact
+    saturation, surface sink): thousands of chunks through the march kernel's
+    claim pipeline, uniform and generic chunks mixed, against the reference."""
+    from paper_2304_11165_b200 import porediff as pd
+    spec = dict(dims=3, n=128, box=(0.0, 1.0), geom="pack", pack=(60, 0.04, 0.09, 2048),
+                channels=["phi", "u", "D", "u_next"], profile=(0.0, 1.0, 0.0, 512.0), u0=("hash_unit", 1),
+                reaction=("surface_sink", 1.0, 1.0), dt_frac=0.4, steps=30, record=15)
+    monkeypatch.setitem(cases.CASES, "pack128", spec)
+    g = cases.ref_case("pack128", ref)
+    keys, masks = g.layout()
+    assert len(keys) > 2000
+    data = {c: g.prop(c) for c in spec["channels"]}
+    dt = dt_of(spec, g.max_diffusivity())
+    geom = pd.GridGeometry.cell_centered_box(128, 0.0, 1.0, 3)
+    ours = pd.SparseBlockGrid.from_layout(geom, spec["channels"], keys, masks, data)
+    code, msg, rows = g.run(oracle_config(spec, dt), None)
+    assert code == 0, msg
+    res = pd.run_simulation(ours, sim_config(spec, dt))
+    assert [tuple(r) for r in rows] == [(d.step, d.time, d.total_mass, d.min_u, d.max_u) for d in res.diagnostics]
+    for c in ("u", "u_next"):
+        assert np.array_equal(ours.channel_data(c).view(np.uint64), g.prop(c).view(np.uint64)), c
