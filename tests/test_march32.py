@@ -194,3 +194,30 @@ def test_fp64_march_128_pack_equals_reference(monkeypatch, ref, cuda):
     assert [tuple(r) for r in rows] == [(d.step, d.time, d.total_mass, d.min_u, d.max_u) for d in res.diagnostics]
     for c in ("u", "u_next"):
         assert np.array_equal(ours.channel_data(c).view(np.uint64), g.prop(c).view(np.uint64)), c
+
+
+@pytest.mark.parametrize("dtype,n", [(np.float64, 48), (np.float32, 40), (np.float64, 37)])
+def test_free_box_dense_kernel_equals_reference(dtype, n, ref, cuda, monkeypatch):
+    """A free box (every node active and fluid, one D, no-flux box — the FRAP
+    fit's probes): interior chunks take the uniform path, box-boundary chunks
+    the generic one (n = 37: partial chunks); equal to the reference."""
+    from paper_2304_11165_b200 import porediff as pd
+    geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
+    sdf = np.ones(n ** 3)
+    rg = ref.grid_from_sdf(geom.size, geom.spacing, geom.origin, sdf, tbytes=np.dtype(dtype).itemsize)
+    keys, masks = rg.layout()
+    D = np.full((len(keys), 512), 0.7, dtype)
+    rg.set_prop("D", D)
+    rg.fill_hash("u", 5)
+    data = {c: rg.prop(c) for c in pd.solver_channels()}
+    dt = 0.45 * pd.stability_dt(geom, 0.7)
+    ours = pd.SparseBlockGrid.from_layout(geom, pd.solver_channels(), keys, masks, data, dtype)
+    from oracle.pyoracle import make_config
+    code, msg, rows = rg.run(make_config(dt, 25, record_every=5), None)
+    assert code == 0, msg
+    cfg = pd.SimulationConfig(dt=dt, n_steps=25, record_every=5)
+    res = pd.run_simulation(ours, cfg)
+    assert [tuple(r) for r in rows] == [(d.step, d.time, d.total_mass, d.min_u, d.max_u) for d in res.diagnostics]
+    view = np.uint64 if dtype == np.float64 else np.uint32
+    for c in ("u", "u_next"):
+        assert np.array_equal(ours.channel_data(c).view(view), rg.prop(c).view(view)), c
