@@ -187,6 +187,7 @@ struct MarchPlan {
     int grid = 0;
     int64_t n = 0;
     bool ready = false;
+    bool half = false;             // FP64 D_eff stored halved (face coefficient h_a + h_b, pd_march.cu)
     struct Sub {  // sub-range schedules (overlapped multi-GPU stepping)
         int64_t begin = 0, end = 0, n = 0;
         int32_t* d_stream = nullptr;

@@ -136,13 +136,19 @@ __device__ __noinline__ double slow_node(const SlowConsts& K, double u_c, double
 }
 
 // Face flux F(a|b) shared by both endpoints; 0 when either side is not fluid.
+// HALF: the ring holds D_eff / 2 (plan.half), so (d_a + d_b) * 0.5 is
+// h_a + h_b — the same double, since halving is exact and commutes with
+// rounding for normal values (the plan checks every fluid D >= 2^-1021) —
+// and the 0.5 multiply disappears.
+template <bool HALF>
 __device__ __forceinline__ double face(double da, double db, double ua, double ub) {
     const double s = da + db;
-    const double f = (s * 0.5) * (ub - ua);
+    const double f = (HALF ? s : s * 0.5) * (ub - ua);
     return ((unsigned)__double2hiint(s) == kSentHi) ? 0.0 : f;
 }
+template <bool HALF>
 __device__ __forceinline__ double fface(double da, double db, double ua, double ub) {
-    return ((da + db) * 0.5) * (ub - ua);
+    return (HALF ? (da + db) : (da + db) * 0.5) * (ub - ua);
 }
 
 // One plane tile: u and D_eff of one z-plane of a chunk, rows y = -1..8 of
@@ -375,19 +381,24 @@ struct ChunkCtx14 {
 // Rare path (Dirichlet-exposed chunk, or a huge / non-finite fast result):
 // re-reads the pair's operands from the ring and applies the exact generic
 // update and the error / mass flags (solver.hpp:360-455, 250-260, 514-515).
-template <int REACTION>
+template <int REACTION, bool HALF>
 __device__ __noinline__ double2 pair_slow14(const MarchArgs& M, const SlowConsts& K, ChunkCtx14 C, int z,
                                             uint32_t tm, uint32_t t0, uint32_t tp, LaneGeo G, double out0,
                                             double out1) {
     const bool un = (C.flags & kFlagUnif) != 0;  // no D_eff in the ring: every d is dv
     const double2 vv = make_double2(C.dv, C.dv);
-    const double2 uc = lds2(t0 + G.s_c), dc = un ? vv : lds2(t0 + kDOff + G.s_c);
-    const double uL = lds1(t0 + G.s_l), dL = un ? C.dv : lds1(t0 + kDOff + G.s_l);
-    const double uR = lds1(t0 + G.s_r), dR = un ? C.dv : lds1(t0 + kDOff + G.s_r);
-    const double2 uym = lds2(t0 + G.s_c - 64), dym = un ? vv : lds2(t0 + kDOff + G.s_c - 64);
-    const double2 uyp = lds2(t0 + G.s_c + 64), dyp = un ? vv : lds2(t0 + kDOff + G.s_c + 64);
-    const double2 uzm = lds2(tm + G.s_c), dzm = un ? vv : lds2(tm + kDOff + G.s_c);
-    const double2 uzp = lds2(tp + G.s_c), dzp = un ? vv : lds2(tp + kDOff + G.s_c);
+    const double2 uc = lds2(t0 + G.s_c), dc0 = un ? vv : lds2(t0 + kDOff + G.s_c);
+    const double uL = lds1(t0 + G.s_l), dL0 = un ? C.dv : lds1(t0 + kDOff + G.s_l);
+    const double uR = lds1(t0 + G.s_r), dR0 = un ? C.dv : lds1(t0 + kDOff + G.s_r);
+    const double2 uym = lds2(t0 + G.s_c - 64), dym0 = un ? vv : lds2(t0 + kDOff + G.s_c - 64);
+    const double2 uyp = lds2(t0 + G.s_c + 64), dyp0 = un ? vv : lds2(t0 + kDOff + G.s_c + 64);
+    const double2 uzm = lds2(tm + G.s_c), dzm0 = un ? vv : lds2(tm + kDOff + G.s_c);
+    const double2 uzp = lds2(tp + G.s_c), dzp0 = un ? vv : lds2(tp + kDOff + G.s_c);
+    // the ring / dv hold D_eff / 2 under HALF: the generic update needs D (exact doubling)
+    auto dd = [](double h) { return HALF ? h + h : h; };
+    auto dd2 = [&](double2 h) { return make_double2(dd(h.x), dd(h.y)); };
+    const double2 dc = dd2(dc0), dym = dd2(dym0), dyp = dd2(dyp0), dzm = dd2(dzm0), dzp = dd2(dzp0);
+    const double dL = dd(dL0), dR = dd(dR0);
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
     const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
     double src0 = 0.0, src1 = 0.0;
@@ -420,7 +431,7 @@ __device__ __noinline__ void push_pair14(const MarchArgs& M, const ChunkCtx14& C
 // coefficient (dv + dv) * 0.5 — the reference's (d_c + d_n) * 0.5 with both
 // sides dv — so only u comes from the ring. Same expression order as the
 // interior path of compute14.
-template <int REACTION, bool PUSH>
+template <int REACTION, bool PUSH, bool HALF>
 __device__ __forceinline__ void compute14u(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
                                            const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
                                            const LaneGeo& G, double* __restrict__ un, bool& pushed) {
@@ -429,7 +440,7 @@ __device__ __forceinline__ void compute14u(const MarchArgs& M, const SlowConsts&
     const double uL = lds1(t0 + G.s_l), uR = lds1(t0 + G.s_r);
     const double2 uym = lds2(t0 + G.s_c - 64), uyp = lds2(t0 + G.s_c + 64);
     const double2 uzm = lds2(tm + G.s_c), uzp = lds2(tp + G.s_c);
-    const double dh = (C.dv + C.dv) * 0.5;
+    const double dh = HALF ? C.dv + C.dv : (C.dv + C.dv) * 0.5;
     const double fxl = dh * (uc.x - uL), fxi = dh * (uc.y - uc.x), fxr = dh * (uR - uc.y);
     const double fy0m = dh * (uc.x - uym.x), fy0p = dh * (uyp.x - uc.x);
     const double fz0m = dh * (uc.x - uzm.x), fz0p = dh * (uzp.x - uc.x);
@@ -455,7 +466,7 @@ __device__ __forceinline__ void compute14u(const MarchArgs& M, const SlowConsts&
     double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
     double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
     if (huge(out0) | huge(out1)) {
-        const double2 r = pair_slow14<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        const double2 r = pair_slow14<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
         out1 = r.y;
     }
@@ -466,12 +477,12 @@ __device__ __forceinline__ void compute14u(const MarchArgs& M, const SlowConsts&
     }
 }
 
-template <int REACTION, bool PUSH>
+template <int REACTION, bool PUSH, bool HALF>
 __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
                                           const ChunkCtx14& C, int z, uint32_t tm, uint32_t t0, uint32_t tp,
                                           const LaneGeo& G, double* __restrict__ un, bool& pushed) {
     if (C.flags & kFlagUnif) {  // warp-uniform
-        compute14u<REACTION, PUSH>(M, K, Q, C, z, tm, t0, tp, G, un, pushed);
+        compute14u<REACTION, PUSH, HALF>(M, K, Q, C, z, tm, t0, tp, G, un, pushed);
         return;
     }
     const uint32_t lz = C.lm >> (2 * z);
@@ -486,29 +497,29 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
     double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
     const bool interior = (C.flags >> (8 + z)) & 1;  // warp-uniform: no walls, no substitution
     if (interior) {
-        fxl = fface(dL, dc.x, uL, uc.x);
-        fxi = fface(dc.x, dc.y, uc.x, uc.y);
-        fxr = fface(dc.y, dR, uc.y, uR);
-        fy0m = fface(dym.x, dc.x, uym.x, uc.x);
-        fy0p = fface(dc.x, dyp.x, uc.x, uyp.x);
-        fz0m = fface(dzm.x, dc.x, uzm.x, uc.x);
-        fz0p = fface(dc.x, dzp.x, uc.x, uzp.x);
-        fy1m = fface(dym.y, dc.y, uym.y, uc.y);
-        fy1p = fface(dc.y, dyp.y, uc.y, uyp.y);
-        fz1m = fface(dzm.y, dc.y, uzm.y, uc.y);
-        fz1p = fface(dc.y, dzp.y, uc.y, uzp.y);
+        fxl = fface<HALF>(dL, dc.x, uL, uc.x);
+        fxi = fface<HALF>(dc.x, dc.y, uc.x, uc.y);
+        fxr = fface<HALF>(dc.y, dR, uc.y, uR);
+        fy0m = fface<HALF>(dym.x, dc.x, uym.x, uc.x);
+        fy0p = fface<HALF>(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = fface<HALF>(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = fface<HALF>(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = fface<HALF>(dym.y, dc.y, uym.y, uc.y);
+        fy1p = fface<HALF>(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = fface<HALF>(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = fface<HALF>(dc.y, dzp.y, uc.y, uzp.y);
     } else {
-        fxl = face(dL, dc.x, uL, uc.x);
-        fxi = face(dc.x, dc.y, uc.x, uc.y);
-        fxr = face(dc.y, dR, uc.y, uR);
-        fy0m = face(dym.x, dc.x, uym.x, uc.x);
-        fy0p = face(dc.x, dyp.x, uc.x, uyp.x);
-        fz0m = face(dzm.x, dc.x, uzm.x, uc.x);
-        fz0p = face(dc.x, dzp.x, uc.x, uzp.x);
-        fy1m = face(dym.y, dc.y, uym.y, uc.y);
-        fy1p = face(dc.y, dyp.y, uc.y, uyp.y);
-        fz1m = face(dzm.y, dc.y, uzm.y, uc.y);
-        fz1p = face(dc.y, dzp.y, uc.y, uzp.y);
+        fxl = face<HALF>(dL, dc.x, uL, uc.x);
+        fxi = face<HALF>(dc.x, dc.y, uc.x, uc.y);
+        fxr = face<HALF>(dc.y, dR, uc.y, uR);
+        fy0m = face<HALF>(dym.x, dc.x, uym.x, uc.x);
+        fy0p = face<HALF>(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = face<HALF>(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = face<HALF>(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = face<HALF>(dym.y, dc.y, uym.y, uc.y);
+        fy1p = face<HALF>(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = face<HALF>(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = face<HALF>(dc.y, dzp.y, uc.y, uzp.y);
     }
     double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
     lap0 += (fxi - fxl) * Q.ix;
@@ -534,7 +545,7 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
         if (sentinel(dc.y)) out1 = uc.y;
     }
     if ((C.flags & kFlagDirichlet) || ((a0 && huge(out0)) | (a1 && huge(out1)))) {
-        const double2 r = pair_slow14<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        const double2 r = pair_slow14<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
         out1 = r.y;
     }
@@ -545,7 +556,7 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
     }
 }
 
-template <int REACTION, bool PUSH>
+template <int REACTION, bool PUSH, bool HALF>
 __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchArgs M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SlowConsts K;
@@ -676,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
             cp_wait<kAhead14>();
             __syncwarp();
             const uint32_t b = base + (uint32_t)z;
-            compute14<REACTION, PUSH>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes, sb + ((b + 1u) & 7u) * kTileBytes,
+            compute14<REACTION, PUSH, HALF>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes, sb + ((b + 1u) & 7u) * kTileBytes,
                                       sb + ((b + 2u) & 7u) * kTileBytes, G, un, pushed);
             __syncwarp();
             issue_next();
@@ -833,14 +844,18 @@ void mark_uniform(pd_grid* g, MarchPlan* plan, B sent_bits) {
     PD_CUDA(cudaGetLastError());
 }
 
+// D_eff = fluid ? D * (half ? 0.5 : 1) : -inf. bad[0] counts fluid nodes with
+// a non-finite D (march disabled), bad[1] those with |D| < 2^-1021, where
+// halving would not be exact (the plan keeps D unhalved then).
 __global__ void deff_kernel(const double* __restrict__ dcol, const uint64_t* __restrict__ fluid,
-                            int64_t n_slots, double* __restrict__ deff, unsigned long long* bad) {
+                            int64_t n_slots, double* __restrict__ deff, unsigned long long* bad, int half) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_slots) return;
     const bool fl = (fluid[i >> 6] >> (i & 63)) & 1ull;
     const double v = dcol[i];
-    deff[i] = fl ? v : sent();
+    deff[i] = fl ? (half ? v * 0.5 : v) : sent();
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
+    if (fl && fabs(v) < 0x1p-1021) atomicAdd(bad + 1, 1ull);
 }
 
 void march_free(MarchPlan* p) {
@@ -940,19 +955,31 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
         plan->d_deff = deff;
         sentinel_fill_kernel<<<1, 512, 0, g->stream>>>(deff + slots);
         unsigned long long* d_bad = nullptr;
-        PD_CUDA(pd_malloc(&d_bad, sizeof(unsigned long long)));
-        PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
+        PD_CUDA(pd_malloc(&d_bad, 2 * sizeof(unsigned long long)));
+        PD_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(unsigned long long), g->stream));
+        static const int half_env = [] {
+            const char* e = getenv("PD_MARCH_HALF");
+            return e ? atoi(e) : 1;
+        }();
         deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>((const double*)d_dcol, d_fluid, slots,
-                                                                            deff, d_bad);
+                                                                            deff, d_bad, half_env);
         PD_CUDA(cudaGetLastError());
-        unsigned long long bad = 0;
-        PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
+        unsigned long long bad[2] = {0, 0};
+        PD_CUDA(cudaMemcpyAsync(bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
         PD_CUDA(cudaStreamSynchronize(g->stream));
-        pd_free(d_bad);
-        if (bad) {  // non-finite D on a fluid node: keep the exact tile kernel
+        if (bad[0]) {  // non-finite D on a fluid node: keep the exact tile kernel
+            pd_free(d_bad);
             march_free(plan);
             return;
         }
+        plan->half = half_env && !bad[1];
+        if (half_env && bad[1]) {  // tiny D somewhere: store D unhalved
+            PD_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(unsigned long long), g->stream));
+            deff_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, g->stream>>>((const double*)d_dcol, d_fluid,
+                                                                                slots, deff, d_bad, 0);
+            PD_CUDA(cudaGetLastError());
+        }
+        pd_free(d_bad);
         mark_uniform<unsigned long long>(g, plan, 0xFFF0000000000000ull);
     }
     const int64_t n = end - begin;
@@ -1014,19 +1041,26 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     if (pl && ver != 14) fail(PD_E_INPUT, "the fused peer halo push needs march v14 (PD_MARCH_V unset)");
     {
         constexpr size_t bytes = (size_t)kWarpBytes14 * kWarps;
-        static const KernT table[2][3] = {
-            {ftcs_march14_kernel<0, false>, ftcs_march14_kernel<1, false>, ftcs_march14_kernel<2, false>},
-            {ftcs_march14_kernel<0, true>, ftcs_march14_kernel<1, true>, ftcs_march14_kernel<2, true>}};
+        static const KernT table[2][2][3] = {  // [half][push][reaction]
+            {{ftcs_march14_kernel<0, false, false>, ftcs_march14_kernel<1, false, false>,
+              ftcs_march14_kernel<2, false, false>},
+             {ftcs_march14_kernel<0, true, false>, ftcs_march14_kernel<1, true, false>,
+              ftcs_march14_kernel<2, true, false>}},
+            {{ftcs_march14_kernel<0, false, true>, ftcs_march14_kernel<1, false, true>,
+              ftcs_march14_kernel<2, false, true>},
+             {ftcs_march14_kernel<0, true, true>, ftcs_march14_kernel<1, true, true>,
+              ftcs_march14_kernel<2, true, true>}}};
         static bool attr_set = false;
         if (!attr_set) {
-            for (auto& row : table)
-                for (auto k : row)
+            for (auto& half : table)
+                for (auto& row : half)
+                    for (auto k : row)
                     PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
             attr_set = true;
         }
         int sms = 148;
         PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        table[pl ? 1 : 0][r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);  // [push][reaction]
+        table[p.half ? 1 : 0][pl ? 1 : 0][r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);
     }
     PD_CUDA(cudaGetLastError());
 }
