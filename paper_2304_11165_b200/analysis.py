@@ -179,7 +179,7 @@ def frap_fit_objective(reference: FrapExperiment, box_geometry: pd.GridGeometry,
                                 n_samples if n_samples > 0 else len(reference.curve), dt)
         candidate = run_frap(grid, box_bleach, d_candidate, schedule)
     finally:
-        grid.close()
+        grid.close(keep=False)  # a probe: its fields are not needed
     total = 0.0
     for s in reference.curve:
         diff = interp_curve(candidate.curve, s.time) - s.recovery

@@ -587,9 +587,15 @@ class SparseBlockGrid:
             for off in np.nonzero(act[j])[0]:
                 yield tuple(int(v) for v in idx[j, off]), j, int(off)
 
-    def close(self):
+    def close(self, keep: bool = True):
+        """Drop the device mirror. keep=True first pulls every property the
+        device advanced, so the host grid stays the full state; keep=False
+        discards them (temporary grids, e.g. the D_eff fit's free boxes)."""
         if self._dev is not None:
-            self._sync_host()
+            if keep:
+                self._sync_host()
+            else:
+                self._dev_newer = set()
             self._dev.close()
             self._dev = None
             self._host_newer = True
