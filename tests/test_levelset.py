@@ -142,3 +142,40 @@ def test_image_to_grid_pipeline_bitwise(ref, cuda):
     rg_b = ref.grid_from_sdf(geom.size, geom.spacing, geom.origin, phi, -0.05, 0.5)
     kb, mb = rg_b.layout()
     assert np.array_equal(grid_b.keys(), kb) and np.array_equal(grid_b.masks(), mb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(8))
+def test_random_masks_through_the_level_set_stage(seed, ref, cuda):
+    """Seeded random images (random-phase GRF-like masks, anisotropic voxels,
+    odd box sizes, 2-D and 3-D, FP64 / FP32): opening with a random window
+    and redistancing with random options, each bitwise against the
+    reference (the z-march sweep for 3-D, the per-node sweep for 2-D)."""
+    from paper_2304_11165_b200 import levelset as ls
+    r = np.random.default_rng(500 + seed)
+    dims = 3 if seed % 4 else 2
+    size = tuple(int(v) for v in r.integers(9, 40, dims))
+    if dims == 2:
+        size = tuple(int(v) * 2 for v in size)
+    vox = tuple(float(v) for v in r.uniform(0.5, 1.5, dims) / 40)
+    k = r.normal(size=(6, dims)) * 6.0
+    ph = r.uniform(0, 2 * np.pi, 6)
+    grids = np.meshgrid(*[np.arange(s) for s in size], indexing="ij")
+    field = sum(np.cos(sum(k[m, a] * grids[a] / size[a] for a in range(dims)) + ph[m]) for m in range(6))
+    bits = (field > np.quantile(field, r.uniform(0.3, 0.7))).astype(np.uint8)
+    bits = np.ascontiguousarray(bits.transpose(tuple(range(dims))[::-1])).reshape(-1)  # axis 0 fastest
+    dtype = np.float32 if seed % 3 == 2 else np.float64
+    mask = ls.VoxelMask(size, vox, bits)
+    ind = ls.mask_to_indicator(mask, dtype)
+    geom = ind.geom
+    w = int(r.integers(1, 4))
+    opened = ls.filter_thin_features(ind, w)
+    code, msg, want = ref.field_filter_thin(geom.size, geom.spacing, np.where(bits > 0, 1.0, -1.0).astype(dtype), w)
+    assert code == 0, msg
+    got = opened.download()
+    assert np.array_equal(got, want)
+    if np.all(got > 0) or np.all(got < 0):
+        return  # the opening removed the interface: nothing to redistance
+    opts = (int(r.integers(5, 200)), float(r.choice([1e-3, 1e-5])), float(r.uniform(0.2, 0.8)),
+            4.0, float(r.uniform(3.0, 8.0)), int(r.integers(0, 2)))
+    _compare(ref, geom, got, opts, dtype)
