@@ -187,7 +187,7 @@ struct MarchPlan {
     int grid = 0;
     int64_t n = 0;
     bool ready = false;
-    bool half = false;             // FP64 D_eff stored halved (face coefficient h_a + h_b, pd_march.cu)
+    bool half = false;             // D_eff stored halved (face coefficient h_a + h_b, pd_march*.cu)
     struct Sub {  // sub-range schedules (overlapped multi-GPU stepping)
         int64_t begin = 0, end = 0, n = 0;
         int32_t* d_stream = nullptr;
@@ -208,7 +208,7 @@ void march_launch(pd_grid* g, MarchPlan& plan, const StepArgs<double>& a, int re
                   const PeerLaunch* pl = nullptr);
 void march_push_flags(pd_grid* g, MarchPlan& p, const int32_t* d_ord);
 // 3-D FP32 grids (pd_march32.cu)
-bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void** out);
+bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void** out, bool* half);
 void march32_launch(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction);
 void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction, const int32_t* sched,
                           int64_t n, int* counter);

@@ -941,7 +941,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
     const int64_t slots = n_all * 512;
     PD_CUDA(pd_malloc(&plan->d_counter, sizeof(int) * 1024));
     if (g->tbytes == 4) {
-        if (!march32_deff(g, d_dcol, d_fluid, &plan->d_deff)) {
+        if (!march32_deff(g, d_dcol, d_fluid, &plan->d_deff, &plan->half)) {
             march_free(plan);  // non-finite D on a fluid node: keep the exact tile kernel
             return;
         }

@@ -128,13 +128,16 @@ __device__ __forceinline__ void stg2f(float* p, float a, float b, bool a0, bool 
         : "memory");
 }
 
+// HALF: the ring holds D_eff / 2 (see face<HALF> in pd_march.cu)
+template <bool HALF>
 __device__ __forceinline__ float face32(float da, float db, float ua, float ub) {
     const float s = da + db;
-    const float f = (s * 0.5f) * (ub - ua);
+    const float f = (HALF ? s : s * 0.5f) * (ub - ua);
     return sent32(s) ? 0.0f : f;
 }
+template <bool HALF>
 __device__ __forceinline__ float fface32(float da, float db, float ua, float ub) {
-    return ((da + db) * 0.5f) * (ub - ua);
+    return (HALF ? (da + db) : (da + db) * 0.5f) * (ub - ua);
 }
 
 // Exact generic node update (solver.hpp:360-441) in float.
@@ -231,18 +234,22 @@ __device__ __forceinline__ void issue32(uint32_t st, const float* __restrict__ u
 
 // Rare path: Dirichlet-exposed chunk (whole chunk exact) or a non-finite fast
 // result (re-derived exactly), then the reference's error flags.
-template <int REACTION>
+template <int REACTION, bool HALF>
 __device__ __noinline__ float2 slow_pair32(const Args32& M, const Slow32& K, Ctx32 C, int z, uint32_t tm, uint32_t t0,
                                            uint32_t tp, Geo32 G, float out0, float out1) {
     const bool un = (C.flags & kFlagUnif32) != 0;  // no D_eff in the ring: every d is dv
     const float2 vv = make_float2(C.dv, C.dv);
-    const float2 uc = lds2f(t0 + G.s_c), dc = un ? vv : lds2f(t0 + kDOff32 + G.s_c);
-    const float uL = lds1f(t0 + G.s_l), dL = un ? C.dv : lds1f(t0 + kDOff32 + G.s_l);
-    const float uR = lds1f(t0 + G.s_r), dR = un ? C.dv : lds1f(t0 + kDOff32 + G.s_r);
-    const float2 uym = lds2f(t0 + G.s_c - 32), dym = un ? vv : lds2f(t0 + kDOff32 + G.s_c - 32);
-    const float2 uyp = lds2f(t0 + G.s_c + 32), dyp = un ? vv : lds2f(t0 + kDOff32 + G.s_c + 32);
-    const float2 uzm = lds2f(tm + G.s_c), dzm = un ? vv : lds2f(tm + kDOff32 + G.s_c);
-    const float2 uzp = lds2f(tp + G.s_c), dzp = un ? vv : lds2f(tp + kDOff32 + G.s_c);
+    const float2 uc = lds2f(t0 + G.s_c), dc0 = un ? vv : lds2f(t0 + kDOff32 + G.s_c);
+    const float uL = lds1f(t0 + G.s_l), dL0 = un ? C.dv : lds1f(t0 + kDOff32 + G.s_l);
+    const float uR = lds1f(t0 + G.s_r), dR0 = un ? C.dv : lds1f(t0 + kDOff32 + G.s_r);
+    const float2 uym = lds2f(t0 + G.s_c - 32), dym0 = un ? vv : lds2f(t0 + kDOff32 + G.s_c - 32);
+    const float2 uyp = lds2f(t0 + G.s_c + 32), dyp0 = un ? vv : lds2f(t0 + kDOff32 + G.s_c + 32);
+    const float2 uzm = lds2f(tm + G.s_c), dzm0 = un ? vv : lds2f(tm + kDOff32 + G.s_c);
+    const float2 uzp = lds2f(tp + G.s_c), dzp0 = un ? vv : lds2f(tp + kDOff32 + G.s_c);
+    auto dd = [](float h) { return HALF ? h + h : h; };  // D from D/2 (exact)
+    auto dd2 = [&](float2 h) { return make_float2(dd(h.x), dd(h.y)); };
+    const float2 dc = dd2(dc0), dym = dd2(dym0), dyp = dd2(dyp0), dzm = dd2(dzm0), dzp = dd2(dzp0);
+    const float dL = dd(dL0), dR = dd(dR0);
     const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
     const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
     float src0 = 0.0f, src1 = 0.0f;
@@ -280,7 +287,7 @@ __device__ __noinline__ float2 slow_pair32(const Args32& M, const Slow32& K, Ctx
 
 // Uniform chunk: every face coefficient is (dv + dv) * 0.5f (compute14u in
 // pd_march.cu, in float).
-template <int REACTION>
+template <int REACTION, bool HALF>
 __device__ __forceinline__ void compute32u(const Args32& M, const Slow32& K, const Ctx32& C, int z, uint32_t tm,
                                            uint32_t t0, uint32_t tp, const Geo32& G, float* __restrict__ un) {
     const uint32_t lz = C.lm >> (2 * z);
@@ -288,7 +295,7 @@ __device__ __forceinline__ void compute32u(const Args32& M, const Slow32& K, con
     const float uL = lds1f(t0 + G.s_l), uR = lds1f(t0 + G.s_r);
     const float2 uym = lds2f(t0 + G.s_c - 32), uyp = lds2f(t0 + G.s_c + 32);
     const float2 uzm = lds2f(tm + G.s_c), uzp = lds2f(tp + G.s_c);
-    const float dh = (C.dv + C.dv) * 0.5f;
+    const float dh = HALF ? C.dv + C.dv : (C.dv + C.dv) * 0.5f;
     const float fxl = dh * (uc.x - uL), fxi = dh * (uc.y - uc.x), fxr = dh * (uR - uc.y);
     const float fy0m = dh * (uc.x - uym.x), fy0p = dh * (uyp.x - uc.x);
     const float fz0m = dh * (uc.x - uzm.x), fz0p = dh * (uzp.x - uc.x);
@@ -316,18 +323,18 @@ __device__ __forceinline__ void compute32u(const Args32& M, const Slow32& K, con
     float out0 = uc.x + dt * lap0 + dt * r0;
     float out1 = uc.y + dt * lap1 + dt * r1;
     if (nonfinite32(out0) | nonfinite32(out1)) {
-        const float2 r = slow_pair32<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        const float2 r = slow_pair32<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
         out1 = r.y;
     }
     stg2f(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, true, true);
 }
 
-template <int REACTION>
+template <int REACTION, bool HALF>
 __device__ __forceinline__ void compute32(const Args32& M, const Slow32& K, const Ctx32& C, int z, uint32_t tm,
                                           uint32_t t0, uint32_t tp, const Geo32& G, float* __restrict__ un) {
     if (C.flags & kFlagUnif32) {  // warp-uniform
-        compute32u<REACTION>(M, K, C, z, tm, t0, tp, G, un);
+        compute32u<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, un);
         return;
     }
     const uint32_t lz = C.lm >> (2 * z);
@@ -342,29 +349,29 @@ __device__ __forceinline__ void compute32(const Args32& M, const Slow32& K, cons
     float fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
     const bool interior = (C.flags >> (8 + z)) & 1;
     if (interior) {
-        fxl = fface32(dL, dc.x, uL, uc.x);
-        fxi = fface32(dc.x, dc.y, uc.x, uc.y);
-        fxr = fface32(dc.y, dR, uc.y, uR);
-        fy0m = fface32(dym.x, dc.x, uym.x, uc.x);
-        fy0p = fface32(dc.x, dyp.x, uc.x, uyp.x);
-        fz0m = fface32(dzm.x, dc.x, uzm.x, uc.x);
-        fz0p = fface32(dc.x, dzp.x, uc.x, uzp.x);
-        fy1m = fface32(dym.y, dc.y, uym.y, uc.y);
-        fy1p = fface32(dc.y, dyp.y, uc.y, uyp.y);
-        fz1m = fface32(dzm.y, dc.y, uzm.y, uc.y);
-        fz1p = fface32(dc.y, dzp.y, uc.y, uzp.y);
+        fxl = fface32<HALF>(dL, dc.x, uL, uc.x);
+        fxi = fface32<HALF>(dc.x, dc.y, uc.x, uc.y);
+        fxr = fface32<HALF>(dc.y, dR, uc.y, uR);
+        fy0m = fface32<HALF>(dym.x, dc.x, uym.x, uc.x);
+        fy0p = fface32<HALF>(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = fface32<HALF>(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = fface32<HALF>(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = fface32<HALF>(dym.y, dc.y, uym.y, uc.y);
+        fy1p = fface32<HALF>(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = fface32<HALF>(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = fface32<HALF>(dc.y, dzp.y, uc.y, uzp.y);
     } else {
-        fxl = face32(dL, dc.x, uL, uc.x);
-        fxi = face32(dc.x, dc.y, uc.x, uc.y);
-        fxr = face32(dc.y, dR, uc.y, uR);
-        fy0m = face32(dym.x, dc.x, uym.x, uc.x);
-        fy0p = face32(dc.x, dyp.x, uc.x, uyp.x);
-        fz0m = face32(dzm.x, dc.x, uzm.x, uc.x);
-        fz0p = face32(dc.x, dzp.x, uc.x, uzp.x);
-        fy1m = face32(dym.y, dc.y, uym.y, uc.y);
-        fy1p = face32(dc.y, dyp.y, uc.y, uyp.y);
-        fz1m = face32(dzm.y, dc.y, uzm.y, uc.y);
-        fz1p = face32(dc.y, dzp.y, uc.y, uzp.y);
+        fxl = face32<HALF>(dL, dc.x, uL, uc.x);
+        fxi = face32<HALF>(dc.x, dc.y, uc.x, uc.y);
+        fxr = face32<HALF>(dc.y, dR, uc.y, uR);
+        fy0m = face32<HALF>(dym.x, dc.x, uym.x, uc.x);
+        fy0p = face32<HALF>(dc.x, dyp.x, uc.x, uyp.x);
+        fz0m = face32<HALF>(dzm.x, dc.x, uzm.x, uc.x);
+        fz0p = face32<HALF>(dc.x, dzp.x, uc.x, uzp.x);
+        fy1m = face32<HALF>(dym.y, dc.y, uym.y, uc.y);
+        fy1p = face32<HALF>(dc.y, dyp.y, uc.y, uyp.y);
+        fz1m = face32<HALF>(dzm.y, dc.y, uzm.y, uc.y);
+        fz1p = face32<HALF>(dc.y, dzp.y, uc.y, uzp.y);
     }
     const float ix = M.A.inv_dx2[0], iy = M.A.inv_dx2[1], iz = M.A.inv_dx2[2];
     float lap0 = 0.0f;  // T lap = T(0) (solver.hpp:420)
@@ -392,14 +399,14 @@ __device__ __forceinline__ void compute32(const Args32& M, const Slow32& K, cons
         if (sent32(dc.y)) out1 = uc.y;
     }
     if ((C.flags & kFlagDir32) || ((a0 && nonfinite32(out0)) | (a1 && nonfinite32(out1)))) {
-        const float2 r = slow_pair32<REACTION>(M, K, C, z, tm, t0, tp, G, out0, out1);
+        const float2 r = slow_pair32<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
         out1 = r.y;
     }
     stg2f(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + G.bp), out0, out1, a0, a1);
 }
 
-template <int REACTION>
+template <int REACTION, bool HALF>
 __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
     extern __shared__ __align__(16) unsigned char smem32[];
     __shared__ Slow32 K;
@@ -523,7 +530,7 @@ __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
             cp_wait32<kAhead32>();
             __syncwarp();
             const uint32_t b = base + (uint32_t)z;
-            compute32<REACTION>(M, K, Cc, z, sb + (b & 7u) * kTile32, sb + ((b + 1u) & 7u) * kTile32,
+            compute32<REACTION, HALF>(M, K, Cc, z, sb + (b & 7u) * kTile32, sb + ((b + 1u) & 7u) * kTile32,
                                 sb + ((b + 2u) & 7u) * kTile32, G, un);
             __syncwarp();
             issue_next();
@@ -539,7 +546,7 @@ __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
 }
 
 __global__ void deff32_kernel(const float* __restrict__ dcol, const uint64_t* __restrict__ fluid, int64_t n_slots,
-                              float* __restrict__ deff, unsigned long long* bad) {
+                              float* __restrict__ deff, unsigned long long* bad, int half) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_slots + 512) return;
     if (i >= n_slots) {  // the sentinel chunk after the last one
@@ -548,29 +555,39 @@ __global__ void deff32_kernel(const float* __restrict__ dcol, const uint64_t* __
     }
     const bool fl = (fluid[i >> 6] >> (i & 63)) & 1ull;
     const float v = dcol[i];
-    deff[i] = fl ? v : __uint_as_float(kSent32);
+    deff[i] = fl ? (half ? v * 0.5f : v) : __uint_as_float(kSent32);
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
+    if (fl && fabsf(v) < 0x1p-125f) atomicAdd(bad + 1, 1ull);  // halving would not be exact
 }
 
 }  // namespace
 
 // D_eff of a float grid (+ trailing sentinel chunk); returns false if a fluid
 // node has a non-finite D (the exact tile kernel is kept then).
-bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void** out) {
+bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void** out, bool* half) {
     const int64_t slots = g->n_chunks * 512;
     float* p = nullptr;
     PD_CUDA(pd_malloc(&p, sizeof(float) * (size_t)(slots + 512)));
     unsigned long long* d_bad = nullptr;
-    PD_CUDA(pd_malloc(&d_bad, sizeof(unsigned long long)));
-    PD_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), g->stream));
-    deff32_kernel<<<(unsigned)((slots + 512 + 255) / 256), 256, 0, g->stream>>>((const float*)d_dcol, d_fluid, slots,
-                                                                               p, d_bad);
-    PD_CUDA(cudaGetLastError());
-    unsigned long long bad = 0;
-    PD_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
-    PD_CUDA(cudaStreamSynchronize(g->stream));
+    PD_CUDA(pd_malloc(&d_bad, 2 * sizeof(unsigned long long)));
+    static const int half_env = [] {
+        const char* e = getenv("PD_MARCH_HALF");
+        return e ? atoi(e) : 1;
+    }();
+    unsigned long long bad[2] = {0, 0};
+    for (int pass = 0; pass < 2; ++pass) {  // second pass only when a tiny D forbids halving
+        const int h = pass == 0 ? half_env : 0;
+        PD_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(unsigned long long), g->stream));
+        deff32_kernel<<<(unsigned)((slots + 512 + 255) / 256), 256, 0, g->stream>>>((const float*)d_dcol, d_fluid,
+                                                                                   slots, p, d_bad, h);
+        PD_CUDA(cudaGetLastError());
+        PD_CUDA(cudaMemcpyAsync(bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost, g->stream));
+        PD_CUDA(cudaStreamSynchronize(g->stream));
+        *half = h && !bad[1];
+        if (bad[0] || !h || !bad[1]) break;
+    }
     pd_free(d_bad);
-    if (bad) {
+    if (bad[0]) {
         pd_free(p);
         return false;
     }
@@ -592,17 +609,20 @@ void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, in
     M.zero = 0;
     M.n_all = g->n_chunks;
     using KernT = void (*)(Args32);
-    static const KernT table[3] = {ftcs_march32_kernel<0>, ftcs_march32_kernel<1>, ftcs_march32_kernel<2>};
+    static const KernT table[2][3] = {
+        {ftcs_march32_kernel<0, false>, ftcs_march32_kernel<1, false>, ftcs_march32_kernel<2, false>},
+        {ftcs_march32_kernel<0, true>, ftcs_march32_kernel<1, true>, ftcs_march32_kernel<2, true>}};
     constexpr size_t bytes = (size_t)kWarpBytes32 * kW32;
     static bool attr = false;
     if (!attr) {
-        for (auto k : table) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        for (auto& row : table)
+            for (auto k : row) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         attr = true;
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
-    table[r]<<<sms * kCtas32, kT32, bytes, g->stream>>>(M);
+    table[p.half ? 1 : 0][r]<<<sms * kCtas32, kT32, bytes, g->stream>>>(M);
     PD_CUDA(cudaGetLastError());
 }
 
