@@ -221,3 +221,34 @@ def test_free_box_dense_kernel_equals_reference(dtype, n, ref, cuda, monkeypatch
     view = np.uint64 if dtype == np.float64 else np.uint32
     for c in ("u", "u_next"):
         assert np.array_equal(ours.channel_data(c).view(view), rg.prop(c).view(view)), c
+
+
+@pytest.mark.parametrize("dtype,tiny", [(np.float64, 1e-310), (np.float32, 1e-39)])
+def test_subnormal_diffusivity_disables_halving_and_stays_exact(dtype, tiny, monkeypatch, ref, cuda):
+    """A fluid node with a subnormal D: halving D_eff would not be exact, so
+    the plan keeps D unhalved (plan.half = false); results still equal the
+    reference bit for bit."""
+    from paper_2304_11165_b200 import porediff as pd
+    spec = dict(dims=3, n=40, box=(0.0, 1.0), geom="pack", pack=(20, 0.05, 0.12, 9),
+                channels=["phi", "u", "D", "u_next"], profile=(0.05, 1.0, 0.0, 160.0), u0=("hash_unit", 3),
+                fp32=dtype == np.float32, reaction=("surface_sink", 1.0, 1.0), dt_frac=0.4, steps=12, record=4)
+    monkeypatch.setitem(cases.CASES, "tinyD", spec)
+    g = cases.ref_case("tinyD", ref)
+    keys, masks = g.layout()
+    D = g.prop("D")
+    phi = g.prop("phi")
+    act = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).astype(bool)
+    j, off = [int(v[len(v) // 2]) for v in np.nonzero(act & (phi > 0.05))]
+    D[j, off] = dtype(tiny)
+    g.set_prop("D", D)
+    data = {c: g.prop(c) for c in spec["channels"]}
+    dt = dt_of(spec, g.max_diffusivity())
+    geom = pd.GridGeometry.cell_centered_box(40, 0.0, 1.0, 3)
+    ours = pd.SparseBlockGrid.from_layout(geom, spec["channels"], keys, masks, data, dtype)
+    code, msg, rows = g.run(oracle_config(spec, dt), None)
+    assert code == 0, msg
+    res = pd.run_simulation(ours, sim_config(spec, dt))
+    assert [tuple(r) for r in rows] == [(d.step, d.time, d.total_mass, d.min_u, d.max_u) for d in res.diagnostics]
+    view = np.uint64 if dtype == np.float64 else np.uint32
+    for c in ("u", "u_next"):
+        assert np.array_equal(ours.channel_data(c).view(view), g.prop(c).view(view)), c
