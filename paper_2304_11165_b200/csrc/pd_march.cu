@@ -32,6 +32,14 @@
 //   halos hit L2 (a static interleave was measured to lose that). The claim ->
 //   schedule id -> lane masks/descriptor pipeline runs ahead through a
 //   per-warp context ring in shared memory.
+// * D_eff is stored halved (HALF): (d_a + d_b) * 0.5 == h_a + h_b exactly for
+//   normal values, so faces need no 0.5 multiply (plan falls back for tiny D).
+// * Uniform chunks (kFlagUnif: all fluid, one D_eff value also on the
+//   neighbours' facing layers) load no D_eff and form every face coefficient
+//   once (compute14u).
+// * PUSH (multi-GPU): boundary chunks also store their new z=0 / z=7 planes
+//   into the neighbour GPU's ghost chunks (pd_peer.cu).
+// * 3-D FP32 grids run the same design in pd_march32.cu.
 //
 // Earlier layouts (four nodes per lane "v15/v16", a whole x-row per lane
 // "v17") were measured and retired; see DESIGN.md section 4 and commit d37e7fc.
