@@ -298,6 +298,11 @@ def run_ours(args):
                    "sample": f"reference run_simulation (oracle/_ref, -O3 -ffp-contract=off, "
                              f"{cores} std::thread workers) on the [0,{args.cpu_sample})^3 crop of the same "
                              f"geometry: {a} active nodes x {st} steps in {secs:.2f} s"}
+            # SURVEY §8d also asks for the single-thread figure (RD_THREADS=1)
+            v1, a1, secs1, _, st1 = cpu_sample(args, pack, args.cpu_sample, args.cpu_steps, threads=1,
+                                               target_s=max(2.0, args.cpu_seconds / 4))
+            cpu["single_thread"] = {"value": v1 / 1e9, "unit": "GPts/s", "cores": 1,
+                                    "sample": f"same crop, 1 worker: {a1} active nodes x {st1} steps in {secs1:.2f} s"}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "GPts/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
     if rank == 0:
