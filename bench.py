@@ -190,6 +190,10 @@ def cpu_sample(args, pack, edge, steps, threads=None, target_s=None):
     # spheres that can touch the crop (exact: the others are never the min)
     lo, hi = 0.0, edge * h
     near = np.all((centers > lo - radii[:, None] - 2 * h) & (centers < hi + radii[:, None] + 2 * h), axis=1)
+    if not near.any():  # crop inside the pore space (small custom boxes): the nearest spheres keep the SDF
+        # finite (a timing sample; the default configuration always has spheres in the crop)
+        mid = 0.5 * (lo + hi)
+        near[np.argsort(np.linalg.norm(centers - mid, axis=1))[:8]] = True
     sub = type(pack)(list(map(tuple, centers[near])), list(radii[near]))
     sdf = sub.fluid_sdf_field(geom)
     g = R.grid_from_sdf(geom.size, geom.spacing, geom.origin, sdf)
