@@ -8,6 +8,7 @@ at the configured sizes.
 """
 import argparse
 import math
+import os
 import sys
 import time
 from pathlib import Path
@@ -106,6 +107,9 @@ def c3(T, n=512, steps=1000):
     cfg.reaction = pd.ReactionSpec.surface_sink(2.0, 1.0)
     cfg.outer_bc[0] = pd.FaceBc.dirichlet(1.0)
     steps_rate(grid, cfg, f"{steps} FTCS steps (sink + inlet)", T)
+    if os.environ.get("C3_NO_INLET"):
+        cfg.outer_bc[0] = pd.FaceBc.no_flux()
+        steps_rate(grid, cfg, f"{steps} FTCS steps (sink, no inlet)", T)
     grid.close()
 
 
