@@ -19,7 +19,10 @@ namespace {
 
 constexpr int kW32 = 4;                 // warps per CTA
 constexpr int kT32 = 32 * kW32;
-constexpr int kCtas32 = 6;              // CTAs per SM
+#ifndef PD_M32_CTAS
+#define PD_M32_CTAS 6
+#endif
+constexpr int kCtas32 = PD_M32_CTAS;    // CTAs per SM
 constexpr int kRing32 = 8;
 constexpr int kAhead32 = kRing32 - 3;   // planes z-1, z, z+1 resident
 constexpr unsigned kSent32 = 0xFF800000u;  // -inf

@@ -1,5 +1,5 @@
-"""FP32 vs FP64 step throughput on the same device-built sphere pack (the
-FP32 grids run the generic staged-tile kernel; FP64 the march kernel).
+"""FP32 vs FP64 step throughput on the same device-built sphere pack (both
+take their march kernels: pd_march32.cu / pd_march.cu).
 
     python scripts/fp32_timing.py [--n 1024] [--steps 50]
 """
