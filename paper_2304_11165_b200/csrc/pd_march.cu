@@ -597,7 +597,17 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     Q.ix = A.inv_dx2[0];
     Q.iy = A.inv_dx2[1];
     Q.iz = A.inv_dx2[2];
-    const LaneGeo G = lane_geo(lane);
+    LaneGeo G = lane_geo(lane);
+#ifndef PD_M14_NOPIN
+    // opaque copies: ptxas cannot rematerialise a shuffle result inside the
+    // plane loop, so the lane constants stay in registers
+    G.s_c = __shfl_sync(0xffffffffu, G.s_c, lane);
+    G.s_l = __shfl_sync(0xffffffffu, G.s_l, lane);
+    G.s_r = __shfl_sync(0xffffffffu, G.s_r, lane);
+    G.s_hx = __shfl_sync(0xffffffffu, G.s_hx, lane);
+    G.s_hy = __shfl_sync(0xffffffffu, G.s_hy, lane);
+    G.bp = __shfl_sync(0xffffffffu, G.bp, lane);
+#endif
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes14;
     const double* __restrict__ u = A.u;
     const double* __restrict__ de = M.deff;

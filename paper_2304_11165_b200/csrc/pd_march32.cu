@@ -435,7 +435,17 @@ __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
         K.dirichlet = A.dirichlet;
     }
     __syncthreads();
-    const Geo32 G = geo32(lane);
+    Geo32 G = geo32(lane);
+#ifndef PD_M32_NOPIN
+    // opaque copies: ptxas cannot rematerialise a shuffle result inside the
+    // plane loop, so the lane constants stay in registers
+    G.s_c = __shfl_sync(0xffffffffu, G.s_c, lane);
+    G.s_l = __shfl_sync(0xffffffffu, G.s_l, lane);
+    G.s_r = __shfl_sync(0xffffffffu, G.s_r, lane);
+    G.s_hx = __shfl_sync(0xffffffffu, G.s_hx, lane);
+    G.s_hy = __shfl_sync(0xffffffffu, G.s_hy, lane);
+    G.bp = __shfl_sync(0xffffffffu, G.bp, lane);
+#endif
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem32) + (uint32_t)warp * kWarpBytes32;
     const float* __restrict__ u = A.u;
     const float* __restrict__ de = M.deff;
