@@ -608,7 +608,12 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     G.s_hy = __shfl_sync(0xffffffffu, G.s_hy, lane);
     G.bp = __shfl_sync(0xffffffffu, G.bp, lane);
 #endif
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes14;
+    uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes14;
+#ifndef PD_NOPIN2
+    sb = __shfl_sync(0xffffffffu, sb, lane);
+    G.xface = __shfl_sync(0xffffffffu, (int)G.xface, lane) != 0;
+    G.yface = __shfl_sync(0xffffffffu, (int)G.yface, lane) != 0;
+#endif
     const double* __restrict__ u = A.u;
     const double* __restrict__ de = M.deff;
     double* __restrict__ un = A.un;

@@ -446,7 +446,12 @@ __global__ void __launch_bounds__(kT32, kCtas32) ftcs_march32_kernel(Args32 M) {
     G.s_hy = __shfl_sync(0xffffffffu, G.s_hy, lane);
     G.bp = __shfl_sync(0xffffffffu, G.bp, lane);
 #endif
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem32) + (uint32_t)warp * kWarpBytes32;
+    uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem32) + (uint32_t)warp * kWarpBytes32;
+#ifndef PD_NOPIN2
+    sb = __shfl_sync(0xffffffffu, sb, lane);
+    G.xface = __shfl_sync(0xffffffffu, (int)G.xface, lane) != 0;
+    G.yface = __shfl_sync(0xffffffffu, (int)G.yface, lane) != 0;
+#endif
     const float* __restrict__ u = A.u;
     const float* __restrict__ de = M.deff;
     float* __restrict__ un = A.un;
