@@ -15,10 +15,18 @@ A "step" is one FTCS time step over every active node. value = active
 nodes x K / (max-over-ranks device time of the K steps). The grid (~3 x 25 GB
 of u/u_next/D) is far larger than L2, so no L2 flush is needed between steps.
 
-Multi-GPU (torchrun, one rank per GPU): z-slab decomposition by chunk
-layers; each rank builds its slab plus one ghost chunk layer per side and
-exchanges boundary u planes with NCCL every step. Strong scaling: the same
-2048^3 domain is split over N GPUs. See DESIGN.md.
+Multi-GPU (one rank per GPU): `bench.py --gpus N` re-launches itself under
+torch.distributed.run with N ranks when it is not already inside one (the
+driver's torchrun launch works the same). z-slab decomposition by chunk
+layers, cut at equal prefix sums of per-layer cost; each rank builds its slab
+plus one ghost chunk layer per side, and the step kernel pushes its boundary
+planes into the neighbours' ghost layers over NVLink peer memory. Strong
+scaling: the same 2048^3 domain is split over N GPUs.
+
+The reference arm (--impl reference) and the cpu_baseline leg run the
+UNMODIFIED reference (oracle/_ref, compiled in place) through one shared
+sampling protocol (reference_rate below); the reference arm imports nothing
+from the product package.
 """
 from __future__ import annotations
 
@@ -54,18 +62,28 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=192, help="edge of the CPU sample crop")
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
-    ap.add_argument("--e2e-n", type=int, default=512, help="box edge of the end-to-end host-buffer run")
-    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--e2e-n", type=int, default=0,
+                    help="box edge of the end-to-end host-buffer run (0: the bench box when host RAM allows)")
+    ap.add_argument("--e2e-steps", type=int, default=1000)
+    ap.add_argument("--cpu-calls", type=int, default=3, help="timed reference calls of the cpu_baseline leg")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
 
+def pack_count(psi, radius):
+    """Sphere count of pack_for_porosity (Boolean model, unit box):
+    psi = exp(-count * 4/3 pi r^3)."""
+    return int(round(math.log(1.0 / psi) / (4.0 / 3.0 * math.pi * radius ** 3)))
+
+
 def workload(args):
+    """The bench's sphere pack, drawn by the product's SpherePacking.random
+    (bit-identical to the reference's SpherePacking::random,
+    synthetic.hpp:42-55)."""
     from paper_2304_11165_b200 import synthetic as sy
     r = args.radius_vox / args.n
-    pack = sy.pack_for_porosity(args.psi, r, args.seed)
-    return pack
+    return sy.SpherePacking.random((0, 0, 0), (1, 1, 1), pack_count(args.psi, r), r, r, args.seed)
 
 
 def config_dict(args, n_gpus):
@@ -168,55 +186,80 @@ def ncu_traffic(n):
 # ---------------------------------------------------------------------------
 
 
-_REF_GRID_CACHE = {}
+def ref_spheres(R, args):
+    """The same pack drawn by the reference itself (synthetic.hpp:42-55)."""
+    r = args.radius_vox / args.n
+    return R.sphere_packing((0, 0, 0), (1, 1, 1), pack_count(args.psi, r), r, r, args.seed)
 
 
-def cpu_sample(args, pack, edge, steps, threads=None, target_s=None):
-    """Times the reference's own run_simulation on a crop [0,edge)^3 of the
-    same pore geometry (same spheres and spacing); geometry build untimed.
-    With target_s, a short calibration run sizes the step count so the timed
-    run takes about target_s seconds of CPU wall time."""
-    import ctypes as C
+def crop_spheres(R, centers, radii, size, h, origin):
+    """Spheres that can be the minimum of fluid_sdf somewhere in the crop
+    (exact, see tests/test_headline_parity.py): M = max over the crop of the
+    field of the spheres meeting the crop box bounds the true field, and a
+    sphere whose box distance minus radius exceeds M is never the minimum."""
+    lo = np.asarray(origin, float)
+    hi = lo + (np.asarray(size) - 1) * h
+    d = np.linalg.norm(np.maximum(0.0, np.maximum(lo - centers, centers - hi)), axis=1) - radii
+    first = d <= 0.0
+    if not first.any():
+        return centers, radii
+    f0 = R.field_sphere_pack(size, (h,) * 3, origin, centers[first], radii[first])
+    keep = d <= float(np.max(f0))
+    return centers[keep], radii[keep]
 
+
+def reference_rate(args, edge, calls, per_call_s, threads=None, warm=True):
+    """THE CPU sampling protocol of both the reference arm and the
+    cpu_baseline leg: the reference's own pipeline (field_from over the pack,
+    build_sparse_grid, populate_diffusion_channel, u = hash_unit_value(1, .),
+    surface sink 1/1, dt = 0.4 * stability_dt(max D)) on the [0, edge)^3 crop
+    of the bench geometry (same spheres, spacing and origin), built once
+    (untimed); a calibration call sizes S steps per call to ~per_call_s; then
+    `calls` run_simulation calls of S steps each are timed back to back on the
+    same grid. Returns (G pts/s, per-call seconds, S, active nodes, worker
+    threads). Only oracle/ is touched (test infrastructure)."""
     from oracle.pyoracle import Ref, make_config
-    from paper_2304_11165_b200 import porediff as pd
-
+    import ctypes as C
     R = Ref()
-    if threads:
-        R.L.ref_set_worker_count(threads)
-    h = 1.0 / args.n
-    geom = pd.GridGeometry.make((edge,) * 3, (h,) * 3, (0.5 * h,) * 3)
-    centers, radii = pack.arrays()
-    # spheres that can touch the crop (exact: the others are never the min)
-    lo, hi = 0.0, edge * h
-    near = np.all((centers > lo - radii[:, None] - 2 * h) & (centers < hi + radii[:, None] + 2 * h), axis=1)
-    if not near.any():  # crop inside the pore space (small custom boxes): the nearest spheres keep the SDF
-        # finite (a timing sample; the default configuration always has spheres in the crop)
-        mid = 0.5 * (lo + hi)
-        near[np.argsort(np.linalg.norm(centers - mid, axis=1))[:8]] = True
-    sub = type(pack)(list(map(tuple, centers[near])), list(radii[near]))
-    sdf = sub.fluid_sdf_field(geom)
-    g = R.grid_from_sdf(geom.size, geom.spacing, geom.origin, sdf)
-    g.populate_diffusion(0.0, 1.0, 0.0, 4.0 * args.n)
-    g.fill_hash("u", 1)
-    dmax = g.max_diffusivity()
-    dt = 0.4 * pd.stability_dt(geom, dmax)
-    if target_s:
-        cal = make_config(dt, 5, reaction="surface_sink", rate=1.0, band_half_width=1.0, record_every=5)
-        t0 = time.perf_counter()
-        g.run(cal)
-        per_step = (time.perf_counter() - t0) / 5
-        steps = max(5, int(target_s / max(per_step, 1e-6)))
-    cfg = make_config(dt, steps, reaction="surface_sink", rate=1.0, band_half_width=1.0, record_every=steps)
-    t0 = time.perf_counter()
-    code, msg, rows = g.run(cfg)
-    secs = time.perf_counter() - t0
-    assert code == 0, msg
-    active = g.active_count()
-    cores = R.L.ref_worker_count()
-    if threads:
+    R.L.ref_set_worker_count(threads or 0)
+    try:
+        h = 1.0 / args.n
+        size, origin = (edge,) * 3, (0.5 * h,) * 3
+        centers, radii = ref_spheres(R, args)
+        sc, sr = crop_spheres(R, centers, radii, size, h, origin)
+        g = R.grid_from_sdf(size, (h,) * 3, origin, R.field_sphere_pack(size, (h,) * 3, origin, sc, sr))
+        g.populate_diffusion(0.0, 1.0, 0.0, 4.0 * args.n)
+        g.fill_hash("u", 1)
+        code = C.c_int()
+        bound = R.L.ref_stability_dt(3, (C.c_double * 3)(h, h, h), g.max_diffusivity(), C.byref(code))
+        dt = 0.4 * bound
+
+        def call(steps):
+            cfg = make_config(dt, steps, reaction="surface_sink", rate=1.0, band_half_width=1.0, record_every=steps)
+            t0 = time.perf_counter()
+            rc, msg, _ = g.run(cfg)
+            secs = time.perf_counter() - t0
+            assert rc == 0, msg
+            return secs
+
+        cal = 4
+        per_step = call(cal) / cal
+        if warm:
+            call(cal)
+            per_step = min(per_step, call(cal) / cal)
+        steps = max(2, int(per_call_s / max(per_step, 1e-9)))
+        secs = [call(steps) for _ in range(calls)]
+        active = g.active_count()
+        return active * steps * calls / sum(secs) / 1e9, secs, steps, active, R.L.ref_worker_count()
+    finally:
         R.L.ref_set_worker_count(0)
-    return active * steps / secs, active, secs, cores, steps
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
 
 
 # ---------------------------------------------------------------------------
@@ -228,12 +271,13 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2304_11165_b200 import porediff as pd
     from paper_2304_11165_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # test hooks for exercising the N > 1 path on a one-GPU box: every rank on
     # cuda:0 (PD_BENCH_SAME_GPU=1) with a gloo control plane
     # (PD_DIST_BACKEND=gloo); the peer exchange itself is CUDA IPC either way
@@ -249,8 +293,10 @@ def run_ours(args):
     red_dev = "cuda" if backend == "nccl" else "cpu"
 
     pack = workload(args)
+    t_build = time.perf_counter()
     dom = shard.build_domain(args.n, pack, rank, world, device=local)
     stepper = dom.stepper(dt_frac=0.4, sink_rate=1.0)
+    t_build = time.perf_counter() - t_build
 
     def sync():
         torch.cuda.synchronize()
@@ -273,40 +319,60 @@ def run_ours(args):
     launches += dom.extra_launches_per_step * args.steps
     # exact global diagnostics of the final state (all ranks take part)
     diag = dom.diagnostics(stepper)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-    act_t = torch.tensor([dom.owned_active], dtype=torch.float64, device=red_dev)
+    kern_ms = dom.last_kernel_ms / args.steps
+    mine = torch.tensor([ms, kern_ms, float(dom.owned_active), float(dom.owned_chunks)], dtype=torch.float64,
+                        device=red_dev)
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(act_t, op=dist.ReduceOp.SUM)
-    ms_max = float(ms_t.item())
-    active = float(act_t.item())
+        allv = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allv, mine)
+        per_rank = torch.stack(allv).cpu().numpy()
+    else:
+        per_rank = mine.cpu().numpy()[None, :]
+    ms_max = float(per_rank[:, 0].max())
+    active = float(per_rank[:, 2].sum())
     step_ms = ms_max / args.steps
     value = active * args.steps / (ms_max / 1e3)
     peak, peak_src = measured_peak()
     # dominant kernel: the step kernel alone (CUDA events on its stream),
-    # timed region only
-    kern_ms = dom.last_kernel_ms / args.steps
-    achieved = dom.owned_active * BYTES_PER_UPDATE / (kern_ms / 1e3) / 1e9
+    # timed region only, on the slowest rank
+    kmax = int(per_rank[:, 1].argmax())
+    kern_ms_max = float(per_rank[kmax, 1])
+    achieved = float(per_rank[kmax, 2]) * BYTES_PER_UPDATE / (kern_ms_max / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic(args.n)
+    chunks_total = int(per_rank[:, 3].sum())
+    ranks = [{"rank": r, "step_ms": float(per_rank[r, 0]) / args.steps, "kernel_ms": float(per_rank[r, 1]),
+              "active_nodes": int(per_rank[r, 2]), "chunks": int(per_rank[r, 3])} for r in range(world)]
+    imbalance = float(per_rank[:, 0].max() / per_rank[:, 0].mean() - 1.0)
+    # the bench domain leaves the device before the end-to-end run needs it
+    dom.close(stepper)
+    del dom
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
 
-    chunks_total = int(dom.total_chunks(world))  # a collective: every rank takes part
     e2e = None
     if not args.no_e2e and rank == 0:
-        e2e = run_e2e(args, pack)
+        try:
+            e2e = run_e2e(args, pack)
+        except Exception as e:  # reported, not fatal
+            e2e = {"value": None, "unit": "GPts/s", "error": f"{type(e).__name__}: {e}"}
     cpu = None
     if not args.no_cpu and rank == 0:
         try:
-            v, a, secs, cores, st = cpu_sample(args, pack, args.cpu_sample, args.cpu_steps,
-                                               target_s=args.cpu_seconds)
-            cpu = {"value": v / 1e9, "unit": "GPts/s", "cores": cores, "kind": "reference",
-                   "sample": f"reference run_simulation (oracle/_ref, -O3 -ffp-contract=off, "
-                             f"{cores} std::thread workers) on the [0,{args.cpu_sample})^3 crop of the same "
-                             f"geometry: {a} active nodes x {st} steps in {secs:.2f} s"}
+            per = args.cpu_seconds / max(1, args.cpu_calls)
+            v, secs, st, a, cores = reference_rate(args, args.cpu_sample, args.cpu_calls, per)
+            cpu = {"value": v, "unit": "GPts/s", "cores": cores, "kind": "reference",
+                   "sample": f"reference_rate(): unmodified reference run_simulation (oracle/_ref, -O3 "
+                             f"-ffp-contract=off, {cores} std::thread workers of {host_cores()} host cores) on the "
+                             f"[0,{args.cpu_sample})^3 crop of the same geometry: {a} active nodes, "
+                             f"{args.cpu_calls} calls x {st} steps in {sum(secs):.2f} s (the reference arm's "
+                             f"protocol)"}
             # SURVEY §8d also asks for the single-thread figure (RD_THREADS=1)
-            v1, a1, secs1, _, st1 = cpu_sample(args, pack, args.cpu_sample, args.cpu_steps, threads=1,
-                                               target_s=max(2.0, args.cpu_seconds / 4))
-            cpu["single_thread"] = {"value": v1 / 1e9, "unit": "GPts/s", "cores": 1,
-                                    "sample": f"same crop, 1 worker: {a1} active nodes x {st1} steps in {secs1:.2f} s"}
+            v1, secs1, st1, a1, _ = reference_rate(args, args.cpu_sample, 1, max(2.0, per / 2), threads=1,
+                                                   warm=False)
+            cpu["single_thread"] = {"value": v1, "unit": "GPts/s", "cores": 1,
+                                    "sample": f"same crop, 1 worker: {a1} active nodes x {st1} steps in "
+                                              f"{sum(secs1):.2f} s"}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "GPts/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
     if rank == 0:
@@ -318,35 +384,55 @@ def run_ours(args):
             "active_nodes": int(active), "chunks": chunks_total,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
-                         "algorithmic_bytes_per_launch": dom.owned_active * BYTES_PER_UPDATE,
+                         "algorithmic_bytes_per_launch": float(per_rank[kmax, 2]) * BYTES_PER_UPDATE,
                          "peak_source": peak_src, "bytes_per_update": BYTES_PER_UPDATE,
-                         "kernel_ms_per_step": kern_ms, "traffic_source": traffic_src and "profiles/ftcs_step_traffic.json"},
-            "roofline_frac_of_step": dom.owned_active * BYTES_PER_UPDATE / (step_ms / 1e3) / 1e9 / peak,
+                         "kernel_ms_per_step": kern_ms_max, "traffic_source": traffic_src and "profiles/ftcs_step_traffic.json"},
+            "roofline_frac_of_step": active * BYTES_PER_UPDATE / (step_ms / 1e3) / 1e9 / peak / world,
+            "per_rank": ranks, "load_imbalance": imbalance,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
-            "wall_s_timed_region": wall,
+            "wall_s_timed_region": wall, "build_s": t_build,
             "final_diagnostics": {"total_mass": diag[0], "min_u": diag[1], "max_u": diag[2],
                                   "note": "exact across ranks: rank-ordered per-chunk partials + pairwise_sum"},
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_e2e(args, pack):
-    """Same metric through the reference-facing API with HOST buffers: one
-    run_simulation call on a host SparseBlockGrid (pinned upload of every
-    channel, the FTCS steps, diagnostics rows, download of u and u_next), on a
-    --e2e-n^3 crop of the same geometry."""
-    import ctypes as C
+def host_ram_bytes():
+    try:
+        import psutil
+        return psutil.virtual_memory().available
+    except Exception:
+        return os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
 
+
+def run_e2e(args, pack):
+    """The same metric through the reference-facing API with HOST buffers:
+    one run_simulation call (args.e2e_steps steps) on a host SparseBlockGrid
+    whose four channel slabs live in pinned host memory. Timed: creation of
+    the device mirror and the upload of every channel (H2D), the stepper
+    build, the steps, the diagnostics rows, and the download of u and u_next
+    (D2H, what the steps changed). Default box: the bench box itself, when
+    the host has the RAM for its pinned slabs; else the largest power-of-two
+    crop of the same geometry that fits (stated in `workload`)."""
     import torch
 
     from paper_2304_11165_b200 import porediff as pd
 
     n = args.e2e_n
     h = 1.0 / args.n
-    geom = pd.GridGeometry.make((n,) * 3, (h,) * 3, (0.5 * h,) * 3)
     centers, radii = pack.arrays()
+    if n <= 0:
+        n = args.n
+        while n > 256:
+            geom = pd.GridGeometry.make((n,) * 3, (h,) * 3, (0.5 * h,) * 3)
+            _, act_chunks = _layer_chunks(pd, geom, centers, radii)
+            need = act_chunks * 512 * 8 * 4
+            if need * 1.3 < host_ram_bytes():
+                break
+            n //= 2
+    geom = pd.GridGeometry.make((n,) * 3, (h,) * 3, (0.5 * h,) * 3)
     dev = pd.DeviceGrid.sphere_pack(geom, centers, radii, n_props=4, prop_phi=0)
     dev.populate_diffusion(0, 2, pd.DiffusionProfile(0.0, 1.0, 0.0, 4.0 * args.n))
     dev.fill_hash(1, 1)
@@ -357,18 +443,20 @@ def run_e2e(args, pack):
     for p, name in enumerate(pd.solver_channels()):
         t = torch.empty((nch, 512), dtype=torch.float64, pin_memory=True)
         arr = t.numpy()
-        arr[:] = dev.download(p)
+        dev.download_into(p, arr)
         host[name] = (t, arr)
+    dmax = dev.max_active(2)
     dev.close()
-    dmax = float(host["D"][1].max())
     cfg = pd.SimulationConfig(dt=0.4 * pd.stability_dt(geom, dmax), n_steps=args.e2e_steps,
                               record_every=args.e2e_steps)
     cfg.reaction = pd.ReactionSpec.surface_sink(1.0, 1.0)
+    keep = {name: host[name][1].copy() if n <= 512 else None for name in ("u", "u_next")}
 
     def once():
         g = pd.SparseBlockGrid.from_layout(geom, pd.solver_channels(), keys, masks, None)
         for name in pd.solver_channels():
             g._data[name] = host[name][1]  # zero-copy: the pinned host buffers
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = pd.run_simulation(g, cfg)
         out_u = g.channel_data("u")
@@ -377,54 +465,79 @@ def run_e2e(args, pack):
         g.close()
         return secs, res
 
-    once()  # warm-up (context, allocator)
+    if n <= 512:  # small boxes: one untimed warm-up call (context, allocator), state restored
+        once()
+        for name in ("u", "u_next"):
+            host[name][1][:] = keep[name]
     secs, res = once()
-    active = int(host["phi"][1].size and sum(bin(int(w)).count("1") for w in masks.ravel()))
+    active = int(np.bitwise_count(masks).sum())
     slab = nch * 512 * 8
     return {"value": active * args.e2e_steps / secs / 1e9, "unit": "GPts/s", "h2d_bytes_per_step": 4 * slab,
             # run_simulation leaves u and u_next device-newer; the reads of
             # both pull exactly those two slabs (phi and D never change)
             "d2h_bytes_per_step": 2 * slab + 40 * len(res.diagnostics),
-            "workload": f"run_simulation on a host grid, [0,{n})^3 crop of the same geometry, "
-                        f"{args.e2e_steps} steps per call (one call = one e2e step)",
-            "active_nodes": active, "seconds": secs}
+            "workload": f"one run_simulation call on a host grid (pinned slabs): the [0,{n})^3 box of the bench "
+                        f"geometry{' (the whole bench box)' if n == args.n else ' (crop: host RAM)'}, "
+                        f"{args.e2e_steps} steps per call (one call = one e2e step); device mirror build, "
+                        f"uploads, stepper build, steps and downloads all timed",
+            "active_nodes": active, "seconds": secs, "box": n}
+
+
+def _layer_chunks(pd, geom, centers, radii):
+    from paper_2304_11165_b200 import shard
+
+    class _P:
+        def arrays(self):
+            return centers, radii
+    chunks, active = shard.layer_work(geom, _P())
+    return int(active.sum()), int(chunks.sum())
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    headers compiled in place) through reference_rate(), the same protocol as
+    the cpu_baseline leg. Imports nothing from paper_2304_11165_b200."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    pack = workload(args)
+    per = max(0.5, args.cpu_seconds / max(1, args.steps))
     edge = args.cpu_sample
-    vals = []
-    for _ in range(min(args.warmup, 1)):
-        cpu_sample(args, pack, edge, 3)
-    # each timed step is a bounded sample: ~cpu_seconds / steps of CPU work
-    per = max(1.0, args.cpu_seconds / max(1, args.steps))
-    total_pts, total_s, cores, active, st = 0.0, 0.0, None, 0, 0
-    for _ in range(args.steps):
-        v, active, secs, cores, st = cpu_sample(args, pack, edge, args.cpu_steps, target_s=per)
-        total_pts += active * st
-        total_s += secs
-        vals.append(v)
-    value = total_pts / total_s / 1e9
+    if args.warmup > 0:
+        reference_rate(args, edge, 1, 0.2, warm=False)
+    value, secs, st, active, cores = reference_rate(args, edge, args.steps, per)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(secs) / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(args, world),
         "cpu_baseline": {"value": value, "unit": "GPts/s", "cores": cores, "kind": "reference",
-                         "sample": f"each step = reference run_simulation (oracle/_ref, {cores} std::thread "
-                                   f"workers) of ~{st} FTCS steps on the [0,{edge})^3 crop ({active} active "
-                                   f"nodes) of the same geometry"},
+                         "sample": f"reference_rate(): each step = one reference run_simulation call (oracle/_ref, "
+                                   f"{cores} std::thread workers of {host_cores()} host cores) of {st} FTCS steps "
+                                   f"on the [0,{edge})^3 crop ({active} active nodes) of the same geometry"},
         "e2e": {"value": value, "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+
+
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: re-execute this command under
+    torch.distributed.run with N ranks on 127.0.0.1 and pass its output and
+    exit code through."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))).returncode
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -104,39 +104,25 @@ inline double apply_reaction(double u, double phi, const ReactionSpec& spec, dou
 }
 
 /// Max of a channel over active nodes, 0 on an empty grid (solver.hpp:139-154).
+/// Evaluated on the device mirror (pd_grid_max_active; the max is
+/// order-free, so the fold order does not matter).
 template <typename T, int Dims>
 double max_diffusivity(const SparseBlockGrid<T, Dims>& grid, std::string_view channel = "D") {
-    using G = SparseBlockGrid<T, Dims>;
     const int prop = grid.property_index(channel);
-    double best = -std::numeric_limits<double>::infinity();
-    bool any = false;
-    grid.for_each_chunk([&](const typename G::Chunk& c) {
-        const T* d = grid.channel_data(c, prop);
-        for (int o = 0; o < G::chunk_volume; ++o)
-            if (c.test(o)) {
-                best = std::max(best, static_cast<double>(d[o]));
-                any = true;
-            }
-    });
-    return any ? best : 0.0;
+    double out = 0.0;
+    b200::check(pd_grid_max_active(const_cast<SparseBlockGrid<T, Dims>&>(grid).device_grid(), prop, &out));
+    return out;
 }
 
 /// sum(u) * cell volume: per-chunk sequential sums, pairwise over chunks
-/// (solver.hpp:158-171).
+/// (solver.hpp:158-171), on the device mirror (pd_grid_total_mass keeps the
+/// reference's summation order, so the bits are the same).
 template <typename T, int Dims>
 double total_mass(const SparseBlockGrid<T, Dims>& grid, std::string_view channel = "u") {
-    using G = SparseBlockGrid<T, Dims>;
     const int prop = grid.property_index(channel);
-    std::vector<double> per_chunk;
-    per_chunk.reserve(static_cast<std::size_t>(grid.chunk_count()));
-    grid.for_each_chunk([&](const typename G::Chunk& c) {
-        const T* u = grid.channel_data(c, prop);
-        double s = 0.0;
-        for (int o = 0; o < G::chunk_volume; ++o)
-            if (c.test(o)) s += static_cast<double>(u[o]);
-        per_chunk.push_back(s);
-    });
-    return pairwise_sum(std::move(per_chunk)) * grid.geometry().cell_volume();
+    double out = 0.0;
+    b200::check(pd_grid_total_mass(const_cast<SparseBlockGrid<T, Dims>&>(grid).device_grid(), prop, &out));
+    return out;
 }
 
 inline constexpr const char* scratch_channel = "u_next";
@@ -192,15 +178,40 @@ class FtcsStepper {
 
     const SimulationConfig& config() const { return cfg_; }
 
+    /// stability_dt(max D over active nodes), or +inf if that max is <= 0
+    /// (solver.hpp:220-224), evaluated by the device stepper.
     double stability_bound() const {
-        const double d_max = max_diffusivity(grid_);
-        return d_max > 0.0 ? stability_dt(grid_.geometry(), d_max) : std::numeric_limits<double>::infinity();
+        const_cast<FtcsStepper*>(this)->bind();
+        double out = 0.0;
+        b200::check(pd_stepper_stability_bound(st_, &out));
+        return out;
     }
 
     /// One step from state u(step_index*dt) (reference solver.hpp:228-279).
+    /// A non-finite node throws numeric_error; a non-finite total mass is
+    /// returned in the row (run_simulation checks it, solver.hpp:514-515).
     StepDiagnostics step(std::int64_t step_index) {
-        auto rows = advance(step_index, 1, step_index + 1);
-        return rows.front();
+        const auto t0 = std::chrono::steady_clock::now();
+        bind();
+        double factor = 1.0;
+        if (cfg_.reaction.kind == ReactionSpec::Kind::volumetric && cfg_.reaction.time_factor)
+            factor = static_cast<double>(
+                static_cast<T>(cfg_.reaction.time_factor(static_cast<double>(step_index) * cfg_.dt)));
+        int col_before = 0, col_after = 0;
+        b200::check(pd_grid_column_of(dev_.get(), i_u_, &col_before));
+        pd_diag d{};
+        const int rc = pd_stepper_step(st_, step_index, factor, &d);
+        const std::string err = rc == PD_OK ? std::string() : std::string(pd_last_error());
+        b200::check(pd_grid_column_of(dev_.get(), i_u_, &col_after));
+        if (col_after != col_before)
+            grid_.note_device_swap(i_u_, i_next_);
+        else {
+            grid_.mark_device_newer(i_u_);
+            grid_.mark_device_newer(i_next_);
+        }
+        if (rc != PD_OK) b200::raise(rc, err);
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return {d.step, d.time, d.total_mass, d.min_u, d.max_u, wall};
     }
 
     /// `n` consecutive steps in one device call; returns the rows

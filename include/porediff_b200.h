@@ -186,6 +186,12 @@ int pd_stepper_snapshot_diag(pd_stepper* s, pd_diag* out);
  * exactly as the reference leaves it (u = pre-step state, u_next written). */
 int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_step,
                    const double* factors, pd_diag* rows, int64_t* n_rows);
+/* One step from global step index step_index with a diagnostics row: exactly
+ * FtcsStepper::step (solver.hpp:228-279) -- a non-finite node raises the
+ * numeric_error, a non-finite total mass does NOT (that check belongs to
+ * run_simulation, solver.hpp:514-515) and is returned in the row. factor:
+ * the step's source factor T(g(t)) (1 without a time factor). */
+int pd_stepper_step(pd_stepper* s, int64_t step_index, double factor, pd_diag* row);
 /* Device time (ms, CUDA events) of the last pd_stepper_run's step kernels. */
 int pd_stepper_last_ms(const pd_stepper* s, double* ms);
 /* Launches of the step kernel so far (benchmark accounting). */
@@ -214,9 +220,16 @@ int pd_build_sphere_pack_region(int scalar_bytes, const int64_t* size, const dou
                                 const int64_t* chunk_lo, const int64_t* chunk_hi, int n_props,
                                 int prop_phi, int device, pd_grid** out);
 /* D = d_min + d_max/(1+exp(-(g1+g2*phi))) on active nodes
- * (geometry.hpp:182-206; device exp, may differ from glibc by <= 1 ulp). */
+ * (populate_diffusion_channel, geometry.hpp:182-206). exp is the reference
+ * libm's, restated bit for bit (csrc/pd_libm_exp.h), so D is the reference's
+ * bits. */
 int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_min,
                                double d_max, double gamma1, double gamma2);
+/* smooth_diffusion_coefficient (geometry.hpp:182-187) for n host values of
+ * phi, evaluated on `device` (same bits as the reference); validation as the
+ * reference (input_error on d_min < 0 or d_max <= 0). */
+int pd_smooth_diffusion_coefficients(const double* phi, int64_t n, double d_min, double d_max,
+                                     double gamma1, double gamma2, double* out, int device);
 /* u = hash_unit_value(seed, flat_index) on active nodes (config.hpp:558-564). */
 int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed);
 /* Fills a property with a constant on active nodes. */

@@ -121,6 +121,7 @@ _SIGNATURES = [
     ("pd_stepper_stability_bound", C.c_int, [_P, _DP]),
     ("pd_stepper_snapshot_diag", C.c_int, [_P, C.POINTER(pd_diag)]),
     ("pd_stepper_run", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _DP, C.POINTER(pd_diag), _I64P]),
+    ("pd_stepper_step", C.c_int, [_P, C.c_int64, C.c_double, C.POINTER(pd_diag)]),
     ("pd_stepper_last_ms", C.c_int, [_P, _DP]),
     ("pd_stepper_launch_count", C.c_int, [_P, _I64P]),
     ("pd_build_sphere_pack_grid", C.c_int, [C.c_int, _I64P, _DP, _DP, C.c_int64, _DP, _DP, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
@@ -128,6 +129,8 @@ _SIGNATURES = [
     ("pd_grid_populate_diffusion", C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double]),
     ("pd_grid_fill_hash", C.c_int, [_P, C.c_int, C.c_uint64]),
     ("pd_grid_fill_const", C.c_int, [_P, C.c_int, C.c_double]),
+    ("pd_smooth_diffusion_coefficients", C.c_int, [_P, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double,
+                                                   _P, C.c_int]),
     ("pd_grid_create_full", C.c_int, [C.c_int, C.c_int, _I64P, _DP, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(_P)]),
     ("pd_grid_frap_init", C.c_int, [_P, C.c_int, C.c_int, _I64P, _I64P, C.c_double, _I64P, _I64P]),
     ("pd_grid_box_sum", C.c_int, [_P, C.c_int, _I64P, _I64P, _DP]),

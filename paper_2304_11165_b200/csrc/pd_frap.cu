@@ -194,7 +194,7 @@ int pd_grid_frap_init(pd_grid* g, int prop_u, int prop_d, const int64_t* lo, con
             PD_CUDA(cudaStreamSynchronize(g->stream));
             *region = (int64_t)h[0];
             *phase = (int64_t)h[1];
-            g->generation++;
+            note_write(g, -1);
         } catch (...) {
             pd_free(d_counts);
             throw;

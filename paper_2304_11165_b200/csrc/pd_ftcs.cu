@@ -38,7 +38,7 @@ __device__ __forceinline__ double max_left(double l, double r) { return (l < r) 
 // |x| >= 2^990 (or non-finite): a non-record step whose values are this large
 // could overflow the total mass, which the reference checks every step
 // (solver.hpp:514-515); such steps fall back to an exact mass evaluation.
-__device__ __forceinline__ bool is_huge(double x) { return !(fabs(x) < 0x1p990); }
+__device__ __forceinline__ bool is_huge(double x, double thr) { return !(fabs(x) < thr); }
 
 template <class T, int D, bool DIAG>
 __global__ void __launch_bounds__(Geo<D>::V) ftcs_step_kernel(StepArgs<T> a) {
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(Geo<D>::V) ftcs_step_kernel(StepArgs<T> a) {
         atomicOr(&a.flags[a.k], 1);
     }
     if constexpr (!DIAG) {
-        if (act && !bad && is_huge(v)) atomicOr(&a.flags[a.k], 2);
+        if (act && !bad && is_huge(v, a.huge_abs)) atomicOr(&a.flags[a.k], 2);
     } else {
         // per-chunk partials (solver.hpp:444-454)
         __syncthreads();  // tile no longer needed: reuse su as scratch
@@ -310,6 +310,11 @@ struct pd_stepper {
     double* d_region = nullptr;  // one per row of the batch
     std::vector<double> region_out;
     pdb::PeerState peer;  // fused multi-GPU halo push (pd_peer.cu)
+    int e_huge = 990;     // huge_exponent(): set at creation
+    uint64_t ver_phi = 0, ver_d = 0;  // prop versions the static state was built from
+    // run_simulation's per-step non-finite-mass check (solver.hpp:514-515);
+    // off for pd_stepper_step, which is FtcsStepper::step (returns the row)
+    bool check_mass = true;
 };
 
 namespace {
@@ -335,6 +340,60 @@ void march_build_for(pd_stepper* s, int64_t begin, int64_t end) {
         if (s->cfg.bc_type[f] == PD_BC_DIRICHLET) dir |= 1 << f;
     const void* dcol = g->cols[(size_t)g->column_of[(size_t)s->prop_d]];
     march_build(g, s->d_nbr, s->d_fluid, s->d_sink, dcol, dir, begin, end, &s->plan);
+}
+
+// Static per-run state derived from phi (fluid / sink bitmasks) and the
+// neighbour table (solver.hpp:206-215, 333-351).
+void build_predicates(pd_stepper* s) {
+    pd_grid* g = s->g;
+    if (g->n_chunks > 0) {
+        const void* phi = g->cols[(size_t)g->column_of[(size_t)s->prop_phi]];
+        const double sink_band = s->cfg.band_half_width * s->hmin;  // solver.hpp:212
+        const unsigned nb = (unsigned)g->n_chunks;
+        if (g->tbytes == 8) {
+            // wall = T(b_low) + T(eps)   (solver.hpp:210-211)
+            const double wall = (double)s->cfg.b_low + (double)s->cfg.boundary_epsilon;
+            if (g->dims == 3)
+                predicate_kernel<double, 3><<<nb, 512, 0, g->stream>>>(
+                    (const double*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+            else
+                predicate_kernel<double, 2><<<nb, 64, 0, g->stream>>>(
+                    (const double*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+        } else {
+            const float wall = (float)s->cfg.b_low + (float)s->cfg.boundary_epsilon;
+            if (g->dims == 3)
+                predicate_kernel<float, 3><<<nb, 512, 0, g->stream>>>(
+                    (const float*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+            else
+                predicate_kernel<float, 2><<<nb, 64, 0, g->stream>>>(
+                    (const float*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
+        }
+        PD_CUDA(cudaGetLastError());
+        const int blocks = (int)((g->n_chunks + 255) / 256);
+        if (g->dims == 3)
+            neighbor_kernel<3><<<blocks, 256, 0, g->stream>>>(
+                g->d_keys, g->d_table, g->n_chunks, g->cc[0], g->cc[1], g->cc[2], s->d_nbr);
+        else
+            neighbor_kernel<2><<<blocks, 256, 0, g->stream>>>(
+                g->d_keys, g->d_table, g->n_chunks, g->cc[0], g->cc[1], 1, s->d_nbr);
+        PD_CUDA(cudaGetLastError());
+    }
+    s->ver_phi = prop_version(g, s->prop_phi);
+    s->ver_d = prop_version(g, s->prop_d);
+}
+
+// phi or D was written since the stepper derived its static state (the
+// reference reads both on every step, solver.hpp:407-441): rebuild the
+// predicates and the march plan over the owned range.
+void refresh_if_stale(pd_stepper* s) {
+    pd_grid* g = s->g;
+    if (prop_version(g, s->prop_phi) == s->ver_phi && prop_version(g, s->prop_d) == s->ver_d) return;
+    build_predicates(s);
+    if (s->use_march) {
+        march_build_for(s, s->begin, s->end);
+        s->peer.flags_dirty = s->peer.on;
+    }
+    PD_CUDA(cudaStreamSynchronize(g->stream));
 }
 
 void validate(const pd_grid* g, const pd_sim_config* c, int prop_src,
@@ -394,6 +453,22 @@ void fill_args(const pd_stepper* s, StepArgs<T>& a, const void* u, void* un, dou
     a.p_mx = g->red.part[2];
     a.bad_key = s->d_bad;
     a.flags = s->d_flags;
+    a.huge_abs = std::ldexp(1.0, s->e_huge);
+    a.huge_hi = s->e_huge < -1022 ? 0u : (uint32_t)(s->e_huge + 1023) << 20;
+}
+
+// Exponent below which no value can make the step's total mass non-finite
+// (the reference checks pairwise_sum(partials) * cell_volume every step,
+// solver.hpp:264-267, 514-515): n_slots values of magnitude < 2^e sum, in
+// any order, to < n_slots * 2^e <= 2^1022, and times cell_volume stays finite
+// while n_slots * 2^e * max(1, cell_volume) <= 2^1022.
+int huge_exponent(const pd_grid* g) {
+    const double n_slots = std::max(1.0, (double)g->n_chunks * (g->dims == 3 ? 512.0 : 64.0));
+    double cv = 1.0;
+    for (int ax = 0; ax < g->dims; ++ax) cv *= g->spacing[ax];
+    const int ln = (int)std::ceil(std::log2(n_slots));
+    const int lc = cv > 1.0 ? (int)std::ceil(std::log2(cv)) : 0;
+    return std::max(-1100, 1022 - ln - lc);
 }
 
 // One step of the owned range with the fused halo push: wait for the
@@ -513,41 +588,16 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
             PD_CUDA(cudaEventCreate(&s->ev0));
             PD_CUDA(cudaEventCreate(&s->ev1));
-            if (g->n_chunks > 0) {
-                const void* phi = g->cols[(size_t)g->column_of[(size_t)prop_phi]];
-                const double sink_band = cfg->band_half_width * s->hmin;  // solver.hpp:212
-                const unsigned nb = (unsigned)g->n_chunks;
-                if (g->tbytes == 8) {
-                    // wall = T(b_low) + T(eps)   (solver.hpp:210-211)
-                    const double wall = (double)cfg->b_low + (double)cfg->boundary_epsilon;
-                    if (g->dims == 3)
-                        predicate_kernel<double, 3><<<nb, 512, 0, g->stream>>>(
-                            (const double*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
-                    else
-                        predicate_kernel<double, 2><<<nb, 64, 0, g->stream>>>(
-                            (const double*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
-                } else {
-                    const float wall = (float)cfg->b_low + (float)cfg->boundary_epsilon;
-                    if (g->dims == 3)
-                        predicate_kernel<float, 3><<<nb, 512, 0, g->stream>>>(
-                            (const float*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
-                    else
-                        predicate_kernel<float, 2><<<nb, 64, 0, g->stream>>>(
-                            (const float*)phi, g->d_masks, wall, sink_band, s->d_fluid, s->d_sink);
-                }
-                PD_CUDA(cudaGetLastError());
-                const int blocks = (int)((g->n_chunks + 255) / 256);
-                if (g->dims == 3)
-                    neighbor_kernel<3><<<blocks, 256, 0, g->stream>>>(
-                        g->d_keys, g->d_table, g->n_chunks, g->cc[0], g->cc[1], g->cc[2], s->d_nbr);
-                else
-                    neighbor_kernel<2><<<blocks, 256, 0, g->stream>>>(
-                        g->d_keys, g->d_table, g->n_chunks, g->cc[0], g->cc[1], 1, s->d_nbr);
-                PD_CUDA(cudaGetLastError());
-            }
+            build_predicates(s);
             ensure_scratch(g);
+            // 4 bits of margin: a sharded domain's global mass sums up to 16
+            // ranks' slots (shard.py)
+            s->e_huge = huge_exponent(g) - 4;
             const char* nm = getenv("PD_NO_MARCH");
             s->use_march = !(nm && nm[0] == '1');
+            // the FP32 march kernel has no huge-value check: float values
+            // (< 2^128) must not be able to overflow the double total mass
+            if (g->tbytes == 4 && s->e_huge < 129) s->use_march = false;
             if (s->use_march) march_build_for(s, 0, g->n_chunks);
             PD_CUDA(cudaStreamSynchronize(g->stream));
         } catch (...) {
@@ -638,6 +688,7 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
         if (n_steps <= 0) return;
         pd_grid* g = s->g;
         DeviceGuard dg(g->device);
+        refresh_if_stale(s);
         const pd_sim_config& c = s->cfg;
         const int64_t rec = c.record_every;
         double total_ms = 0.0;
@@ -688,8 +739,9 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
             total_ms += ms;
 
             int64_t fail_k = -1;
+            const int fail_mask = s->check_mass ? ~0 : 1;  // step(): only non-finite nodes throw
             for (int64_t k = 0; k < nb; ++k)
-                if (hflags[(size_t)k]) {
+                if (hflags[(size_t)k] & fail_mask) {
                     fail_k = k;
                     break;
                 }
@@ -745,6 +797,14 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
     });
 }
 
+int pd_stepper_step(pd_stepper* s, int64_t step_index, double factor, pd_diag* row) {
+    s->check_mass = false;
+    int64_t n = 0;
+    const int rc = pd_stepper_run(s, step_index, 1, step_index + 1, &factor, row, &n);
+    s->check_mass = true;
+    return rc;
+}
+
 int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t end, double factor) {
     return guarded([&] {
         pd_grid* g = s->g;
@@ -752,6 +812,7 @@ int pd_stepper_enqueue(pd_stepper* s, int64_t step_index, int64_t begin, int64_t
             fail(PD_E_INPUT, "enqueue range outside the stepper's owned range");
         if (end == begin) return;
         DeviceGuard dg(g->device);
+        refresh_if_stale(s);
         (void)step_index;  // steps are stream-ordered; errors accumulate in flags[0]
         const void* u = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
         void* un = g->cols[(size_t)g->column_of[(size_t)s->prop_next]];

@@ -15,6 +15,7 @@
 #include <limits>
 
 #include "pd_internal.cuh"
+#include "pd_libm_exp.h"
 
 namespace pdb {
 
@@ -186,7 +187,8 @@ __global__ void __launch_bounds__(Geo<D>::V)
 }
 
 // smooth_diffusion_coefficient (geometry.hpp:182-187) on active nodes
-// (populate_diffusion_channel, geometry.hpp:191-206).
+// (populate_diffusion_channel, geometry.hpp:191-206), with the reference's
+// libm exp restated bit for bit (pd_libm_exp.h): D is the reference's bits.
 template <class T, int D>
 __global__ void __launch_bounds__(Geo<D>::V)
     populate_d_kernel(const T* __restrict__ phi, T* __restrict__ d,
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(Geo<D>::V)
     const int off = threadIdx.x;
     if (!((masks[i * W + (off >> 6)] >> (off & 63)) & 1u)) return;
     const double p = (double)phi[i * V + off];
-    d[i * V + off] = (T)(dmin + dmax / (1.0 + exp(-(g1 + g2 * p))));
+    d[i * V + off] = (T)pd_smooth_diffusion(p, dmin, dmax, g1, g2);
 }
 
 // ---------------------------------------------------------------------------
@@ -697,7 +699,7 @@ int pd_grid_destroy(pd_grid* g) {
 
 int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs) {
     return guarded([&] {
-        g->generation++;
+        note_write(g, prop);
         DeviceGuard dg(g->device);
         void* c = col_ptr(g, prop);
         if (g->n_chunks == 0) return;
@@ -708,7 +710,7 @@ int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs) {
 
 int pd_grid_upload_device(pd_grid* g, int prop, const void* dev_slabs) {
     return guarded([&] {
-        g->generation++;
+        note_write(g, prop);
         DeviceGuard dg(g->device);
         void* c = col_ptr(g, prop);
         if (g->n_chunks == 0) return;
@@ -764,7 +766,8 @@ int pd_grid_swap(pd_grid* g, int a, int b) {
         check_prop(g, a);
         check_prop(g, b);
         std::swap(g->column_of[(size_t)a], g->column_of[(size_t)b]);
-        g->generation++;
+        note_write(g, a);
+        note_write(g, b);
     });
 }
 
@@ -777,7 +780,7 @@ int pd_grid_column_of(const pd_grid* g, int prop, int* column) {
 
 int pd_grid_device_ptr(pd_grid* g, int prop, void** ptr) {
     return guarded([&] {
-        g->generation++; *ptr = col_ptr(g, prop); });
+        note_write(g, prop); *ptr = col_ptr(g, prop); });
 }
 
 int pd_grid_info(const pd_grid* g, int64_t* n_chunks, int64_t* active_nodes) {
@@ -847,7 +850,7 @@ int pd_grid_max_active(pd_grid* g, int prop, double* out) {
 int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_min, double d_max,
                                double gamma1, double gamma2) {
     return guarded([&] {
-        g->generation++;
+        note_write(g, prop_d);
         if (d_min < 0.0) fail(PD_E_INPUT, "d_min must be non-negative");
         if (!(d_max > 0.0)) fail(PD_E_INPUT, "d_max must be positive");
         DeviceGuard dg(g->device);
@@ -867,7 +870,7 @@ int pd_grid_populate_diffusion(pd_grid* g, int prop_phi, int prop_d, double d_mi
 
 int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed) {
     return guarded([&] {
-        g->generation++;
+        note_write(g, prop);
         DeviceGuard dg(g->device);
         void* x = col_ptr(g, prop);
         if (g->n_chunks == 0) return;
@@ -882,9 +885,32 @@ int pd_grid_fill_hash(pd_grid* g, int prop, uint64_t seed) {
     });
 }
 
+__global__ void smooth_diffusion_kernel(const double* __restrict__ phi, double* __restrict__ out, int64_t n,
+                                        double dmin, double dmax, double g1, double g2) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = pd_smooth_diffusion(phi[i], dmin, dmax, g1, g2);
+}
+
+int pd_smooth_diffusion_coefficients(const double* phi, int64_t n, double d_min, double d_max,
+                                     double gamma1, double gamma2, double* out, int device) {
+    return guarded([&] {
+        if (d_min < 0.0) fail(PD_E_INPUT, "d_min must be non-negative");
+        if (!(d_max > 0.0)) fail(PD_E_INPUT, "d_max must be positive");
+        if (n <= 0) return;
+        DeviceGuard dg(device);
+        double* buf = nullptr;
+        PD_CUDA(cudaMalloc(&buf, 2 * n * sizeof(double)));
+        struct Free { double* p; ~Free() { cudaFree(p); } } fr{buf};
+        PD_CUDA(cudaMemcpy(buf, phi, n * sizeof(double), cudaMemcpyHostToDevice));
+        smooth_diffusion_kernel<<<148 * 8, 256>>>(buf, buf + n, n, d_min, d_max, gamma1, gamma2);
+        PD_CUDA(cudaGetLastError());
+        PD_CUDA(cudaMemcpy(out, buf + n, n * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
 int pd_grid_fill_const(pd_grid* g, int prop, double value) {
     return guarded([&] {
-        g->generation++;
+        note_write(g, prop);
         DeviceGuard dg(g->device);
         void* x = col_ptr(g, prop);
         if (g->n_chunks == 0) return;

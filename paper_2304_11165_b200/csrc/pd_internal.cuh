@@ -119,7 +119,23 @@ struct pd_grid {
     pdb::ReduceScratch red;
     double* d_row = nullptr;  // 3 doubles: mass, min, max
     uint64_t generation = 0;  // bumped by every host-visible write to a column
+    std::vector<uint64_t> prop_ver;  // per logical property: bumped by each write to it
 };
+
+// Records a write to logical property `prop` (all properties if prop < 0):
+// steppers compare the versions of phi and D before stepping and rebuild
+// their static predicates / march plan when either changed.
+inline void note_write(pd_grid* g, int prop) {
+    g->generation++;
+    if (g->prop_ver.size() < g->column_of.size()) g->prop_ver.resize(g->column_of.size(), 0);
+    if (prop < 0)
+        for (auto& v : g->prop_ver) ++v;
+    else if ((size_t)prop < g->prop_ver.size())
+        ++g->prop_ver[(size_t)prop];
+}
+inline uint64_t prop_version(const pd_grid* g, int prop) {
+    return (size_t)prop < g->prop_ver.size() ? g->prop_ver[(size_t)prop] : 0;
+}
 
 // A dense field on the device (pd_levelset.cu, pd_snapshot.cu).
 struct pd_field {
@@ -172,6 +188,12 @@ struct StepArgs {
     double* p_mx;
     unsigned long long* bad_key;  // (ordinal << 10) | offset, atomicMin
     int* flags;                   // per step of the batch: 1 bad, 2 huge, 4 mass
+    // "huge": |u_next| >= 2^e_huge, below which the step's total mass
+    // (pairwise_sum * cell_volume over <= n_slots values) cannot overflow;
+    // e_huge = 1022 - ceil(log2 n_slots) - max(0, ceil(log2 cell_volume))
+    // (huge_hi: the same as a high-word threshold on the absolute value)
+    double huge_abs;
+    uint32_t huge_hi;
     int k;                        // step index within the batch
     int64_t ord0;                 // first chunk ordinal of the launch
 };

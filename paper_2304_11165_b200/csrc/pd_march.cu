@@ -103,6 +103,7 @@ struct SlowConsts {
     double bcv[6];
     double dt, neg_k, src_factor;
     int dirichlet;
+    uint32_t huge_hi;
 };
 
 // Exact generic node update (solver.hpp:360-441) on already-loaded neighbour
@@ -205,9 +206,10 @@ __device__ __forceinline__ LaneGeo lane_geo(int lane) {
     return G;
 }
 
-// |x| >= 2^990 or non-finite, from the high word (integer pipe)
-__device__ __forceinline__ bool huge(double x) {
-    return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= 0x7DD00000u;
+// |x| >= 2^e_huge or non-finite, from the high word (integer pipe); hi is
+// StepArgs::huge_hi (e_huge depends on the grid's slot count and cell volume)
+__device__ __forceinline__ bool huge(double x, uint32_t hi) {
+    return ((unsigned)__double2hiint(x) & 0x7fffffffu) >= hi;
 }
 
 struct Consts {
@@ -245,11 +247,11 @@ __device__ __noinline__ double2 pair_slow(unsigned long long* bad_key, int* flag
     if (dirichlet) {  // the whole chunk takes the exact generic update
         if (!sentinel(dc0)) out0 = slow_node<REACTION>(K, uc0, dc0, nu0, nd0, gx, gy, gz, s0, src0);
         if (!sentinel(dc1)) out1 = slow_node<REACTION>(K, uc1, dc1, nu1, nd1, gx + 1, gy, gz, s1, src1);
-        h0 = a0 && huge(out0);
-        h1 = a1 && huge(out1);
+        h0 = a0 && huge(out0, K.huge_hi);
+        h1 = a1 && huge(out1, K.huge_hi);
     } else {  // a huge fast result: re-derive the non-finite ones exactly
-        h0 = a0 && huge(out0);
-        h1 = a1 && huge(out1);
+        h0 = a0 && huge(out0, K.huge_hi);
+        h1 = a1 && huge(out1, K.huge_hi);
         if (h0 && !isfinite(out0) && !sentinel(dc0))
             out0 = slow_node<REACTION>(K, uc0, dc0, nu0, nd0, gx, gy, gz, s0, src0);
         if (h1 && !isfinite(out1) && !sentinel(dc1))
@@ -473,7 +475,7 @@ __device__ __forceinline__ void compute14u(const MarchArgs& M, const SlowConsts&
     }
     double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
     double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
-    if (huge(out0) | huge(out1)) {
+    if (huge(out0, M.A.huge_hi) | huge(out1, M.A.huge_hi)) {
         const double2 r = pair_slow14<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
         out1 = r.y;
@@ -552,7 +554,7 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
         if (sentinel(dc.x)) out0 = uc.x;
         if (sentinel(dc.y)) out1 = uc.y;
     }
-    if ((C.flags & kFlagDirichlet) || ((a0 && huge(out0)) | (a1 && huge(out1)))) {
+    if ((C.flags & kFlagDirichlet) || ((a0 && huge(out0, M.A.huge_hi)) | (a1 && huge(out1, M.A.huge_hi)))) {
         const double2 r = pair_slow14<REACTION, HALF>(M, K, C, z, tm, t0, tp, G, out0, out1);
         out0 = r.x;
         out1 = r.y;
@@ -588,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
         K.neg_k = A.neg_k;
         K.src_factor = A.src_factor;
         K.dirichlet = A.dirichlet;
+        K.huge_hi = A.huge_hi;
     }
     __syncthreads();
     Consts Q;

@@ -96,7 +96,7 @@ int pd_grid_make_shareable(pd_grid* g) {
             g->cols[i] = p;
             g->col_ipc[i] = 1;
         }
-        g->generation++;
+        g->generation++;  // same data, new addresses
     });
 }
 

@@ -846,9 +846,17 @@ class FtcsStepper:
                 for r in rows[: nr.value]]
 
     def step(self, step_index: int = 0) -> StepDiagnostics:
-        """One validated step with diagnostics (solver.hpp:228-279)."""
-        rows = self.run(step_index, 1, step_index + 1)
-        return rows[0]
+        """One validated step with diagnostics (solver.hpp:228-279): a
+        non-finite node raises NumericError; a non-finite total mass is
+        returned in the row (only run_simulation checks it)."""
+        row = _lib.pd_diag()
+        fac = self._factors(step_index, 1)
+        t0 = _time.perf_counter()
+        rc = lib.pd_stepper_step(self.h, step_index, fac[0] if fac is not None else 1.0, C.byref(row))
+        self.grid._mark_device_newer(["u", scratch_channel])
+        _check(rc)
+        return StepDiagnostics(row.step, row.time, row.total_mass, row.min_u, row.max_u,
+                               _time.perf_counter() - t0)
 
     def set_region(self, lo, hi):
         a, b = DeviceGrid._box(lo, hi)

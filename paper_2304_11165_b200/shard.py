@@ -392,6 +392,23 @@ class Domain:
         pd._check(lib.pd_reduce_partials(self.dev.h, P(glob[0]), P(glob[1]), P(glob[2]), glob.shape[1], row))
         return row[0], row[1], row[2]
 
+    def close(self, stepper=None):
+        """Frees the rank's device state (stepper, peer mappings, grid,
+        exchange buffers)."""
+        self.torch.cuda.synchronize(self.device)
+        if stepper is not None:
+            self.lib.pd_stepper_destroy(stepper)
+        if self._ipc:
+            self.close_peer()
+        if self.world > 1:  # no rank frees memory a neighbour still maps
+            import torch.distributed as dist
+            dist.barrier()
+        self.dev.close()
+        for k in ("d_send_down", "d_send_up", "d_recv_down", "d_recv_up", "b_send_down", "b_send_up",
+                  "b_recv_down", "b_recv_up"):
+            setattr(self, k, None)
+        self.torch.cuda.empty_cache()
+
     def kernel_ms(self, stepper) -> float:
         """Average device time of one step kernel launch so far."""
         return self._kernel_ms / max(1, self._steps)

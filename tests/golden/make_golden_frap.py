@@ -30,6 +30,9 @@ CASES = {
                    dt_frac=0.4, dt_dmax=1.2, d_lo=0.2, d_hi=1.2, rel_tol=1e-2),
     "frap32": dict(n=32, count=40, r_min=0.1, r_max=0.15, seed=2024, bleach=0.25, t_final=0.05, n_samples=100,
                    dt_frac=0.4, dt_dmax=1.2, d_lo=0.2, d_hi=1.2, rel_tol=1e-3),
+    # SURVEY.md §8d second D_eff/tau KAT (64^3: 0.84242584501724482 / 1.1870481015210657)
+    "frap64": dict(n=64, count=40, r_min=0.1, r_max=0.15, seed=2024, bleach=0.25, t_final=0.05, n_samples=100,
+                   dt_frac=0.4, dt_dmax=1.2, d_lo=0.2, d_hi=1.2, rel_tol=1e-3),
 }
 
 

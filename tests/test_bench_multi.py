@@ -46,3 +46,23 @@ def test_multi_rank_bench_matches_single_rank(ranks):
     assert b["active_nodes"] == a["active_nodes"] and b["chunks"] == a["chunks"]
     fa, fb = a["final_diagnostics"], b["final_diagnostics"]
     assert (fa["total_mass"], fa["min_u"], fa["max_u"]) == (fb["total_mass"], fb["min_u"], fb["max_u"])
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`python bench.py --gpus 2` with no torchrun around it re-launches
+    itself with two ranks and reports n_gpus 2, per-rank
+    timings and the single-rank run's exact final diagnostics."""
+    args = ["--box", "256", "--steps", "4", "--warmup", "3", "--no-cpu", "--no-e2e"]
+    one = subprocess.run([sys.executable, "bench.py", "--gpus", "1"] + args, cwd=ROOT, capture_output=True, text=True,
+                         timeout=900)
+    assert one.returncode == 0, one.stderr[-3000:]
+    env = dict(os.environ, PD_BENCH_SAME_GPU="1", PD_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    two = subprocess.run([sys.executable, "bench.py", "--gpus", "2"] + args, cwd=ROOT, capture_output=True,
+                         text=True, timeout=900, env=env)
+    assert two.returncode == 0, (two.stdout[-2000:], two.stderr[-3000:])
+    a, b = _line(one.stdout), _line(two.stdout)
+    assert b["n_gpus"] == 2 and len(b["per_rank"]) == 2 and b["load_imbalance"] >= 0
+    assert sum(r["active_nodes"] for r in b["per_rank"]) == a["active_nodes"]
+    fa, fb = a["final_diagnostics"], b["final_diagnostics"]
+    assert (fa["total_mass"], fa["min_u"], fa["max_u"]) == (fb["total_mass"], fb["min_u"], fb["max_u"])

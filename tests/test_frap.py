@@ -26,6 +26,10 @@ def test_golden_pinned_to_survey_kat():
     g = GOLD["frap32"]
     assert hx(g["d_eff"]) == 0.83841401729453335
     assert hx(g["tau"]) == 1.1927281502602809
+    # the second KAT: 64^3, same pack and schedule
+    g = GOLD["frap64"]
+    assert hx(g["d_eff"]) == 0.84242584501724482
+    assert hx(g["tau"]) == 1.1870481015210657
 
 
 def test_reference_reproduces_golden_frap16(ref):
@@ -78,7 +82,7 @@ def _pack_grid(c):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["frap16", "frap32"])
+@pytest.mark.parametrize("name", ["frap16", "frap32", "frap64"])
 def test_frap_curve_and_fit_bitwise(name, cuda):
     from paper_2304_11165_b200 import analysis as an
     c = GOLD[name]
