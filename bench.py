@@ -66,6 +66,7 @@ def parse():
                     help="box edge of the end-to-end host-buffer run (0: the bench box when host RAM allows)")
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--cpu-calls", type=int, default=3, help="timed reference calls of the cpu_baseline leg")
+    ap.add_argument("--ref-threads", type=int, default=0, help="reference arm worker threads (0: all host cores)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -358,23 +359,7 @@ def run_ours(args):
             e2e = {"value": None, "unit": "GPts/s", "error": f"{type(e).__name__}: {e}"}
     cpu = None
     if not args.no_cpu and rank == 0:
-        try:
-            per = args.cpu_seconds / max(1, args.cpu_calls)
-            v, secs, st, a, cores = reference_rate(args, args.cpu_sample, args.cpu_calls, per)
-            cpu = {"value": v, "unit": "GPts/s", "cores": cores, "kind": "reference",
-                   "sample": f"reference_rate(): unmodified reference run_simulation (oracle/_ref, -O3 "
-                             f"-ffp-contract=off, {cores} std::thread workers of {host_cores()} host cores) on the "
-                             f"[0,{args.cpu_sample})^3 crop of the same geometry: {a} active nodes, "
-                             f"{args.cpu_calls} calls x {st} steps in {sum(secs):.2f} s (the reference arm's "
-                             f"protocol)"}
-            # SURVEY §8d also asks for the single-thread figure (RD_THREADS=1)
-            v1, secs1, st1, a1, _ = reference_rate(args, args.cpu_sample, 1, max(2.0, per / 2), threads=1,
-                                                   warm=False)
-            cpu["single_thread"] = {"value": v1, "unit": "GPts/s", "cores": 1,
-                                    "sample": f"same crop, 1 worker: {a1} active nodes x {st1} steps in "
-                                              f"{sum(secs1):.2f} s"}
-        except Exception as e:  # reported, not fatal
-            cpu = {"value": None, "unit": "GPts/s", "cores": None, "kind": "reference", "sample": f"failed: {e}"}
+        cpu = cpu_baseline_leg(args)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value / 1e9, "unit": "GPts/s", "n_gpus": world, "steps": args.steps,
@@ -397,6 +382,30 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_baseline_leg(args):
+    """The cpu_baseline object: the reference arm itself (`bench.py --impl
+    reference`, a fresh process that loads only oracle/_ref) on this box's
+    host cores, all threads and then one thread -- the same protocol and the
+    same process state as the driver's reference arm."""
+    common = ["--box", str(args.n), "--psi", str(args.psi), "--radius-vox", str(args.radius_vox),
+              "--seed", str(args.seed), "--cpu-sample", str(args.cpu_sample)]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = {}
+    for key, threads, steps, secs in (("all", 0, args.cpu_calls, args.cpu_seconds),
+                                      ("one", 1, 1, max(2.0, args.cpu_seconds / 4))):
+        cmd = [sys.executable, str(Path(__file__).resolve()), "--impl", "reference", "--steps", str(steps),
+               "--warmup", "1", "--cpu-seconds", str(secs), "--ref-threads", str(threads)] + common
+        try:
+            p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+            line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+            out[key] = json.loads(line[-1])["cpu_baseline"] if line else {"value": None, "sample": p.stderr[-400:]}
+        except Exception as e:  # reported, not fatal
+            out[key] = {"value": None, "sample": f"failed: {e}"}
+    cpu = dict(out["all"])
+    cpu["single_thread"] = out["one"]
+    return cpu
 
 
 def host_ram_bytes():
@@ -503,9 +512,10 @@ def run_reference(args):
         return
     per = max(0.5, args.cpu_seconds / max(1, args.steps))
     edge = args.cpu_sample
+    thr = args.ref_threads or None
     if args.warmup > 0:
-        reference_rate(args, edge, 1, 0.2, warm=False)
-    value, secs, st, active, cores = reference_rate(args, edge, args.steps, per)
+        reference_rate(args, edge, 1, 0.2, threads=thr, warm=False)
+    value, secs, st, active, cores = reference_rate(args, edge, args.steps, per, threads=thr)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GPts/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(secs) / args.steps * 1e3,
