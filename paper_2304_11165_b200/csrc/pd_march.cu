@@ -731,6 +731,288 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     if (PUSH && pushed) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------------
+// v20 (default): v14's per-node arithmetic and tile layout with a bulk-copy
+// load side. One elected lane per warp moves each staged plane with
+// cp.async.bulk (TMA bulk copies, UBLKCP): the own u plane and D_eff plane
+// (512 B each, contiguous in the column), the y-halo rows of the y
+// neighbours (64 B each) and the z-halo planes, completing on one mbarrier
+// per ring slot (expect_tx). Only the x-halo cells (8 B at a 64-B stride,
+// below the 16-B bulk granule) stay per-lane cp.async, tracked by the same
+// mbarrier (cp.async.mbarrier.arrive). This replaces v14's per-lane
+// predicated 16-B copies and their address / sentinel selection (~55 of
+// v14's ~265 warp instructions per plane). Whole planes are copied, inactive
+// slots included: their D_eff is the -inf sentinel in the plan's D_eff
+// array and their u is never used, so results are unchanged.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kBarOff20 = kRing14 * kTileBytes + 3 * kCtxBytes14;  // 8 mbarriers (8 B each)
+constexpr uint32_t kWarpBytes20 = kBarOff20 + 8u * kRing14;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+// the lane's prior cp.async copies arrive on bar when they complete (the
+// pending count is raised first, so the phase waits for them)
+__device__ __forceinline__ void cp_mbar_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+// Sources of one chunk's loads (element offsets; warp-uniform except the
+// x-halo fields).
+struct LoadCtx20 {
+    uint32_t own, zl, zh, yl, yh;  // own plane 0, z-halo planes, y-halo rows (plane 0)
+    uint32_t xo;                   // x-halo cell of this lane (plane 0)
+    bool ok, zlok, zhok, ylok, yhok, xok;
+    bool dl;                       // load D_eff (false for kFlagUnif chunks)
+};
+
+__device__ __forceinline__ LoadCtx20 make_load_ctx20(int c, int dv, int dbg, const LaneGeo& G,
+                                                     uint32_t sent_off) {
+    int nb[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) nb[f] = __shfl_sync(0xffffffffu, dv, 24 + f);
+    LoadCtx20 L;
+    L.ok = c >= 0;
+    L.dl = L.ok && !(__shfl_sync(0xffffffffu, dv, 31) & kFlagUnif);
+    L.own = L.ok ? (uint32_t)c * 512u : 0u;
+    L.zlok = L.ok && nb[4] >= 0 && !(dbg & 4);
+    L.zhok = L.ok && nb[5] >= 0 && !(dbg & 4);
+    // D_eff of a missing neighbour comes from the sentinel chunk (-inf)
+    L.zl = L.zlok ? (uint32_t)nb[4] * 512u + 448u : sent_off;
+    L.zh = L.zhok ? (uint32_t)nb[5] * 512u : sent_off;
+    L.ylok = L.ok && nb[2] >= 0 && !(dbg & 2);
+    L.yhok = L.ok && nb[3] >= 0 && !(dbg & 2);
+    L.yl = L.ylok ? (uint32_t)nb[2] * 512u + 56u : sent_off;
+    L.yh = L.yhok ? (uint32_t)nb[3] * 512u : sent_off;
+    const int jx = G.xp == 0 ? nb[0] : nb[1];
+    L.xok = L.ok && G.xface && jx >= 0 && !(dbg & 1);
+    L.xo = L.xok ? (uint32_t)jx * 512u + (uint32_t)G.y * 8u + (G.xp == 0 ? 7u : 0u) : sent_off + G.bp;
+    return L;
+}
+
+// Load i (0..9, warp-uniform) of a chunk into the ring slot at st, completing
+// on bar: i = 0 / 9 the z-halo planes (plane 7 of the z- neighbour, plane 0
+// of the z+ neighbour), i = 1..8 own plane i-1 with its x / y halos.
+__device__ __forceinline__ void issue20(uint32_t st, uint32_t bar, const double* __restrict__ u,
+                                        const double* __restrict__ de, const LoadCtx20& L, int i,
+                                        const LaneGeo& G, int lane) {
+    const bool body = i >= 1 && i <= 8;
+    const uint32_t p64 = body ? (uint32_t)(i - 1) * 64u : 0u;
+    if (body) {  // x-halo cells: per-lane 8-B copies (x-face lanes)
+        const uint32_t ox = L.xo + (L.xok ? p64 : 0u);
+        cp8_ud(st + G.s_hx, u + ox, L.xok, st + kDOff + G.s_hx, de + ox, G.xface && L.dl);
+    }
+    cp_mbar_arrive(bar);
+    __syncwarp();
+    if (lane == 0) {
+        // the ring slot's previous contents were read through the generic
+        // proxy (all lanes, ordered by the __syncwarp); order those reads
+        // before the async-proxy writes below
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        bool pu;
+        uint32_t src;
+        if (body) {
+            pu = L.ok;
+            src = L.own + p64;
+        } else {
+            pu = i == 0 ? L.zlok : L.zhok;
+            src = i == 0 ? L.zl : L.zh;
+        }
+        uint32_t bytes = (pu ? 512u : 0u) + (L.dl ? 512u : 0u);
+        if (body) bytes += (L.ylok ? 64u : 0u) + (L.yhok ? 64u : 0u) + (L.dl ? 128u : 0u);
+        mbar_arrive_tx(bar, bytes);
+        if (pu) bulk_g2s(st + 64u, u + src, 512u, bar);
+        if (L.dl) bulk_g2s(st + kDOff + 64u, de + src, 512u, bar);
+        if (body) {
+            const uint32_t yl = L.yl + (L.ylok ? p64 : 0u), yh = L.yh + (L.yhok ? p64 : 0u);
+            if (L.ylok) bulk_g2s(st, u + yl, 64u, bar);
+            if (L.yhok) bulk_g2s(st + 576u, u + yh, 64u, bar);
+            if (L.dl) {
+                bulk_g2s(st + kDOff, de + yl, 64u, bar);
+                bulk_g2s(st + kDOff + 576u, de + yh, 64u, bar);
+            }
+        }
+    }
+}
+
+template <int REACTION, bool PUSH, bool HALF>
+__global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march20_kernel(MarchArgs M) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+        K.huge_hi = A.huge_hi;
+    }
+    __syncthreads();
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    LaneGeo G = lane_geo(lane);
+    // opaque copies: ptxas cannot rematerialise a shuffle result inside the
+    // plane loop, so the lane constants stay in registers
+    G.s_c = __shfl_sync(0xffffffffu, G.s_c, lane);
+    G.s_l = __shfl_sync(0xffffffffu, G.s_l, lane);
+    G.s_r = __shfl_sync(0xffffffffu, G.s_r, lane);
+    G.s_hx = __shfl_sync(0xffffffffu, G.s_hx, lane);
+    G.bp = __shfl_sync(0xffffffffu, G.bp, lane);
+    uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw) + (uint32_t)warp * kWarpBytes20;
+    sb = __shfl_sync(0xffffffffu, sb, lane);
+    G.xface = __shfl_sync(0xffffffffu, (int)G.xface, lane) != 0;
+    const uint32_t bars = sb + kBarOff20;
+    if (lane < kRing14) mbar_init(bars + 8u * (uint32_t)lane, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    double* __restrict__ un = A.un;
+    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
+
+    // chunk pipeline: as v14 (context ring, claims 3 chunks ahead)
+    int* ctr_l = M.counter + ((t >> 5) & M.zero);
+    const int n = (int)M.n;
+    const uint32_t cb = sb + kRing14 * kTileBytes;  // context ring
+    auto cent = [&](int e) -> uint32_t { return cb + (uint32_t)e * kCtxBytes14; };
+    int raw = 0;
+    auto claim_issue = [&]() {
+        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(raw) : "l"(ctr_l) : "memory");
+    };
+    auto sched_sync = [&]() -> int {
+        claim_issue();
+        const int p = __shfl_sync(0xffffffffu, raw, 0);
+        return p < n ? __ldg(&M.sched[p]) : -1;
+    };
+    auto fetch_ctx = [&](uint32_t e, int c) {  // masks + descriptor + uniform D of chunk c into entry e
+        cp4(e + 4u * (uint32_t)lane, M.lm + (int64_t)(c < 0 ? 0 : c) * 32 + lane, c >= 0);
+        cp4(e + 128u + 4u * (uint32_t)(lane & 7), M.desc + (int64_t)(c < 0 ? 0 : c) * 8 + (lane & 7),
+            c >= 0 && lane < 8);
+        cp4(e + 168u + 4u * (uint32_t)(lane & 1),
+            reinterpret_cast<const uint32_t*>(M.dv + (c < 0 ? 0 : c)) + (lane & 1), c >= 0 && lane < 2);
+    };
+    {
+        const int id0 = sched_sync();
+        if (id0 < 0) return;
+        const int id1 = sched_sync();
+        if (lane == 0) {
+            sts_u32(cent(0) + 160u, (uint32_t)id0);
+            sts_u32(cent(1) + 160u, (uint32_t)id1);
+        }
+        fetch_ctx(cent(0), id0);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        claim_issue();
+    }
+    int ek = 0;  // entry of the load-side chunk
+    ChunkCtx14 Cld;
+    LoadCtx20 Lld;
+    auto advance = [&]() {
+        const uint32_t e0 = cent(ek);
+        const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
+        const uint32_t e1 = cent(e1i), e2 = cent(e2i);
+        const int c = (int)lds_u32(e0 + 160u);
+        const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
+        // descriptor word j lives at lane 24 + j (make_load_ctx20 / ChunkCtx14)
+        const int dv = (int)lds_u32(e0 + 128u + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
+        Cld = ChunkCtx14{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm,
+                         lds1(e0 + 168u)};
+        Lld = make_load_ctx20(c, c >= 0 ? dv : -1, M.dbg, G, sent_off);
+        const int c1 = (int)lds_u32(e1 + 160u);
+        fetch_ctx(e1, c1);
+        if (lane == 0) {
+            const bool ok = raw < n;
+            cp4(e2 + 160u, M.sched + (ok ? raw : 0), ok);
+            if (!ok) sts_u32(e2 + 160u, 0xFFFFFFFFu);
+        }
+        claim_issue();
+        ek = e1i;
+    };
+    advance();
+    int p_ld = 0;     // next load index (0..9) of the load-side chunk
+    uint32_t Lc = 0;  // loads issued
+    auto issue_next = [&]() {
+        const uint32_t slot = Lc & (kRing14 - 1);
+        issue20(sb + slot * kTileBytes, bars + 8u * slot, u, de, Lld, p_ld, G, lane);
+        if (++p_ld == 10) {  // the load side moves on to the next chunk
+            p_ld = 0;
+            advance();
+        }
+        ++Lc;
+    };
+    auto wait_load = [&](uint32_t l) { mbar_wait(bars + 8u * (l & (kRing14 - 1)), (l >> 3) & 1u); };
+    ChunkCtx14 Cc = Cld;
+    uint32_t base = 0;  // load index of plane -1 of Cc
+    bool pushed = false;
+#pragma unroll 1
+    for (int k = 0; k < 3 + kAhead14; ++k) issue_next();
+#pragma unroll 1
+    while (Cc.c >= 0) {
+        wait_load(base);
+        wait_load(base + 1u);
+#pragma unroll 1
+        for (int z = 0; z < 8; ++z) {
+            const uint32_t b = base + (uint32_t)z;
+            wait_load(b + 2u);
+            compute14<REACTION, PUSH, HALF>(M, K, Q, Cc, z, sb + (b & 7u) * kTileBytes,
+                                            sb + ((b + 1u) & 7u) * kTileBytes, sb + ((b + 2u) & 7u) * kTileBytes,
+                                            G, un, pushed);
+            __syncwarp();
+            issue_next();
+            if (z == 7) {  // plane 8 of this chunk and plane -1 of the next
+                issue_next();
+                issue_next();
+            }
+        }
+        base += 10u;
+        Cc = Cld;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    // the pushed planes are visible system-wide before this kernel completes
+    // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
+    if (PUSH && pushed) __threadfence_system();
+}
+
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 // desc flags of the fused halo push: bit set iff the chunk has a peer ghost
@@ -1060,34 +1342,34 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.n_all = g->n_chunks;
     static const int ver = [] {
         const char* e = getenv("PD_MARCH_V");
-        return e ? atoi(e) : 14;
+        return e ? atoi(e) : 20;
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
-    if (pl && ver != 14) fail(PD_E_INPUT, "the fused peer halo push needs march v14 (PD_MARCH_V unset)");
-    {
-        constexpr size_t bytes = (size_t)kWarpBytes14 * kWarps;
-        static const KernT table[2][2][3] = {  // [half][push][reaction]
-            {{ftcs_march14_kernel<0, false, false>, ftcs_march14_kernel<1, false, false>,
-              ftcs_march14_kernel<2, false, false>},
-             {ftcs_march14_kernel<0, true, false>, ftcs_march14_kernel<1, true, false>,
-              ftcs_march14_kernel<2, true, false>}},
-            {{ftcs_march14_kernel<0, false, true>, ftcs_march14_kernel<1, false, true>,
-              ftcs_march14_kernel<2, false, true>},
-             {ftcs_march14_kernel<0, true, true>, ftcs_march14_kernel<1, true, true>,
-              ftcs_march14_kernel<2, true, true>}}};
-        static bool attr_set = false;
-        if (!attr_set) {
-            for (auto& half : table)
-                for (auto& row : half)
-                    for (auto k : row)
+#define PD_M_TABLE(K)                                                                            \
+    {{{K<0, false, false>, K<1, false, false>, K<2, false, false>},                              \
+      {K<0, true, false>, K<1, true, false>, K<2, true, false>}},                                \
+     {{K<0, false, true>, K<1, false, true>, K<2, false, true>},                                 \
+      {K<0, true, true>, K<1, true, true>, K<2, true, true>}}}
+    static const KernT t14[2][2][3] = PD_M_TABLE(ftcs_march14_kernel);  // [half][push][reaction]
+    static const KernT t20[2][2][3] = PD_M_TABLE(ftcs_march20_kernel);
+#undef PD_M_TABLE
+    const bool v20 = ver != 14;
+    const size_t bytes = (size_t)(v20 ? kWarpBytes20 : kWarpBytes14) * kWarps;
+    // the dynamic shared-memory opt-in is per device: set it once per device
+    static uint64_t attr_done[2] = {0, 0};
+    const int dev = g->device;
+    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
+    if (!((attr_done[v20] >> dev) & 1u)) {
+        for (auto& half : (v20 ? t20 : t14))
+            for (auto& row : half)
+                for (auto k : row)
                     PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-            attr_set = true;
-        }
-        int sms = 148;
-        PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-        table[p.half ? 1 : 0][pl ? 1 : 0][r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);
+        attr_done[v20] |= 1ull << dev;
     }
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    (v20 ? t20 : t14)[p.half ? 1 : 0][pl ? 1 : 0][r]<<<sms * kCtas14, kThreads, bytes, g->stream>>>(M);
     PD_CUDA(cudaGetLastError());
 }
 
