@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
 }
 
 // ---------------------------------------------------------------------------
-// v20 (default): v14's per-node arithmetic and tile layout with a bulk-copy
+// v20 (PD_MARCH_V=20, measured and kept for A/B): v14's per-node arithmetic and tile layout with a bulk-copy
 // load side. One elected lane per warp moves each staged plane with
 // cp.async.bulk (TMA bulk copies, UBLKCP): the own u plane and D_eff plane
 // (512 B each, contiguous in the column), the y-halo rows of the y
@@ -744,6 +744,10 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
 // v14's ~265 warp instructions per plane). Whole planes are copied, inactive
 // slots included: their D_eff is the -inf sentinel in the plan's D_eff
 // array and their u is never used, so results are unchanged.
+// Measured (profiles/r02_ab_v14_v20.txt): bitwise equal, DRAM unchanged, but
+// 1.34x slower: each single-lane cp.async.bulk compiles to an R2UR waterfall
+// of ~14 issue slots, so 6 copies per plane cost more than v14's per-lane
+// LDGSTS (one warp instruction per 512 B).
 // ---------------------------------------------------------------------------
 constexpr uint32_t kBarOff20 = kRing14 * kTileBytes + 3 * kCtxBytes14;  // 8 mbarriers (8 B each)
 constexpr uint32_t kWarpBytes20 = kBarOff20 + 8u * kRing14;
@@ -1342,7 +1346,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.n_all = g->n_chunks;
     static const int ver = [] {
         const char* e = getenv("PD_MARCH_V");
-        return e ? atoi(e) : 20;
+        return e ? atoi(e) : 14;
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
