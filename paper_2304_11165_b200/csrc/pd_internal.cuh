@@ -206,6 +206,7 @@ struct MarchPlan {
     void* d_dv = nullptr;          // per chunk: uniform D_eff of kFlagUnif chunks (grid scalar type)
     int* d_counter = nullptr;      // per-step dynamic batch counters
     uint32_t* d_lm = nullptr;      // per chunk and lane: active / sink bits [c][32]
+    uint32_t* d_ctx = nullptr;     // v30: packed chunk record [c][44]: lm[32] | desc[8] | dv | pad
     int grid = 0;
     int64_t n = 0;
     bool ready = false;

@@ -51,6 +51,9 @@
 #include <numeric>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "pd_internal.cuh"
 
 namespace pdb {
@@ -1017,6 +1020,362 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march20_kernel(MarchAr
     if (PUSH && pushed) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------------
+// v30: CTA-staged chunk pipeline fed by TMA.
+// * A CTA = 4 compute warps + 1 producer warp; 4 CTAs per SM. The CTA works
+//   on one chunk at a time per stage; compute warp w owns planes 2w and 2w+1
+//   of the chunk, lane (y, xp) the x-pairs (2xp, 2xp+1) of row y: 4 nodes per
+//   lane, the two own planes being each other's z neighbours.
+// * Three 16.25 KB stages per CTA. One elected producer thread moves a whole
+//   chunk per stage with ~15 asynchronous copies completing on the stage's
+//   "full" mbarrier: the chunk record (lane masks, descriptor, uniform D;
+//   176 B), the own u and D_eff slabs (4 KB bulk copies each), the x-halo
+//   columns and y-halo rows of the four lateral neighbours (4-D TMA tensor
+//   boxes {2,8,8,1} / {8,1,8,1} over the [chunk][z][y][x] columns) and the
+//   two z-halo planes (512-B bulk copies). A v14 plane load needed ~60 warp
+//   instructions per 512 B; here one instruction moves up to 4 KB.
+// * The compute warps release a stage on its "empty" mbarrier; the producer
+//   runs up to three chunks ahead, its claim -> schedule -> descriptor chain
+//   software-pipelined two chunks deep.
+// * Missing lateral / z neighbours: D_eff comes from the sentinel chunk
+//   (-inf), u is not copied (never used, the face term is substituted).
+//   Uniform chunks (kFlagUnif) copy no D_eff at all.
+// * Per-node arithmetic, walls, reactions, rare path, push: as v14 (same
+//   expressions, same order), so results are bitwise identical.
+// ---------------------------------------------------------------------------
+constexpr int kW30 = 4;                        // compute warps per CTA
+constexpr int kThreads30 = 32 * (kW30 + 1);    // + one producer warp
+constexpr int kStages30 = 3;
+constexpr int kCtas30 = 4;
+// stage layout (bytes): the D_eff half mirrors the u half at +kDHalf30
+constexpr uint32_t kOwn30 = 0;      // [z][y][x] own slab (4096)
+constexpr uint32_t kYL30 = 4096;    // [z][x]    y- neighbour's row 7 (512)
+constexpr uint32_t kYH30 = 4608;    // [z][x]    y+ neighbour's row 0 (512)
+constexpr uint32_t kXL30 = 5120;    // [z][y][2] x- neighbour's columns 6..7 (1024)
+constexpr uint32_t kXH30 = 6144;    // [z][y][2] x+ neighbour's columns 0..1 (1024)
+constexpr uint32_t kZL30 = 7168;    // [y][x]    z- neighbour's plane 7 (512)
+constexpr uint32_t kZH30 = 7680;    // [y][x]    z+ neighbour's plane 0 (512)
+constexpr uint32_t kDHalf30 = 8192;
+constexpr uint32_t kCtx30 = 16384;  // chunk record (176 B), then the chunk id at +176
+constexpr uint32_t kCtxWords30 = 44;
+constexpr uint32_t kStage30 = 16384 + 256;
+constexpr uint32_t kBar30 = kStages30 * kStage30;  // full[3] then empty[3]
+constexpr uint32_t kSmem30 = kBar30 + 8u * 2u * kStages30;
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma4(uint32_t dst, const CUtensorMap* map, int x, int y, int z, int c, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(c), "r"(bar)
+        : "memory");
+}
+
+// Shared-memory byte addresses (u side; D_eff at +kDHalf30) of one plane's
+// operands for the lane: own pair, z- / z+ pairs, y- / y+ pairs, x- / x+ cells.
+struct Addr30 {
+    uint32_t c, zm, zp, ym, yp, l, r;
+};
+
+// Rare path: operands re-read from the stage, exact generic update and the
+// error / mass flags (solver.hpp:360-455, 250-260, 514-515).
+template <int REACTION, bool HALF>
+__device__ __noinline__ double2 pair_slow30(const MarchArgs& M, const SlowConsts& K, const ChunkCtx14& C, int z,
+                                            int xp, int y, uint32_t bp, Addr30 a, double out0, double out1) {
+    const bool un = (C.flags & kFlagUnif) != 0;  // no D_eff in the stage: every d is dv
+    const double2 vv = make_double2(C.dv, C.dv);
+    const double2 uc = lds2(a.c), dc0 = un ? vv : lds2(a.c + kDHalf30);
+    const double uL = lds1(a.l), dL0 = un ? C.dv : lds1(a.l + kDHalf30);
+    const double uR = lds1(a.r), dR0 = un ? C.dv : lds1(a.r + kDHalf30);
+    const double2 uym = lds2(a.ym), dym0 = un ? vv : lds2(a.ym + kDHalf30);
+    const double2 uyp = lds2(a.yp), dyp0 = un ? vv : lds2(a.yp + kDHalf30);
+    const double2 uzm = lds2(a.zm), dzm0 = un ? vv : lds2(a.zm + kDHalf30);
+    const double2 uzp = lds2(a.zp), dzp0 = un ? vv : lds2(a.zp + kDHalf30);
+    auto dd = [](double h) { return HALF ? h + h : h; };
+    auto dd2 = [&](double2 h) { return make_double2(dd(h.x), dd(h.y)); };
+    const double2 dc = dd2(dc0), dym = dd2(dym0), dyp = dd2(dyp0), dzm = dd2(dzm0), dzp = dd2(dzp0);
+    const double dL = dd(dL0), dR = dd(dR0);
+    const bool s0 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (16 + 2 * z)) & 1u);
+    const bool s1 = REACTION == PD_REACTION_SURFACE_SINK && ((C.lm >> (17 + 2 * z)) & 1u);
+    double src0 = 0.0, src1 = 0.0;
+    if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const double* sp = M.A.src + (int64_t)C.c * 512 + z * 64 + bp;
+        src0 = sp[0];
+        src1 = sp[1];
+    }
+    const double nu0[6] = {uL, uc.y, uym.x, uyp.x, uzm.x, uzp.x};
+    const double nd0[6] = {dL, dc.y, dym.x, dyp.x, dzm.x, dzp.x};
+    const double nu1[6] = {uc.x, uR, uym.y, uyp.y, uzm.y, uzp.y};
+    const double nd1[6] = {dc.x, dR, dym.y, dyp.y, dzm.y, dzp.y};
+    return pair_slow<REACTION>(M.A.bad_key, M.A.flags + M.A.k, K, C.c, C.key, C.flags, C.lm, z, xp, y, nu0, nd0,
+                               nu1, nd1, uc.x, uc.y, dc.x, dc.y, s0, s1, src0, src1, out0, out1);
+}
+
+// One plane of one lane (v14's compute14 / compute14u arithmetic). uc / dc
+// (own pair) and the z neighbours are passed in registers (the warp's two
+// planes share them); the lateral neighbours are read here.
+template <int REACTION, bool PUSH, bool HALF>
+__device__ __forceinline__ void compute30(const MarchArgs& M, const SlowConsts& K, const Consts& Q,
+                                          const ChunkCtx14& C, int z, int xp, int y, uint32_t bp, const Addr30& a,
+                                          double2 uc, double2 dc, double2 uzm, double2 dzm, double2 uzp,
+                                          double2 dzp, double* __restrict__ un, bool& pushed) {
+    const uint32_t lz = C.lm >> (2 * z);
+    const bool unif = (C.flags & kFlagUnif) != 0;  // warp-uniform
+    const double uL = lds1(a.l), uR = lds1(a.r);
+    const double2 uym = lds2(a.ym), uyp = lds2(a.yp);
+    bool a0, a1, interior;
+    double fxl, fxi, fxr, fy0m, fy0p, fz0m, fz0p, fy1m, fy1p, fz1m, fz1p;
+    if (unif) {
+        a0 = a1 = interior = true;
+        const double dh = HALF ? C.dv + C.dv : (C.dv + C.dv) * 0.5;
+        fxl = dh * (uc.x - uL);
+        fxi = dh * (uc.y - uc.x);
+        fxr = dh * (uR - uc.y);
+        fy0m = dh * (uc.x - uym.x);
+        fy0p = dh * (uyp.x - uc.x);
+        fz0m = dh * (uc.x - uzm.x);
+        fz0p = dh * (uzp.x - uc.x);
+        fy1m = dh * (uc.y - uym.y);
+        fy1p = dh * (uyp.y - uc.y);
+        fz1m = dh * (uc.y - uzm.y);
+        fz1p = dh * (uzp.y - uc.y);
+    } else {
+        a0 = lz & 1u;
+        a1 = (lz >> 1) & 1u;
+        const double dL = lds1(a.l + kDHalf30), dR = lds1(a.r + kDHalf30);
+        const double2 dym = lds2(a.ym + kDHalf30), dyp = lds2(a.yp + kDHalf30);
+        interior = (C.flags >> (8 + z)) & 1;  // warp-uniform: no walls, no substitution
+        if (interior) {
+            fxl = fface<HALF>(dL, dc.x, uL, uc.x);
+            fxi = fface<HALF>(dc.x, dc.y, uc.x, uc.y);
+            fxr = fface<HALF>(dc.y, dR, uc.y, uR);
+            fy0m = fface<HALF>(dym.x, dc.x, uym.x, uc.x);
+            fy0p = fface<HALF>(dc.x, dyp.x, uc.x, uyp.x);
+            fz0m = fface<HALF>(dzm.x, dc.x, uzm.x, uc.x);
+            fz0p = fface<HALF>(dc.x, dzp.x, uc.x, uzp.x);
+            fy1m = fface<HALF>(dym.y, dc.y, uym.y, uc.y);
+            fy1p = fface<HALF>(dc.y, dyp.y, uc.y, uyp.y);
+            fz1m = fface<HALF>(dzm.y, dc.y, uzm.y, uc.y);
+            fz1p = fface<HALF>(dc.y, dzp.y, uc.y, uzp.y);
+        } else {
+            fxl = face<HALF>(dL, dc.x, uL, uc.x);
+            fxi = face<HALF>(dc.x, dc.y, uc.x, uc.y);
+            fxr = face<HALF>(dc.y, dR, uc.y, uR);
+            fy0m = face<HALF>(dym.x, dc.x, uym.x, uc.x);
+            fy0p = face<HALF>(dc.x, dyp.x, uc.x, uyp.x);
+            fz0m = face<HALF>(dzm.x, dc.x, uzm.x, uc.x);
+            fz0p = face<HALF>(dc.x, dzp.x, uc.x, uzp.x);
+            fy1m = face<HALF>(dym.y, dc.y, uym.y, uc.y);
+            fy1p = face<HALF>(dc.y, dyp.y, uc.y, uyp.y);
+            fz1m = face<HALF>(dzm.y, dc.y, uzm.y, uc.y);
+            fz1p = face<HALF>(dc.y, dzp.y, uc.y, uzp.y);
+        }
+    }
+    double lap0 = 0.0;  // lap starts at T{0} (solver.hpp:420)
+    lap0 += (fxi - fxl) * Q.ix;
+    lap0 += (fy0p - fy0m) * Q.iy;
+    lap0 += (fz0p - fz0m) * Q.iz;
+    double lap1 = 0.0;
+    lap1 += (fxr - fxi) * Q.ix;
+    lap1 += (fy1p - fy1m) * Q.iy;
+    lap1 += (fz1p - fz1m) * Q.iz;
+    double r0 = 0.0, r1 = 0.0;
+    if (REACTION == PD_REACTION_SURFACE_SINK) {
+        r0 = ((lz >> 16) & 1u) ? Q.neg_k * uc.x : 0.0;
+        r1 = ((lz >> 17) & 1u) ? Q.neg_k * uc.y : 0.0;
+    } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+        const double* sp = M.A.src + (int64_t)C.c * 512 + z * 64 + bp;
+        r0 = sp[0] * Q.src_factor;
+        r1 = sp[1] * Q.src_factor;
+    }
+    double out0 = uc.x + Q.dt * lap0 + Q.dt * r0;
+    double out1 = uc.y + Q.dt * lap1 + Q.dt * r1;
+    if (!interior) {  // walls stay frozen (solver.hpp:413-417)
+        if (sentinel(dc.x)) out0 = uc.x;
+        if (sentinel(dc.y)) out1 = uc.y;
+    }
+    if ((C.flags & kFlagDirichlet) || ((a0 && huge(out0, M.A.huge_hi)) | (a1 && huge(out1, M.A.huge_hi)))) {
+        const double2 r = pair_slow30<REACTION, HALF>(M, K, C, z, xp, y, bp, a, out0, out1);
+        out0 = r.x;
+        out1 = r.y;
+    }
+    stg_pair(un + ((uint32_t)C.c * 512u + (uint32_t)z * 64u + bp), out0, out1, a0, a1);
+    if (PUSH && (C.flags & (kFlagPushLo | kFlagPushHi)) && (z == 0 || z == 7)) {
+        push_pair14(M, C, z, bp, out0, out1, a0, a1);
+        pushed = true;
+    }
+}
+
+template <int REACTION, bool PUSH, bool HALF>
+__global__ void __launch_bounds__(kThreads30, kCtas30)
+    ftcs_march30_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
+                        const __grid_constant__ CUtensorMap mux, const __grid_constant__ CUtensorMap muy,
+                        const __grid_constant__ CUtensorMap mdx, const __grid_constant__ CUtensorMap mdy) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = sm0 + kBar30, empty0 = full0 + 8u * kStages30;
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+        K.huge_hi = A.huge_hi;
+        for (int s = 0; s < kStages30; ++s) {
+            mbar_init(full0 + 8u * s, 1u);
+            mbar_init(empty0 + 8u * s, (uint32_t)kW30);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    const int n = (int)M.n;
+
+    if (warp == kW30) {  // ---------------- producer (one thread) ----------------
+        if (lane != 0) return;
+        int* ctr = M.counter;
+        auto claim = [&]() -> int {
+            int r;
+            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(ctr) : "memory");
+            return r;
+        };
+        auto id_of = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
+        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
+        const int sent_c = (int)M.n_all;  // D_eff sentinel chunk
+        // pipeline: chunk k's id and descriptor halves are loaded one
+        // iteration ahead, its schedule position two iterations ahead
+        int c_cur = id_of(claim());
+        int p_next = claim();
+        int4 d0 = c_cur >= 0 ? __ldg(desc4 + 2 * (int64_t)c_cur) : make_int4(0, 0, 0, 0);
+        int4 d1 = c_cur >= 0 ? __ldg(desc4 + 2 * (int64_t)c_cur + 1) : make_int4(0, 0, 0, 0);
+#pragma unroll 1
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t s = k % kStages30, ph = (k / kStages30) & 1u;
+            const int c_nxt = id_of(p_next);
+            if (c_cur >= 0) p_next = claim();
+            const uint32_t st = sm0 + s * kStage30, full = full0 + 8u * s;
+            if (k >= (uint32_t)kStages30) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+            sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
+            if (c_cur < 0) {  // end marker: the compute warps stop at this stage
+                mbar_arrive(full);
+                break;
+            }
+            const int nb0 = d0.x, nb1 = d0.y, nb2 = d0.z, nb3 = d0.w, nb4 = d1.x, nb5 = d1.y;
+            const bool dl = !(d1.w & kFlagUnif);
+            uint32_t bytes = 176u + 4096u;
+            bytes += (nb0 >= 0 ? 1024u : 0u) + (nb1 >= 0 ? 1024u : 0u) + (nb2 >= 0 ? 512u : 0u) +
+                     (nb3 >= 0 ? 512u : 0u) + (nb4 >= 0 ? 512u : 0u) + (nb5 >= 0 ? 512u : 0u);
+            if (dl) bytes += 4096u + 2u * 1024u + 4u * 512u;
+            mbar_arrive_tx(full, bytes);
+            const int64_t cb = (int64_t)c_cur * 512;
+            bulk_g2s(st + kCtx30, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
+            bulk_g2s(st + kOwn30, u + cb, 4096u, full);
+            if (nb0 >= 0) tma4(st + kXL30, &mux, 6, 0, 0, nb0, full);
+            if (nb1 >= 0) tma4(st + kXH30, &mux, 0, 0, 0, nb1, full);
+            if (nb2 >= 0) tma4(st + kYL30, &muy, 0, 7, 0, nb2, full);
+            if (nb3 >= 0) tma4(st + kYH30, &muy, 0, 0, 0, nb3, full);
+            if (nb4 >= 0) bulk_g2s(st + kZL30, u + (int64_t)nb4 * 512 + 448, 512u, full);
+            if (nb5 >= 0) bulk_g2s(st + kZH30, u + (int64_t)nb5 * 512, 512u, full);
+            if (dl) {
+                const uint32_t sd = st + kDHalf30;
+                bulk_g2s(sd + kOwn30, de + cb, 4096u, full);
+                tma4(sd + kXL30, &mdx, 6, 0, 0, nb0 >= 0 ? nb0 : sent_c, full);
+                tma4(sd + kXH30, &mdx, 0, 0, 0, nb1 >= 0 ? nb1 : sent_c, full);
+                tma4(sd + kYL30, &mdy, 0, 7, 0, nb2 >= 0 ? nb2 : sent_c, full);
+                tma4(sd + kYH30, &mdy, 0, 0, 0, nb3 >= 0 ? nb3 : sent_c, full);
+                bulk_g2s(sd + kZL30, de + (nb4 >= 0 ? (int64_t)nb4 * 512 + 448 : (int64_t)sent_c * 512), 512u, full);
+                bulk_g2s(sd + kZH30, de + (nb5 >= 0 ? (int64_t)nb5 * 512 : (int64_t)sent_c * 512), 512u, full);
+            }
+            c_cur = c_nxt;
+            if (c_cur >= 0) {
+                d0 = __ldg(desc4 + 2 * (int64_t)c_cur);
+                d1 = __ldg(desc4 + 2 * (int64_t)c_cur + 1);
+            }
+        }
+        return;
+    }
+
+    // ---------------- compute warps ----------------
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);  // own pair offset in a plane (elements)
+    const uint32_t oc = bp * 8u;                     // (bytes)
+    // lateral operands: base + z * stride (stage-relative); lanes on a chunk
+    // face read the halo buffers
+    const uint32_t b_ym = y > 0 ? kOwn30 + oc - 64u : kYL30 + 16u * xp, s_ym = y > 0 ? 512u : 64u;
+    const uint32_t b_yp = y < 7 ? kOwn30 + oc + 64u : kYH30 + 16u * xp, s_yp = y < 7 ? 512u : 64u;
+    const uint32_t b_l = xp > 0 ? kOwn30 + oc - 8u : kXL30 + 16u * y + 8u, s_l = xp > 0 ? 512u : 128u;
+    const uint32_t b_r = xp < 3 ? kOwn30 + oc + 16u : kXH30 + 16u * y, s_r = xp < 3 ? 512u : 128u;
+    const int z0 = 2 * warp, z1 = z0 + 1;
+    double* __restrict__ un = A.un;
+    bool pushed = false;
+#pragma unroll 1
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t s = k % kStages30, ph = (k / kStages30) & 1u;
+        const uint32_t st = sm0 + s * kStage30;
+        mbar_wait(full0 + 8u * s, ph);
+        const int c = (int)lds_u32(st + kCtx30 + 176u);
+        if (c < 0) break;
+        ChunkCtx14 C;
+        C.c = c;
+        C.lm = lds_u32(st + kCtx30 + 4u * (uint32_t)lane);
+        C.key = (int)lds_u32(st + kCtx30 + 128u + 24u);
+        C.flags = (int)lds_u32(st + kCtx30 + 128u + 28u);
+        C.dv = lds1(st + kCtx30 + 160u);
+        const bool unif = (C.flags & kFlagUnif) != 0;
+        Addr30 a0, a1;
+        a0.c = st + kOwn30 + oc + (uint32_t)z0 * 512u;
+        a1.c = a0.c + 512u;
+        a0.zm = warp == 0 ? st + kZL30 + oc : a0.c - 512u;
+        a0.zp = a1.c;
+        a1.zm = a0.c;
+        a1.zp = warp == kW30 - 1 ? st + kZH30 + oc : a1.c + 512u;
+        a0.ym = st + b_ym + (uint32_t)z0 * s_ym;
+        a1.ym = a0.ym + s_ym;
+        a0.yp = st + b_yp + (uint32_t)z0 * s_yp;
+        a1.yp = a0.yp + s_yp;
+        a0.l = st + b_l + (uint32_t)z0 * s_l;
+        a1.l = a0.l + s_l;
+        a0.r = st + b_r + (uint32_t)z0 * s_r;
+        a1.r = a0.r + s_r;
+        const double2 vv = make_double2(C.dv, C.dv);
+        const double2 uc0 = lds2(a0.c), uc1 = lds2(a1.c), uzm = lds2(a0.zm), uzp = lds2(a1.zp);
+        const double2 dc0 = unif ? vv : lds2(a0.c + kDHalf30), dc1 = unif ? vv : lds2(a1.c + kDHalf30);
+        const double2 dzm = unif ? vv : lds2(a0.zm + kDHalf30), dzp = unif ? vv : lds2(a1.zp + kDHalf30);
+        compute30<REACTION, PUSH, HALF>(M, K, Q, C, z0, xp, y, bp, a0, uc0, dc0, uzm, dzm, uc1, dc1, un, pushed);
+        compute30<REACTION, PUSH, HALF>(M, K, Q, C, z1, xp, y, bp, a1, uc1, dc1, uc0, dc0, uzp, dzp, un, pushed);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8u * s);
+    }
+    // the pushed planes are visible system-wide before this kernel completes
+    // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
+    if (PUSH && pushed) __threadfence_system();
+}
+
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 // desc flags of the fused halo push: bit set iff the chunk has a peer ghost
@@ -1029,10 +1388,34 @@ __global__ void push_flags_kernel(int32_t* __restrict__ desc, const int32_t* __r
     desc[i * 8 + 7] = f;
 }
 
+// v30 chunk records: lm[32] | desc[8] | dv (2 words) | 2 pad words, one
+// 176-B bulk copy per chunk
+__global__ void pack_ctx_kernel(const uint32_t* __restrict__ lm, const int32_t* __restrict__ desc,
+                                const uint32_t* __restrict__ dv, int64_t n, uint32_t* __restrict__ ctx) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n * 44) return;
+    const int64_t c = i / 44;
+    const int w = (int)(i - c * 44);
+    uint32_t v = 0;
+    if (w < 32) v = lm[c * 32 + w];
+    else if (w < 40) v = (uint32_t)desc[c * 8 + (w - 32)];
+    else if (w < 42) v = dv[c * 2 + (w - 40)];
+    ctx[i] = v;
+}
+
+void march_pack_ctx(pd_grid* g, MarchPlan& p) {
+    const int64_t n = g->n_chunks;
+    if (!p.d_ctx) PD_CUDA(pd_malloc(&p.d_ctx, sizeof(uint32_t) * 44 * (size_t)n));
+    pack_ctx_kernel<<<(unsigned)((n * 44 + 255) / 256), 256, 0, g->stream>>>(
+        p.d_lm, p.d_desc, static_cast<const uint32_t*>(p.d_dv), n, p.d_ctx);
+    PD_CUDA(cudaGetLastError());
+}
+
 void march_push_flags(pd_grid* g, MarchPlan& p, const int32_t* d_ord) {
     if (!p.ready || g->n_chunks == 0) return;
     push_flags_kernel<<<(unsigned)((g->n_chunks + 255) / 256), 256, 0, g->stream>>>(p.d_desc, d_ord, g->n_chunks);
     PD_CUDA(cudaGetLastError());
+    if (p.d_ctx) march_pack_ctx(g, p);
 }
 
 __global__ void desc_kernel(const int32_t* __restrict__ nbr, const int32_t* __restrict__ keys,
@@ -1181,6 +1564,7 @@ void march_free(MarchPlan* p) {
     pd_free(p->d_deff);
     pd_free(p->d_counter);
     pd_free(p->d_lm);
+    pd_free(p->d_ctx);
     *p = MarchPlan{};
 }
 
@@ -1293,6 +1677,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
         }
         pd_free(d_bad);
         mark_uniform<unsigned long long>(g, plan, 0xFFF0000000000000ull);
+        march_pack_ctx(g, *plan);
     }
     const int64_t n = end - begin;
     plan->d_stream = march_schedule(g, begin, end);
@@ -1321,6 +1706,68 @@ MarchPlan::Sub& march_sub(pd_grid* g, MarchPlan& p, int64_t begin, int64_t end) 
     PD_CUDA(pd_malloc(&sp.d_counter, sizeof(int)));
     p.subs.push_back(sp);
     return p.subs.back();
+}
+
+// ---- v30 host side: TMA tensor maps over the [chunk][z][y][x] columns ----
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    if (!fn) fail(PD_E_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old for TMA)");
+    return fn;
+}
+
+// 4-D FP64 view of a column: dims (x 8, y 8, z 8, chunk n), box `box`
+CUtensorMap column_map(const double* base, int64_t n_chunks, const cuuint32_t box[4]) {
+    CUtensorMap m;
+    const cuuint64_t dims[4] = {8, 8, 8, (cuuint64_t)n_chunks};
+    const cuuint64_t strides[3] = {64, 512, 4096};  // bytes, dims 1..3
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PD_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+}  // namespace
+
+void march30_launch(pd_grid* g, MarchPlan& p, const MarchArgs& M, int r, bool push) {
+    if (!p.d_ctx) fail(PD_E_INPUT, "march v30 needs the packed chunk records (3-D FP64 plan)");
+    static const cuuint32_t bx[4] = {2, 8, 8, 1}, by[4] = {8, 1, 8, 1};
+    const CUtensorMap mux = column_map(M.A.u, g->n_chunks, bx), muy = column_map(M.A.u, g->n_chunks, by);
+    const CUtensorMap mdx = column_map(M.deff, g->n_chunks + 1, bx), mdy = column_map(M.deff, g->n_chunks + 1, by);
+    using K30 = void (*)(const MarchArgs, const uint32_t*, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                         const CUtensorMap);
+#define PD_M_TABLE(K)                                                                            \
+    {{{K<0, false, false>, K<1, false, false>, K<2, false, false>},                              \
+      {K<0, true, false>, K<1, true, false>, K<2, true, false>}},                                \
+     {{K<0, false, true>, K<1, false, true>, K<2, false, true>},                                 \
+      {K<0, true, true>, K<1, true, true>, K<2, true, true>}}}
+    static const K30 t30[2][2][3] = PD_M_TABLE(ftcs_march30_kernel);
+#undef PD_M_TABLE
+    static uint64_t attr_done = 0;
+    const int dev = g->device;
+    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
+    if (!((attr_done >> dev) & 1u)) {
+        for (auto& half : t30)
+            for (auto& row : half)
+                for (auto k : row)
+                    PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem30));
+        attr_done |= 1ull << dev;
+    }
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    t30[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas30, kThreads30, kSmem30, g->stream>>>(M, p.d_ctx, mux, muy, mdx,
+                                                                                            mdy);
+    PD_CUDA(cudaGetLastError());
 }
 
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
@@ -1358,6 +1805,10 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     static const KernT t14[2][2][3] = PD_M_TABLE(ftcs_march14_kernel);  // [half][push][reaction]
     static const KernT t20[2][2][3] = PD_M_TABLE(ftcs_march20_kernel);
 #undef PD_M_TABLE
+    if (ver == 30) {
+        march30_launch(g, p, M, r, pl != nullptr);
+        return;
+    }
     const bool v20 = ver != 14;
     const size_t bytes = (size_t)(v20 ? kWarpBytes20 : kWarpBytes14) * kWarps;
     // the dynamic shared-memory opt-in is per device: set it once per device
