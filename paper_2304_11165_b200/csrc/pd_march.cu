@@ -1045,8 +1045,8 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march20_kernel(MarchAr
 // ---------------------------------------------------------------------------
 constexpr int kW30 = 4;                        // compute warps per CTA
 constexpr int kThreads30 = 32 * (kW30 + 1);    // + one producer warp
-constexpr int kStages30 = 3;
-constexpr int kCtas30 = 4;
+// stages per CTA (template NST) x CTAs per SM: 3 x 4 (default), 4 x 3, 6 x 2
+__host__ __device__ constexpr int ctas30(int nst) { return nst <= 3 ? 4 : nst == 4 ? 3 : 2; }
 // stage layout (bytes): the D_eff half mirrors the u half at +kDHalf30
 constexpr uint32_t kOwn30 = 0;      // [z][y][x] own slab (4096)
 constexpr uint32_t kYL30 = 4096;    // [z][x]    y- neighbour's row 7 (512)
@@ -1059,8 +1059,8 @@ constexpr uint32_t kDHalf30 = 8192;
 constexpr uint32_t kCtx30 = 16384;  // chunk record (176 B), then the chunk id at +176
 constexpr uint32_t kCtxWords30 = 44;
 constexpr uint32_t kStage30 = 16384 + 256;
-constexpr uint32_t kBar30 = kStages30 * kStage30;  // full[3] then empty[3]
-constexpr uint32_t kSmem30 = kBar30 + 8u * 2u * kStages30;
+__host__ __device__ constexpr uint32_t bar30(int nst) { return (uint32_t)nst * kStage30; }  // full[nst] then empty[nst]
+__host__ __device__ constexpr uint32_t smem30(int nst) { return bar30(nst) + 16u * (uint32_t)nst; }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
@@ -1208,8 +1208,8 @@ __device__ __forceinline__ void compute30(const MarchArgs& M, const SlowConsts& 
     }
 }
 
-template <int REACTION, bool PUSH, bool HALF>
-__global__ void __launch_bounds__(kThreads30, kCtas30)
+template <int REACTION, bool PUSH, bool HALF, int NST>
+__global__ void __launch_bounds__(kThreads30, ctas30(NST))
     ftcs_march30_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
                         const __grid_constant__ CUtensorMap mux, const __grid_constant__ CUtensorMap muy,
                         const __grid_constant__ CUtensorMap mdx, const __grid_constant__ CUtensorMap mdy) {
@@ -1226,7 +1226,8 @@ __global__ void __launch_bounds__(kThreads30, kCtas30)
         }
     }
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t full0 = sm0 + kBar30, empty0 = full0 + 8u * kStages30;
+    constexpr int kStages30 = NST;
+    const uint32_t full0 = sm0 + bar30(NST), empty0 = full0 + 8u * kStages30;
     if (t == 0) {
         for (int a = 0; a < 3; ++a) {
             K.size[a] = A.size[a];
@@ -1258,19 +1259,32 @@ __global__ void __launch_bounds__(kThreads30, kCtas30)
             return r;
         };
         auto id_of = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
+        auto prefetch = [&](const void* g, uint32_t bytes) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
+        };
         const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
         const int sent_c = (int)M.n_all;  // D_eff sentinel chunk
-        // pipeline: chunk k's id and descriptor halves are loaded one
-        // iteration ahead, its schedule position two iterations ahead
+        // Look-ahead (the stages alone hold too few chunks to cover the DRAM
+        // latency): chunk k+3's position is claimed, chunk k+2's u slab and
+        // record are prefetched into L2 as soon as its id is known, chunk k+1's
+        // descriptor is loaded and its D_eff slab prefetched (non-uniform
+        // chunks), chunk k is copied into its stage.
         int c_cur = id_of(claim());
-        int p_next = claim();
-        int4 d0 = c_cur >= 0 ? __ldg(desc4 + 2 * (int64_t)c_cur) : make_int4(0, 0, 0, 0);
-        int4 d1 = c_cur >= 0 ? __ldg(desc4 + 2 * (int64_t)c_cur + 1) : make_int4(0, 0, 0, 0);
+        int c1 = id_of(claim());
+        int c2 = id_of(claim());
+        int p3 = claim();
+        int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, e0 = d0, e1 = d0;
+        if (c_cur >= 0) {
+            d0 = __ldg(desc4 + 2 * (int64_t)c_cur);
+            d1 = __ldg(desc4 + 2 * (int64_t)c_cur + 1);
+        }
+        if (c1 >= 0) {
+            e0 = __ldg(desc4 + 2 * (int64_t)c1);
+            e1 = __ldg(desc4 + 2 * (int64_t)c1 + 1);
+        }
 #pragma unroll 1
         for (uint32_t k = 0;; ++k) {
             const uint32_t s = k % kStages30, ph = (k / kStages30) & 1u;
-            const int c_nxt = id_of(p_next);
-            if (c_cur >= 0) p_next = claim();
             const uint32_t st = sm0 + s * kStage30, full = full0 + 8u * s;
             if (k >= (uint32_t)kStages30) mbar_wait(empty0 + 8u * s, ph ^ 1u);
             sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
@@ -1304,11 +1318,27 @@ __global__ void __launch_bounds__(kThreads30, kCtas30)
                 bulk_g2s(sd + kZL30, de + (nb4 >= 0 ? (int64_t)nb4 * 512 + 448 : (int64_t)sent_c * 512), 512u, full);
                 bulk_g2s(sd + kZH30, de + (nb5 >= 0 ? (int64_t)nb5 * 512 : (int64_t)sent_c * 512), 512u, full);
             }
-            c_cur = c_nxt;
-            if (c_cur >= 0) {
-                d0 = __ldg(desc4 + 2 * (int64_t)c_cur);
-                d1 = __ldg(desc4 + 2 * (int64_t)c_cur + 1);
+            // look-ahead work after the copies: its latency overlaps the next
+            // stage wait
+            const int c3 = id_of(p3);
+            p3 = claim();
+            int4 f0 = make_int4(0, 0, 0, 0), f1 = f0;
+            if (c2 >= 0) {
+                f0 = __ldg(desc4 + 2 * (int64_t)c2);
+                f1 = __ldg(desc4 + 2 * (int64_t)c2 + 1);
             }
+            if (c1 >= 0 && !(e1.w & kFlagUnif)) prefetch(de + (int64_t)c1 * 512, 4096u);
+            if (c3 >= 0) {
+                prefetch(u + (int64_t)c3 * 512, 4096u);
+                prefetch(ctxa + (int64_t)c3 * kCtxWords30, 176u);
+            }
+            c_cur = c1;
+            c1 = c2;
+            c2 = c3;
+            d0 = e0;
+            d1 = e1;
+            e0 = f0;
+            e1 = f1;
         }
         return;
     }
@@ -1746,27 +1776,40 @@ void march30_launch(pd_grid* g, MarchPlan& p, const MarchArgs& M, int r, bool pu
     const CUtensorMap mdx = column_map(M.deff, g->n_chunks + 1, bx), mdy = column_map(M.deff, g->n_chunks + 1, by);
     using K30 = void (*)(const MarchArgs, const uint32_t*, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                          const CUtensorMap);
-#define PD_M_TABLE(K)                                                                            \
-    {{{K<0, false, false>, K<1, false, false>, K<2, false, false>},                              \
-      {K<0, true, false>, K<1, true, false>, K<2, true, false>}},                                \
-     {{K<0, false, true>, K<1, false, true>, K<2, false, true>},                                 \
-      {K<0, true, true>, K<1, true, true>, K<2, true, true>}}}
-    static const K30 t30[2][2][3] = PD_M_TABLE(ftcs_march30_kernel);
+#define PD_M_TABLE(N)                                                                                         \
+    {{{ftcs_march30_kernel<0, false, false, N>, ftcs_march30_kernel<1, false, false, N>,                       \
+       ftcs_march30_kernel<2, false, false, N>},                                                               \
+      {ftcs_march30_kernel<0, true, false, N>, ftcs_march30_kernel<1, true, false, N>,                         \
+       ftcs_march30_kernel<2, true, false, N>}},                                                               \
+     {{ftcs_march30_kernel<0, false, true, N>, ftcs_march30_kernel<1, false, true, N>,                         \
+       ftcs_march30_kernel<2, false, true, N>},                                                                \
+      {ftcs_march30_kernel<0, true, true, N>, ftcs_march30_kernel<1, true, true, N>,                           \
+       ftcs_march30_kernel<2, true, true, N>}}}
+    static const K30 t3[2][2][3] = PD_M_TABLE(3);
+    static const K30 t4[2][2][3] = PD_M_TABLE(4);
+    static const K30 t6[2][2][3] = PD_M_TABLE(6);
 #undef PD_M_TABLE
+    static const int nst = [] {
+        const char* e = getenv("PD_M30_STAGES");
+        const int v = e ? atoi(e) : 3;
+        return v == 4 || v == 6 ? v : 3;
+    }();
+    const K30(*tab)[2][3] = nst == 3 ? t3 : nst == 4 ? t4 : t6;
+    const uint32_t smem = nst == 3 ? smem30(3) : nst == 4 ? smem30(4) : smem30(6);
+    const int ctas = nst == 3 ? ctas30(3) : nst == 4 ? ctas30(4) : ctas30(6);
     static uint64_t attr_done = 0;
     const int dev = g->device;
     if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
     if (!((attr_done >> dev) & 1u)) {
-        for (auto& half : t30)
-            for (auto& row : half)
-                for (auto k : row)
-                    PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem30));
+        for (int h = 0; h < 2; ++h)
+            for (int q = 0; q < 2; ++q)
+                for (int rr = 0; rr < 3; ++rr)
+                    PD_CUDA(cudaFuncSetAttribute(tab[h][q][rr], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_done |= 1ull << dev;
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    t30[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas30, kThreads30, kSmem30, g->stream>>>(M, p.d_ctx, mux, muy, mdx,
-                                                                                            mdy);
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * ctas, kThreads30, smem, g->stream>>>(M, p.d_ctx, mux, muy, mdx, mdy);
     PD_CUDA(cudaGetLastError());
 }
 

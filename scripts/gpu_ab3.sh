@@ -1,0 +1,18 @@
+#!/bin/bash
+# A/B of march variants: "V[:STAGES]" entries (PD_MARCH_V, PD_M30_STAGES).
+# usage: VARS="14 30 30:4 30:6" CAND=30 bash scripts/gpu_ab3.sh
+mkdir -p gpurun_out
+VARS=${VARS:-"14 30"}
+CAND=${CAND:-30}
+PD_MARCH_V=$CAND timeout 900 python -m pytest -q -m gpu -x tests/test_gpu_parity.py tests/test_fuzz_parity.py tests/test_headline_parity.py tests/test_gpu_kats.py tests/test_march32.py tests/test_gpu_shard.py > gpurun_out/ab_pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab_pytest.log
+run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=3; PD_MARCH_V=$v PD_M30_STAGES=$st "${@:2}"; }
+for rep in 1 2; do for x in $VARS; do
+  run $x timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu --no-e2e > gpurun_out/ab_bench_${x/:/_}_$rep.log 2>&1
+done; done
+M=smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__issue_active.avg.pct_of_peak_sustained_elapsed,smsp__warps_eligible.avg.per_cycle_active,launch__registers_per_thread,lts__t_sector_op_read_hit_rate.pct
+for x in $VARS; do
+  run $x timeout 600 ncu --metrics $M --clock-control none -k regex:ftcs_march -s 3 -c 1 --csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ab_ncu_${x/:/_}.csv 2>&1
+done
+tail -3 gpurun_out/ab_pytest.log
+for f in gpurun_out/ab_bench_*; do echo $f $(grep '^{' $f | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['roofline']['kernel_ms_per_step'],3), d['clocks']['sm_mhz'])"); done
+for x in $VARS; do echo "== $x"; grep -E '"(smsp__inst|gpu__time|dram__bytes|sm__issue|smsp__warps|launch__reg|lts__t)' gpurun_out/ab_ncu_${x/:/_}.csv | awk -F'","' '{print $(NF-2), $NF}'; done
