@@ -1043,10 +1043,17 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march20_kernel(MarchAr
 // * Per-node arithmetic, walls, reactions, rare path, push: as v14 (same
 //   expressions, same order), so results are bitwise identical.
 // ---------------------------------------------------------------------------
-constexpr int kW30 = 4;                        // compute warps per CTA
-constexpr int kThreads30 = 32 * (kW30 + 1);    // + one producer warp
-// stages per CTA (template NST) x CTAs per SM: 3 x 4 (default), 4 x 3, 6 x 2
-__host__ __device__ constexpr int ctas30(int nst) { return nst <= 3 ? 4 : nst == 4 ? 3 : 2; }
+// configurations (template CFG): stages per CTA, planes per compute warp
+// (2: 4 compute warps, 1: 8), CTAs per SM
+//   0: 3 stages, 2 planes, 4 CTAs (16 compute warps / SM)
+//   1: 4 stages, 1 plane,  3 CTAs (24)
+//   2: 3 stages, 1 plane,  3 CTAs (24)
+//   3: 5 stages, 1 plane,  2 CTAs (16)
+__host__ __device__ constexpr int nst30(int cfg) { return cfg == 1 ? 4 : cfg == 3 ? 5 : 3; }
+__host__ __device__ constexpr int pw30(int cfg) { return cfg == 0 ? 2 : 1; }
+__host__ __device__ constexpr int ctas30(int cfg) { return cfg == 0 ? 4 : cfg == 3 ? 2 : 3; }
+__host__ __device__ constexpr int nw30(int cfg) { return 8 / pw30(cfg); }  // compute warps per CTA
+__host__ __device__ constexpr int threads30(int cfg) { return 32 * (nw30(cfg) + 1); }  // + one producer warp
 // stage layout (bytes): the D_eff half mirrors the u half at +kDHalf30
 constexpr uint32_t kOwn30 = 0;      // [z][y][x] own slab (4096)
 constexpr uint32_t kYL30 = 4096;    // [z][x]    y- neighbour's row 7 (512)
@@ -1208,8 +1215,8 @@ __device__ __forceinline__ void compute30(const MarchArgs& M, const SlowConsts& 
     }
 }
 
-template <int REACTION, bool PUSH, bool HALF, int NST>
-__global__ void __launch_bounds__(kThreads30, ctas30(NST))
+template <int REACTION, bool PUSH, bool HALF, int CFG>
+__global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
     ftcs_march30_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
                         const __grid_constant__ CUtensorMap mux, const __grid_constant__ CUtensorMap muy,
                         const __grid_constant__ CUtensorMap mdx, const __grid_constant__ CUtensorMap mdy) {
@@ -1226,8 +1233,8 @@ __global__ void __launch_bounds__(kThreads30, ctas30(NST))
         }
     }
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    constexpr int kStages30 = NST;
-    const uint32_t full0 = sm0 + bar30(NST), empty0 = full0 + 8u * kStages30;
+    constexpr int kStages30 = nst30(CFG), kW30 = nw30(CFG), PW = pw30(CFG);
+    const uint32_t full0 = sm0 + bar30(kStages30), empty0 = full0 + 8u * kStages30;
     if (t == 0) {
         for (int a = 0; a < 3; ++a) {
             K.size[a] = A.size[a];
@@ -1377,27 +1384,45 @@ __global__ void __launch_bounds__(kThreads30, ctas30(NST))
         C.flags = (int)lds_u32(st + kCtx30 + 128u + 28u);
         C.dv = lds1(st + kCtx30 + 160u);
         const bool unif = (C.flags & kFlagUnif) != 0;
-        Addr30 a0, a1;
-        a0.c = st + kOwn30 + oc + (uint32_t)z0 * 512u;
-        a1.c = a0.c + 512u;
-        a0.zm = warp == 0 ? st + kZL30 + oc : a0.c - 512u;
-        a0.zp = a1.c;
-        a1.zm = a0.c;
-        a1.zp = warp == kW30 - 1 ? st + kZH30 + oc : a1.c + 512u;
-        a0.ym = st + b_ym + (uint32_t)z0 * s_ym;
-        a1.ym = a0.ym + s_ym;
-        a0.yp = st + b_yp + (uint32_t)z0 * s_yp;
-        a1.yp = a0.yp + s_yp;
-        a0.l = st + b_l + (uint32_t)z0 * s_l;
-        a1.l = a0.l + s_l;
-        a0.r = st + b_r + (uint32_t)z0 * s_r;
-        a1.r = a0.r + s_r;
         const double2 vv = make_double2(C.dv, C.dv);
-        const double2 uc0 = lds2(a0.c), uc1 = lds2(a1.c), uzm = lds2(a0.zm), uzp = lds2(a1.zp);
-        const double2 dc0 = unif ? vv : lds2(a0.c + kDHalf30), dc1 = unif ? vv : lds2(a1.c + kDHalf30);
-        const double2 dzm = unif ? vv : lds2(a0.zm + kDHalf30), dzp = unif ? vv : lds2(a1.zp + kDHalf30);
-        compute30<REACTION, PUSH, HALF>(M, K, Q, C, z0, xp, y, bp, a0, uc0, dc0, uzm, dzm, uc1, dc1, un, pushed);
-        compute30<REACTION, PUSH, HALF>(M, K, Q, C, z1, xp, y, bp, a1, uc1, dc1, uc0, dc0, uzp, dzp, un, pushed);
+        if constexpr (PW == 2) {
+            Addr30 a0, a1;
+            a0.c = st + kOwn30 + oc + (uint32_t)z0 * 512u;
+            a1.c = a0.c + 512u;
+            a0.zm = warp == 0 ? st + kZL30 + oc : a0.c - 512u;
+            a0.zp = a1.c;
+            a1.zm = a0.c;
+            a1.zp = warp == kW30 - 1 ? st + kZH30 + oc : a1.c + 512u;
+            a0.ym = st + b_ym + (uint32_t)z0 * s_ym;
+            a1.ym = a0.ym + s_ym;
+            a0.yp = st + b_yp + (uint32_t)z0 * s_yp;
+            a1.yp = a0.yp + s_yp;
+            a0.l = st + b_l + (uint32_t)z0 * s_l;
+            a1.l = a0.l + s_l;
+            a0.r = st + b_r + (uint32_t)z0 * s_r;
+            a1.r = a0.r + s_r;
+            const double2 uc0 = lds2(a0.c), uc1 = lds2(a1.c), uzm = lds2(a0.zm), uzp = lds2(a1.zp);
+            const double2 dc0 = unif ? vv : lds2(a0.c + kDHalf30), dc1 = unif ? vv : lds2(a1.c + kDHalf30);
+            const double2 dzm = unif ? vv : lds2(a0.zm + kDHalf30), dzp = unif ? vv : lds2(a1.zp + kDHalf30);
+            compute30<REACTION, PUSH, HALF>(M, K, Q, C, z0, xp, y, bp, a0, uc0, dc0, uzm, dzm, uc1, dc1, un,
+                                            pushed);
+            compute30<REACTION, PUSH, HALF>(M, K, Q, C, z1, xp, y, bp, a1, uc1, dc1, uc0, dc0, uzp, dzp, un,
+                                            pushed);
+        } else {  // one plane per warp: z = warp
+            const int z = warp;
+            Addr30 a;
+            a.c = st + kOwn30 + oc + (uint32_t)z * 512u;
+            a.zm = z == 0 ? st + kZL30 + oc : a.c - 512u;
+            a.zp = z == 7 ? st + kZH30 + oc : a.c + 512u;
+            a.ym = st + b_ym + (uint32_t)z * s_ym;
+            a.yp = st + b_yp + (uint32_t)z * s_yp;
+            a.l = st + b_l + (uint32_t)z * s_l;
+            a.r = st + b_r + (uint32_t)z * s_r;
+            const double2 uc = lds2(a.c), uzm = lds2(a.zm), uzp = lds2(a.zp);
+            const double2 dc = unif ? vv : lds2(a.c + kDHalf30);
+            const double2 dzm = unif ? vv : lds2(a.zm + kDHalf30), dzp = unif ? vv : lds2(a.zp + kDHalf30);
+            compute30<REACTION, PUSH, HALF>(M, K, Q, C, z, xp, y, bp, a, uc, dc, uzm, dzm, uzp, dzp, un, pushed);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8u * s);
     }
@@ -1785,18 +1810,16 @@ void march30_launch(pd_grid* g, MarchPlan& p, const MarchArgs& M, int r, bool pu
        ftcs_march30_kernel<2, false, true, N>},                                                                \
       {ftcs_march30_kernel<0, true, true, N>, ftcs_march30_kernel<1, true, true, N>,                           \
        ftcs_march30_kernel<2, true, true, N>}}}
-    static const K30 t3[2][2][3] = PD_M_TABLE(3);
-    static const K30 t4[2][2][3] = PD_M_TABLE(4);
-    static const K30 t6[2][2][3] = PD_M_TABLE(6);
+    static const K30 tabs[4][2][2][3] = {PD_M_TABLE(0), PD_M_TABLE(1), PD_M_TABLE(2), PD_M_TABLE(3)};
 #undef PD_M_TABLE
-    static const int nst = [] {
-        const char* e = getenv("PD_M30_STAGES");
-        const int v = e ? atoi(e) : 3;
-        return v == 4 || v == 6 ? v : 3;
+    static const int cfg = [] {
+        const char* e = getenv("PD_M30_CFG");
+        const int v = e ? atoi(e) : 0;
+        return v >= 0 && v <= 3 ? v : 0;
     }();
-    const K30(*tab)[2][3] = nst == 3 ? t3 : nst == 4 ? t4 : t6;
-    const uint32_t smem = nst == 3 ? smem30(3) : nst == 4 ? smem30(4) : smem30(6);
-    const int ctas = nst == 3 ? ctas30(3) : nst == 4 ? ctas30(4) : ctas30(6);
+    const K30(*tab)[2][3] = tabs[cfg];
+    const uint32_t smem = smem30(nst30(cfg));
+    const int ctas = ctas30(cfg);
     static uint64_t attr_done = 0;
     const int dev = g->device;
     if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
@@ -1809,7 +1832,8 @@ void march30_launch(pd_grid* g, MarchPlan& p, const MarchArgs& M, int r, bool pu
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * ctas, kThreads30, smem, g->stream>>>(M, p.d_ctx, mux, muy, mdx, mdy);
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * ctas, threads30(cfg), smem, g->stream>>>(M, p.d_ctx, mux, muy, mdx,
+                                                                                          mdy);
     PD_CUDA(cudaGetLastError());
 }
 

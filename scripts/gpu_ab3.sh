@@ -1,11 +1,11 @@
 #!/bin/bash
-# A/B of march variants: "V[:STAGES]" entries (PD_MARCH_V, PD_M30_STAGES).
+# A/B of march variants: "V[:CFG]" entries (PD_MARCH_V, PD_M30_CFG).
 # usage: VARS="14 30 30:4 30:6" CAND=30 bash scripts/gpu_ab3.sh
 mkdir -p gpurun_out
 VARS=${VARS:-"14 30"}
 CAND=${CAND:-30}
 PD_MARCH_V=$CAND timeout 900 python -m pytest -q -m gpu -x tests/test_gpu_parity.py tests/test_fuzz_parity.py tests/test_headline_parity.py tests/test_gpu_kats.py tests/test_march32.py tests/test_gpu_shard.py > gpurun_out/ab_pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab_pytest.log
-run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=3; PD_MARCH_V=$v PD_M30_STAGES=$st "${@:2}"; }
+run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=0; PD_MARCH_V=$v PD_M30_CFG=$st "${@:2}"; }
 for rep in 1 2; do for x in $VARS; do
   run $x timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu --no-e2e > gpurun_out/ab_bench_${x/:/_}_$rep.log 2>&1
 done; done
