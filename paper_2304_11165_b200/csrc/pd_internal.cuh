@@ -207,6 +207,8 @@ struct MarchPlan {
     int* d_counter = nullptr;      // per-step dynamic batch counters
     uint32_t* d_lm = nullptr;      // per chunk and lane: active / sink bits [c][32]
     uint32_t* d_ctx = nullptr;     // v30: packed chunk record [c][44]: lm[32] | desc[8] | dv | pad
+    // v30: schedules with bit 31 set on uniform chunks (keyed by the plain schedule)
+    std::vector<std::pair<const int32_t*, int32_t*>> flagged;
     int grid = 0;
     int64_t n = 0;
     bool ready = false;

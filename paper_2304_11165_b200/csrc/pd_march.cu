@@ -1265,33 +1265,52 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
             asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(ctr) : "memory");
             return r;
         };
+        // schedule entries carry bit 31 for uniform chunks (no D_eff needed)
         auto id_of = [&](int p) -> int { return p < n ? __ldg(&M.sched[p]) : -1; };
         auto prefetch = [&](const void* g, uint32_t bytes) {
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
         };
+        auto prefetch_chunk = [&](int e) {  // e: flagged schedule entry (>= 0: none pending)
+            if (e == -1) return;
+            const int64_t c = (int64_t)((uint32_t)e & 0x7FFFFFFFu);
+            prefetch(u + c * 512, 4096u);
+            prefetch(ctxa + c * kCtxWords30, 176u);
+            if (e >= 0) prefetch(de + c * 512, 4096u);
+        };
+        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
         const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
         const int sent_c = (int)M.n_all;  // D_eff sentinel chunk
         // Look-ahead (the stages alone hold too few chunks to cover the DRAM
-        // latency): chunk k+3's position is claimed, chunk k+2's u slab and
-        // record are prefetched into L2 as soon as its id is known, chunk k+1's
-        // descriptor is loaded and its D_eff slab prefetched (non-uniform
-        // chunks), chunk k is copied into its stage.
-        int c_cur = id_of(claim());
-        int c1 = id_of(claim());
-        int c2 = id_of(claim());
-        int p3 = claim();
-        int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, e0 = d0, e1 = d0;
+        // latency): the schedule position of chunk k+kLook+1 is claimed, chunk
+        // k+kLook's slabs (u, record, and D_eff unless uniform) are prefetched
+        // into L2 as soon as its id is known, chunk k+1's descriptor is loaded,
+        // chunk k is copied into its stage.
+        constexpr int kLook = 6;
+        int q[kLook + 1];  // flagged entries of chunks k .. k+kLook
+#pragma unroll
+        for (int j = 0; j <= kLook; ++j) {
+            q[j] = id_of(claim());
+            if (j > 0) prefetch_chunk(q[j]);
+        }
+        int p_nxt = claim();
+        int c_cur = chunk_of(q[0]);
+        int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
         if (c_cur >= 0) {
             d0 = __ldg(desc4 + 2 * (int64_t)c_cur);
             d1 = __ldg(desc4 + 2 * (int64_t)c_cur + 1);
         }
-        if (c1 >= 0) {
-            e0 = __ldg(desc4 + 2 * (int64_t)c1);
-            e1 = __ldg(desc4 + 2 * (int64_t)c1 + 1);
-        }
 #pragma unroll 1
         for (uint32_t k = 0;; ++k) {
             const uint32_t s = k % kStages30, ph = (k / kStages30) & 1u;
+            // descriptor of the next chunk and the look-ahead, before the wait
+            const int c_nx = chunk_of(q[1]);
+            int4 e0 = make_int4(0, 0, 0, 0), e1 = e0;
+            if (c_nx >= 0) {
+                e0 = __ldg(desc4 + 2 * (int64_t)c_nx);
+                e1 = __ldg(desc4 + 2 * (int64_t)c_nx + 1);
+            }
+            const int qn = id_of(p_nxt);
+            if (c_cur >= 0) p_nxt = claim();
             const uint32_t st = sm0 + s * kStage30, full = full0 + 8u * s;
             if (k >= (uint32_t)kStages30) mbar_wait(empty0 + 8u * s, ph ^ 1u);
             sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
@@ -1325,27 +1344,13 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
                 bulk_g2s(sd + kZL30, de + (nb4 >= 0 ? (int64_t)nb4 * 512 + 448 : (int64_t)sent_c * 512), 512u, full);
                 bulk_g2s(sd + kZH30, de + (nb5 >= 0 ? (int64_t)nb5 * 512 : (int64_t)sent_c * 512), 512u, full);
             }
-            // look-ahead work after the copies: its latency overlaps the next
-            // stage wait
-            const int c3 = id_of(p3);
-            p3 = claim();
-            int4 f0 = make_int4(0, 0, 0, 0), f1 = f0;
-            if (c2 >= 0) {
-                f0 = __ldg(desc4 + 2 * (int64_t)c2);
-                f1 = __ldg(desc4 + 2 * (int64_t)c2 + 1);
-            }
-            if (c1 >= 0 && !(e1.w & kFlagUnif)) prefetch(de + (int64_t)c1 * 512, 4096u);
-            if (c3 >= 0) {
-                prefetch(u + (int64_t)c3 * 512, 4096u);
-                prefetch(ctxa + (int64_t)c3 * kCtxWords30, 176u);
-            }
-            c_cur = c1;
-            c1 = c2;
-            c2 = c3;
+            prefetch_chunk(qn);
+#pragma unroll
+            for (int j = 0; j < kLook; ++j) q[j] = q[j + 1];
+            q[kLook] = qn;
+            c_cur = c_nx;
             d0 = e0;
             d1 = e1;
-            e0 = f0;
-            e1 = f1;
         }
         return;
     }
@@ -1620,6 +1625,7 @@ void march_free(MarchPlan* p) {
     pd_free(p->d_counter);
     pd_free(p->d_lm);
     pd_free(p->d_ctx);
+    for (auto& f : p->flagged) pd_free(f.second);
     *p = MarchPlan{};
 }
 
@@ -1794,8 +1800,30 @@ CUtensorMap column_map(const double* base, int64_t n_chunks, const cuuint32_t bo
 }
 }  // namespace
 
-void march30_launch(pd_grid* g, MarchPlan& p, const MarchArgs& M, int r, bool push) {
+__global__ void flag_sched_kernel(const int32_t* __restrict__ sched, const int32_t* __restrict__ desc, int64_t n,
+                                  int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t c = sched[i];
+    out[i] = (desc[(int64_t)c * 8 + 7] & kFlagUnif) ? (int32_t)((uint32_t)c | 0x80000000u) : c;
+}
+
+const int32_t* flagged_schedule(pd_grid* g, MarchPlan& p, const int32_t* sched, int64_t n) {
+    for (auto& f : p.flagged)
+        if (f.first == sched) return f.second;
+    int32_t* d = nullptr;
+    PD_CUDA(pd_malloc(&d, sizeof(int32_t) * (size_t)std::max<int64_t>(1, n)));
+    if (n > 0) {
+        flag_sched_kernel<<<(unsigned)((n + 255) / 256), 256, 0, g->stream>>>(sched, p.d_desc, n, d);
+        PD_CUDA(cudaGetLastError());
+    }
+    p.flagged.emplace_back(sched, d);
+    return d;
+}
+
+void march30_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     if (!p.d_ctx) fail(PD_E_INPUT, "march v30 needs the packed chunk records (3-D FP64 plan)");
+    M.sched = flagged_schedule(g, p, M.sched, M.n);
     static const cuuint32_t bx[4] = {2, 8, 8, 1}, by[4] = {8, 1, 8, 1};
     const CUtensorMap mux = column_map(M.A.u, g->n_chunks, bx), muy = column_map(M.A.u, g->n_chunks, by);
     const CUtensorMap mdx = column_map(M.deff, g->n_chunks + 1, bx), mdy = column_map(M.deff, g->n_chunks + 1, by);
