@@ -1049,9 +1049,11 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march20_kernel(MarchAr
 //   1: 4 stages, 1 plane,  3 CTAs (24)
 //   2: 3 stages, 1 plane,  3 CTAs (24)
 //   3: 5 stages, 1 plane,  2 CTAs (16)
+//   4, 5, 6: as 0 with an L2 look-ahead of 2, 4, 6 chunks (0-3: 3)
 __host__ __device__ constexpr int nst30(int cfg) { return cfg == 1 ? 4 : cfg == 3 ? 5 : 3; }
-__host__ __device__ constexpr int pw30(int cfg) { return cfg == 0 ? 2 : 1; }
-__host__ __device__ constexpr int ctas30(int cfg) { return cfg == 0 ? 4 : cfg == 3 ? 2 : 3; }
+__host__ __device__ constexpr int pw30(int cfg) { return cfg == 1 || cfg == 2 || cfg == 3 ? 1 : 2; }
+__host__ __device__ constexpr int ctas30(int cfg) { return cfg == 1 || cfg == 2 ? 3 : cfg == 3 ? 2 : 4; }
+__host__ __device__ constexpr int look30(int cfg) { return cfg == 4 ? 2 : cfg == 5 ? 4 : cfg == 6 ? 6 : 3; }
 __host__ __device__ constexpr int nw30(int cfg) { return 8 / pw30(cfg); }  // compute warps per CTA
 __host__ __device__ constexpr int threads30(int cfg) { return 32 * (nw30(cfg) + 1); }  // + one producer warp
 // stage layout (bytes): the D_eff half mirrors the u half at +kDHalf30
@@ -1285,7 +1287,7 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
         // k+kLook's slabs (u, record, and D_eff unless uniform) are prefetched
         // into L2 as soon as its id is known, chunk k+1's descriptor is loaded,
         // chunk k is copied into its stage.
-        constexpr int kLook = 6;
+        constexpr int kLook = look30(CFG);
         int q[kLook + 1];  // flagged entries of chunks k .. k+kLook
 #pragma unroll
         for (int j = 0; j <= kLook; ++j) {
@@ -1838,12 +1840,13 @@ void march30_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
        ftcs_march30_kernel<2, false, true, N>},                                                                \
       {ftcs_march30_kernel<0, true, true, N>, ftcs_march30_kernel<1, true, true, N>,                           \
        ftcs_march30_kernel<2, true, true, N>}}}
-    static const K30 tabs[4][2][2][3] = {PD_M_TABLE(0), PD_M_TABLE(1), PD_M_TABLE(2), PD_M_TABLE(3)};
+    static const K30 tabs[7][2][2][3] = {PD_M_TABLE(0), PD_M_TABLE(1), PD_M_TABLE(2), PD_M_TABLE(3),
+                                         PD_M_TABLE(4), PD_M_TABLE(5), PD_M_TABLE(6)};
 #undef PD_M_TABLE
     static const int cfg = [] {
         const char* e = getenv("PD_M30_CFG");
         const int v = e ? atoi(e) : 0;
-        return v >= 0 && v <= 3 ? v : 0;
+        return v >= 0 && v <= 6 ? v : 0;
     }();
     const K30(*tab)[2][3] = tabs[cfg];
     const uint32_t smem = smem30(nst30(cfg));
