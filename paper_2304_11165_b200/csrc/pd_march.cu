@@ -1060,14 +1060,16 @@ __host__ __device__ constexpr int threads30(int cfg) { return 32 * (nw30(cfg) + 
 constexpr uint32_t kOwn30 = 0;      // [z][y][x] own slab (4096)
 constexpr uint32_t kYL30 = 4096;    // [z][x]    y- neighbour's row 7 (512)
 constexpr uint32_t kYH30 = 4608;    // [z][x]    y+ neighbour's row 0 (512)
-constexpr uint32_t kXL30 = 5120;    // [z][y][2] x- neighbour's columns 6..7 (1024)
-constexpr uint32_t kXH30 = 6144;    // [z][y][2] x+ neighbour's columns 0..1 (1024)
-constexpr uint32_t kZL30 = 7168;    // [y][x]    z- neighbour's plane 7 (512)
-constexpr uint32_t kZH30 = 7680;    // [y][x]    z+ neighbour's plane 0 (512)
-constexpr uint32_t kDHalf30 = 8192;
-constexpr uint32_t kCtx30 = 16384;  // chunk record (176 B), then the chunk id at +176
+constexpr uint32_t kXL30 = 5120;    // [z][y]    x- neighbour's column 7 (512; per-lane copies)
+constexpr uint32_t kXH30 = 5632;    // [z][y]    x+ neighbour's column 0 (512; per-lane copies)
+constexpr uint32_t kZL30 = 6144;    // [y][x]    z- neighbour's plane 7 (512)
+constexpr uint32_t kZH30 = 6656;    // [y][x]    z+ neighbour's plane 0 (512)
+constexpr uint32_t kDHalf30 = 7168;
+// chunk record (176 B), then at +176 the chunk id and, for the compute
+// warps' x-halo prefetch, the next chunk's x- / x+ neighbours, flags and id
+constexpr uint32_t kCtx30 = 14336;
 constexpr uint32_t kCtxWords30 = 44;
-constexpr uint32_t kStage30 = 16384 + 256;
+constexpr uint32_t kStage30 = 14336 + 256;
 __host__ __device__ constexpr uint32_t bar30(int nst) { return (uint32_t)nst * kStage30; }  // full[nst] then empty[nst]
 __host__ __device__ constexpr uint32_t smem30(int nst) { return bar30(nst) + 16u * (uint32_t)nst; }
 
@@ -1320,18 +1322,21 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
                 mbar_arrive(full);
                 break;
             }
-            const int nb0 = d0.x, nb1 = d0.y, nb2 = d0.z, nb3 = d0.w, nb4 = d1.x, nb5 = d1.y;
+            const int nb2 = d0.z, nb3 = d0.w, nb4 = d1.x, nb5 = d1.y;
             const bool dl = !(d1.w & kFlagUnif);
             uint32_t bytes = 176u + 4096u;
-            bytes += (nb0 >= 0 ? 1024u : 0u) + (nb1 >= 0 ? 1024u : 0u) + (nb2 >= 0 ? 512u : 0u) +
-                     (nb3 >= 0 ? 512u : 0u) + (nb4 >= 0 ? 512u : 0u) + (nb5 >= 0 ? 512u : 0u);
-            if (dl) bytes += 4096u + 2u * 1024u + 4u * 512u;
+            bytes += (nb2 >= 0 ? 512u : 0u) + (nb3 >= 0 ? 512u : 0u) + (nb4 >= 0 ? 512u : 0u) +
+                     (nb5 >= 0 ? 512u : 0u);
+            if (dl) bytes += 4096u + 4u * 512u;
+            // the next chunk's x neighbours, for the compute warps' x-halo copies
+            sts_u32(st + kCtx30 + 180u, (uint32_t)e0.x);
+            sts_u32(st + kCtx30 + 184u, (uint32_t)e0.y);
+            sts_u32(st + kCtx30 + 188u, (uint32_t)e1.w);
+            sts_u32(st + kCtx30 + 192u, (uint32_t)c_nx);
             mbar_arrive_tx(full, bytes);
             const int64_t cb = (int64_t)c_cur * 512;
             bulk_g2s(st + kCtx30, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
             bulk_g2s(st + kOwn30, u + cb, 4096u, full);
-            if (nb0 >= 0) tma4(st + kXL30, &mux, 6, 0, 0, nb0, full);
-            if (nb1 >= 0) tma4(st + kXH30, &mux, 0, 0, 0, nb1, full);
             if (nb2 >= 0) tma4(st + kYL30, &muy, 0, 7, 0, nb2, full);
             if (nb3 >= 0) tma4(st + kYH30, &muy, 0, 0, 0, nb3, full);
             if (nb4 >= 0) bulk_g2s(st + kZL30, u + (int64_t)nb4 * 512 + 448, 512u, full);
@@ -1339,8 +1344,6 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
             if (dl) {
                 const uint32_t sd = st + kDHalf30;
                 bulk_g2s(sd + kOwn30, de + cb, 4096u, full);
-                tma4(sd + kXL30, &mdx, 6, 0, 0, nb0 >= 0 ? nb0 : sent_c, full);
-                tma4(sd + kXH30, &mdx, 0, 0, 0, nb1 >= 0 ? nb1 : sent_c, full);
                 tma4(sd + kYL30, &mdy, 0, 7, 0, nb2 >= 0 ? nb2 : sent_c, full);
                 tma4(sd + kYH30, &mdy, 0, 0, 0, nb3 >= 0 ? nb3 : sent_c, full);
                 bulk_g2s(sd + kZL30, de + (nb4 >= 0 ? (int64_t)nb4 * 512 + 448 : (int64_t)sent_c * 512), 512u, full);
@@ -1372,18 +1375,55 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
     // face read the halo buffers
     const uint32_t b_ym = y > 0 ? kOwn30 + oc - 64u : kYL30 + 16u * xp, s_ym = y > 0 ? 512u : 64u;
     const uint32_t b_yp = y < 7 ? kOwn30 + oc + 64u : kYH30 + 16u * xp, s_yp = y < 7 ? 512u : 64u;
-    const uint32_t b_l = xp > 0 ? kOwn30 + oc - 8u : kXL30 + 16u * y + 8u, s_l = xp > 0 ? 512u : 128u;
-    const uint32_t b_r = xp < 3 ? kOwn30 + oc + 16u : kXH30 + 16u * y, s_r = xp < 3 ? 512u : 128u;
-    const int z0 = 2 * warp, z1 = z0 + 1;
+    const uint32_t b_l = xp > 0 ? kOwn30 + oc - 8u : kXL30 + 8u * y, s_l = xp > 0 ? 512u : 64u;
+    const uint32_t b_r = xp < 3 ? kOwn30 + oc + 16u : kXH30 + 8u * y, s_r = xp < 3 ? 512u : 64u;
+    const int z0 = PW == 2 ? 2 * warp : warp, z1 = z0 + 1;
     double* __restrict__ un = A.un;
     bool pushed = false;
+    const uint32_t sent_off = (uint32_t)M.n_all * 512u;
+    // x-halo cells of this warp's planes, copied per lane (a TMA box would
+    // need a 16-B inner dimension: 64 16-B requests per box) into the stage
+    // of chunk cn, one chunk ahead: lanes xp = 0 / 3 copy column 7 of the x-
+    // neighbour / column 0 of the x+ neighbour (u, and D_eff unless uniform;
+    // the sentinel chunk's D_eff for a missing neighbour)
+    auto issue_xh = [&](uint32_t stn, int nbl, int nbh, int flags_n) {
+        if (xp == 0 || xp == 3) {
+            const int j = xp == 0 ? nbl : nbh;
+            const uint32_t dst = stn + (xp == 0 ? kXL30 : kXH30) + (uint32_t)(z0 * 8 + y) * 8u;
+            const uint32_t src = (uint32_t)j * 512u + (uint32_t)(z0 * 64 + y * 8) + (xp == 0 ? 7u : 0u);
+            const bool dl = !(flags_n & kFlagUnif);
+#pragma unroll
+            for (int q = 0; q < PW; ++q) {
+                const uint32_t o = src + 64u * q;
+                cp8_ud(dst + 64u * q, u + (j >= 0 ? o : 0u), j >= 0, dst + kDHalf30 + 64u * q,
+                       de + (j >= 0 ? o : sent_off), dl);
+            }
+        }
+        cp_commit();
+    };
+    uint32_t k = 0;
+    {
+        mbar_wait(full0, 0u);
+        const int c = (int)lds_u32(sm0 + kCtx30 + 176u);
+        if (c < 0) return;
+        issue_xh(sm0, (int)lds_u32(sm0 + kCtx30 + 128u), (int)lds_u32(sm0 + kCtx30 + 132u),
+                 (int)lds_u32(sm0 + kCtx30 + 156u));
+    }
 #pragma unroll 1
-    for (uint32_t k = 0;; ++k) {
-        const uint32_t s = k % kStages30, ph = (k / kStages30) & 1u;
+    for (;; ++k) {
+        const uint32_t s = k % kStages30;
         const uint32_t st = sm0 + s * kStage30;
-        mbar_wait(full0 + 8u * s, ph);
         const int c = (int)lds_u32(st + kCtx30 + 176u);
-        if (c < 0) break;
+        {  // x halos of the next chunk (its stage is free of them: this warp is done with it)
+            const int cn = (int)lds_u32(st + kCtx30 + 192u);
+            const uint32_t sn = (k + 1) % kStages30;
+            if (cn >= 0)
+                issue_xh(sm0 + sn * kStage30, (int)lds_u32(st + kCtx30 + 180u), (int)lds_u32(st + kCtx30 + 184u),
+                         (int)lds_u32(st + kCtx30 + 188u));
+            else
+                cp_commit();
+        }
+        cp_wait<1>();  // this chunk's x halos (this lane's own copies)
         ChunkCtx14 C;
         C.c = c;
         C.lm = lds_u32(st + kCtx30 + 4u * (uint32_t)lane);
@@ -1416,7 +1456,7 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
             compute30<REACTION, PUSH, HALF>(M, K, Q, C, z1, xp, y, bp, a1, uc1, dc1, uc0, dc0, uzp, dzp, un,
                                             pushed);
         } else {  // one plane per warp: z = warp
-            const int z = warp;
+            const int z = z0;
             Addr30 a;
             a.c = st + kOwn30 + oc + (uint32_t)z * 512u;
             a.zm = z == 0 ? st + kZL30 + oc : a.c - 512u;
@@ -1432,7 +1472,11 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8u * s);
+        const uint32_t s1 = (k + 1) % kStages30;
+        mbar_wait(full0 + 8u * s1, ((k + 1) / kStages30) & 1u);
+        if ((int)lds_u32(sm0 + s1 * kStage30 + kCtx30 + 176u) < 0) break;
     }
+    cp_wait<0>();
     // the pushed planes are visible system-wide before this kernel completes
     // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
     if (PUSH && pushed) __threadfence_system();
