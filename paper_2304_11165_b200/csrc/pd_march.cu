@@ -97,7 +97,14 @@ struct MarchArgs {
     double* peer_un[2];
     const int32_t* __restrict__ peer_ord;
     const double* __restrict__ dv;     // per chunk: the uniform D_eff of kFlagUnif chunks
+    int pf;                            // v14: L2 prefetch of the next load-side chunk's slabs
 };
+
+// Schedule entries carry bit 31 on uniform chunks (flagged_schedule); -1 ends.
+__device__ __forceinline__ int sched_id(int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); }
+__device__ __forceinline__ void prefetch_l2(const void* g, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
+}
 
 
 struct SlowConsts {
@@ -645,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
     auto sched_sync = [&]() -> int {
         claim_issue();
         const int p = __shfl_sync(0xffffffffu, raw, 0);
-        return p < n ? __ldg(&M.sched[p]) : -1;
+        return p < n ? sched_id(__ldg(&M.sched[p])) : -1;
     };
     auto fetch_ctx = [&](uint32_t e, int c) {  // masks + descriptor + uniform D of chunk c into entry e
         cp4(e + 4u * (uint32_t)lane, M.lm + (int64_t)(c < 0 ? 0 : c) * 32 + lane, c >= 0);
@@ -675,15 +682,22 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
         const uint32_t e0 = cent(ek);
         const int e1i = ek == 2 ? 0 : ek + 1, e2i = e1i == 2 ? 0 : e1i + 1;
         const uint32_t e1 = cent(e1i), e2 = cent(e2i);
-        const int c = (int)lds_u32(e0 + 160u);
+        const int c = sched_id((int)lds_u32(e0 + 160u));
         const uint32_t lm = c >= 0 ? lds_u32(e0 + 4u * (uint32_t)lane) : 0u;
         // descriptor word j lives at lane 24 + j (make_load_ctx14 / ChunkCtx14)
         const int dv = (int)lds_u32(e0 + 128u + 4u * (uint32_t)(lane >= 24 ? lane - 24 : 0));
         Cld = ChunkCtx14{c, __shfl_sync(0xffffffffu, dv, 30), __shfl_sync(0xffffffffu, dv, 31), lm,
                          lds1(e0 + 168u)};
         Lld = make_load_ctx14(c, lm, c >= 0 ? dv : -1, M.dbg, G);
-        const int c1 = (int)lds_u32(e1 + 160u);
+        const int e1raw = (int)lds_u32(e1 + 160u);
+        const int c1 = sched_id(e1raw);
         fetch_ctx(e1, c1);
+        // DRAM concurrency: also pull chunk c1's slabs towards L2 now (its
+        // plane loads start one chunk later); D_eff only for non-uniform chunks
+        if (M.pf && lane == 0 && c1 >= 0) {
+            prefetch_l2(u + (int64_t)c1 * 512, 4096u);
+            if (e1raw >= 0) prefetch_l2(de + (int64_t)c1 * 512, 4096u);
+        }
         if (lane == 0) {
             const bool ok = raw < n;
             cp4(e2 + 160u, M.sched + (ok ? raw : 0), ok);
@@ -1951,6 +1965,12 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
         march30_launch(g, p, M, r, pl != nullptr);
         return;
     }
+    static const int pf = [] {
+        const char* e = getenv("PD_M14_PF");
+        return e ? atoi(e) : 1;
+    }();
+    M.pf = pf;
+    if (ver == 14) M.sched = flagged_schedule(g, p, M.sched, M.n);
     const bool v20 = ver != 14;
     const size_t bytes = (size_t)(v20 ? kWarpBytes20 : kWarpBytes14) * kWarps;
     // the dynamic shared-memory opt-in is per device: set it once per device

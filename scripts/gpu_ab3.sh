@@ -5,7 +5,8 @@ mkdir -p gpurun_out
 VARS=${VARS:-"14 30"}
 CAND=${CAND:-30}
 PD_MARCH_V=$CAND timeout 900 python -m pytest -q -m gpu -x tests/test_gpu_parity.py tests/test_fuzz_parity.py tests/test_headline_parity.py tests/test_gpu_kats.py tests/test_march32.py tests/test_gpu_shard.py > gpurun_out/ab_pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab_pytest.log
-run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=0; PD_MARCH_V=$v PD_M30_CFG=$st "${@:2}"; }
+# "14:0" -> PD_M14_PF=0 (v14 without the L2 prefetch); "30:N" -> PD_M30_CFG=N
+run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=""; if [ "$v" = 14 ]; then PD_MARCH_V=$v PD_M14_PF=${st:-1} "${@:2}"; else PD_MARCH_V=$v PD_M30_CFG=${st:-0} "${@:2}"; fi; }
 for rep in 1 2; do for x in $VARS; do
   run $x timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu --no-e2e > gpurun_out/ab_bench_${x/:/_}_$rep.log 2>&1
 done; done
