@@ -1903,8 +1903,8 @@ void march30_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
 #undef PD_M_TABLE
     static const int cfg = [] {
         const char* e = getenv("PD_M30_CFG");
-        const int v = e ? atoi(e) : 0;
-        return v >= 0 && v <= 6 ? v : 0;
+        const int v = e ? atoi(e) : 5;
+        return v >= 0 && v <= 6 ? v : 5;
     }();
     const K30(*tab)[2][3] = tabs[cfg];
     const uint32_t smem = smem30(nst30(cfg));
@@ -1949,7 +1949,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.n_all = g->n_chunks;
     static const int ver = [] {
         const char* e = getenv("PD_MARCH_V");
-        return e ? atoi(e) : 14;
+        return e ? atoi(e) : 30;
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;

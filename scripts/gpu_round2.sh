@@ -1,0 +1,12 @@
+#!/bin/bash
+# Round evidence: full GPU suite, smoke, default bench (+ reference arm),
+# launch list and one full ncu capture of the step kernel.
+mkdir -p gpurun_out
+{ nvidia-smi --query-gpu=name,memory.total,clocks.max.sm,clocks.sm --format=csv; nproc; free -g; } > gpurun_out/env.txt 2>&1
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench exit $?" >> gpurun_out/bench_default.log
+timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref exit $?" >> gpurun_out/bench_ref.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/launches.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:ftcs_march -s 3 -c 1 -o gpurun_out/${NCU_NAME:-march_round} -f python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_round.log 2>&1
+tail -3 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; grep "^{" gpurun_out/bench_default.log | tail -1 | cut -c1-400; grep "^{" gpurun_out/bench_ref.log | tail -1 | cut -c1-200
