@@ -136,7 +136,7 @@ void write_sparse_snapshot(const SparseBlockGrid<T, Dims>& grid, const std::file
 }
 
 /// read_sparse_snapshot (snapshot.hpp:245-297): validated and loaded on the
-/// device, then rebuilt as a host grid chunk by chunk.
+/// device; the host grid adopts it (slabs fetched on first host access).
 template <typename T, int Dims>
 SparseBlockGrid<T, Dims> read_sparse_snapshot(const std::filesystem::path& path) {
     using Grid = SparseBlockGrid<T, Dims>;
@@ -147,27 +147,13 @@ SparseBlockGrid<T, Dims> read_sparse_snapshot(const std::filesystem::path& path)
     b200::check(pd_grid_read_snapshot(path.string().c_str(), Dims, static_cast<int>(sizeof(T)),
                                       b200::default_device(), &h.g, origin, buf.data(), buf.size(), &n_names));
     Grid grid(detail::geometry_of<Dims>(peek_snapshot(path)), detail::split_names(buf, n_names));
-    std::int64_t nc = 0;
-    b200::check(pd_grid_info(h.g, &nc, nullptr));
-    std::vector<std::int32_t> keys(static_cast<std::size_t>(nc) * Dims);
-    std::vector<std::uint64_t> masks(static_cast<std::size_t>(nc) * Grid::mask_words);
-    b200::check(pd_grid_download_layout(h.g, keys.data(), masks.data()));
-    std::vector<std::vector<T>> slabs(static_cast<std::size_t>(n_names));
-    for (int p = 0; p < n_names; ++p) {
-        slabs[static_cast<std::size_t>(p)].resize(static_cast<std::size_t>(nc) * Grid::chunk_volume);
-        b200::check(pd_grid_download(h.g, p, slabs[static_cast<std::size_t>(p)].data()));
-    }
-    for (std::int64_t c = 0; c < nc; ++c) {
-        typename Grid::Key key{};
-        for (int a = 0; a < Dims; ++a) key[a] = keys[static_cast<std::size_t>(c * Dims + a)];
-        for (int off = 0; off < Grid::chunk_volume; ++off)
-            if ((masks[static_cast<std::size_t>(c * Grid::mask_words + (off >> 6))] >> (off & 63)) & 1u)
-                grid.insert(Grid::node_index(key, off));
-        auto* chunk = grid.chunk_at_table(grid.chunk_linear_index(key));
-        for (int p = 0; p < n_names; ++p)
-            std::copy_n(slabs[static_cast<std::size_t>(p)].data() + c * Grid::chunk_volume, Grid::chunk_volume,
-                        grid.channel_data(*chunk, p));
-    }
+    // the host grid adopts the device grid as its mirror: layout now, slabs
+    // on first host access
+    std::vector<int> all(static_cast<std::size_t>(n_names));
+    for (int p = 0; p < n_names; ++p) all[static_cast<std::size_t>(p)] = p;
+    pd_grid* g = h.g;
+    h.g = nullptr;
+    grid.adopt_device(g, b200::default_device(), all);
     return grid;
 }
 

@@ -575,7 +575,9 @@ __global__ void deff32_kernel(const float* __restrict__ dcol, const uint64_t* __
     const float v = dcol[i];
     deff[i] = fl ? (half ? v * 0.5f : v) : __uint_as_float(kSent32);
     if (fl && !isfinite(v)) atomicAdd(bad, 1ull);
-    if (fl && fabsf(v) < 0x1p-125f) atomicAdd(bad + 1, 1ull);  // halving would not be exact
+    // halving would not be exact (tiny D), or the reference's d_a + d_b could
+    // overflow where h_a + h_b does not (huge D)
+    if (fl && (fabsf(v) < 0x1p-125f || fabsf(v) >= 0x1p126f)) atomicAdd(bad + 1, 1ull);
 }
 
 }  // namespace
@@ -631,11 +633,13 @@ void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, in
         {ftcs_march32_kernel<0, false>, ftcs_march32_kernel<1, false>, ftcs_march32_kernel<2, false>},
         {ftcs_march32_kernel<0, true>, ftcs_march32_kernel<1, true>, ftcs_march32_kernel<2, true>}};
     constexpr size_t bytes = (size_t)kWarpBytes32 * kW32;
-    static bool attr = false;
-    if (!attr) {
+    // the dynamic shared-memory opt-in is per device: set it once per device
+    static uint64_t attr_done = 0;
+    if (g->device < 0 || g->device >= 64) fail(PD_E_INPUT, "device index out of range");
+    if (!((attr_done >> g->device) & 1u)) {
         for (auto& row : table)
             for (auto k : row) PD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        attr = true;
+        attr_done |= 1ull << g->device;
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));

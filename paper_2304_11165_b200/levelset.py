@@ -144,15 +144,23 @@ def sussman_redistance(phi: DeviceField, opts: LevelSetOptions = LevelSetOptions
 
 def build_sparse_grid(sdf: DeviceField, band: pd.PhaseBand = pd.PhaseBand(),
                       channels: Sequence[str] = ("phi", "u", "D")) -> pd.SparseBlockGrid:
-    """geometry.hpp:148-176 on the device: the grid's state stays in HBM."""
+    """geometry.hpp:148-176 on the device: the grid's state stays in HBM.
+    Checks in the reference's order: band, finiteness, "phi" channel, empty
+    result."""
     chans = list(channels)
-    if "phi" not in chans:
-        raise InputError('channel list must contain "phi" to receive the level set')
+    has_phi = "phi" in chans
     h = C.c_void_p()
-    _check(lib.pd_build_grid_from_field(sdf.h, band.b_low, band.b_up, len(chans), chans.index("phi"),
-                                        C.byref(h)))
+    # without "phi" a one-property build still runs the finiteness check first
+    _check(lib.pd_build_grid_from_field(sdf.h, band.b_low, band.b_up, len(chans) if has_phi else 1,
+                                        chans.index("phi") if has_phi else 0, C.byref(h)))
     n = C.c_int64()
-    lib.pd_grid_info(h, C.byref(n), None)
+    act = C.c_int64()
+    lib.pd_grid_info(h, C.byref(n), C.byref(act))
+    if not has_phi or act.value == 0:
+        lib.pd_grid_destroy(h)
+        if not has_phi:
+            raise InputError('channel list must contain "phi" to receive the level set')
+        raise InputError("no node lies inside the phase band: the grid would be empty")
     dev = pd.DeviceGrid(h, sdf.geom, sdf.dtype, int(n.value), len(chans))
     return pd.SparseBlockGrid.from_device(sdf.geom, chans, dev, sdf.dtype)
 

@@ -32,11 +32,32 @@ def _run(name):
     return p.stdout
 
 
-# Host-only suites: the sparse block grid store and the geometry build never
-# touch the device, so they run in the CPU suite too.
-@pytest.mark.parametrize("suite", ["grid_test", "geometry_test"])
-def test_reference_host_suites(suite):
-    _run(suite)
+# Host-only suite: the sparse block grid store never touches the device, so
+# it runs in the CPU suite too.
+def test_reference_grid_suite_on_host():
+    _run("grid_test")
+
+
+@pytest.mark.gpu
+def test_reference_geometry_suite_on_b200():
+    # indicator, opening, band activation / chunk allocation and D(phi) run
+    # on the device through the drop-in geometry.hpp
+    out = _run("geometry_test")
+    assert "[  PASSED  ]" in out
+
+
+@pytest.mark.gpu
+def test_dropin_geometry_stage_large_box():
+    """The reference-API pipeline mask -> indicator -> opening -> grid -> D ->
+    run_simulation through the drop-in headers at 256^3 (cpp/geometry_timing)."""
+    exe = BIN / "geometry_timing"
+    if not exe.exists():
+        _ensure_built()
+    if not exe.exists():
+        pytest.skip("geometry_timing not built")
+    p = subprocess.run([str(exe), "256", "10"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
+    assert "build_sparse_grid" in p.stdout and "final mass" in p.stdout
 
 
 @pytest.mark.gpu

@@ -157,3 +157,44 @@ def test_nonfinite_total_mass_on_unrecorded_step_matches_reference(log2h, u_exp,
     for c in ("u", "u_next"):
         assert np.array_equal(ours.channel_data(c).view(np.uint64), g.prop(c).view(np.uint64)), c
     ours.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tbytes", [8, 4])
+def test_huge_diffusivity_is_not_halved(tbytes, cuda, ref):
+    """with |D| >= 2^1022 (2^126 in FP32) the reference's face sum
+    d_a + d_b overflows while the march path's halved h_a + h_b would not;
+    the plan must keep D unhalved so the result (here a numeric error) and
+    the state left behind are the reference's."""
+    from oracle.pyoracle import make_config
+    from paper_2304_11165_b200 import porediff as pd
+    n = 24
+    h = 1.0 / n
+    size, origin = (n,) * 3, (0.5 * h,) * 3
+    dt_np = np.float64 if tbytes == 8 else np.float32
+    sdf = ref.field_ball(size, (h,) * 3, origin, (0.5, 0.45, 0.5), 0.35, -1.0)
+    g = ref.grid_from_sdf(size, (h,) * 3, origin, sdf, tbytes=tbytes)
+    g.fill_hash("u", 4)
+    big = 2.0 ** 1023 if tbytes == 8 else 2.0 ** 127
+    d = g.prop("D")
+    keys, masks = g.layout()
+    act = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).astype(bool)
+    d[act] = big * (0.5 + 0.5 * g.prop("u")[act])
+    g.set_prop("D", d.astype(dt_np))
+    geom = pd.GridGeometry.make(size, (h,) * 3, origin)
+    data = {c: g.prop(c) for c in ("phi", "u", "D", "u_next")}
+    ours = pd.SparseBlockGrid.from_layout(geom, pd.solver_channels(), keys, masks, data, dt_np)
+    dt = 1e-300 if tbytes == 8 else 1e-40
+    code, msg, rows = g.run(make_config(dt, 3, record_every=1, enforce_stability=False))
+    cfg = pd.SimulationConfig(dt=dt, n_steps=3, record_every=1, enforce_stability=False)
+    if code == 0:
+        res = pd.run_simulation(ours, cfg)
+        assert [tuple(r) for r in rows] == [(x.step, x.time, x.total_mass, x.min_u, x.max_u) for x in res.diagnostics]
+    else:
+        with pytest.raises(pd.PorediffError) as ei:
+            pd.run_simulation(ours, cfg)
+        assert str(ei.value) == msg
+    view = np.uint64 if tbytes == 8 else np.uint32
+    for c in ("u", "u_next"):
+        assert np.array_equal(ours.channel_data(c).view(view), g.prop(c).view(view)), c
+    ours.close()
