@@ -308,6 +308,7 @@ def run_ours(args):
     dom.run(stepper, 0, args.warmup)
     sync()
     launches0 = dom.launches(stepper)
+    wait0 = dom.peer_wait_ns(stepper)
     with Clocks(local) as clk:
         sync()
         t0 = time.perf_counter()
@@ -321,8 +322,9 @@ def run_ours(args):
     # exact global diagnostics of the final state (all ranks take part)
     diag = dom.diagnostics(stepper)
     kern_ms = dom.last_kernel_ms / args.steps
-    mine = torch.tensor([ms, kern_ms, float(dom.owned_active), float(dom.owned_chunks)], dtype=torch.float64,
-                        device=red_dev)
+    wait_ms = (dom.peer_wait_ns(stepper) - wait0) / 1e6 / args.steps
+    mine = torch.tensor([ms, kern_ms, float(dom.owned_active), float(dom.owned_chunks), wait_ms],
+                        dtype=torch.float64, device=red_dev)
     if world > 1:
         allv = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allv, mine)
@@ -342,8 +344,12 @@ def run_ours(args):
     traffic, traffic_src = ncu_traffic(args.n)
     chunks_total = int(per_rank[:, 3].sum())
     ranks = [{"rank": r, "step_ms": float(per_rank[r, 0]) / args.steps, "kernel_ms": float(per_rank[r, 1]),
-              "active_nodes": int(per_rank[r, 2]), "chunks": int(per_rank[r, 3])} for r in range(world)]
-    imbalance = float(per_rank[:, 0].max() / per_rank[:, 0].mean() - 1.0)
+              "active_nodes": int(per_rank[r, 2]), "chunks": int(per_rank[r, 3]),
+              "halo_wait_ms_per_step": float(per_rank[r, 4])} for r in range(world)]
+    # work imbalance: per-rank step-kernel time minus the time spent blocked
+    # on the neighbours (the fused exchange's per-step wait)
+    work = per_rank[:, 1] - per_rank[:, 4]
+    imbalance = float(work.max() / work.mean() - 1.0) if work.mean() > 0 else 0.0
     # the bench domain leaves the device before the end-to-end run needs it
     dom.close(stepper)
     del dom
@@ -498,7 +504,7 @@ def _layer_chunks(pd, geom, centers, radii):
     class _P:
         def arrays(self):
             return centers, radii
-    chunks, active = shard.layer_work(geom, _P())
+    chunks, active, _ = shard.layer_work(geom, _P())
     return int(active.sum()), int(chunks.sum())
 
 

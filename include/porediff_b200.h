@@ -340,6 +340,13 @@ int pd_peek_snapshot(const char* path, pd_snapshot_info* info, char* names_buf, 
 int pd_sphere_pack_layer_work(int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
                               int64_t n_spheres, const double* centers, const double* radii, double b_low,
                               double b_up, int device, int64_t* chunks_per_layer, int64_t* active_per_layer);
+/* Same, plus the fully active chunks per layer (the candidates for the march
+ * kernels' cheaper uniform path): the per-layer step cost model of the
+ * cost-weighted slab cuts (shard.py). */
+int pd_sphere_pack_layer_cost(int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
+                              int64_t n_spheres, const double* centers, const double* radii, double b_low,
+                              double b_up, int device, int64_t* chunks_per_layer, int64_t* active_per_layer,
+                              int64_t* full_per_layer);
 
 /* ---- fused multi-GPU halo exchange over peer memory (
  * pd_peer.cu) ---------------------------------------------------------------
@@ -371,6 +378,10 @@ int pd_stepper_set_peer(pd_stepper* s, int side, void* const* peer_cols, int n_c
                         const int32_t* src_ords, const int32_t* dst_ords, int64_t n);
 /* zero the own counters and the step epoch (all ranks, then a host barrier,
  * before the first exchanged step) */
+/* Time the fused exchange's per-step wait spent blocked on the neighbours'
+ * step counters (total ns and number of waits since the last reset): the
+ * load imbalance between slabs (bench.py reports it per rank). */
+int pd_stepper_peer_stats(pd_stepper* s, uint64_t* wait_ns, int64_t* waits);
 int pd_stepper_peer_reset(pd_stepper* s);
 
 /* ---- VTK export (reference vtk.hpp:57-143, scalar_text.hpp:20-28; SURVEY

@@ -902,8 +902,9 @@ int pd_stepper_set_peer(pd_stepper* s, int side, void* const* peer_cols, int n_c
             PD_CUDA(pd_malloc(&s->peer.d_ord, sizeof(int32_t) * 2 * (size_t)std::max<int64_t>(1, g->n_chunks)));
             PD_CUDA(cudaMemsetAsync(s->peer.d_ord, 0xff, sizeof(int32_t) * 2 * (size_t)std::max<int64_t>(1, g->n_chunks),
                                     g->stream));
-            PD_CUDA(pd_malloc(&s->peer.d_err, sizeof(int)));
-            PD_CUDA(cudaMemsetAsync(s->peer.d_err, 0, sizeof(int), g->stream));
+            // [0] timeout flag, [2..3] total wait ns, [4..5] waits (pd_peer.cu)
+            PD_CUDA(pd_malloc(&s->peer.d_err, 32));
+            PD_CUDA(cudaMemsetAsync(s->peer.d_err, 0, 32, g->stream));
         }
         std::vector<int32_t> ord((size_t)g->n_chunks * 2);
         PD_CUDA(cudaMemcpyAsync(ord.data(), s->peer.d_ord, sizeof(int32_t) * ord.size(), cudaMemcpyDeviceToHost,
@@ -930,9 +931,23 @@ int pd_stepper_peer_reset(pd_stepper* s) {
     return guarded([&] {
         DeviceGuard dg(s->g->device);
         if (s->peer.d_sync) PD_CUDA(cudaMemset(s->peer.d_sync, 0, 64));
-        if (s->peer.d_err) PD_CUDA(cudaMemset(s->peer.d_err, 0, sizeof(int)));
+        if (s->peer.d_err) PD_CUDA(cudaMemset(s->peer.d_err, 0, 32));
         s->peer.epoch = 0;
         PD_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+int pd_stepper_peer_stats(pd_stepper* s, uint64_t* wait_ns, int64_t* waits) {
+    return guarded([&] {
+        unsigned long long h[2] = {0, 0};
+        if (s->peer.d_err) {
+            DeviceGuard dg(s->g->device);
+            PD_CUDA(cudaStreamSynchronize(s->g->stream));
+            PD_CUDA(cudaMemcpy(h, reinterpret_cast<unsigned long long*>(s->peer.d_err) + 1, sizeof h,
+                               cudaMemcpyDeviceToHost));
+        }
+        if (wait_ns) *wait_ns = h[0];
+        if (waits) *waits = (int64_t)h[1];
     });
 }
 

@@ -580,7 +580,7 @@ namespace pdb {
 // per chunk layer (z): allocated chunks and active nodes of a slot-mask pass
 __global__ void layer_work_kernel(const uint64_t* __restrict__ slot_masks, const int32_t* __restrict__ slot_flag,
                                   int64_t per_layer, int64_t layers, unsigned long long* __restrict__ chunks,
-                                  unsigned long long* __restrict__ active) {
+                                  unsigned long long* __restrict__ active, unsigned long long* __restrict__ full) {
     const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (slot >= per_layer * layers) return;
     if (!slot_flag[slot]) return;
@@ -589,6 +589,7 @@ __global__ void layer_work_kernel(const uint64_t* __restrict__ slot_masks, const
     for (int w = 0; w < 8; ++w) a += (unsigned long long)__popcll(slot_masks[slot * 8 + w]);
     atomicAdd(chunks + z, 1ull);
     atomicAdd(active + z, a);
+    if (a == 512) atomicAdd(full + z, 1ull);
 }
 }  // namespace pdb
 
@@ -940,6 +941,14 @@ int pd_build_sphere_pack_grid(int scalar_bytes, const int64_t* size, const doubl
 int pd_sphere_pack_layer_work(int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
                               int64_t n_spheres, const double* centers, const double* radii, double b_low,
                               double b_up, int device, int64_t* chunks_per_layer, int64_t* active_per_layer) {
+    return pd_sphere_pack_layer_cost(scalar_bytes, size, spacing, origin, n_spheres, centers, radii, b_low, b_up,
+                                     device, chunks_per_layer, active_per_layer, nullptr);
+}
+
+int pd_sphere_pack_layer_cost(int scalar_bytes, const int64_t* size, const double* spacing, const double* origin,
+                              int64_t n_spheres, const double* centers, const double* radii, double b_low,
+                              double b_up, int device, int64_t* chunks_per_layer, int64_t* active_per_layer,
+                              int64_t* full_per_layer) {
     return guarded([&] {
         pd_grid tmp;
         init_geometry(&tmp, 3, scalar_bytes, size, spacing, device);
@@ -985,9 +994,9 @@ int pd_sphere_pack_layer_work(int scalar_bytes, const int64_t* size, const doubl
         PD_CUDA(pd_malloc(&slot_flag, sizeof(int32_t) * (size_t)slots));
         fr.p.push_back(slot_flag);
         const int64_t layers = tmp.cc[2];
-        PD_CUDA(pd_malloc(&d_cnt, sizeof(unsigned long long) * 2 * (size_t)layers));
+        PD_CUDA(pd_malloc(&d_cnt, sizeof(unsigned long long) * 3 * (size_t)layers));
         fr.p.push_back(d_cnt);
-        PD_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 2 * (size_t)layers, st));
+        PD_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 3 * (size_t)layers, st));
         if (scalar_bytes == 8) {
             const double eps = std::numeric_limits<double>::epsilon();
             pack_mask_kernel<double><<<(unsigned)slots, 512, 0, st>>>(p, b_low + eps, b_up - eps, slot_masks,
@@ -999,14 +1008,16 @@ int pd_sphere_pack_layer_work(int scalar_bytes, const int64_t* size, const doubl
         }
         auto* cnt = static_cast<unsigned long long*>(d_cnt);
         layer_work_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(slot_masks, slot_flag, tmp.cc[0] * tmp.cc[1],
-                                                                           layers, cnt, cnt + layers);
+                                                                           layers, cnt, cnt + layers,
+                                                                           cnt + 2 * layers);
         PD_CUDA(cudaGetLastError());
-        std::vector<unsigned long long> h((size_t)(2 * layers));
+        std::vector<unsigned long long> h((size_t)(3 * layers));
         PD_CUDA(cudaMemcpyAsync(h.data(), d_cnt, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
         PD_CUDA(cudaStreamSynchronize(st));
         for (int64_t z = 0; z < layers; ++z) {
             if (chunks_per_layer) chunks_per_layer[z] = (int64_t)h[(size_t)z];
             if (active_per_layer) active_per_layer[z] = (int64_t)h[(size_t)(layers + z)];
+            if (full_per_layer) full_per_layer[z] = (int64_t)h[(size_t)(2 * layers + z)];
         }
     });
 }

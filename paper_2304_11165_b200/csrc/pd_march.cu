@@ -442,9 +442,13 @@ __device__ __noinline__ void push_pair14(const MarchArgs& M, const ChunkCtx14& C
     const int side = z == 0 ? 0 : 1;
     if (!(C.flags & (side ? kFlagPushHi : kFlagPushLo))) return;
     const int32_t o = __ldg(M.peer_ord + 2 * (int64_t)C.c + side);
-    double* p = M.peer_un[side] + (int64_t)o * 512 + z * 64 + bp;
-    if (a0) p[0] = out0;
-    if (a1) p[1] = out1;
+    double* p = M.peer_un[side] + (int64_t)o * 512 + z * 64 + bp;  // bp even: 16-B aligned pair
+    if (a0 && a1) {  // one 16-B remote store (NVLink) for a fully active pair
+        *reinterpret_cast<double2*>(p) = make_double2(out0, out1);
+    } else {
+        if (a0) p[0] = out0;
+        if (a1) p[1] = out1;
+    }
 }
 
 // Uniform chunk (kFlagUnif): every node active and fluid, every face

@@ -41,6 +41,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
+// err[0]: timeout flag; err + 8 B: total wait ns and wait count (the per-step
+// barrier time of the fused exchange, pd_stepper_peer_stats)
 __global__ void peer_wait_kernel(const unsigned* sync, int need_lo, int need_hi, unsigned epoch, int* err) {
     const unsigned long long t0 = global_ns();
     for (int side = 0; side < 2; ++side) {
@@ -53,6 +55,9 @@ __global__ void peer_wait_kernel(const unsigned* sync, int need_lo, int need_hi,
             }
         }
     }
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(err) + 1;
+    st[0] += global_ns() - t0;
+    st[1] += 1;
 }
 
 __global__ void peer_signal_kernel(unsigned* lo, unsigned* hi, unsigned v) {

@@ -152,10 +152,11 @@ class Domain:
         # cut the z chunk layers at equal prefix sums of work (allocated chunks
         # per layer; the step costs per chunk), not at equal layer counts
         if balance is None:
-            balance = os.environ.get("PD_BALANCE", "chunks") if world > 1 else "layers"
+            balance = os.environ.get("PD_BALANCE", "cost") if world > 1 else "layers"
         weights = None
-        if balance in ("chunks", "active"):
-            weights = layer_work(self.geom, pack, dtype, device)[0 if balance == "chunks" else 1]
+        if balance in ("chunks", "active", "cost"):
+            ch, ac, fu = layer_work(self.geom, pack, dtype, device)
+            weights = {"chunks": ch, "active": ac, "cost": layer_cost(ch, fu)}[balance]
         self.balance = balance
         z0, z1 = slab_bounds(cc[2], world, rank, weights)
         lo = (C.c_int64 * 3)(0, 0, max(0, z0 - 1))
@@ -409,6 +410,16 @@ class Domain:
             setattr(self, k, None)
         self.torch.cuda.empty_cache()
 
+    def peer_wait_ns(self, stepper) -> int:
+        """Total ns the fused exchange's per-step waits spent blocked on the
+        neighbours' step counters (0 without the peer exchange)."""
+        if self.exchange_mode != "peer":
+            return 0
+        ns = C.c_uint64()
+        n = C.c_int64()
+        self.pd._check(self.lib.pd_stepper_peer_stats(stepper, C.byref(ns), C.byref(n)))
+        return int(ns.value)
+
     def kernel_ms(self, stepper) -> float:
         """Average device time of one step kernel launch so far."""
         return self._kernel_ms / max(1, self._steps)
@@ -420,20 +431,33 @@ class Domain:
 
 
 def layer_work(geom, pack, dtype=np.float64, device: int = 0):
-    """(allocated chunks, active nodes) per z chunk layer of the sphere-pack
-    domain, from the builder's mask pass without building the grid
-    (pd_sphere_pack_layer_work)."""
+    """(allocated chunks, active nodes, fully active chunks) per z chunk layer
+    of the sphere-pack domain, from the builder's mask pass without building
+    the grid (pd_sphere_pack_layer_cost)."""
     from . import porediff as pd
     from ._lib import lib
     centers, radii = pack.arrays()
     layers = (geom.size[2] + 7) // 8
     chunks = np.zeros(layers, np.int64)
     active = np.zeros(layers, np.int64)
-    pd._check(lib.pd_sphere_pack_layer_work(
+    full = np.zeros(layers, np.int64)
+    pd._check(lib.pd_sphere_pack_layer_cost(
         np.dtype(dtype).itemsize, (C.c_int64 * 3)(*geom.size), (C.c_double * 3)(*geom.spacing),
         (C.c_double * 3)(*geom.origin), len(radii), centers.ctypes.data_as(C.POINTER(C.c_double)),
-        radii.ctypes.data_as(C.POINTER(C.c_double)), 0.0, math.inf, device, chunks.ctypes.data, active.ctypes.data))
-    return chunks, active
+        radii.ctypes.data_as(C.POINTER(C.c_double)), 0.0, math.inf, device, chunks.ctypes.data, active.ctypes.data,
+        full.ctypes.data))
+    return chunks, active, full
+
+
+# Step cost of a fully active chunk relative to a partial one: fully active
+# chunks mostly take the march kernels' uniform path (no D_eff traffic, ~40 %
+# fewer FP64 operations: 8 KB instead of 12 KB per chunk, DESIGN.md section 4).
+UNIFORM_COST = 2.0 / 3.0
+
+
+def layer_cost(chunks: np.ndarray, full: np.ndarray) -> np.ndarray:
+    """Per-layer step cost for the slab cuts (PD_BALANCE=cost, the default)."""
+    return (chunks - full) + UNIFORM_COST * full
 
 
 def build_domain(n, pack, rank, world, device=0, dtype=np.float64) -> Domain:

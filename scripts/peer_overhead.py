@@ -7,7 +7,13 @@ the shard kernels plus the exchange overhead; the difference to the
 unsharded step is what the exchange costs. Results are also checked bit for
 bit against the unsharded run (owned u of every shard).
 
-    python scripts/peer_overhead.py [--n 1024] [--world 2] [--steps 20]
+Slab balance: before the exchange is wired up, every shard is stepped alone
+(pd_stepper_run over its owned range) and the per-shard kernel times give
+the load imbalance max/mean - 1 of the cuts (--balance layers | chunks |
+cost, the per-layer cost model of shard.layer_cost; --balance all measures
+the three and runs the exchange with "cost").
+
+    python scripts/peer_overhead.py [--n 1024] [--world 2] [--steps 20] [--balance cost]
 """
 import argparse
 import ctypes as C
@@ -56,6 +62,7 @@ def main():
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--balance", default="cost", choices=["layers", "chunks", "cost", "all"])
     a = ap.parse_args()
     n, world, steps = a.n, a.world, a.steps
     geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
@@ -79,18 +86,52 @@ def main():
     lib.pd_stepper_destroy(s_full)
     full.close()
 
-    shards = []
-    for rk in range(world):
-        z0, z1 = shard.slab_bounds(cc, world, rk)
-        dev = build(geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)))
-        keys, _ = dev.layout()
-        plan = shard.exchange_plan(keys, z0, z1, rk, world)
-        s = stepper(dev, dt, (plan.begin, plan.end))
-        cols = (C.c_void_p * 4)()
-        pd._check(lib.pd_grid_column_ptrs(dev.h, cols))
-        sync = C.c_void_p()
-        pd._check(lib.pd_stepper_sync_words(s, C.byref(sync)))
-        shards.append((dev, plan, s, keys, cols, sync))
+    ch, ac, fu = shard.layer_work(geom, pack)
+    weights = {"layers": None, "chunks": ch, "cost": shard.layer_cost(ch, fu)}
+
+    def make_shards(mode):
+        out = []
+        for rk in range(world):
+            z0, z1 = shard.slab_bounds(cc, world, rk, weights[mode])
+            dev = build(geom, centers, radii, (0, 0, max(0, z0 - 1)), (cc, cc, min(cc, z1 + 1)))
+            keys, _ = dev.layout()
+            plan = shard.exchange_plan(keys, z0, z1, rk, world)
+            s = stepper(dev, dt, (plan.begin, plan.end))
+            cols = (C.c_void_p * 4)()
+            pd._check(lib.pd_grid_column_ptrs(dev.h, cols))
+            sync = C.c_void_p()
+            pd._check(lib.pd_stepper_sync_words(s, C.byref(sync)))
+            out.append((dev, plan, s, keys, cols, sync))
+        return out
+
+    def shard_times(shs):
+        """Each shard stepped alone (no exchange): its kernel ms per step."""
+        ts = []
+        for dev, plan, s, *_ in shs:
+            pd._check(lib.pd_stepper_run(s, 0, 2, 1 << 40, None, rows, C.byref(nr)))
+            pd._check(lib.pd_stepper_run(s, 2, steps, 1 << 40, None, rows, C.byref(nr)))
+            lib.pd_stepper_last_ms(s, C.byref(ms))
+            ts.append(ms.value / steps)
+            pd._check(lib.pd_stepper_run(s, 2 + steps, steps + 2, 1 << 40, None, rows, C.byref(nr)))  # even count
+        return ts
+
+    modes = ["layers", "chunks", "cost"] if a.balance == "all" else [a.balance]
+    for mode in modes:
+        shs = make_shards(mode)
+        ts = shard_times(shs)
+        print(f"{n}^3, {world} shards, balance={mode}: shard kernel ms/step {[round(t, 3) for t in ts]}, "
+              f"sum {sum(ts):.3f} (unsharded {t_full:.3f}), imbalance max/mean-1 = "
+              f"{max(ts) / (sum(ts) / len(ts)) - 1:+.2%}", flush=True)
+        if mode != modes[-1]:
+            for dev, plan, s, *_ in shs:
+                lib.pd_stepper_destroy(s)
+                dev.close()
+    shards = shs
+    # the timing runs above advanced every shard an even number of steps from
+    # the same state; restart all of them from u0 for the exchange check
+    for dev, *_ in shards:
+        dev.fill_hash(1, 1)
+        dev.fill_const(3, 0.0)
     for rk, (dev, plan, s, keys, cols, sync) in enumerate(shards):
         for side, nb, src in ((0, rk - 1, plan.send_down), (1, rk + 1, plan.send_up)):
             if 0 <= nb < world:

@@ -343,7 +343,7 @@ def test_layer_work_matches_built_grid_and_balances(cuda):
     n = 96
     geom = pd.GridGeometry.cell_centered_box(n, 0.0, 1.0, 3)
     pack = sy.SpherePacking.random((0, 0, 0), (1, 1, 1), 50, 0.05, 0.2, 77)
-    chunks, active = shard.layer_work(geom, pack)
+    chunks, active, full = shard.layer_work(geom, pack)
     c, r = pack.arrays()
     dev = pd.DeviceGrid.sphere_pack(geom, c, r)
     keys, masks = dev.layout()
@@ -352,6 +352,8 @@ def test_layer_work_matches_built_grid_and_balances(cuda):
     pop = np.unpackbits(masks.view(np.uint8), bitorder="little").reshape(len(masks), -1).sum(axis=1)
     want_a = np.bincount(keys[:, 2], weights=pop, minlength=cc).astype(np.int64)
     assert np.array_equal(chunks, want_c) and np.array_equal(active, want_a)
+    want_f = np.bincount(keys[:, 2], weights=(pop == 512), minlength=cc).astype(np.int64)
+    assert np.array_equal(full, want_f) and full.sum() > 0
     dev.close()
     for world in (2, 3, 5):
         b = [shard.slab_bounds(cc, world, r, chunks) for r in range(world)]
