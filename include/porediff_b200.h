@@ -192,6 +192,20 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
  * run_simulation, solver.hpp:514-515) and is returned in the row. factor:
  * the step's source factor T(g(t)) (1 without a time factor). */
 int pd_stepper_step(pd_stepper* s, int64_t step_index, double factor, pd_diag* row);
+/* ---- steady-state observers (north_star (3); no reference counterpart:
+ * checked against a NumPy restatement, tests/test_observe.py) ------------- */
+/* With on != 0, every row pd_stepper_run records also yields the convergence
+ * norm max over active nodes of |u(step) - u(step-1)| (exact, order-free). */
+int pd_stepper_set_convergence(pd_stepper* s, int on);
+/* Convergence norms of the rows of the last pd_stepper_run (row order). */
+int pd_stepper_convergence(const pd_stepper* s, double* out, int64_t cap, int64_t* n);
+/* Diffusive flux of the current u through the plane between node layers
+ * `layer` and `layer`+1 of `axis`: face_sum = sum over faces with both nodes
+ * fluid of dh * (u_{L+1} - u_L), dh = (d_a + d_b) * T(0.5) (the reference's
+ * face coefficient, solver.hpp:430-433), chunk sums folded pairwise in
+ * ordinal order; flux = -face_sum / h_axis * (face area). */
+int pd_stepper_plane_flux(pd_stepper* s, int axis, int64_t layer, double* face_sum, double* flux,
+                          int64_t* faces);
 /* Device time (ms, CUDA events) of the last pd_stepper_run's step kernels. */
 int pd_stepper_last_ms(const pd_stepper* s, double* ms);
 /* Launches of the step kernel so far (benchmark accounting). */

@@ -170,6 +170,9 @@ _SIGNATURES = [
     ("pd_stepper_sync_words", C.c_int, [_P, C.POINTER(C.c_void_p)]),
     ("pd_stepper_sync_ipc_handle", C.c_int, [_P, _P]),
     ("pd_stepper_set_peer", C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p), C.c_int, _P, _P, _P, C.c_int64]),
+    ("pd_stepper_set_convergence", C.c_int, [_P, C.c_int]),
+    ("pd_stepper_convergence", C.c_int, [_P, _DP, C.c_int64, _I64P]),
+    ("pd_stepper_plane_flux", C.c_int, [_P, C.c_int, C.c_int64, _DP, _DP, _I64P]),
     ("pd_stepper_peer_stats", C.c_int, [_P, C.POINTER(C.c_uint64), _I64P]),
     ("pd_stepper_peer_reset", C.c_int, [_P]),
     ("pd_format_scalar", C.c_int, [C.c_double, C.c_int, C.c_char_p, C.c_size_t, C.POINTER(C.c_int)]),

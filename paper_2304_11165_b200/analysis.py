@@ -250,3 +250,99 @@ def write_frap_csv(path: str, exp: FrapExperiment) -> None:
                 f.write(f"{format_scalar(s.time)},{format_scalar(s.recovery)}\n")
     except OSError:
         raise pd.IoError(f"cannot open '{path}' for writing") from None
+
+
+# ---------------------------------------------------------------------------
+# Steady-state flux estimator of D_eff and tortuosity (north_star (3)).
+# The reference has no flux-based estimator (its only D_eff path is the FRAP
+# fit above), so this has no reference counterpart: "parity unpinned". It is
+# checked against a NumPy restatement (tests/test_observe.py) and, on a free
+# box, against the exact answer D_eff = D.
+# ---------------------------------------------------------------------------
+
+@dataclass
+class SteadyStateResult:
+    steps: int                 # FTCS steps taken
+    converged: bool            # rate criterion met before max_steps
+    rate: float                # last normalised rate max|du| L^2 / (dt D_mol |dc|)
+    flux: float                # total diffusive flux through the measuring plane (+axis direction)
+    plane_fluxes: List[float]  # flux through every interior plane (conservation check)
+    d_bulk: float              # F L / (A dc): bulk effective diffusivity
+    porosity: float            # fluid nodes / box nodes
+    d_eff: float               # d_bulk / porosity: pore-scale effective diffusivity
+    tau: float                 # D_mol / d_eff (the FRAP fit's tau_d convention)
+    norms: List[float] = field(default_factory=list)
+
+
+def steady_state_diffusivity(grid: pd.SparseBlockGrid, axis: int = 0, c_in: float = 1.0, c_out: float = 0.0,
+                             d_molecular: float = 1.0, dt: float = 0.0, tol: float = 1e-8,
+                             check_every: int = 200, max_steps: int = 10 ** 7,
+                             plane: int = -1) -> SteadyStateResult:
+    """Drives the grid's u to the steady state of a through-diffusion
+    experiment -- Dirichlet c_in on the low face of `axis`, c_out on the high
+    face, no flux elsewhere and at the pore walls -- with the device FTCS
+    stepper, stopping when the normalised rate max|u^{n+1}-u^n| L^2 /
+    (dt D_mol |c_in - c_out|) of a recorded step drops below `tol` (device
+    convergence observer). Then the flux F through the plane between node
+    layers `plane` and `plane`+1 (default: the middle) gives
+    d_bulk = F L / (A |dc|), with A the box cross-section and L =
+    (size[axis] + 1) h the distance between the two Dirichlet ghost planes
+    (so a free box with uniform D returns D exactly), d_eff = d_bulk /
+    porosity and tau = D_mol / d_eff. The grid's D channel is used as is
+    (populate it with D_mol in the pore space for a molecular-diffusion
+    experiment); u starts from its current values."""
+    geom = grid.geometry()
+    if not (0 <= axis < geom.dims):
+        raise InputError("flux axis out of range")
+    dc = c_in - c_out
+    if not (dc != 0.0) or not math.isfinite(dc):
+        raise InputError("steady state needs c_in != c_out")
+    if not (d_molecular > 0.0):
+        raise InputError("molecular diffusivity must be positive and finite")
+    if check_every < 1 or max_steps < 1:
+        raise InputError("check_every and max_steps must be at least 1")
+    n_ax = geom.size[axis]
+    if plane < 0:
+        plane = (n_ax - 1) // 2
+    if not (0 <= plane < n_ax - 1):
+        raise InputError("flux plane outside the box interior")
+    dmax = pd.max_diffusivity(grid)
+    bound = pd.stability_dt(geom, dmax) if dmax > 0 else math.inf
+    if dt == 0.0:
+        dt = 0.4 * bound
+    elif not (0.0 < dt < bound):
+        raise InputError("time step must lie in (0, " + format_scalar(bound) + ")")
+    cfg = pd.SimulationConfig(dt=dt, n_steps=max_steps, record_every=check_every)
+    cfg.outer_bc[2 * axis] = pd.FaceBc.dirichlet(c_in)
+    cfg.outer_bc[2 * axis + 1] = pd.FaceBc.dirichlet(c_out)
+    h = geom.spacing[axis]
+    length = (n_ax + 1) * h
+    scale = length * length / (dt * d_molecular * abs(dc))
+    st = pd.FtcsStepper(grid, cfg)
+    try:
+        st.set_convergence(True)
+        steps, rate, norms, converged = 0, math.inf, [], False
+        while steps < max_steps:
+            n = min(check_every * 16, max_steps - steps)
+            st.run(steps, n, steps + n)
+            got = st.convergence_norms()
+            norms.extend(got)
+            steps += n
+            if got:
+                rate = got[-1] * scale
+                if rate < tol:
+                    converged = True
+                    break
+        fluxes = [st.plane_flux(axis, L)[1] for L in range(n_ax - 1)]
+        flux = fluxes[plane]
+    finally:
+        st.close()
+    area = 1.0
+    for a in range(geom.dims):
+        if a != axis:
+            area *= geom.size[a] * geom.spacing[a]
+    d_bulk = flux * length / (area * dc)
+    porosity = grid.active_node_count() / geom.node_count()
+    d_eff = d_bulk / porosity
+    return SteadyStateResult(steps, converged, rate, flux, fluxes, d_bulk, porosity, d_eff,
+                             d_molecular / d_eff if d_eff > 0 else math.inf, norms)

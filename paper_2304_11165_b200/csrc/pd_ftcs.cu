@@ -27,6 +27,7 @@
 #include <cstring>
 
 #include "pd_internal.cuh"
+#include <cstring>
 
 namespace pdb {
 
@@ -309,6 +310,10 @@ struct pd_stepper {
     int64_t rlo[3] = {0, 0, 0}, rhi[3] = {0, 0, 0};
     double* d_region = nullptr;  // one per row of the batch
     std::vector<double> region_out;
+    // steady-state observer (pd_observe.cu): max |u_new - u_old| per record
+    bool has_conv = false;
+    unsigned long long* d_conv = nullptr;  // one per row of the batch (bit patterns)
+    std::vector<double> conv_out;
     pdb::PeerState peer;  // fused multi-GPU halo push (pd_peer.cu)
     int e_huge = 990;     // huge_exponent(): set at creation
     uint64_t ver_phi = 0, ver_d = 0;  // prop versions the static state was built from
@@ -584,6 +589,7 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
             PD_CUDA(pd_malloc(&s->d_bad, sizeof(unsigned long long)));
             PD_CUDA(pd_malloc(&s->d_rows, sizeof(double) * 3 * (size_t)kBatch));
             PD_CUDA(pd_malloc(&s->d_region, sizeof(double) * (size_t)kBatch));
+            PD_CUDA(pd_malloc(&s->d_conv, sizeof(unsigned long long) * (size_t)kBatch));
             PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)kBatch, g->stream));
             PD_CUDA(cudaMemsetAsync(s->d_bad, 0xff, sizeof(unsigned long long), g->stream));
             PD_CUDA(cudaEventCreate(&s->ev0));
@@ -620,6 +626,7 @@ int pd_stepper_destroy(pd_stepper* s) {
         pd_free(s->d_bad);
         pd_free(s->d_rows);
         pd_free(s->d_region);
+        pd_free(s->d_conv);
         pd_free(s->peer.d_ord);
         pd_free(s->peer.d_err);
         if (s->peer.d_sync) cudaFree(s->peer.d_sync);
@@ -697,7 +704,9 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
         std::vector<double> hrows((size_t)kBatch * 3);
         std::vector<int64_t> row_step((size_t)kBatch);
         std::vector<double> hregion((size_t)kBatch);
+        std::vector<unsigned long long> hconv((size_t)kBatch);
         s->region_out.clear();
+        s->conv_out.clear();
         while (j < n_steps) {
             const int64_t nb = std::min<int64_t>(kBatch, n_steps - j);
             PD_CUDA(cudaMemsetAsync(s->d_flags, 0, sizeof(int) * (size_t)nb, g->stream));
@@ -706,6 +715,8 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                 PD_CUDA(cudaMemsetAsync(s->plan.d_counter, 0,
                                         sizeof(int) * (size_t)(nb * march_counters_per_step()), g->stream));
             int64_t nr = 0;
+            if (s->has_conv)
+                PD_CUDA(cudaMemsetAsync(s->d_conv, 0, sizeof(unsigned long long) * (size_t)nb, g->stream));
             PD_CUDA(cudaEventRecord(s->ev0, g->stream));
             for (int64_t k = 0; k < nb; ++k) {
                 const int64_t st = step0 + j + k;  // global step index being taken
@@ -718,6 +729,7 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                     launch_pairwise_finalize(g, s->d_rows + 3 * nr, s->d_flags + k, s->begin,
                                              s->end - s->begin);
                     if (s->has_region) launch_box_sum(g, g->cols[(size_t)cn], s->rlo, s->rhi, s->d_region + nr);
+                    if (s->has_conv) launch_absdiff_max(g, g->cols[(size_t)cn], g->cols[(size_t)cu], s->d_conv + nr);
                     row_step[(size_t)nr] = st + 1;
                     ++nr;
                 }
@@ -732,6 +744,9 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                                         cudaMemcpyDeviceToHost, g->stream));
             if (nr > 0 && s->has_region)
                 PD_CUDA(cudaMemcpyAsync(hregion.data(), s->d_region, sizeof(double) * (size_t)nr,
+                                        cudaMemcpyDeviceToHost, g->stream));
+            if (nr > 0 && s->has_conv)
+                PD_CUDA(cudaMemcpyAsync(hconv.data(), s->d_conv, sizeof(unsigned long long) * (size_t)nr,
                                         cudaMemcpyDeviceToHost, g->stream));
             PD_CUDA(cudaStreamSynchronize(g->stream));
             float ms = 0.f;
@@ -756,6 +771,11 @@ int pd_stepper_run(pd_stepper* s, int64_t step0, int64_t n_steps, int64_t final_
                 d.min_u = hrows[(size_t)r * 3 + 1];
                 d.max_u = hrows[(size_t)r * 3 + 2];
                 if (s->has_region) s->region_out.push_back(hregion[(size_t)r]);
+                if (s->has_conv) {
+                    double v;
+                    std::memcpy(&v, &hconv[(size_t)r], sizeof v);
+                    s->conv_out.push_back(v);
+                }
             }
             if (fail_k < 0) {
                 j += nb;
@@ -1035,6 +1055,39 @@ int pd_stepper_region_sums(const pd_stepper* s, double* out, int64_t cap, int64_
     *n = (int64_t)s->region_out.size();
     for (int64_t i = 0; i < std::min<int64_t>(cap, *n); ++i) out[i] = s->region_out[(size_t)i];
     return PD_OK;
+}
+
+int pd_stepper_set_convergence(pd_stepper* s, int on) {
+    s->has_conv = on != 0;
+    return PD_OK;
+}
+
+int pd_stepper_convergence(const pd_stepper* s, double* out, int64_t cap, int64_t* n) {
+    *n = (int64_t)s->conv_out.size();
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n); ++i) out[i] = s->conv_out[(size_t)i];
+    return PD_OK;
+}
+
+int pd_stepper_plane_flux(pd_stepper* s, int axis, int64_t layer, double* face_sum, double* flux,
+                          int64_t* faces) {
+    return guarded([&] {
+        pd_grid* g = s->g;
+        if (axis < 0 || axis >= g->dims) fail(PD_E_INPUT, "flux axis out of range");
+        if (layer < 0 || layer + 1 >= g->size[axis]) fail(PD_E_INPUT, "flux plane outside the box interior");
+        DeviceGuard dg(g->device);
+        refresh_if_stale(s);
+        const void* u = g->cols[(size_t)g->column_of[(size_t)s->prop_u]];
+        const void* d = g->cols[(size_t)g->column_of[(size_t)s->prop_d]];
+        int64_t nf = 0;
+        const double sum = plane_face_sum(g, u, d, s->d_fluid, s->d_nbr, axis, layer, &nf);
+        // Fick's law across the faces: F = -sum dh (u_{L+1} - u_L) / h_axis * A_face
+        double area = 1.0;
+        for (int a = 0; a < g->dims; ++a)
+            if (a != axis) area *= g->spacing[a];
+        if (face_sum) *face_sum = sum;
+        if (flux) *flux = -sum / g->spacing[axis] * area;
+        if (faces) *faces = nf;
+    });
 }
 
 int pd_stepper_last_ms(const pd_stepper* s, double* ms) {

@@ -274,6 +274,11 @@ void count_active(pd_grid* g);
 void launch_box_sum(pd_grid* g, const void* col, const int64_t* lo, const int64_t* hi, double* dst);
 void check_box(const pd_grid* g, const int64_t* lo, const int64_t* hi);
 
+// Steady-state observers (pd_observe.cu).
+void launch_absdiff_max(pd_grid* g, const void* a, const void* b, unsigned long long* out);
+double plane_face_sum(pd_grid* g, const void* u, const void* d, const uint64_t* fluid, const int32_t* nbr,
+                      int axis, int64_t layer, int64_t* faces);
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {

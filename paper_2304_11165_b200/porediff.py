@@ -872,6 +872,26 @@ class FtcsStepper:
         lib.pd_stepper_region_sums(self.h, buf, n.value, C.byref(n))
         return list(buf[: n.value])
 
+    # -- steady-state observers (pd_observe.cu; no reference counterpart) ---
+    def set_convergence(self, on: bool = True):
+        """Every recorded row also yields max |u(step) - u(step-1)|."""
+        _check(lib.pd_stepper_set_convergence(self.h, 1 if on else 0))
+
+    def convergence_norms(self) -> List[float]:
+        n = C.c_int64()
+        lib.pd_stepper_convergence(self.h, None, 0, C.byref(n))
+        buf = (C.c_double * max(1, n.value))()
+        lib.pd_stepper_convergence(self.h, buf, n.value, C.byref(n))
+        return list(buf[: n.value])
+
+    def plane_flux(self, axis: int, layer: int) -> Tuple[float, float]:
+        """(face_sum, flux) of the current u through the plane between node
+        layers `layer` and `layer`+1 of `axis` (pd_stepper_plane_flux)."""
+        fs, fl = C.c_double(), C.c_double()
+        nf = C.c_int64()
+        _check(lib.pd_stepper_plane_flux(self.h, axis, layer, C.byref(fs), C.byref(fl), C.byref(nf)))
+        return fs.value, fl.value
+
     def last_ms(self) -> float:
         ms = C.c_double()
         lib.pd_stepper_last_ms(self.h, C.byref(ms))
