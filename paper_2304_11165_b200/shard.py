@@ -152,7 +152,10 @@ class Domain:
         # cut the z chunk layers at equal prefix sums of work (allocated chunks
         # per layer; the step costs per chunk), not at equal layer counts
         if balance is None:
-            balance = os.environ.get("PD_BALANCE", "cost") if world > 1 else "layers"
+            # "chunks" measured best at C5 (profiles/r02_slab_balance.txt: 2.3 % / 3.5 %
+            # per-shard kernel-time imbalance at 4 / 8 shards; "cost" 2.4 / 3.7 %,
+            # even layers 8.2 / 13.4 %)
+            balance = os.environ.get("PD_BALANCE", "chunks") if world > 1 else "layers"
         weights = None
         if balance in ("chunks", "active", "cost"):
             ch, ac, fu = layer_work(self.geom, pack, dtype, device)
@@ -456,7 +459,7 @@ UNIFORM_COST = 2.0 / 3.0
 
 
 def layer_cost(chunks: np.ndarray, full: np.ndarray) -> np.ndarray:
-    """Per-layer step cost for the slab cuts (PD_BALANCE=cost, the default)."""
+    """Per-layer step cost model for the slab cuts (PD_BALANCE=cost)."""
     return (chunks - full) + UNIFORM_COST * full
 
 

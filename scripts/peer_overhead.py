@@ -11,7 +11,7 @@ Slab balance: before the exchange is wired up, every shard is stepped alone
 (pd_stepper_run over its owned range) and the per-shard kernel times give
 the load imbalance max/mean - 1 of the cuts (--balance layers | chunks |
 cost, the per-layer cost model of shard.layer_cost; --balance all measures
-the three and runs the exchange with "cost").
+the three and runs the exchange with "cost"; the bench default is "chunks").
 
     python scripts/peer_overhead.py [--n 1024] [--world 2] [--steps 20] [--balance cost]
 """
