@@ -571,6 +571,7 @@ int pd_stepper_create(pd_grid* g, const pd_sim_config* cfg, int prop_phi, int pr
         auto* s = new pd_stepper();
         try {
             s->g = g;
+            ++g->refs;
             s->cfg = *cfg;
             s->prop_phi = prop_phi;
             s->prop_u = prop_u;
@@ -634,6 +635,7 @@ int pd_stepper_destroy(pd_stepper* s) {
         if (s->ev0) cudaEventDestroy(s->ev0);
         if (s->ev1) cudaEventDestroy(s->ev1);
     }
+    grid_release(s->g);
     delete s;
     return PD_OK;
 }

@@ -673,6 +673,12 @@ int pd_grid_create(int dims, int scalar_bytes, const int64_t* size, const double
 
 int pd_grid_destroy(pd_grid* g) {
     if (!g) return PD_OK;
+    grid_release(g);
+    return PD_OK;
+}
+
+extern "C++" void grid_release(pd_grid* g) {
+    if (--g->refs > 0) return;
     {
         DeviceGuard dg(g->device);
         if (g->stream) cudaStreamSynchronize(g->stream);
@@ -695,7 +701,6 @@ int pd_grid_destroy(pd_grid* g) {
         if (g->own_stream) cudaStreamDestroy(g->own_stream);
     }
     delete g;
-    return PD_OK;
 }
 
 int pd_grid_upload(pd_grid* g, int prop, const void* host_slabs) {

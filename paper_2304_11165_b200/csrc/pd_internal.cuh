@@ -120,7 +120,14 @@ struct pd_grid {
     double* d_row = nullptr;  // 3 doubles: mass, min, max
     uint64_t generation = 0;  // bumped by every host-visible write to a column
     std::vector<uint64_t> prop_ver;  // per logical property: bumped by each write to it
+    // owners: the handle returned to the caller plus one per live stepper, so
+    // a stepper destroyed after its grid's handle (any finaliser order) still
+    // finds the grid; the storage is released when the last owner goes
+    int refs = 1;
 };
+
+// Drops one owner of g; frees it when none is left (pd_grid.cu).
+void grid_release(pd_grid* g);
 
 // Records a write to logical property `prop` (all properties if prop < 0):
 // steppers compare the versions of phi and D before stepping and rebuild

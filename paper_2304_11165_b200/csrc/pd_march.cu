@@ -1500,6 +1500,410 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
     if (PUSH && pushed) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------------
+// v31: v30's CTA-staged chunk pipeline with a lean compute side.
+// * The producer is a whole warp: lane 0 claims chunks and issues the bulk /
+//   TMA copies (as v30); all 32 lanes copy the x-halo cells (8-B cp.async)
+//   and arrive on the stage's "full" mbarrier when those land
+//   (cp.async.mbarrier.arrive.noinc), so the compute warps issue no copies.
+// * Compute warp w owns planes 2w, 2w+1 of the staged chunk; lane (y, xp)
+//   the pairs (2xp, 2xp+1) of row y. Its eleven operand offsets inside a
+//   stage are lane constants pinned in registers (no per-chunk address
+//   arithmetic beyond stage base + offset).
+// * Both planes are computed in one straight-line block (the face between
+//   them once), on one of three warp-uniform paths: uniform chunk (no D_eff
+//   staged), both planes interior-fluid (select-free faces), generic
+//   (sentinel faces, walls). The huge / non-finite test is folded into one
+//   max of high words per lane and one warp vote; the exact rare path
+//   re-reads everything from the stage.
+// * Per-node arithmetic, expression order and stores: as v14 / v30, so the
+//   results are bitwise identical.
+// ---------------------------------------------------------------------------
+constexpr int kW31 = 4;                       // compute warps per CTA
+constexpr int kThreads31 = 32 * (kW31 + 1);   // + the producer warp
+constexpr int kCtas31 = 4;
+__host__ __device__ constexpr int nst31(int cfg) { return cfg == 1 ? 5 : 3; }
+__host__ __device__ constexpr int ctas31(int cfg) { return cfg == 1 ? 3 : kCtas31; }
+__host__ __device__ constexpr int batch31(int cfg) { return cfg == 2 ? 8 : 4; }  // chunks claimed per atomic
+
+__device__ __forceinline__ void cp_mbar_arrive_noinc(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void cp8(uint32_t dst, const void* src, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(dst),
+        "l"(src), "r"((int)pred)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t pin(uint32_t v, int lane) { return __shfl_sync(0xffffffffu, v, lane); }
+
+// Rare path of one plane pair: everything (chunk record, operands) re-read
+// from the stage at st.
+template <int REACTION, bool HALF>
+__device__ __noinline__ double2 pair_slow31(const MarchArgs& M, const SlowConsts& K, uint32_t st, int lane, int z,
+                                            double out0, double out1) {
+    ChunkCtx14 C;
+    C.c = (int)lds_u32(st + kCtx30 + 176u);
+    C.lm = lds_u32(st + kCtx30 + 4u * (uint32_t)lane);
+    C.key = (int)lds_u32(st + kCtx30 + 152u);
+    C.flags = (int)lds_u32(st + kCtx30 + 156u);
+    C.dv = lds1(st + kCtx30 + 160u);
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp), oc = bp * 8u, zz = (uint32_t)z;
+    Addr30 a;
+    a.c = st + kOwn30 + oc + zz * 512u;
+    a.zm = z == 0 ? st + kZL30 + oc : a.c - 512u;
+    a.zp = z == 7 ? st + kZH30 + oc : a.c + 512u;
+    a.ym = y > 0 ? a.c - 64u : st + kYL30 + zz * 64u + 16u * (uint32_t)xp;
+    a.yp = y < 7 ? a.c + 64u : st + kYH30 + zz * 64u + 16u * (uint32_t)xp;
+    a.l = xp > 0 ? a.c - 8u : st + kXL30 + zz * 64u + 8u * (uint32_t)y;
+    a.r = xp < 3 ? a.c + 16u : st + kXH30 + zz * 64u + 8u * (uint32_t)y;
+    return pair_slow30<REACTION, HALF>(M, K, C, z, xp, y, bp, a, out0, out1);
+}
+
+// lap and explicit Euler update of one node, the reference's order
+// (solver.hpp:420-441): lap = 0 + dx term + dy term + dz term;
+// u + dt * lap + dt * r
+template <int REACTION>
+__device__ __forceinline__ double node31(const Consts& Q, double uc, double fxm, double fxp, double fym, double fyp,
+                                         double fzm, double fzp, bool sink, double src) {
+    double lap = 0.0;
+    lap += (fxp - fxm) * Q.ix;
+    lap += (fyp - fym) * Q.iy;
+    lap += (fzp - fzm) * Q.iz;
+    double r = 0.0;
+    if (REACTION == PD_REACTION_SURFACE_SINK) r = sink ? Q.neg_k * uc : 0.0;
+    else if (REACTION == PD_REACTION_VOLUMETRIC) r = src * Q.src_factor;
+    return uc + Q.dt * lap + Q.dt * r;
+}
+
+template <int REACTION, bool PUSH, bool HALF, int CFG>
+__global__ void __launch_bounds__(kThreads31, ctas31(CFG))
+    ftcs_march31_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
+                        const __grid_constant__ CUtensorMap muy, const __grid_constant__ CUtensorMap mdy) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    constexpr int kSt = nst31(CFG);
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = sm0 + bar30(kSt), empty0 = full0 + 8u * kSt;
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+        K.huge_hi = A.huge_hi;
+        for (int s = 0; s < kSt; ++s) {
+            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 x-halo arrivals
+            mbar_init(empty0 + 8u * s, (uint32_t)kW31);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    const int n = (int)M.n;
+
+    if (warp == kW31) {  // ---------------- producer warp ----------------
+        constexpr int kB31 = batch31(CFG);
+        // Chunks are claimed kB31 schedule positions per atomic; lane j < kB31
+        // holds chunk j of a batch (flagged schedule entry, descriptor). The
+        // chain claim -> entries -> descriptors runs one batch per stage: the
+        // claim of batch b+3, the entries of b+2, the descriptors and the L2
+        // prefetch of b+1 are issued while batch b is copied, so no
+        // long-latency result is consumed in the batch it was requested in.
+        int* ctr = M.counter;
+        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
+        const int sent_c = (int)M.n_all;  // D_eff sentinel chunk
+        const uint32_t sent_off = (uint32_t)M.n_all * 512u;
+        auto claim = [&]() -> int {  // lane 0 holds the result
+            int r = 0;
+            if (lane == 0)
+                asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(ctr), "r"(kB31) : "memory");
+            return r;
+        };
+        auto entries = [&](int p0) -> int {  // lane j < kB31: entry of position p0 + j
+            const int p = __shfl_sync(0xffffffffu, p0, 0) + lane;
+            return lane < kB31 && p < n ? __ldg(&M.sched[p]) : -1;
+        };
+        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
+        auto descs = [&](int e, int4& d0, int4& d1) {
+            const int c = chunk_of(e);
+            if (lane < kB31 && c >= 0) {
+                d0 = __ldg(desc4 + 2 * (int64_t)c);
+                d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
+            }
+        };
+        auto prefetch = [&](int e) {  // the batch's slabs into L2 (u, record, and D_eff unless uniform)
+            const int64_t c = (int64_t)chunk_of(e);
+            if (lane < kB31 && c >= 0) {
+                prefetch_l2(u + c * 512, 4096u);
+                prefetch_l2(ctxa + c * kCtxWords30, 176u);
+                if (e >= 0) prefetch_l2(de + c * 512, 4096u);
+            }
+        };
+        int e_c = entries(claim());
+        int e_n = entries(claim());
+        int p_nn = claim();
+        int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
+        descs(e_c, d0c, d1c);
+        prefetch(e_c);
+        const uint32_t xo0 = (uint32_t)lane * 8u;  // this lane's x-halo cells: (z, y) = lane + 32 j
+        uint32_t s = 0, ph = 0, k = 0;
+#pragma unroll 1
+        for (;;) {
+            int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
+            descs(e_n, d0n, d1n);
+            prefetch(e_n);
+            const int e_nn = entries(p_nn);
+            p_nn = claim();
+            bool done = false;
+#pragma unroll 1
+            for (int j = 0; j < kB31; ++j, ++k) {
+                const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
+                const uint32_t st = sm0 + s * kStage30, full = full0 + 8u * s;
+                if (k >= (uint32_t)kSt) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+                if (c_cur < 0) {  // end marker: the compute warps stop at this stage
+                    if (lane == 0) {
+                        sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
+                        mbar_arrive(full);
+                    }
+                    cp_mbar_arrive_noinc(full);
+                    done = true;
+                    break;
+                }
+                const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
+                const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
+                const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
+                const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
+                if (lane == 0) {
+                    sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
+                    uint32_t bytes = 176u + 4096u;
+                    bytes += (nb2 >= 0 ? 512u : 0u) + (nb3 >= 0 ? 512u : 0u) + (nb4 >= 0 ? 512u : 0u) +
+                             (nb5 >= 0 ? 512u : 0u);
+                    if (dl) bytes += 4096u + 4u * 512u;
+                    mbar_arrive_tx(full, bytes);
+                    const int64_t cb = (int64_t)c_cur * 512;
+                    bulk_g2s(st + kCtx30, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
+                    bulk_g2s(st + kOwn30, u + cb, 4096u, full);
+                    if (nb2 >= 0) tma4(st + kYL30, &muy, 0, 7, 0, nb2, full);
+                    if (nb3 >= 0) tma4(st + kYH30, &muy, 0, 0, 0, nb3, full);
+                    if (nb4 >= 0) bulk_g2s(st + kZL30, u + (int64_t)nb4 * 512 + 448, 512u, full);
+                    if (nb5 >= 0) bulk_g2s(st + kZH30, u + (int64_t)nb5 * 512, 512u, full);
+                    if (dl) {
+                        const uint32_t sd = st + kDHalf30;
+                        bulk_g2s(sd + kOwn30, de + cb, 4096u, full);
+                        tma4(sd + kYL30, &mdy, 0, 7, 0, nb2 >= 0 ? nb2 : sent_c, full);
+                        tma4(sd + kYH30, &mdy, 0, 0, 0, nb3 >= 0 ? nb3 : sent_c, full);
+                        bulk_g2s(sd + kZL30, de + (nb4 >= 0 ? (int64_t)nb4 * 512 + 448 : (int64_t)sent_c * 512),
+                                 512u, full);
+                        bulk_g2s(sd + kZH30, de + (nb5 >= 0 ? (int64_t)nb5 * 512 : (int64_t)sent_c * 512), 512u,
+                                 full);
+                    }
+                }
+                {  // x halos: column 7 of the x- neighbour, column 0 of the x+ neighbour
+                    // (u only where the neighbour exists; D_eff from the sentinel chunk otherwise)
+                    const uint32_t gl = (uint32_t)nb0 * 512u + (uint32_t)lane * 8u + 7u;
+                    const uint32_t gh = (uint32_t)nb1 * 512u + (uint32_t)lane * 8u;
+                    const uint32_t gs = sent_off + (uint32_t)lane * 8u;
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {  // cells (z, y) = lane + 32 jj of each side
+                        const uint32_t dL = st + kXL30 + xo0 + (uint32_t)jj * 256u;
+                        const uint32_t dH = st + kXH30 + xo0 + (uint32_t)jj * 256u;
+                        const uint32_t oL = gl + (uint32_t)jj * 256u, oH = gh + (uint32_t)jj * 256u;
+                        cp8(dL, u + (nb0 >= 0 ? oL : 0u), nb0 >= 0);
+                        cp8(dH, u + (nb1 >= 0 ? oH : 0u), nb1 >= 0);
+                        cp8(dL + kDHalf30, de + (nb0 >= 0 ? oL : gs + (uint32_t)jj * 256u), dl);
+                        cp8(dH + kDHalf30, de + (nb1 >= 0 ? oH : gs + (uint32_t)jj * 256u), dl);
+                    }
+                    cp_mbar_arrive_noinc(full);
+                }
+                if (++s == (uint32_t)kSt) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+            if (done) break;
+            e_c = e_n;
+            d0c = d0n;
+            d1c = d1n;
+            e_n = e_nn;
+        }
+        return;
+    }
+
+    // ---------------- compute warps ----------------
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t z0 = 2u * (uint32_t)warp;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);  // own pair offset in a plane (elements)
+    const uint32_t oc = bp * 8u;
+    // operand offsets inside a stage (u side; D_eff at +kDHalf30), pinned
+    const uint32_t o_c = pin(kOwn30 + oc + z0 * 512u, lane);
+    const uint32_t o_zm = pin(warp == 0 ? kZL30 + oc : kOwn30 + oc + z0 * 512u - 512u, lane);
+    const uint32_t o_zp = pin(warp == kW31 - 1 ? kZH30 + oc : kOwn30 + oc + z0 * 512u + 1024u, lane);
+    const uint32_t s_ym = y > 0 ? 512u : 64u, s_yp = y < 7 ? 512u : 64u;
+    const uint32_t s_l = xp > 0 ? 512u : 64u, s_r = xp < 3 ? 512u : 64u;
+    const uint32_t b_ym = y > 0 ? kOwn30 + oc - 64u + z0 * 512u : kYL30 + 16u * (uint32_t)xp + z0 * 64u;
+    const uint32_t b_yp = y < 7 ? kOwn30 + oc + 64u + z0 * 512u : kYH30 + 16u * (uint32_t)xp + z0 * 64u;
+    const uint32_t b_l = xp > 0 ? kOwn30 + oc - 8u + z0 * 512u : kXL30 + 8u * (uint32_t)y + z0 * 64u;
+    const uint32_t b_r = xp < 3 ? kOwn30 + oc + 16u + z0 * 512u : kXH30 + 8u * (uint32_t)y + z0 * 64u;
+    const uint32_t o_ym0 = pin(b_ym, lane), o_ym1 = pin(b_ym + s_ym, lane);
+    const uint32_t o_yp0 = pin(b_yp, lane), o_yp1 = pin(b_yp + s_yp, lane);
+    const uint32_t o_l0 = pin(b_l, lane), o_l1 = pin(b_l + s_l, lane);
+    const uint32_t o_r0 = pin(b_r, lane), o_r1 = pin(b_r + s_r, lane);
+    const uint32_t o_lm = pin(kCtx30 + 4u * (uint32_t)lane, lane);
+    const uint32_t g_off = pin(z0 * 64u + bp, lane);  // element offset of the lane's plane-z0 pair in a chunk
+    const uint32_t zsh = 2u * z0;                      // lm bit of plane z0
+    double* __restrict__ un = A.un;
+    const uint32_t huge_hi = A.huge_hi;
+    bool pushed = false;
+    uint32_t s = 0, ph = 0;
+#pragma unroll 1
+    for (;;) {
+        mbar_wait(full0 + 8u * s, ph);
+        const uint32_t st = sm0 + s * kStage30;
+        const int c = (int)lds_u32(st + kCtx30 + 176u);
+        if (c < 0) break;
+        const uint32_t lm = lds_u32(st + o_lm);
+        const int flags = (int)lds_u32(st + kCtx30 + 156u);
+        const uint32_t ab = (lm >> zsh) & 0xFu;  // active bits: plane z0 (x0, x1), plane z1 (x0, x1)
+        const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
+        double src[4] = {0.0, 0.0, 0.0, 0.0};
+        if (REACTION == PD_REACTION_VOLUMETRIC) {
+            const double* sp = A.src + (int64_t)c * 512 + g_off;
+            src[0] = sp[0];
+            src[1] = sp[1];
+            src[2] = sp[64];
+            src[3] = sp[65];
+        }
+        // u operands (both planes)
+        const double2 uc0 = lds2(st + o_c), uc1 = lds2(st + o_c + 512u);
+        const double2 uzm = lds2(st + o_zm), uzp = lds2(st + o_zp);
+        const double uL0 = lds1(st + o_l0), uR0 = lds1(st + o_r0), uL1 = lds1(st + o_l1), uR1 = lds1(st + o_r1);
+        const double2 uym0 = lds2(st + o_ym0), uyp0 = lds2(st + o_yp0);
+        const double2 uym1 = lds2(st + o_ym1), uyp1 = lds2(st + o_yp1);
+        double o00, o01, o10, o11;  // plane z0 (x0, x1), plane z1 (x0, x1)
+        const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
+        if (flags & kFlagUnif) {
+            const double dv = lds1(st + kCtx30 + 160u);
+            const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
+            const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);  // face z0 | z1
+            const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
+            o00 = node31<REACTION>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
+                                   dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
+            o01 = node31<REACTION>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
+                                   dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
+            o10 = node31<REACTION>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
+                                   fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
+            o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
+                                   fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
+        } else {
+            const uint32_t dh_ = kDHalf30;
+            const double2 dc0 = lds2(st + o_c + dh_), dc1 = lds2(st + o_c + 512u + dh_);
+            const double2 dzm = lds2(st + o_zm + dh_), dzp = lds2(st + o_zp + dh_);
+            const double dL0 = lds1(st + o_l0 + dh_), dR0 = lds1(st + o_r0 + dh_);
+            const double dL1 = lds1(st + o_l1 + dh_), dR1 = lds1(st + o_r1 + dh_);
+            const double2 dym0 = lds2(st + o_ym0 + dh_), dyp0 = lds2(st + o_yp0 + dh_);
+            const double2 dym1 = lds2(st + o_ym1 + dh_), dyp1 = lds2(st + o_yp1 + dh_);
+            if (ib == 3u) {  // both planes interior-fluid: no sentinel faces, no walls
+                const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
+                const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
+                o00 = node31<REACTION>(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                                       fface<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), fface<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
+                                       fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
+                o01 = node31<REACTION>(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       fface<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), fface<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
+                                       fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
+                o10 = node31<REACTION>(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       fface<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), fface<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
+                                       fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
+                o11 = node31<REACTION>(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       fface<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), fface<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
+                                       fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+            } else {  // generic: faces with a sentinel side contribute 0; walls stay frozen
+                const double fzx = face<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = face<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
+                const double f0i = face<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = face<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
+                o00 = node31<REACTION>(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                                       face<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), face<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
+                                       face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
+                o01 = node31<REACTION>(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       face<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), face<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
+                                       face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
+                o10 = node31<REACTION>(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       face<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), face<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
+                                       fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
+                o11 = node31<REACTION>(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       face<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), face<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
+                                       fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+                if (sentinel(dc0.x)) o00 = uc0.x;  // walls (solver.hpp:413-417)
+                if (sentinel(dc0.y)) o01 = uc0.y;
+                if (sentinel(dc1.x)) o10 = uc1.x;
+                if (sentinel(dc1.y)) o11 = uc1.y;
+            }
+        }
+        // rare path: Dirichlet-exposed chunk, or a huge / non-finite result
+        // (inactive slots keep u there: a huge one only costs the re-check)
+        const uint32_t hm = max(max((uint32_t)__double2hiint(o00) & 0x7fffffffu, (uint32_t)__double2hiint(o01) & 0x7fffffffu),
+                                max((uint32_t)__double2hiint(o10) & 0x7fffffffu, (uint32_t)__double2hiint(o11) & 0x7fffffffu));
+        const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
+        if (__any_sync(0xffffffffu, slow)) {
+            if (slow) {
+                const double2 r0 = pair_slow31<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
+                const double2 r1 = pair_slow31<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
+                o00 = r0.x;
+                o01 = r0.y;
+                o10 = r1.x;
+                o11 = r1.y;
+            }
+        }
+        double* gp = un + ((uint32_t)c * 512u + g_off);
+        stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
+        stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
+        if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (z0 == 0 || z0 == 6)) {
+            ChunkCtx14 C;
+            C.c = c;
+            C.key = (int)lds_u32(st + kCtx30 + 152u);
+            C.flags = flags;
+            C.lm = lm;
+            C.dv = 0.0;
+            if (z0 == 0) push_pair14(M, C, 0, bp, o00, o01, ab & 1u, ab & 2u);
+            else push_pair14(M, C, 7, bp, o10, o11, ab & 4u, ab & 8u);
+            pushed = true;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8u * s);
+        if (++s == (uint32_t)kSt) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+    // the pushed planes are visible system-wide before this kernel completes
+    // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
+    if (PUSH && pushed) __threadfence_system();
+}
+
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 // desc flags of the fused halo push: bit set iff the chunk has a peer ghost
@@ -1933,6 +2337,49 @@ void march30_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     PD_CUDA(cudaGetLastError());
 }
 
+void march31_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
+    if (!p.d_ctx) fail(PD_E_INPUT, "march v31 needs the packed chunk records (3-D FP64 plan)");
+    M.sched = flagged_schedule(g, p, M.sched, M.n);
+    static const cuuint32_t by[4] = {8, 1, 8, 1};
+    const CUtensorMap muy = column_map(M.A.u, g->n_chunks, by);
+    const CUtensorMap mdy = column_map(M.deff, g->n_chunks + 1, by);
+    using K31 = void (*)(const MarchArgs, const uint32_t*, const CUtensorMap, const CUtensorMap);
+#define PD_M_TABLE(N)                                                                                         \
+    {{{ftcs_march31_kernel<0, false, false, N>, ftcs_march31_kernel<1, false, false, N>,                       \
+       ftcs_march31_kernel<2, false, false, N>},                                                               \
+      {ftcs_march31_kernel<0, true, false, N>, ftcs_march31_kernel<1, true, false, N>,                         \
+       ftcs_march31_kernel<2, true, false, N>}},                                                               \
+     {{ftcs_march31_kernel<0, false, true, N>, ftcs_march31_kernel<1, false, true, N>,                         \
+       ftcs_march31_kernel<2, false, true, N>},                                                                \
+      {ftcs_march31_kernel<0, true, true, N>, ftcs_march31_kernel<1, true, true, N>,                           \
+       ftcs_march31_kernel<2, true, true, N>}}}
+    static const K31 tabs[3][2][2][3] = {PD_M_TABLE(0), PD_M_TABLE(1), PD_M_TABLE(2)};
+#undef PD_M_TABLE
+    static const int cfg = [] {
+        const char* e = getenv("PD_M31_CFG");
+        const int v = e ? atoi(e) : 0;
+        return v >= 0 && v <= 2 ? v : 0;
+    }();
+    const K31(*tab)[2][3] = tabs[cfg];
+    const int nst = cfg == 1 ? nst31(1) : cfg == 2 ? nst31(2) : nst31(0);
+    const int ctas = cfg == 1 ? ctas31(1) : cfg == 2 ? ctas31(2) : ctas31(0);
+    const uint32_t smem = smem30(nst);
+    static uint64_t attr_done[3] = {0, 0, 0};
+    const int dev = g->device;
+    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
+    if (!((attr_done[cfg] >> dev) & 1u)) {
+        for (int h = 0; h < 2; ++h)
+            for (int q = 0; q < 2; ++q)
+                for (int rr = 0; rr < 3; ++rr)
+                    PD_CUDA(cudaFuncSetAttribute(tab[h][q][rr], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done[cfg] |= 1ull << dev;
+    }
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * ctas, kThreads31, smem, g->stream>>>(M, p.d_ctx, muy, mdy);
+    PD_CUDA(cudaGetLastError());
+}
+
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
                         int64_t n, int* counter, const PeerLaunch* pl) {
     MarchArgs M;
@@ -1970,6 +2417,10 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
 #undef PD_M_TABLE
     if (ver == 30) {
         march30_launch(g, p, M, r, pl != nullptr);
+        return;
+    }
+    if (ver == 31) {
+        march31_launch(g, p, M, r, pl != nullptr);
         return;
     }
     static const int pf = [] {

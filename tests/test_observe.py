@@ -131,7 +131,11 @@ def test_convergence_norm_and_plane_flux_bitwise(cuda):
             fs, fl = st.plane_flux(axis, layer)
             want = np_plane_face_sum(keys, fluid, u, d, geom.size, axis, layer)
             assert fs == want, (axis, layer, fs, want)
-            assert fl == -want / geom.spacing[axis] * geom.spacing[(axis + 1) % 3] * geom.spacing[(axis + 2) % 3]
+            area = 1.0  # face area, other axes in ascending order (pd_stepper_plane_flux)
+            for a in range(3):
+                if a != axis:
+                    area *= geom.spacing[a]
+            assert fl == -want / geom.spacing[axis] * area
     with pytest.raises(pd.InputError):
         st.plane_flux(0, n - 1)
     st.close()
