@@ -47,6 +47,7 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -1110,18 +1111,18 @@ struct Addr30 {
 
 // Rare path: operands re-read from the stage, exact generic update and the
 // error / mass flags (solver.hpp:360-455, 250-260, 514-515).
-template <int REACTION, bool HALF>
+template <int REACTION, bool HALF, uint32_t DH = kDHalf30>
 __device__ __noinline__ double2 pair_slow30(const MarchArgs& M, const SlowConsts& K, const ChunkCtx14& C, int z,
                                             int xp, int y, uint32_t bp, Addr30 a, double out0, double out1) {
     const bool un = (C.flags & kFlagUnif) != 0;  // no D_eff in the stage: every d is dv
     const double2 vv = make_double2(C.dv, C.dv);
-    const double2 uc = lds2(a.c), dc0 = un ? vv : lds2(a.c + kDHalf30);
-    const double uL = lds1(a.l), dL0 = un ? C.dv : lds1(a.l + kDHalf30);
-    const double uR = lds1(a.r), dR0 = un ? C.dv : lds1(a.r + kDHalf30);
-    const double2 uym = lds2(a.ym), dym0 = un ? vv : lds2(a.ym + kDHalf30);
-    const double2 uyp = lds2(a.yp), dyp0 = un ? vv : lds2(a.yp + kDHalf30);
-    const double2 uzm = lds2(a.zm), dzm0 = un ? vv : lds2(a.zm + kDHalf30);
-    const double2 uzp = lds2(a.zp), dzp0 = un ? vv : lds2(a.zp + kDHalf30);
+    const double2 uc = lds2(a.c), dc0 = un ? vv : lds2(a.c + DH);
+    const double uL = lds1(a.l), dL0 = un ? C.dv : lds1(a.l + DH);
+    const double uR = lds1(a.r), dR0 = un ? C.dv : lds1(a.r + DH);
+    const double2 uym = lds2(a.ym), dym0 = un ? vv : lds2(a.ym + DH);
+    const double2 uyp = lds2(a.yp), dyp0 = un ? vv : lds2(a.yp + DH);
+    const double2 uzm = lds2(a.zm), dzm0 = un ? vv : lds2(a.zm + DH);
+    const double2 uzp = lds2(a.zp), dzp0 = un ? vv : lds2(a.zp + DH);
     auto dd = [](double h) { return HALF ? h + h : h; };
     auto dd2 = [&](double2 h) { return make_double2(dd(h.x), dd(h.y)); };
     const double2 dc = dd2(dc0), dym = dd2(dym0), dyp = dd2(dyp0), dzm = dd2(dzm0), dzp = dd2(dzp0);
@@ -1519,12 +1520,28 @@ __global__ void __launch_bounds__(threads30(CFG), ctas30(CFG))
 // * Per-node arithmetic, expression order and stores: as v14 / v30, so the
 //   results are bitwise identical.
 // ---------------------------------------------------------------------------
-constexpr int kW31 = 4;                       // compute warps per CTA
-constexpr int kThreads31 = 32 * (kW31 + 1);   // + the producer warp
-constexpr int kCtas31 = 4;
-__host__ __device__ constexpr int nst31(int cfg) { return cfg == 1 ? 5 : 3; }
-__host__ __device__ constexpr int ctas31(int cfg) { return cfg == 1 ? 3 : kCtas31; }
-__host__ __device__ constexpr int batch31(int cfg) { return cfg == 2 ? 8 : 4; }  // chunks claimed per atomic
+// configurations (template CFG): compute groups of 4 warps per CTA (a group
+// works on one staged chunk; groups take stages round-robin), stages per CTA,
+// CTAs per SM, and how the halos travel (TMA / bulk copies issued by lane 0,
+// or per-lane cp.async by the whole producer warp)
+//   0: 1 group,  3 stages, 4 CTAs, bulk/TMA halos   (16 compute warps / SM, 12 stages)
+//   1: 1 group,  4 stages, 3 CTAs, bulk/TMA halos   (12, 12; 128 registers)
+//   2: 1 group,  3 stages, 4 CTAs, per-lane halos
+//   3: as 0, the lane's stage offsets re-read from a shared-memory table each
+//      chunk instead of held (pinned) in registers
+constexpr int kW31 = 4;  // compute warps per group (planes 2w, 2w+1 of the group's chunk)
+__host__ __device__ constexpr int grp31(int cfg) { return 1; }
+__host__ __device__ constexpr int nst31(int cfg) { return cfg == 1 ? 4 : 3; }
+__host__ __device__ constexpr int ctas31(int cfg) { return cfg == 1 ? 3 : 4; }
+__host__ __device__ constexpr bool lanehalo31(int cfg) { return cfg == 2; }
+__host__ __device__ constexpr bool tab31(int cfg) { return cfg == 3; }
+__host__ __device__ constexpr int threads31(int cfg) { return 32 * (kW31 * grp31(cfg) + 1); }  // + the producer warp
+// register cap: an SM sub-partition holds 16 K registers for its warps (the
+// CTAs' warps spread round-robin over the 4 sub-partitions); multiples of 8
+__host__ __device__ constexpr int maxreg31(int cfg) {
+    return 16384 / (32 * ((threads31(cfg) / 32 * ctas31(cfg) + 3) / 4)) / 8 * 8;
+}
+constexpr int kB31 = 4;  // chunks claimed per atomic (producer batch)
 
 __device__ __forceinline__ void cp_mbar_arrive_noinc(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
@@ -1535,6 +1552,21 @@ __device__ __forceinline__ void cp8(uint32_t dst, const void* src, bool pred) {
         " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(dst),
         "l"(src), "r"((int)pred)
         : "memory");
+}
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+        " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(dst),
+        "l"(src), "r"((int)pred)
+        : "memory");
+}
+__device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
 }
 __device__ __forceinline__ uint32_t pin(uint32_t v, int lane) { return __shfl_sync(0xffffffffu, v, lane); }
 
@@ -1579,12 +1611,12 @@ __device__ __forceinline__ double node31(const Consts& Q, double uc, double fxm,
 }
 
 template <int REACTION, bool PUSH, bool HALF, int CFG>
-__global__ void __launch_bounds__(kThreads31, ctas31(CFG))
+__global__ void __maxnreg__(maxreg31(CFG))
     ftcs_march31_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
                         const __grid_constant__ CUtensorMap muy, const __grid_constant__ CUtensorMap mdy) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ SlowConsts K;
-    constexpr int kSt = nst31(CFG);
+    constexpr int kSt = nst31(CFG), kG = grp31(CFG);
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
     const StepArgs<double>& A = M.A;
@@ -1619,8 +1651,7 @@ __global__ void __launch_bounds__(kThreads31, ctas31(CFG))
     const double* __restrict__ de = M.deff;
     const int n = (int)M.n;
 
-    if (warp == kW31) {  // ---------------- producer warp ----------------
-        constexpr int kB31 = batch31(CFG);
+    if (warp == kW31 * kG) {  // ---------------- producer warp ----------------
         // Chunks are claimed kB31 schedule positions per atomic; lane j < kB31
         // holds chunk j of a batch (flagged schedule entry, descriptor). The
         // chain claim -> entries -> descriptors runs one batch per stage: the
@@ -1678,12 +1709,23 @@ __global__ void __launch_bounds__(kThreads31, ctas31(CFG))
                 const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
                 const uint32_t st = sm0 + s * kStage30, full = full0 + 8u * s;
                 if (k >= (uint32_t)kSt) mbar_wait(empty0 + 8u * s, ph ^ 1u);
-                if (c_cur < 0) {  // end marker: the compute warps stop at this stage
-                    if (lane == 0) {
-                        sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
-                        mbar_arrive(full);
+                if (c_cur < 0) {  // end markers: one per group, in its next stage
+#pragma unroll 1
+                    for (int m = 0; m < kG; ++m) {
+                        if (m > 0) {
+                            if (++s == (uint32_t)kSt) {
+                                s = 0;
+                                ph ^= 1u;
+                            }
+                            if (k + m >= (uint32_t)kSt) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+                        }
+                        const uint32_t stm = sm0 + s * kStage30, fm = full0 + 8u * s;
+                        if (lane == 0) {
+                            sts_u32(stm + kCtx30 + 176u, 0xFFFFFFFFu);
+                            mbar_arrive(fm);
+                        }
+                        cp_mbar_arrive_noinc(fm);
                     }
-                    cp_mbar_arrive_noinc(full);
                     done = true;
                     break;
                 }
@@ -1691,7 +1733,25 @@ __global__ void __launch_bounds__(kThreads31, ctas31(CFG))
                 const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
                 const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
                 const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
-                if (lane == 0) {
+                if (M.dbg & 48) {  // measurement only: no copies (16) / own slabs only (32)
+                    if (lane == 0) {
+                        sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
+                        if (M.dbg & 16) {
+                            mbar_arrive(full);
+                        } else {
+                            mbar_arrive_tx(full, dl ? 8192u : 4096u);
+                            bulk_g2s(st + kOwn30, u + (int64_t)c_cur * 512, 4096u, full);
+                            if (dl) bulk_g2s(st + kDHalf30 + kOwn30, de + (int64_t)c_cur * 512, 4096u, full);
+                        }
+                    }
+                    cp_mbar_arrive_noinc(full);
+                    if (++s == (uint32_t)kSt) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                    continue;
+                }
+                if (!lanehalo31(CFG) && lane == 0) {
                     sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
                     uint32_t bytes = 176u + 4096u;
                     bytes += (nb2 >= 0 ? 512u : 0u) + (nb3 >= 0 ? 512u : 0u) + (nb4 >= 0 ? 512u : 0u) +
@@ -1715,6 +1775,33 @@ __global__ void __launch_bounds__(kThreads31, ctas31(CFG))
                         bulk_g2s(sd + kZH30, de + (nb5 >= 0 ? (int64_t)nb5 * 512 : (int64_t)sent_c * 512), 512u,
                                  full);
                     }
+                }
+                if (lanehalo31(CFG)) {
+                    // lane 0: the two own slabs (4 KB bulk copies); every lane:
+                    // its 16-B pieces of the chunk record and of the y / z halos
+                    if (lane == 0) {
+                        sts_u32(st + kCtx30 + 176u, (uint32_t)c_cur);
+                        mbar_arrive_tx(full, dl ? 8192u : 4096u);
+                        const int64_t cb = (int64_t)c_cur * 512;
+                        bulk_g2s(st + kOwn30, u + cb, 4096u, full);
+                        if (dl) bulk_g2s(st + kDHalf30 + kOwn30, de + cb, 4096u, full);
+                    }
+                    if (lane < 11) cp16(st + kCtx30 + 16u * (uint32_t)lane, ctxa + (int64_t)c_cur * kCtxWords30 + 4 * lane, true);
+                    const uint32_t l16 = 16u * (uint32_t)lane, l2 = 2u * (uint32_t)lane;
+                    // z halos: plane 7 of the z- neighbour, plane 0 of the z+ neighbour (16 B per lane)
+                    const uint32_t zl = (uint32_t)nb4 * 512u + 448u + l2, zh = (uint32_t)nb5 * 512u + l2;
+                    cp16(st + kZL30 + l16, u + (nb4 >= 0 ? zl : 0u), nb4 >= 0);
+                    cp16(st + kZH30 + l16, u + (nb5 >= 0 ? zh : 0u), nb5 >= 0);
+                    cp16(st + kDHalf30 + kZL30 + l16, de + (nb4 >= 0 ? zl : sent_off + l2), dl);
+                    cp16(st + kDHalf30 + kZH30 + l16, de + (nb5 >= 0 ? zh : sent_off + l2), dl);
+                    // y halos: row 7 of the y- neighbour, row 0 of the y+ neighbour, as [z][x];
+                    // 32 16-B pieces per side: lane -> plane lane >> 2, x pair lane & 3
+                    const uint32_t yo = (uint32_t)(lane >> 2) * 64u + 2u * (uint32_t)(lane & 3);
+                    const uint32_t yl = (uint32_t)nb2 * 512u + 56u + yo, yh = (uint32_t)nb3 * 512u + yo;
+                    cp16(st + kYL30 + l16, u + (nb2 >= 0 ? yl : 0u), nb2 >= 0);
+                    cp16(st + kYH30 + l16, u + (nb3 >= 0 ? yh : 0u), nb3 >= 0);
+                    cp16(st + kDHalf30 + kYL30 + l16, de + (nb2 >= 0 ? yl : sent_off + yo), dl);
+                    cp16(st + kDHalf30 + kYH30 + l16, de + (nb3 >= 0 ? yh : sent_off + yo), dl);
                 }
                 {  // x halos: column 7 of the x- neighbour, column 0 of the x+ neighbour
                     // (u only where the neighbour exists; D_eff from the sentinel chunk otherwise)
@@ -1756,32 +1843,52 @@ __global__ void __launch_bounds__(kThreads31, ctas31(CFG))
     Q.iy = A.inv_dx2[1];
     Q.iz = A.inv_dx2[2];
     const int y = lane >> 2, xp = lane & 3;
-    const uint32_t z0 = 2u * (uint32_t)warp;
+    const int grp = warp / kW31, wq = warp % kW31;  // group, plane pair
+    const uint32_t z0 = 2u * (uint32_t)wq;
     const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);  // own pair offset in a plane (elements)
     const uint32_t oc = bp * 8u;
-    // operand offsets inside a stage (u side; D_eff at +kDHalf30), pinned
-    const uint32_t o_c = pin(kOwn30 + oc + z0 * 512u, lane);
-    const uint32_t o_zm = pin(warp == 0 ? kZL30 + oc : kOwn30 + oc + z0 * 512u - 512u, lane);
-    const uint32_t o_zp = pin(warp == kW31 - 1 ? kZH30 + oc : kOwn30 + oc + z0 * 512u + 1024u, lane);
+    // operand offsets inside a stage (u side; D_eff at +kDHalf30): pinned in
+    // registers, or (tab31) a per-warp table in shared memory re-read each
+    // chunk (3 LDS.128 + 1 LDS issued before the stage wait)
     const uint32_t s_ym = y > 0 ? 512u : 64u, s_yp = y < 7 ? 512u : 64u;
     const uint32_t s_l = xp > 0 ? 512u : 64u, s_r = xp < 3 ? 512u : 64u;
     const uint32_t b_ym = y > 0 ? kOwn30 + oc - 64u + z0 * 512u : kYL30 + 16u * (uint32_t)xp + z0 * 64u;
     const uint32_t b_yp = y < 7 ? kOwn30 + oc + 64u + z0 * 512u : kYH30 + 16u * (uint32_t)xp + z0 * 64u;
     const uint32_t b_l = xp > 0 ? kOwn30 + oc - 8u + z0 * 512u : kXL30 + 8u * (uint32_t)y + z0 * 64u;
     const uint32_t b_r = xp < 3 ? kOwn30 + oc + 16u + z0 * 512u : kXH30 + 8u * (uint32_t)y + z0 * 64u;
-    const uint32_t o_ym0 = pin(b_ym, lane), o_ym1 = pin(b_ym + s_ym, lane);
-    const uint32_t o_yp0 = pin(b_yp, lane), o_yp1 = pin(b_yp + s_yp, lane);
-    const uint32_t o_l0 = pin(b_l, lane), o_l1 = pin(b_l + s_l, lane);
-    const uint32_t o_r0 = pin(b_r, lane), o_r1 = pin(b_r + s_r, lane);
-    const uint32_t o_lm = pin(kCtx30 + 4u * (uint32_t)lane, lane);
-    const uint32_t g_off = pin(z0 * 64u + bp, lane);  // element offset of the lane's plane-z0 pair in a chunk
-    const uint32_t zsh = 2u * z0;                      // lm bit of plane z0
+    const uint32_t v_c = kOwn30 + oc + z0 * 512u;
+    const uint32_t v_zm = wq == 0 ? kZL30 + oc : kOwn30 + oc + z0 * 512u - 512u;
+    const uint32_t v_zp = wq == kW31 - 1 ? kZH30 + oc : kOwn30 + oc + z0 * 512u + 1024u;
+    const uint32_t v_lm = kCtx30 + 4u * (uint32_t)lane, v_g = z0 * 64u + bp;
+    uint32_t tab = 0, p_c = 0, p_zm = 0, p_zp = 0, p_ym0 = 0, p_ym1 = 0, p_yp0 = 0, p_yp1 = 0, p_l0 = 0, p_l1 = 0,
+             p_r0 = 0, p_r1 = 0, p_lm = 0, p_g = 0;
+    if (tab31(CFG)) {
+        tab = pin(sm0 + smem30(kSt) + (uint32_t)warp * 2048u + 16u * (uint32_t)lane, lane);
+        sts4(tab, v_c, v_zm, v_zp, b_ym);
+        sts4(tab + 512u, b_ym + s_ym, b_yp, b_yp + s_yp, b_l);
+        sts4(tab + 1024u, b_l + s_l, b_r, b_r + s_r, v_lm);
+        sts4(tab + 1536u, v_g, 0u, 0u, 0u);
+    } else {
+        p_c = pin(v_c, lane), p_zm = pin(v_zm, lane), p_zp = pin(v_zp, lane);
+        p_ym0 = pin(b_ym, lane), p_ym1 = pin(b_ym + s_ym, lane), p_yp0 = pin(b_yp, lane);
+        p_yp1 = pin(b_yp + s_yp, lane), p_l0 = pin(b_l, lane), p_l1 = pin(b_l + s_l, lane);
+        p_r0 = pin(b_r, lane), p_r1 = pin(b_r + s_r, lane), p_lm = pin(v_lm, lane), p_g = pin(v_g, lane);
+    }
+    const uint32_t zsh = 2u * z0;  // lm bit of plane z0
     double* __restrict__ un = A.un;
     const uint32_t huge_hi = A.huge_hi;
     bool pushed = false;
-    uint32_t s = 0, ph = 0;
+    uint32_t s = (uint32_t)grp, ph = 0;  // this group's chunks: k = grp, grp + kG, ...
 #pragma unroll 1
     for (;;) {
+        uint32_t o_c = p_c, o_zm = p_zm, o_zp = p_zp, o_ym0 = p_ym0, o_ym1 = p_ym1, o_yp0 = p_yp0, o_yp1 = p_yp1;
+        uint32_t o_l0 = p_l0, o_l1 = p_l1, o_r0 = p_r0, o_r1 = p_r1, o_lm = p_lm, g_off = p_g;
+        if (tab31(CFG)) {
+            const uint4 t0 = lds4(tab), t1 = lds4(tab + 512u), t2 = lds4(tab + 1024u);
+            g_off = lds_u32(tab + 1536u);
+            o_c = t0.x, o_zm = t0.y, o_zp = t0.z, o_ym0 = t0.w, o_ym1 = t1.x, o_yp0 = t1.y;
+            o_yp1 = t1.z, o_l0 = t1.w, o_l1 = t2.x, o_r0 = t2.y, o_r1 = t2.z, o_lm = t2.w;
+        }
         mbar_wait(full0 + 8u * s, ph);
         const uint32_t st = sm0 + s * kStage30;
         const int c = (int)lds_u32(st + kCtx30 + 176u);
@@ -1894,13 +2001,373 @@ __global__ void __launch_bounds__(kThreads31, ctas31(CFG))
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8u * s);
-        if (++s == (uint32_t)kSt) {
-            s = 0;
+        s += (uint32_t)kG;
+        if (s >= (uint32_t)kSt) {
+            s -= (uint32_t)kSt;
             ph ^= 1u;
         }
     }
     // the pushed planes are visible system-wide before this kernel completes
     // (the stream's next kernel raises the peer's step counter, pd_peer.cu)
+    if (PUSH && pushed) __threadfence_system();
+}
+
+// ---------------------------------------------------------------------------
+// v40: v31's pipeline with a padded stage layout, so that every operand of a
+// lane sits at a constant offset from its own pair except the x-halo cells.
+// * A stage holds u and D_eff as 10 planes (z = -1..8) of 768 B each: rows
+//   y = -1..8 (64 B: x = 0..7), then the x- and x+ halo columns (8 cells
+//   each). Own node (x, y, z) at (z+1)*768 + (y+1)*64 + 8x; the y halos are
+//   rows -1 and 8 of each plane, the z halos planes -1 and 8.
+// * A lane's z / y neighbours are its own address -+768 / -+64, its x
+//   neighbours -8 / +16 except on the chunk's x faces: three pinned offsets
+//   per lane (v31: eleven), so the compute warps neither spill nor
+//   rematerialise their stage offsets.
+// * The producer warp moves the chunk with per-lane 16-B / 8-B cp.async into
+//   that layout (a bulk or TMA copy cannot scatter rows to a 768-B pitch):
+//   8 + 8 row-pair copies for the own u / D_eff slabs, one for each z / y
+//   halo, two for each x halo; the 176-B chunk record is one bulk copy.
+//   Completion: lane 0's expect_tx (record) + 32 cp.async arrivals.
+// * Arithmetic, paths, rare path and stores: as v31 (bitwise identical).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPP40 = 768;                 // plane pitch
+constexpr uint32_t kHalf40 = 10 * kPP40;        // D_eff half (7680)
+constexpr uint32_t kCtx40 = 2 * kHalf40;        // chunk record, then the chunk id at +176
+constexpr uint32_t kStage40 = kCtx40 + 256;     // 15616
+constexpr uint32_t kXL40 = 640, kXH40 = 704;    // x-halo columns inside a plane
+constexpr int kSt40 = 3, kCtas40 = 4;
+constexpr int kThreads40 = 32 * (kW31 + 1);
+constexpr uint32_t smem40() { return kSt40 * kStage40 + 16u * kSt40; }
+
+template <int REACTION, bool HALF>
+__device__ __noinline__ double2 pair_slow40(const MarchArgs& M, const SlowConsts& K, uint32_t st, int lane, int z,
+                                            double out0, double out1) {
+    ChunkCtx14 C;
+    C.c = (int)lds_u32(st + kCtx40 + 176u);
+    C.lm = lds_u32(st + kCtx40 + 4u * (uint32_t)lane);
+    C.key = (int)lds_u32(st + kCtx40 + 152u);
+    C.flags = (int)lds_u32(st + kCtx40 + 156u);
+    C.dv = lds1(st + kCtx40 + 160u);
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp), pz = st + (uint32_t)(z + 1) * kPP40;
+    Addr30 a;
+    a.c = pz + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
+    a.zm = a.c - kPP40;
+    a.zp = a.c + kPP40;
+    a.ym = a.c - 64u;
+    a.yp = a.c + 64u;
+    a.l = xp > 0 ? a.c - 8u : pz + kXL40 + 8u * (uint32_t)y;
+    a.r = xp < 3 ? a.c + 16u : pz + kXH40 + 8u * (uint32_t)y;
+    return pair_slow30<REACTION, HALF, kHalf40>(M, K, C, z, xp, y, bp, a, out0, out1);
+}
+
+template <int REACTION, bool PUSH, bool HALF>
+__global__ void __launch_bounds__(kThreads40, kCtas40)
+    ftcs_march40_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = sm0 + kSt40 * kStage40, empty0 = full0 + 8u * kSt40;
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+        K.huge_hi = A.huge_hi;
+        for (int s = 0; s < kSt40; ++s) {
+            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 cp.async arrivals
+            mbar_init(empty0 + 8u * s, (uint32_t)kW31);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    const int n = (int)M.n;
+
+    if (warp == kW31) {  // ---------------- producer warp ----------------
+        // batch pipeline as v31: claim of batch b+3, entries of b+2,
+        // descriptors and L2 prefetch of b+1 issued while batch b is copied
+        int* ctr = M.counter;
+        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
+        const uint32_t sent_off = (uint32_t)M.n_all * 512u;  // D_eff sentinel chunk (elements)
+        auto claim = [&]() -> int {
+            int r = 0;
+            if (lane == 0)
+                asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(ctr), "r"(kB31) : "memory");
+            return r;
+        };
+        auto entries = [&](int p0) -> int {
+            const int p = __shfl_sync(0xffffffffu, p0, 0) + lane;
+            return lane < kB31 && p < n ? __ldg(&M.sched[p]) : -1;
+        };
+        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
+        auto descs = [&](int e, int4& d0, int4& d1) {
+            const int c = chunk_of(e);
+            if (lane < kB31 && c >= 0) {
+                d0 = __ldg(desc4 + 2 * (int64_t)c);
+                d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
+            }
+        };
+        auto prefetch = [&](int e) {
+            const int64_t c = (int64_t)chunk_of(e);
+            if (lane < kB31 && c >= 0) {
+                prefetch_l2(u + c * 512, 4096u);
+                prefetch_l2(ctxa + c * kCtxWords30, 176u);
+                if (e >= 0) prefetch_l2(de + c * 512, 4096u);
+            }
+        };
+        int e_c = entries(claim());
+        int e_n = entries(claim());
+        int p_nn = claim();
+        int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
+        descs(e_c, d0c, d1c);
+        prefetch(e_c);
+        // per-lane destinations (stage-relative) and source element offsets
+        const uint32_t L = (uint32_t)lane;
+        const uint32_t d_own = kPP40 + 64u + 16u * L;                        // + 768 i: row pair L of plane i
+        const uint32_t d_ylo = kPP40 * ((L >> 2) + 1u) + 16u * (L & 3u);      // row -1 of plane L/4
+        const uint32_t s_ylo = 64u * (L >> 2) + 2u * (L & 3u);                // of the y- / y+ neighbour
+        const uint32_t d_x0 = kPP40 * ((L >> 3) + 1u) + 8u * (L & 7u);       // x cell (z, y) = L
+        const uint32_t d_x1 = d_x0 + 4u * kPP40;                              //              = L + 32
+        uint32_t s = 0, ph = 0, k = 0;
+#pragma unroll 1
+        for (;;) {
+            int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
+            descs(e_n, d0n, d1n);
+            prefetch(e_n);
+            const int e_nn = entries(p_nn);
+            p_nn = claim();
+            bool done = false;
+#pragma unroll 1
+            for (int j = 0; j < kB31; ++j, ++k) {
+                const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
+                const uint32_t st = sm0 + s * kStage40, full = full0 + 8u * s;
+                if (k >= (uint32_t)kSt40) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+                if (c_cur < 0) {  // end marker: the compute warps stop at this stage
+                    if (lane == 0) {
+                        sts_u32(st + kCtx40 + 176u, 0xFFFFFFFFu);
+                        mbar_arrive(full);
+                    }
+                    cp_mbar_arrive_noinc(full);
+                    done = true;
+                    break;
+                }
+                const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
+                const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
+                const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
+                const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
+                if (lane == 0) {
+                    sts_u32(st + kCtx40 + 176u, (uint32_t)c_cur);
+                    mbar_arrive_tx(full, 176u);
+                    bulk_g2s(st + kCtx40, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
+                }
+                // own slabs: plane i, rows 2 (L/8).. as 16-B pieces (8 per lane)
+                const uint32_t so = (uint32_t)c_cur * 512u + 2u * L;
+                const double* gu = u + so;
+                const double* gd = de + so;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    cp16(st + d_own + (uint32_t)i * kPP40, gu + 64 * i, true);
+                    cp16(st + kHalf40 + d_own + (uint32_t)i * kPP40, gd + 64 * i, dl);
+                }
+                // z halos: plane 7 of the z- neighbour -> plane -1, plane 0 of the z+ neighbour -> plane 8
+                {
+                    const uint32_t zl = (uint32_t)nb4 * 512u + 448u + 2u * L, zh = (uint32_t)nb5 * 512u + 2u * L;
+                    cp16(st + 64u + 16u * L, u + (nb4 >= 0 ? zl : 0u), nb4 >= 0);
+                    cp16(st + 9u * kPP40 + 64u + 16u * L, u + (nb5 >= 0 ? zh : 0u), nb5 >= 0);
+                    cp16(st + kHalf40 + 64u + 16u * L, de + (nb4 >= 0 ? zl : sent_off + 2u * L), dl);
+                    cp16(st + kHalf40 + 9u * kPP40 + 64u + 16u * L, de + (nb5 >= 0 ? zh : sent_off + 2u * L), dl);
+                }
+                // y halos: row 7 of the y- neighbour -> row -1, row 0 of the y+ neighbour -> row 8
+                {
+                    const uint32_t yl = (uint32_t)nb2 * 512u + 56u + s_ylo, yh = (uint32_t)nb3 * 512u + s_ylo;
+                    cp16(st + d_ylo, u + (nb2 >= 0 ? yl : 0u), nb2 >= 0);
+                    cp16(st + d_ylo + 576u, u + (nb3 >= 0 ? yh : 0u), nb3 >= 0);
+                    cp16(st + kHalf40 + d_ylo, de + (nb2 >= 0 ? yl : sent_off + s_ylo), dl);
+                    cp16(st + kHalf40 + d_ylo + 576u, de + (nb3 >= 0 ? yh : sent_off + s_ylo), dl);
+                }
+                // x halos: column 7 of the x- neighbour, column 0 of the x+ neighbour, cells (z, y) = L, L + 32
+                {
+                    const uint32_t xl = (uint32_t)nb0 * 512u + 8u * L + 7u, xh = (uint32_t)nb1 * 512u + 8u * L;
+                    const uint32_t xs = sent_off + 8u * L;
+                    cp8(st + d_x0 + kXL40, u + (nb0 >= 0 ? xl : 0u), nb0 >= 0);
+                    cp8(st + d_x1 + kXL40, u + (nb0 >= 0 ? xl + 256u : 0u), nb0 >= 0);
+                    cp8(st + d_x0 + kXH40, u + (nb1 >= 0 ? xh : 0u), nb1 >= 0);
+                    cp8(st + d_x1 + kXH40, u + (nb1 >= 0 ? xh + 256u : 0u), nb1 >= 0);
+                    cp8(st + kHalf40 + d_x0 + kXL40, de + (nb0 >= 0 ? xl : xs), dl);
+                    cp8(st + kHalf40 + d_x1 + kXL40, de + (nb0 >= 0 ? xl + 256u : xs + 256u), dl);
+                    cp8(st + kHalf40 + d_x0 + kXH40, de + (nb1 >= 0 ? xh : xs), dl);
+                    cp8(st + kHalf40 + d_x1 + kXH40, de + (nb1 >= 0 ? xh + 256u : xs + 256u), dl);
+                }
+                cp_mbar_arrive_noinc(full);
+                if (++s == (uint32_t)kSt40) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+            if (done) break;
+            e_c = e_n;
+            d0c = d0n;
+            d1c = d1n;
+            e_n = e_nn;
+        }
+        return;
+    }
+
+    // ---------------- compute warps ----------------
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t z0 = 2u * (uint32_t)warp;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);
+    const uint32_t pz0 = (z0 + 1u) * kPP40;
+    const uint32_t v_c = pz0 + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
+    const uint32_t o_c = pin(v_c, lane);
+    const uint32_t o_l = pin(xp > 0 ? v_c - 8u : pz0 + kXL40 + 8u * (uint32_t)y, lane);
+    const uint32_t o_r = pin(xp < 3 ? v_c + 16u : pz0 + kXH40 + 8u * (uint32_t)y, lane);
+    const uint32_t zsh = 2u * z0;
+    double* __restrict__ un = A.un;
+    const uint32_t huge_hi = A.huge_hi;
+    bool pushed = false;
+    uint32_t s = 0, ph = 0;
+#pragma unroll 1
+    for (;;) {
+        mbar_wait(full0 + 8u * s, ph);
+        const uint32_t st = sm0 + s * kStage40;
+        const int c = (int)lds_u32(st + kCtx40 + 176u);
+        if (c < 0) break;
+        const uint32_t lm = lds_u32(st + kCtx40 + 4u * (uint32_t)lane);
+        const int flags = (int)lds_u32(st + kCtx40 + 156u);
+        const uint32_t ab = (lm >> zsh) & 0xFu;
+        const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
+        const uint32_t g_off = z0 * 64u + bp;
+        double src[4] = {0.0, 0.0, 0.0, 0.0};
+        if (REACTION == PD_REACTION_VOLUMETRIC) {
+            const double* sp = A.src + (int64_t)c * 512 + g_off;
+            src[0] = sp[0];
+            src[1] = sp[1];
+            src[2] = sp[64];
+            src[3] = sp[65];
+        }
+        const uint32_t a = st + o_c, al = st + o_l, ar = st + o_r;
+        const double2 uc0 = lds2(a), uc1 = lds2(a + kPP40);
+        const double2 uzm = lds2(a - kPP40), uzp = lds2(a + 2u * kPP40);
+        const double uL0 = lds1(al), uR0 = lds1(ar), uL1 = lds1(al + kPP40), uR1 = lds1(ar + kPP40);
+        const double2 uym0 = lds2(a - 64u), uyp0 = lds2(a + 64u);
+        const double2 uym1 = lds2(a + kPP40 - 64u), uyp1 = lds2(a + kPP40 + 64u);
+        double o00, o01, o10, o11;
+        const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
+        if (flags & kFlagUnif) {
+            const double dv = lds1(st + kCtx40 + 160u);
+            const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
+            const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
+            const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
+            o00 = node31<REACTION>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
+                                   dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
+            o01 = node31<REACTION>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
+                                   dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
+            o10 = node31<REACTION>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
+                                   fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
+            o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
+                                   fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
+        } else {
+            const uint32_t b = a + kHalf40, bl = al + kHalf40, br = ar + kHalf40;
+            const double2 dc0 = lds2(b), dc1 = lds2(b + kPP40);
+            const double2 dzm = lds2(b - kPP40), dzp = lds2(b + 2u * kPP40);
+            const double dL0 = lds1(bl), dR0 = lds1(br), dL1 = lds1(bl + kPP40), dR1 = lds1(br + kPP40);
+            const double2 dym0 = lds2(b - 64u), dyp0 = lds2(b + 64u);
+            const double2 dym1 = lds2(b + kPP40 - 64u), dyp1 = lds2(b + kPP40 + 64u);
+            if (ib == 3u) {
+                const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
+                const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
+                o00 = node31<REACTION>(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                                       fface<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), fface<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
+                                       fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
+                o01 = node31<REACTION>(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       fface<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), fface<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
+                                       fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
+                o10 = node31<REACTION>(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       fface<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), fface<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
+                                       fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
+                o11 = node31<REACTION>(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       fface<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), fface<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
+                                       fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+            } else {
+                const double fzx = face<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = face<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
+                const double f0i = face<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = face<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
+                o00 = node31<REACTION>(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                                       face<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), face<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
+                                       face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
+                o01 = node31<REACTION>(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       face<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), face<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
+                                       face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
+                o10 = node31<REACTION>(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       face<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), face<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
+                                       fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
+                o11 = node31<REACTION>(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       face<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), face<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
+                                       fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+                if (sentinel(dc0.x)) o00 = uc0.x;
+                if (sentinel(dc0.y)) o01 = uc0.y;
+                if (sentinel(dc1.x)) o10 = uc1.x;
+                if (sentinel(dc1.y)) o11 = uc1.y;
+            }
+        }
+        const uint32_t hm = max(max((uint32_t)__double2hiint(o00) & 0x7fffffffu, (uint32_t)__double2hiint(o01) & 0x7fffffffu),
+                                max((uint32_t)__double2hiint(o10) & 0x7fffffffu, (uint32_t)__double2hiint(o11) & 0x7fffffffu));
+        const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
+        if (__any_sync(0xffffffffu, slow)) {
+            if (slow) {
+                const double2 r0 = pair_slow40<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
+                const double2 r1 = pair_slow40<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
+                o00 = r0.x;
+                o01 = r0.y;
+                o10 = r1.x;
+                o11 = r1.y;
+            }
+        }
+        double* gp = un + ((uint32_t)c * 512u + g_off);
+        stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
+        stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
+        if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (z0 == 0 || z0 == 6)) {
+            ChunkCtx14 C;
+            C.c = c;
+            C.key = (int)lds_u32(st + kCtx40 + 152u);
+            C.flags = flags;
+            C.lm = lm;
+            C.dv = 0.0;
+            if (z0 == 0) push_pair14(M, C, 0, bp, o00, o01, ab & 1u, ab & 2u);
+            else push_pair14(M, C, 7, bp, o10, o11, ab & 4u, ab & 8u);
+            pushed = true;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8u * s);
+        if (++s == (uint32_t)kSt40) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
     if (PUSH && pushed) __threadfence_system();
 }
 
@@ -2353,18 +2820,16 @@ void march31_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
        ftcs_march31_kernel<2, false, true, N>},                                                                \
       {ftcs_march31_kernel<0, true, true, N>, ftcs_march31_kernel<1, true, true, N>,                           \
        ftcs_march31_kernel<2, true, true, N>}}}
-    static const K31 tabs[3][2][2][3] = {PD_M_TABLE(0), PD_M_TABLE(1), PD_M_TABLE(2)};
+    static const K31 tabs[4][2][2][3] = {PD_M_TABLE(0), PD_M_TABLE(1), PD_M_TABLE(2), PD_M_TABLE(3)};
 #undef PD_M_TABLE
     static const int cfg = [] {
         const char* e = getenv("PD_M31_CFG");
         const int v = e ? atoi(e) : 0;
-        return v >= 0 && v <= 2 ? v : 0;
+        return v >= 0 && v <= 3 ? v : 0;
     }();
     const K31(*tab)[2][3] = tabs[cfg];
-    const int nst = cfg == 1 ? nst31(1) : cfg == 2 ? nst31(2) : nst31(0);
-    const int ctas = cfg == 1 ? ctas31(1) : cfg == 2 ? ctas31(2) : ctas31(0);
-    const uint32_t smem = smem30(nst);
-    static uint64_t attr_done[3] = {0, 0, 0};
+    const uint32_t smem = smem30(nst31(cfg)) + (tab31(cfg) ? 2048u * (uint32_t)(kW31 * grp31(cfg)) : 0u);  // + offset tables
+    static uint64_t attr_done[4] = {0, 0, 0, 0};
     const int dev = g->device;
     if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
     if (!((attr_done[cfg] >> dev) & 1u)) {
@@ -2376,7 +2841,42 @@ void march31_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * ctas, kThreads31, smem, g->stream>>>(M, p.d_ctx, muy, mdy);
+    if (M.dbg & 64) {  // measurement only: resident CTAs per SM of this configuration
+        static bool said = false;
+        int occ = 0;
+        PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tab[p.half ? 1 : 0][push ? 1 : 0][r],
+                                                              threads31(cfg), smem));
+        if (!said) fprintf(stderr, "march31 cfg %d: %d threads, %u B smem, %d CTAs/SM resident (launching %d)\n", cfg,
+                           threads31(cfg), smem, occ, ctas31(cfg));
+        said = true;
+    }
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * ctas31(cfg), threads31(cfg), smem, g->stream>>>(M, p.d_ctx, muy, mdy);
+    PD_CUDA(cudaGetLastError());
+}
+
+void march40_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
+    if (!p.d_ctx) fail(PD_E_INPUT, "march v40 needs the packed chunk records (3-D FP64 plan)");
+    M.sched = flagged_schedule(g, p, M.sched, M.n);
+    using K40 = void (*)(const MarchArgs, const uint32_t*);
+    static const K40 tab[2][2][3] = {
+        {{ftcs_march40_kernel<0, false, false>, ftcs_march40_kernel<1, false, false>, ftcs_march40_kernel<2, false, false>},
+         {ftcs_march40_kernel<0, true, false>, ftcs_march40_kernel<1, true, false>, ftcs_march40_kernel<2, true, false>}},
+        {{ftcs_march40_kernel<0, false, true>, ftcs_march40_kernel<1, false, true>, ftcs_march40_kernel<2, false, true>},
+         {ftcs_march40_kernel<0, true, true>, ftcs_march40_kernel<1, true, true>, ftcs_march40_kernel<2, true, true>}}};
+    const uint32_t smem = smem40();
+    static uint64_t attr_done = 0;
+    const int dev = g->device;
+    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
+    if (!((attr_done >> dev) & 1u)) {
+        for (int h = 0; h < 2; ++h)
+            for (int q = 0; q < 2; ++q)
+                for (int rr = 0; rr < 3; ++rr)
+                    PD_CUDA(cudaFuncSetAttribute(tab[h][q][rr], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done |= 1ull << dev;
+    }
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas40, kThreads40, smem, g->stream>>>(M, p.d_ctx);
     PD_CUDA(cudaGetLastError());
 }
 
@@ -2421,6 +2921,10 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     }
     if (ver == 31) {
         march31_launch(g, p, M, r, pl != nullptr);
+        return;
+    }
+    if (ver == 40) {
+        march40_launch(g, p, M, r, pl != nullptr);
         return;
     }
     static const int pf = [] {
