@@ -2371,6 +2371,371 @@ __global__ void __launch_bounds__(kThreads40, kCtas40)
     if (PUSH && pushed) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------------
+// v41: v40 with the x halos moved out of the planes and x neighbours taken by
+// shuffles. ncu of v40: 42 % of the shared-memory wavefronts were bank-
+// conflict replays, most of them the 8-B x-neighbour loads (rows 64 B apart:
+// four rows on the same banks) and the 8-B x-halo writes (planes 768 B apart).
+// * Stage half: planes z = -1..8 at a 640-B pitch (rows y = -1..8), then the
+//   x- halo column block [z][y] (512 B) and, 64 B further (other banks), the
+//   x+ block.
+// * A lane's x neighbours are its row neighbours' pair halves (shfl up /
+//   down); lanes on the chunk's x faces take the halo cell instead, read by
+//   one conflict-free 8-B load per plane (the other lanes re-read their row's
+//   x- cell: a broadcast).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPP41 = 640;                 // plane pitch
+constexpr uint32_t kXL41 = 10 * kPP41, kXH41 = kXL41 + 576;  // x-halo blocks [z][y]
+constexpr uint32_t kHalf41 = kXH41 + 512;       // D_eff half (7488)
+constexpr uint32_t kCtx41 = 2 * kHalf41;        // chunk record, then the chunk id at +176
+constexpr uint32_t kStage41 = kCtx41 + 256;     // 15232
+constexpr int kSt41 = 3, kCtas41 = 4;
+constexpr int kThreads41 = 32 * (kW31 + 1);
+constexpr uint32_t smem41() { return kSt41 * kStage41 + 16u * kSt41; }
+
+template <int REACTION, bool HALF>
+__device__ __noinline__ double2 pair_slow41(const MarchArgs& M, const SlowConsts& K, uint32_t st, int lane, int z,
+                                            double out0, double out1) {
+    ChunkCtx14 C;
+    C.c = (int)lds_u32(st + kCtx41 + 176u);
+    C.lm = lds_u32(st + kCtx41 + 4u * (uint32_t)lane);
+    C.key = (int)lds_u32(st + kCtx41 + 152u);
+    C.flags = (int)lds_u32(st + kCtx41 + 156u);
+    C.dv = lds1(st + kCtx41 + 160u);
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp), pz = st + (uint32_t)(z + 1) * kPP41;
+    Addr30 a;
+    a.c = pz + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
+    a.zm = a.c - kPP41;
+    a.zp = a.c + kPP41;
+    a.ym = a.c - 64u;
+    a.yp = a.c + 64u;
+    a.l = xp > 0 ? a.c - 8u : st + kXL41 + (uint32_t)z * 64u + 8u * (uint32_t)y;
+    a.r = xp < 3 ? a.c + 16u : st + kXH41 + (uint32_t)z * 64u + 8u * (uint32_t)y;
+    return pair_slow30<REACTION, HALF, kHalf41>(M, K, C, z, xp, y, bp, a, out0, out1);
+}
+
+template <int REACTION, bool PUSH, bool HALF>
+__global__ void __launch_bounds__(kThreads41, kCtas41)
+    ftcs_march41_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ SlowConsts K;
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<double>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t full0 = sm0 + kSt41 * kStage41, empty0 = full0 + 8u * kSt41;
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+        K.huge_hi = A.huge_hi;
+        for (int s = 0; s < kSt41; ++s) {
+            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 cp.async arrivals
+            mbar_init(empty0 + 8u * s, (uint32_t)kW31);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* __restrict__ u = A.u;
+    const double* __restrict__ de = M.deff;
+    const int n = (int)M.n;
+
+    if (warp == kW31) {  // ---------------- producer warp ----------------
+        // batch pipeline as v31: claim of batch b+3, entries of b+2,
+        // descriptors and L2 prefetch of b+1 issued while batch b is copied
+        int* ctr = M.counter;
+        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
+        const uint32_t sent_off = (uint32_t)M.n_all * 512u;  // D_eff sentinel chunk (elements)
+        auto claim = [&]() -> int {
+            int r = 0;
+            if (lane == 0)
+                asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(ctr), "r"(kB31) : "memory");
+            return r;
+        };
+        auto entries = [&](int p0) -> int {
+            const int p = __shfl_sync(0xffffffffu, p0, 0) + lane;
+            return lane < kB31 && p < n ? __ldg(&M.sched[p]) : -1;
+        };
+        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
+        auto descs = [&](int e, int4& d0, int4& d1) {
+            const int c = chunk_of(e);
+            if (lane < kB31 && c >= 0) {
+                d0 = __ldg(desc4 + 2 * (int64_t)c);
+                d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
+            }
+        };
+        auto prefetch = [&](int e) {
+            const int64_t c = (int64_t)chunk_of(e);
+            if (lane < kB31 && c >= 0) {
+                prefetch_l2(u + c * 512, 4096u);
+                prefetch_l2(ctxa + c * kCtxWords30, 176u);
+                if (e >= 0) prefetch_l2(de + c * 512, 4096u);
+            }
+        };
+        int e_c = entries(claim());
+        int e_n = entries(claim());
+        int p_nn = claim();
+        int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
+        descs(e_c, d0c, d1c);
+        prefetch(e_c);
+        // per-lane destinations (stage-relative) and source element offsets
+        const uint32_t L = (uint32_t)lane;
+        const uint32_t d_own = kPP41 + 64u + 16u * L;                        // + 640 i: row pair L of plane i
+        const uint32_t d_ylo = kPP41 * ((L >> 2) + 1u) + 16u * (L & 3u);      // row -1 of plane L/4
+        const uint32_t s_ylo = 64u * (L >> 2) + 2u * (L & 3u);                // of the y- / y+ neighbour
+        const uint32_t d_x0 = 8u * L;                                         // x cell (z, y) = L
+        const uint32_t d_x1 = d_x0 + 256u;                                    //              = L + 32
+        uint32_t s = 0, ph = 0, k = 0;
+#pragma unroll 1
+        for (;;) {
+            int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
+            descs(e_n, d0n, d1n);
+            prefetch(e_n);
+            const int e_nn = entries(p_nn);
+            p_nn = claim();
+            bool done = false;
+#pragma unroll 1
+            for (int j = 0; j < kB31; ++j, ++k) {
+                const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
+                const uint32_t st = sm0 + s * kStage41, full = full0 + 8u * s;
+                if (k >= (uint32_t)kSt41) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+                if (c_cur < 0) {  // end marker: the compute warps stop at this stage
+                    if (lane == 0) {
+                        sts_u32(st + kCtx41 + 176u, 0xFFFFFFFFu);
+                        mbar_arrive(full);
+                    }
+                    cp_mbar_arrive_noinc(full);
+                    done = true;
+                    break;
+                }
+                const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
+                const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
+                const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
+                const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
+                if (lane == 0) {
+                    sts_u32(st + kCtx41 + 176u, (uint32_t)c_cur);
+                    mbar_arrive_tx(full, 176u);
+                    bulk_g2s(st + kCtx41, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
+                }
+                // own slabs: plane i, rows 2 (L/8).. as 16-B pieces (8 per lane)
+                const uint32_t so = (uint32_t)c_cur * 512u + 2u * L;
+                const double* gu = u + so;
+                const double* gd = de + so;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    cp16(st + d_own + (uint32_t)i * kPP41, gu + 64 * i, true);
+                    cp16(st + kHalf41 + d_own + (uint32_t)i * kPP41, gd + 64 * i, dl);
+                }
+                // z halos: plane 7 of the z- neighbour -> plane -1, plane 0 of the z+ neighbour -> plane 8
+                {
+                    const uint32_t zl = (uint32_t)nb4 * 512u + 448u + 2u * L, zh = (uint32_t)nb5 * 512u + 2u * L;
+                    cp16(st + 64u + 16u * L, u + (nb4 >= 0 ? zl : 0u), nb4 >= 0);
+                    cp16(st + 9u * kPP41 + 64u + 16u * L, u + (nb5 >= 0 ? zh : 0u), nb5 >= 0);
+                    cp16(st + kHalf41 + 64u + 16u * L, de + (nb4 >= 0 ? zl : sent_off + 2u * L), dl);
+                    cp16(st + kHalf41 + 9u * kPP41 + 64u + 16u * L, de + (nb5 >= 0 ? zh : sent_off + 2u * L), dl);
+                }
+                // y halos: row 7 of the y- neighbour -> row -1, row 0 of the y+ neighbour -> row 8
+                {
+                    const uint32_t yl = (uint32_t)nb2 * 512u + 56u + s_ylo, yh = (uint32_t)nb3 * 512u + s_ylo;
+                    cp16(st + d_ylo, u + (nb2 >= 0 ? yl : 0u), nb2 >= 0);
+                    cp16(st + d_ylo + 576u, u + (nb3 >= 0 ? yh : 0u), nb3 >= 0);
+                    cp16(st + kHalf41 + d_ylo, de + (nb2 >= 0 ? yl : sent_off + s_ylo), dl);
+                    cp16(st + kHalf41 + d_ylo + 576u, de + (nb3 >= 0 ? yh : sent_off + s_ylo), dl);
+                }
+                // x halos: column 7 of the x- neighbour, column 0 of the x+ neighbour, cells (z, y) = L, L + 32
+                {
+                    const uint32_t xl = (uint32_t)nb0 * 512u + 8u * L + 7u, xh = (uint32_t)nb1 * 512u + 8u * L;
+                    const uint32_t xs = sent_off + 8u * L;
+                    cp8(st + d_x0 + kXL41, u + (nb0 >= 0 ? xl : 0u), nb0 >= 0);
+                    cp8(st + d_x1 + kXL41, u + (nb0 >= 0 ? xl + 256u : 0u), nb0 >= 0);
+                    cp8(st + d_x0 + kXH41, u + (nb1 >= 0 ? xh : 0u), nb1 >= 0);
+                    cp8(st + d_x1 + kXH41, u + (nb1 >= 0 ? xh + 256u : 0u), nb1 >= 0);
+                    cp8(st + kHalf41 + d_x0 + kXL41, de + (nb0 >= 0 ? xl : xs), dl);
+                    cp8(st + kHalf41 + d_x1 + kXL41, de + (nb0 >= 0 ? xl + 256u : xs + 256u), dl);
+                    cp8(st + kHalf41 + d_x0 + kXH41, de + (nb1 >= 0 ? xh : xs), dl);
+                    cp8(st + kHalf41 + d_x1 + kXH41, de + (nb1 >= 0 ? xh + 256u : xs + 256u), dl);
+                }
+                cp_mbar_arrive_noinc(full);
+                if (++s == (uint32_t)kSt41) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+            if (done) break;
+            e_c = e_n;
+            d0c = d0n;
+            d1c = d1n;
+            e_n = e_nn;
+        }
+        return;
+    }
+
+    // ---------------- compute warps ----------------
+    Consts Q;
+    Q.dt = A.dt;
+    Q.neg_k = A.neg_k;
+    Q.src_factor = A.src_factor;
+    Q.ix = A.inv_dx2[0];
+    Q.iy = A.inv_dx2[1];
+    Q.iz = A.inv_dx2[2];
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t z0 = 2u * (uint32_t)warp;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);
+    const uint32_t pz0 = (z0 + 1u) * kPP41;
+    const uint32_t v_c = pz0 + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
+    const uint32_t o_c = pin(v_c, lane);
+    // x-halo cell of plane z0 (x+ block for xp = 3; x- block otherwise: the
+    // interior lanes' copy of their row's x- cell is a broadcast, unused)
+    const uint32_t o_x = pin((xp == 3 ? kXH41 : kXL41) + z0 * 64u + 8u * (uint32_t)y, lane);
+    const bool xlo = xp == 0, xhi = xp == 3;
+    const uint32_t zsh = 2u * z0;
+    double* __restrict__ un = A.un;
+    const uint32_t huge_hi = A.huge_hi;
+    bool pushed = false;
+    uint32_t s = 0, ph = 0;
+#pragma unroll 1
+    for (;;) {
+        mbar_wait(full0 + 8u * s, ph);
+        const uint32_t st = sm0 + s * kStage41;
+        const int c = (int)lds_u32(st + kCtx41 + 176u);
+        if (c < 0) break;
+        const uint32_t lm = lds_u32(st + kCtx41 + 4u * (uint32_t)lane);
+        const int flags = (int)lds_u32(st + kCtx41 + 156u);
+        const uint32_t ab = (lm >> zsh) & 0xFu;
+        const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
+        const uint32_t g_off = z0 * 64u + bp;
+        double src[4] = {0.0, 0.0, 0.0, 0.0};
+        if (REACTION == PD_REACTION_VOLUMETRIC) {
+            const double* sp = A.src + (int64_t)c * 512 + g_off;
+            src[0] = sp[0];
+            src[1] = sp[1];
+            src[2] = sp[64];
+            src[3] = sp[65];
+        }
+        const uint32_t a = st + o_c, ax = st + o_x;
+        const double2 uc0 = lds2(a), uc1 = lds2(a + kPP41);
+        const double2 uzm = lds2(a - kPP41), uzp = lds2(a + 2u * kPP41);
+        const double uh0 = lds1(ax), uh1 = lds1(ax + 64u);
+        // every lane shuffles (full mask), then the face lanes take the halo cell
+        const double su0 = __shfl_up_sync(0xffffffffu, uc0.y, 1), sd0 = __shfl_down_sync(0xffffffffu, uc0.x, 1);
+        const double su1 = __shfl_up_sync(0xffffffffu, uc1.y, 1), sd1 = __shfl_down_sync(0xffffffffu, uc1.x, 1);
+        const double uL0 = xlo ? uh0 : su0, uR0 = xhi ? uh0 : sd0;
+        const double uL1 = xlo ? uh1 : su1, uR1 = xhi ? uh1 : sd1;
+        const double2 uym0 = lds2(a - 64u), uyp0 = lds2(a + 64u);
+        const double2 uym1 = lds2(a + kPP41 - 64u), uyp1 = lds2(a + kPP41 + 64u);
+        double o00, o01, o10, o11;
+        const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
+        if (flags & kFlagUnif) {
+            const double dv = lds1(st + kCtx41 + 160u);
+            const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
+            const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
+            const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
+            o00 = node31<REACTION>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
+                                   dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
+            o01 = node31<REACTION>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
+                                   dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
+            o10 = node31<REACTION>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
+                                   fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
+            o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
+                                   fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
+        } else {
+            const uint32_t b = a + kHalf41, bx = ax + kHalf41;
+            const double2 dc0 = lds2(b), dc1 = lds2(b + kPP41);
+            const double2 dzm = lds2(b - kPP41), dzp = lds2(b + 2u * kPP41);
+            const double dh0 = lds1(bx), dh1 = lds1(bx + 64u);
+            const double tu0 = __shfl_up_sync(0xffffffffu, dc0.y, 1), td0 = __shfl_down_sync(0xffffffffu, dc0.x, 1);
+            const double tu1 = __shfl_up_sync(0xffffffffu, dc1.y, 1), td1 = __shfl_down_sync(0xffffffffu, dc1.x, 1);
+            const double dL0 = xlo ? dh0 : tu0, dR0 = xhi ? dh0 : td0;
+            const double dL1 = xlo ? dh1 : tu1, dR1 = xhi ? dh1 : td1;
+            const double2 dym0 = lds2(b - 64u), dyp0 = lds2(b + 64u);
+            const double2 dym1 = lds2(b + kPP41 - 64u), dyp1 = lds2(b + kPP41 + 64u);
+            if (ib == 3u) {
+                const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
+                const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
+                o00 = node31<REACTION>(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                                       fface<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), fface<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
+                                       fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
+                o01 = node31<REACTION>(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       fface<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), fface<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
+                                       fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
+                o10 = node31<REACTION>(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       fface<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), fface<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
+                                       fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
+                o11 = node31<REACTION>(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       fface<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), fface<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
+                                       fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+            } else {
+                const double fzx = face<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = face<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
+                const double f0i = face<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = face<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
+                o00 = node31<REACTION>(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                                       face<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), face<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
+                                       face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
+                o01 = node31<REACTION>(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       face<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), face<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
+                                       face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
+                o10 = node31<REACTION>(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       face<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), face<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
+                                       fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
+                o11 = node31<REACTION>(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       face<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), face<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
+                                       fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+                if (sentinel(dc0.x)) o00 = uc0.x;
+                if (sentinel(dc0.y)) o01 = uc0.y;
+                if (sentinel(dc1.x)) o10 = uc1.x;
+                if (sentinel(dc1.y)) o11 = uc1.y;
+            }
+        }
+        const uint32_t hm = max(max((uint32_t)__double2hiint(o00) & 0x7fffffffu, (uint32_t)__double2hiint(o01) & 0x7fffffffu),
+                                max((uint32_t)__double2hiint(o10) & 0x7fffffffu, (uint32_t)__double2hiint(o11) & 0x7fffffffu));
+        const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
+        if (__any_sync(0xffffffffu, slow)) {
+            if (slow) {
+                const double2 r0 = pair_slow41<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
+                const double2 r1 = pair_slow41<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
+                o00 = r0.x;
+                o01 = r0.y;
+                o10 = r1.x;
+                o11 = r1.y;
+            }
+        }
+        double* gp = un + ((uint32_t)c * 512u + g_off);
+        stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
+        stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
+        if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (z0 == 0 || z0 == 6)) {
+            ChunkCtx14 C;
+            C.c = c;
+            C.key = (int)lds_u32(st + kCtx41 + 152u);
+            C.flags = flags;
+            C.lm = lm;
+            C.dv = 0.0;
+            if (z0 == 0) push_pair14(M, C, 0, bp, o00, o01, ab & 1u, ab & 2u);
+            else push_pair14(M, C, 7, bp, o10, o11, ab & 4u, ab & 8u);
+            pushed = true;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8u * s);
+        if (++s == (uint32_t)kSt41) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+    if (PUSH && pushed) __threadfence_system();
+}
+
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 // desc flags of the fused halo push: bit set iff the chunk has a peer ghost
@@ -2880,6 +3245,32 @@ void march40_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     PD_CUDA(cudaGetLastError());
 }
 
+void march41_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
+    if (!p.d_ctx) fail(PD_E_INPUT, "march v41 needs the packed chunk records (3-D FP64 plan)");
+    M.sched = flagged_schedule(g, p, M.sched, M.n);
+    using K41 = void (*)(const MarchArgs, const uint32_t*);
+    static const K41 tab[2][2][3] = {
+        {{ftcs_march41_kernel<0, false, false>, ftcs_march41_kernel<1, false, false>, ftcs_march41_kernel<2, false, false>},
+         {ftcs_march41_kernel<0, true, false>, ftcs_march41_kernel<1, true, false>, ftcs_march41_kernel<2, true, false>}},
+        {{ftcs_march41_kernel<0, false, true>, ftcs_march41_kernel<1, false, true>, ftcs_march41_kernel<2, false, true>},
+         {ftcs_march41_kernel<0, true, true>, ftcs_march41_kernel<1, true, true>, ftcs_march41_kernel<2, true, true>}}};
+    const uint32_t smem = smem41();
+    static uint64_t attr_done = 0;
+    const int dev = g->device;
+    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
+    if (!((attr_done >> dev) & 1u)) {
+        for (int h = 0; h < 2; ++h)
+            for (int q = 0; q < 2; ++q)
+                for (int rr = 0; rr < 3; ++rr)
+                    PD_CUDA(cudaFuncSetAttribute(tab[h][q][rr], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done |= 1ull << dev;
+    }
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas41, kThreads41, smem, g->stream>>>(M, p.d_ctx);
+    PD_CUDA(cudaGetLastError());
+}
+
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
                         int64_t n, int* counter, const PeerLaunch* pl) {
     MarchArgs M;
@@ -2925,6 +3316,10 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     }
     if (ver == 40) {
         march40_launch(g, p, M, r, pl != nullptr);
+        return;
+    }
+    if (ver == 41) {
+        march41_launch(g, p, M, r, pl != nullptr);
         return;
     }
     static const int pf = [] {
