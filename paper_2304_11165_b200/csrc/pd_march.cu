@@ -2013,376 +2013,24 @@ __global__ void __maxnreg__(maxreg31(CFG))
 }
 
 // ---------------------------------------------------------------------------
-// v40: v31's pipeline with a padded stage layout, so that every operand of a
-// lane sits at a constant offset from its own pair except the x-halo cells.
-// * A stage holds u and D_eff as 10 planes (z = -1..8) of 768 B each: rows
-//   y = -1..8 (64 B: x = 0..7), then the x- and x+ halo columns (8 cells
-//   each). Own node (x, y, z) at (z+1)*768 + (y+1)*64 + 8x; the y halos are
-//   rows -1 and 8 of each plane, the z halos planes -1 and 8.
-// * A lane's z / y neighbours are its own address -+768 / -+64, its x
-//   neighbours -8 / +16 except on the chunk's x faces: three pinned offsets
-//   per lane (v31: eleven), so the compute warps neither spill nor
-//   rematerialise their stage offsets.
+// v41: v31's pipeline with a padded stage layout (v40, commit history) and x
+// neighbours by shuffle.
+// * A stage half (u; D_eff at +kHalf41) holds 10 planes z = -1..8 at a 640-B
+//   pitch, rows y = -1..8 of 64 B: own node (x, y, z) at (z+1)*640 +
+//   (y+1)*64 + 8x, the y halos as rows -1 / 8 of each plane, the z halos as
+//   planes -1 / 8; then the x- halo column block [z][y] (512 B) and, 64 B
+//   further (other banks), the x+ block.
+// * A lane's z / y neighbours are its own address -+640 / -+64 (no per-lane
+//   halo offsets: v31 pinned eleven stage offsets per lane and spilled); its
+//   x neighbours are its row neighbours' pair halves (shfl up / down), lanes
+//   on the chunk's x faces take the halo cell, read by one conflict-free 8-B
+//   load per plane (v40 read x neighbours with 8-B loads: rows 64 B apart put
+//   four rows on the same banks, 3x replays).
 // * The producer warp moves the chunk with per-lane 16-B / 8-B cp.async into
-//   that layout (a bulk or TMA copy cannot scatter rows to a 768-B pitch):
-//   8 + 8 row-pair copies for the own u / D_eff slabs, one for each z / y
-//   halo, two for each x halo; the 176-B chunk record is one bulk copy.
-//   Completion: lane 0's expect_tx (record) + 32 cp.async arrivals.
+//   that layout (a bulk or TMA copy cannot scatter rows to a 640-B pitch);
+//   the 176-B chunk record is one bulk copy. Completion: lane 0's expect_tx
+//   + 32 cp.async arrivals (cp.async.mbarrier.arrive.noinc).
 // * Arithmetic, paths, rare path and stores: as v31 (bitwise identical).
-// ---------------------------------------------------------------------------
-constexpr uint32_t kPP40 = 768;                 // plane pitch
-constexpr uint32_t kHalf40 = 10 * kPP40;        // D_eff half (7680)
-constexpr uint32_t kCtx40 = 2 * kHalf40;        // chunk record, then the chunk id at +176
-constexpr uint32_t kStage40 = kCtx40 + 256;     // 15616
-constexpr uint32_t kXL40 = 640, kXH40 = 704;    // x-halo columns inside a plane
-constexpr int kSt40 = 3, kCtas40 = 4;
-constexpr int kThreads40 = 32 * (kW31 + 1);
-constexpr uint32_t smem40() { return kSt40 * kStage40 + 16u * kSt40; }
-
-template <int REACTION, bool HALF>
-__device__ __noinline__ double2 pair_slow40(const MarchArgs& M, const SlowConsts& K, uint32_t st, int lane, int z,
-                                            double out0, double out1) {
-    ChunkCtx14 C;
-    C.c = (int)lds_u32(st + kCtx40 + 176u);
-    C.lm = lds_u32(st + kCtx40 + 4u * (uint32_t)lane);
-    C.key = (int)lds_u32(st + kCtx40 + 152u);
-    C.flags = (int)lds_u32(st + kCtx40 + 156u);
-    C.dv = lds1(st + kCtx40 + 160u);
-    const int y = lane >> 2, xp = lane & 3;
-    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp), pz = st + (uint32_t)(z + 1) * kPP40;
-    Addr30 a;
-    a.c = pz + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
-    a.zm = a.c - kPP40;
-    a.zp = a.c + kPP40;
-    a.ym = a.c - 64u;
-    a.yp = a.c + 64u;
-    a.l = xp > 0 ? a.c - 8u : pz + kXL40 + 8u * (uint32_t)y;
-    a.r = xp < 3 ? a.c + 16u : pz + kXH40 + 8u * (uint32_t)y;
-    return pair_slow30<REACTION, HALF, kHalf40>(M, K, C, z, xp, y, bp, a, out0, out1);
-}
-
-template <int REACTION, bool PUSH, bool HALF>
-__global__ void __launch_bounds__(kThreads40, kCtas40)
-    ftcs_march40_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ SlowConsts K;
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const StepArgs<double>& A = M.A;
-    if (A.k > 0) {
-        const int prev = A.flags[A.k - 1];
-        if (prev) {
-            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
-            return;
-        }
-    }
-    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t full0 = sm0 + kSt40 * kStage40, empty0 = full0 + 8u * kSt40;
-    if (t == 0) {
-        for (int a = 0; a < 3; ++a) {
-            K.size[a] = A.size[a];
-            K.inv_dx2[a] = A.inv_dx2[a];
-        }
-        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
-        K.dt = A.dt;
-        K.neg_k = A.neg_k;
-        K.src_factor = A.src_factor;
-        K.dirichlet = A.dirichlet;
-        K.huge_hi = A.huge_hi;
-        for (int s = 0; s < kSt40; ++s) {
-            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 cp.async arrivals
-            mbar_init(empty0 + 8u * s, (uint32_t)kW31);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    const double* __restrict__ u = A.u;
-    const double* __restrict__ de = M.deff;
-    const int n = (int)M.n;
-
-    if (warp == kW31) {  // ---------------- producer warp ----------------
-        // batch pipeline as v31: claim of batch b+3, entries of b+2,
-        // descriptors and L2 prefetch of b+1 issued while batch b is copied
-        int* ctr = M.counter;
-        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
-        const uint32_t sent_off = (uint32_t)M.n_all * 512u;  // D_eff sentinel chunk (elements)
-        auto claim = [&]() -> int {
-            int r = 0;
-            if (lane == 0)
-                asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(ctr), "r"(kB31) : "memory");
-            return r;
-        };
-        auto entries = [&](int p0) -> int {
-            const int p = __shfl_sync(0xffffffffu, p0, 0) + lane;
-            return lane < kB31 && p < n ? __ldg(&M.sched[p]) : -1;
-        };
-        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
-        auto descs = [&](int e, int4& d0, int4& d1) {
-            const int c = chunk_of(e);
-            if (lane < kB31 && c >= 0) {
-                d0 = __ldg(desc4 + 2 * (int64_t)c);
-                d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
-            }
-        };
-        auto prefetch = [&](int e) {
-            const int64_t c = (int64_t)chunk_of(e);
-            if (lane < kB31 && c >= 0) {
-                prefetch_l2(u + c * 512, 4096u);
-                prefetch_l2(ctxa + c * kCtxWords30, 176u);
-                if (e >= 0) prefetch_l2(de + c * 512, 4096u);
-            }
-        };
-        int e_c = entries(claim());
-        int e_n = entries(claim());
-        int p_nn = claim();
-        int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
-        descs(e_c, d0c, d1c);
-        prefetch(e_c);
-        // per-lane destinations (stage-relative) and source element offsets
-        const uint32_t L = (uint32_t)lane;
-        const uint32_t d_own = kPP40 + 64u + 16u * L;                        // + 768 i: row pair L of plane i
-        const uint32_t d_ylo = kPP40 * ((L >> 2) + 1u) + 16u * (L & 3u);      // row -1 of plane L/4
-        const uint32_t s_ylo = 64u * (L >> 2) + 2u * (L & 3u);                // of the y- / y+ neighbour
-        const uint32_t d_x0 = kPP40 * ((L >> 3) + 1u) + 8u * (L & 7u);       // x cell (z, y) = L
-        const uint32_t d_x1 = d_x0 + 4u * kPP40;                              //              = L + 32
-        uint32_t s = 0, ph = 0, k = 0;
-#pragma unroll 1
-        for (;;) {
-            int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
-            descs(e_n, d0n, d1n);
-            prefetch(e_n);
-            const int e_nn = entries(p_nn);
-            p_nn = claim();
-            bool done = false;
-#pragma unroll 1
-            for (int j = 0; j < kB31; ++j, ++k) {
-                const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
-                const uint32_t st = sm0 + s * kStage40, full = full0 + 8u * s;
-                if (k >= (uint32_t)kSt40) mbar_wait(empty0 + 8u * s, ph ^ 1u);
-                if (c_cur < 0) {  // end marker: the compute warps stop at this stage
-                    if (lane == 0) {
-                        sts_u32(st + kCtx40 + 176u, 0xFFFFFFFFu);
-                        mbar_arrive(full);
-                    }
-                    cp_mbar_arrive_noinc(full);
-                    done = true;
-                    break;
-                }
-                const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
-                const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
-                const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
-                const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
-                if (lane == 0) {
-                    sts_u32(st + kCtx40 + 176u, (uint32_t)c_cur);
-                    mbar_arrive_tx(full, 176u);
-                    bulk_g2s(st + kCtx40, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
-                }
-                // own slabs: plane i, rows 2 (L/8).. as 16-B pieces (8 per lane)
-                const uint32_t so = (uint32_t)c_cur * 512u + 2u * L;
-                const double* gu = u + so;
-                const double* gd = de + so;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    cp16(st + d_own + (uint32_t)i * kPP40, gu + 64 * i, true);
-                    cp16(st + kHalf40 + d_own + (uint32_t)i * kPP40, gd + 64 * i, dl);
-                }
-                // z halos: plane 7 of the z- neighbour -> plane -1, plane 0 of the z+ neighbour -> plane 8
-                {
-                    const uint32_t zl = (uint32_t)nb4 * 512u + 448u + 2u * L, zh = (uint32_t)nb5 * 512u + 2u * L;
-                    cp16(st + 64u + 16u * L, u + (nb4 >= 0 ? zl : 0u), nb4 >= 0);
-                    cp16(st + 9u * kPP40 + 64u + 16u * L, u + (nb5 >= 0 ? zh : 0u), nb5 >= 0);
-                    cp16(st + kHalf40 + 64u + 16u * L, de + (nb4 >= 0 ? zl : sent_off + 2u * L), dl);
-                    cp16(st + kHalf40 + 9u * kPP40 + 64u + 16u * L, de + (nb5 >= 0 ? zh : sent_off + 2u * L), dl);
-                }
-                // y halos: row 7 of the y- neighbour -> row -1, row 0 of the y+ neighbour -> row 8
-                {
-                    const uint32_t yl = (uint32_t)nb2 * 512u + 56u + s_ylo, yh = (uint32_t)nb3 * 512u + s_ylo;
-                    cp16(st + d_ylo, u + (nb2 >= 0 ? yl : 0u), nb2 >= 0);
-                    cp16(st + d_ylo + 576u, u + (nb3 >= 0 ? yh : 0u), nb3 >= 0);
-                    cp16(st + kHalf40 + d_ylo, de + (nb2 >= 0 ? yl : sent_off + s_ylo), dl);
-                    cp16(st + kHalf40 + d_ylo + 576u, de + (nb3 >= 0 ? yh : sent_off + s_ylo), dl);
-                }
-                // x halos: column 7 of the x- neighbour, column 0 of the x+ neighbour, cells (z, y) = L, L + 32
-                {
-                    const uint32_t xl = (uint32_t)nb0 * 512u + 8u * L + 7u, xh = (uint32_t)nb1 * 512u + 8u * L;
-                    const uint32_t xs = sent_off + 8u * L;
-                    cp8(st + d_x0 + kXL40, u + (nb0 >= 0 ? xl : 0u), nb0 >= 0);
-                    cp8(st + d_x1 + kXL40, u + (nb0 >= 0 ? xl + 256u : 0u), nb0 >= 0);
-                    cp8(st + d_x0 + kXH40, u + (nb1 >= 0 ? xh : 0u), nb1 >= 0);
-                    cp8(st + d_x1 + kXH40, u + (nb1 >= 0 ? xh + 256u : 0u), nb1 >= 0);
-                    cp8(st + kHalf40 + d_x0 + kXL40, de + (nb0 >= 0 ? xl : xs), dl);
-                    cp8(st + kHalf40 + d_x1 + kXL40, de + (nb0 >= 0 ? xl + 256u : xs + 256u), dl);
-                    cp8(st + kHalf40 + d_x0 + kXH40, de + (nb1 >= 0 ? xh : xs), dl);
-                    cp8(st + kHalf40 + d_x1 + kXH40, de + (nb1 >= 0 ? xh + 256u : xs + 256u), dl);
-                }
-                cp_mbar_arrive_noinc(full);
-                if (++s == (uint32_t)kSt40) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-            if (done) break;
-            e_c = e_n;
-            d0c = d0n;
-            d1c = d1n;
-            e_n = e_nn;
-        }
-        return;
-    }
-
-    // ---------------- compute warps ----------------
-    Consts Q;
-    Q.dt = A.dt;
-    Q.neg_k = A.neg_k;
-    Q.src_factor = A.src_factor;
-    Q.ix = A.inv_dx2[0];
-    Q.iy = A.inv_dx2[1];
-    Q.iz = A.inv_dx2[2];
-    const int y = lane >> 2, xp = lane & 3;
-    const uint32_t z0 = 2u * (uint32_t)warp;
-    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);
-    const uint32_t pz0 = (z0 + 1u) * kPP40;
-    const uint32_t v_c = pz0 + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
-    const uint32_t o_c = pin(v_c, lane);
-    const uint32_t o_l = pin(xp > 0 ? v_c - 8u : pz0 + kXL40 + 8u * (uint32_t)y, lane);
-    const uint32_t o_r = pin(xp < 3 ? v_c + 16u : pz0 + kXH40 + 8u * (uint32_t)y, lane);
-    const uint32_t zsh = 2u * z0;
-    double* __restrict__ un = A.un;
-    const uint32_t huge_hi = A.huge_hi;
-    bool pushed = false;
-    uint32_t s = 0, ph = 0;
-#pragma unroll 1
-    for (;;) {
-        mbar_wait(full0 + 8u * s, ph);
-        const uint32_t st = sm0 + s * kStage40;
-        const int c = (int)lds_u32(st + kCtx40 + 176u);
-        if (c < 0) break;
-        const uint32_t lm = lds_u32(st + kCtx40 + 4u * (uint32_t)lane);
-        const int flags = (int)lds_u32(st + kCtx40 + 156u);
-        const uint32_t ab = (lm >> zsh) & 0xFu;
-        const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
-        const uint32_t g_off = z0 * 64u + bp;
-        double src[4] = {0.0, 0.0, 0.0, 0.0};
-        if (REACTION == PD_REACTION_VOLUMETRIC) {
-            const double* sp = A.src + (int64_t)c * 512 + g_off;
-            src[0] = sp[0];
-            src[1] = sp[1];
-            src[2] = sp[64];
-            src[3] = sp[65];
-        }
-        const uint32_t a = st + o_c, al = st + o_l, ar = st + o_r;
-        const double2 uc0 = lds2(a), uc1 = lds2(a + kPP40);
-        const double2 uzm = lds2(a - kPP40), uzp = lds2(a + 2u * kPP40);
-        const double uL0 = lds1(al), uR0 = lds1(ar), uL1 = lds1(al + kPP40), uR1 = lds1(ar + kPP40);
-        const double2 uym0 = lds2(a - 64u), uyp0 = lds2(a + 64u);
-        const double2 uym1 = lds2(a + kPP40 - 64u), uyp1 = lds2(a + kPP40 + 64u);
-        double o00, o01, o10, o11;
-        const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
-        if (flags & kFlagUnif) {
-            const double dv = lds1(st + kCtx40 + 160u);
-            const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
-            const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
-            const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
-            o00 = node31<REACTION>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
-                                   dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
-            o01 = node31<REACTION>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
-                                   dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
-            o10 = node31<REACTION>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
-                                   fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
-            o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
-                                   fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
-        } else {
-            const uint32_t b = a + kHalf40, bl = al + kHalf40, br = ar + kHalf40;
-            const double2 dc0 = lds2(b), dc1 = lds2(b + kPP40);
-            const double2 dzm = lds2(b - kPP40), dzp = lds2(b + 2u * kPP40);
-            const double dL0 = lds1(bl), dR0 = lds1(br), dL1 = lds1(bl + kPP40), dR1 = lds1(br + kPP40);
-            const double2 dym0 = lds2(b - 64u), dyp0 = lds2(b + 64u);
-            const double2 dym1 = lds2(b + kPP40 - 64u), dyp1 = lds2(b + kPP40 + 64u);
-            if (ib == 3u) {
-                const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
-                const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
-                o00 = node31<REACTION>(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
-                                       fface<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), fface<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
-                                       fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
-                o01 = node31<REACTION>(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
-                                       fface<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), fface<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
-                                       fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
-                o10 = node31<REACTION>(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
-                                       fface<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), fface<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
-                                       fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
-                o11 = node31<REACTION>(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
-                                       fface<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), fface<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
-                                       fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
-            } else {
-                const double fzx = face<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = face<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
-                const double f0i = face<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = face<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
-                o00 = node31<REACTION>(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
-                                       face<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), face<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
-                                       face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
-                o01 = node31<REACTION>(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
-                                       face<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), face<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
-                                       face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
-                o10 = node31<REACTION>(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
-                                       face<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), face<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
-                                       fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
-                o11 = node31<REACTION>(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
-                                       face<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), face<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
-                                       fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
-                if (sentinel(dc0.x)) o00 = uc0.x;
-                if (sentinel(dc0.y)) o01 = uc0.y;
-                if (sentinel(dc1.x)) o10 = uc1.x;
-                if (sentinel(dc1.y)) o11 = uc1.y;
-            }
-        }
-        const uint32_t hm = max(max((uint32_t)__double2hiint(o00) & 0x7fffffffu, (uint32_t)__double2hiint(o01) & 0x7fffffffu),
-                                max((uint32_t)__double2hiint(o10) & 0x7fffffffu, (uint32_t)__double2hiint(o11) & 0x7fffffffu));
-        const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
-        if (__any_sync(0xffffffffu, slow)) {
-            if (slow) {
-                const double2 r0 = pair_slow40<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
-                const double2 r1 = pair_slow40<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
-                o00 = r0.x;
-                o01 = r0.y;
-                o10 = r1.x;
-                o11 = r1.y;
-            }
-        }
-        double* gp = un + ((uint32_t)c * 512u + g_off);
-        stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
-        stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
-        if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (z0 == 0 || z0 == 6)) {
-            ChunkCtx14 C;
-            C.c = c;
-            C.key = (int)lds_u32(st + kCtx40 + 152u);
-            C.flags = flags;
-            C.lm = lm;
-            C.dv = 0.0;
-            if (z0 == 0) push_pair14(M, C, 0, bp, o00, o01, ab & 1u, ab & 2u);
-            else push_pair14(M, C, 7, bp, o10, o11, ab & 4u, ab & 8u);
-            pushed = true;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8u * s);
-        if (++s == (uint32_t)kSt40) {
-            s = 0;
-            ph ^= 1u;
-        }
-    }
-    if (PUSH && pushed) __threadfence_system();
-}
-
-// ---------------------------------------------------------------------------
-// v41: v40 with the x halos moved out of the planes and x neighbours taken by
-// shuffles. ncu of v40: 42 % of the shared-memory wavefronts were bank-
-// conflict replays, most of them the 8-B x-neighbour loads (rows 64 B apart:
-// four rows on the same banks) and the 8-B x-halo writes (planes 768 B apart).
-// * Stage half: planes z = -1..8 at a 640-B pitch (rows y = -1..8), then the
-//   x- halo column block [z][y] (512 B) and, 64 B further (other banks), the
-//   x+ block.
-// * A lane's x neighbours are its row neighbours' pair halves (shfl up /
-//   down); lanes on the chunk's x faces take the halo cell instead, read by
-//   one conflict-free 8-B load per plane (the other lanes re-read their row's
-//   x- cell: a broadcast).
 // ---------------------------------------------------------------------------
 constexpr uint32_t kPP41 = 640;                 // plane pitch
 constexpr uint32_t kXL41 = 10 * kPP41, kXH41 = kXL41 + 576;  // x-halo blocks [z][y]
@@ -2737,76 +2385,50 @@ __global__ void __launch_bounds__(kThreads41, kCtas41)
 }
 
 // ---------------------------------------------------------------------------
-// v42: every copy on the TMA / bulk-copy engine, x and y neighbours partly
-// by shuffle. ncu of v41: the shared-memory pipe carried ~424 wavefronts
-// per chunk, ~270 of them the producer's per-lane cp.async (8 wavefronts per
-// 512-B own-slab row copy, 15 per 8-B x-halo gather). Bulk / TMA copies
-// write shared memory without going through the LSU.
-// * Stage half (u; D_eff at +kHalf42): own slab [z][y][x] 4 KB (one bulk
-//   copy), z halos (512-B bulk copies), y halos [z][x] (TMA box {8,1,8,1}),
-//   x halos [z][y][x pair] (TMA box {2,8,8,1}: columns 6-7 of the x-
-//   neighbour, 0-1 of the x+ one). Chunk record: one bulk copy. Completion:
-//   lane 0's expect_tx on the stage's "full" mbarrier.
-// * Compute lane (y, xp), planes z0, z0+1: own pairs at c, c+512; z
-//   neighbours c -+ 512 or the z-halo planes (warp-uniform select); y
-//   neighbours c -+ 64 or, on the chunk's y faces, the y-halo row (one
-//   pinned offset, address select); x neighbours by shuffles, face lanes
-//   from the x-halo block (one pinned offset, conflict-free 8-B loads).
-// * The next stage's try_wait is issued before the current chunk's stores
-//   (an mbarrier try_wait costs ~90 cycles even when the phase is complete),
-//   and the operand loads before the end-marker test.
-// * Arithmetic, paths, rare path and stores: as v31 (bitwise identical).
+// v43: v41 with the x halos on the TMA engine. In v41 the producer's 8-B
+// x-halo gathers (64 rows of a neighbour's column per side) cost ~94
+// shared-memory wavefronts per chunk (15 per instruction against 2 ideal).
+// A TMA box {2,8,8,1} moves columns 6-7 of the x- neighbour / 0-1 of the x+
+// neighbour into an [z][y][pair] block (1 KB per side) without the LSU;
+// lanes on the x faces read x = 7 / x = 0 of their row's pair
+// (conflict-free: the x- and x+ blocks use alternate 8-B halves of a bank
+// pair). Everything else as v41.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kOwn42 = 64;                  // own slab [z][y][x] (after a 64-B pad: the
-                                                 // y-face lanes' unused row loads stay inside)
-constexpr uint32_t kZL42 = 4160, kZH42 = 4672;   // z halos [y][x]
-constexpr uint32_t kYL42 = 5248, kYH42 = 5760;   // y halos [z][x] (TMA destinations: 128-B aligned)
-constexpr uint32_t kXL42 = 6272, kXH42 = 7296;   // x halos [z][y][2] (128-B aligned)
-constexpr uint32_t kHalf42 = 8320;               // D_eff half
-constexpr uint32_t kCtx42 = 2 * kHalf42;         // chunk record, then the chunk id at +176
-constexpr uint32_t kStage42 = kCtx42 + 256;      // 16896
-constexpr int kSt42 = 3, kCtas42 = 4;
-constexpr int kThreads42 = 32 * (kW31 + 1);
-constexpr uint32_t smem42() { return kSt42 * kStage42 + 16u * kSt42; }
-
-__device__ __forceinline__ uint32_t try_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return done;
-}
+constexpr uint32_t kPP43 = 640;                 // plane pitch
+constexpr uint32_t kXL43 = 10 * kPP43, kXH43 = kXL43 + 1024;  // x-halo blocks [z][y][pair] (TMA, 128-B aligned)
+constexpr uint32_t kHalf43 = kXH43 + 1024;      // D_eff half (8448)
+constexpr uint32_t kCtx43 = 2 * kHalf43;        // chunk record, then the chunk id at +176
+constexpr uint32_t kStage43 = kCtx43 + 256;     // 17152
+constexpr int kSt43 = 3, kCtas43 = 4;
+constexpr int kThreads43 = 32 * (kW31 + 1);
+constexpr uint32_t smem43() { return kSt43 * kStage43 + 16u * kSt43; }
 
 template <int REACTION, bool HALF>
-__device__ __noinline__ double2 pair_slow42(const MarchArgs& M, const SlowConsts& K, uint32_t st, int lane, int z,
+__device__ __noinline__ double2 pair_slow43(const MarchArgs& M, const SlowConsts& K, uint32_t st, int lane, int z,
                                             double out0, double out1) {
     ChunkCtx14 C;
-    C.c = (int)lds_u32(st + kCtx42 + 176u);
-    C.lm = lds_u32(st + kCtx42 + 4u * (uint32_t)lane);
-    C.key = (int)lds_u32(st + kCtx42 + 152u);
-    C.flags = (int)lds_u32(st + kCtx42 + 156u);
-    C.dv = lds1(st + kCtx42 + 160u);
+    C.c = (int)lds_u32(st + kCtx43 + 176u);
+    C.lm = lds_u32(st + kCtx43 + 4u * (uint32_t)lane);
+    C.key = (int)lds_u32(st + kCtx43 + 152u);
+    C.flags = (int)lds_u32(st + kCtx43 + 156u);
+    C.dv = lds1(st + kCtx43 + 160u);
     const int y = lane >> 2, xp = lane & 3;
-    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp), oc = bp * 8u, zz = (uint32_t)z;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp), pz = st + (uint32_t)(z + 1) * kPP43;
     Addr30 a;
-    a.c = st + kOwn42 + oc + zz * 512u;
-    a.zm = z == 0 ? st + kZL42 + oc : a.c - 512u;
-    a.zp = z == 7 ? st + kZH42 + oc : a.c + 512u;
-    a.ym = y > 0 ? a.c - 64u : st + kYL42 + zz * 64u + 16u * (uint32_t)xp;
-    a.yp = y < 7 ? a.c + 64u : st + kYH42 + zz * 64u + 16u * (uint32_t)xp;
-    a.l = xp > 0 ? a.c - 8u : st + kXL42 + (zz * 8u + (uint32_t)y) * 16u + 8u;
-    a.r = xp < 3 ? a.c + 16u : st + kXH42 + (zz * 8u + (uint32_t)y) * 16u;
-    return pair_slow30<REACTION, HALF, kHalf42>(M, K, C, z, xp, y, bp, a, out0, out1);
+    a.c = pz + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
+    a.zm = a.c - kPP43;
+    a.zp = a.c + kPP43;
+    a.ym = a.c - 64u;
+    a.yp = a.c + 64u;
+    a.l = xp > 0 ? a.c - 8u : st + kXL43 + ((uint32_t)z * 8u + (uint32_t)y) * 16u + 8u;
+    a.r = xp < 3 ? a.c + 16u : st + kXH43 + ((uint32_t)z * 8u + (uint32_t)y) * 16u;
+    return pair_slow30<REACTION, HALF, kHalf43>(M, K, C, z, xp, y, bp, a, out0, out1);
 }
 
 template <int REACTION, bool PUSH, bool HALF>
-__global__ void __launch_bounds__(kThreads42, kCtas42)
-    ftcs_march42_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
-                        const __grid_constant__ CUtensorMap mux, const __grid_constant__ CUtensorMap muy,
-                        const __grid_constant__ CUtensorMap mdx, const __grid_constant__ CUtensorMap mdy) {
+__global__ void __launch_bounds__(kThreads43, kCtas43)
+    ftcs_march43_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
+                        const __grid_constant__ CUtensorMap mux, const __grid_constant__ CUtensorMap mdx) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
@@ -2820,7 +2442,7 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
         }
     }
     const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t full0 = sm0 + kSt42 * kStage42, empty0 = full0 + 8u * kSt42;
+    const uint32_t full0 = sm0 + kSt43 * kStage43, empty0 = full0 + 8u * kSt43;
     if (t == 0) {
         for (int a = 0; a < 3; ++a) {
             K.size[a] = A.size[a];
@@ -2832,8 +2454,8 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
         K.src_factor = A.src_factor;
         K.dirichlet = A.dirichlet;
         K.huge_hi = A.huge_hi;
-        for (int s = 0; s < kSt42; ++s) {
-            mbar_init(full0 + 8u * s, 1u);  // lane 0's expect_tx arrive (+ the transaction bytes)
+        for (int s = 0; s < kSt43; ++s) {
+            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 cp.async arrivals
             mbar_init(empty0 + 8u * s, (uint32_t)kW31);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -2844,9 +2466,11 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
     const int n = (int)M.n;
 
     if (warp == kW31) {  // ---------------- producer warp ----------------
+        // batch pipeline as v31: claim of batch b+3, entries of b+2,
+        // descriptors and L2 prefetch of b+1 issued while batch b is copied
         int* ctr = M.counter;
         const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
-        const int sent_c = (int)M.n_all;  // D_eff sentinel chunk
+        const uint32_t sent_off = (uint32_t)M.n_all * 512u;  // D_eff sentinel chunk (elements)
         auto claim = [&]() -> int {
             int r = 0;
             if (lane == 0)
@@ -2865,13 +2489,24 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
                 d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
             }
         };
+        // M.pf: bit 0 L2 prefetch of the next batch's u slabs and records,
+        // bit 1 of its D_eff slabs, bit 2 skip the own-slab copies of pairs
+        // with no active node (their D_eff is written as the sentinel)
+        const int pf = M.pf;
         auto prefetch = [&](int e) {
             const int64_t c = (int64_t)chunk_of(e);
             if (lane < kB31 && c >= 0) {
-                prefetch_l2(u + c * 512, 4096u);
-                prefetch_l2(ctxa + c * kCtxWords30, 176u);
-                if (e >= 0) prefetch_l2(de + c * 512, 4096u);
+                if (pf & 1) {
+                    prefetch_l2(u + c * 512, 4096u);
+                    prefetch_l2(ctxa + c * kCtxWords30, 176u);
+                }
+                if ((pf & 2) && e >= 0) prefetch_l2(de + c * 512, 4096u);
             }
+        };
+        // this lane's active-pair word (chunk record lm[lane]) of chunk j of a batch
+        auto lm_of = [&](int e, int j) -> uint32_t {
+            const int c = chunk_of(__shfl_sync(0xffffffffu, e, j));
+            return (pf & 4) && c >= 0 ? __ldg(ctxa + (int64_t)c * kCtxWords30 + lane) : 0xFFFFu;
         };
         int e_c = entries(claim());
         int e_n = entries(claim());
@@ -2879,64 +2514,88 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
         int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
         descs(e_c, d0c, d1c);
         prefetch(e_c);
+        uint32_t lc0 = lm_of(e_c, 0), lc1 = lm_of(e_c, 1), lc2 = lm_of(e_c, 2), lc3 = lm_of(e_c, 3);
+        // per-lane destinations (stage-relative) and source element offsets
+        const uint32_t L = (uint32_t)lane;
+        const uint32_t d_own = kPP43 + 64u + 16u * L;                        // + 640 i: row pair L of plane i
+        const uint32_t d_ylo = kPP43 * ((L >> 2) + 1u) + 16u * (L & 3u);      // row -1 of plane L/4
+        const uint32_t s_ylo = 64u * (L >> 2) + 2u * (L & 3u);                // of the y- / y+ neighbour
         uint32_t s = 0, ph = 0, k = 0;
 #pragma unroll 1
         for (;;) {
             int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
             descs(e_n, d0n, d1n);
             prefetch(e_n);
+            const uint32_t ln0 = lm_of(e_n, 0), ln1 = lm_of(e_n, 1), ln2 = lm_of(e_n, 2), ln3 = lm_of(e_n, 3);
             const int e_nn = entries(p_nn);
             p_nn = claim();
             bool done = false;
 #pragma unroll 1
             for (int j = 0; j < kB31; ++j, ++k) {
                 const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
+                const uint32_t st = sm0 + s * kStage43, full = full0 + 8u * s;
+                if (k >= (uint32_t)kSt43) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+                if (c_cur < 0) {  // end marker: the compute warps stop at this stage
+                    if (lane == 0) {
+                        sts_u32(st + kCtx43 + 176u, 0xFFFFFFFFu);
+                        mbar_arrive(full);
+                    }
+                    cp_mbar_arrive_noinc(full);
+                    done = true;
+                    break;
+                }
                 const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
                 const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
                 const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
                 const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
                 if (lane == 0) {
-                    const uint32_t st = sm0 + s * kStage42, full = full0 + 8u * s;
-                    if (k >= (uint32_t)kSt42) mbar_wait(empty0 + 8u * s, ph ^ 1u);
-                    if (c_cur < 0) {  // end marker: the compute warps stop at this stage
-                        sts_u32(st + kCtx42 + 176u, 0xFFFFFFFFu);
-                        mbar_arrive(full);
-                    } else {
-                        sts_u32(st + kCtx42 + 176u, (uint32_t)c_cur);
-                        uint32_t bytes = 176u + 4096u;
-                        bytes += (nb4 >= 0 ? 512u : 0u) + (nb5 >= 0 ? 512u : 0u) + (nb2 >= 0 ? 512u : 0u) +
-                                 (nb3 >= 0 ? 512u : 0u) + (nb0 >= 0 ? 1024u : 0u) + (nb1 >= 0 ? 1024u : 0u);
-                        if (dl) bytes += 4096u + 4u * 512u + 2u * 1024u;
-                        mbar_arrive_tx(full, bytes);
-                        const int64_t cb = (int64_t)c_cur * 512;
-                        bulk_g2s(st + kCtx42, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
-                        bulk_g2s(st + kOwn42, u + cb, 4096u, full);
-                        if (nb4 >= 0) bulk_g2s(st + kZL42, u + (int64_t)nb4 * 512 + 448, 512u, full);
-                        if (nb5 >= 0) bulk_g2s(st + kZH42, u + (int64_t)nb5 * 512, 512u, full);
-                        if (nb2 >= 0) tma4(st + kYL42, &muy, 0, 7, 0, nb2, full);
-                        if (nb3 >= 0) tma4(st + kYH42, &muy, 0, 0, 0, nb3, full);
-                        if (nb0 >= 0) tma4(st + kXL42, &mux, 6, 0, 0, nb0, full);
-                        if (nb1 >= 0) tma4(st + kXH42, &mux, 0, 0, 0, nb1, full);
-                        if (dl) {
-                            const uint32_t sd = st + kHalf42;
-                            bulk_g2s(sd + kOwn42, de + cb, 4096u, full);
-                            bulk_g2s(sd + kZL42, de + (nb4 >= 0 ? (int64_t)nb4 * 512 + 448 : (int64_t)sent_c * 512),
-                                     512u, full);
-                            bulk_g2s(sd + kZH42, de + (nb5 >= 0 ? (int64_t)nb5 * 512 : (int64_t)sent_c * 512), 512u,
-                                     full);
-                            tma4(sd + kYL42, &mdy, 0, 7, 0, nb2 >= 0 ? nb2 : sent_c, full);
-                            tma4(sd + kYH42, &mdy, 0, 0, 0, nb3 >= 0 ? nb3 : sent_c, full);
-                            tma4(sd + kXL42, &mdx, 6, 0, 0, nb0 >= 0 ? nb0 : sent_c, full);
-                            tma4(sd + kXH42, &mdx, 0, 0, 0, nb1 >= 0 ? nb1 : sent_c, full);
-                        }
+                    sts_u32(st + kCtx43 + 176u, (uint32_t)c_cur);
+                    mbar_arrive_tx(full, 176u + (nb0 >= 0 ? 1024u : 0u) + (nb1 >= 0 ? 1024u : 0u) + (dl ? 2048u : 0u));
+                    bulk_g2s(st + kCtx43, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
+                    if (nb0 >= 0) tma4(st + kXL43, &mux, 6, 0, 0, nb0, full);
+                    if (nb1 >= 0) tma4(st + kXH43, &mux, 0, 0, 0, nb1, full);
+                    if (dl) {
+                        const int sent_c = (int)M.n_all;
+                        tma4(st + kHalf43 + kXL43, &mdx, 6, 0, 0, nb0 >= 0 ? nb0 : sent_c, full);
+                        tma4(st + kHalf43 + kXH43, &mdx, 0, 0, 0, nb1 >= 0 ? nb1 : sent_c, full);
                     }
                 }
-                __syncwarp();
-                if (c_cur < 0) {
-                    done = true;
-                    break;
+                // own slabs: plane i, rows 2 (L/8).. as 16-B pieces (8 per lane)
+                const uint32_t so = (uint32_t)c_cur * 512u + 2u * L;
+                const double* gu = u + so;
+                const double* gd = de + so;
+                const uint32_t lmj = lc0;  // this lane's pair bits (2 per plane)
+                lc0 = lc1;
+                lc1 = lc2;
+                lc2 = lc3;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const bool act = (lmj >> (2 * i)) & 3u;
+                    cp16(st + d_own + (uint32_t)i * kPP43, gu + 64 * i, act);
+                    cp16(st + kHalf43 + d_own + (uint32_t)i * kPP43, gd + 64 * i, dl && act);
+                    if (dl && !act) {  // no active node: D_eff = sentinel, u never used
+                        const uint32_t sh = kSentHi;
+                        sts4(st + kHalf43 + d_own + (uint32_t)i * kPP43, 0u, sh, 0u, sh);
+                    }
                 }
-                if (++s == (uint32_t)kSt42) {
+                // z halos: plane 7 of the z- neighbour -> plane -1, plane 0 of the z+ neighbour -> plane 8
+                {
+                    const uint32_t zl = (uint32_t)nb4 * 512u + 448u + 2u * L, zh = (uint32_t)nb5 * 512u + 2u * L;
+                    cp16(st + 64u + 16u * L, u + (nb4 >= 0 ? zl : 0u), nb4 >= 0);
+                    cp16(st + 9u * kPP43 + 64u + 16u * L, u + (nb5 >= 0 ? zh : 0u), nb5 >= 0);
+                    cp16(st + kHalf43 + 64u + 16u * L, de + (nb4 >= 0 ? zl : sent_off + 2u * L), dl);
+                    cp16(st + kHalf43 + 9u * kPP43 + 64u + 16u * L, de + (nb5 >= 0 ? zh : sent_off + 2u * L), dl);
+                }
+                // y halos: row 7 of the y- neighbour -> row -1, row 0 of the y+ neighbour -> row 8
+                {
+                    const uint32_t yl = (uint32_t)nb2 * 512u + 56u + s_ylo, yh = (uint32_t)nb3 * 512u + s_ylo;
+                    cp16(st + d_ylo, u + (nb2 >= 0 ? yl : 0u), nb2 >= 0);
+                    cp16(st + d_ylo + 576u, u + (nb3 >= 0 ? yh : 0u), nb3 >= 0);
+                    cp16(st + kHalf43 + d_ylo, de + (nb2 >= 0 ? yl : sent_off + s_ylo), dl);
+                    cp16(st + kHalf43 + d_ylo + 576u, de + (nb3 >= 0 ? yh : sent_off + s_ylo), dl);
+                }
+                cp_mbar_arrive_noinc(full);
+                if (++s == (uint32_t)kSt43) {
                     s = 0;
                     ph ^= 1u;
                 }
@@ -2946,6 +2605,10 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
             d0c = d0n;
             d1c = d1n;
             e_n = e_nn;
+            lc0 = ln0;
+            lc1 = ln1;
+            lc2 = ln2;
+            lc3 = ln3;
         }
         return;
     }
@@ -2961,36 +2624,26 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
     const int y = lane >> 2, xp = lane & 3;
     const uint32_t z0 = 2u * (uint32_t)warp;
     const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);
-    const uint32_t o_c = pin(kOwn42 + bp * 8u + z0 * 512u, lane);
-    // y-halo pair of plane z0 for the y-face lanes (others: a broadcast copy
-    // of the y- row), x-halo cell of plane z0 for the x-face lanes (others:
-    // their row's x- cell)
-    const uint32_t o_y = pin((y == 7 ? kYH42 : kYL42) + z0 * 64u + 16u * (uint32_t)xp, lane);
-    const uint32_t o_x = pin(xp == 3 ? kXH42 + (z0 * 8u + (uint32_t)y) * 16u
-                                     : kXL42 + (z0 * 8u + (uint32_t)y) * 16u + 8u, lane);
-    const bool xlo = xp == 0, xhi = xp == 3, ylo = y == 0, yhi = y == 7;
-    const bool zlo = warp == 0, zhi = warp == kW31 - 1;
+    const uint32_t pz0 = (z0 + 1u) * kPP43;
+    const uint32_t v_c = pz0 + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
+    const uint32_t o_c = pin(v_c, lane);
+    // x-halo cell of plane z0 (x+ block for xp = 3; x- block otherwise: the
+    // interior lanes' copy of their row's x- cell is a broadcast, unused)
+    const uint32_t o_x = pin(xp == 3 ? kXH43 + (z0 * 8u + (uint32_t)y) * 16u : kXL43 + (z0 * 8u + (uint32_t)y) * 16u + 8u, lane);
+    const bool xlo = xp == 0, xhi = xp == 3;
     const uint32_t zsh = 2u * z0;
     double* __restrict__ un = A.un;
     const uint32_t huge_hi = A.huge_hi;
     bool pushed = false;
     uint32_t s = 0, ph = 0;
-    uint32_t ready = try_wait(full0, 0u);
 #pragma unroll 1
     for (;;) {
-        if (!ready) mbar_wait(full0 + 8u * s, ph);
-        const uint32_t st = sm0 + s * kStage42;
-        const int c = (int)lds_u32(st + kCtx42 + 176u);
-        const uint32_t lm = lds_u32(st + kCtx42 + 4u * (uint32_t)lane);
-        const int flags = (int)lds_u32(st + kCtx42 + 156u);
-        const uint32_t a = st + o_c, ay = st + o_y, ax = st + o_x;
-        const uint32_t azm = zlo ? a + (kZL42 - kOwn42) : a - 512u, azp = zhi ? a + (kZH42 - kOwn42 - 3072u) : a + 1024u;
-        const double2 uc0 = lds2(a), uc1 = lds2(a + 512u);
-        const double2 uzm = lds2(azm), uzp = lds2(azp);
-        const double2 yh0 = lds2(ay), yh1 = lds2(ay + 64u);
-        const double xh0 = lds1(ax), xh1 = lds1(ax + 128u);
-        const double2 rm0 = lds2(a - 64u), rp0 = lds2(a + 64u), rm1 = lds2(a + 448u), rp1 = lds2(a + 576u);
+        mbar_wait(full0 + 8u * s, ph);
+        const uint32_t st = sm0 + s * kStage43;
+        const int c = (int)lds_u32(st + kCtx43 + 176u);
         if (c < 0) break;
+        const uint32_t lm = lds_u32(st + kCtx43 + 4u * (uint32_t)lane);
+        const int flags = (int)lds_u32(st + kCtx43 + 156u);
         const uint32_t ab = (lm >> zsh) & 0xFu;
         const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
         const uint32_t g_off = z0 * 64u + bp;
@@ -3002,19 +2655,21 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
             src[2] = sp[64];
             src[3] = sp[65];
         }
-        // y neighbours: own slab rows, or the halo row on the chunk's y faces
-        // (the in-slab loads of face lanes read a neighbouring plane: unused)
-        const double2 uym0 = ylo ? yh0 : rm0, uyp0 = yhi ? yh0 : rp0;
-        const double2 uym1 = ylo ? yh1 : rm1, uyp1 = yhi ? yh1 : rp1;
-        // x neighbours: every lane shuffles (full mask), face lanes take the halo cell
+        const uint32_t a = st + o_c, ax = st + o_x;
+        const double2 uc0 = lds2(a), uc1 = lds2(a + kPP43);
+        const double2 uzm = lds2(a - kPP43), uzp = lds2(a + 2u * kPP43);
+        const double uh0 = lds1(ax), uh1 = lds1(ax + 128u);
+        // every lane shuffles (full mask), then the face lanes take the halo cell
         const double su0 = __shfl_up_sync(0xffffffffu, uc0.y, 1), sd0 = __shfl_down_sync(0xffffffffu, uc0.x, 1);
         const double su1 = __shfl_up_sync(0xffffffffu, uc1.y, 1), sd1 = __shfl_down_sync(0xffffffffu, uc1.x, 1);
-        const double uL0 = xlo ? xh0 : su0, uR0 = xhi ? xh0 : sd0;
-        const double uL1 = xlo ? xh1 : su1, uR1 = xhi ? xh1 : sd1;
+        const double uL0 = xlo ? uh0 : su0, uR0 = xhi ? uh0 : sd0;
+        const double uL1 = xlo ? uh1 : su1, uR1 = xhi ? uh1 : sd1;
+        const double2 uym0 = lds2(a - 64u), uyp0 = lds2(a + 64u);
+        const double2 uym1 = lds2(a + kPP43 - 64u), uyp1 = lds2(a + kPP43 + 64u);
         double o00, o01, o10, o11;
         const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
         if (flags & kFlagUnif) {
-            const double dv = lds1(st + kCtx42 + 160u);
+            const double dv = lds1(st + kCtx43 + 160u);
             const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
             const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
             const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
@@ -3027,19 +2682,16 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
             o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
                                    fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
         } else {
-            const uint32_t H = kHalf42;
-            const double2 dc0 = lds2(a + H), dc1 = lds2(a + H + 512u);
-            const double2 dzm = lds2(azm + H), dzp = lds2(azp + H);
-            const double2 dyh0 = lds2(ay + H), dyh1 = lds2(ay + H + 64u);
-            const double dxh0 = lds1(ax + H), dxh1 = lds1(ax + H + 128u);
-            const double2 qm0 = lds2(a + H - 64u), qp0 = lds2(a + H + 64u), qm1 = lds2(a + H + 448u),
-                          qp1 = lds2(a + H + 576u);
-            const double2 dym0 = ylo ? dyh0 : qm0, dyp0 = yhi ? dyh0 : qp0;
-            const double2 dym1 = ylo ? dyh1 : qm1, dyp1 = yhi ? dyh1 : qp1;
+            const uint32_t b = a + kHalf43, bx = ax + kHalf43;
+            const double2 dc0 = lds2(b), dc1 = lds2(b + kPP43);
+            const double2 dzm = lds2(b - kPP43), dzp = lds2(b + 2u * kPP43);
+            const double dh0 = lds1(bx), dh1 = lds1(bx + 128u);
             const double tu0 = __shfl_up_sync(0xffffffffu, dc0.y, 1), td0 = __shfl_down_sync(0xffffffffu, dc0.x, 1);
             const double tu1 = __shfl_up_sync(0xffffffffu, dc1.y, 1), td1 = __shfl_down_sync(0xffffffffu, dc1.x, 1);
-            const double dL0 = xlo ? dxh0 : tu0, dR0 = xhi ? dxh0 : td0;
-            const double dL1 = xlo ? dxh1 : tu1, dR1 = xhi ? dxh1 : td1;
+            const double dL0 = xlo ? dh0 : tu0, dR0 = xhi ? dh0 : td0;
+            const double dL1 = xlo ? dh1 : tu1, dR1 = xhi ? dh1 : td1;
+            const double2 dym0 = lds2(b - 64u), dyp0 = lds2(b + 64u);
+            const double2 dym1 = lds2(b + kPP43 - 64u), dyp1 = lds2(b + kPP43 + 64u);
             if (ib == 3u) {
                 const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
                 const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
@@ -3081,28 +2733,21 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
         const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
         if (__any_sync(0xffffffffu, slow)) {
             if (slow) {
-                const double2 r0 = pair_slow42<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
-                const double2 r1 = pair_slow42<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
+                const double2 r0 = pair_slow43<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
+                const double2 r1 = pair_slow43<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
                 o00 = r0.x;
                 o01 = r0.y;
                 o10 = r1.x;
                 o11 = r1.y;
             }
         }
-        // the next stage's readiness, overlapped with this chunk's stores
-        uint32_t s1 = s + 1u, ph1 = ph;
-        if (s1 == (uint32_t)kSt42) {
-            s1 = 0;
-            ph1 ^= 1u;
-        }
-        ready = try_wait(full0 + 8u * s1, ph1);
         double* gp = un + ((uint32_t)c * 512u + g_off);
         stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
         stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
         if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (z0 == 0 || z0 == 6)) {
             ChunkCtx14 C;
             C.c = c;
-            C.key = (int)lds_u32(st + kCtx42 + 152u);
+            C.key = (int)lds_u32(st + kCtx43 + 152u);
             C.flags = flags;
             C.lm = lm;
             C.dv = 0.0;
@@ -3112,8 +2757,10 @@ __global__ void __launch_bounds__(kThreads42, kCtas42)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8u * s);
-        s = s1;
-        ph = ph1;
+        if (++s == (uint32_t)kSt43) {
+            s = 0;
+            ph ^= 1u;
+        }
     }
     if (PUSH && pushed) __threadfence_system();
 }
@@ -3601,32 +3248,6 @@ void march31_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     PD_CUDA(cudaGetLastError());
 }
 
-void march40_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
-    if (!p.d_ctx) fail(PD_E_INPUT, "march v40 needs the packed chunk records (3-D FP64 plan)");
-    M.sched = flagged_schedule(g, p, M.sched, M.n);
-    using K40 = void (*)(const MarchArgs, const uint32_t*);
-    static const K40 tab[2][2][3] = {
-        {{ftcs_march40_kernel<0, false, false>, ftcs_march40_kernel<1, false, false>, ftcs_march40_kernel<2, false, false>},
-         {ftcs_march40_kernel<0, true, false>, ftcs_march40_kernel<1, true, false>, ftcs_march40_kernel<2, true, false>}},
-        {{ftcs_march40_kernel<0, false, true>, ftcs_march40_kernel<1, false, true>, ftcs_march40_kernel<2, false, true>},
-         {ftcs_march40_kernel<0, true, true>, ftcs_march40_kernel<1, true, true>, ftcs_march40_kernel<2, true, true>}}};
-    const uint32_t smem = smem40();
-    static uint64_t attr_done = 0;
-    const int dev = g->device;
-    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
-    if (!((attr_done >> dev) & 1u)) {
-        for (int h = 0; h < 2; ++h)
-            for (int q = 0; q < 2; ++q)
-                for (int rr = 0; rr < 3; ++rr)
-                    PD_CUDA(cudaFuncSetAttribute(tab[h][q][rr], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_done |= 1ull << dev;
-    }
-    int sms = 148;
-    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas40, kThreads40, smem, g->stream>>>(M, p.d_ctx);
-    PD_CUDA(cudaGetLastError());
-}
-
 void march41_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     if (!p.d_ctx) fail(PD_E_INPUT, "march v41 needs the packed chunk records (3-D FP64 plan)");
     M.sched = flagged_schedule(g, p, M.sched, M.n);
@@ -3653,20 +3274,23 @@ void march41_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     PD_CUDA(cudaGetLastError());
 }
 
-void march42_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
-    if (!p.d_ctx) fail(PD_E_INPUT, "march v42 needs the packed chunk records (3-D FP64 plan)");
+void march43_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
+    static const int pf = [] {
+        const char* e = getenv("PD_M43_PF");
+        return e ? atoi(e) : 5;
+    }();
+    M.pf = pf;
+    if (!p.d_ctx) fail(PD_E_INPUT, "march v43 needs the packed chunk records (3-D FP64 plan)");
     M.sched = flagged_schedule(g, p, M.sched, M.n);
-    static const cuuint32_t bx[4] = {2, 8, 8, 1}, by[4] = {8, 1, 8, 1};
-    const CUtensorMap mux = column_map(M.A.u, g->n_chunks, bx), muy = column_map(M.A.u, g->n_chunks, by);
-    const CUtensorMap mdx = column_map(M.deff, g->n_chunks + 1, bx), mdy = column_map(M.deff, g->n_chunks + 1, by);
-    using K42 = void (*)(const MarchArgs, const uint32_t*, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-                         const CUtensorMap);
-    static const K42 tab[2][2][3] = {
-        {{ftcs_march42_kernel<0, false, false>, ftcs_march42_kernel<1, false, false>, ftcs_march42_kernel<2, false, false>},
-         {ftcs_march42_kernel<0, true, false>, ftcs_march42_kernel<1, true, false>, ftcs_march42_kernel<2, true, false>}},
-        {{ftcs_march42_kernel<0, false, true>, ftcs_march42_kernel<1, false, true>, ftcs_march42_kernel<2, false, true>},
-         {ftcs_march42_kernel<0, true, true>, ftcs_march42_kernel<1, true, true>, ftcs_march42_kernel<2, true, true>}}};
-    const uint32_t smem = smem42();
+    static const cuuint32_t bx[4] = {2, 8, 8, 1};
+    const CUtensorMap mux = column_map(M.A.u, g->n_chunks, bx), mdx = column_map(M.deff, g->n_chunks + 1, bx);
+    using K43 = void (*)(const MarchArgs, const uint32_t*, const CUtensorMap, const CUtensorMap);
+    static const K43 tab[2][2][3] = {
+        {{ftcs_march43_kernel<0, false, false>, ftcs_march43_kernel<1, false, false>, ftcs_march43_kernel<2, false, false>},
+         {ftcs_march43_kernel<0, true, false>, ftcs_march43_kernel<1, true, false>, ftcs_march43_kernel<2, true, false>}},
+        {{ftcs_march43_kernel<0, false, true>, ftcs_march43_kernel<1, false, true>, ftcs_march43_kernel<2, false, true>},
+         {ftcs_march43_kernel<0, true, true>, ftcs_march43_kernel<1, true, true>, ftcs_march43_kernel<2, true, true>}}};
+    const uint32_t smem = smem43();
     static uint64_t attr_done = 0;
     const int dev = g->device;
     if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
@@ -3679,8 +3303,7 @@ void march42_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas42, kThreads42, smem, g->stream>>>(M, p.d_ctx, mux, muy, mdx,
-                                                                                        mdy);
+    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas43, kThreads43, smem, g->stream>>>(M, p.d_ctx, mux, mdx);
     PD_CUDA(cudaGetLastError());
 }
 
@@ -3707,7 +3330,7 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     M.n_all = g->n_chunks;
     static const int ver = [] {
         const char* e = getenv("PD_MARCH_V");
-        return e ? atoi(e) : 30;
+        return e ? atoi(e) : 43;
     }();
     using KernT = void (*)(MarchArgs);
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
@@ -3727,16 +3350,12 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
         march31_launch(g, p, M, r, pl != nullptr);
         return;
     }
-    if (ver == 40) {
-        march40_launch(g, p, M, r, pl != nullptr);
-        return;
-    }
     if (ver == 41) {
         march41_launch(g, p, M, r, pl != nullptr);
         return;
     }
-    if (ver == 42) {
-        march42_launch(g, p, M, r, pl != nullptr);
+    if (ver == 43) {
+        march43_launch(g, p, M, r, pl != nullptr);
         return;
     }
     static const int pf = [] {

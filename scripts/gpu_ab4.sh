@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 VARS=${VARS:-"30:5 31:0"}
 CANDS=${CANDS:-"31:0"}
-run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=""; PD_MARCH_V=$v PD_M30_CFG=${st:-5} PD_M31_CFG=${st:-0} "${@:2}"; }
+run() { local v=${1%%:*}; local st=${1#*:}; [ "$st" = "$1" ] && st=""; PD_MARCH_V=$v PD_M30_CFG=${st:-5} PD_M31_CFG=${st:-0} PD_M43_PF=${st:-3} "${@:2}"; }
 # a new kernel that hangs must not eat the call: 2-minute probe first, and
 # variants that fail it are dropped from the benches
 OK=""
