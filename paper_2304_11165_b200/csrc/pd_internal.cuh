@@ -242,6 +242,8 @@ void march_push_flags(pd_grid* g, MarchPlan& p, const int32_t* d_ord);
 // 3-D FP32 grids (pd_march32.cu)
 bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void** out, bool* half);
 void march32_launch(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction);
+// chunk schedule with bit 31 set on uniform chunks (pd_march.cu; built once per schedule)
+const int32_t* march_flagged_schedule(pd_grid* g, MarchPlan& p, const int32_t* sched, int64_t n);
 void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction, const int32_t* sched,
                           int64_t n, int* counter);
 int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end);

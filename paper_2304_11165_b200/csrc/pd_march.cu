@@ -56,6 +56,7 @@
 #include <cudaTypedefs.h>
 
 #include "pd_internal.cuh"
+#include "pd_async.cuh"
 
 namespace pdb {
 
@@ -103,9 +104,6 @@ struct MarchArgs {
 
 // Schedule entries carry bit 31 on uniform chunks (flagged_schedule); -1 ends.
 __device__ __forceinline__ int sched_id(int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); }
-__device__ __forceinline__ void prefetch_l2(const void* g, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
-}
 
 
 struct SlowConsts {
@@ -314,14 +312,6 @@ __device__ __forceinline__ void cp4(uint32_t sa, const void* g, bool pred) {
         "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
         " @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(sa),
         "l"(g), "r"((int)pred));
-}
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(a), "r"(v));
 }
 
 struct LoadCtx14 {
@@ -774,34 +764,6 @@ __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchAr
 constexpr uint32_t kBarOff20 = kRing14 * kTileBytes + 3 * kCtxBytes14;  // 8 mbarriers (8 B each)
 constexpr uint32_t kWarpBytes20 = kBarOff20 + 8u * kRing14;
 
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-// the lane's prior cp.async copies arrive on bar when they complete (the
-// pending count is raised first, so the phase waits for them)
-__device__ __forceinline__ void cp_mbar_arrive(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
 
 // Sources of one chunk's loads (element offsets; warp-uniform except the
 // x-halo fields).
@@ -1092,16 +1054,6 @@ constexpr uint32_t kStage30 = 14336 + 256;
 __host__ __device__ constexpr uint32_t bar30(int nst) { return (uint32_t)nst * kStage30; }  // full[nst] then empty[nst]
 __host__ __device__ constexpr uint32_t smem30(int nst) { return bar30(nst) + 16u * (uint32_t)nst; }
 
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tma4(uint32_t dst, const CUtensorMap* map, int x, int y, int z, int c, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-        "%5}], [%6];\n" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(c), "r"(bar)
-        : "memory");
-}
 
 // Shared-memory byte addresses (u side; D_eff at +kDHalf30) of one plane's
 // operands for the lane: own pair, z- / z+ pairs, y- / y+ pairs, x- / x+ cells.
@@ -1543,32 +1495,6 @@ __host__ __device__ constexpr int maxreg31(int cfg) {
 }
 constexpr int kB31 = 4;  // chunks claimed per atomic (producer batch)
 
-__device__ __forceinline__ void cp_mbar_arrive_noinc(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void cp8(uint32_t dst, const void* src, bool pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
-        " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(dst),
-        "l"(src), "r"((int)pred)
-        : "memory");
-}
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
-        " @p cp.async.cg.shared.global [%0], [%1], 16;\n}\n" ::"r"(dst),
-        "l"(src), "r"((int)pred)
-        : "memory");
-}
-__device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
-}
-__device__ __forceinline__ uint4 lds4(uint32_t a) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t pin(uint32_t v, int lane) { return __shfl_sync(0xffffffffu, v, lane); }
 
 // Rare path of one plane pair: everything (chunk record, operands) re-read
 // from the stage at st.
@@ -2780,7 +2706,7 @@ __global__ void push_flags_kernel(int32_t* __restrict__ desc, const int32_t* __r
 // v30 chunk records: lm[32] | desc[8] | dv (2 words) | 2 pad words, one
 // 176-B bulk copy per chunk
 __global__ void pack_ctx_kernel(const uint32_t* __restrict__ lm, const int32_t* __restrict__ desc,
-                                const uint32_t* __restrict__ dv, int64_t n, uint32_t* __restrict__ ctx) {
+                                const uint32_t* __restrict__ dv, int dvw, int64_t n, uint32_t* __restrict__ ctx) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n * 44) return;
     const int64_t c = i / 44;
@@ -2788,7 +2714,7 @@ __global__ void pack_ctx_kernel(const uint32_t* __restrict__ lm, const int32_t* 
     uint32_t v = 0;
     if (w < 32) v = lm[c * 32 + w];
     else if (w < 40) v = (uint32_t)desc[c * 8 + (w - 32)];
-    else if (w < 42) v = dv[c * 2 + (w - 40)];
+    else if (w < 40 + dvw) v = dv[c * dvw + (w - 40)];  // uniform D_eff: FP64 2 words, FP32 1
     ctx[i] = v;
 }
 
@@ -2796,7 +2722,7 @@ void march_pack_ctx(pd_grid* g, MarchPlan& p) {
     const int64_t n = g->n_chunks;
     if (!p.d_ctx) PD_CUDA(pd_malloc(&p.d_ctx, sizeof(uint32_t) * 44 * (size_t)n));
     pack_ctx_kernel<<<(unsigned)((n * 44 + 255) / 256), 256, 0, g->stream>>>(
-        p.d_lm, p.d_desc, static_cast<const uint32_t*>(p.d_dv), n, p.d_ctx);
+        p.d_lm, p.d_desc, static_cast<const uint32_t*>(p.d_dv), g->tbytes / 4, n, p.d_ctx);
     PD_CUDA(cudaGetLastError());
 }
 
@@ -3035,6 +2961,7 @@ void march_build(pd_grid* g, const int32_t* d_nbr, const uint64_t* d_fluid, cons
             return;
         }
         mark_uniform<unsigned>(g, plan, 0xFF800000u);
+        march_pack_ctx(g, *plan);
     } else {
         // one extra chunk of sentinels after the last one: the source of every
         // D_eff cell a plane load does not read from the grid (inactive pairs,
@@ -3151,6 +3078,10 @@ const int32_t* flagged_schedule(pd_grid* g, MarchPlan& p, const int32_t* sched, 
     }
     p.flagged.emplace_back(sched, d);
     return d;
+}
+
+const int32_t* march_flagged_schedule(pd_grid* g, MarchPlan& p, const int32_t* sched, int64_t n) {
+    return flagged_schedule(g, p, sched, n);
 }
 
 void march30_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {

@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "pd_internal.cuh"
+#include "pd_async.cuh"
 
 namespace pdb {
 
@@ -237,18 +238,23 @@ __device__ __forceinline__ void issue32(uint32_t st, const float* __restrict__ u
 
 // Rare path: Dirichlet-exposed chunk (whole chunk exact) or a non-finite fast
 // result (re-derived exactly), then the reference's error flags.
-template <int REACTION, bool HALF>
-__device__ __noinline__ float2 slow_pair32(const Args32& M, const Slow32& K, Ctx32 C, int z, uint32_t tm, uint32_t t0,
-                                           uint32_t tp, Geo32 G, float out0, float out1) {
-    const bool un = (C.flags & kFlagUnif32) != 0;  // no D_eff in the ring: every d is dv
+// shared-memory addresses (u side; D_eff at +DH) of a pair's operands
+struct Addr32 {
+    uint32_t c, l, r, ym, yp, zm, zp;
+};
+
+template <int REACTION, bool HALF, uint32_t DH>
+__device__ __noinline__ float2 slow_pair32a(const Args32& M, const Slow32& K, const Ctx32& C, int z, const Geo32& G,
+                                            Addr32 a, float out0, float out1) {
+    const bool un = (C.flags & kFlagUnif32) != 0;  // no D_eff staged: every d is dv
     const float2 vv = make_float2(C.dv, C.dv);
-    const float2 uc = lds2f(t0 + G.s_c), dc0 = un ? vv : lds2f(t0 + kDOff32 + G.s_c);
-    const float uL = lds1f(t0 + G.s_l), dL0 = un ? C.dv : lds1f(t0 + kDOff32 + G.s_l);
-    const float uR = lds1f(t0 + G.s_r), dR0 = un ? C.dv : lds1f(t0 + kDOff32 + G.s_r);
-    const float2 uym = lds2f(t0 + G.s_c - 32), dym0 = un ? vv : lds2f(t0 + kDOff32 + G.s_c - 32);
-    const float2 uyp = lds2f(t0 + G.s_c + 32), dyp0 = un ? vv : lds2f(t0 + kDOff32 + G.s_c + 32);
-    const float2 uzm = lds2f(tm + G.s_c), dzm0 = un ? vv : lds2f(tm + kDOff32 + G.s_c);
-    const float2 uzp = lds2f(tp + G.s_c), dzp0 = un ? vv : lds2f(tp + kDOff32 + G.s_c);
+    const float2 uc = lds2f(a.c), dc0 = un ? vv : lds2f(a.c + DH);
+    const float uL = lds1f(a.l), dL0 = un ? C.dv : lds1f(a.l + DH);
+    const float uR = lds1f(a.r), dR0 = un ? C.dv : lds1f(a.r + DH);
+    const float2 uym = lds2f(a.ym), dym0 = un ? vv : lds2f(a.ym + DH);
+    const float2 uyp = lds2f(a.yp), dyp0 = un ? vv : lds2f(a.yp + DH);
+    const float2 uzm = lds2f(a.zm), dzm0 = un ? vv : lds2f(a.zm + DH);
+    const float2 uzp = lds2f(a.zp), dzp0 = un ? vv : lds2f(a.zp + DH);
     auto dd = [](float h) { return HALF ? h + h : h; };  // D from D/2 (exact)
     auto dd2 = [&](float2 h) { return make_float2(dd(h.x), dd(h.y)); };
     const float2 dc = dd2(dc0), dym = dd2(dym0), dyp = dd2(dyp0), dzm = dd2(dzm0), dzp = dd2(dzp0);
@@ -286,6 +292,21 @@ __device__ __noinline__ float2 slow_pair32(const Args32& M, const Slow32& K, Ctx
         atomicOr(M.A.flags + M.A.k, 1);
     }
     return make_float2(out0, out1);
+}
+
+// the ring-tile rare path of ftcs_march32_kernel
+template <int REACTION, bool HALF>
+__device__ __forceinline__ float2 slow_pair32(const Args32& M, const Slow32& K, const Ctx32& C, int z, uint32_t tm,
+                                              uint32_t t0, uint32_t tp, const Geo32& G, float out0, float out1) {
+    Addr32 a;
+    a.c = t0 + G.s_c;
+    a.l = t0 + G.s_l;
+    a.r = t0 + G.s_r;
+    a.ym = t0 + G.s_c - 32;
+    a.yp = t0 + G.s_c + 32;
+    a.zm = tm + G.s_c;
+    a.zp = tp + G.s_c;
+    return slow_pair32a<REACTION, HALF, kDOff32>(M, K, C, z, G, a, out0, out1);
 }
 
 // Uniform chunk: every face coefficient is (dv + dv) * 0.5f (compute14u in
@@ -580,6 +601,356 @@ __global__ void deff32_kernel(const float* __restrict__ dcol, const uint64_t* __
     if (fl && (fabsf(v) < 0x1p-125f || fabsf(v) >= 0x1p126f)) atomicAdd(bad + 1, 1ull);
 }
 
+// ---------------------------------------------------------------------------
+// FP32 v43: the FP64 march v43 design (pd_march.cu) in float.
+// * CTA = 4 compute warps + 1 producer warp; the producer claims chunks four
+//   at a time and moves each chunk with per-lane cp.async into a padded stage
+//   (u half; D_eff at +kHalf32b): 10 planes z = -1..8 at a 320-B pitch (rows
+//   y = -1..8 of 32 B), then the x- halo block [z][y] (4-B cells) and, 32 B
+//   further (other banks), the x+ block; the 176-B chunk record is one bulk
+//   copy. Completion: lane 0's expect_tx + 32 cp.async arrivals on the
+//   stage's "full" mbarrier; the compute warps release it on "empty".
+// * Compute warp w: planes 2w, 2w+1; lane (y, xp): the x pair (2xp, 2xp+1)
+//   of row y as one 8-B word. z / y neighbours at -+320 / -+32 from the own
+//   pair, x neighbours by shuffle (face lanes: the halo cell); both planes in
+//   one straight-line block on a warp-uniform path (uniform chunk /
+//   interior-fluid planes / generic); one vote for the rare path
+//   (Dirichlet-exposed chunk or a non-finite result).
+// * float arithmetic in the reference's order (ftcs_march32_kernel's
+//   expressions): bitwise equal to the reference's T = float path.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPP32b = 320;                              // plane pitch
+constexpr uint32_t kXL32b = 10 * kPP32b, kXH32b = kXL32b + 288;  // x-halo blocks [z][y]
+constexpr uint32_t kHalf32b = kXH32b + 256;                   // D_eff half (3744)
+constexpr uint32_t kCtx32b = 2 * kHalf32b;                    // record; chunk id at +176
+constexpr uint32_t kStage32b = kCtx32b + 256;                 // 7744
+constexpr int kW32b = 4, kB32b = 4;
+constexpr int kThreads32b = 32 * (kW32b + 1);
+// configurations: CTAs per SM and stages per CTA
+__host__ __device__ constexpr int ctas32b(int cfg) { return cfg == 1 ? 5 : cfg == 2 ? 4 : 6; }
+__host__ __device__ constexpr int nst32b(int cfg) { return cfg == 0 ? 3 : 4; }
+__host__ __device__ constexpr int maxreg32b(int cfg) {
+    return 16384 / (32 * ((kThreads32b / 32 * ctas32b(cfg) + 3) / 4)) / 8 * 8;
+}
+__host__ __device__ constexpr uint32_t smem32b(int cfg) { return nst32b(cfg) * kStage32b + 16u * nst32b(cfg); }
+
+template <int REACTION, bool HALF>
+__device__ __noinline__ float2 pair_slow32b(const Args32& M, const Slow32& K, uint32_t st, int lane, int z, float out0,
+                                            float out1) {
+    Ctx32 C;
+    C.c = (int)ldsu(st + kCtx32b + 176u);
+    C.lm = ldsu(st + kCtx32b + 4u * (uint32_t)lane);
+    C.key = (int)ldsu(st + kCtx32b + 152u);
+    C.flags = (int)ldsu(st + kCtx32b + 156u);
+    C.dv = lds1f(st + kCtx32b + 160u);
+    Geo32 G = geo32(lane);
+    const uint32_t zz = (uint32_t)z, pz = st + (zz + 1u) * kPP32b;
+    Addr32 a;
+    a.c = pz + (uint32_t)(G.y + 1) * 32u + 8u * (uint32_t)G.xp;
+    a.zm = a.c - kPP32b;
+    a.zp = a.c + kPP32b;
+    a.ym = a.c - 32u;
+    a.yp = a.c + 32u;
+    a.l = G.xp > 0 ? a.c - 4u : st + kXL32b + zz * 32u + 4u * (uint32_t)G.y;
+    a.r = G.xp < 3 ? a.c + 8u : st + kXH32b + zz * 32u + 4u * (uint32_t)G.y;
+    return slow_pair32a<REACTION, HALF, kHalf32b>(M, K, C, z, G, a, out0, out1);
+}
+
+template <int REACTION>
+__device__ __forceinline__ float node32b(float dt, float neg_k, float sfac, float ix, float iy, float iz, float uc,
+                                         float fxm, float fxp, float fym, float fyp, float fzm, float fzp, bool sink,
+                                         float src) {
+    float lap = 0.0f;  // T lap = T(0) (solver.hpp:420)
+    lap += (fxp - fxm) * ix;
+    lap += (fyp - fym) * iy;
+    lap += (fzp - fzm) * iz;
+    float r = 0.0f;
+    if (REACTION == PD_REACTION_SURFACE_SINK) r = sink ? neg_k * uc : 0.0f;
+    else if (REACTION == PD_REACTION_VOLUMETRIC) r = src * sfac;
+    return uc + dt * lap + dt * r;
+}
+
+template <int REACTION, bool HALF, int CFG>
+__global__ void __maxnreg__(maxreg32b(CFG)) ftcs_march32b_kernel(const __grid_constant__ Args32 M,
+                                                                  const uint32_t* __restrict__ ctxa) {
+    extern __shared__ __align__(128) unsigned char smem32b_raw[];
+    __shared__ Slow32 K;
+    constexpr int kSt = nst32b(CFG);
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const StepArgs<float>& A = M.A;
+    if (A.k > 0) {
+        const int prev = A.flags[A.k - 1];
+        if (prev) {
+            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
+            return;
+        }
+    }
+    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem32b_raw);
+    const uint32_t full0 = sm0 + kSt * kStage32b, empty0 = full0 + 8u * kSt;
+    if (t == 0) {
+        for (int a = 0; a < 3; ++a) {
+            K.size[a] = A.size[a];
+            K.inv_dx2[a] = A.inv_dx2[a];
+        }
+        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
+        K.dt = A.dt;
+        K.neg_k = A.neg_k;
+        K.src_factor = A.src_factor;
+        K.dirichlet = A.dirichlet;
+        for (int s = 0; s < kSt; ++s) {
+            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 cp.async arrivals
+            mbar_init(empty0 + 8u * s, (uint32_t)kW32b);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const float* __restrict__ u = A.u;
+    const float* __restrict__ de = M.deff;
+    const int n = (int)M.n;
+
+    if (warp == kW32b) {  // ---------------- producer warp ----------------
+        int* ctr = M.counter;
+        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
+        const uint32_t sent_off = (uint32_t)M.n_all * 512u;  // D_eff sentinel chunk (elements)
+        auto claim = [&]() -> int {
+            int r = 0;
+            if (lane == 0)
+                asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(ctr), "r"(kB32b) : "memory");
+            return r;
+        };
+        auto entries = [&](int p0) -> int {
+            const int p = __shfl_sync(0xffffffffu, p0, 0) + lane;
+            return lane < kB32b && p < n ? __ldg(&M.sched[p]) : -1;
+        };
+        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
+        auto descs = [&](int e, int4& d0, int4& d1) {
+            const int c = chunk_of(e);
+            if (lane < kB32b && c >= 0) {
+                d0 = __ldg(desc4 + 2 * (int64_t)c);
+                d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
+            }
+        };
+        auto prefetch = [&](int e) {  // the batch's u slabs and records into L2
+            const int64_t c = (int64_t)chunk_of(e);
+            if (lane < kB32b && c >= 0) {
+                prefetch_l2(u + c * 512, 2048u);
+                prefetch_l2(ctxa + c * 44, 176u);
+            }
+        };
+        int e_c = entries(claim());
+        int e_n = entries(claim());
+        int p_nn = claim();
+        int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
+        descs(e_c, d0c, d1c);
+        prefetch(e_c);
+        const uint32_t L = (uint32_t)lane;
+        // own slab: 16-B pieces p = L + 32 i -> plane 2 i + L / 16, row (L % 16) / 2, half L % 2
+        const uint32_t d_own = ((L >> 4) + 1u) * kPP32b + (((L & 15u) >> 1) + 1u) * 32u + 16u * (L & 1u);
+        // z halos: lanes 0-15 the z- neighbour's plane 7 -> plane -1, lanes 16-31 the z+ one's plane 0 -> plane 8
+        const bool zh = L >= 16u;
+        const uint32_t Lq = L & 15u;
+        const uint32_t d_z = (zh ? 9u * kPP32b : 0u) + 32u + 16u * Lq, s_z = (zh ? 0u : 448u) + 4u * Lq;
+        // y halos: lanes 0-15 row 7 of the y- neighbour -> row -1, lanes 16-31 row 0 of the y+ one -> row 8
+        const uint32_t d_y = ((Lq >> 1) + 1u) * kPP32b + (zh ? 288u : 0u) + 16u * (L & 1u);
+        const uint32_t s_y = (Lq >> 1) * 64u + (zh ? 0u : 56u) + 4u * (L & 1u);
+        uint32_t s = 0, ph = 0, k = 0;
+#pragma unroll 1
+        for (;;) {
+            int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
+            descs(e_n, d0n, d1n);
+            prefetch(e_n);
+            const int e_nn = entries(p_nn);
+            p_nn = claim();
+            bool done = false;
+#pragma unroll 1
+            for (int j = 0; j < kB32b; ++j, ++k) {
+                const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
+                const uint32_t st = sm0 + s * kStage32b, full = full0 + 8u * s;
+                if (k >= (uint32_t)kSt) mbar_wait(empty0 + 8u * s, ph ^ 1u);
+                if (c_cur < 0) {  // end marker
+                    if (lane == 0) {
+                        sts_u32(st + kCtx32b + 176u, 0xFFFFFFFFu);
+                        mbar_arrive(full);
+                    }
+                    cp_mbar_arrive_noinc(full);
+                    done = true;
+                    break;
+                }
+                const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
+                const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
+                const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
+                const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif32);
+                if (lane == 0) {
+                    sts_u32(st + kCtx32b + 176u, (uint32_t)c_cur);
+                    mbar_arrive_tx(full, 176u);
+                    bulk_g2s(st + kCtx32b, ctxa + (int64_t)c_cur * 44, 176u, full);
+                }
+                const uint32_t so = (uint32_t)c_cur * 512u + 4u * L;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    cp16(st + d_own + 640u * (uint32_t)i, u + so + 128 * i, true);
+                    cp16(st + kHalf32b + d_own + 640u * (uint32_t)i, de + so + 128 * i, dl);
+                }
+                {
+                    const int nz = zh ? nb5 : nb4;
+                    const uint32_t oz = (uint32_t)nz * 512u + s_z;
+                    cp16(st + d_z, u + (nz >= 0 ? oz : 0u), nz >= 0);
+                    cp16(st + kHalf32b + d_z, de + (nz >= 0 ? oz : sent_off + s_z), dl);
+                    const int ny = zh ? nb3 : nb2;
+                    const uint32_t oy = (uint32_t)ny * 512u + s_y;
+                    cp16(st + d_y, u + (ny >= 0 ? oy : 0u), ny >= 0);
+                    cp16(st + kHalf32b + d_y, de + (ny >= 0 ? oy : sent_off + s_y), dl);
+                }
+                {  // x halos: cells (z, y) = L, L + 32 of column 7 of the x- / column 0 of the x+ neighbour
+                    const uint32_t xl = (uint32_t)nb0 * 512u + 8u * L + 7u, xh = (uint32_t)nb1 * 512u + 8u * L;
+                    const uint32_t xs = sent_off + 8u * L;
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const uint32_t o = 256u * (uint32_t)jj;  // +32 cells: 8 elements each
+                        cpa(st + kXL32b + 4u * L + 128u * (uint32_t)jj, u + (nb0 >= 0 ? xl + o : 0u), 0, nb0 >= 0);
+                        cpa(st + kXH32b + 4u * L + 128u * (uint32_t)jj, u + (nb1 >= 0 ? xh + o : 0u), 0, nb1 >= 0);
+                        cpa(st + kHalf32b + kXL32b + 4u * L + 128u * (uint32_t)jj, de + (nb0 >= 0 ? xl + o : xs + o), 0, dl);
+                        cpa(st + kHalf32b + kXH32b + 4u * L + 128u * (uint32_t)jj, de + (nb1 >= 0 ? xh + o : xs + o), 0, dl);
+                    }
+                }
+                cp_mbar_arrive_noinc(full);
+                if (++s == (uint32_t)kSt) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+            if (done) break;
+            e_c = e_n;
+            d0c = d0n;
+            d1c = d1n;
+            e_n = e_nn;
+        }
+        return;
+    }
+
+    // ---------------- compute warps ----------------
+    const float dt = A.dt, neg_k = A.neg_k, sfac = A.src_factor;
+    const float ix = A.inv_dx2[0], iy = A.inv_dx2[1], iz = A.inv_dx2[2];
+    const int y = lane >> 2, xp = lane & 3;
+    const uint32_t z0 = 2u * (uint32_t)warp;
+    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);
+    const uint32_t o_c = pin((z0 + 1u) * kPP32b + (uint32_t)(y + 1) * 32u + 8u * (uint32_t)xp, lane);
+    const uint32_t o_x = pin((xp == 3 ? kXH32b : kXL32b) + z0 * 32u + 4u * (uint32_t)y, lane);
+    const bool xlo = xp == 0, xhi = xp == 3;
+    const uint32_t zsh = 2u * z0;
+    float* __restrict__ un = A.un;
+    uint32_t s = 0, ph = 0;
+#pragma unroll 1
+    for (;;) {
+        mbar_wait(full0 + 8u * s, ph);
+        const uint32_t st = sm0 + s * kStage32b;
+        const int c = (int)ldsu(st + kCtx32b + 176u);
+        if (c < 0) break;
+        const uint32_t lm = ldsu(st + kCtx32b + 4u * (uint32_t)lane);
+        const int flags = (int)ldsu(st + kCtx32b + 156u);
+        const uint32_t ab = (lm >> zsh) & 0xFu;
+        const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
+        const uint32_t g_off = z0 * 64u + bp;
+        float src[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        if (REACTION == PD_REACTION_VOLUMETRIC) {
+            const float* sp = A.src + (int64_t)c * 512 + g_off;
+            src[0] = sp[0];
+            src[1] = sp[1];
+            src[2] = sp[64];
+            src[3] = sp[65];
+        }
+        const uint32_t a = st + o_c, ax = st + o_x;
+        const float2 uc0 = lds2f(a), uc1 = lds2f(a + kPP32b);
+        const float2 uzm = lds2f(a - kPP32b), uzp = lds2f(a + 2u * kPP32b);
+        const float2 uym0 = lds2f(a - 32u), uyp0 = lds2f(a + 32u);
+        const float2 uym1 = lds2f(a + kPP32b - 32u), uyp1 = lds2f(a + kPP32b + 32u);
+        const float uh0 = lds1f(ax), uh1 = lds1f(ax + 32u);
+        const float su0 = __shfl_up_sync(0xffffffffu, uc0.y, 1), sd0 = __shfl_down_sync(0xffffffffu, uc0.x, 1);
+        const float su1 = __shfl_up_sync(0xffffffffu, uc1.y, 1), sd1 = __shfl_down_sync(0xffffffffu, uc1.x, 1);
+        const float uL0 = xlo ? uh0 : su0, uR0 = xhi ? uh0 : sd0;
+        const float uL1 = xlo ? uh1 : su1, uR1 = xhi ? uh1 : sd1;
+        float o00, o01, o10, o11;
+        const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
+        if (flags & kFlagUnif32) {
+            const float dv = lds1f(st + kCtx32b + 160u);
+            const float dh = HALF ? dv + dv : (dv + dv) * 0.5f;
+            const float fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
+            const float f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
+            o00 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x),
+                                    dh * (uyp0.x - uc0.x), dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
+            o01 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y),
+                                    dh * (uyp0.y - uc0.y), dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
+            o10 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x),
+                                    dh * (uyp1.x - uc1.x), fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
+            o11 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y),
+                                    dh * (uyp1.y - uc1.y), fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
+        } else {
+            const uint32_t b = a + kHalf32b, bx = ax + kHalf32b;
+            const float2 dc0 = lds2f(b), dc1 = lds2f(b + kPP32b);
+            const float2 dzm = lds2f(b - kPP32b), dzp = lds2f(b + 2u * kPP32b);
+            const float2 dym0 = lds2f(b - 32u), dyp0 = lds2f(b + 32u);
+            const float2 dym1 = lds2f(b + kPP32b - 32u), dyp1 = lds2f(b + kPP32b + 32u);
+            const float dh0 = lds1f(bx), dh1 = lds1f(bx + 32u);
+            const float tu0 = __shfl_up_sync(0xffffffffu, dc0.y, 1), td0 = __shfl_down_sync(0xffffffffu, dc0.x, 1);
+            const float tu1 = __shfl_up_sync(0xffffffffu, dc1.y, 1), td1 = __shfl_down_sync(0xffffffffu, dc1.x, 1);
+            const float dL0 = xlo ? dh0 : tu0, dR0 = xhi ? dh0 : td0;
+            const float dL1 = xlo ? dh1 : tu1, dR1 = xhi ? dh1 : td1;
+#define PD_F32B(F)                                                                                                  \
+    {                                                                                                               \
+        const float fzx = F(dc0.x, dc1.x, uc0.x, uc1.x), fzy = F(dc0.y, dc1.y, uc0.y, uc1.y);                       \
+        const float f0i = F(dc0.x, dc0.y, uc0.x, uc0.y), f1i = F(dc1.x, dc1.y, uc1.x, uc1.y);                       \
+        o00 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.x, F(dL0, dc0.x, uL0, uc0.x), f0i,                  \
+                                F(dym0.x, dc0.x, uym0.x, uc0.x), F(dc0.x, dyp0.x, uc0.x, uyp0.x),                    \
+                                F(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);                                \
+        o01 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.y, f0i, F(dc0.y, dR0, uc0.y, uR0),                  \
+                                F(dym0.y, dc0.y, uym0.y, uc0.y), F(dc0.y, dyp0.y, uc0.y, uyp0.y),                    \
+                                F(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);                                \
+        o10 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.x, F(dL1, dc1.x, uL1, uc1.x), f1i,                  \
+                                F(dym1.x, dc1.x, uym1.x, uc1.x), F(dc1.x, dyp1.x, uc1.x, uyp1.x), fzx,               \
+                                F(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);                                     \
+        o11 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.y, f1i, F(dc1.y, dR1, uc1.y, uR1),                  \
+                                F(dym1.y, dc1.y, uym1.y, uc1.y), F(dc1.y, dyp1.y, uc1.y, uyp1.y), fzy,               \
+                                F(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);                                     \
+    }
+            if (ib == 3u) {
+                PD_F32B(fface32<HALF>)
+            } else {
+                PD_F32B(face32<HALF>)
+                if (sent32(dc0.x)) o00 = uc0.x;  // walls (solver.hpp:413-417)
+                if (sent32(dc0.y)) o01 = uc0.y;
+                if (sent32(dc1.x)) o10 = uc1.x;
+                if (sent32(dc1.y)) o11 = uc1.y;
+            }
+#undef PD_F32B
+        }
+        // rare path: Dirichlet-exposed chunk or a non-finite result (inactive
+        // slots keep u there: a non-finite one only costs the re-check)
+        const uint32_t em = max(max(__float_as_uint(o00) & 0x7f800000u, __float_as_uint(o01) & 0x7f800000u),
+                                max(__float_as_uint(o10) & 0x7f800000u, __float_as_uint(o11) & 0x7f800000u));
+        const bool slow = (flags & kFlagDir32) || em == 0x7f800000u;
+        if (__any_sync(0xffffffffu, slow)) {
+            if (slow) {
+                const float2 r0 = pair_slow32b<REACTION, HALF>(M, K, st, lane, (int)z0, o00, o01);
+                const float2 r1 = pair_slow32b<REACTION, HALF>(M, K, st, lane, (int)z0 + 1, o10, o11);
+                o00 = r0.x;
+                o01 = r0.y;
+                o10 = r1.x;
+                o11 = r1.y;
+            }
+        }
+        float* gp = un + ((uint32_t)c * 512u + g_off);
+        stg2f(gp, o00, o01, ab & 1u, ab & 2u);
+        stg2f(gp + 64, o10, o11, ab & 4u, ab & 8u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8u * s);
+        if (++s == (uint32_t)kSt) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
 }  // namespace
 
 // D_eff of a float grid (+ trailing sentinel chunk); returns false if a fluid
@@ -615,6 +986,32 @@ bool march32_deff(pd_grid* g, const void* d_dcol, const uint64_t* d_fluid, void*
     return true;
 }
 
+void march32b_launch(pd_grid* g, MarchPlan& p, const Args32& M, int r) {
+    using KB = void (*)(const Args32, const uint32_t*);
+#define PD_T(C)                                                                                                  \
+    {{ftcs_march32b_kernel<0, false, C>, ftcs_march32b_kernel<1, false, C>, ftcs_march32b_kernel<2, false, C>},  \
+     {ftcs_march32b_kernel<0, true, C>, ftcs_march32b_kernel<1, true, C>, ftcs_march32b_kernel<2, true, C>}}
+    static const KB tabs[3][2][3] = {PD_T(0), PD_T(1), PD_T(2)};
+#undef PD_T
+    static const int cfg = [] {
+        const char* e = getenv("PD_M32B_CFG");
+        const int v = e ? atoi(e) : 0;
+        return v >= 0 && v <= 2 ? v : 0;
+    }();
+    const uint32_t smem = cfg == 1 ? smem32b(1) : cfg == 2 ? smem32b(2) : smem32b(0);
+    const int ctas = cfg == 1 ? ctas32b(1) : cfg == 2 ? ctas32b(2) : ctas32b(0);
+    static uint64_t attr_done[3] = {0, 0, 0};
+    if (!((attr_done[cfg] >> g->device) & 1u)) {
+        for (auto& row : tabs[cfg])
+            for (auto kf : row) PD_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done[cfg] |= 1ull << g->device;
+    }
+    int sms = 148;
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+    tabs[cfg][p.half ? 1 : 0][r]<<<sms * ctas, kThreads32b, smem, g->stream>>>(M, p.d_ctx);
+    PD_CUDA(cudaGetLastError());
+}
+
 void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, int reaction, const int32_t* sched,
                           int64_t n, int* counter) {
     Args32 M;
@@ -628,6 +1025,16 @@ void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, in
     M.counter = counter;
     M.zero = 0;
     M.n_all = g->n_chunks;
+    const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
+    static const int ver = [] {
+        const char* e = getenv("PD_MARCH32_V");
+        return e ? atoi(e) : 43;
+    }();
+    if (ver == 43 && p.d_ctx) {
+        M.sched = march_flagged_schedule(g, p, sched, n);
+        march32b_launch(g, p, M, r);
+        return;
+    }
     using KernT = void (*)(Args32);
     static const KernT table[2][3] = {
         {ftcs_march32_kernel<0, false>, ftcs_march32_kernel<1, false>, ftcs_march32_kernel<2, false>},
@@ -643,7 +1050,6 @@ void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, in
     }
     int sms = 148;
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
-    const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
     table[p.half ? 1 : 0][r]<<<sms * kCtas32, kT32, bytes, g->stream>>>(M);
     PD_CUDA(cudaGetLastError());
 }
