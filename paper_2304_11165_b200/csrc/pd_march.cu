@@ -2540,6 +2540,20 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
     }
 
     // ---------------- compute warps ----------------
+    if (M.dbg & 8) {  // measurement only (PD_MARCH_DBG=8): release every stage unread (the copy pipeline alone)
+        uint32_t s = 0, ph = 0;
+        for (;;) {
+            mbar_wait(full0 + 8u * s, ph);
+            if ((int)lds_u32(sm0 + s * kStage43 + kCtx43 + 176u) < 0) break;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8u * s);
+            if (++s == (uint32_t)kSt43) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        return;
+    }
     Consts Q;
     Q.dt = A.dt;
     Q.neg_k = A.neg_k;
