@@ -117,6 +117,23 @@ __device__ __forceinline__ T min_ref(T a, T b) {  // std::min: (b < a) ? b : a
     return (b < a) ? b : a;
 }
 
+// x, or 1 where `one` holds, through an opaque select (inline PTX): the
+// compiler cannot fold it into the surrounding select, so a square root /
+// division fed with it never sees the zero that sends the library routine
+// down its out-of-line special-case path
+__device__ __forceinline__ double or_one(double x, bool one) {
+    double r;
+    asm("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n selp.f64 %0, 0d3FF0000000000000, %1, p;\n}\n"
+        : "=d"(r) : "d"(x), "r"((unsigned)one));
+    return r;
+}
+__device__ __forceinline__ float or_one(float x, bool one) {
+    float r;
+    asm("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n selp.f32 %0, 0f3F800000, %1, p;\n}\n"
+        : "=f"(r) : "f"(x), "r"((unsigned)one));
+    return r;
+}
+
 // detail::godunov_axis_sq (levelset.hpp:43-53)
 template <class T>
 __device__ __forceinline__ T godunov_sq(T dm, T dp, bool pos) {
@@ -181,10 +198,12 @@ __global__ void __launch_bounds__(256)
             if (!has_p) dp = dm;
             sum += godunov_sq(dm, dp, pos);
         }
-        // sqrt(+0) = +0: skip the library sqrt's special-case path (same bits)
-        const T grad = sum == T(0) ? T(0) : sqrt(sum);
+        // the zero cases are selected; the routines see a dummy 1 there (see
+        // sussman_zmarch_kernel)
+        const bool zs = sum == T(0), zc = c == T(0);
+        const T grad = zs ? T(0) : sqrt(or_one(sum, zs));
         // smoothed_sign (levelset.hpp:30-34): phi / sqrt(phi^2 + |g|^2 h^2)
-        const T ss = (c == T(0)) ? T(0) : c / sqrt(c * c + grad * grad * K.h * K.h);
+        const T ss = zc ? T(0) : c / sqrt(or_one(c * c + grad * grad * K.h * K.h, zc));
         const T update = K.dt * ss * (T(1) - grad);
         next[f] = c + update;
         if (fabs(c) <= K.band) local = fabs(update);
@@ -253,7 +272,15 @@ __global__ void __launch_bounds__(256)
     typename Bits<T>::U lb = 0;
     const bool pos_x_m = x > 0, pos_x_p = x + 1 < g.n[0];
     const bool pos_y_m = y > 0, pos_y_p = y + 1 < g.n[1];
-    for (int64_t z = z0; z < z1; ++z) {
+    // running pointers (no 64-bit index arithmetic per plane): the own column
+    // kAheadZ+1 planes ahead, the halo columns kAheadZ ahead, the output plane
+    const T* pq = phi + (inb ? col : 0) + (z0 + kAheadZ + 1) * g.s2;
+    const T* phx = phi + (hx_ok ? hx_col : 0) + (z0 + kAheadZ) * g.s2;
+    const T* phy = phi + (hy_ok ? hy_col : 0) + (z0 + kAheadZ) * g.s2;
+    T* pn = next + (inb ? col : 0) + z0 * g.s2;
+    const int64_t s2 = g.s2;
+    int64_t left = nz - z0;  // planes from z to the box end
+    for (int64_t z = z0; z < z1; ++z, pq += s2, phx += s2, phy += s2, pn += s2, --left) {
         const T c = q[1];
         __syncthreads();  // the previous plane's readers are done
         tile[ty + 1][tx + 1] = c;
@@ -261,9 +288,9 @@ __global__ void __launch_bounds__(256)
         if (hy) tile[ty == 0 ? 0 : 9][tx + 1] = hyq[0];
         __syncthreads();
         // refill the pipelines (plane z+kAheadZ+1 own, z+kAheadZ halos)
-        const T nq = ld_or0(phi, col + (z + kAheadZ + 1) * g.s2, inb && z + kAheadZ + 1 < nz);
-        const T nhx = ld_or0(phi, hx_col + (z + kAheadZ) * g.s2, hx_ok && z + kAheadZ < nz);
-        const T nhy = ld_or0(phi, hy_col + (z + kAheadZ) * g.s2, hy_ok && z + kAheadZ < nz);
+        const T nq = (inb && left > kAheadZ + 1) ? __ldg(pq) : T(0);
+        const T nhx = (hx_ok && left > kAheadZ) ? __ldg(phx) : T(0);
+        const T nhy = (hy_ok && left > kAheadZ) ? __ldg(phy) : T(0);
         if (inb) {
             const bool pos = !(c < T(0));
             T sum = T(0);
@@ -292,12 +319,16 @@ __global__ void __launch_bounds__(256)
                 if (!has_p) dp = dm;
                 sum += godunov_sq(dm, dp, pos);
             }
-            // sqrt(+0) = +0: skip the library sqrt's special-case path (same bits)
-            const T grad = sum == T(0) ? T(0) : sqrt(sum);
+            // sqrt(+0) = +0 and smoothed_sign(0) = 0 are selected, and the
+            // square roots / division then see a dummy 1 instead of the zero:
+            // the library routines' special-case (out-of-line) path is never
+            // taken for those nodes (a select alone still evaluates them)
+            const bool zs = sum == T(0), zc = c == T(0);
+            const T grad = zs ? T(0) : sqrt(or_one(sum, zs));
             // smoothed_sign (levelset.hpp:30-34): phi / sqrt(phi^2 + |g|^2 h^2)
-            const T ss = (c == T(0)) ? T(0) : c / sqrt(c * c + grad * grad * K.h * K.h);
+            const T ss = zc ? T(0) : c / sqrt(or_one(c * c + grad * grad * K.h * K.h, zc));
             const T update = K.dt * ss * (T(1) - grad);
-            next[col + z * g.s2] = c + update;
+            *pn = c + update;
             if (fabs(c) <= K.band) {
                 const typename Bits<T>::U ub = Bits<T>::of(fabs(update));
                 lb = ub > lb ? ub : lb;
