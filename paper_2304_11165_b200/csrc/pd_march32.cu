@@ -55,6 +55,7 @@ struct Args32 {
     int* counter;
     int zero;
     int64_t n_all;
+    int dbg;  // measurement only (PD_MARCH_DBG): 8 = compute warps release every stage unread
 };
 
 struct Slow32 {
@@ -830,6 +831,20 @@ __global__ void __maxnreg__(maxreg32b(CFG)) ftcs_march32b_kernel(const __grid_co
     }
 
     // ---------------- compute warps ----------------
+    if (M.dbg & 8) {  // measurement only: the copy pipeline alone
+        uint32_t s = 0, ph = 0;
+        for (;;) {
+            mbar_wait(full0 + 8u * s, ph);
+            if ((int)ldsu(sm0 + s * kStage32b + kCtx32b + 176u) < 0) break;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8u * s);
+            if (++s == (uint32_t)kSt) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        return;
+    }
     const float dt = A.dt, neg_k = A.neg_k, sfac = A.src_factor;
     const float ix = A.inv_dx2[0], iy = A.inv_dx2[1], iz = A.inv_dx2[2];
     const int y = lane >> 2, xp = lane & 3;
@@ -1025,6 +1040,11 @@ void march32_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<float>& a, in
     M.counter = counter;
     M.zero = 0;
     M.n_all = g->n_chunks;
+    static const int dbg = [] {
+        const char* e = getenv("PD_MARCH_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    M.dbg = dbg;
     const int r = reaction == PD_REACTION_SURFACE_SINK ? 1 : reaction == PD_REACTION_VOLUMETRIC ? 2 : 0;
     static const int ver = [] {
         const char* e = getenv("PD_MARCH32_V");
