@@ -1530,6 +1530,9 @@ __device__ __forceinline__ double node31(const Consts& Q, double uc, double fxm,
     lap += (fxp - fxm) * Q.ix;
     lap += (fyp - fym) * Q.iy;
     lap += (fzp - fzm) * Q.iz;
+    // no reaction: dt * 0 is +0 (dt is validated positive and finite,
+    // solver.hpp:305), so the reference's u + dt*lap + dt*r is u + dt*lap + 0
+    if (REACTION == PD_REACTION_NONE) return uc + Q.dt * lap + 0.0;
     double r = 0.0;
     if (REACTION == PD_REACTION_SURFACE_SINK) r = sink ? Q.neg_k * uc : 0.0;
     else if (REACTION == PD_REACTION_VOLUMETRIC) r = src * Q.src_factor;
@@ -2613,6 +2616,19 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
             const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
             const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
             const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
+            // no sink node in the warp's planes (uniform chunks lie inside the
+            // pores): the reaction term is +0 for every node
+            constexpr int RU = REACTION == PD_REACTION_SURFACE_SINK ? PD_REACTION_NONE : REACTION;
+            if (REACTION == PD_REACTION_SURFACE_SINK && !__any_sync(0xffffffffu, sk != 0u)) {
+                o00 = node31<RU>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
+                                 dh * (uc0.x - uzm.x), fzx, false, 0.0);
+                o01 = node31<RU>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
+                                 dh * (uc0.y - uzm.y), fzy, false, 0.0);
+                o10 = node31<RU>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x), fzx,
+                                 dh * (uzp.x - uc1.x), false, 0.0);
+                o11 = node31<RU>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y), fzy,
+                                 dh * (uzp.y - uc1.y), false, 0.0);
+            } else {
             o00 = node31<REACTION>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
                                    dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
             o01 = node31<REACTION>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
@@ -2621,6 +2637,7 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
                                    fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
             o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
                                    fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
+            }
         } else {
             const uint32_t b = a + kHalf43, bx = ax + kHalf43;
             const double2 dc0 = lds2(b), dc1 = lds2(b + kPP43);
