@@ -573,7 +573,7 @@ __device__ __forceinline__ void compute14(const MarchArgs& M, const SlowConsts& 
 
 template <int REACTION, bool PUSH, bool HALF>
 __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march14_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
@@ -845,7 +845,7 @@ __device__ __forceinline__ void issue20(uint32_t st, uint32_t bar, const double*
 
 template <int REACTION, bool PUSH, bool HALF>
 __global__ void __launch_bounds__(kThreads, kCtas14) ftcs_march20_kernel(MarchArgs M) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ SlowConsts K;
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
