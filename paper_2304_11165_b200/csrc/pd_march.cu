@@ -2354,6 +2354,17 @@ __device__ __noinline__ double2 pair_slow43(const MarchArgs& M, const SlowConsts
     return pair_slow30<REACTION, HALF, kHalf43>(M, K, C, z, xp, y, bp, a, out0, out1);
 }
 
+// u + dt * lap of one node (solver.hpp:420-441 without the reaction term,
+// which ftcs_march43_kernel adds per warp)
+__device__ __forceinline__ double node31x(const Consts& Q, double uc, double fxm, double fxp, double fym, double fyp,
+                                          double fzm, double fzp) {
+    double lap = 0.0;
+    lap += (fxp - fxm) * Q.ix;
+    lap += (fyp - fym) * Q.iy;
+    lap += (fzp - fzm) * Q.iz;
+    return uc + Q.dt * lap;
+}
+
 template <int REACTION, bool PUSH, bool HALF>
 __global__ void __launch_bounds__(kThreads43, kCtas43)
     ftcs_march43_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
@@ -2609,35 +2620,22 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
         const double uL1 = xlo ? uh1 : su1, uR1 = xhi ? uh1 : sd1;
         const double2 uym0 = lds2(a - 64u), uyp0 = lds2(a + 64u);
         const double2 uym1 = lds2(a + kPP43 - 64u), uyp1 = lds2(a + kPP43 + 64u);
-        double o00, o01, o10, o11;
+        double o00, o01, o10, o11;  // u + dt * lap first, the reaction term below
+        bool w00 = false, w01 = false, w10 = false, w11 = false;
         const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
         if (flags & kFlagUnif) {
             const double dv = lds1(st + kCtx43 + 160u);
             const double dh = HALF ? dv + dv : (dv + dv) * 0.5;
             const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
             const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
-            // no sink node in the warp's planes (uniform chunks lie inside the
-            // pores): the reaction term is +0 for every node
-            constexpr int RU = REACTION == PD_REACTION_SURFACE_SINK ? PD_REACTION_NONE : REACTION;
-            if (REACTION == PD_REACTION_SURFACE_SINK && !__any_sync(0xffffffffu, sk != 0u)) {
-                o00 = node31<RU>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
-                                 dh * (uc0.x - uzm.x), fzx, false, 0.0);
-                o01 = node31<RU>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
-                                 dh * (uc0.y - uzm.y), fzy, false, 0.0);
-                o10 = node31<RU>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x), fzx,
-                                 dh * (uzp.x - uc1.x), false, 0.0);
-                o11 = node31<RU>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y), fzy,
-                                 dh * (uzp.y - uc1.y), false, 0.0);
-            } else {
-            o00 = node31<REACTION>(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
-                                   dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
-            o01 = node31<REACTION>(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
-                                   dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
-            o10 = node31<REACTION>(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
-                                   fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
-            o11 = node31<REACTION>(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
-                                   fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
-            }
+            o00 = node31x(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
+                                   dh * (uc0.x - uzm.x), fzx);
+            o01 = node31x(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
+                                   dh * (uc0.y - uzm.y), fzy);
+            o10 = node31x(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
+                                   fzx, dh * (uzp.x - uc1.x));
+            o11 = node31x(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
+                                   fzy, dh * (uzp.y - uc1.y));
         } else {
             const uint32_t b = a + kHalf43, bx = ax + kHalf43;
             const double2 dc0 = lds2(b), dc1 = lds2(b + kPP43);
@@ -2652,39 +2650,62 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
             if (ib == 3u) {
                 const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
                 const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
-                o00 = node31<REACTION>(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                o00 = node31x(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
                                        fface<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), fface<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
-                                       fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
-                o01 = node31<REACTION>(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx);
+                o01 = node31x(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
                                        fface<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), fface<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
-                                       fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
-                o10 = node31<REACTION>(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy);
+                o10 = node31x(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
                                        fface<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), fface<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
-                                       fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
-                o11 = node31<REACTION>(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x));
+                o11 = node31x(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
                                        fface<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), fface<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
-                                       fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
+                                       fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y));
             } else {
                 const double fzx = face<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = face<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
                 const double f0i = face<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = face<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
-                o00 = node31<REACTION>(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
+                o00 = node31x(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
                                        face<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), face<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
-                                       face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);
-                o01 = node31<REACTION>(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
+                                       face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx);
+                o01 = node31x(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
                                        face<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), face<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
-                                       face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);
-                o10 = node31<REACTION>(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
+                                       face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy);
+                o10 = node31x(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
                                        face<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), face<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
-                                       fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);
-                o11 = node31<REACTION>(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
+                                       fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x));
+                o11 = node31x(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
                                        face<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), face<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
-                                       fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);
-                if (sentinel(dc0.x)) o00 = uc0.x;
-                if (sentinel(dc0.y)) o01 = uc0.y;
-                if (sentinel(dc1.x)) o10 = uc1.x;
-                if (sentinel(dc1.y)) o11 = uc1.y;
+                                       fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y));
+                w00 = sentinel(dc0.x);  // walls (solver.hpp:413-417), applied after the reaction term
+                w01 = sentinel(dc0.y);
+                w10 = sentinel(dc1.x);
+                w11 = sentinel(dc1.y);
             }
         }
+        // + dt * r (solver.hpp:437-441): r = 0 on nodes without a reaction, and
+        // dt * 0 = +0 (dt validated positive and finite), so warps without a
+        // sink node add +0 and skip the two products
+        if (REACTION == PD_REACTION_SURFACE_SINK && __any_sync(0xffffffffu, sk != 0u)) {
+            o00 = o00 + Q.dt * ((sk & 1u) ? Q.neg_k * uc0.x : 0.0);
+            o01 = o01 + Q.dt * ((sk & 2u) ? Q.neg_k * uc0.y : 0.0);
+            o10 = o10 + Q.dt * ((sk & 4u) ? Q.neg_k * uc1.x : 0.0);
+            o11 = o11 + Q.dt * ((sk & 8u) ? Q.neg_k * uc1.y : 0.0);
+        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+            o00 = o00 + Q.dt * (src[0] * Q.src_factor);
+            o01 = o01 + Q.dt * (src[1] * Q.src_factor);
+            o10 = o10 + Q.dt * (src[2] * Q.src_factor);
+            o11 = o11 + Q.dt * (src[3] * Q.src_factor);
+        } else {
+            o00 = o00 + 0.0;
+            o01 = o01 + 0.0;
+            o10 = o10 + 0.0;
+            o11 = o11 + 0.0;
+        }
+        if (w00) o00 = uc0.x;
+        if (w01) o01 = uc0.y;
+        if (w10) o10 = uc1.x;
+        if (w11) o11 = uc1.y;
         const uint32_t hm = max(max((uint32_t)__double2hiint(o00) & 0x7fffffffu, (uint32_t)__double2hiint(o01) & 0x7fffffffu),
                                 max((uint32_t)__double2hiint(o10) & 0x7fffffffu, (uint32_t)__double2hiint(o11) & 0x7fffffffu));
         const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
