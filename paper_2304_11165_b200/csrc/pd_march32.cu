@@ -671,6 +671,16 @@ __device__ __forceinline__ float node32b(float dt, float neg_k, float sfac, floa
     return uc + dt * lap + dt * r;
 }
 
+// u + dt * lap of one node in float (the reaction term is added per warp)
+__device__ __forceinline__ float node32bx(float dt, float ix, float iy, float iz, float uc, float fxm, float fxp,
+                                          float fym, float fyp, float fzm, float fzp) {
+    float lap = 0.0f;  // T lap = T(0) (solver.hpp:420)
+    lap += (fxp - fxm) * ix;
+    lap += (fyp - fym) * iy;
+    lap += (fzp - fzm) * iz;
+    return uc + dt * lap;
+}
+
 template <int REACTION, bool HALF, int CFG>
 __global__ void __maxnreg__(maxreg32b(CFG)) ftcs_march32b_kernel(const __grid_constant__ Args32 M,
                                                                   const uint32_t* __restrict__ ctxa) {
@@ -846,6 +856,7 @@ __global__ void __maxnreg__(maxreg32b(CFG)) ftcs_march32b_kernel(const __grid_co
         return;
     }
     const float dt = A.dt, neg_k = A.neg_k, sfac = A.src_factor;
+    const bool dt_fin = isfinite(dt);  // the float dt (positive; inf only if the double dt exceeds FLT_MAX)
     const float ix = A.inv_dx2[0], iy = A.inv_dx2[1], iz = A.inv_dx2[2];
     const int y = lane >> 2, xp = lane & 3;
     const uint32_t z0 = 2u * (uint32_t)warp;
@@ -885,21 +896,22 @@ __global__ void __maxnreg__(maxreg32b(CFG)) ftcs_march32b_kernel(const __grid_co
         const float su1 = __shfl_up_sync(0xffffffffu, uc1.y, 1), sd1 = __shfl_down_sync(0xffffffffu, uc1.x, 1);
         const float uL0 = xlo ? uh0 : su0, uR0 = xhi ? uh0 : sd0;
         const float uL1 = xlo ? uh1 : su1, uR1 = xhi ? uh1 : sd1;
-        float o00, o01, o10, o11;
+        float o00, o01, o10, o11;  // u + dt * lap first, the reaction term below
+        bool w00 = false, w01 = false, w10 = false, w11 = false;
         const uint32_t ib = ((uint32_t)flags >> (8u + z0)) & 3u;
         if (flags & kFlagUnif32) {
             const float dv = lds1f(st + kCtx32b + 160u);
             const float dh = HALF ? dv + dv : (dv + dv) * 0.5f;
             const float fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
             const float f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
-            o00 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x),
-                                    dh * (uyp0.x - uc0.x), dh * (uc0.x - uzm.x), fzx, sk & 1u, src[0]);
-            o01 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y),
-                                    dh * (uyp0.y - uc0.y), dh * (uc0.y - uzm.y), fzy, sk & 2u, src[1]);
-            o10 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x),
-                                    dh * (uyp1.x - uc1.x), fzx, dh * (uzp.x - uc1.x), sk & 4u, src[2]);
-            o11 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y),
-                                    dh * (uyp1.y - uc1.y), fzy, dh * (uzp.y - uc1.y), sk & 8u, src[3]);
+            o00 = node32bx(dt, ix, iy, iz, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x),
+                                    dh * (uyp0.x - uc0.x), dh * (uc0.x - uzm.x), fzx);
+            o01 = node32bx(dt, ix, iy, iz, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y),
+                                    dh * (uyp0.y - uc0.y), dh * (uc0.y - uzm.y), fzy);
+            o10 = node32bx(dt, ix, iy, iz, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x),
+                                    dh * (uyp1.x - uc1.x), fzx, dh * (uzp.x - uc1.x));
+            o11 = node32bx(dt, ix, iy, iz, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y),
+                                    dh * (uyp1.y - uc1.y), fzy, dh * (uzp.y - uc1.y));
         } else {
             const uint32_t b = a + kHalf32b, bx = ax + kHalf32b;
             const float2 dc0 = lds2f(b), dc1 = lds2f(b + kPP32b);
@@ -915,30 +927,57 @@ __global__ void __maxnreg__(maxreg32b(CFG)) ftcs_march32b_kernel(const __grid_co
     {                                                                                                               \
         const float fzx = F(dc0.x, dc1.x, uc0.x, uc1.x), fzy = F(dc0.y, dc1.y, uc0.y, uc1.y);                       \
         const float f0i = F(dc0.x, dc0.y, uc0.x, uc0.y), f1i = F(dc1.x, dc1.y, uc1.x, uc1.y);                       \
-        o00 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.x, F(dL0, dc0.x, uL0, uc0.x), f0i,                  \
+        o00 = node32bx(dt, ix, iy, iz, uc0.x, F(dL0, dc0.x, uL0, uc0.x), f0i,                  \
                                 F(dym0.x, dc0.x, uym0.x, uc0.x), F(dc0.x, dyp0.x, uc0.x, uyp0.x),                    \
-                                F(dzm.x, dc0.x, uzm.x, uc0.x), fzx, sk & 1u, src[0]);                                \
-        o01 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc0.y, f0i, F(dc0.y, dR0, uc0.y, uR0),                  \
+                                F(dzm.x, dc0.x, uzm.x, uc0.x), fzx);                                \
+        o01 = node32bx(dt, ix, iy, iz, uc0.y, f0i, F(dc0.y, dR0, uc0.y, uR0),                  \
                                 F(dym0.y, dc0.y, uym0.y, uc0.y), F(dc0.y, dyp0.y, uc0.y, uyp0.y),                    \
-                                F(dzm.y, dc0.y, uzm.y, uc0.y), fzy, sk & 2u, src[1]);                                \
-        o10 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.x, F(dL1, dc1.x, uL1, uc1.x), f1i,                  \
+                                F(dzm.y, dc0.y, uzm.y, uc0.y), fzy);                                \
+        o10 = node32bx(dt, ix, iy, iz, uc1.x, F(dL1, dc1.x, uL1, uc1.x), f1i,                  \
                                 F(dym1.x, dc1.x, uym1.x, uc1.x), F(dc1.x, dyp1.x, uc1.x, uyp1.x), fzx,               \
-                                F(dc1.x, dzp.x, uc1.x, uzp.x), sk & 4u, src[2]);                                     \
-        o11 = node32b<REACTION>(dt, neg_k, sfac, ix, iy, iz, uc1.y, f1i, F(dc1.y, dR1, uc1.y, uR1),                  \
+                                F(dc1.x, dzp.x, uc1.x, uzp.x));                                     \
+        o11 = node32bx(dt, ix, iy, iz, uc1.y, f1i, F(dc1.y, dR1, uc1.y, uR1),                  \
                                 F(dym1.y, dc1.y, uym1.y, uc1.y), F(dc1.y, dyp1.y, uc1.y, uyp1.y), fzy,               \
-                                F(dc1.y, dzp.y, uc1.y, uzp.y), sk & 8u, src[3]);                                     \
+                                F(dc1.y, dzp.y, uc1.y, uzp.y));                                     \
     }
             if (ib == 3u) {
                 PD_F32B(fface32<HALF>)
             } else {
                 PD_F32B(face32<HALF>)
-                if (sent32(dc0.x)) o00 = uc0.x;  // walls (solver.hpp:413-417)
-                if (sent32(dc0.y)) o01 = uc0.y;
-                if (sent32(dc1.x)) o10 = uc1.x;
-                if (sent32(dc1.y)) o11 = uc1.y;
+                w00 = sent32(dc0.x);  // walls (solver.hpp:413-417), applied after the reaction term
+                w01 = sent32(dc0.y);
+                w10 = sent32(dc1.x);
+                w11 = sent32(dc1.y);
             }
 #undef PD_F32B
         }
+        // + dt * r (solver.hpp:437-441); dt * 0 = +0 when the float dt is
+        // finite, so warps without a sink node then add +0 and skip the products
+        if (REACTION == PD_REACTION_SURFACE_SINK && (!dt_fin || __any_sync(0xffffffffu, sk != 0u))) {
+            o00 = o00 + dt * ((sk & 1u) ? neg_k * uc0.x : 0.0f);
+            o01 = o01 + dt * ((sk & 2u) ? neg_k * uc0.y : 0.0f);
+            o10 = o10 + dt * ((sk & 4u) ? neg_k * uc1.x : 0.0f);
+            o11 = o11 + dt * ((sk & 8u) ? neg_k * uc1.y : 0.0f);
+        } else if (REACTION == PD_REACTION_VOLUMETRIC) {
+            o00 = o00 + dt * (src[0] * sfac);
+            o01 = o01 + dt * (src[1] * sfac);
+            o10 = o10 + dt * (src[2] * sfac);
+            o11 = o11 + dt * (src[3] * sfac);
+        } else if (dt_fin) {
+            o00 = o00 + 0.0f;
+            o01 = o01 + 0.0f;
+            o10 = o10 + 0.0f;
+            o11 = o11 + 0.0f;
+        } else {
+            o00 = o00 + dt * 0.0f;
+            o01 = o01 + dt * 0.0f;
+            o10 = o10 + dt * 0.0f;
+            o11 = o11 + dt * 0.0f;
+        }
+        if (w00) o00 = uc0.x;
+        if (w01) o01 = uc0.y;
+        if (w10) o10 = uc1.x;
+        if (w11) o11 = uc1.y;
         // rare path: Dirichlet-exposed chunk or a non-finite result (inactive
         // slots keep u there: a non-finite one only costs the re-check)
         const uint32_t em = max(max(__float_as_uint(o00) & 0x7f800000u, __float_as_uint(o01) & 0x7f800000u),
