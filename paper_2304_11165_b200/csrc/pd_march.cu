@@ -281,6 +281,9 @@ __device__ __noinline__ double2 pair_slow(unsigned long long* bad_key, int* flag
 
 // u_next stores: streaming (evict-first) — the values are next read one
 // step later, long after they would have left L2.
+__device__ __forceinline__ void stg2(double* p, double a, double b) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
 __device__ __forceinline__ void stg_pair(double* p, double a, double b, bool a0, bool a1) {
     asm volatile(
         "{\n .reg .pred p, q, r;\n setp.ne.b32 p, %3, 0;\n setp.ne.b32 q, %4, 0;\n"
@@ -2720,8 +2723,13 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
             }
         }
         double* gp = un + ((uint32_t)c * 512u + g_off);
-        stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
-        stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
+        if ((flags & kFlagUnif) || ib == 3u) {  // every node of both planes active: plain 16-B stores
+            stg2(gp, o00, o01);
+            stg2(gp + 64, o10, o11);
+        } else {
+            stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
+            stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
+        }
         if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (z0 == 0 || z0 == 6)) {
             ChunkCtx14 C;
             C.c = c;
