@@ -2457,6 +2457,7 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
         int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
         descs(e_c, d0c, d1c);
         prefetch(e_c);
+        static_assert(kB31 == 4, "v43 rotates four per-chunk lane-mask words per batch");
         uint32_t lc0 = lm_of(e_c, 0), lc1 = lm_of(e_c, 1), lc2 = lm_of(e_c, 2), lc3 = lm_of(e_c, 3);
         // per-lane destinations (stage-relative) and source element offsets
         const uint32_t L = (uint32_t)lane;
