@@ -24,7 +24,6 @@ VARIANTS = [
     {"PD_MARCH_V": "41"},
     {"PD_MARCH_V": "43", "PD_M43_PF": "3"},
     {"PD_MARCH_V": "43", "PD_M43_PF": "7"},
-    {"PD_MARCH_V": "44"},
     {"PD_MARCH32_V": "14"},
     {"PD_MARCH32_V": "43", "PD_M32B_CFG": "1"},
     {"PD_MARCH32_V": "43", "PD_M32B_CFG": "2"},
