@@ -63,7 +63,7 @@ namespace pdb {
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kCtasPerSm = 4;  // march v14 (default): 4 CTAs x 4 warps per SM
-constexpr int kSeg = 16;
+constexpr int kSeg = 8;  // measured: 16 and 32 read 0.6 / 2.3 GB more DRAM per C5 step (profiles/r02_ab_schedule.txt)
 constexpr unsigned kSentHi = 0xFFF00000u;  // high word of -inf
 constexpr int kFlagDirichlet = 2;  // chunk touches a Dirichlet outer face
 constexpr int kFlagPushLo = 1 << 16;  // push the new z=0 plane to the lower peer's ghost chunk
@@ -2952,13 +2952,15 @@ void march_free(MarchPlan* p) {
 // layers, 4x4 column tiles, column, z), so the chunks in flight form one
 // short window and neighbour halos hit L2.
 __global__ void sched_key_kernel(const int32_t* __restrict__ keys, int64_t begin, int64_t n,
-                                 unsigned long long* __restrict__ sk, int32_t* __restrict__ ord) {
+                                 unsigned long long* __restrict__ sk, int32_t* __restrict__ ord, int seg, int tx,
+                                 int ty) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int32_t* k = keys + (begin + i) * 3;
     const unsigned long long x = (unsigned)k[0], y = (unsigned)k[1], z = (unsigned)k[2];
-    // (z-block of kSeg layers, 4x4 column tile, column, z); keys < 1024 per axis
-    sk[i] = ((z / kSeg) << 50) | ((y >> 2) << 42) | ((x >> 2) << 34) | (y << 20) | (x << 10) | z;
+    // (z-block of seg layers, 2^tx x 2^ty column tile, column, z); keys < 1024
+    // per axis, 10 bits per field
+    sk[i] = ((z / (unsigned)seg) << 50) | ((y >> ty) << 40) | ((x >> tx) << 30) | (y << 20) | (x << 10) | z;
     ord[i] = (int32_t)(begin + i);
 }
 
@@ -2977,7 +2979,17 @@ int32_t* march_schedule(pd_grid* g, int64_t begin, int64_t end) {
         PD_CUDA(pd_malloc(&k_in, sizeof(unsigned long long) * (size_t)n));
         PD_CUDA(pd_malloc(&k_out, sizeof(unsigned long long) * (size_t)n));
         PD_CUDA(pd_malloc(&o_in, sizeof(int32_t) * (size_t)n));
-        sched_key_kernel<<<(unsigned)((n + 255) / 256), 256, 0, g->stream>>>(g->d_keys, begin, n, k_in, o_in);
+        // PD_SCHED="seg,tx,ty" (A/B only): z-block depth and log2 column-tile sides
+        static const int3 sc = [] {
+            int3 v = make_int3(kSeg, 2, 2);
+            if (const char* e = getenv("PD_SCHED")) {
+                if (sscanf(e, "%d,%d,%d", &v.x, &v.y, &v.z) != 3 || v.x < 1 || v.y < 0 || v.y > 9 || v.z < 0 || v.z > 9)
+                    v = make_int3(kSeg, 2, 2);
+            }
+            return v;
+        }();
+        sched_key_kernel<<<(unsigned)((n + 255) / 256), 256, 0, g->stream>>>(g->d_keys, begin, n, k_in, o_in, sc.x,
+                                                                               sc.y, sc.z);
         PD_CUDA(cudaGetLastError());
         PD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, o_in, d, (int)n, 0, 60, g->stream));
         PD_CUDA(pd_malloc(&tmp, tb));
