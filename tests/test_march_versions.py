@@ -1,5 +1,5 @@
 """Every march kernel kept in the library (selected per process by
-PD_MARCH_V / PD_M31_CFG / PD_M43_PF for FP64 and PD_MARCH32_V / PD_M32B_CFG for
+PD_MARCH_V / PD_M31_CFG / PD_M43_PF / PD_SCHED for FP64 and PD_MARCH32_V / PD_M32B_CFG for
 FP32) reproduces the golden cases bit for bit. The default kernels run in the
 whole suite; the A/B variants run here, each in its own process, on the golden
 FTCS cases of test_gpu_parity.py."""
@@ -24,6 +24,8 @@ VARIANTS = [
     {"PD_MARCH_V": "41"},
     {"PD_MARCH_V": "43", "PD_M43_PF": "3"},
     {"PD_MARCH_V": "43", "PD_M43_PF": "7"},
+    {"PD_MARCH_V": "43", "PD_SCHED": "16,2,2"},  # schedule orders: same bits in any order
+    {"PD_MARCH_V": "43", "PD_SCHED": "1,0,0"},
     {"PD_MARCH32_V": "14"},
     {"PD_MARCH32_V": "43", "PD_M32B_CFG": "1"},
     {"PD_MARCH32_V": "43", "PD_M32B_CFG": "2"},
