@@ -2752,410 +2752,6 @@ __global__ void __launch_bounds__(kThreads43, kCtas43)
     if (PUSH && pushed) __threadfence_system();
 }
 
-// ---------------------------------------------------------------------------
-// v45: v43 with 4 planes per compute warp: two groups of two warps take
-// alternate chunks, and a warp walks its 4 planes as two pairs, carrying the
-// shared z planes in registers (u / D_eff of 6 planes staged per 4 computed
-// instead of 8; one stage handshake per 4 planes). Producer and stage layout
-// as v43 (two end markers, one per group).
-// ---------------------------------------------------------------------------
-template <int REACTION, bool PUSH, bool HALF>
-__global__ void __launch_bounds__(kThreads43, kCtas43)
-    ftcs_march45_kernel(const __grid_constant__ MarchArgs M, const uint32_t* __restrict__ ctxa,
-                        const __grid_constant__ CUtensorMap mux, const __grid_constant__ CUtensorMap mdx) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ SlowConsts K;
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const StepArgs<double>& A = M.A;
-    if (A.k > 0) {
-        const int prev = A.flags[A.k - 1];
-        if (prev) {
-            if (t == 0 && blockIdx.x == 0) A.flags[A.k] = prev;
-            return;
-        }
-    }
-    const uint32_t sm0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t full0 = sm0 + kSt43 * kStage43, empty0 = full0 + 8u * kSt43;
-    if (t == 0) {
-        for (int a = 0; a < 3; ++a) {
-            K.size[a] = A.size[a];
-            K.inv_dx2[a] = A.inv_dx2[a];
-        }
-        for (int f = 0; f < 6; ++f) K.bcv[f] = A.bcv[f];
-        K.dt = A.dt;
-        K.neg_k = A.neg_k;
-        K.src_factor = A.src_factor;
-        K.dirichlet = A.dirichlet;
-        K.huge_hi = A.huge_hi;
-        for (int s = 0; s < kSt43; ++s) {
-            mbar_init(full0 + 8u * s, 33u);  // lane 0's expect_tx arrive + 32 cp.async arrivals
-            mbar_init(empty0 + 8u * s, (uint32_t)(kW31 / 2));  // two warps per chunk
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    const double* __restrict__ u = A.u;
-    const double* __restrict__ de = M.deff;
-    const int n = (int)M.n;
-
-    if (warp == kW31) {  // ---------------- producer warp ----------------
-        // batch pipeline as v31: claim of batch b+3, entries of b+2,
-        // descriptors and L2 prefetch of b+1 issued while batch b is copied
-        int* ctr = M.counter;
-        const int4* desc4 = reinterpret_cast<const int4*>(M.desc);
-        const uint32_t sent_off = (uint32_t)M.n_all * 512u;  // D_eff sentinel chunk (elements)
-        auto claim = [&]() -> int {
-            int r = 0;
-            if (lane == 0)
-                asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(ctr), "r"(kB31) : "memory");
-            return r;
-        };
-        auto entries = [&](int p0) -> int {
-            const int p = __shfl_sync(0xffffffffu, p0, 0) + lane;
-            return lane < kB31 && p < n ? __ldg(&M.sched[p]) : -1;
-        };
-        auto chunk_of = [](int e) { return e == -1 ? -1 : (int)((uint32_t)e & 0x7FFFFFFFu); };
-        auto descs = [&](int e, int4& d0, int4& d1) {
-            const int c = chunk_of(e);
-            if (lane < kB31 && c >= 0) {
-                d0 = __ldg(desc4 + 2 * (int64_t)c);
-                d1 = __ldg(desc4 + 2 * (int64_t)c + 1);
-            }
-        };
-        // M.pf: bit 0 L2 prefetch of the next batch's u slabs and records,
-        // bit 1 of its D_eff slabs, bit 2 skip the own-slab copies of pairs
-        // with no active node (their D_eff is written as the sentinel)
-        const int pf = M.pf;
-        auto prefetch = [&](int e) {
-            const int64_t c = (int64_t)chunk_of(e);
-            if (lane < kB31 && c >= 0) {
-                if (pf & 1) {
-                    prefetch_l2(u + c * 512, 4096u);
-                    prefetch_l2(ctxa + c * kCtxWords30, 176u);
-                }
-                if ((pf & 2) && e >= 0) prefetch_l2(de + c * 512, 4096u);
-            }
-        };
-        // this lane's active-pair word (chunk record lm[lane]) of chunk j of a batch
-        auto lm_of = [&](int e, int j) -> uint32_t {
-            const int c = chunk_of(__shfl_sync(0xffffffffu, e, j));
-            return (pf & 4) && c >= 0 ? __ldg(ctxa + (int64_t)c * kCtxWords30 + lane) : 0xFFFFu;
-        };
-        int e_c = entries(claim());
-        int e_n = entries(claim());
-        int p_nn = claim();
-        int4 d0c = make_int4(0, 0, 0, 0), d1c = d0c;
-        descs(e_c, d0c, d1c);
-        prefetch(e_c);
-        static_assert(kB31 == 4, "v43 rotates four per-chunk lane-mask words per batch");
-        uint32_t lc0 = lm_of(e_c, 0), lc1 = lm_of(e_c, 1), lc2 = lm_of(e_c, 2), lc3 = lm_of(e_c, 3);
-        // per-lane destinations (stage-relative) and source element offsets
-        const uint32_t L = (uint32_t)lane;
-        const uint32_t d_own = kPP43 + 64u + 16u * L;                        // + 640 i: row pair L of plane i
-        const uint32_t d_ylo = kPP43 * ((L >> 2) + 1u) + 16u * (L & 3u);      // row -1 of plane L/4
-        const uint32_t s_ylo = 64u * (L >> 2) + 2u * (L & 3u);                // of the y- / y+ neighbour
-        uint32_t s = 0, ph = 0, k = 0;
-#pragma unroll 1
-        for (;;) {
-            int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
-            descs(e_n, d0n, d1n);
-            prefetch(e_n);
-            const uint32_t ln0 = lm_of(e_n, 0), ln1 = lm_of(e_n, 1), ln2 = lm_of(e_n, 2), ln3 = lm_of(e_n, 3);
-            const int e_nn = entries(p_nn);
-            p_nn = claim();
-            bool done = false;
-#pragma unroll 1
-            for (int j = 0; j < kB31; ++j, ++k) {
-                const int c_cur = chunk_of(__shfl_sync(0xffffffffu, e_c, j));
-                const uint32_t st = sm0 + s * kStage43, full = full0 + 8u * s;
-                if (k >= (uint32_t)kSt43) mbar_wait(empty0 + 8u * s, ph ^ 1u);
-                if (c_cur < 0) {  // end markers: one per compute group (this stage and the next)
-                    if (lane == 0) {
-                        sts_u32(st + kCtx43 + 176u, 0xFFFFFFFFu);
-                        mbar_arrive(full);
-                    }
-                    cp_mbar_arrive_noinc(full);
-                    if (++s == (uint32_t)kSt43) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                    if (++k >= (uint32_t)kSt43) mbar_wait(empty0 + 8u * s, ph ^ 1u);
-                    const uint32_t st2 = sm0 + s * kStage43, full2 = full0 + 8u * s;
-                    if (lane == 0) {
-                        sts_u32(st2 + kCtx43 + 176u, 0xFFFFFFFFu);
-                        mbar_arrive(full2);
-                    }
-                    cp_mbar_arrive_noinc(full2);
-                    done = true;
-                    break;
-                }
-                const int nb0 = __shfl_sync(0xffffffffu, d0c.x, j), nb1 = __shfl_sync(0xffffffffu, d0c.y, j);
-                const int nb2 = __shfl_sync(0xffffffffu, d0c.z, j), nb3 = __shfl_sync(0xffffffffu, d0c.w, j);
-                const int nb4 = __shfl_sync(0xffffffffu, d1c.x, j), nb5 = __shfl_sync(0xffffffffu, d1c.y, j);
-                const bool dl = !(__shfl_sync(0xffffffffu, d1c.w, j) & kFlagUnif);
-                if (lane == 0) {
-                    sts_u32(st + kCtx43 + 176u, (uint32_t)c_cur);
-                    mbar_arrive_tx(full, 176u + (nb0 >= 0 ? 1024u : 0u) + (nb1 >= 0 ? 1024u : 0u) + (dl ? 2048u : 0u));
-                    bulk_g2s(st + kCtx43, ctxa + (int64_t)c_cur * kCtxWords30, 176u, full);
-                    if (nb0 >= 0) tma4(st + kXL43, &mux, 6, 0, 0, nb0, full);
-                    if (nb1 >= 0) tma4(st + kXH43, &mux, 0, 0, 0, nb1, full);
-                    if (dl) {
-                        const int sent_c = (int)M.n_all;
-                        tma4(st + kHalf43 + kXL43, &mdx, 6, 0, 0, nb0 >= 0 ? nb0 : sent_c, full);
-                        tma4(st + kHalf43 + kXH43, &mdx, 0, 0, 0, nb1 >= 0 ? nb1 : sent_c, full);
-                    }
-                }
-                // own slabs: plane i, rows 2 (L/8).. as 16-B pieces (8 per lane)
-                const uint32_t so = (uint32_t)c_cur * 512u + 2u * L;
-                const double* gu = u + so;
-                const double* gd = de + so;
-                const uint32_t lmj = lc0;  // this lane's pair bits (2 per plane)
-                lc0 = lc1;
-                lc1 = lc2;
-                lc2 = lc3;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const bool act = (lmj >> (2 * i)) & 3u;
-                    cp16(st + d_own + (uint32_t)i * kPP43, gu + 64 * i, act);
-                    cp16(st + kHalf43 + d_own + (uint32_t)i * kPP43, gd + 64 * i, dl && act);
-                    if (dl && !act) {  // no active node: D_eff = sentinel, u never used
-                        const uint32_t sh = kSentHi;
-                        sts4(st + kHalf43 + d_own + (uint32_t)i * kPP43, 0u, sh, 0u, sh);
-                    }
-                }
-                // z halos: plane 7 of the z- neighbour -> plane -1, plane 0 of the z+ neighbour -> plane 8
-                {
-                    const uint32_t zl = (uint32_t)nb4 * 512u + 448u + 2u * L, zh = (uint32_t)nb5 * 512u + 2u * L;
-                    cp16(st + 64u + 16u * L, u + (nb4 >= 0 ? zl : 0u), nb4 >= 0);
-                    cp16(st + 9u * kPP43 + 64u + 16u * L, u + (nb5 >= 0 ? zh : 0u), nb5 >= 0);
-                    cp16(st + kHalf43 + 64u + 16u * L, de + (nb4 >= 0 ? zl : sent_off + 2u * L), dl);
-                    cp16(st + kHalf43 + 9u * kPP43 + 64u + 16u * L, de + (nb5 >= 0 ? zh : sent_off + 2u * L), dl);
-                }
-                // y halos: row 7 of the y- neighbour -> row -1, row 0 of the y+ neighbour -> row 8
-                {
-                    const uint32_t yl = (uint32_t)nb2 * 512u + 56u + s_ylo, yh = (uint32_t)nb3 * 512u + s_ylo;
-                    cp16(st + d_ylo, u + (nb2 >= 0 ? yl : 0u), nb2 >= 0);
-                    cp16(st + d_ylo + 576u, u + (nb3 >= 0 ? yh : 0u), nb3 >= 0);
-                    cp16(st + kHalf43 + d_ylo, de + (nb2 >= 0 ? yl : sent_off + s_ylo), dl);
-                    cp16(st + kHalf43 + d_ylo + 576u, de + (nb3 >= 0 ? yh : sent_off + s_ylo), dl);
-                }
-                cp_mbar_arrive_noinc(full);
-                if (++s == (uint32_t)kSt43) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-            if (done) break;
-            e_c = e_n;
-            d0c = d0n;
-            d1c = d1n;
-            e_n = e_nn;
-            lc0 = ln0;
-            lc1 = ln1;
-            lc2 = ln2;
-            lc3 = ln3;
-        }
-        return;
-    }
-
-    // ---------------- compute warps ----------------
-    // two groups of two warps; group g takes the chunks k = g, g + 2, ... of
-    // the stage sequence (stage k % 3, phase (k / 3) & 1); warp half h of a
-    // group owns planes 4h..4h+3 and walks them as two plane pairs, carrying
-    // planes z+1 / z+2 of the first pair in registers as z-1 / z of the second
-    Consts Q;
-    Q.dt = A.dt;
-    Q.neg_k = A.neg_k;
-    Q.src_factor = A.src_factor;
-    Q.ix = A.inv_dx2[0];
-    Q.iy = A.inv_dx2[1];
-    Q.iz = A.inv_dx2[2];
-    const int y = lane >> 2, xp = lane & 3;
-    const uint32_t grp = (uint32_t)warp >> 1, z0 = 4u * ((uint32_t)warp & 1u);
-    const uint32_t bp = (uint32_t)(y * 8 + 2 * xp);
-    const uint32_t pz0 = (z0 + 1u) * kPP43;
-    const uint32_t v_c = pz0 + (uint32_t)(y + 1) * 64u + 16u * (uint32_t)xp;
-    const uint32_t o_c = pin(v_c, lane);
-    const uint32_t o_x = pin(xp == 3 ? kXH43 + (z0 * 8u + (uint32_t)y) * 16u : kXL43 + (z0 * 8u + (uint32_t)y) * 16u + 8u, lane);
-    const bool xlo = xp == 0, xhi = xp == 3;
-    double* __restrict__ un = A.un;
-    const uint32_t huge_hi = A.huge_hi;
-    bool pushed = false;
-    uint32_t kk = grp;
-#pragma unroll 1
-    for (;; kk += 2u) {
-        const uint32_t s = kk % (uint32_t)kSt43, ph = (kk / (uint32_t)kSt43) & 1u;
-        mbar_wait(full0 + 8u * s, ph);
-        const uint32_t st = sm0 + s * kStage43;
-        const int c = (int)lds_u32(st + kCtx43 + 176u);
-        if (c < 0) break;
-        const uint32_t lm = lds_u32(st + kCtx43 + 4u * (uint32_t)lane);
-        const int flags = (int)lds_u32(st + kCtx43 + 156u);
-        const uint32_t a = st + o_c, ax = st + o_x;
-        const bool unif = (flags & kFlagUnif) != 0;
-        double dh = 0.0;
-        if (unif) {
-            const double dv = lds1(st + kCtx43 + 160u);
-            dh = HALF ? dv + dv : (dv + dv) * 0.5;
-        }
-        // carried planes: u / D_eff of planes z-1 and z of the current pair
-        double2 cm = lds2(a - kPP43), c0 = lds2(a);
-        double2 em = make_double2(0.0, 0.0), e0 = em;
-        if (!unif) {
-            em = lds2(a + kHalf43 - kPP43);
-            e0 = lds2(a + kHalf43);
-        }
-#pragma unroll
-        for (uint32_t hh = 0; hh < 2u; ++hh) {
-            const uint32_t zz = z0 + 2u * hh;
-            const uint32_t ah = a + 2u * hh * kPP43, axh = ax + 2u * hh * 128u;
-            const uint32_t zsh = 2u * zz;
-            const uint32_t ab = (lm >> zsh) & 0xFu;
-            const uint32_t sk = (lm >> (16u + zsh)) & 0xFu;
-            const uint32_t g_off = zz * 64u + bp;
-            double src[4] = {0.0, 0.0, 0.0, 0.0};
-            if (REACTION == PD_REACTION_VOLUMETRIC) {
-                const double* sp = A.src + (int64_t)c * 512 + g_off;
-                src[0] = sp[0];
-                src[1] = sp[1];
-                src[2] = sp[64];
-                src[3] = sp[65];
-            }
-            const double2 uc0 = c0, uzm = cm;
-            const double2 uc1 = lds2(ah + kPP43), uzp = lds2(ah + 2u * kPP43);
-            const double uh0 = lds1(axh), uh1 = lds1(axh + 128u);
-            const double su0 = __shfl_up_sync(0xffffffffu, uc0.y, 1), sd0 = __shfl_down_sync(0xffffffffu, uc0.x, 1);
-            const double su1 = __shfl_up_sync(0xffffffffu, uc1.y, 1), sd1 = __shfl_down_sync(0xffffffffu, uc1.x, 1);
-            const double uL0 = xlo ? uh0 : su0, uR0 = xhi ? uh0 : sd0;
-            const double uL1 = xlo ? uh1 : su1, uR1 = xhi ? uh1 : sd1;
-            const double2 uym0 = lds2(ah - 64u), uyp0 = lds2(ah + 64u);
-            const double2 uym1 = lds2(ah + kPP43 - 64u), uyp1 = lds2(ah + kPP43 + 64u);
-            double o00, o01, o10, o11;
-            bool w00 = false, w01 = false, w10 = false, w11 = false;
-            const uint32_t ib = ((uint32_t)flags >> (8u + zz)) & 3u;
-            if (unif) {
-                const double fzx = dh * (uc1.x - uc0.x), fzy = dh * (uc1.y - uc0.y);
-                const double f0i = dh * (uc0.y - uc0.x), f1i = dh * (uc1.y - uc1.x);
-                o00 = node31x(Q, uc0.x, dh * (uc0.x - uL0), f0i, dh * (uc0.x - uym0.x), dh * (uyp0.x - uc0.x),
-                              dh * (uc0.x - uzm.x), fzx);
-                o01 = node31x(Q, uc0.y, f0i, dh * (uR0 - uc0.y), dh * (uc0.y - uym0.y), dh * (uyp0.y - uc0.y),
-                              dh * (uc0.y - uzm.y), fzy);
-                o10 = node31x(Q, uc1.x, dh * (uc1.x - uL1), f1i, dh * (uc1.x - uym1.x), dh * (uyp1.x - uc1.x),
-                              fzx, dh * (uzp.x - uc1.x));
-                o11 = node31x(Q, uc1.y, f1i, dh * (uR1 - uc1.y), dh * (uc1.y - uym1.y), dh * (uyp1.y - uc1.y),
-                              fzy, dh * (uzp.y - uc1.y));
-            } else {
-                const uint32_t b = ah + kHalf43, bx = axh + kHalf43;
-                const double2 dc0 = e0, dzm = em;
-                const double2 dc1 = lds2(b + kPP43), dzp = lds2(b + 2u * kPP43);
-                const double dh0 = lds1(bx), dh1 = lds1(bx + 128u);
-                const double tu0 = __shfl_up_sync(0xffffffffu, dc0.y, 1), td0 = __shfl_down_sync(0xffffffffu, dc0.x, 1);
-                const double tu1 = __shfl_up_sync(0xffffffffu, dc1.y, 1), td1 = __shfl_down_sync(0xffffffffu, dc1.x, 1);
-                const double dL0 = xlo ? dh0 : tu0, dR0 = xhi ? dh0 : td0;
-                const double dL1 = xlo ? dh1 : tu1, dR1 = xhi ? dh1 : td1;
-                const double2 dym0 = lds2(b - 64u), dyp0 = lds2(b + 64u);
-                const double2 dym1 = lds2(b + kPP43 - 64u), dyp1 = lds2(b + kPP43 + 64u);
-                if (ib == 3u) {
-                    const double fzx = fface<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = fface<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
-                    const double f0i = fface<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = fface<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
-                    o00 = node31x(Q, uc0.x, fface<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
-                                  fface<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), fface<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
-                                  fface<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx);
-                    o01 = node31x(Q, uc0.y, f0i, fface<HALF>(dc0.y, dR0, uc0.y, uR0),
-                                  fface<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), fface<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
-                                  fface<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy);
-                    o10 = node31x(Q, uc1.x, fface<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
-                                  fface<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), fface<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
-                                  fzx, fface<HALF>(dc1.x, dzp.x, uc1.x, uzp.x));
-                    o11 = node31x(Q, uc1.y, f1i, fface<HALF>(dc1.y, dR1, uc1.y, uR1),
-                                  fface<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), fface<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
-                                  fzy, fface<HALF>(dc1.y, dzp.y, uc1.y, uzp.y));
-                } else {
-                    const double fzx = face<HALF>(dc0.x, dc1.x, uc0.x, uc1.x), fzy = face<HALF>(dc0.y, dc1.y, uc0.y, uc1.y);
-                    const double f0i = face<HALF>(dc0.x, dc0.y, uc0.x, uc0.y), f1i = face<HALF>(dc1.x, dc1.y, uc1.x, uc1.y);
-                    o00 = node31x(Q, uc0.x, face<HALF>(dL0, dc0.x, uL0, uc0.x), f0i,
-                                  face<HALF>(dym0.x, dc0.x, uym0.x, uc0.x), face<HALF>(dc0.x, dyp0.x, uc0.x, uyp0.x),
-                                  face<HALF>(dzm.x, dc0.x, uzm.x, uc0.x), fzx);
-                    o01 = node31x(Q, uc0.y, f0i, face<HALF>(dc0.y, dR0, uc0.y, uR0),
-                                  face<HALF>(dym0.y, dc0.y, uym0.y, uc0.y), face<HALF>(dc0.y, dyp0.y, uc0.y, uyp0.y),
-                                  face<HALF>(dzm.y, dc0.y, uzm.y, uc0.y), fzy);
-                    o10 = node31x(Q, uc1.x, face<HALF>(dL1, dc1.x, uL1, uc1.x), f1i,
-                                  face<HALF>(dym1.x, dc1.x, uym1.x, uc1.x), face<HALF>(dc1.x, dyp1.x, uc1.x, uyp1.x),
-                                  fzx, face<HALF>(dc1.x, dzp.x, uc1.x, uzp.x));
-                    o11 = node31x(Q, uc1.y, f1i, face<HALF>(dc1.y, dR1, uc1.y, uR1),
-                                  face<HALF>(dym1.y, dc1.y, uym1.y, uc1.y), face<HALF>(dc1.y, dyp1.y, uc1.y, uyp1.y),
-                                  fzy, face<HALF>(dc1.y, dzp.y, uc1.y, uzp.y));
-                    w00 = sentinel(dc0.x);  // walls (solver.hpp:413-417), applied after the reaction term
-                    w01 = sentinel(dc0.y);
-                    w10 = sentinel(dc1.x);
-                    w11 = sentinel(dc1.y);
-                }
-                em = dc1;  // carried D_eff planes of the next pair
-                e0 = dzp;
-            }
-            cm = uc1;  // carried u planes of the next pair
-            c0 = uzp;
-            // + dt * r (solver.hpp:437-441), as ftcs_march43_kernel
-            if (REACTION == PD_REACTION_SURFACE_SINK && __any_sync(0xffffffffu, sk != 0u)) {
-                o00 = o00 + Q.dt * ((sk & 1u) ? Q.neg_k * uc0.x : 0.0);
-                o01 = o01 + Q.dt * ((sk & 2u) ? Q.neg_k * uc0.y : 0.0);
-                o10 = o10 + Q.dt * ((sk & 4u) ? Q.neg_k * uc1.x : 0.0);
-                o11 = o11 + Q.dt * ((sk & 8u) ? Q.neg_k * uc1.y : 0.0);
-            } else if (REACTION == PD_REACTION_VOLUMETRIC) {
-                o00 = o00 + Q.dt * (src[0] * Q.src_factor);
-                o01 = o01 + Q.dt * (src[1] * Q.src_factor);
-                o10 = o10 + Q.dt * (src[2] * Q.src_factor);
-                o11 = o11 + Q.dt * (src[3] * Q.src_factor);
-            } else {
-                o00 = o00 + 0.0;
-                o01 = o01 + 0.0;
-                o10 = o10 + 0.0;
-                o11 = o11 + 0.0;
-            }
-            if (w00) o00 = uc0.x;
-            if (w01) o01 = uc0.y;
-            if (w10) o10 = uc1.x;
-            if (w11) o11 = uc1.y;
-            const uint32_t hm = max(max((uint32_t)__double2hiint(o00) & 0x7fffffffu, (uint32_t)__double2hiint(o01) & 0x7fffffffu),
-                                    max((uint32_t)__double2hiint(o10) & 0x7fffffffu, (uint32_t)__double2hiint(o11) & 0x7fffffffu));
-            const bool slow = (flags & kFlagDirichlet) || hm >= huge_hi;
-            if (__any_sync(0xffffffffu, slow)) {
-                if (slow) {
-                    const double2 r0 = pair_slow43<REACTION, HALF>(M, K, st, lane, (int)zz, o00, o01);
-                    const double2 r1 = pair_slow43<REACTION, HALF>(M, K, st, lane, (int)zz + 1, o10, o11);
-                    o00 = r0.x;
-                    o01 = r0.y;
-                    o10 = r1.x;
-                    o11 = r1.y;
-                }
-            }
-            double* gp = un + ((uint32_t)c * 512u + g_off);
-            if (unif || ib == 3u) {  // every node of both planes active: plain 16-B stores
-                stg2(gp, o00, o01);
-                stg2(gp + 64, o10, o11);
-            } else {
-                stg_pair(gp, o00, o01, ab & 1u, ab & 2u);
-                stg_pair(gp + 64, o10, o11, ab & 4u, ab & 8u);
-            }
-            if (PUSH && (flags & (kFlagPushLo | kFlagPushHi)) && (zz == 0 || zz == 6)) {
-                ChunkCtx14 C;
-                C.c = c;
-                C.key = (int)lds_u32(st + kCtx43 + 152u);
-                C.flags = flags;
-                C.lm = lm;
-                C.dv = 0.0;
-                if (zz == 0) push_pair14(M, C, 0, bp, o00, o01, ab & 1u, ab & 2u);
-                else push_pair14(M, C, 7, bp, o10, o11, ab & 4u, ab & 8u);
-                pushed = true;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8u * s);
-    }
-    if (PUSH && pushed) __threadfence_system();
-}
-
 __global__ void sentinel_fill_kernel(double* p) { p[threadIdx.x] = sent(); }
 
 // desc flags of the fused halo push: bit set iff the chunk has a peer ghost
@@ -3715,39 +3311,6 @@ void march43_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
     PD_CUDA(cudaGetLastError());
 }
 
-void march45_launch(pd_grid* g, MarchPlan& p, MarchArgs M, int r, bool push) {
-    static const int pf = [] {
-        const char* e = getenv("PD_M43_PF");
-        return e ? atoi(e) : 5;
-    }();
-    M.pf = pf;
-    if (!p.d_ctx) fail(PD_E_INPUT, "march v45 needs the packed chunk records (3-D FP64 plan)");
-    M.sched = flagged_schedule(g, p, M.sched, M.n);
-    static const cuuint32_t bx[4] = {2, 8, 8, 1};
-    const CUtensorMap mux = column_map(M.A.u, g->n_chunks, bx), mdx = column_map(M.deff, g->n_chunks + 1, bx);
-    using K43 = void (*)(const MarchArgs, const uint32_t*, const CUtensorMap, const CUtensorMap);
-    static const K43 tab[2][2][3] = {
-        {{ftcs_march45_kernel<0, false, false>, ftcs_march45_kernel<1, false, false>, ftcs_march45_kernel<2, false, false>},
-         {ftcs_march45_kernel<0, true, false>, ftcs_march45_kernel<1, true, false>, ftcs_march45_kernel<2, true, false>}},
-        {{ftcs_march45_kernel<0, false, true>, ftcs_march45_kernel<1, false, true>, ftcs_march45_kernel<2, false, true>},
-         {ftcs_march45_kernel<0, true, true>, ftcs_march45_kernel<1, true, true>, ftcs_march45_kernel<2, true, true>}}};
-    const uint32_t smem = smem43();
-    static uint64_t attr_done = 0;
-    const int dev = g->device;
-    if (dev < 0 || dev >= 64) fail(PD_E_INPUT, "device index out of range");
-    if (!((attr_done >> dev) & 1u)) {
-        for (int h = 0; h < 2; ++h)
-            for (int q = 0; q < 2; ++q)
-                for (int rr = 0; rr < 3; ++rr)
-                    PD_CUDA(cudaFuncSetAttribute(tab[h][q][rr], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_done |= 1ull << dev;
-    }
-    int sms = 148;
-    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    tab[p.half ? 1 : 0][push ? 1 : 0][r]<<<sms * kCtas43, kThreads43, smem, g->stream>>>(M, p.d_ctx, mux, mdx);
-    PD_CUDA(cudaGetLastError());
-}
-
 void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int reaction, const int32_t* sched,
                         int64_t n, int* counter, const PeerLaunch* pl) {
     MarchArgs M;
@@ -3797,10 +3360,6 @@ void march_launch_sched(pd_grid* g, MarchPlan& p, const StepArgs<double>& a, int
     }
     if (ver == 43) {
         march43_launch(g, p, M, r, pl != nullptr);
-        return;
-    }
-    if (ver == 45) {
-        march45_launch(g, p, M, r, pl != nullptr);
         return;
     }
     static const int pf = [] {
